@@ -1,0 +1,270 @@
+/* fsgg.h — C ABI of the B200-native KDE-driven similarity-graph sampler.
+ *
+ * Drop-in for the hot path of arXiv 2310.13870 as implemented by the
+ * reference C++ library `fsg` (/root/reference/proj). Every entry point
+ * names the reference interface it replaces (file:line). Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.
+ *
+ * Error contract (proj/include/fsg/common.hpp:13-66): every function that
+ * can fail returns FSGG_OK (0) or the reference's exit-code class —
+ * 2 config (TooFewPoints, InvalidConfig, LengthMismatch), 3 I/O,
+ * 4 numeric (sparsity invariant) — plus 5 for a CUDA/device failure. There
+ * is no CPU fallback: without a usable sm_100 device every compute call
+ * returns FSGG_ERR_DEVICE. fsgg_last_error() returns a thread-local message.
+ *
+ * Threading: calls are synchronous. A dataset handle owns its device,
+ * stream and memory pool; do not use one handle from two threads at once.
+ */
+#ifndef FSGG_H
+#define FSGG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSGG_OK 0
+#define FSGG_ERR_CONFIG 2
+#define FSGG_ERR_IO 3
+#define FSGG_ERR_NUMERIC 4
+#define FSGG_ERR_DEVICE 5
+
+/* proj/include/fsg/kernel.hpp:12 KernelFamily */
+#define FSGG_KERNEL_GAUSSIAN 0
+#define FSGG_KERNEL_EXPONENTIAL 1
+#define FSGG_KERNEL_LAPLACIAN 2
+
+/* Routing random stream.
+ * REFERENCE: the reference's keyed splitmix64 streams
+ *   (proj/include/fsg/rng.hpp:11-71, keyed as in proj/src/sampler.cpp:213-216),
+ *   reproduced bit-exactly, so graphs match the reference edge for edge.
+ * PHILOX: counter-based Philox4x32-10 keyed by (seed, node, query, ticket);
+ *   same distribution, validated by chi-squared, not edge-for-edge. */
+#define FSGG_RNG_REFERENCE 0
+#define FSGG_RNG_PHILOX 1
+
+/* proj/include/fsg/kernel.hpp:21-58 (Kernel: family + bandwidth sigma). */
+typedef struct fsgg_kernel {
+  int family;
+  double sigma;
+} fsgg_kernel;
+
+/* Mirrors fsg::SparsifierConfig (proj/include/fsg/sparsifier.hpp:14-26).
+ * `epsilon` and the KDE backend selection are accepted for ABI parity but
+ * the device always computes exact kernel sums (epsilon() == 0). */
+typedef struct fsgg_config {
+  double C;                  /* default 1 */
+  double lambda_k1_estimate; /* default 1 */
+  uint32_t rounds;           /* 0 = ceil(6 C log(n) / lambda) */
+  double epsilon;            /* ignored by the exact device path */
+  int log_base;              /* 0 = log2 (default), 1 = natural */
+  uint64_t seed;             /* default 1 */
+  int rng_mode;              /* FSGG_RNG_REFERENCE (default) | FSGG_RNG_PHILOX */
+  /* Query shard [query_begin, query_end) for multi-GPU runs; (0, 0) = all.
+   * Results for a query never depend on the shard layout. */
+  uint32_t query_begin;
+  uint32_t query_end;
+} fsgg_config;
+
+/* Mirrors fsg::BuildReport (proj/include/fsg/sparsifier.hpp:40-58), plus
+ * device counters. Phase times are device (CUDA event) seconds. */
+typedef struct fsgg_report {
+  uint32_t n;
+  uint32_t rounds;
+  double epsilon;
+  char backend[32];
+  uint64_t sampled_pairs;
+  uint64_t self_pairs_discarded;
+  uint64_t underflow_edges_discarded;
+  uint64_t edge_count;
+  uint64_t degenerate_draws;
+  double estimator_build_seconds; /* node table + bounding boxes */
+  double sampling_seconds;        /* level-synchronous descent */
+  double degree_kde_seconds;      /* 0: fused into level 0 of the descent */
+  double weighting_seconds;       /* pair collapse, weights, CSR, degrees */
+  double total_seconds;
+  uint64_t estimator_bytes;
+  uint64_t graph_bytes;
+  /* device extras */
+  uint64_t kernel_evals;      /* Gaussian evaluations performed */
+  uint64_t kde_tiled_evals;   /* of which in the tiled (big-node) kernel */
+  double kde_tiled_seconds;   /* device time of the tiled kernel launches */
+  uint32_t kde_tiled_launches;
+  uint32_t levels;
+  uint64_t peak_entries;
+  uint32_t gpu_launches;      /* kernels launched by this call */
+} fsgg_report;
+
+/* Per-edge quantities of the weighting step (sparsifier.hpp:29-38). */
+typedef struct fsgg_edge_estimate {
+  uint32_t i, j;
+  double k_ij, g_i, g_j, p_hat_i_j, p_hat_j_i, p_hat;
+} fsgg_edge_estimate;
+
+/* Undirected graph, edges stored once with u < v, sorted by (u, v): the
+ * layout of fsg::WeightedGraph (proj/include/fsg/graph.hpp:20-40), plus the
+ * equivalent upper-triangular CSR row_ptr (n + 1 entries, row u holds the
+ * v > u neighbours). Host memory owned by the library; release with
+ * fsgg_graph_free. */
+typedef struct fsgg_graph {
+  uint32_t n;
+  uint64_t num_edges;
+  uint32_t* u;
+  uint32_t* v;
+  double* w;
+  uint64_t* row_ptr;
+  double* degrees; /* n entries, summed in the reference's order */
+  double total_weight;
+} fsgg_graph;
+
+/* Same graph left in device memory (pointers valid until the next build on
+ * the same dataset handle or fsgg_dataset_destroy). */
+typedef struct fsgg_device_graph {
+  uint32_t n;
+  uint64_t num_edges;
+  const uint32_t* u;
+  const uint32_t* v;
+  const double* w;
+  const uint64_t* row_ptr;
+  const double* degrees;
+  double total_weight;
+} fsgg_device_graph;
+
+typedef struct fsgg_dataset fsgg_dataset;
+
+const char* fsgg_version(void);
+const char* fsgg_last_error(void);
+/* 1 when a usable sm_100 device is visible, else 0. */
+int fsgg_device_available(void);
+
+void fsgg_config_init(fsgg_config* cfg);
+
+/* proj/src/sparsifier.cpp:17-23 (SparsifierConfig::rounds_for) */
+int fsgg_rounds_for(const fsgg_config* cfg, uint32_t n, uint32_t* out);
+/* proj/src/kde.cpp:15-18 (default_epsilon) */
+double fsgg_default_epsilon(uint32_t n, int log_base);
+
+/* fsg::Dataset (proj/include/fsg/dataset.hpp:12-25; ctor dataset.cpp:14-23):
+ * n x d row-major, index order defines the tree. Points are fp32 on the
+ * device. `points_on_device` != 0 means `points` is a device pointer on
+ * `device`. Validates n >= 1, d >= 1 and finiteness (InvalidConfig). */
+int fsgg_dataset_create(const float* points, uint32_t n, uint32_t d,
+                        int points_on_device, int device, fsgg_dataset** out);
+/* Same, from fp64 host coordinates (rounded to fp32). */
+int fsgg_dataset_create_f64(const double* points, uint32_t n, uint32_t d,
+                            int device, fsgg_dataset** out);
+/* Replace the coordinates of an existing dataset (same n, d) from host
+ * memory: one host->device copy, no reallocation. */
+int fsgg_dataset_upload(fsgg_dataset* ds, const float* host_points);
+void fsgg_dataset_destroy(fsgg_dataset* ds);
+uint32_t fsgg_dataset_size(const fsgg_dataset* ds);
+uint32_t fsgg_dataset_dim(const fsgg_dataset* ds);
+/* Raw device pointer of the fp32 coordinates. */
+const float* fsgg_dataset_device_points(const fsgg_dataset* ds);
+
+/* fsg::build_similarity_graph (proj/include/fsg/sparsifier.hpp:64-67,
+ * proj/src/sparsifier.cpp:51-142). Host output. `estimates` (nullable)
+ * receives a malloc'd array of num_edges records (free with fsgg_free). */
+int fsgg_build_similarity_graph(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                                const fsgg_config* cfg, fsgg_graph* out,
+                                fsgg_report* report,
+                                fsgg_edge_estimate** estimates);
+
+/* Device-resident variant (no device->host copy of the graph). */
+int fsgg_build_similarity_graph_device(fsgg_dataset* ds,
+                                       const fsgg_kernel* kernel,
+                                       const fsgg_config* cfg,
+                                       fsgg_device_graph* out,
+                                       fsgg_report* report);
+
+/* One-call drop-in from host fp32 points to a host graph. */
+int fsgg_build_similarity_graph_host(const float* points, uint32_t n,
+                                     uint32_t d, const fsgg_kernel* kernel,
+                                     const fsgg_config* cfg, int device,
+                                     fsgg_graph* out, fsgg_report* report);
+
+void fsgg_graph_free(fsgg_graph* g);
+void fsgg_free(void* p);
+
+/* fsg::SampleDiagnostics (proj/include/fsg/sampler.hpp:22-26). */
+typedef struct fsgg_sample_diag {
+  uint32_t nlevels;
+  uint64_t entries_per_level[64];
+  uint64_t tickets_per_level[64];
+  uint64_t degenerate_draws;
+} fsgg_sample_diag;
+
+/* fsg::sample_neighbors_counted (proj/include/fsg/sampler.hpp:48-51,
+ * proj/src/sampler.cpp:77-247). `queries` is a host array; duplicates are
+ * merged as the reference does (:89-106). Output: malloc'd triples
+ * (query, source, count) sorted by (query, source), 3 u32 each. */
+int fsgg_sample_neighbors_counted(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                                  const uint32_t* queries, size_t num_queries,
+                                  uint32_t rounds, uint64_t seed, int rng_mode,
+                                  uint32_t** triples, size_t* count,
+                                  fsgg_sample_diag* diag);
+
+/* fsg::KdeEstimator::eval (proj/include/fsg/kde.hpp:54-58, exact backend
+ * proj/src/kde.cpp:57-71): out[t] = max(sum_{j in [first,last)} k(x_t, x_j),
+ * 1e-300) for a non-empty range, 0 for an empty one. Host arrays. */
+int fsgg_kde_eval(fsgg_dataset* ds, const fsgg_kernel* kernel, uint32_t first,
+                  uint32_t last, const uint32_t* targets, size_t m,
+                  double* out);
+
+/* ---- input side (proj/src/datasets.cpp:32-124), host generators ------ */
+/* make_moons: outer arc first, keyed Box-Muller noise; fp64 output. */
+int fsgg_make_moons(uint32_t n, double noise, uint64_t seed, double* points,
+                    uint32_t* labels);
+/* make_blobs: centers k x d, n split as evenly as possible. */
+int fsgg_make_blobs(uint32_t n, const double* centers, uint32_t k, uint32_t d,
+                    double stddev, uint64_t seed, double* points,
+                    uint32_t* labels);
+/* Harness-defined configs without a reference generator:
+ * C4 synthetic image pixels (row/H, col/W, r, g, b), H x W raster, 8 seeded
+ * Voronoi colour regions, noise std 0.03. */
+int fsgg_make_image_features(uint32_t height, uint32_t width,
+                             uint32_t regions, double noise, uint64_t seed,
+                             double* points, uint32_t* labels);
+/* C5 Gaussian mixture: k components in make_blobs order, centres U[0,1]^d,
+ * per-component std, values clipped to [0,1]. */
+int fsgg_make_gmm(uint32_t n, uint32_t d, uint32_t k, double stddev,
+                  uint64_t seed, double* points, uint32_t* labels);
+
+/* ---- multi-GPU shard pipeline (one process per GPU) ------------------ */
+/* Phase 1 on every rank: descent for queries [query_begin, query_end) of
+ * cfg, producing the shard's sorted unique undirected pair keys and its
+ * slice of the degree KDE g_full. Device pointers, valid until the next
+ * call on this dataset. pair keys encode (u << 32) | v with u < v. */
+typedef struct fsgg_shard {
+  uint32_t query_begin, query_end;
+  uint32_t rounds;
+  uint64_t num_pairs;
+  const uint64_t* pairs;   /* device */
+  const double* g_full;    /* device, query_end - query_begin entries */
+  uint64_t sampled_pairs;
+  uint64_t self_pairs;
+  uint64_t degenerate_draws;
+} fsgg_shard;
+int fsgg_sample_shard(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                      const fsgg_config* cfg, fsgg_shard* out,
+                      fsgg_report* report);
+/* Phase 2 after the caller all-gathers g_full (n doubles, device) and the
+ * shards' pair keys (concatenated, device, any order, duplicates allowed):
+ * dedupe, weight, CSR and degrees exactly as the 1-GPU path. */
+int fsgg_finish_graph(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                      uint32_t rounds, const double* g_full_device,
+                      const uint64_t* pairs_device, uint64_t num_pairs,
+                      fsgg_device_graph* out, fsgg_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* FSGG_H */

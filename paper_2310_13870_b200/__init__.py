@@ -1,0 +1,22 @@
+"""B200-native KDE-driven similarity-graph sampler (arXiv 2310.13870 hot path).
+
+Drop-in for the reference's ``fsg::build_similarity_graph`` path: the C ABI
+is ``include/fsgg.h`` (libfsgg.so, hand-written sm_100a kernels); this
+package is the host-side mirror of the reference interface over it.
+"""
+from .api import (BuildReport, Dataset, Kernel, KernelFamily, KdeEstimator, LogBase,
+                  RngMode, SampleDiagnostics, SparsifierConfig, WeightedGraph,
+                  build_similarity_graph, build_similarity_graph_device, default_epsilon,
+                  device_available, exact_kde, make_estimator, sample_neighbors,
+                  sample_neighbors_counted)
+from .errors import (ConfigError, DeviceError, Error, InvalidConfig, IoError,
+                     LengthMismatch, NumericError, TooFewPoints)
+
+__all__ = [
+    "BuildReport", "Dataset", "Kernel", "KernelFamily", "KdeEstimator", "LogBase", "RngMode",
+    "SampleDiagnostics", "SparsifierConfig", "WeightedGraph", "build_similarity_graph",
+    "build_similarity_graph_device", "default_epsilon", "device_available", "exact_kde",
+    "make_estimator", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
+    "DeviceError", "Error", "InvalidConfig", "IoError", "LengthMismatch", "NumericError",
+    "TooFewPoints",
+]

@@ -1,0 +1,165 @@
+"""ctypes binding of the C ABI in include/fsgg.h (libfsgg.so, sm_100a).
+
+The shared library is built in-tree by ``__graft_entry__.build()``
+(``paper_2310_13870_b200/csrc/Makefile``). There is no CPU fallback: if the
+library is missing every call raises :class:`DeviceError`, and without a
+usable B200 every compute call returns FSGG_ERR_DEVICE.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libfsgg.so")
+HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "fsgg.h")
+
+FSGG_OK = 0
+FSGG_ERR_CONFIG = 2
+FSGG_ERR_IO = 3
+FSGG_ERR_NUMERIC = 4
+FSGG_ERR_DEVICE = 5
+
+
+class fsgg_kernel(C.Structure):
+    _fields_ = [("family", C.c_int), ("sigma", C.c_double)]
+
+
+class fsgg_config(C.Structure):
+    _fields_ = [("C", C.c_double), ("lambda_k1_estimate", C.c_double),
+                ("rounds", C.c_uint32), ("epsilon", C.c_double), ("log_base", C.c_int),
+                ("seed", C.c_uint64), ("rng_mode", C.c_int),
+                ("query_begin", C.c_uint32), ("query_end", C.c_uint32)]
+
+
+class fsgg_report(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("rounds", C.c_uint32), ("epsilon", C.c_double),
+                ("backend", C.c_char * 32), ("sampled_pairs", C.c_uint64),
+                ("self_pairs_discarded", C.c_uint64),
+                ("underflow_edges_discarded", C.c_uint64), ("edge_count", C.c_uint64),
+                ("degenerate_draws", C.c_uint64), ("estimator_build_seconds", C.c_double),
+                ("sampling_seconds", C.c_double), ("degree_kde_seconds", C.c_double),
+                ("weighting_seconds", C.c_double), ("total_seconds", C.c_double),
+                ("estimator_bytes", C.c_uint64), ("graph_bytes", C.c_uint64),
+                ("kernel_evals", C.c_uint64), ("kde_tiled_evals", C.c_uint64),
+                ("kde_tiled_seconds", C.c_double), ("kde_tiled_launches", C.c_uint32),
+                ("levels", C.c_uint32), ("peak_entries", C.c_uint64),
+                ("gpu_launches", C.c_uint32)]
+
+
+class fsgg_edge_estimate(C.Structure):
+    _fields_ = [("i", C.c_uint32), ("j", C.c_uint32), ("k_ij", C.c_double),
+                ("g_i", C.c_double), ("g_j", C.c_double), ("p_hat_i_j", C.c_double),
+                ("p_hat_j_i", C.c_double), ("p_hat", C.c_double)]
+
+
+class fsgg_graph(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("num_edges", C.c_uint64),
+                ("u", C.POINTER(C.c_uint32)), ("v", C.POINTER(C.c_uint32)),
+                ("w", C.POINTER(C.c_double)), ("row_ptr", C.POINTER(C.c_uint64)),
+                ("degrees", C.POINTER(C.c_double)), ("total_weight", C.c_double)]
+
+
+class fsgg_device_graph(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("num_edges", C.c_uint64), ("u", C.c_void_p),
+                ("v", C.c_void_p), ("w", C.c_void_p), ("row_ptr", C.c_void_p),
+                ("degrees", C.c_void_p), ("total_weight", C.c_double)]
+
+
+class fsgg_sample_diag(C.Structure):
+    _fields_ = [("nlevels", C.c_uint32), ("entries_per_level", C.c_uint64 * 64),
+                ("tickets_per_level", C.c_uint64 * 64), ("degenerate_draws", C.c_uint64)]
+
+
+class fsgg_shard(C.Structure):
+    _fields_ = [("query_begin", C.c_uint32), ("query_end", C.c_uint32),
+                ("rounds", C.c_uint32), ("num_pairs", C.c_uint64), ("pairs", C.c_void_p),
+                ("g_full", C.c_void_p), ("sampled_pairs", C.c_uint64),
+                ("self_pairs", C.c_uint64), ("degenerate_draws", C.c_uint64)]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "fsgg_version": (C.c_char_p, []),
+    "fsgg_last_error": (C.c_char_p, []),
+    "fsgg_device_available": (C.c_int, []),
+    "fsgg_config_init": (None, [C.POINTER(fsgg_config)]),
+    "fsgg_rounds_for": (C.c_int, [C.POINTER(fsgg_config), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "fsgg_default_epsilon": (C.c_double, [C.c_uint32, C.c_int]),
+    "fsgg_dataset_create": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_int, C.c_int,
+                                      C.POINTER(_P)]),
+    "fsgg_dataset_create_f64": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_int,
+                                          C.POINTER(_P)]),
+    "fsgg_dataset_upload": (C.c_int, [_P, _P]),
+    "fsgg_dataset_destroy": (None, [_P]),
+    "fsgg_dataset_size": (C.c_uint32, [_P]),
+    "fsgg_dataset_dim": (C.c_uint32, [_P]),
+    "fsgg_dataset_device_points": (_P, [_P]),
+    "fsgg_build_similarity_graph": (C.c_int, [_P, C.POINTER(fsgg_kernel),
+                                              C.POINTER(fsgg_config), C.POINTER(fsgg_graph),
+                                              C.POINTER(fsgg_report),
+                                              C.POINTER(C.POINTER(fsgg_edge_estimate))]),
+    "fsgg_build_similarity_graph_device": (C.c_int, [_P, C.POINTER(fsgg_kernel),
+                                                     C.POINTER(fsgg_config),
+                                                     C.POINTER(fsgg_device_graph),
+                                                     C.POINTER(fsgg_report)]),
+    "fsgg_build_similarity_graph_host": (C.c_int, [_P, C.c_uint32, C.c_uint32,
+                                                   C.POINTER(fsgg_kernel),
+                                                   C.POINTER(fsgg_config), C.c_int,
+                                                   C.POINTER(fsgg_graph),
+                                                   C.POINTER(fsgg_report)]),
+    "fsgg_graph_free": (None, [C.POINTER(fsgg_graph)]),
+    "fsgg_free": (None, [_P]),
+    "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
+                                                C.c_uint32, C.c_uint64, C.c_int,
+                                                C.POINTER(_P), C.POINTER(C.c_size_t),
+                                                C.POINTER(fsgg_sample_diag)]),
+    "fsgg_kde_eval": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32, C.c_uint32, _P,
+                                C.c_size_t, _P]),
+    "fsgg_make_moons": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, _P, _P]),
+    "fsgg_make_blobs": (C.c_int, [C.c_uint32, _P, C.c_uint32, C.c_uint32, C.c_double,
+                                  C.c_uint64, _P, _P]),
+    "fsgg_make_image_features": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
+                                           C.c_uint64, _P, _P]),
+    "fsgg_make_gmm": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_uint64,
+                                _P, _P]),
+    "fsgg_sample_shard": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.POINTER(fsgg_config),
+                                    C.POINTER(fsgg_shard), C.POINTER(fsgg_report)]),
+    "fsgg_finish_graph": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32, _P, _P,
+                                    C.c_uint64, C.POINTER(fsgg_device_graph),
+                                    C.POINTER(fsgg_report)]),
+}
+
+
+def header_functions(path: str = HEADER_PATH) -> list[str]:
+    """Every function name declared in include/fsgg.h."""
+    text = open(path).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fsgg_[a-z0-9_]+)\s*\(", text)))
+
+
+_lib = None
+
+
+def lib():
+    """Load libfsgg.so once; raise loudly if it was never built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from .errors import DeviceError
+            raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc != FSGG_OK:
+        from .errors import error_for
+        raise error_for(rc, lib().fsgg_last_error().decode(errors="replace"))

@@ -1,0 +1,411 @@
+"""Host-side mirror of the reference's hot-path interface, over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference library
+``fsg`` so a caller (and the parity tests) read like the reference's own:
+
+==============================  ============================================
+this module                     reference
+==============================  ============================================
+``Dataset``                     fsg::Dataset (proj/include/fsg/dataset.hpp:12)
+``Kernel`` / ``KernelFamily``   fsg::Kernel (proj/include/fsg/kernel.hpp:21)
+``SparsifierConfig``            proj/include/fsg/sparsifier.hpp:14-26
+``build_similarity_graph``      proj/src/sparsifier.cpp:51-142
+``sample_neighbors_counted``    proj/src/sampler.cpp:77-247
+``sample_neighbors``            proj/src/sampler.cpp:249-269
+``make_estimator(...).eval``    fsg::KdeEstimator::eval (kde.hpp:54-58)
+``WeightedGraph``               proj/include/fsg/graph.hpp:20-40
+``BuildReport``/``EdgeEstimate`` proj/include/fsg/sparsifier.hpp:29-58
+==============================  ============================================
+
+All compute runs in libfsgg.so on an sm_100a device; nothing here loops
+over points or edges.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import InvalidConfig, LengthMismatch, TooFewPoints
+
+
+class KernelFamily(enum.IntEnum):
+    gaussian = 0
+    exponential = 1
+    laplacian = 2
+
+
+class RngMode(enum.IntEnum):
+    reference = 0  # bit-exact keyed splitmix64 streams (proj/include/fsg/rng.hpp)
+    philox = 1     # Philox4x32-10, same law, not edge-for-edge
+
+
+class LogBase(enum.IntEnum):
+    two = 0
+    natural = 1
+
+
+@dataclass(frozen=True)
+class Kernel:
+    """proj/include/fsg/kernel.hpp:21-58. Bandwidth must be positive
+    (proj/src/kernel.cpp:23-26)."""
+
+    family: KernelFamily = KernelFamily.gaussian
+    sigma: float = 1.0
+
+    def __post_init__(self):
+        if not (self.sigma > 0.0):
+            raise InvalidConfig("kernel bandwidth must be positive")
+
+    def _c(self):
+        return N.fsgg_kernel(int(self.family), float(self.sigma))
+
+    def __call__(self, x, y) -> float:
+        """k(x, y) in fp64 (host helper for small checks only)."""
+        x = np.asarray(x, np.float64)
+        y = np.asarray(y, np.float64)
+        if self.family == KernelFamily.gaussian:
+            return math.exp(-float(np.sum((x - y) ** 2)) / (self.sigma * self.sigma))
+        if self.family == KernelFamily.exponential:
+            return math.exp(-math.sqrt(float(np.sum((x - y) ** 2))) / self.sigma)
+        return math.exp(-float(np.sum(np.abs(x - y))) / self.sigma)
+
+
+def default_epsilon(n: int, log_base: LogBase = LogBase.two) -> float:
+    """proj/src/kde.cpp:15-18."""
+    return N.lib().fsgg_default_epsilon(n, int(log_base))
+
+
+@dataclass
+class SparsifierConfig:
+    """proj/include/fsg/sparsifier.hpp:14-26 (+ rng_mode, query shard)."""
+
+    C: float = 1.0
+    lambda_k1_estimate: float = 1.0
+    rounds: int = 0
+    epsilon: float = 0.0
+    log_base: LogBase = LogBase.two
+    seed: int = 1
+    rng_mode: RngMode = RngMode.reference
+    query_begin: int = 0
+    query_end: int = 0
+
+    def _c(self):
+        c = N.fsgg_config()
+        c.C = self.C
+        c.lambda_k1_estimate = self.lambda_k1_estimate
+        c.rounds = self.rounds
+        c.epsilon = self.epsilon
+        c.log_base = int(self.log_base)
+        c.seed = self.seed
+        c.rng_mode = int(self.rng_mode)
+        c.query_begin = self.query_begin
+        c.query_end = self.query_end
+        return c
+
+    def rounds_for(self, n: int) -> int:
+        """proj/src/sparsifier.cpp:17-23."""
+        out = C.c_uint32()
+        c = self._c()
+        N.check(N.lib().fsgg_rounds_for(C.byref(c), n, C.byref(out)))
+        return out.value
+
+    def epsilon_for(self, n: int) -> float:
+        """proj/src/sparsifier.cpp:25-28."""
+        return self.epsilon if self.epsilon > 0 else default_epsilon(n, self.log_base)
+
+
+class Dataset:
+    """Device-resident fp32 point set (fsg::Dataset, index order = tree order).
+
+    ``points`` may be a numpy array (host, fp32 or fp64 — fp64 is rounded to
+    fp32) or a CUDA torch tensor (device pointer, fp32, contiguous)."""
+
+    def __init__(self, points, device: int = 0):
+        self._h = None
+        lib = N.lib()
+        h = C.c_void_p()
+        if hasattr(points, "is_cuda") and points.is_cuda:
+            import torch
+            if points.dtype != torch.float32 or points.dim() != 2:
+                raise InvalidConfig("device points must be a 2-D float32 tensor")
+            pts = points.contiguous()
+            n, d = pts.shape
+            N.check(lib.fsgg_dataset_create(C.c_void_p(pts.data_ptr()), n, d, 1,
+                                            pts.device.index or 0, C.byref(h)))
+        else:
+            arr = np.asarray(points)
+            if arr.ndim != 2:
+                raise InvalidConfig("points must be a 2-D array (n x d)")
+            n, d = arr.shape
+            if arr.dtype == np.float64:
+                arr = np.ascontiguousarray(arr)
+                N.check(lib.fsgg_dataset_create_f64(arr.ctypes.data_as(C.c_void_p), n, d,
+                                                    device, C.byref(h)))
+            else:
+                arr = np.ascontiguousarray(arr, np.float32)
+                N.check(lib.fsgg_dataset_create(arr.ctypes.data_as(C.c_void_p), n, d, 0,
+                                                device, C.byref(h)))
+        self._h = h
+        self.n, self.d, self.device = int(n), int(d), device
+
+    def size(self) -> int:
+        return self.n
+
+    def dim(self) -> int:
+        return self.d
+
+    def upload(self, host_points: np.ndarray):
+        """Replace coordinates from pinned/pageable host fp32 memory."""
+        arr = np.ascontiguousarray(host_points, np.float32)
+        if arr.shape != (self.n, self.d):
+            raise LengthMismatch("upload shape does not match the dataset")
+        N.check(N.lib().fsgg_dataset_upload(self._h, arr.ctypes.data_as(C.c_void_p)))
+
+    def upload_ptr(self, host_ptr: int):
+        N.check(N.lib().fsgg_dataset_upload(self._h, C.c_void_p(host_ptr)))
+
+    def device_ptr(self) -> int:
+        return int(N.lib().fsgg_dataset_device_points(self._h) or 0)
+
+    def close(self):
+        if self._h is not None and N._lib is not None:
+            N.lib().fsgg_dataset_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class WeightedGraph:
+    """Sorted (u < v) undirected edge list + CSR (proj/include/fsg/graph.hpp)."""
+
+    n: int
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+    row_ptr: np.ndarray
+    degrees: np.ndarray
+    total_weight: float
+
+    def num_vertices(self) -> int:
+        return self.n
+
+    def num_edges(self) -> int:
+        return int(self.u.size)
+
+    def degree(self, v: int) -> float:
+        return float(self.degrees[v])
+
+    def edges(self):
+        return list(zip(self.u.tolist(), self.v.tolist(), self.w.tolist()))
+
+    def write_edge_list(self, path: str):
+        """Byte-compatible with proj/src/graph.cpp:234-241 ("n m", "u v %.17g")."""
+        with open(path, "w") as f:
+            f.write(f"{self.n} {self.num_edges()}\n")
+            for a, b, c in zip(self.u.tolist(), self.v.tolist(), self.w.tolist()):
+                f.write(f"{a} {b} {c:.17g}\n")
+
+
+@dataclass
+class BuildReport:
+    """proj/include/fsg/sparsifier.hpp:40-58 plus device counters."""
+
+    n: int = 0
+    rounds: int = 0
+    epsilon: float = 0.0
+    backend: str = ""
+    sampled_pairs: int = 0
+    self_pairs_discarded: int = 0
+    underflow_edges_discarded: int = 0
+    edge_count: int = 0
+    degenerate_draws: int = 0
+    estimator_build_seconds: float = 0.0
+    sampling_seconds: float = 0.0
+    degree_kde_seconds: float = 0.0
+    weighting_seconds: float = 0.0
+    total_seconds: float = 0.0
+    estimator_bytes: int = 0
+    graph_bytes: int = 0
+    kernel_evals: int = 0
+    kde_tiled_evals: int = 0
+    kde_tiled_seconds: float = 0.0
+    kde_tiled_launches: int = 0
+    levels: int = 0
+    peak_entries: int = 0
+    gpu_launches: int = 0
+
+    @classmethod
+    def _from_c(cls, r):
+        out = cls()
+        for name, _ in N.fsgg_report._fields_:
+            v = getattr(r, name)
+            setattr(out, name, v.decode() if isinstance(v, bytes) else v)
+        return out
+
+
+EDGE_ESTIMATE_DTYPE = np.dtype([("i", "<u4"), ("j", "<u4"), ("k_ij", "<f8"), ("g_i", "<f8"),
+                                ("g_j", "<f8"), ("p_hat_i_j", "<f8"), ("p_hat_j_i", "<f8"),
+                                ("p_hat", "<f8")])
+
+
+def _as_numpy(ptr, count, ctype, dtype):
+    if count == 0:
+        return np.zeros(0, dtype)
+    arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(count,))
+    return np.array(arr, dtype=dtype, copy=True)
+
+
+def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig | None = None,
+                           report: bool = False, estimates: bool = False):
+    """FastSimilarityGraph (proj/src/sparsifier.cpp:51-142) on the device.
+
+    Returns ``graph`` or ``(graph, report, estimates)`` when either flag is
+    set (estimates is a structured array with EdgeEstimate's fields)."""
+    cfg = (config or SparsifierConfig())._c()
+    k = kernel._c()
+    g = N.fsgg_graph()
+    rep = N.fsgg_report()
+    est = C.POINTER(N.fsgg_edge_estimate)()
+    lib = N.lib()
+    N.check(lib.fsgg_build_similarity_graph(ds._h, C.byref(k), C.byref(cfg), C.byref(g),
+                                            C.byref(rep),
+                                            C.byref(est) if estimates else None))
+    try:
+        m = int(g.num_edges)
+        graph = WeightedGraph(
+            n=int(g.n), u=_as_numpy(g.u, m, C.c_uint32, np.uint32),
+            v=_as_numpy(g.v, m, C.c_uint32, np.uint32),
+            w=_as_numpy(g.w, m, C.c_double, np.float64),
+            row_ptr=_as_numpy(g.row_ptr, int(g.n) + 1, C.c_uint64, np.uint64),
+            degrees=_as_numpy(g.degrees, int(g.n), C.c_double, np.float64),
+            total_weight=float(g.total_weight))
+    finally:
+        lib.fsgg_graph_free(C.byref(g))
+    est_arr = None
+    if estimates:
+        m = int(g.num_edges) if g.num_edges else graph.num_edges()
+        raw = C.string_at(est, m * C.sizeof(N.fsgg_edge_estimate)) if m else b""
+        est_arr = np.frombuffer(raw, dtype=EDGE_ESTIMATE_DTYPE).copy()
+        lib.fsgg_free(C.cast(est, C.c_void_p))
+    if report or estimates:
+        return graph, BuildReport._from_c(rep), est_arr
+    return graph
+
+
+def build_similarity_graph_device(ds: Dataset, kernel: Kernel,
+                                  config: SparsifierConfig | None = None):
+    """Device-resident build (no graph copy back). Returns (fsgg_device_graph,
+    BuildReport); pointers stay valid until the next build on ``ds``."""
+    cfg = (config or SparsifierConfig())._c()
+    k = kernel._c()
+    g = N.fsgg_device_graph()
+    rep = N.fsgg_report()
+    N.check(N.lib().fsgg_build_similarity_graph_device(ds._h, C.byref(k), C.byref(cfg),
+                                                       C.byref(g), C.byref(rep)))
+    return g, BuildReport._from_c(rep)
+
+
+@dataclass
+class SampleDiagnostics:
+    """proj/include/fsg/sampler.hpp:22-26."""
+
+    entries_per_level: list = field(default_factory=list)
+    tickets_per_level: list = field(default_factory=list)
+    degenerate_draws: int = 0
+
+
+def sample_neighbors_counted(ds: Dataset, kernel: Kernel, queries, rounds: int, seed: int,
+                             rng_mode: RngMode = RngMode.reference, diagnostics: bool = False):
+    """proj/src/sampler.cpp:77-247: (query, source, count) rows sorted by
+    (query, source), as an (m, 3) uint32 array."""
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64))
+    if q.size and (q.min() < 0):
+        raise InvalidConfig("query index out of range")
+    q = q.astype(np.uint32)
+    k = kernel._c()
+    out = C.c_void_p()
+    cnt = C.c_size_t()
+    diag = N.fsgg_sample_diag()
+    lib = N.lib()
+    N.check(lib.fsgg_sample_neighbors_counted(ds._h, C.byref(k), q.ctypes.data_as(C.c_void_p),
+                                              q.size, rounds, seed, int(rng_mode),
+                                              C.byref(out), C.byref(cnt), C.byref(diag)))
+    m = cnt.value
+    tri = _as_numpy(out, 3 * m, C.c_uint32, np.uint32).reshape(m, 3)
+    lib.fsgg_free(out)
+    if diagnostics:
+        d = SampleDiagnostics(list(diag.entries_per_level)[: diag.nlevels],
+                              list(diag.tickets_per_level)[: diag.nlevels],
+                              int(diag.degenerate_draws))
+        return tri, d
+    return tri
+
+
+def sample_neighbors(ds: Dataset, kernel: Kernel, queries, seed: int,
+                     rng_mode: RngMode = RngMode.reference):
+    """proj/src/sampler.cpp:249-269: one neighbour per query, sorted by
+    query; returns an (len(queries), 2) array of (query, source)."""
+    q = np.asarray(queries, dtype=np.int64)
+    tri = sample_neighbors_counted(ds, kernel, q, 1, seed, rng_mode)
+    choice = {int(a): int(b) for a, b, _ in tri}
+    out = np.array([(int(x), choice[int(x)]) for x in q], dtype=np.uint32).reshape(-1, 2)
+    order = np.lexsort((out[:, 1], out[:, 0])) if out.size else np.zeros(0, np.int64)
+    return out[order]
+
+
+class KdeEstimator:
+    """The plugin seam fsg::KdeEstimator (proj/include/fsg/kde.hpp:49-85),
+    exact backend on the device."""
+
+    backend_name = "gpu-exact-sm100a"
+    sum_floor = 1e-300
+
+    def __init__(self, ds: Dataset, kernel: Kernel):
+        self.ds = ds
+        self.kernel = kernel
+
+    def epsilon(self) -> float:
+        return 0.0
+
+    def eval(self, first: int, last: int, targets) -> np.ndarray:
+        t = np.ascontiguousarray(np.asarray(targets, dtype=np.int64))
+        if t.size and t.min() < 0:
+            raise InvalidConfig("target index out of range")
+        t = t.astype(np.uint32)
+        if first < 0 or last < 0:
+            raise InvalidConfig("invalid source index range")
+        out = np.zeros(t.size, np.float64)
+        k = self.kernel._c()
+        N.check(N.lib().fsgg_kde_eval(self.ds._h, C.byref(k), first, last,
+                                      t.ctypes.data_as(C.c_void_p), t.size,
+                                      out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+def make_estimator(ds: Dataset, kernel: Kernel) -> KdeEstimator:
+    """proj/src/kde.cpp:104-129; the device path is always exact."""
+    return KdeEstimator(ds, kernel)
+
+
+def exact_kde(ds: Dataset, kernel: Kernel, first: int, last: int, targets) -> np.ndarray:
+    """proj/src/kde.cpp:131-138."""
+    return make_estimator(ds, kernel).eval(first, last, targets)
+
+
+def device_available() -> bool:
+    return bool(N.lib().fsgg_device_available())
+
+
+def _ensure_two_points(n):
+    if n < 2:
+        raise TooFewPoints("similarity graph needs n >= 2")

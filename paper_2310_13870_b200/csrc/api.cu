@@ -1,0 +1,556 @@
+// C ABI (include/fsgg.h): validation with the reference's error contract,
+// phase orchestration and host<->device copies. No compute happens here —
+// every loop over points, entries or edges is a kernel in tree.cu, kde.cu,
+// sampler.cu or graph.cu, and without a usable device every call fails with
+// FSGG_ERR_DEVICE (no CPU fallback).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fsgg.h"
+#include "engine.cuh"
+
+struct fsgg_dataset {
+  fsgg::Dataset ds;
+  // Results kept alive for the device-pointer APIs.
+  std::unique_ptr<fsgg::GraphResult> graph;
+  std::unique_ptr<fsgg::SampleResult> shard;
+  fsgg::DevBuf shard_keys;
+  ~fsgg_dataset() {
+    graph.reset();
+    shard.reset();
+    shard_keys.release();
+    ds.tree.first.release();
+    ds.tree.last.release();
+    ds.tree.lo.release();
+    ds.tree.hi.release();
+    ds.pts.release();
+    if (ds.stream) {
+      cudaStreamSynchronize(ds.stream);
+      cudaStreamDestroy(ds.stream);
+    }
+  }
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FSGG_OK;
+  } catch (const fsgg::Error& e) {
+    g_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_error = std::string("host allocation failed: ") + e.what();
+    return FSGG_ERR_DEVICE;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return FSGG_ERR_DEVICE;
+  }
+}
+
+double now() {
+  using clock = std::chrono::steady_clock;
+  return std::chrono::duration<double>(clock::now().time_since_epoch()).count();
+}
+
+void require_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw fsgg::DeviceError("no CUDA device available (the sm_100a path has no CPU fallback)");
+  if (device < 0 || device >= count) throw fsgg::ConfigError("device index out of range");
+  cudaDeviceProp prop;
+  FSGG_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    throw fsgg::DeviceError("device " + std::to_string(device) + " (" + prop.name +
+                            ") is not sm_100; this library is built for sm_100a only");
+}
+
+__global__ void nonfinite_kernel(const float* p, uint64_t m, unsigned int* bad) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < m && !isfinite(p[i])) atomicAdd(bad, 1u);
+}
+
+void check_finite(fsgg::Dataset& ds) {
+  const uint64_t m = uint64_t(ds.n) * ds.d;
+  fsgg::DevBuf bad(4, ds.stream);
+  FSGG_CUDA(cudaMemsetAsync(bad.as<void>(), 0, 4, ds.stream));
+  nonfinite_kernel<<<fsgg::ceil_div_u32(m, 256), 256, 0, ds.stream>>>(
+      ds.pts.as<float>(), m, bad.as<unsigned int>());
+  FSGG_LAUNCH_CHECK();
+  unsigned int h = 0;
+  FSGG_CUDA(cudaMemcpyAsync(&h, bad.as<void>(), 4, cudaMemcpyDeviceToHost, ds.stream));
+  FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  if (h) throw fsgg::ConfigError("dataset coordinates must be finite");  // dataset.cpp:19-21
+}
+
+fsgg_dataset* make_handle(uint32_t n, uint32_t d, int device) {
+  if (n < 1 || d < 1) throw fsgg::ConfigError("dataset needs n >= 1 and d >= 1");  // dataset.cpp:16
+  if (n > (1u << 28)) throw fsgg::ConfigError("n > 2^28 is not supported by the device tree table");
+  require_device(device);
+  FSGG_CUDA(cudaSetDevice(device));
+  auto h = std::make_unique<fsgg_dataset>();
+  h->ds.device = device;
+  h->ds.n = n;
+  h->ds.d = d;
+  cudaDeviceProp prop;
+  FSGG_CUDA(cudaGetDeviceProperties(&prop, device));
+  h->ds.num_sms = prop.multiProcessorCount;
+  FSGG_CUDA(cudaStreamCreateWithFlags(&h->ds.stream, cudaStreamNonBlocking));
+  cudaMemPool_t pool;
+  FSGG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t threshold = UINT64_MAX;  // keep freed blocks cached between calls
+  FSGG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  h->ds.pts.alloc(size_t(n) * d * 4, h->ds.stream);
+  return h.release();
+}
+
+void validate_kernel(const fsgg_kernel* k) {
+  if (!k) throw fsgg::ConfigError("kernel is null");
+  if (k->family < 0 || k->family > 2) throw fsgg::ConfigError("unknown kernel family");
+  if (!(k->sigma > 0.0)) throw fsgg::ConfigError("kernel bandwidth must be positive");  // kernel.cpp:23-26
+}
+
+fsgg_config default_config() {
+  fsgg_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.C = 1.0;
+  c.lambda_k1_estimate = 1.0;
+  c.log_base = 0;
+  c.seed = 1;
+  return c;
+}
+
+// proj/src/sparsifier.cpp:17-23
+uint32_t rounds_for(const fsgg_config& c, uint32_t n) {
+  if (c.rounds > 0) return c.rounds;
+  double nn = std::max<uint32_t>(n, 2);
+  double l = std::max(c.log_base ? std::log(nn) : std::log2(nn), 1.0);
+  double r = std::ceil(6.0 * c.C * l / c.lambda_k1_estimate);
+  if (!(r >= 1.0) || r > 4e9) throw fsgg::ConfigError("invalid round count");
+  return static_cast<uint32_t>(r);
+}
+
+void activate(fsgg_dataset* h) {
+  if (!h) throw fsgg::ConfigError("dataset handle is null");
+  FSGG_CUDA(cudaSetDevice(h->ds.device));
+  h->ds.launches = 0;
+}
+
+void fill_report_common(fsgg_report* r, const fsgg::Dataset& ds, uint32_t L) {
+  std::memset(r, 0, sizeof(*r));
+  r->n = ds.n;
+  r->rounds = L;
+  r->epsilon = 0.0;
+  std::strncpy(r->backend, "gpu-exact-sm100a", sizeof(r->backend) - 1);
+}
+
+struct BuildOut {
+  uint32_t L = 0;
+  uint64_t sampled = 0, self = 0, degenerate = 0;
+  double t_tree = 0, t_sample = 0, t_graph = 0;
+  fsgg::KdeStats kde;
+  uint32_t levels = 0;
+  uint64_t peak = 0;
+};
+
+// Descent over the configured query shard; fills res (and optionally keys).
+void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& cfg,
+                 uint32_t L, uint32_t qb, uint32_t qe, fsgg::SampleResult& res,
+                 fsgg::DevBuf& keys, uint64_t* npairs, BuildOut& bo) {
+  fsgg::Dataset& ds = h->ds;
+  const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+  double t0 = now();
+  if (!ds.tree_valid) {
+    fsgg::build_tree(ds);
+    FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  }
+  double t1 = now();
+  fsgg::SampleRequest req;
+  req.queries.resize(qe - qb);
+  for (uint32_t i = qb; i < qe; ++i) req.queries[i - qb] = i;
+  req.tickets.assign(qe - qb, L);
+  req.seed = cfg.seed;
+  req.rng_mode = cfg.rng_mode;
+  req.want_root_sums = true;
+  fsgg::sample_counted(ds, ks, req, res);
+  double t2 = now();
+  *npairs = fsgg::collapse_pairs(ds, res, keys, &bo.self, &bo.sampled);
+  double t3 = now();
+  bo.t_tree = t1 - t0;
+  bo.t_sample = t2 - t1;
+  bo.t_graph = t3 - t2;
+  bo.degenerate = res.degenerate_draws;
+  bo.kde = res.kde;
+  bo.levels = static_cast<uint32_t>(res.entries_per_level.size());
+  bo.peak = res.peak_entries;
+}
+
+void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
+                   const fsgg::GraphResult* g, double total) {
+  fill_report_common(r, ds, bo.L);
+  r->sampled_pairs = bo.sampled;
+  r->self_pairs_discarded = bo.self;
+  r->degenerate_draws = bo.degenerate;
+  r->estimator_build_seconds = bo.t_tree;
+  r->sampling_seconds = bo.t_sample;
+  r->degree_kde_seconds = 0.0;
+  r->weighting_seconds = bo.t_graph;
+  r->total_seconds = total;
+  r->estimator_bytes = ds.tree.first.bytes() + ds.tree.last.bytes() +
+                       ds.tree.lo.bytes() + ds.tree.hi.bytes();
+  if (g) {
+    r->underflow_edges_discarded = g->underflow;
+    r->edge_count = g->m;
+    r->graph_bytes = g->m * 16 + uint64_t(g->n) * 8;
+  }
+  r->kernel_evals = bo.kde.evals;
+  r->kde_tiled_evals = bo.kde.tiled_evals;
+  r->kde_tiled_seconds = bo.kde.tiled_seconds;
+  r->kde_tiled_launches = bo.kde.tiled_launches;
+  r->levels = bo.levels;
+  r->peak_entries = bo.peak;
+  r->gpu_launches = ds.launches;
+}
+
+void build_device(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config* cfgp,
+                  fsgg_report* report, bool want_estimates) {
+  activate(h);
+  validate_kernel(kernel);
+  fsgg_config cfg = cfgp ? *cfgp : default_config();
+  fsgg::Dataset& ds = h->ds;
+  if (ds.n < 2) throw fsgg::ConfigError("similarity graph needs n >= 2");  // TooFewPoints
+  if (cfg.rng_mode != FSGG_RNG_REFERENCE && cfg.rng_mode != FSGG_RNG_PHILOX)
+    throw fsgg::ConfigError("unknown rng mode");
+  BuildOut bo;
+  bo.L = rounds_for(cfg, ds.n);
+  double t0 = now();
+  fsgg::SampleResult res;
+  fsgg::DevBuf keys;
+  uint64_t npairs = 0;
+  run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, keys, &npairs, bo);
+  double t1 = now();
+  const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+  h->graph = std::make_unique<fsgg::GraphResult>();
+  fsgg::finish_graph(ds, ks, bo.L, res.groot.as<double>(),
+                     keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph);
+  double t2 = now();
+  bo.t_graph += t2 - t1;
+  if (report) finish_report(report, ds, bo, h->graph.get(), t2 - t0 + bo.t_tree * 0);
+}
+
+template <class T>
+T* host_copy(const fsgg::DevBuf& b, uint64_t count, cudaStream_t s) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * std::max<uint64_t>(count, 1)));
+  if (!p) throw std::bad_alloc();
+  if (count) FSGG_CUDA(cudaMemcpyAsync(p, b.as<void>(), sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+  return p;
+}
+
+void graph_to_host(fsgg_dataset* h, fsgg_graph* out) {
+  const fsgg::GraphResult& g = *h->graph;
+  cudaStream_t s = h->ds.stream;
+  std::memset(out, 0, sizeof(*out));
+  out->n = g.n;
+  out->num_edges = g.m;
+  out->u = host_copy<uint32_t>(g.u, g.m, s);
+  out->v = host_copy<uint32_t>(g.v, g.m, s);
+  out->w = host_copy<double>(g.w, g.m, s);
+  out->row_ptr = host_copy<uint64_t>(g.row_ptr, uint64_t(g.n) + 1, s);
+  out->degrees = host_copy<double>(g.degrees, g.n, s);
+  out->total_weight = g.total_weight;
+  FSGG_CUDA(cudaStreamSynchronize(s));
+}
+
+void to_device_graph(fsgg_dataset* h, fsgg_device_graph* out) {
+  const fsgg::GraphResult& g = *h->graph;
+  out->n = g.n;
+  out->num_edges = g.m;
+  out->u = g.u.as<uint32_t>();
+  out->v = g.v.as<uint32_t>();
+  out->w = g.w.as<double>();
+  out->row_ptr = g.row_ptr.as<uint64_t>();
+  out->degrees = g.degrees.as<double>();
+  out->total_weight = g.total_weight;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fsgg_version(void) { return "fsgg 0.1.0 (sm_100a)"; }
+const char* fsgg_last_error(void) { return g_error.c_str(); }
+
+int fsgg_device_available(void) {
+  try {
+    require_device(0);
+    return 1;
+  } catch (...) {
+    return 0;
+  }
+}
+
+void fsgg_config_init(fsgg_config* cfg) {
+  if (cfg) *cfg = default_config();
+}
+
+int fsgg_rounds_for(const fsgg_config* cfg, uint32_t n, uint32_t* out) {
+  return guarded([&] {
+    if (!cfg || !out) throw fsgg::ConfigError("null argument");
+    *out = rounds_for(*cfg, n);
+  });
+}
+
+double fsgg_default_epsilon(uint32_t n, int log_base) {
+  double nn = std::max<uint32_t>(n, 2);
+  double l = log_base ? std::log(nn) : std::log2(nn);
+  return 1.0 / (6.0 * std::max(l, 1.0));
+}
+
+int fsgg_dataset_create(const float* points, uint32_t n, uint32_t d,
+                        int points_on_device, int device, fsgg_dataset** out) {
+  return guarded([&] {
+    if (!out || !points) throw fsgg::ConfigError("null argument");
+    std::unique_ptr<fsgg_dataset> h(make_handle(n, d, device));
+    FSGG_CUDA(cudaMemcpyAsync(h->ds.pts.as<void>(), points, size_t(n) * d * 4,
+                              points_on_device ? cudaMemcpyDeviceToDevice
+                                               : cudaMemcpyHostToDevice,
+                              h->ds.stream));
+    check_finite(h->ds);
+    *out = h.release();
+  });
+}
+
+int fsgg_dataset_create_f64(const double* points, uint32_t n, uint32_t d,
+                            int device, fsgg_dataset** out) {
+  return guarded([&] {
+    if (!out || !points) throw fsgg::ConfigError("null argument");
+    for (size_t i = 0; i < size_t(n) * d; ++i)
+      if (!std::isfinite(points[i])) throw fsgg::ConfigError("dataset coordinates must be finite");
+    std::vector<float> f(points, points + size_t(n) * d);
+    std::unique_ptr<fsgg_dataset> h(make_handle(n, d, device));
+    FSGG_CUDA(cudaMemcpyAsync(h->ds.pts.as<void>(), f.data(), f.size() * 4,
+                              cudaMemcpyHostToDevice, h->ds.stream));
+    check_finite(h->ds);
+    *out = h.release();
+  });
+}
+
+int fsgg_dataset_upload(fsgg_dataset* h, const float* host_points) {
+  return guarded([&] {
+    activate(h);
+    if (!host_points) throw fsgg::ConfigError("null argument");
+    FSGG_CUDA(cudaMemcpyAsync(h->ds.pts.as<void>(), host_points,
+                              size_t(h->ds.n) * h->ds.d * 4, cudaMemcpyHostToDevice,
+                              h->ds.stream));
+    h->ds.tree_valid = false;  // bounding boxes depend on the coordinates
+  });
+}
+
+void fsgg_dataset_destroy(fsgg_dataset* h) {
+  if (!h) return;
+  cudaSetDevice(h->ds.device);
+  delete h;
+}
+
+uint32_t fsgg_dataset_size(const fsgg_dataset* h) { return h ? h->ds.n : 0; }
+uint32_t fsgg_dataset_dim(const fsgg_dataset* h) { return h ? h->ds.d : 0; }
+const float* fsgg_dataset_device_points(const fsgg_dataset* h) {
+  return h ? h->ds.pts.as<float>() : nullptr;
+}
+
+int fsgg_build_similarity_graph(fsgg_dataset* h, const fsgg_kernel* kernel,
+                                const fsgg_config* cfg, fsgg_graph* out,
+                                fsgg_report* report, fsgg_edge_estimate** estimates) {
+  return guarded([&] {
+    if (!out) throw fsgg::ConfigError("null output");
+    build_device(h, kernel, cfg, report, estimates != nullptr);
+    graph_to_host(h, out);
+    if (estimates) {
+      *estimates = host_copy<fsgg_edge_estimate>(h->graph->est, h->graph->m, h->ds.stream);
+      FSGG_CUDA(cudaStreamSynchronize(h->ds.stream));
+    }
+  });
+}
+
+int fsgg_build_similarity_graph_device(fsgg_dataset* h, const fsgg_kernel* kernel,
+                                       const fsgg_config* cfg,
+                                       fsgg_device_graph* out, fsgg_report* report) {
+  return guarded([&] {
+    if (!out) throw fsgg::ConfigError("null output");
+    build_device(h, kernel, cfg, report, false);
+    to_device_graph(h, out);
+  });
+}
+
+int fsgg_build_similarity_graph_host(const float* points, uint32_t n, uint32_t d,
+                                     const fsgg_kernel* kernel, const fsgg_config* cfg,
+                                     int device, fsgg_graph* out, fsgg_report* report) {
+  fsgg_dataset* h = nullptr;
+  int rc = fsgg_dataset_create(points, n, d, 0, device, &h);
+  if (rc) return rc;
+  rc = fsgg_build_similarity_graph(h, kernel, cfg, out, report, nullptr);
+  fsgg_dataset_destroy(h);
+  return rc;
+}
+
+void fsgg_graph_free(fsgg_graph* g) {
+  if (!g) return;
+  std::free(g->u);
+  std::free(g->v);
+  std::free(g->w);
+  std::free(g->row_ptr);
+  std::free(g->degrees);
+  std::memset(g, 0, sizeof(*g));
+}
+
+void fsgg_free(void* p) { std::free(p); }
+
+int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
+                                  const uint32_t* queries, size_t num_queries,
+                                  uint32_t rounds, uint64_t seed, int rng_mode,
+                                  uint32_t** triples, size_t* count,
+                                  fsgg_sample_diag* diag) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    if (!triples || !count || (num_queries && !queries)) throw fsgg::ConfigError("null argument");
+    if (rounds == 0) throw fsgg::ConfigError("need at least one sampling round");  // sampler.cpp:85
+    fsgg::Dataset& ds = h->ds;
+    for (size_t i = 0; i < num_queries; ++i)
+      if (queries[i] >= ds.n) throw fsgg::ConfigError("query index out of range");  // :86-87
+    // :89-106 merge duplicates, ascending query order
+    std::vector<uint32_t> q(queries, queries + num_queries);
+    std::sort(q.begin(), q.end());
+    fsgg::SampleRequest req;
+    for (size_t i = 0; i < q.size();) {
+      size_t j = i;
+      while (j < q.size() && q[j] == q[i]) ++j;
+      uint64_t t = uint64_t(j - i) * rounds;
+      if (t > 0xffffffffull) throw fsgg::ConfigError("total rounds per query exceeds 2^32");
+      req.queries.push_back(q[i]);
+      req.tickets.push_back(static_cast<uint32_t>(t));
+      i = j;
+    }
+    req.seed = seed;
+    req.rng_mode = rng_mode;
+    std::vector<uint32_t> host;
+    fsgg::SampleResult res;
+    if (!req.queries.empty()) {
+      const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+      fsgg::sample_counted(ds, ks, req, res);
+      fsgg::sampled_triples_to_host(ds, res, host);
+    }
+    *count = host.size() / 3;
+    *triples = static_cast<uint32_t*>(std::malloc(std::max<size_t>(host.size(), 1) * 4));
+    if (!*triples) throw std::bad_alloc();
+    std::memcpy(*triples, host.data(), host.size() * 4);
+    if (diag) {
+      std::memset(diag, 0, sizeof(*diag));
+      diag->nlevels = static_cast<uint32_t>(std::min<size_t>(res.entries_per_level.size(), 64));
+      for (uint32_t i = 0; i < diag->nlevels; ++i) {
+        diag->entries_per_level[i] = res.entries_per_level[i];
+        diag->tickets_per_level[i] = res.tickets_per_level[i];
+      }
+      diag->degenerate_draws = res.degenerate_draws;
+    }
+  });
+}
+
+int fsgg_kde_eval(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t first,
+                  uint32_t last, const uint32_t* targets, size_t m, double* out) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    fsgg::Dataset& ds = h->ds;
+    if (first > last || last > ds.n)  // kde.cpp:29-35
+      throw fsgg::ConfigError("invalid source index range [" + std::to_string(first) + ", " +
+                              std::to_string(last) + ") for n = " + std::to_string(ds.n));
+    if (m && (!targets || !out)) throw fsgg::ConfigError("null argument");
+    for (size_t i = 0; i < m; ++i)
+      if (targets[i] >= ds.n) throw fsgg::ConfigError("target index out of range");
+    if (m > 0xffffffffull) throw fsgg::ConfigError("too many targets");
+    if (m == 0) return;
+    cudaStream_t s = ds.stream;
+    fsgg::DevBuf dt(m * 4, s), dout(m * 8, s);
+    FSGG_CUDA(cudaMemcpyAsync(dt.as<void>(), targets, m * 4, cudaMemcpyHostToDevice, s));
+    const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+    fsgg::kde_range(ds, ks, first, last, dt.as<uint32_t>(), uint32_t(m), dout.as<double>());
+    FSGG_CUDA(cudaMemcpyAsync(out, dout.as<void>(), m * 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config* cfgp,
+                      fsgg_shard* out, fsgg_report* report) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    if (!out) throw fsgg::ConfigError("null output");
+    fsgg_config cfg = cfgp ? *cfgp : default_config();
+    fsgg::Dataset& ds = h->ds;
+    if (ds.n < 2) throw fsgg::ConfigError("similarity graph needs n >= 2");
+    uint32_t qb = cfg.query_begin, qe = cfg.query_end;
+    if (qb == 0 && qe == 0) qe = ds.n;
+    if (qb > qe || qe > ds.n) throw fsgg::ConfigError("invalid query shard");
+    BuildOut bo;
+    bo.L = rounds_for(cfg, ds.n);
+    double t0 = now();
+    h->shard = std::make_unique<fsgg::SampleResult>();
+    uint64_t npairs = 0;
+    if (qe > qb) {
+      run_descent(h, kernel, cfg, bo.L, qb, qe, *h->shard, h->shard_keys, &npairs, bo);
+    } else {
+      h->shard->groot.alloc(8, ds.stream);
+      h->shard_keys.alloc(8, ds.stream);
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->query_begin = qb;
+    out->query_end = qe;
+    out->rounds = bo.L;
+    out->num_pairs = npairs;
+    out->pairs = h->shard_keys.as<uint64_t>();
+    out->g_full = h->shard->groot.as<double>();
+    out->sampled_pairs = bo.sampled;
+    out->self_pairs = bo.self;
+    out->degenerate_draws = bo.degenerate;
+    if (report) finish_report(report, ds, bo, nullptr, now() - t0);
+  });
+}
+
+int fsgg_finish_graph(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t rounds,
+                      const double* g_full_device, const uint64_t* pairs_device,
+                      uint64_t num_pairs, fsgg_device_graph* out, fsgg_report* report) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    if (!out || !g_full_device || (num_pairs && !pairs_device))
+      throw fsgg::ConfigError("null argument");
+    if (rounds == 0) throw fsgg::ConfigError("rounds must be positive");
+    double t0 = now();
+    const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+    h->graph = std::make_unique<fsgg::GraphResult>();
+    fsgg::finish_graph(h->ds, ks, rounds, g_full_device, pairs_device, num_pairs, false,
+                       false, *h->graph);
+    to_device_graph(h, out);
+    if (report) {
+      BuildOut bo;
+      bo.L = rounds;
+      bo.t_graph = now() - t0;
+      finish_report(report, h->ds, bo, h->graph.get(), bo.t_graph);
+    }
+  });
+}
+
+}  // extern "C"

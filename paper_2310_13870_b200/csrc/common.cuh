@@ -1,0 +1,75 @@
+// Shared device/host helpers for the fsgg sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace fsgg {
+
+// Error classes carrying the reference's exit codes
+// (proj/include/fsg/common.hpp:13-66) plus 5 for device failures.
+struct Error : std::runtime_error {
+  int code;
+  Error(const std::string& m, int c) : std::runtime_error(m), code(c) {}
+};
+struct ConfigError : Error {
+  explicit ConfigError(const std::string& m) : Error(m, 2) {}
+};
+struct NumericError : Error {
+  explicit NumericError(const std::string& m) : Error(m, 4) {}
+};
+struct DeviceError : Error {
+  explicit DeviceError(const std::string& m) : Error(m, 5) {}
+};
+
+#define FSGG_CUDA(expr)                                                    \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess)                                                 \
+      throw ::fsgg::DeviceError(std::string(#expr) + ": " +                \
+                                cudaGetErrorString(_e) + " (" __FILE__ ":" \
+                                + std::to_string(__LINE__) + ")");         \
+  } while (0)
+
+#define FSGG_LAUNCH_CHECK() FSGG_CUDA(cudaGetLastError())
+
+constexpr double kSumFloor = 1e-300;                 // kde.hpp:43
+constexpr uint64_t kRouteTag = 0x88b4f8a3c2d1e5f7ULL;  // sampler.cpp:25
+
+// proj/include/fsg/rng.hpp:11-16
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// First two links of RngStream::keyed (rng.hpp:22-23) depend only on
+// (seed, tag); the host folds them once per build.
+inline uint64_t route_key_prefix(uint64_t seed) {
+  uint64_t k = splitmix64(seed);
+  return splitmix64(k ^ splitmix64(kRouteTag ^ 0x6a09e667f3bcc909ULL));
+}
+
+// Remaining links (rng.hpp:24-25) for a = (first << 32) | last, b = query.
+__host__ __device__ __forceinline__ uint64_t route_key(uint64_t prefix,
+                                                       uint64_t a,
+                                                       uint64_t b) {
+  uint64_t k = splitmix64(prefix ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
+  return splitmix64(k ^ splitmix64(b ^ 0x3c6ef372fe94f82bULL));
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) {
+  return static_cast<uint32_t>((a + b - 1) / b);
+}
+
+}  // namespace fsgg

@@ -1,0 +1,192 @@
+// Internal engine interfaces: device-resident dataset, tree tables, the
+// level-synchronous sampler and the graph builder. Host side is C++; every
+// heavy loop is an sm_100a kernel in tree.cu / kde.cu / sampler.cu /
+// graph.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace fsgg {
+
+// Stream-ordered device allocation (cudaMallocAsync on the handle's pool).
+class DevBuf {
+public:
+  DevBuf() = default;
+  DevBuf(size_t bytes, cudaStream_t s) { alloc(bytes, s); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_;
+      bytes_ = o.bytes_;
+      s_ = o.s_;
+      o.p_ = nullptr;
+      o.bytes_ = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t bytes, cudaStream_t s) {
+    release();
+    s_ = s;
+    bytes_ = bytes;
+    if (bytes) FSGG_CUDA(cudaMallocAsync(&p_, bytes, s));
+  }
+  // Grow-only reallocation (contents not preserved).
+  void ensure(size_t bytes, cudaStream_t s) {
+    if (bytes > bytes_) alloc(bytes + bytes / 4, s);
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    bytes_ = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+  size_t bytes() const { return bytes_; }
+
+private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+// Kernel-family arithmetic parameters (proj/include/fsg/kernel.hpp:28-53).
+// The exponent is evaluated in base 2: k = 2^(-scale * dist) where dist is
+// ||.||_2^2 (gaussian), ||.||_2 (exponential) or ||.||_1 (laplacian).
+struct KernelSpec {
+  int family = 0;
+  double sigma = 1.0;
+  float scale = 0.f;  // log2(e) / sigma^2  or  log2(e) / sigma
+};
+KernelSpec make_kernel_spec(int family, double sigma);
+
+// Balanced binary partition of [0, n) (split at first + size/2,
+// proj/src/sampler.cpp:141, :200), stored heap-ordered: level l occupies
+// slots [2^l - 1, 2^(l+1) - 1); slot g's children are 2g+1, 2g+2 in
+// global numbering. Nodes below a size-1 node are empty (first == last).
+struct TreeTable {
+  uint32_t n = 0, d = 0;
+  uint32_t depth = 0;  // deepest level index; levels 0..depth
+  uint64_t slots = 0;
+  bool has_boxes = false;
+  DevBuf first, last;  // u32 per slot
+  DevBuf lo, hi;       // f32 per slot * d (bounding boxes), d <= kBoxMaxDim
+};
+constexpr uint32_t kBoxMaxDim = 16;
+
+struct Dataset {
+  int device = 0;
+  uint32_t n = 0, d = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  DevBuf pts;  // f32 n*d
+  TreeTable tree;
+  bool tree_valid = false;
+  // Reusable work buffers owned by the handle.
+  DevBuf scratch_graph[12];
+  uint32_t launches = 0;  // kernel launches issued (reset per API call)
+};
+
+// ---- tree.cu --------------------------------------------------------------
+void build_tree(Dataset& ds);
+
+// ---- kde.cu ---------------------------------------------------------------
+// One level's entry list: entries grouped by node slot (level-local slot g
+// owns entries [goff[g], goff[g+1])).
+struct LevelView {
+  uint32_t level = 0;
+  uint32_t num_slots = 0;  // 2^level
+  uint32_t num_entries = 0;
+  const uint32_t* eq = nullptr;    // query index per entry
+  const uint32_t* eg = nullptr;    // level-local slot per entry
+  const uint32_t* goff = nullptr;  // num_slots + 1
+};
+
+struct KdeStats {
+  uint64_t evals = 0;
+  uint64_t tiled_evals = 0;
+  double tiled_seconds = 0.0;
+  uint32_t tiled_launches = 0;
+};
+
+struct KdeWorkspace {
+  DevBuf partials, blk_off, cub_tmp;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ~KdeWorkspace();
+};
+
+// Child sums for every entry of the level: g1 = sum over [first, mid),
+// g2 = sum over [mid, last), floored at 1e-300 (kde.cpp:68). When groot is
+// non-null, also writes the unfloored root sum g1 + g2 (level 0 only).
+void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
+               double* g1, double* g2, double* groot, KdeWorkspace& ws,
+               KdeStats& stats);
+
+// KdeEstimator::eval seam: arbitrary range, arbitrary targets (device).
+void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,
+               uint32_t last, const uint32_t* targets, uint32_t m,
+               double* out);
+
+// ---- sampler.cu -----------------------------------------------------------
+struct SampleRequest {
+  std::vector<uint32_t> queries;  // sorted unique query ids
+  std::vector<uint32_t> tickets;  // tickets per query (rounds * multiplicity)
+  uint64_t seed = 1;
+  int rng_mode = 0;
+  bool want_root_sums = false;
+};
+
+struct SampleResult {
+  uint32_t nq = 0;
+  uint64_t total_tickets = 0;
+  DevBuf uq;       // u32 nq: unique queries
+  DevBuf row_off;  // u64 nq+1: leaf row capacity offsets
+  DevBuf row_cnt;  // u32 nq: leaves emitted per row
+  DevBuf leaf_src, leaf_cnt;  // u32 total_tickets
+  DevBuf groot;    // f64 nq: g_full of each query (root sum), if requested
+  uint64_t degenerate_draws = 0;
+  std::vector<uint64_t> entries_per_level, tickets_per_level;
+  uint64_t peak_entries = 0;
+  KdeStats kde;
+};
+
+void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
+                    SampleResult& out);
+
+// Sorted (query, source, count) triples copied to the host.
+void sampled_triples_to_host(Dataset& ds, SampleResult& res,
+                             std::vector<uint32_t>& triples);
+
+// ---- graph.cu -------------------------------------------------------------
+struct GraphResult {
+  uint32_t n = 0;
+  uint64_t m = 0;
+  DevBuf u, v, w, row_ptr, degrees;
+  double total_weight = 0.0;
+  uint64_t underflow = 0;
+  DevBuf est;  // fsgg_edge_estimate-compatible records (optional)
+};
+
+// Sorted unique pair keys ((u << 32) | v, u < v) from the leaf rows;
+// self samples counted into *self_pairs. Returns count.
+uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
+                        uint64_t* self_pairs, uint64_t* sampled_pairs);
+
+// Dedupe (keys may repeat across shards), weight, CSR, degrees.
+void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
+                  const double* g_full, const uint64_t* keys, uint64_t nkeys,
+                  bool keys_sorted_unique, bool want_estimates,
+                  GraphResult& out);
+
+}  // namespace fsgg

@@ -1,0 +1,382 @@
+// Pair collapse, weighting and graph assembly: the device replacement of
+// proj/src/sparsifier.cpp:78-121 and the WeightedGraph constructor
+// (proj/src/graph.cpp:14-21).
+//
+//  * collapse_pairs: self samples dropped (:83-86), canonical (min, max)
+//    keys (:87-89), radix sort + unique (:91-92) — compact keys of 2*ceil
+//    (log2 n) bits so the sort touches only significant bits.
+//  * finish_graph: k_ij in fp64 from the fp32 coordinates, underflow drop
+//    (:105-109), p_i = min(L k / g_i, 1), p_hat = p_i + p_j - p_i p_j,
+//    w = k / p_hat (:110-113) with the reference's operation order and no
+//    FMA contraction; sparsity invariant (:120-121); degrees summed per
+//    vertex in exactly the reference's edge order via a transposed CSR.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "engine.cuh"
+
+namespace fsgg {
+
+namespace {
+
+struct EdgeEstimateDev {  // layout of fsgg_edge_estimate
+  uint32_t i, j;
+  double k_ij, g_i, g_j, p_i, p_j, p_hat;
+};
+
+uint32_t index_bits(uint32_t n) {
+  uint32_t b = 1;
+  while (b < 32 && (1ull << b) < n) ++b;
+  return b;
+}
+
+__global__ void rows_to_keys_kernel(uint32_t nq, const uint32_t* __restrict__ uq,
+                                    const uint64_t* __restrict__ row_off,
+                                    const uint32_t* __restrict__ row_cnt,
+                                    const uint32_t* __restrict__ leaf_src,
+                                    const uint32_t* __restrict__ leaf_cnt,
+                                    uint32_t bits, unsigned long long* __restrict__ keys,
+                                    unsigned long long* __restrict__ counters) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long self = 0, sampled = 0;
+  if (r < nq) {
+    const uint32_t q = uq[r], cnt = row_cnt[r];
+    const uint64_t a = row_off[r], b = row_off[r + 1];
+    sampled = cnt;
+    for (uint64_t k = a; k < b; ++k) {
+      unsigned long long key = ~0ull;
+      if (k - a < cnt) {
+        const uint32_t s = leaf_src[k];
+        if (s == q) {
+          self += leaf_cnt[k];
+        } else {
+          const uint32_t lo = min(q, s), hi = max(q, s);
+          key = (static_cast<unsigned long long>(lo) << bits) | hi;
+        }
+      }
+      keys[k] = key;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    self += __shfl_xor_sync(0xffffffffu, self, o);
+    sampled += __shfl_xor_sync(0xffffffffu, sampled, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (self) atomicAdd(counters + 0, self);
+    if (sampled) atomicAdd(counters + 1, sampled);
+  }
+}
+
+__global__ void compact_to_public_kernel(unsigned long long* keys, uint64_t m,
+                                         uint32_t bits) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  const unsigned long long k = keys[i];
+  const unsigned long long mask = (1ull << bits) - 1;
+  keys[i] = ((k >> bits) << 32) | (k & mask);
+}
+
+__global__ void public_to_compact_kernel(const unsigned long long* in,
+                                         unsigned long long* out, uint64_t m,
+                                         uint32_t bits) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  const unsigned long long k = in[i];
+  out[i] = ((k >> 32) << bits) | (k & 0xffffffffull);
+}
+
+// fp64 kernel value, same operation order as proj/include/fsg/kernel.hpp:28-53.
+__device__ __forceinline__ double kernel_f64(int family, double sigma,
+                                             const float* x, const float* y,
+                                             uint32_t d) {
+  double s = 0.0;
+  if (family == 2) {
+    for (uint32_t k = 0; k < d; ++k)
+      s = __dadd_rn(s, fabs(__dsub_rn(double(x[k]), double(y[k]))));
+    return exp(-s / sigma);
+  }
+  for (uint32_t k = 0; k < d; ++k) {
+    const double t = __dsub_rn(double(x[k]), double(y[k]));
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  if (family == 1) return exp(-sqrt(s) / sigma);
+  return exp(-s / __dmul_rn(sigma, sigma));
+}
+
+__global__ void underflow_flags_kernel(const unsigned long long* __restrict__ keys,
+                                       uint64_t m, const float* __restrict__ pts,
+                                       uint32_t d, int family, double sigma,
+                                       unsigned char* __restrict__ keep,
+                                       unsigned long long* __restrict__ dropped) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
+  const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
+  const bool ok = k >= 1e-300;
+  keep[e] = ok;
+  if (!ok) atomicAdd(dropped, 1ull);
+}
+
+__global__ void weights_kernel(const unsigned long long* __restrict__ keys,
+                               uint64_t m, const float* __restrict__ pts,
+                               uint32_t d, int family, double sigma, double L,
+                               const double* __restrict__ g_full,
+                               uint32_t* __restrict__ u, uint32_t* __restrict__ v,
+                               double* __restrict__ w, EdgeEstimateDev* est) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
+  const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
+  const double gi = g_full[i], gj = g_full[j];
+  const double pi = fmin(__ddiv_rn(__dmul_rn(L, k), gi), 1.0);
+  const double pj = fmin(__ddiv_rn(__dmul_rn(L, k), gj), 1.0);
+  const double ph = __dsub_rn(__dadd_rn(pi, pj), __dmul_rn(pi, pj));
+  u[e] = i;
+  v[e] = j;
+  w[e] = __ddiv_rn(k, ph);
+  if (est) est[e] = EdgeEstimateDev{i, j, k, gi, gj, pi, pj, ph};
+}
+
+// row_ptr[x] = first edge index with key-row >= x (keys sorted).
+__global__ void row_ptr_kernel(const uint32_t* __restrict__ rows, uint64_t m,
+                               uint32_t n, uint64_t* __restrict__ row_ptr) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x > n) return;
+  uint64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (rows[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  row_ptr[x] = lo;
+}
+
+__global__ void transpose_keys_kernel(const uint32_t* __restrict__ u,
+                                      const uint32_t* __restrict__ v, uint64_t m,
+                                      uint32_t bits,
+                                      unsigned long long* __restrict__ keys) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  keys[e] = (static_cast<unsigned long long>(v[e]) << bits) | u[e];
+}
+
+__global__ void key_rows_kernel(const unsigned long long* __restrict__ keys,
+                                uint64_t m, uint32_t bits, uint32_t* __restrict__ rows) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e >= m) return;
+  rows[e] = uint32_t(keys[e] >> bits);
+}
+
+// Degree of x in the reference's accumulation order (graph.cpp:14-21):
+// edges (u, x), u < x ascending, then edges (x, v), v ascending.
+__global__ void degrees_kernel(uint32_t n, const uint64_t* __restrict__ rpt,
+                               const double* __restrict__ wt,
+                               const uint64_t* __restrict__ rp,
+                               const double* __restrict__ w,
+                               double* __restrict__ deg) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  double s = 0.0;
+  for (uint64_t e = rpt[x]; e < rpt[x + 1]; ++e) s = __dadd_rn(s, wt[e]);
+  for (uint64_t e = rp[x]; e < rp[x + 1]; ++e) s = __dadd_rn(s, w[e]);
+  deg[x] = s;
+}
+
+template <class F>
+void cub_call(DevBuf& tmp, cudaStream_t s, F&& f) {
+  size_t bytes = 0;
+  FSGG_CUDA(f(static_cast<void*>(nullptr), bytes));
+  tmp.ensure(bytes + 16, s);
+  FSGG_CUDA(f(tmp.as<void>(), bytes));
+}
+
+// Sort + unique compact keys in place; returns unique count (sentinel
+// ~0 entries, if any, are dropped).
+uint64_t sort_unique_compact(Dataset& ds, DevBuf& keys, uint64_t m,
+                             uint32_t bits) {
+  cudaStream_t s = ds.stream;
+  if (m == 0) return 0;
+  DevBuf alt(m * 8, s), tmp, cnt(16, s);
+  cub::DoubleBuffer<unsigned long long> db(keys.as<unsigned long long>(),
+                                           alt.as<unsigned long long>());
+  cub_call(tmp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, m, 0, int(2 * bits), s);
+  });
+  unsigned long long* sorted = db.Current();
+  unsigned long long* other = db.Alternate();
+  cub_call(tmp, s, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, sorted, other, cnt.as<uint64_t>(), m, s);
+  });
+  ds.launches += 8;
+  uint64_t u = 0;
+  unsigned long long last = 0;
+  FSGG_CUDA(cudaMemcpyAsync(&u, cnt.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  if (u) {
+    FSGG_CUDA(cudaMemcpyAsync(&last, other + u - 1, 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    if (last == ~0ull) --u;
+  }
+  if (other != keys.as<unsigned long long>()) std::swap(keys, alt);
+  return u;
+}
+
+}  // namespace
+
+uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
+                        uint64_t* self_pairs, uint64_t* sampled_pairs) {
+  cudaStream_t s = ds.stream;
+  const uint64_t cap = res.total_tickets;
+  const uint32_t bits = index_bits(ds.n);
+  keys.alloc(std::max<uint64_t>(cap, 1) * 8, s);
+  DevBuf counters(16, s);
+  FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
+  rows_to_keys_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(
+      res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(),
+      res.row_cnt.as<uint32_t>(), res.leaf_src.as<uint32_t>(),
+      res.leaf_cnt.as<uint32_t>(), bits, keys.as<unsigned long long>(),
+      counters.as<unsigned long long>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+  unsigned long long c[2];
+  FSGG_CUDA(cudaMemcpyAsync(c, counters.as<void>(), 16, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  *self_pairs = c[0];
+  *sampled_pairs = c[1];
+  const uint64_t m = sort_unique_compact(ds, keys, cap, bits);
+  if (m) {
+    compact_to_public_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), m, bits);
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
+  return m;
+}
+
+void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
+                  const double* g_full, const uint64_t* keys_in, uint64_t nkeys,
+                  bool keys_sorted_unique, bool want_estimates,
+                  GraphResult& out) {
+  cudaStream_t s = ds.stream;
+  const uint32_t n = ds.n, d = ds.d;
+  const uint32_t bits = index_bits(n);
+  const float* pts = ds.pts.as<float>();
+  out.n = n;
+
+  // 1. canonical sorted unique public keys
+  DevBuf keys(std::max<uint64_t>(nkeys, 1) * 8, s);
+  uint64_t m = nkeys;
+  if (keys_sorted_unique) {
+    if (m)
+      FSGG_CUDA(cudaMemcpyAsync(keys.as<void>(), keys_in, m * 8,
+                                cudaMemcpyDeviceToDevice, s));
+  } else if (m) {
+    public_to_compact_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        reinterpret_cast<const unsigned long long*>(keys_in),
+        keys.as<unsigned long long>(), m, bits);
+    FSGG_LAUNCH_CHECK();
+    m = sort_unique_compact(ds, keys, m, bits);
+    if (m) {
+      compact_to_public_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+          keys.as<unsigned long long>(), m, bits);
+      FSGG_LAUNCH_CHECK();
+    }
+    ds.launches += 2;
+  }
+
+  // 2. drop underflowing pairs (k_ij < 1e-300)
+  DevBuf tmp, cnt(16, s);
+  out.underflow = 0;
+  if (m) {
+    DevBuf keep(m, s);
+    FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
+    underflow_flags_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
+        keep.as<unsigned char>(), cnt.as<unsigned long long>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+    unsigned long long dropped = 0;
+    FSGG_CUDA(cudaMemcpyAsync(&dropped, cnt.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    if (dropped) {
+      DevBuf kept(m * 8, s);
+      cub_call(tmp, s, [&](void* t, size_t& b) {
+        return cub::DeviceSelect::Flagged(t, b, keys.as<unsigned long long>(),
+                                          keep.as<unsigned char>(),
+                                          kept.as<unsigned long long>(),
+                                          cnt.as<uint64_t>() + 1, m, s);
+      });
+      ds.launches++;
+      std::swap(keys, kept);
+      m -= dropped;
+      out.underflow = dropped;
+    }
+  }
+  if (m > uint64_t(n) * rounds)
+    throw NumericError("sparsity invariant violated: more than n*L edges");
+
+  // 3. weights (+ estimates)
+  out.m = m;
+  const uint64_t mm = std::max<uint64_t>(m, 1);
+  out.u.alloc(mm * 4, s);
+  out.v.alloc(mm * 4, s);
+  out.w.alloc(mm * 8, s);
+  if (want_estimates) out.est.alloc(mm * sizeof(EdgeEstimateDev), s);
+  if (m) {
+    weights_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
+        double(rounds), g_full, out.u.as<uint32_t>(), out.v.as<uint32_t>(),
+        out.w.as<double>(), want_estimates ? out.est.as<EdgeEstimateDev>() : nullptr);
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
+
+  // 4. upper CSR, transposed CSR, degrees, total weight
+  out.row_ptr.alloc(size_t(n + 1) * 8, s);
+  out.degrees.alloc(size_t(n) * 8, s);
+  DevBuf rpt(size_t(n + 1) * 8, s), tkeys(mm * 8, s), tkeys2(mm * 8, s),
+      wt(mm * 8, s), wt2(mm * 8, s), trows(mm * 4, s);
+  row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
+      out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
+  FSGG_LAUNCH_CHECK();
+  if (m) {
+    transpose_keys_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        out.u.as<uint32_t>(), out.v.as<uint32_t>(), m, bits,
+        tkeys.as<unsigned long long>());
+    FSGG_LAUNCH_CHECK();
+    cub::DoubleBuffer<unsigned long long> dk(tkeys.as<unsigned long long>(),
+                                             tkeys2.as<unsigned long long>());
+    FSGG_CUDA(cudaMemcpyAsync(wt.as<void>(), out.w.as<void>(), m * 8,
+                              cudaMemcpyDeviceToDevice, s));
+    cub::DoubleBuffer<double> dv(wt.as<double>(), wt2.as<double>());
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(2 * bits), s);
+    });
+    key_rows_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(dk.Current(), m, bits,
+                                                         trows.as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
+        trows.as<uint32_t>(), m, n, rpt.as<uint64_t>());
+    FSGG_LAUNCH_CHECK();
+    degrees_kernel<<<ceil_div_u32(n, 256), 256, 0, s>>>(
+        n, rpt.as<uint64_t>(), dv.Current(), out.row_ptr.as<uint64_t>(),
+        out.w.as<double>(), out.degrees.as<double>());
+    FSGG_LAUNCH_CHECK();
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceReduce::Sum(t, b, out.w.as<double>(), wt.as<double>(), m, s);
+    });
+    FSGG_CUDA(cudaMemcpyAsync(&out.total_weight, wt.as<void>(), 8,
+                              cudaMemcpyDeviceToHost, s));
+    ds.launches += 12;
+  } else {
+    FSGG_CUDA(cudaMemsetAsync(out.degrees.as<void>(), 0, size_t(n) * 8, s));
+    out.total_weight = 0.0;
+  }
+  FSGG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace fsgg

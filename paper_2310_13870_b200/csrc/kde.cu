@@ -1,0 +1,838 @@
+// Fused kernel-sum ("KDE") kernels: the device replacement of the
+// reference's ExactKdeEstimator::eval / compensated_range_sum
+// (proj/src/kde.cpp:38-71) and of the sampler's inline sums
+// (proj/src/sampler.cpp:34-73), batched over a whole tree level.
+//
+// For every entry (node, query) of a level the sampler needs the two child
+// sums g1 = sum_{j in [first,mid)} k(x_q, x_j) and g2 over [mid, last)
+// (proj/src/sampler.cpp:141-149). The n x n kernel matrix is never
+// materialised: sources stream through shared memory, exponentials go
+// through MUFU.EX2 and each sum is reduced in registers.
+//
+// Numerics (SURVEY.md §8a'):
+//  * direct differences (q - x) in fp32 (the expanded ||q||^2+||x||^2-2q.x
+//    form loses 1e-4 by cancellation at n = 1M), exponent in base 2;
+//  * each (entry, source-chunk) pair carries an exponent offset
+//    off = scale * dist(q, bbox(chunk)) <= every term's exponent, so terms
+//    are evaluated as 2^(off - scale*dist) <= 1 and never flush to zero in
+//    fp32 while they are representable in fp64; the chunk sum is rescaled by
+//    2^-off in fp64. Algebraically exact, so the offset's own rounding does
+//    not matter;
+//  * fp32 accumulation within a shared-memory tile, fp64 across tiles and
+//    chunks, combined in a fixed order: results depend only on (node, query),
+//    never on how entries are batched or sharded across GPUs.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cfloat>
+
+#include "engine.cuh"
+
+namespace fsgg {
+
+KernelSpec make_kernel_spec(int family, double sigma) {
+  KernelSpec k;
+  k.family = family;
+  k.sigma = sigma;
+  const double log2e = 1.4426950408889634074;
+  k.scale = static_cast<float>(family == 0 ? log2e / (sigma * sigma)
+                                           : log2e / sigma);
+  return k;
+}
+
+KdeWorkspace::~KdeWorkspace() {
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+}
+
+namespace {
+
+constexpr int kThreads = 128;        // low-d tiled kernel CTA
+constexpr int kBE = 2 * kThreads;    // entries per low-d work item (2/thread)
+constexpr int kXThreads = 128;       // high-d tiled kernel CTA
+constexpr int kXBM = 64;             // entries per high-d work item
+constexpr int kXBN = 64;             // sources per high-d tile
+constexpr int kXBK = 16;             // dims per high-d k-step
+constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
+constexpr uint64_t kMaxPartials = 64ull << 20;  // doubles
+constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
+
+template <int D>
+struct LowDTile {
+  static constexpr int T = D <= 2 ? 2048 : (D <= 4 ? 1024 : 512);
+};
+
+// ---- kernel-family arithmetic (proj/include/fsg/kernel.hpp:28-53) ---------
+// FAM 0 gaussian: dist = sum dk^2; 1 exponential: sqrt(sum dk^2);
+// 2 laplacian: sum |dk|.
+template <int FAM>
+__device__ __forceinline__ float2 fam_first(float2 dk) {
+  if constexpr (FAM == 2) return make_float2(fabsf(dk.x), fabsf(dk.y));
+  return __fmul2_rn(dk, dk);
+}
+template <int FAM>
+__device__ __forceinline__ float2 fam_next(float2 dk, float2 t) {
+  if constexpr (FAM == 2)
+    return __fadd2_rn(t, make_float2(fabsf(dk.x), fabsf(dk.y)));
+  return __ffma2_rn(dk, dk, t);
+}
+template <int FAM>
+__device__ __forceinline__ float2 fam_finish(float2 t) {
+  if constexpr (FAM == 1) return make_float2(sqrtf(t.x), sqrtf(t.y));
+  return t;
+}
+template <int FAM>
+__device__ __forceinline__ float fam_acc1(float dk, float t) {
+  if constexpr (FAM == 2) return t + fabsf(dk);
+  return fmaf(dk, dk, t);
+}
+template <int FAM>
+__device__ __forceinline__ float fam_finish1(float t) {
+  if constexpr (FAM == 1) return sqrtf(t);
+  return t;
+}
+
+// Lower bound of dist(q, box) for the exponent offset.
+template <int FAM>
+__device__ __forceinline__ float box_dist(const float* q, const float* lo,
+                                          const float* hi, uint32_t d) {
+  float acc = 0.f;
+  for (uint32_t k = 0; k < d; ++k) {
+    float v = fmaxf(fmaxf(lo[k] - q[k], q[k] - hi[k]), 0.f);
+    acc = (FAM == 2) ? acc + v : fmaf(v, v, acc);
+  }
+  return fam_finish1<FAM>(acc);
+}
+
+__device__ __forceinline__ double rescale(double acc, float off) {
+  return off > 0.f ? acc * exp2(-static_cast<double>(off)) : acc;
+}
+
+// Work-item -> node slot lookup: largest g with blk_off[g] <= blk.
+__device__ __forceinline__ uint32_t find_slot(const uint32_t* blk_off,
+                                              uint32_t num_slots,
+                                              uint32_t blk) {
+  uint32_t lo = 0, hi = num_slots;  // blk_off[lo] <= blk < blk_off[hi]
+  while (hi - lo > 1) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (blk_off[mid] <= blk)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// Sum of 2^(off - scale*dist) over sources [cf, cl) for two packed entries;
+// sources staged negated and duplicated in shared memory.
+template <int D, int FAM>
+__device__ __forceinline__ void lowd_range_sum(
+    const float* __restrict__ pts, float2* sm, const float2 (&q2)[D],
+    float2 off2, float scale, uint32_t cf, uint32_t cl, double& accA,
+    double& accB) {
+  constexpr int T = LowDTile<D>::T;
+  const float2 ms = make_float2(-scale, -scale);
+  for (uint32_t t0 = cf; t0 < cl; t0 += T) {
+    const uint32_t len = min(uint32_t(T), cl - t0);
+    const uint32_t lenp = (len + 3u) & ~3u;
+    __syncthreads();
+    const float* src = pts + size_t(t0) * D;
+    for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
+      float v = idx < len * D ? -__ldg(src + idx) : -kPad;
+      sm[idx] = make_float2(v, v);
+    }
+    __syncthreads();
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (uint32_t j = 0; j < lenp; ++j) {
+      const float2* x = sm + j * D;
+      float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
+#pragma unroll
+      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
+      t = fam_finish<FAM>(t);
+      const float2 arg = __ffma2_rn(t, ms, off2);
+      acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+    }
+    accA += acc.x;
+    accB += acc.y;
+  }
+}
+
+// ---- low-d tiled kernel (node size > direct threshold) --------------------
+// One CTA = (node slot, block of <= 256 entries, child side, source chunk).
+// Chunks are the node's descendants `cdepth` levels below the child, so
+// their boundaries and bounding boxes come from the tree table and depend
+// only on the node. Writes one fp64 partial per (entry, side, chunk).
+template <int D, int FAM>
+__global__ void __launch_bounds__(kThreads)
+    kde_lowd_tiled_kernel(const float* __restrict__ pts,
+                          const uint32_t* __restrict__ eq,
+                          const uint32_t* __restrict__ goff,
+                          const uint32_t* __restrict__ blk_off,
+                          uint32_t num_slots, uint32_t level, uint32_t cdepth,
+                          const uint32_t* __restrict__ tfirst,
+                          const uint32_t* __restrict__ tlast,
+                          const float* __restrict__ tlo,
+                          const float* __restrict__ thi, int has_boxes,
+                          float scale, double* __restrict__ partials) {
+  constexpr int T = LowDTile<D>::T;
+  __shared__ __align__(16) float2 sm[T * D];
+  const uint32_t K = 1u << cdepth;
+  const uint32_t item = blockIdx.x;
+  const uint32_t blk = item >> (cdepth + 1);
+  const uint32_t side = (item >> cdepth) & 1u;
+  const uint32_t kk = item & (K - 1);
+  const uint32_t g = find_slot(blk_off, num_slots, blk);
+  const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kBE;
+  const uint32_t e1 = min(e0 + kBE, goff[g + 1]);
+
+  const uint32_t lc = level + 1 + cdepth;
+  const uint64_t h = ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
+  const uint32_t cf = tfirst[h], cl = tlast[h];
+
+  const uint32_t ia = e0 + threadIdx.x, ib = ia + kThreads;
+  const bool va = ia < e1, vb = ib < e1;
+  const uint32_t qa = eq[va ? ia : e0], qb = eq[vb ? ib : e0];
+  float qa_c[D], qb_c[D];
+  float2 q2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    qa_c[k] = __ldg(pts + size_t(qa) * D + k);
+    qb_c[k] = __ldg(pts + size_t(qb) * D + k);
+    q2[k] = make_float2(qa_c[k], qb_c[k]);
+  }
+  float offA = 0.f, offB = 0.f;
+  if (has_boxes) {
+    offA = scale * box_dist<FAM>(qa_c, tlo + h * D, thi + h * D, D);
+    offB = scale * box_dist<FAM>(qb_c, tlo + h * D, thi + h * D, D);
+  }
+  double accA = 0.0, accB = 0.0;
+  lowd_range_sum<D, FAM>(pts, sm, q2, make_float2(offA, offB), scale, cf, cl,
+                         accA, accB);
+  const uint32_t stride = 2u * K, col = side * K + kk;
+  if (va) partials[size_t(ia) * stride + col] = rescale(accA, offA);
+  if (vb) partials[size_t(ib) * stride + col] = rescale(accB, offB);
+}
+
+// ---- low-d direct kernel (small nodes: one thread per entry) --------------
+template <int D, int FAM>
+__global__ void __launch_bounds__(256)
+    kde_lowd_direct_kernel(const float* __restrict__ pts,
+                           const uint32_t* __restrict__ eq,
+                           const uint32_t* __restrict__ eg, uint32_t E,
+                           uint32_t level, const uint32_t* __restrict__ tfirst,
+                           const uint32_t* __restrict__ tlast,
+                           const float* __restrict__ tlo,
+                           const float* __restrict__ thi, int has_boxes,
+                           float scale, double* __restrict__ g1,
+                           double* __restrict__ g2, double* __restrict__ groot) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const uint64_t h = ((1ull << level) - 1) + eg[i];
+  const uint32_t f = tfirst[h], l = tlast[h];
+  if (l - f < 2) {
+    g1[i] = g2[i] = 0.0;
+    return;
+  }
+  const uint32_t mid = f + (l - f) / 2;
+  const uint32_t q = eq[i];
+  float qc[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
+  double s[2];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const uint64_t hc = 2 * h + 1 + side;
+    const uint32_t a = side ? mid : f, b = side ? l : mid;
+    const float off =
+        has_boxes ? scale * box_dist<FAM>(qc, tlo + hc * D, thi + hc * D, D) : 0.f;
+    float acc = 0.f;
+    for (uint32_t j = a; j < b; ++j) {
+      const float* x = pts + size_t(j) * D;
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) t = fam_acc1<FAM>(qc[k] - __ldg(x + k), t);
+      t = fam_finish1<FAM>(t);
+      acc += ex2_approx(fmaf(t, -scale, off));
+    }
+    s[side] = rescale(acc, off);
+  }
+  g1[i] = fmax(s[0], kSumFloor);
+  g2[i] = fmax(s[1], kSumFloor);
+  if (groot) groot[i] = fmax(s[0] + s[1], kSumFloor);
+}
+
+// ---- high-d tiled kernel (CUDA-core micro-tiles, direct differences) ------
+// 64 entries x 64 sources per tile, k-steps of 16 dims; each thread owns a
+// 4 x 8 block of (entry, source) squared distances.
+template <int FAM>
+__device__ __forceinline__ void xd_tile_sums(
+    const float* __restrict__ pts, uint32_t d, const uint32_t* qrow,  // smem
+    float (*sq)[kXBM], float (*sx)[kXBN], uint32_t cf, uint32_t cl,
+    const float* off /*4 rows*/, float scale, double* racc /*4 rows*/) {
+  const int tid = threadIdx.x;
+  const int tr = tid >> 3;  // row group: rows tr*4 .. tr*4+3
+  const int tc = tid & 7;   // cols tc*4..+3 and 32+tc*4..+3
+  for (uint32_t s0 = cf; s0 < cl; s0 += kXBN) {
+    const uint32_t len = min(uint32_t(kXBN), cl - s0);
+    float acc[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+    for (uint32_t k0 = 0; k0 < d; k0 += kXBK) {
+      __syncthreads();
+      for (int idx = tid; idx < kXBK * kXBM; idx += kXThreads) {
+        const int m = idx / kXBK, k = idx % kXBK;
+        const uint32_t kg = k0 + k;
+        sq[k][m] = kg < d ? __ldg(pts + size_t(qrow[m]) * d + kg) : 0.f;
+      }
+      for (int idx = tid; idx < kXBK * kXBN; idx += kXThreads) {
+        const int c = idx / kXBK, k = idx % kXBK;
+        const uint32_t kg = k0 + k;
+        float v = 0.f;
+        if (kg < d) v = c < int(len) ? -__ldg(pts + size_t(s0 + c) * d + kg) : -kPad;
+        sx[k][c] = v;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int k = 0; k < kXBK; ++k) {
+        const float4 qv = *reinterpret_cast<const float4*>(&sq[k][tr * 4]);
+        const float4 x0 = *reinterpret_cast<const float4*>(&sx[k][tc * 4]);
+        const float4 x1 = *reinterpret_cast<const float4*>(&sx[k][32 + tc * 4]);
+        const float qr[4] = {qv.x, qv.y, qv.z, qv.w};
+        const float xc[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float2 qq = make_float2(qr[r], qr[r]);
+#pragma unroll
+          for (int c = 0; c < 8; c += 2) {
+            const float2 dk = __fadd2_rn(qq, make_float2(xc[c], xc[c + 1]));
+            float2 t = make_float2(acc[r][c], acc[r][c + 1]);
+            t = fam_next<FAM>(dk, t);
+            acc[r][c] = t.x;
+            acc[r][c + 1] = t.y;
+          }
+        }
+      }
+    }
+    // epilogue: exponentials and per-row sums for this source tile
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int col = c < 4 ? tc * 4 + c : 32 + tc * 4 + (c - 4);
+        const float t = fam_finish1<FAM>(acc[r][c]);
+        const float e = ex2_approx(fmaf(t, -scale, off[r]));
+        rs += col < int(len) ? e : 0.f;
+      }
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 4);
+      racc[r] += rs;
+    }
+  }
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(kXThreads)
+    kde_xd_tiled_kernel(const float* __restrict__ pts, uint32_t d,
+                        const uint32_t* __restrict__ eq,
+                        const uint32_t* __restrict__ goff,
+                        const uint32_t* __restrict__ blk_off,
+                        uint32_t num_slots, uint32_t level, uint32_t cdepth,
+                        const uint32_t* __restrict__ tfirst,
+                        const uint32_t* __restrict__ tlast,
+                        const float* __restrict__ tlo,
+                        const float* __restrict__ thi, int has_boxes,
+                        float scale, double* __restrict__ partials) {
+  __shared__ __align__(16) float sq[kXBK][kXBM];
+  __shared__ __align__(16) float sx[kXBK][kXBN];
+  __shared__ uint32_t qrow[kXBM];
+  __shared__ float soff[kXBM];
+  const uint32_t K = 1u << cdepth;
+  const uint32_t item = blockIdx.x;
+  const uint32_t blk = item >> (cdepth + 1);
+  const uint32_t side = (item >> cdepth) & 1u;
+  const uint32_t kk = item & (K - 1);
+  const uint32_t g = find_slot(blk_off, num_slots, blk);
+  const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kXBM;
+  const uint32_t e1 = min(e0 + kXBM, goff[g + 1]);
+  const uint32_t lc = level + 1 + cdepth;
+  const uint64_t h = ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
+  const uint32_t cf = tfirst[h], cl = tlast[h];
+  if (threadIdx.x < kXBM) {
+    const uint32_t e = e0 + threadIdx.x;
+    const uint32_t q = eq[e < e1 ? e : e0];
+    qrow[threadIdx.x] = q;
+    float off = 0.f;
+    if (has_boxes) {
+      float qc[kBoxMaxDim];
+      for (uint32_t k = 0; k < d; ++k) qc[k] = __ldg(pts + size_t(q) * d + k);
+      off = scale * box_dist<FAM>(qc, tlo + h * d, thi + h * d, d);
+    }
+    soff[threadIdx.x] = off;
+  }
+  __syncthreads();
+  const int tr = threadIdx.x >> 3;
+  float off[4];
+  double racc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < 4; ++r) off[r] = soff[tr * 4 + r];
+  xd_tile_sums<FAM>(pts, d, qrow, sq, sx, cf, cl, off, scale, racc);
+  if ((threadIdx.x & 7) == 0) {
+    const uint32_t stride = 2u * K, col = side * K + kk;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t e = e0 + tr * 4 + r;
+      if (e < e1) partials[size_t(e) * stride + col] = rescale(racc[r], off[r]);
+    }
+  }
+}
+
+// ---- high-d direct kernel: one warp per entry ------------------------------
+template <int FAM>
+__global__ void __launch_bounds__(256)
+    kde_xd_direct_kernel(const float* __restrict__ pts, uint32_t d,
+                         const uint32_t* __restrict__ eq,
+                         const uint32_t* __restrict__ eg, uint32_t E,
+                         uint32_t level, const uint32_t* __restrict__ tfirst,
+                         const uint32_t* __restrict__ tlast,
+                         const float* __restrict__ tlo,
+                         const float* __restrict__ thi, int has_boxes,
+                         float scale, double* __restrict__ g1,
+                         double* __restrict__ g2, double* __restrict__ groot) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= E) return;
+  const uint64_t h = ((1ull << level) - 1) + eg[w];
+  const uint32_t f = tfirst[h], l = tlast[h];
+  if (l - f < 2) {
+    if (lane == 0) g1[w] = g2[w] = 0.0;
+    return;
+  }
+  const uint32_t mid = f + (l - f) / 2;
+  const float* q = pts + size_t(eq[w]) * d;
+  double s[2];
+  for (int side = 0; side < 2; ++side) {
+    const uint64_t hc = 2 * h + 1 + side;
+    const uint32_t a = side ? mid : f, b = side ? l : mid;
+    float off = 0.f;
+    if (has_boxes) {
+      float part = 0.f;
+      for (uint32_t k = lane; k < d; k += 32) {
+        float v = fmaxf(fmaxf(tlo[hc * d + k] - q[k], q[k] - thi[hc * d + k]), 0.f);
+        part = (FAM == 2) ? part + v : fmaf(v, v, part);
+      }
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      off = scale * fam_finish1<FAM>(part);
+    }
+    float acc = 0.f;
+    for (uint32_t j = a; j < b; ++j) {
+      const float* x = pts + size_t(j) * d;
+      float part = 0.f;
+      for (uint32_t k = lane; k < d; k += 32) part = fam_acc1<FAM>(__ldg(q + k) - __ldg(x + k), part);
+      for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      acc += ex2_approx(fmaf(fam_finish1<FAM>(part), -scale, off));
+    }
+    s[side] = rescale(acc, off);
+  }
+  if (lane == 0) {
+    g1[w] = fmax(s[0], kSumFloor);
+    g2[w] = fmax(s[1], kSumFloor);
+    if (groot) groot[w] = fmax(s[0] + s[1], kSumFloor);
+  }
+}
+
+// ---- level bookkeeping -----------------------------------------------------
+// Per slot: work blocks (size >= 2 nodes only) and evaluations
+// (entries x node size, the reference's "kernel evals").
+__global__ void slot_blocks_kernel(const uint32_t* __restrict__ goff,
+                                   uint32_t num_slots, uint32_t level,
+                                   const uint32_t* __restrict__ tfirst,
+                                   const uint32_t* __restrict__ tlast,
+                                   uint32_t be, uint32_t* __restrict__ nb,
+                                   unsigned long long* __restrict__ evals) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long ev = 0;
+  if (g < num_slots) {
+    const uint64_t h = ((1ull << level) - 1) + g;
+    const uint32_t size = tlast[h] - tfirst[h];
+    const uint32_t ne = goff[g + 1] - goff[g];
+    const bool work = size >= 2 && ne > 0;
+    if (nb) nb[g] = work ? (ne + be - 1) / be : 0;
+    ev = work ? (unsigned long long)ne * size : 0ull;
+  } else if (nb && g == num_slots) {
+    nb[g] = 0;
+  }
+  for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+}
+
+__global__ void finalize_kernel(const double* __restrict__ partials,
+                                uint32_t K, const uint32_t* __restrict__ eg,
+                                uint32_t E, uint32_t level,
+                                const uint32_t* __restrict__ tfirst,
+                                const uint32_t* __restrict__ tlast,
+                                double* __restrict__ g1,
+                                double* __restrict__ g2,
+                                double* __restrict__ groot) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const uint64_t h = ((1ull << level) - 1) + eg[i];
+  if (tlast[h] - tfirst[h] < 2) {
+    g1[i] = g2[i] = 0.0;
+    return;
+  }
+  const double* p = partials + size_t(i) * 2 * K;
+  double a = 0.0, b = 0.0;
+  for (uint32_t k = 0; k < K; ++k) a += p[k];
+  for (uint32_t k = 0; k < K; ++k) b += p[K + k];
+  g1[i] = fmax(a, kSumFloor);
+  g2[i] = fmax(b, kSumFloor);
+  if (groot) groot[i] = fmax(a + b, kSumFloor);
+}
+
+// ---- arbitrary-range evaluation (KdeEstimator::eval seam) -----------------
+__global__ void range_box_kernel(const float* __restrict__ pts, uint32_t d,
+                                 uint32_t first, uint32_t last, float* lo,
+                                 float* hi) {
+  // one CTA per dimension
+  const uint32_t k = blockIdx.x;
+  float mn = FLT_MAX, mx = -FLT_MAX;
+  for (uint32_t j = first + threadIdx.x; j < last; j += blockDim.x) {
+    const float v = pts[size_t(j) * d + k];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  __shared__ float smn[32], smx[32];
+  for (int o = 16; o; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smn[threadIdx.x >> 5] = mn;
+    smx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < blockDim.x / 32; ++w) {
+      mn = fminf(mn, smn[w]);
+      mx = fmaxf(mx, smx[w]);
+    }
+    lo[k] = mn;
+    hi[k] = mx;
+  }
+}
+
+template <int D, int FAM>
+__global__ void __launch_bounds__(kThreads)
+    kde_lowd_range_kernel(const float* __restrict__ pts,
+                          const uint32_t* __restrict__ targets, uint32_t m,
+                          uint32_t first, uint32_t last, uint32_t chunk,
+                          uint32_t nchunks, const float* __restrict__ lo,
+                          const float* __restrict__ hi, float scale,
+                          double* __restrict__ partials) {
+  constexpr int T = LowDTile<D>::T;
+  __shared__ __align__(16) float2 sm[T * D];
+  const uint32_t blk = blockIdx.x / nchunks, c = blockIdx.x % nchunks;
+  const uint32_t cf = first + c * chunk, cl = min(last, cf + chunk);
+  const uint32_t e0 = blk * kBE;
+  const uint32_t ia = e0 + threadIdx.x, ib = ia + kThreads;
+  const bool va = ia < m, vb = ib < m;
+  const uint32_t qa = targets[va ? ia : e0], qb = targets[vb ? ib : e0];
+  float qa_c[D], qb_c[D];
+  float2 q2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    qa_c[k] = pts[size_t(qa) * D + k];
+    qb_c[k] = pts[size_t(qb) * D + k];
+    q2[k] = make_float2(qa_c[k], qb_c[k]);
+  }
+  const float offA = scale * box_dist<FAM>(qa_c, lo, hi, D);
+  const float offB = scale * box_dist<FAM>(qb_c, lo, hi, D);
+  double accA = 0.0, accB = 0.0;
+  lowd_range_sum<D, FAM>(pts, sm, q2, make_float2(offA, offB), scale, cf, cl,
+                         accA, accB);
+  if (va) partials[size_t(ia) * nchunks + c] = rescale(accA, offA);
+  if (vb) partials[size_t(ib) * nchunks + c] = rescale(accB, offB);
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(256)
+    kde_xd_range_kernel(const float* __restrict__ pts, uint32_t d,
+                        const uint32_t* __restrict__ targets, uint32_t m,
+                        uint32_t first, uint32_t last, uint32_t chunk,
+                        uint32_t nchunks, const float* __restrict__ lo,
+                        const float* __restrict__ hi, int has_box, float scale,
+                        double* __restrict__ partials) {
+  const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= uint64_t(m) * nchunks) return;
+  const uint32_t t = w / nchunks, c = w % nchunks;
+  const uint32_t a = first + c * chunk, b = min(last, a + chunk);
+  const float* q = pts + size_t(targets[t]) * d;
+  float off = 0.f;
+  if (has_box) {
+    float part = 0.f;
+    for (uint32_t k = lane; k < d; k += 32) {
+      float v = fmaxf(fmaxf(lo[k] - q[k], q[k] - hi[k]), 0.f);
+      part = (FAM == 2) ? part + v : fmaf(v, v, part);
+    }
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    off = scale * fam_finish1<FAM>(part);
+  }
+  float acc = 0.f;
+  for (uint32_t j = a; j < b; ++j) {
+    const float* x = pts + size_t(j) * d;
+    float part = 0.f;
+    for (uint32_t k = lane; k < d; k += 32) part = fam_acc1<FAM>(q[k] - x[k], part);
+    for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    acc += ex2_approx(fmaf(fam_finish1<FAM>(part), -scale, off));
+  }
+  if (lane == 0) partials[size_t(t) * nchunks + c] = rescale(acc, off);
+}
+
+__global__ void range_finalize_kernel(const double* __restrict__ partials,
+                                      uint32_t nchunks, uint32_t m,
+                                      int empty, double* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (uint32_t c = 0; c < nchunks; ++c) s += partials[size_t(i) * nchunks + c];
+  out[i] = empty ? 0.0 : fmax(s, kSumFloor);
+}
+
+// ---- dispatch --------------------------------------------------------------
+template <int D, int FAM>
+struct LowD {
+  static void tiled(dim3 grid, cudaStream_t s, const float* pts,
+                    const LevelView& lv, const uint32_t* blk_off,
+                    uint32_t cdepth, const TreeTable& t, float scale,
+                    double* partials) {
+    kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
+        pts, lv.eq, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
+        t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
+        t.hi.as<float>(), t.has_boxes, scale, partials);
+  }
+  static void direct(cudaStream_t s, const float* pts, const LevelView& lv,
+                     const TreeTable& t, float scale, double* g1, double* g2,
+                     double* groot) {
+    kde_lowd_direct_kernel<D, FAM><<<ceil_div_u32(lv.num_entries, 256), 256, 0, s>>>(
+        pts, lv.eq, lv.eg, lv.num_entries, lv.level, t.first.as<uint32_t>(),
+        t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+        t.has_boxes, scale, g1, g2, groot);
+  }
+  static void range(dim3 grid, cudaStream_t s, const float* pts,
+                    const uint32_t* targets, uint32_t m, uint32_t first,
+                    uint32_t last, uint32_t chunk, uint32_t nchunks,
+                    const float* lo, const float* hi, float scale,
+                    double* partials) {
+    kde_lowd_range_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
+        pts, targets, m, first, last, chunk, nchunks, lo, hi, scale, partials);
+  }
+};
+
+template <template <int, int> class Op, int FAM>
+struct ByDim {
+  template <class F>
+  static void run(uint32_t d, F&& f) {
+    switch (d) {
+      case 1: f(Op<1, FAM>{}); break;
+      case 2: f(Op<2, FAM>{}); break;
+      case 3: f(Op<3, FAM>{}); break;
+      case 4: f(Op<4, FAM>{}); break;
+      case 5: f(Op<5, FAM>{}); break;
+      case 6: f(Op<6, FAM>{}); break;
+      case 7: f(Op<7, FAM>{}); break;
+      case 8: f(Op<8, FAM>{}); break;
+      default: throw ConfigError("low-d path supports d <= 8");
+    }
+  }
+};
+
+template <class F>
+void with_lowd(int family, uint32_t d, F&& f) {
+  switch (family) {
+    case 0: ByDim<LowD, 0>::run(d, f); break;
+    case 1: ByDim<LowD, 1>::run(d, f); break;
+    case 2: ByDim<LowD, 2>::run(d, f); break;
+    default: throw ConfigError("unknown kernel family");
+  }
+}
+
+template <class F>
+void with_family(int family, F&& f) {
+  switch (family) {
+    case 0: f(std::integral_constant<int, 0>{}); break;
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    default: throw ConfigError("unknown kernel family");
+  }
+}
+
+constexpr uint32_t kLowDMax = 8;
+uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
+
+}  // namespace
+
+void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
+               double* g1, double* g2, double* groot, KdeWorkspace& ws,
+               KdeStats& stats) {
+  const uint32_t E = lv.num_entries;
+  if (E == 0) return;
+  const uint32_t n = ds.n, d = ds.d;
+  const uint32_t s_max = uint32_t((uint64_t(n) + (1ull << lv.level) - 1) >> lv.level);
+  if (s_max < 2) return;  // every node is a leaf: routing emits, no sums
+  cudaStream_t s = ds.stream;
+  const TreeTable& t = ds.tree;
+  const float* pts = ds.pts.as<float>();
+  const bool lowd = d <= kLowDMax;
+  const bool direct = s_max <= direct_threshold(d);
+  const uint32_t be = lowd ? kBE : kXBM;
+
+  // blocks per slot + exact evaluation count of the level
+  const uint32_t G = lv.num_slots;
+  ws.blk_off.ensure(size_t(G + 2) * 4 + 64, s);
+  uint32_t* nb = ws.blk_off.as<uint32_t>();
+  unsigned long long* d_evals =
+      reinterpret_cast<unsigned long long*>(nb + G + 2 + (G & 1));
+  FSGG_CUDA(cudaMemsetAsync(d_evals, 0, 8, s));
+  slot_blocks_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
+      lv.goff, G, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(), be,
+      direct ? nullptr : nb, d_evals);
+  FSGG_LAUNCH_CHECK();
+  ds.launches += 1;
+
+  if (direct) {
+    if (lowd) {
+      with_lowd(ks.family, d, [&](auto op) {
+        op.direct(s, pts, lv, t, ks.scale, g1, g2, groot);
+      });
+    } else {
+      with_family(ks.family, [&](auto fam) {
+        constexpr int FAM = decltype(fam)::value;
+        kde_xd_direct_kernel<FAM><<<ceil_div_u32(uint64_t(E) * 32, 256), 256, 0, s>>>(
+            pts, d, lv.eq, lv.eg, E, lv.level, t.first.as<uint32_t>(),
+            t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+            t.has_boxes, ks.scale, g1, g2, groot);
+      });
+    }
+    FSGG_LAUNCH_CHECK();
+    ds.launches += 1;
+    unsigned long long ev = 0;
+    FSGG_CUDA(cudaMemcpyAsync(&ev, d_evals, 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    stats.evals += ev;
+    return;
+  }
+
+  // exclusive scan of blocks per slot -> blk_off (in place, G + 1 entries)
+  size_t tmp_bytes = 0;
+  FSGG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, nb, nb, G + 1, s));
+  ws.cub_tmp.ensure(tmp_bytes, s);
+  FSGG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.as<void>(), tmp_bytes, nb,
+                                          nb, G + 1, s));
+  uint32_t total_blocks = 0;
+  unsigned long long ev = 0;
+  FSGG_CUDA(cudaMemcpyAsync(&total_blocks, nb + G, 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(&ev, d_evals, 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  ds.launches += 1;
+  stats.evals += ev;
+  if (total_blocks == 0) return;
+
+  // chunk depth: enough independent items to fill the GPU many times over,
+  // chunks no smaller than kChunkMin, partials bounded.
+  const uint32_t node_min = uint32_t(uint64_t(n) >> lv.level);
+  const uint32_t child_min = node_min / 2;
+  const uint64_t target_items = uint64_t(ds.num_sms) * 8 * 40;
+  uint32_t c = 0;
+  while ((child_min >> (c + 1)) >= kChunkMin &&
+         (uint64_t(total_blocks) << (c + 1)) < target_items &&
+         (uint64_t(E) << (c + 2)) <= kMaxPartials &&
+         lv.level + 2 + c <= t.depth)
+    ++c;
+  const uint32_t K = 1u << c;
+  ws.partials.ensure(size_t(E) * 2 * K * sizeof(double), s);
+  double* partials = ws.partials.as<double>();
+  const uint64_t items = uint64_t(total_blocks) * 2 * K;
+  if (items > 0x7fffffffull) throw ConfigError("level too large for one launch");
+  const dim3 grid(static_cast<uint32_t>(items));
+
+  if (!ws.ev0) {
+    FSGG_CUDA(cudaEventCreate(&ws.ev0));
+    FSGG_CUDA(cudaEventCreate(&ws.ev1));
+  }
+  FSGG_CUDA(cudaEventRecord(ws.ev0, s));
+  if (lowd) {
+    with_lowd(ks.family, d, [&](auto op) {
+      op.tiled(grid, s, pts, lv, nb, c, t, ks.scale, partials);
+    });
+  } else {
+    with_family(ks.family, [&](auto fam) {
+      constexpr int FAM = decltype(fam)::value;
+      kde_xd_tiled_kernel<FAM><<<grid, kXThreads, 0, s>>>(
+          pts, d, lv.eq, lv.goff, nb, G, lv.level, c, t.first.as<uint32_t>(),
+          t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+          t.has_boxes, ks.scale, partials);
+    });
+  }
+  FSGG_LAUNCH_CHECK();
+  FSGG_CUDA(cudaEventRecord(ws.ev1, s));
+  finalize_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+      partials, K, lv.eg, E, lv.level, t.first.as<uint32_t>(),
+      t.last.as<uint32_t>(), g1, g2, groot);
+  FSGG_LAUNCH_CHECK();
+  ds.launches += 2;
+  FSGG_CUDA(cudaEventSynchronize(ws.ev1));
+  float ms = 0.f;
+  FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
+  stats.tiled_seconds += ms * 1e-3;
+  stats.tiled_evals += ev;
+  stats.tiled_launches += 1;
+}
+
+void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,
+               uint32_t last, const uint32_t* targets, uint32_t m,
+               double* out) {
+  if (m == 0) return;
+  cudaStream_t s = ds.stream;
+  const uint32_t d = ds.d;
+  const float* pts = ds.pts.as<float>();
+  const uint32_t len = last - first;
+  const uint32_t chunk = 8192;
+  const uint32_t nchunks = len == 0 ? 1 : (len + chunk - 1) / chunk;
+  DevBuf box(size_t(2) * d * 4, s), partials(size_t(m) * nchunks * 8, s);
+  float* lo = box.as<float>();
+  float* hi = lo + d;
+  const bool lowd = d <= kLowDMax;
+  if (len > 0) {
+    range_box_kernel<<<d, 256, 0, s>>>(pts, d, first, last, lo, hi);
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+    if (lowd) {
+      const dim3 grid(ceil_div_u32(m, kBE) * nchunks);
+      with_lowd(ks.family, d, [&](auto op) {
+        op.range(grid, s, pts, targets, m, first, last, chunk, nchunks, lo, hi,
+                 ks.scale, partials.as<double>());
+      });
+    } else {
+      with_family(ks.family, [&](auto fam) {
+        constexpr int FAM = decltype(fam)::value;
+        kde_xd_range_kernel<FAM><<<ceil_div_u32(uint64_t(m) * nchunks * 32, 256), 256, 0, s>>>(
+            pts, d, targets, m, first, last, chunk, nchunks, lo, hi,
+            d <= kBoxMaxDim, ks.scale, partials.as<double>());
+      });
+    }
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
+  range_finalize_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+      partials.as<double>(), len == 0 ? 0 : nchunks, m, len == 0, out);
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+}
+
+}  // namespace fsgg

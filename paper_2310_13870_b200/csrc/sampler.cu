@@ -1,0 +1,378 @@
+// Level-synchronous tree descent: the device replacement of
+// fsg::sample_neighbors_counted (proj/src/sampler.cpp:77-247).
+//
+// State per level is an entry list grouped by node slot (SoA: query,
+// tickets, slot) with a CSR-style offset array goff over the level's 2^l
+// slots, so entries of one node stay contiguous exactly like the reference's
+// node groups (:131-137). One level is:
+//   1. kde_level (kde.cu)      child sums g1, g2 for every entry;
+//   2. route_kernel            p = g1/(g1+g2) in fp64, Binomial(t, p) as t
+//                              Bernoulli trials on the reference's keyed
+//                              splitmix64 stream (bit-exact) or Philox;
+//                              size-1 nodes emit (query, source, count) into
+//                              a per-query leaf row with an atomic slot;
+//   3. one 64-bit exclusive scan of packed (has_left, has_right) flags;
+//   4. scatter_kernel / goff_kernel: deterministic stable placement, left
+//      children of a node before its right children (:217-222), no atomics.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <algorithm>
+
+#include "engine.cuh"
+
+namespace fsgg {
+
+namespace {
+
+__global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
+                                 uint32_t nq, uint32_t* __restrict__ qrow,
+                                 uint32_t* __restrict__ eq,
+                                 uint32_t* __restrict__ et,
+                                 uint32_t* __restrict__ eg,
+                                 const uint32_t* __restrict__ tickets) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  qrow[uq[i]] = i;
+  eq[i] = uq[i];
+  et[i] = tickets[i];
+  eg[i] = 0;
+}
+
+// Philox4x32-10 (Salmon et al. 2011), for rng_mode = PHILOX.
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// proj/src/sampler.cpp:186-225 per entry.
+__global__ void route_kernel(uint32_t E, uint32_t level,
+                             const uint32_t* __restrict__ eq,
+                             const uint32_t* __restrict__ et,
+                             const uint32_t* __restrict__ eg,
+                             const double* __restrict__ g1,
+                             const double* __restrict__ g2,
+                             const uint32_t* __restrict__ tfirst,
+                             const uint32_t* __restrict__ tlast,
+                             uint64_t key_prefix, int rng_mode, uint64_t seed,
+                             const uint32_t* __restrict__ qrow,
+                             const uint64_t* __restrict__ row_off,
+                             uint32_t* __restrict__ row_cnt,
+                             uint32_t* __restrict__ leaf_src,
+                             uint32_t* __restrict__ leaf_cnt,
+                             uint32_t* __restrict__ tl,
+                             unsigned long long* __restrict__ flags,
+                             unsigned long long* __restrict__ counters) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long tsum = 0, degen = 0;
+  if (i < E) {
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h];
+    const uint32_t q = eq[i], t = et[i];
+    tsum = t;
+    unsigned long long fl = 0;
+    if (l - f == 1) {
+      // :196-198 leaf: (query, source = first, count = tickets)
+      const uint32_t row = qrow[q];
+      const uint32_t slot = atomicAdd(row_cnt + row, 1u);
+      const uint64_t at = row_off[row] + slot;
+      leaf_src[at] = f;
+      leaf_cnt[at] = t;
+      tl[i] = 0;
+    } else {
+      const double a = g1[i], b = g2[i];
+      double p;
+      if (a <= kSumFloor && b <= kSumFloor) {  // :207-209
+        p = 0.5;
+        degen = t;
+      } else {
+        p = a / (a + b);  // :211
+      }
+      uint32_t left;
+      if (p <= 0.0) {  // rng.hpp:66-67
+        left = 0;
+      } else if (p >= 1.0) {
+        left = t;
+      } else {
+        // u_c = (x_c >> 11) * 2^-53 < p  <=>  (x_c >> 11) < ceil(p * 2^53)
+        const uint64_t thr = static_cast<uint64_t>(ceil(p * 9007199254740992.0));
+        left = 0;
+        if (rng_mode == 0) {
+          // RngStream::keyed(seed, kRouteTag, (first<<32)|last, query)
+          const uint64_t key =
+              route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
+          for (uint32_t c = 0; c < t; ++c)
+            left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+        } else {
+          const uint2 k = make_uint2(uint32_t(seed), uint32_t(seed >> 32));
+          for (uint32_t c = 0; c < t; c += 2) {
+            const uint4 r = philox4x32(make_uint4(c >> 1, q, f, l), k);
+            const uint64_t x0 = (uint64_t(r.x) << 32) | r.y;
+            const uint64_t x1 = (uint64_t(r.z) << 32) | r.w;
+            left += (x0 >> 11) < thr ? 1u : 0u;
+            if (c + 1 < t) left += (x1 >> 11) < thr ? 1u : 0u;
+          }
+        }
+      }
+      tl[i] = left;
+      fl = (static_cast<unsigned long long>(left > 0) << 32) |
+           static_cast<unsigned long long>(left < t);
+    }
+    flags[i] = fl;
+  } else if (i == E) {
+    flags[i] = 0;
+  }
+  for (int o = 16; o; o >>= 1) {
+    tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+    degen += __shfl_xor_sync(0xffffffffu, degen, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (tsum) atomicAdd(counters + 0, tsum);
+    if (degen) atomicAdd(counters + 1, degen);
+  }
+}
+
+__device__ __forceinline__ uint32_t hiw(unsigned long long x) {
+  return uint32_t(x >> 32);
+}
+__device__ __forceinline__ uint32_t low(unsigned long long x) {
+  return uint32_t(x);
+}
+
+// Stable placement: slot g's left children occupy [A[s]+B[s], A[e]+B[s]),
+// its right children [A[e]+B[s], A[e]+B[e]), where A/B are the exclusive
+// prefix counts of left/right children and [s, e) = goff[g], goff[g+1].
+__global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
+                               const uint32_t* __restrict__ et,
+                               const uint32_t* __restrict__ eg,
+                               const uint32_t* __restrict__ tl,
+                               const unsigned long long* __restrict__ flags,
+                               const uint32_t* __restrict__ goff,
+                               const unsigned long long* __restrict__ P,
+                               uint32_t* __restrict__ neq,
+                               uint32_t* __restrict__ net,
+                               uint32_t* __restrict__ neg) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const unsigned long long fl = flags[i];
+  if (!fl) return;
+  const uint32_t g = eg[i], q = eq[i], t = et[i], l = tl[i];
+  const unsigned long long Pi = P[i];
+  if (hiw(fl)) {
+    const uint32_t pos = hiw(Pi) + low(P[goff[g]]);
+    neq[pos] = q;
+    net[pos] = l;
+    neg[pos] = 2 * g;
+  }
+  if (low(fl)) {
+    const uint32_t pos = hiw(P[goff[g + 1]]) + low(Pi);
+    neq[pos] = q;
+    net[pos] = t - l;
+    neg[pos] = 2 * g + 1;
+  }
+}
+
+__global__ void goff_kernel(uint32_t G, const uint32_t* __restrict__ goff,
+                            const unsigned long long* __restrict__ P,
+                            uint32_t* __restrict__ ngoff) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G) {
+    const unsigned long long Ps = P[goff[g]], Pe = P[goff[g + 1]];
+    ngoff[2 * g] = hiw(Ps) + low(Ps);
+    ngoff[2 * g + 1] = hiw(Pe) + low(Ps);
+  } else if (g == G) {
+    const unsigned long long Pe = P[goff[G]];
+    ngoff[2 * G] = hiw(Pe) + low(Pe);
+  }
+}
+
+__global__ void row_ends_kernel(const uint64_t* __restrict__ row_off,
+                                const uint32_t* __restrict__ row_cnt,
+                                uint32_t nq, uint64_t* __restrict__ ends) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) ends[i] = row_off[i] + row_cnt[i];
+}
+
+}  // namespace
+
+void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
+                    SampleResult& out) {
+  cudaStream_t s = ds.stream;
+  if (!ds.tree_valid) build_tree(ds);
+  const TreeTable& t = ds.tree;
+  const uint32_t nq = static_cast<uint32_t>(req.queries.size());
+  out.nq = nq;
+  uint64_t total = 0;
+  for (uint32_t x : req.tickets) total += x;
+  out.total_tickets = total;
+  if (total > 0xffffffffull)
+    throw ConfigError("total tickets exceed 2^32 - 1 (entries are 32-bit)");
+
+  // host -> device: queries, tickets, leaf row offsets
+  std::vector<uint64_t> row_off(nq + 1, 0);
+  for (uint32_t i = 0; i < nq; ++i) row_off[i + 1] = row_off[i] + req.tickets[i];
+  out.uq.alloc(size_t(nq) * 4 + 4, s);
+  out.row_off.alloc(size_t(nq + 1) * 8, s);
+  out.row_cnt.alloc(size_t(nq) * 4 + 4, s);
+  out.leaf_src.alloc(total * 4 + 4, s);
+  out.leaf_cnt.alloc(total * 4 + 4, s);
+  DevBuf dtk(size_t(nq) * 4 + 4, s), qrow(size_t(ds.n) * 4, s);
+  FSGG_CUDA(cudaMemcpyAsync(out.uq.as<void>(), req.queries.data(), size_t(nq) * 4,
+                            cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemcpyAsync(dtk.as<void>(), req.tickets.data(), size_t(nq) * 4,
+                            cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemcpyAsync(out.row_off.as<void>(), row_off.data(),
+                            size_t(nq + 1) * 8, cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemsetAsync(out.row_cnt.as<void>(), 0, size_t(nq) * 4 + 4, s));
+  if (req.want_root_sums) out.groot.alloc(size_t(nq) * 8 + 8, s);
+
+  // double-buffered entry lists, capacity = total tickets (>= entries)
+  const uint64_t cap = std::max<uint64_t>(total, 1);
+  DevBuf eq[2], et[2], eg[2];
+  for (int b = 0; b < 2; ++b) {
+    eq[b].alloc(cap * 4, s);
+    et[b].alloc(cap * 4, s);
+    eg[b].alloc(cap * 4, s);
+  }
+  DevBuf g1(cap * 8, s), g2(cap * 8, s), tl(cap * 4, s), flags((cap + 1) * 8, s),
+      P((cap + 1) * 8, s);
+  const uint64_t max_slots = 1ull << t.depth;
+  DevBuf goff[2];
+  goff[0].alloc((max_slots + 1) * 4, s);
+  goff[1].alloc((max_slots + 1) * 4, s);
+  DevBuf counters(64, s), cub_tmp;
+  KdeWorkspace ws;
+
+  init_rows_kernel<<<ceil_div_u32(std::max<uint32_t>(nq, 1), 256), 256, 0, s>>>(
+      out.uq.as<uint32_t>(), nq, qrow.as<uint32_t>(), eq[0].as<uint32_t>(),
+      et[0].as<uint32_t>(), eg[0].as<uint32_t>(), dtk.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+  const uint32_t goff0[2] = {0, nq};
+  FSGG_CUDA(cudaMemcpyAsync(goff[0].as<void>(), goff0, 8, cudaMemcpyHostToDevice, s));
+
+  const uint64_t prefix = route_key_prefix(req.seed);
+  uint32_t E = nq;
+  int cur = 0;
+  out.entries_per_level.clear();
+  out.tickets_per_level.clear();
+  out.degenerate_draws = 0;
+  out.peak_entries = 0;
+  for (uint32_t level = 0; E > 0; ++level) {
+    if (level > t.depth) throw NumericError("descent exceeded tree depth");
+    const uint32_t G = 1u << level;
+    out.entries_per_level.push_back(E);
+    out.peak_entries = std::max<uint64_t>(out.peak_entries, E);
+    LevelView lv;
+    lv.level = level;
+    lv.num_slots = G;
+    lv.num_entries = E;
+    lv.eq = eq[cur].as<uint32_t>();
+    lv.eg = eg[cur].as<uint32_t>();
+    lv.goff = goff[cur].as<uint32_t>();
+    kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
+              level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr,
+              ws, out.kde);
+
+    FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
+    route_kernel<<<ceil_div_u32(uint64_t(E) + 1, 256), 256, 0, s>>>(
+        E, level, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(),
+        eg[cur].as<uint32_t>(), g1.as<double>(), g2.as<double>(),
+        t.first.as<uint32_t>(), t.last.as<uint32_t>(), prefix, req.rng_mode,
+        req.seed, qrow.as<uint32_t>(), out.row_off.as<uint64_t>(),
+        out.row_cnt.as<uint32_t>(), out.leaf_src.as<uint32_t>(),
+        out.leaf_cnt.as<uint32_t>(), tl.as<uint32_t>(),
+        flags.as<unsigned long long>(), counters.as<unsigned long long>());
+    FSGG_LAUNCH_CHECK();
+
+    size_t tmp_bytes = 0;
+    FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
+        nullptr, tmp_bytes, flags.as<unsigned long long>(),
+        P.as<unsigned long long>(), uint64_t(E) + 1, s));
+    cub_tmp.ensure(tmp_bytes, s);
+    FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
+        cub_tmp.as<void>(), tmp_bytes, flags.as<unsigned long long>(),
+        P.as<unsigned long long>(), uint64_t(E) + 1, s));
+    const int nxt = cur ^ 1;
+    scatter_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+        E, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(), eg[cur].as<uint32_t>(),
+        tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur].as<uint32_t>(),
+        P.as<unsigned long long>(), eq[nxt].as<uint32_t>(), et[nxt].as<uint32_t>(),
+        eg[nxt].as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    if (level < t.depth) {
+      goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
+          G, goff[cur].as<uint32_t>(), P.as<unsigned long long>(),
+          goff[nxt].as<uint32_t>());
+      FSGG_LAUNCH_CHECK();
+      ds.launches++;
+    }
+    ds.launches += 3;
+
+    unsigned long long host[3];
+    FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 16, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaMemcpyAsync(host + 2, P.as<unsigned long long>() + E, 8,
+                              cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    out.tickets_per_level.push_back(host[0]);
+    out.degenerate_draws += host[1];
+    const uint64_t next = uint64_t(host[2] >> 32) + uint64_t(host[2] & 0xffffffffull);
+    if (next > cap) throw NumericError("entry list overflow");
+    if (next > 0 && level >= t.depth)
+      throw NumericError("tickets remain below the deepest level");
+    E = static_cast<uint32_t>(next);
+    cur = nxt;
+  }
+}
+
+void sampled_triples_to_host(Dataset& ds, SampleResult& res,
+                             std::vector<uint32_t>& triples) {
+  cudaStream_t s = ds.stream;
+  const uint32_t nq = res.nq;
+  const uint64_t total = res.total_tickets;
+  triples.clear();
+  if (nq == 0 || total == 0) return;
+  if (total > 0x7fffffffull) throw ConfigError("too many tickets for host output");
+  DevBuf ends(size_t(nq) * 8, s), src_out(total * 4, s), cnt_out(total * 4, s), tmp;
+  row_ends_kernel<<<ceil_div_u32(nq, 256), 256, 0, s>>>(
+      res.row_off.as<uint64_t>(), res.row_cnt.as<uint32_t>(), nq, ends.as<uint64_t>());
+  FSGG_LAUNCH_CHECK();
+  size_t tmp_bytes = 0;
+  FSGG_CUDA(cub::DeviceSegmentedSort::SortPairs(
+      nullptr, tmp_bytes, res.leaf_src.as<uint32_t>(), src_out.as<uint32_t>(),
+      res.leaf_cnt.as<uint32_t>(), cnt_out.as<uint32_t>(), int(total), int(nq),
+      res.row_off.as<uint64_t>(), ends.as<uint64_t>(), s));
+  tmp.alloc(tmp_bytes, s);
+  FSGG_CUDA(cub::DeviceSegmentedSort::SortPairs(
+      tmp.as<void>(), tmp_bytes, res.leaf_src.as<uint32_t>(), src_out.as<uint32_t>(),
+      res.leaf_cnt.as<uint32_t>(), cnt_out.as<uint32_t>(), int(total), int(nq),
+      res.row_off.as<uint64_t>(), ends.as<uint64_t>(), s));
+  ds.launches += 2;
+  std::vector<uint32_t> uq(nq), cnt(nq), src(total), c(total);
+  std::vector<uint64_t> off(nq + 1);
+  FSGG_CUDA(cudaMemcpyAsync(uq.data(), res.uq.as<void>(), size_t(nq) * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(cnt.data(), res.row_cnt.as<void>(), size_t(nq) * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(off.data(), res.row_off.as<void>(), size_t(nq + 1) * 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(src.data(), src_out.as<void>(), total * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(c.data(), cnt_out.as<void>(), total * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  uint64_t m = 0;
+  for (uint32_t i = 0; i < nq; ++i) m += cnt[i];
+  triples.resize(m * 3);
+  uint64_t at = 0;
+  for (uint32_t i = 0; i < nq; ++i)
+    for (uint32_t k = 0; k < cnt[i]; ++k, ++at) {
+      triples[3 * at] = uq[i];
+      triples[3 * at + 1] = src[off[i] + k];
+      triples[3 * at + 2] = c[off[i] + k];
+    }
+}
+
+}  // namespace fsgg
