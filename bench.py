@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the KDE-driven similarity-graph sampler (arXiv 2310.13870).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3]
+    python bench.py --impl reference ...       # the reference's CPU path
+
+One step = one full ``build_similarity_graph`` (tree, level-synchronous
+descent with the fused KDE, pair collapse, weights, CSR, degrees) over the
+workload, here BASELINE.json configs[2]: two-moons, n = 1,000,000 fp32,
+sigma = 0.05, 64 samples/point (it fits one GPU). Prints ONE JSON line.
+
+* value      sampled edges/s (n * L tickets per step / step time), whole job;
+             inputs resident in HBM; every step timed with CUDA events on the
+             library's launch stream, barrier + synchronize on both sides, L2
+             flushed (512 MiB write) between steps outside the timed events;
+             max over ranks.
+* e2e        same metric through the public API with HOST buffers: each step
+             uploads the points from pinned memory and copies the whole graph
+             (u, v, w, row_ptr, degrees) back to host.
+* roofline   the tiled low-d KDE kernel (MUFU-bound): algorithmic Gaussian
+             evaluations (one ex2 each) per launch / its mean launch time
+             (CUDA events around each launch on its stream), against the
+             MUFU.EX2 throughput measured on this GPU in this run.
+* cpu_baseline  the reference's own code (oracle/_ref, compiled in place from
+             /root/reference) on the host cores, default (auto = FGT for this
+             config) backend, bounded sample: a contiguous block of queries.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIG_DOC = {
+    "C1": "two 2-D blobs n=2000 sigma=0.5 L=32",
+    "C2": "two-moons n=100k sigma=0.1 L=64",
+    "C3": "two-moons n=1M sigma=0.05 L=64",
+    "C4": "synthetic image pixels n=154401 d=5 sigma=0.2 L=32",
+    "C5": "GMM n=70000 d=784 sigma=median dist L=32",
+}
+NOMINAL_EX2_PER_CLK_PER_SM = 16
+SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def metric_name(cfg: str) -> str:
+    return f"sampled edges/sec ({cfg}: {CONFIG_DOC[cfg]})"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C3", choices=sorted(CONFIG_DOC))
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target seconds of CPU work for the cpu_baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- clocks ----
+class ClockSampler:
+    """nvidia-smi -lms 200 during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={SMI_FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax),
+                "power_w_max": max(power), "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- reference ----
+def reference_sample(points64, sigma, rounds, seed, target_s, threads):
+    """The reference's own CPU path on a bounded sample of the workload.
+
+    Builds the reference's default estimator (make_estimator, auto backend:
+    FGT for d<=3, n>=4096, else exact; proj/src/kde.cpp:104-129) once, then
+    times sample_neighbors_counted (proj/src/sampler.cpp:77) plus the degree
+    KDE for a contiguous block of queries (their descent is exactly the one
+    the full job performs for them). The block size is calibrated to
+    ~target_s of CPU time."""
+    from oracle.pyoracle import Oracle, Ref
+    n = points64.shape[0]
+    if Ref.available:
+        ref = Ref()
+        ref.set_threads(threads)
+        t0 = time.perf_counter()
+        est = ref.estimator(points64, 0, sigma, 2)
+        t_build = time.perf_counter() - t0
+        kind, backend = "reference", est.backend
+
+        def run(qs):
+            est.sample_counted(qs, rounds, seed)
+            est.eval(0, n, qs)
+    else:  # C restatement (exact backend), single thread
+        orc = Oracle()
+        t_build, kind, backend, threads = 0.0, "port", "exact (oracle restatement)", 1
+
+        def run(qs):
+            orc.sample_counted(points64, qs, rounds, seed, sigma)
+            orc.kde_exact(points64, 0, n, qs, sigma)
+    start = n // 4
+    s = 64
+    while True:  # calibrate: fixed per-call overheads make tiny probes pessimistic
+        t0 = time.perf_counter()
+        run(np.arange(start, start + s, dtype=np.uint32))
+        t = max(time.perf_counter() - t0, 1e-6)
+        if t >= target_s / 4 or s >= n - start:
+            break
+        s = int(min(n - start, s * min(8.0, 0.5 * target_s / t)))
+    s = int(min(n - start, max(64, s * target_s / t)))
+    return dict(run=run, start=start, block=s, t_build=t_build, kind=kind, backend=backend,
+                threads=threads)
+
+
+def cpu_baseline(points64, sigma, rounds, seed, target_s):
+    threads = os.cpu_count() or 1
+    rs = reference_sample(points64, sigma, rounds, seed, target_s, threads)
+    qs = np.arange(rs["start"], rs["start"] + rs["block"], dtype=np.uint32)
+    t0 = time.perf_counter()
+    rs["run"](qs)
+    dt = time.perf_counter() - t0
+    n = points64.shape[0]
+    value = rs["block"] * rounds / dt
+    return {
+        "value": value, "unit": "sampled edges/s", "cores": rs["threads"], "kind": rs["kind"],
+        "sample": (f"{rs['backend']} backend; sample_neighbors_counted + degree KDE for a "
+                   f"contiguous block of {rs['block']} of {n} queries (L={rounds}) on the full "
+                   f"point set; estimator build {rs['t_build']:.2f}s excluded"),
+        "sample_seconds": dt, "estimator_build_seconds": rs["t_build"],
+        "extrapolated_full_job_seconds": rs["t_build"] + dt * n / rs["block"],
+    }
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2310_13870_b200 import datasets
+    w = datasets.config(args.config)
+    p64 = w.points.astype(np.float64)
+    threads = os.cpu_count() or 1
+    rs = reference_sample(p64, w.sigma, w.rounds, 1, 6.0, threads)
+    qs = np.arange(rs["start"], rs["start"] + rs["block"], dtype=np.uint32)
+    for _ in range(args.warmup):
+        rs["run"](qs)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rs["run"](qs)
+        times.append(time.perf_counter() - t0)
+    step = float(np.mean(times))
+    value = rs["block"] * w.rounds / step
+    sample = (f"{rs['backend']} backend; each step = sample_neighbors_counted + degree KDE "
+              f"for a contiguous block of {rs['block']} of {w.n} queries (L={w.rounds}); "
+              f"estimator build {rs['t_build']:.2f}s once, untimed")
+    print(json.dumps({
+        "impl": "reference", "metric": metric_name(args.config),
+        "value": value, "unit": "sampled edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DOC[args.config]}",
+                   "query_block": rs["block"], "backend": rs["backend"]},
+        "cpu_baseline": {"value": value, "unit": "sampled edges/s", "cores": rs["threads"],
+                         "kind": rs["kind"], "sample": sample},
+        "e2e": {"value": value, "unit": "sampled edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ ours ----
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_13870_b200 as F
+    from paper_2310_13870_b200 import _native as N
+    from paper_2310_13870_b200 import datasets, parallel
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    w = datasets.config(args.config)
+    n, L = w.n, w.rounds
+    kernel = F.Kernel(F.KernelFamily.gaussian, w.sigma)
+    cfg = F.SparsifierConfig(rounds=L, seed=1)
+    ds = F.Dataset(w.points, device=local)
+    stream = torch.cuda.ExternalStream(N.lib().fsgg_dataset_stream(ds._h), device=local)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step():
+        if world == 1:
+            g, rep = F.build_similarity_graph_device(ds, kernel, cfg)
+            return g, rep
+        res = parallel.build_similarity_graph_distributed(ds, kernel, cfg)
+        return res.graph, res.report
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    total_ms, reps, edges = 0.0, [], 0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g, rep = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+        reps.append(rep)
+        edges = int(g.num_edges)
+    clk = clocks.stop() if clocks else None
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_s = float(t.item()) * 1e-3
+    K = args.steps
+    sampled_edges = n * L * K                     # tickets routed to leaves
+    value = sampled_edges / total_s
+    evals = sum(r.kernel_evals for r in reps)
+    tiled_evals = sum(r.kde_tiled_evals for r in reps)
+    tiled_s = sum(r.kde_tiled_seconds for r in reps)
+    tiled_launches = sum(r.kde_tiled_launches for r in reps)
+    launches = sum(r.gpu_launches for r in reps)
+    if world > 1:
+        agg = torch.tensor([evals, tiled_evals], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(agg)
+        evals = float(agg[0])
+
+    # ---- end-to-end through the public host API --------------------------
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.empty(w.points.shape, dtype=torch.float32, pin_memory=True)
+        pinned.numpy()[:] = w.points
+        host_ptr = pinned.data_ptr()
+        h2d = w.points.nbytes
+        e2e_ms, d2h = 0.0, 0
+        for i in range(args.warmup + K):
+            torch.cuda.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            ds.upload_ptr(host_ptr)
+            if world == 1:
+                g = F.build_similarity_graph(ds, kernel, cfg)
+                nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+            else:
+                parallel.build_similarity_graph_distributed(ds, kernel, cfg)
+                g = F.api.device_graph_to_host(ds)
+                nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+            torch.cuda.synchronize()
+            barrier()
+            if i >= args.warmup:
+                e2e_ms += (time.perf_counter() - t0) * 1e3
+                d2h = nbytes
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": sampled_edges / (float(t.item()) * 1e-3), "unit": "sampled edges/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(t.item()) / K}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----------------------------------
+    import ctypes as C
+    ex2 = C.c_double()
+    clk_mhz = C.c_double()
+    N.lib().fsgg_probe_ex2_throughput(local, C.byref(ex2), C.byref(clk_mhz))
+    props = torch.cuda.get_device_properties(local)
+    nominal = NOMINAL_EX2_PER_CLK_PER_SM * props.multi_processor_count * 1965e6
+    achieved = tiled_evals / max(tiled_s, 1e-12)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "kde_tiled_ncu.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {
+        "bound": "mufu", "kernel": "kde_lowd_tiled_kernel<2,gaussian>",
+        "achieved": achieved / 1e9, "peak": ex2.value / 1e9, "unit": "Gex2/s",
+        "frac": achieved / ex2.value if ex2.value else None,
+        "peak_source": "measured in this run: MUFU.EX2 microbenchmark (fsgg_probe_ex2_throughput)",
+        "nominal_peak": nominal / 1e9, "frac_of_nominal": achieved / nominal,
+        "algorithmic_unit": "one Gaussian kernel evaluation = one ex2 (SURVEY.md §8d)",
+        "evals_per_launch": tiled_evals / max(tiled_launches, 1),
+        "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
+        "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
+        "traffic": traffic,
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(w.points.astype(np.float64), w.sigma, L, 1, args.cpu_seconds)
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "error": repr(exc)}
+    line = {
+        "metric": metric_name(args.config),
+        "value": value, "unit": "sampled edges/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": total_s * 1e3 / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DOC[args.config]}", "n": n, "d": w.d,
+                   "sigma": w.sigma, "samples_per_point": L, "rng": "reference (splitmix64)",
+                   "parallelism": f"query shards x{world}", "l2": "flushed (512 MiB) between steps"},
+        "kernel_evals_per_s": evals / total_s, "kernel_evals_per_step": evals / K / max(world, 1),
+        "undirected_edges": edges, "undirected_edges_per_s": edges * K / total_s,
+        "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -166,6 +166,9 @@ uint32_t fsgg_dataset_size(const fsgg_dataset* ds);
 uint32_t fsgg_dataset_dim(const fsgg_dataset* ds);
 /* Raw device pointer of the fp32 coordinates. */
 const float* fsgg_dataset_device_points(const fsgg_dataset* ds);
+/* The cudaStream_t every kernel of this handle is launched on (for callers
+ * that time or order work around the library with CUDA events). */
+void* fsgg_dataset_stream(const fsgg_dataset* ds);
 
 /* fsg::build_similarity_graph (proj/include/fsg/sparsifier.hpp:64-67,
  * proj/src/sparsifier.cpp:51-142). Host output. `estimates` (nullable)
@@ -187,6 +190,10 @@ int fsgg_build_similarity_graph_host(const float* points, uint32_t n,
                                      uint32_t d, const fsgg_kernel* kernel,
                                      const fsgg_config* cfg, int device,
                                      fsgg_graph* out, fsgg_report* report);
+
+/* Copy the handle's current device graph (from the last device-resident
+ * or distributed build) into host memory (free with fsgg_graph_free). */
+int fsgg_device_graph_to_host(fsgg_dataset* ds, fsgg_graph* out);
 
 void fsgg_graph_free(fsgg_graph* g);
 void fsgg_free(void* p);
@@ -253,6 +260,11 @@ typedef struct fsgg_shard {
 int fsgg_sample_shard(fsgg_dataset* ds, const fsgg_kernel* kernel,
                       const fsgg_config* cfg, fsgg_shard* out,
                       fsgg_report* report);
+/* Copy the last shard's pair keys (num_pairs u64) and g_full slice
+ * (query_end - query_begin f64) into caller-owned device buffers (either
+ * may be NULL); completes before returning. */
+int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
+                      double* g_full_device);
 /* Phase 2 after the caller all-gathers g_full (n doubles, device) and the
  * shards' pair keys (concatenated, device, any order, duplicates allowed):
  * dedupe, weight, CSR and degrees exactly as the 1-GPU path. */

@@ -13,7 +13,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libfsgg.so")
-HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "fsgg.h")
+INCLUDE_DIR = os.path.join(os.path.dirname(HERE), "include")
 
 FSGG_OK = 0
 FSGG_ERR_CONFIG = 2
@@ -96,6 +96,8 @@ _SIGS = {
     "fsgg_dataset_size": (C.c_uint32, [_P]),
     "fsgg_dataset_dim": (C.c_uint32, [_P]),
     "fsgg_dataset_device_points": (_P, [_P]),
+    "fsgg_dataset_stream": (_P, [_P]),
+    "fsgg_shard_export": (C.c_int, [_P, _P, _P]),
     "fsgg_build_similarity_graph": (C.c_int, [_P, C.POINTER(fsgg_kernel),
                                               C.POINTER(fsgg_config), C.POINTER(fsgg_graph),
                                               C.POINTER(fsgg_report),
@@ -110,6 +112,7 @@ _SIGS = {
                                                    C.POINTER(fsgg_graph),
                                                    C.POINTER(fsgg_report)]),
     "fsgg_graph_free": (None, [C.POINTER(fsgg_graph)]),
+    "fsgg_device_graph_to_host": (C.c_int, [_P, C.POINTER(fsgg_graph)]),
     "fsgg_free": (None, [_P]),
     "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
                                                 C.c_uint32, C.c_uint64, C.c_int,
@@ -126,17 +129,23 @@ _SIGS = {
                                 _P, _P]),
     "fsgg_sample_shard": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.POINTER(fsgg_config),
                                     C.POINTER(fsgg_shard), C.POINTER(fsgg_report)]),
+    "fsgg_probe_ex2_throughput": (C.c_int, [C.c_int, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_double)]),
     "fsgg_finish_graph": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32, _P, _P,
                                     C.c_uint64, C.POINTER(fsgg_device_graph),
                                     C.POINTER(fsgg_report)]),
 }
 
 
-def header_functions(path: str = HEADER_PATH) -> list[str]:
-    """Every function name declared in include/fsgg.h."""
-    text = open(path).read()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(fsgg_[a-z0-9_]+)\s*\(", text)))
+def header_functions(include_dir: str = INCLUDE_DIR) -> list[str]:
+    """Every function name declared in include/*.h."""
+    names = set()
+    for fn in sorted(os.listdir(include_dir)):
+        if fn.endswith(".h"):
+            text = open(os.path.join(include_dir, fn)).read()
+            text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+            names |= set(re.findall(r"\b(fsgg_[a-z0-9_]+)\s*\(", text))
+    return sorted(names)
 
 
 _lib = None

@@ -265,6 +265,29 @@ def _as_numpy(ptr, count, ctype, dtype):
     return np.array(arr, dtype=dtype, copy=True)
 
 
+def _graph_from_c(g) -> WeightedGraph:
+    m = int(g.num_edges)
+    return WeightedGraph(
+        n=int(g.n), u=_as_numpy(g.u, m, C.c_uint32, np.uint32),
+        v=_as_numpy(g.v, m, C.c_uint32, np.uint32),
+        w=_as_numpy(g.w, m, C.c_double, np.float64),
+        row_ptr=_as_numpy(g.row_ptr, int(g.n) + 1, C.c_uint64, np.uint64),
+        degrees=_as_numpy(g.degrees, int(g.n), C.c_double, np.float64),
+        total_weight=float(g.total_weight))
+
+
+def device_graph_to_host(ds: Dataset) -> WeightedGraph:
+    """Host copy of the graph left on the device by the last device-resident
+    or distributed build on ``ds``."""
+    g = N.fsgg_graph()
+    lib = N.lib()
+    N.check(lib.fsgg_device_graph_to_host(ds._h, C.byref(g)))
+    try:
+        return _graph_from_c(g)
+    finally:
+        lib.fsgg_graph_free(C.byref(g))
+
+
 def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig | None = None,
                            report: bool = False, estimates: bool = False):
     """FastSimilarityGraph (proj/src/sparsifier.cpp:51-142) on the device.
@@ -281,14 +304,7 @@ def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig
                                             C.byref(rep),
                                             C.byref(est) if estimates else None))
     try:
-        m = int(g.num_edges)
-        graph = WeightedGraph(
-            n=int(g.n), u=_as_numpy(g.u, m, C.c_uint32, np.uint32),
-            v=_as_numpy(g.v, m, C.c_uint32, np.uint32),
-            w=_as_numpy(g.w, m, C.c_double, np.float64),
-            row_ptr=_as_numpy(g.row_ptr, int(g.n) + 1, C.c_uint64, np.uint64),
-            degrees=_as_numpy(g.degrees, int(g.n), C.c_double, np.float64),
-            total_weight=float(g.total_weight))
+        graph = _graph_from_c(g)
     finally:
         lib.fsgg_graph_free(C.byref(g))
     est_arr = None

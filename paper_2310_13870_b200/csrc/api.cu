@@ -22,6 +22,7 @@ struct fsgg_dataset {
   std::unique_ptr<fsgg::GraphResult> graph;
   std::unique_ptr<fsgg::SampleResult> shard;
   fsgg::DevBuf shard_keys;
+  uint64_t shard_npairs = 0;
   ~fsgg_dataset() {
     graph.reset();
     shard.reset();
@@ -370,6 +371,10 @@ const float* fsgg_dataset_device_points(const fsgg_dataset* h) {
   return h ? h->ds.pts.as<float>() : nullptr;
 }
 
+void* fsgg_dataset_stream(const fsgg_dataset* h) {
+  return h ? static_cast<void*>(h->ds.stream) : nullptr;
+}
+
 int fsgg_build_similarity_graph(fsgg_dataset* h, const fsgg_kernel* kernel,
                                 const fsgg_config* cfg, fsgg_graph* out,
                                 fsgg_report* report, fsgg_edge_estimate** estimates) {
@@ -403,6 +408,15 @@ int fsgg_build_similarity_graph_host(const float* points, uint32_t n, uint32_t d
   rc = fsgg_build_similarity_graph(h, kernel, cfg, out, report, nullptr);
   fsgg_dataset_destroy(h);
   return rc;
+}
+
+int fsgg_device_graph_to_host(fsgg_dataset* h, fsgg_graph* out) {
+  return guarded([&] {
+    activate(h);
+    if (!out) throw fsgg::ConfigError("null output");
+    if (!h->graph) throw fsgg::ConfigError("no graph built on this dataset");
+    graph_to_host(h, out);
+  });
 }
 
 void fsgg_graph_free(fsgg_graph* g) {
@@ -520,12 +534,29 @@ int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_con
     out->query_end = qe;
     out->rounds = bo.L;
     out->num_pairs = npairs;
+    h->shard_npairs = npairs;
     out->pairs = h->shard_keys.as<uint64_t>();
     out->g_full = h->shard->groot.as<double>();
     out->sampled_pairs = bo.sampled;
     out->self_pairs = bo.self;
     out->degenerate_draws = bo.degenerate;
     if (report) finish_report(report, ds, bo, nullptr, now() - t0);
+  });
+}
+
+int fsgg_shard_export(fsgg_dataset* h, uint64_t* pairs_device, double* g_full_device) {
+  return guarded([&] {
+    activate(h);
+    if (!h->shard) throw fsgg::ConfigError("no shard sampled on this dataset");
+    cudaStream_t s = h->ds.stream;
+    const fsgg::SampleResult& r = *h->shard;
+    if (pairs_device && h->shard_npairs)
+      FSGG_CUDA(cudaMemcpyAsync(pairs_device, h->shard_keys.as<void>(), h->shard_npairs * 8,
+                                cudaMemcpyDeviceToDevice, s));
+    if (g_full_device && r.nq)
+      FSGG_CUDA(cudaMemcpyAsync(g_full_device, r.groot.as<void>(), size_t(r.nq) * 8,
+                                cudaMemcpyDeviceToDevice, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
   });
 }
 
