@@ -56,6 +56,7 @@ constexpr int kXBK = 16;             // dims per high-d k-step
 constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
 constexpr uint64_t kMaxPartials = 64ull << 20;  // doubles
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
+constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
 
 template <int D>
 struct LowDTile {
@@ -142,19 +143,24 @@ __device__ __forceinline__ void lowd_range_sum(
       sm[idx] = make_float2(v, v);
     }
     __syncthreads();
-    float2 acc = make_float2(0.f, 0.f);
+    // fp32 partial sums over runs of kFlush sources, flushed into fp64:
+    // keeps the accumulation error ~1e-7 relative at no measurable cost.
+    for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
+      const uint32_t j1 = min(lenp, j0 + kFlush);
+      float2 acc = make_float2(0.f, 0.f);
 #pragma unroll 4
-    for (uint32_t j = 0; j < lenp; ++j) {
-      const float2* x = sm + j * D;
-      float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
+      for (uint32_t j = j0; j < j1; ++j) {
+        const float2* x = sm + j * D;
+        float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
 #pragma unroll
-      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
-      t = fam_finish<FAM>(t);
-      const float2 arg = __ffma2_rn(t, ms, off2);
-      acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+        for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
+        t = fam_finish<FAM>(t);
+        const float2 arg = __ffma2_rn(t, ms, off2);
+        acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+      }
+      accA += acc.x;
+      accB += acc.y;
     }
-    accA += acc.x;
-    accB += acc.y;
   }
 }
 

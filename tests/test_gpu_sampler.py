@@ -1,0 +1,297 @@
+"""GPU tests restating the reference's sampler / sparsifier / KDE suites
+(proj/tests/test_sampler.cpp, test_sparsifier.cpp, test_kde.cpp) against the
+CUDA path, plus parity against the C oracle on every kernel family and
+dimension class (low-d tiled/direct kernels, high-d CUDA-core kernels)."""
+import math
+
+import numpy as np
+import pytest
+from scipy.stats import chi2 as chi2_dist
+
+import paper_2310_13870_b200 as F
+from paper_2310_13870_b200 import datasets
+
+pytestmark = pytest.mark.gpu
+
+G = F.KernelFamily.gaussian
+E = F.KernelFamily.exponential
+LAP = F.KernelFamily.laplacian
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+
+
+def exact_distribution(p, kernel, q):
+    k = np.array([kernel(p[q], p[j]) for j in range(p.shape[0])])
+    return k / k.sum()
+
+
+def chi2_ok(obs, expect_p, rounds, alpha=1e-3):
+    # Cochran merge of bins with expected count < 5 (test_sampler.cpp:112-124)
+    e = expect_p * rounds
+    small = e < 5
+    stat = (((obs[~small] - e[~small]) ** 2) / e[~small]).sum()
+    bins = int((~small).sum())
+    if small.any():
+        stat += (obs[small].sum() - e[small].sum()) ** 2 / e[small].sum()
+        bins += 1
+    return stat <= chi2_dist.ppf(1 - alpha, bins - 1)
+
+
+# ---- KDE (proj/tests/test_kde.cpp) -----------------------------------------
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_kde_vs_brute_force(oracle, seed):
+    n = 400 + 300 * seed
+    p = oracle.random_dataset(n, 2, seed).astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.2)
+    t = np.arange(min(n, 150))
+    got = F.exact_kde(ds, k, 0, n, t)
+    ref = oracle.kde_exact(p.astype(np.float64), 0, n, t, 0.2)
+    assert rel(got, ref).max() <= 5e-6
+
+
+def test_kde_range_additivity(oracle):
+    p = oracle.random_dataset(257, 3, 5).astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(E, 0.4)
+    t = np.arange(40)
+    whole = F.exact_kde(ds, k, 0, 257, t)
+    for cut in (1, 2, 100, 128, 200, 256):
+        lo = F.exact_kde(ds, k, 0, cut, t)
+        hi = F.exact_kde(ds, k, cut, 257, t)
+        assert rel(lo + hi, whole).max() <= 1e-6
+
+
+def test_kde_positivity_and_empty_range(oracle):
+    p = oracle.random_dataset(64, 2, 9, 0.0, 100.0).astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.01)  # far-apart points underflow
+    assert F.exact_kde(ds, k, 1, 33, [0])[0] > 0.0
+    assert F.exact_kde(ds, k, 5, 5, [0, 1])[0] == 0.0
+
+
+def test_kde_rejects_malformed(oracle):
+    ds = F.Dataset(oracle.random_dataset(50, 2, 3).astype(np.float32))
+    est = F.make_estimator(ds, F.Kernel(G, 0.5))
+    with pytest.raises(F.InvalidConfig):
+        est.eval(40, 20, [0])
+    with pytest.raises(F.InvalidConfig):
+        est.eval(0, 51, [0])
+    with pytest.raises(F.InvalidConfig):
+        est.eval(0, 50, [50])
+
+
+@pytest.mark.parametrize("d,fam,sigma", [(1, G, 0.1), (3, E, 0.3), (4, LAP, 0.5), (5, G, 0.2),
+                                         (8, G, 0.6), (12, G, 1.0), (33, E, 2.0),
+                                         (784, G, 11.7)])
+def test_kde_dims_families_vs_oracle(oracle, d, fam, sigma):
+    rng = np.random.default_rng(d)
+    n = 3000 if d <= 8 else 1500
+    p = rng.random((n, d)).astype(np.float32)
+    ds = F.Dataset(p)
+    t = rng.choice(n, 100, replace=False)
+    for a, b in [(0, n), (17, n // 3), (n // 2, n)]:
+        got = F.exact_kde(ds, F.Kernel(fam, sigma), a, b, t)
+        ref = oracle.kde_exact(p.astype(np.float64), a, b, t, sigma, family=int(fam))
+        mask = ref >= 1e-30
+        assert rel(got[mask], ref[mask]).max() <= 2e-5
+
+
+# ---- sampler (proj/tests/test_sampler.cpp) ----------------------------------
+def test_single_point_source_set():
+    ds = F.Dataset(np.array([[0.5, 0.5]], np.float32))
+    out = F.sample_neighbors(ds, F.Kernel(G, 1.0), [0, 0, 0], 123)
+    assert out.shape == (3, 2) and np.all(out == 0)
+
+
+def test_n4_empirical_distribution_tv(oracle):
+    p = oracle.random_dataset(4, 2, 17)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.5)
+    for q in range(4):
+        tri = F.sample_neighbors_counted(ds, k, [q], 100000, 7 + q)
+        emp = np.zeros(4)
+        emp[tri[:, 1]] = tri[:, 2] / 100000
+        expect = exact_distribution(p.astype(np.float32).astype(np.float64), k, q)
+        assert 0.5 * np.abs(emp - expect).sum() <= 0.02
+
+
+def test_separated_clusters_stay_on_side():
+    p, lab = datasets.make_blobs(40, [[0.0, 0.0], [100.0, 100.0]], 0.05, 3)
+    ds = F.Dataset(p)
+    tri = F.sample_neighbors_counted(ds, F.Kernel(G, 0.1), [0], 20000, 11)
+    same = tri[lab[tri[:, 1]] == lab[0], 2].sum()
+    assert same / tri[:, 2].sum() >= 0.99
+
+
+@pytest.mark.parametrize("rng_mode", [F.RngMode.reference, F.RngMode.philox])
+def test_chi_squared_goodness_of_fit(oracle, rng_mode):
+    n, rounds = 48, 120000
+    p = oracle.random_dataset(n, 2, 29)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.4)
+    p32 = p.astype(np.float32).astype(np.float64)
+    for q in (0, 17, 40):
+        tri = F.sample_neighbors_counted(ds, k, [q], rounds, 1000 + q, rng_mode=rng_mode)
+        obs = np.zeros(n)
+        obs[tri[:, 1]] = tri[:, 2]
+        assert chi2_ok(obs, exact_distribution(p32, k, q), rounds)
+
+
+def test_reference_mode_matches_oracle_edge_for_edge(oracle):
+    # duplicate queries merge (sampler.cpp:89-106); every family and d class
+    rng = np.random.default_rng(4)
+    for n, d, fam, sigma, L in [(500, 2, G, 0.1, 9), (300, 3, E, 0.3, 11), (260, 5, LAP, 0.7, 6),
+                                (200, 20, G, 1.5, 5), (150, 784, G, 11.0, 4)]:
+        p = rng.random((n, d)).astype(np.float32)
+        ds = F.Dataset(p)
+        q = np.array([3, 1, 3, n - 1, 0, 3, n // 2])
+        got = F.sample_neighbors_counted(ds, F.Kernel(fam, sigma), q, L, 21)
+        ref = oracle.sample_counted(p.astype(np.float64), q, L, 21, sigma, family=int(fam))
+        assert np.array_equal(got, ref["triples"]), (n, d, int(fam))
+
+
+def test_ticket_mass_and_determinism(oracle):
+    p = oracle.random_dataset(128, 2, 8).astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.3)
+    a = F.sample_neighbors(ds, k, np.arange(128), 42)
+    b = F.sample_neighbors(ds, k, np.arange(128), 42)
+    c = F.sample_neighbors(ds, k, np.arange(128), 43)
+    assert np.array_equal(a, b)
+    assert np.any(a[:, 1] != c[:, 1])
+
+
+def test_sampler_validation():
+    ds = F.Dataset(np.random.default_rng(1).random((10, 2)).astype(np.float32))
+    k = F.Kernel(G, 1.0)
+    with pytest.raises(F.InvalidConfig):
+        F.sample_neighbors(ds, k, [10], 1)
+    with pytest.raises(F.InvalidConfig):
+        F.sample_neighbors_counted(ds, k, [1], 0, 1)
+    with pytest.raises(F.InvalidConfig):
+        F.sample_neighbors_counted(ds, k, [1, 1], 2**31, 1)  # 2^32 tickets
+    assert F.sample_neighbors_counted(ds, k, [], 4, 1).shape == (0, 3)
+
+
+def test_dataset_validation():
+    with pytest.raises(F.InvalidConfig):
+        F.Dataset(np.array([[0.0, np.nan]], np.float32))
+    with pytest.raises(F.InvalidConfig):
+        F.Dataset(np.zeros((0, 2), np.float32))
+
+
+# ---- sparsifier (proj/tests/test_sparsifier.cpp) ----------------------------
+def test_build_rejects_single_point():
+    ds = F.Dataset(np.array([[0.0, 0.0]], np.float32))
+    with pytest.raises(F.TooFewPoints):
+        F.build_similarity_graph(ds, F.Kernel(G, 1.0))
+
+
+def test_edge_count_bound_and_invariants(oracle):
+    for seed in (1, 2, 3):
+        p = oracle.random_dataset(120, 2, seed).astype(np.float32)
+        g, rep, _ = F.build_similarity_graph(F.Dataset(p), F.Kernel(G, 0.3),
+                                             F.SparsifierConfig(seed=seed), report=True)
+        assert rep.rounds == 42  # ceil(6 log2 120)
+        assert g.num_edges() <= 120 * rep.rounds
+        assert np.all(g.u < g.v) and np.all(g.w > 0) and np.all(np.isfinite(g.w))
+        key = g.u.astype(np.int64) << 32 | g.v.astype(np.int64)
+        assert np.all(np.diff(key) > 0)
+
+
+@pytest.mark.parametrize("d,fam,sigma,L", [(2, G, 0.25, 0), (3, E, 0.35, 16), (5, LAP, 0.9, 12),
+                                           (9, G, 1.0, 8), (784, G, 11.7, 6)])
+def test_graph_vs_oracle(oracle, d, fam, sigma, L):
+    rng = np.random.default_rng(100 + d)
+    n = 700 if d < 784 else 300
+    p = rng.random((n, d)).astype(np.float32)
+    g, rep, est = F.build_similarity_graph(F.Dataset(p), F.Kernel(fam, sigma),
+                                           F.SparsifierConfig(rounds=L, seed=4), report=True,
+                                           estimates=True)
+    ref = oracle.build_graph(p.astype(np.float64), sigma, L, seed=4, family=int(fam))
+    assert np.array_equal(g.u, ref["u"]) and np.array_equal(g.v, ref["v"])
+    assert rel(g.w, ref["w"]).max() <= 1e-5
+    assert rel(g.degrees, ref["degrees"]).max() <= 1e-5
+    # fp64 kernel value with the reference binary's operation order; only the
+    # libm exp differs (CUDA exp <= 1 ulp vs glibc), so <= 2 ulp apart
+    assert rel(est["k_ij"], ref["estimates"][:, 2]).max() <= 5e-16
+    assert rep.self_pairs_discarded == ref["report"]["self_pairs_discarded"]
+    assert rep.sampled_pairs == ref["report"]["sampled_pairs"]
+
+
+def test_degree_ratio_vs_full_graph():
+    # proj/tests/test_sparsifier.cpp:103-114
+    p, _ = datasets.make_blobs(200, [[0.0, 0.0], [6.0, 0.0]], 0.6, 5)
+    k = F.Kernel(G, 0.7)
+    g = F.build_similarity_graph(F.Dataset(p), k, F.SparsifierConfig(seed=10))
+    p32 = p.astype(np.float32).astype(np.float64)
+    d2 = ((p32[:, None, :] - p32[None, :, :]) ** 2).sum(-1)
+    K = np.exp(-d2 / 0.49)
+    full_deg = K.sum(1) - 1.0
+    ratio = g.degrees / full_deg
+    assert ratio.min() >= 1 / 3 and ratio.max() <= 3
+
+
+def test_same_seed_reproduces_bitwise(oracle):
+    p = oracle.random_dataset(150, 2, 33).astype(np.float32)
+    ds = F.Dataset(p)
+    a = F.build_similarity_graph(ds, F.Kernel(G, 0.3), F.SparsifierConfig(seed=77))
+    b = F.build_similarity_graph(ds, F.Kernel(G, 0.3), F.SparsifierConfig(seed=77))
+    assert np.array_equal(a.u, b.u) and np.array_equal(a.v, b.v)
+    assert np.array_equal(a.w, b.w) and np.array_equal(a.degrees, b.degrees)
+
+
+def test_p_hat_band(oracle):
+    # proj/tests/test_sparsifier.cpp:228-247
+    n = 96
+    p = oracle.random_dataset(n, 2, 55).astype(np.float32)
+    k = F.Kernel(G, 0.35)
+    g, _, est = F.build_similarity_graph(F.Dataset(p), k, F.SparsifierConfig(seed=8),
+                                         estimates=True)
+    p64 = p.astype(np.float64)
+    d2 = ((p64[:, None, :] - p64[None, :, :]) ** 2).sum(-1)
+    K = np.exp(-d2 / 0.35 ** 2)
+    deg = K.sum(1) - 1.0
+    logn = math.log2(n)
+    pi = np.minimum(logn * est["k_ij"] / deg[est["i"]], 1.0)
+    pj = np.minimum(logn * est["k_ij"] / deg[est["j"]], 1.0)
+    pref = pi + pj - pi * pj
+    assert np.all(est["p_hat"] >= 6 / 7 * pref) and np.all(est["p_hat"] <= 36 / 5 * pref)
+
+
+def test_sharded_build_is_bit_identical(oracle):
+    """Query shards processed separately (as on N GPUs) and merged through
+    fsgg_finish_graph reproduce the 1-GPU graph bit for bit."""
+    import torch
+    from paper_2310_13870_b200 import parallel
+    p, _ = datasets.make_moons(3000, 0.05, 2)
+    ds = F.Dataset(p)
+    k = F.Kernel(G, 0.1)
+    cfg = F.SparsifierConfig(rounds=16, seed=3)
+    full = F.build_similarity_graph(ds, k, cfg)
+    for world in (2, 3):
+        pairs, gs = [], []
+        for r in range(world):
+            qb, qe = parallel.shard_range(3000, r, world)
+            sh, _, pr, g = parallel.sample_shard(
+                ds, k, F.SparsifierConfig(rounds=16, seed=3, query_begin=qb, query_end=qe))
+            pairs.append(pr)
+            gs.append(g)
+        parallel.finish_graph(ds, k, 16, torch.cat(gs), torch.cat(pairs))
+        g = F.api.device_graph_to_host(ds)
+        assert np.array_equal(g.u, full.u) and np.array_equal(g.v, full.v)
+        assert np.array_equal(g.w, full.w) and np.array_equal(g.degrees, full.degrees)
+
+
+def test_philox_mode_graph_is_valid():
+    p, _ = datasets.make_moons(2000, 0.05, 1)
+    g, rep, est = F.build_similarity_graph(
+        F.Dataset(p), F.Kernel(G, 0.1),
+        F.SparsifierConfig(rounds=32, seed=5, rng_mode=F.RngMode.philox), report=True,
+        estimates=True)
+    assert rep.sampled_pairs > 0 and g.num_edges() <= 2000 * 32
+    assert np.all(np.abs(g.w * est["p_hat"] - est["k_ij"]) <= 1e-12 * est["k_ij"])
