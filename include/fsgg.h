@@ -69,6 +69,11 @@ typedef struct fsgg_config {
    * Results for a query never depend on the shard layout. */
   uint32_t query_begin;
   uint32_t query_end;
+  /* 0 (default): certified pruning — a source sub-chunk whose bounding-box
+   * bound is below 2^-80 of the entry's node mass is skipped (total skipped
+   * mass < 2^-60 of the node mass; routing decisions unchanged).
+   * 1: evaluate every kernel term (dense). */
+  int dense_kde;
 } fsgg_config;
 
 /* Mirrors fsg::BuildReport (proj/include/fsg/sparsifier.hpp:40-58), plus
@@ -98,6 +103,8 @@ typedef struct fsgg_report {
   uint32_t levels;
   uint64_t peak_entries;
   uint32_t gpu_launches;      /* kernels launched by this call */
+  uint64_t kernel_evals_performed;    /* evaluations actually executed */
+  uint64_t kde_tiled_performed_evals; /* of which in the tiled kernel */
 } fsgg_report;
 
 /* Per-edge quantities of the weighting step (sparsifier.hpp:29-38). */
@@ -213,8 +220,8 @@ typedef struct fsgg_sample_diag {
 int fsgg_sample_neighbors_counted(fsgg_dataset* ds, const fsgg_kernel* kernel,
                                   const uint32_t* queries, size_t num_queries,
                                   uint32_t rounds, uint64_t seed, int rng_mode,
-                                  uint32_t** triples, size_t* count,
-                                  fsgg_sample_diag* diag);
+                                  int dense_kde, uint32_t** triples,
+                                  size_t* count, fsgg_sample_diag* diag);
 
 /* fsg::KdeEstimator::eval (proj/include/fsg/kde.hpp:54-58, exact backend
  * proj/src/kde.cpp:57-71): out[t] = max(sum_{j in [first,last)} k(x_t, x_j),

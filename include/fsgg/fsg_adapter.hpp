@@ -133,7 +133,7 @@ inline std::vector<fsg::CountedNeighborSample> sample_neighbors_counted(
   fsgg_sample_diag diag;
   throw_for(fsgg_sample_neighbors_counted(dd.get(), &k, queries.data(),
                                           queries.size(), rounds, seed,
-                                          FSGG_RNG_REFERENCE, &tri, &count,
+                                          FSGG_RNG_REFERENCE, 0, &tri, &count,
                                           &diag),
             "fsgg_sample_neighbors_counted");
   std::vector<fsg::CountedNeighborSample> out(count);

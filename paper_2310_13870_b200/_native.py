@@ -30,7 +30,8 @@ class fsgg_config(C.Structure):
     _fields_ = [("C", C.c_double), ("lambda_k1_estimate", C.c_double),
                 ("rounds", C.c_uint32), ("epsilon", C.c_double), ("log_base", C.c_int),
                 ("seed", C.c_uint64), ("rng_mode", C.c_int),
-                ("query_begin", C.c_uint32), ("query_end", C.c_uint32)]
+                ("query_begin", C.c_uint32), ("query_end", C.c_uint32),
+                ("dense_kde", C.c_int)]
 
 
 class fsgg_report(C.Structure):
@@ -45,7 +46,8 @@ class fsgg_report(C.Structure):
                 ("kernel_evals", C.c_uint64), ("kde_tiled_evals", C.c_uint64),
                 ("kde_tiled_seconds", C.c_double), ("kde_tiled_launches", C.c_uint32),
                 ("levels", C.c_uint32), ("peak_entries", C.c_uint64),
-                ("gpu_launches", C.c_uint32)]
+                ("gpu_launches", C.c_uint32), ("kernel_evals_performed", C.c_uint64),
+                ("kde_tiled_performed_evals", C.c_uint64)]
 
 
 class fsgg_edge_estimate(C.Structure):
@@ -115,7 +117,7 @@ _SIGS = {
     "fsgg_device_graph_to_host": (C.c_int, [_P, C.POINTER(fsgg_graph)]),
     "fsgg_free": (None, [_P]),
     "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
-                                                C.c_uint32, C.c_uint64, C.c_int,
+                                                C.c_uint32, C.c_uint64, C.c_int, C.c_int,
                                                 C.POINTER(_P), C.POINTER(C.c_size_t),
                                                 C.POINTER(fsgg_sample_diag)]),
     "fsgg_kde_eval": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32, C.c_uint32, _P,

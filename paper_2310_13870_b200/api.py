@@ -93,6 +93,7 @@ class SparsifierConfig:
     rng_mode: RngMode = RngMode.reference
     query_begin: int = 0
     query_end: int = 0
+    dense_kde: bool = False  # True: evaluate every kernel term (no certified pruning)
 
     def _c(self):
         c = N.fsgg_config()
@@ -105,6 +106,7 @@ class SparsifierConfig:
         c.rng_mode = int(self.rng_mode)
         c.query_begin = self.query_begin
         c.query_end = self.query_end
+        c.dense_kde = int(self.dense_kde)
         return c
 
     def rounds_for(self, n: int) -> int:
@@ -243,6 +245,8 @@ class BuildReport:
     levels: int = 0
     peak_entries: int = 0
     gpu_launches: int = 0
+    kernel_evals_performed: int = 0
+    kde_tiled_performed_evals: int = 0
 
     @classmethod
     def _from_c(cls, r):
@@ -341,7 +345,8 @@ class SampleDiagnostics:
 
 
 def sample_neighbors_counted(ds: Dataset, kernel: Kernel, queries, rounds: int, seed: int,
-                             rng_mode: RngMode = RngMode.reference, diagnostics: bool = False):
+                             rng_mode: RngMode = RngMode.reference, diagnostics: bool = False,
+                             dense_kde: bool = False):
     """proj/src/sampler.cpp:77-247: (query, source, count) rows sorted by
     (query, source), as an (m, 3) uint32 array."""
     q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64))
@@ -355,7 +360,8 @@ def sample_neighbors_counted(ds: Dataset, kernel: Kernel, queries, rounds: int, 
     lib = N.lib()
     N.check(lib.fsgg_sample_neighbors_counted(ds._h, C.byref(k), q.ctypes.data_as(C.c_void_p),
                                               q.size, rounds, seed, int(rng_mode),
-                                              C.byref(out), C.byref(cnt), C.byref(diag)))
+                                              int(dense_kde), C.byref(out), C.byref(cnt),
+                                              C.byref(diag)))
     m = cnt.value
     tri = _as_numpy(out, 3 * m, C.c_uint32, np.uint32).reshape(m, 3)
     lib.fsgg_free(out)

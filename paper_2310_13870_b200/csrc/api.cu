@@ -184,6 +184,7 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   req.tickets.assign(qe - qb, L);
   req.seed = cfg.seed;
   req.rng_mode = cfg.rng_mode;
+  req.prune = cfg.dense_kde ? 0 : 1;
   req.want_root_sums = true;
   fsgg::sample_counted(ds, ks, req, res);
   double t2 = now();
@@ -217,6 +218,8 @@ void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
     r->graph_bytes = g->m * 16 + uint64_t(g->n) * 8;
   }
   r->kernel_evals = bo.kde.evals;
+  r->kernel_evals_performed = bo.kde.performed;
+  r->kde_tiled_performed_evals = bo.kde.tiled_performed;
   r->kde_tiled_evals = bo.kde.tiled_evals;
   r->kde_tiled_seconds = bo.kde.tiled_seconds;
   r->kde_tiled_launches = bo.kde.tiled_launches;
@@ -434,7 +437,7 @@ void fsgg_free(void* p) { std::free(p); }
 int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
                                   const uint32_t* queries, size_t num_queries,
                                   uint32_t rounds, uint64_t seed, int rng_mode,
-                                  uint32_t** triples, size_t* count,
+                                  int dense_kde, uint32_t** triples, size_t* count,
                                   fsgg_sample_diag* diag) {
   return guarded([&] {
     activate(h);
@@ -459,6 +462,7 @@ int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
     }
     req.seed = seed;
     req.rng_mode = rng_mode;
+    req.prune = dense_kde ? 0 : 1;
     std::vector<uint32_t> host;
     fsgg::SampleResult res;
     if (!req.queries.empty()) {

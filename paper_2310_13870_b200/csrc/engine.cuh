@@ -109,13 +109,17 @@ struct LevelView {
   uint32_t num_slots = 0;  // 2^level
   uint32_t num_entries = 0;
   const uint32_t* eq = nullptr;    // query index per entry
+  const float* elm = nullptr;      // log2 of the entry's node mass (nullptr: root)
+  int prune = 1;                   // certified pruning of negligible sub-chunks
   const uint32_t* eg = nullptr;    // level-local slot per entry
   const uint32_t* goff = nullptr;  // num_slots + 1
 };
 
 struct KdeStats {
-  uint64_t evals = 0;
+  uint64_t evals = 0;            // algorithmic (reference-equivalent) evaluations
+  uint64_t performed = 0;        // evaluations actually executed
   uint64_t tiled_evals = 0;
+  uint64_t tiled_performed = 0;
   double tiled_seconds = 0.0;
   uint32_t tiled_launches = 0;
 };
@@ -144,6 +148,7 @@ struct SampleRequest {
   std::vector<uint32_t> tickets;  // tickets per query (rounds * multiplicity)
   uint64_t seed = 1;
   int rng_mode = 0;
+  int prune = 1;
   bool want_root_sums = false;
 };
 

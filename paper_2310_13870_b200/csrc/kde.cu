@@ -57,6 +57,8 @@ constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
 constexpr uint64_t kMaxPartials = 64ull << 20;  // doubles
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
+constexpr float kPruneBits = 80.f;   // sub-chunk bound below 2^-80 of the node mass
+constexpr uint32_t kSubMin = 1024;   // smallest sub-chunk (pruning granularity)
 
 template <int D>
 struct LowDTile {
@@ -130,7 +132,7 @@ template <int D, int FAM>
 __device__ __forceinline__ void lowd_range_sum(
     const float* __restrict__ pts, float2* sm, const float2 (&q2)[D],
     float2 off2, float scale, uint32_t cf, uint32_t cl, double& accA,
-    double& accB) {
+    double& accB, bool warp_skip = false) {
   constexpr int T = LowDTile<D>::T;
   const float2 ms = make_float2(-scale, -scale);
   for (uint32_t t0 = cf; t0 < cl; t0 += T) {
@@ -143,6 +145,7 @@ __device__ __forceinline__ void lowd_range_sum(
       sm[idx] = make_float2(v, v);
     }
     __syncthreads();
+    if (warp_skip) continue;  // this warp's entries all prune the range
     // fp32 partial sums over runs of kFlush sources, flushed into fp64:
     // keeps the accumulation error ~1e-7 relative at no measurable cost.
     for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
@@ -165,24 +168,39 @@ __device__ __forceinline__ void lowd_range_sum(
 }
 
 // ---- low-d tiled kernel (node size > direct threshold) --------------------
-// One CTA = (node slot, block of <= 256 entries, child side, source chunk).
-// Chunks are the node's descendants `cdepth` levels below the child, so
-// their boundaries and bounding boxes come from the tree table and depend
-// only on the node. Writes one fp64 partial per (entry, side, chunk).
+// One CTA = (node slot, block of <= 256 entries, child side, chunk group).
+// A chunk group is one of the child's tree descendants `cdepth` levels down;
+// it is walked as its descendants `sdepth` levels below the child
+// ("sub-chunks", ~1-2K sources, one shared-memory tile each). Boundaries and
+// bounding boxes of both come from the tree table, so they depend only on
+// the node. Writes one fp64 partial per (entry, side, group).
+//
+// Certified pruning (prune != 0): a sub-chunk c can contribute at most
+// |c| * 2^-off_c to an entry's sum (off_c = scale * dist(q, bbox(c))). It is
+// skipped when that bound is below 2^-kPruneBits of half the entry's node
+// mass (known from the previous level; >= 1 at the root, which holds the
+// query itself). With at most 2^20 sub-chunks per node the total skipped
+// mass is < 2^-60 of the node mass: routing compares u < p on a 2^-53 grid,
+// so decisions are unchanged (the fp32 evaluation itself perturbs p ~2^40
+// times more). The whole CTA skips when all its entries agree; a warp skips
+// the arithmetic when all of its entries do.
 template <int D, int FAM>
 __global__ void __launch_bounds__(kThreads)
     kde_lowd_tiled_kernel(const float* __restrict__ pts,
                           const uint32_t* __restrict__ eq,
+                          const float* __restrict__ elm,
                           const uint32_t* __restrict__ goff,
                           const uint32_t* __restrict__ blk_off,
                           uint32_t num_slots, uint32_t level, uint32_t cdepth,
-                          const uint32_t* __restrict__ tfirst,
+                          uint32_t sdepth, const uint32_t* __restrict__ tfirst,
                           const uint32_t* __restrict__ tlast,
                           const float* __restrict__ tlo,
                           const float* __restrict__ thi, int has_boxes,
-                          float scale, double* __restrict__ partials) {
+                          float scale, int prune, double* __restrict__ partials,
+                          unsigned long long* __restrict__ performed) {
   constexpr int T = LowDTile<D>::T;
   __shared__ __align__(16) float2 sm[T * D];
+  __shared__ unsigned long long s_done;
   const uint32_t K = 1u << cdepth;
   const uint32_t item = blockIdx.x;
   const uint32_t blk = item >> (cdepth + 1);
@@ -191,10 +209,6 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t g = find_slot(blk_off, num_slots, blk);
   const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kBE;
   const uint32_t e1 = min(e0 + kBE, goff[g + 1]);
-
-  const uint32_t lc = level + 1 + cdepth;
-  const uint64_t h = ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
-  const uint32_t cf = tfirst[h], cl = tlast[h];
 
   const uint32_t ia = e0 + threadIdx.x, ib = ia + kThreads;
   const bool va = ia < e1, vb = ib < e1;
@@ -207,17 +221,50 @@ __global__ void __launch_bounds__(kThreads)
     qb_c[k] = __ldg(pts + size_t(qb) * D + k);
     q2[k] = make_float2(qa_c[k], qb_c[k]);
   }
-  float offA = 0.f, offB = 0.f;
-  if (has_boxes) {
-    offA = scale * box_dist<FAM>(qa_c, tlo + h * D, thi + h * D, D);
-    offB = scale * box_dist<FAM>(qb_c, tlo + h * D, thi + h * D, D);
-  }
+  // log2 of a lower bound of each entry's node mass (half the previous
+  // level's exact sum; the root holds the query itself, so >= 1 there)
+  const float lbA = prune ? (elm ? elm[va ? ia : e0] : 0.f) - 1.f : 0.f;
+  const float lbB = prune ? (elm ? elm[vb ? ib : e0] : 0.f) - 1.f : 0.f;
+  if (threadIdx.x == 0) s_done = 0;
+
+  const uint32_t nsub = 1u << (sdepth - cdepth);
+  const uint32_t ls = level + 1 + sdepth;
+  const uint64_t hbase = ((1ull << ls) - 1) +
+                         ((uint64_t(2 * g + side) << sdepth) + uint64_t(kk) * nsub);
+  const uint32_t nvalid_warp =
+      __popc(__ballot_sync(0xffffffffu, va)) + __popc(__ballot_sync(0xffffffffu, vb));
+  unsigned long long done = 0;
   double accA = 0.0, accB = 0.0;
-  lowd_range_sum<D, FAM>(pts, sm, q2, make_float2(offA, offB), scale, cf, cl,
-                         accA, accB);
+  for (uint32_t sc = 0; sc < nsub; ++sc) {
+    const uint64_t h = hbase + sc;
+    const uint32_t cf = tfirst[h], cl = tlast[h];
+    float offA = 0.f, offB = 0.f;
+    if (has_boxes) {
+      offA = scale * box_dist<FAM>(qa_c, tlo + h * D, thi + h * D, D);
+      offB = scale * box_dist<FAM>(qb_c, tlo + h * D, thi + h * D, D);
+    }
+    bool skip = false;
+    if (prune) {
+      const float lim = __log2f(float(cl - cf)) + kPruneBits;
+      skip = (!va || offA > lim - lbA) && (!vb || offB > lim - lbB);
+    }
+    if (__syncthreads_and(skip)) continue;
+    const bool wskip = __all_sync(0xffffffffu, skip);
+    double sA = 0.0, sB = 0.0;
+    lowd_range_sum<D, FAM>(pts, sm, q2, make_float2(offA, offB), scale, cf, cl, sA, sB,
+                           wskip);
+    accA += rescale(sA, offA);
+    accB += rescale(sB, offB);
+    if (!wskip) done += uint64_t(cl - cf) * nvalid_warp;
+  }
   const uint32_t stride = 2u * K, col = side * K + kk;
-  if (va) partials[size_t(ia) * stride + col] = rescale(accA, offA);
-  if (vb) partials[size_t(ib) * stride + col] = rescale(accB, offB);
+  if (va) partials[size_t(ia) * stride + col] = accA;
+  if (vb) partials[size_t(ib) * stride + col] = accB;
+  if (performed) {
+    if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_done, done);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_done) atomicAdd(performed, s_done);
+  }
 }
 
 // ---- low-d direct kernel (small nodes: one thread per entry) --------------
@@ -615,12 +662,14 @@ template <int D, int FAM>
 struct LowD {
   static void tiled(dim3 grid, cudaStream_t s, const float* pts,
                     const LevelView& lv, const uint32_t* blk_off,
-                    uint32_t cdepth, const TreeTable& t, float scale,
-                    double* partials) {
+                    uint32_t cdepth, uint32_t sdepth, const TreeTable& t,
+                    float scale, double* partials,
+                    unsigned long long* performed) {
     kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
-        pts, lv.eq, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
-        t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
-        t.hi.as<float>(), t.has_boxes, scale, partials);
+        pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
+        sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
+        t.hi.as<float>(), t.has_boxes, scale, lv.prune && t.has_boxes, partials,
+        performed);
   }
   static void direct(cudaStream_t s, const float* pts, const LevelView& lv,
                      const TreeTable& t, float scale, double* g1, double* g2,
@@ -700,11 +749,11 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
 
   // blocks per slot + exact evaluation count of the level
   const uint32_t G = lv.num_slots;
-  ws.blk_off.ensure(size_t(G + 2) * 4 + 64, s);
+  ws.blk_off.ensure(size_t(G + 4) * 4 + 64, s);
   uint32_t* nb = ws.blk_off.as<uint32_t>();
   unsigned long long* d_evals =
       reinterpret_cast<unsigned long long*>(nb + G + 2 + (G & 1));
-  FSGG_CUDA(cudaMemsetAsync(d_evals, 0, 8, s));
+  FSGG_CUDA(cudaMemsetAsync(d_evals, 0, 16, s));
   slot_blocks_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
       lv.goff, G, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(), be,
       direct ? nullptr : nb, d_evals);
@@ -731,6 +780,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     FSGG_CUDA(cudaMemcpyAsync(&ev, d_evals, 8, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
     stats.evals += ev;
+    stats.performed += ev;
     return;
   }
 
@@ -747,18 +797,22 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   FSGG_CUDA(cudaStreamSynchronize(s));
   ds.launches += 1;
   stats.evals += ev;
+  stats.performed += ev;
   if (total_blocks == 0) return;
 
-  // chunk depth: enough independent items to fill the GPU many times over,
-  // chunks no smaller than kChunkMin, partials bounded.
+  // sub-chunk depth (pruning / tiling granularity, ~kSubMin..2*kSubMin
+  // sources) and chunk-group depth c <= sd: enough independent items to fill
+  // the GPU many times over, partials bounded.
   const uint32_t node_min = uint32_t(uint64_t(n) >> lv.level);
   const uint32_t child_min = node_min / 2;
   const uint64_t target_items = uint64_t(ds.num_sms) * 8 * 40;
+  uint32_t sd = 0;
+  while ((child_min >> (sd + 1)) >= kSubMin && lv.level + 2 + sd <= t.depth) ++sd;
   uint32_t c = 0;
-  while ((child_min >> (c + 1)) >= kChunkMin &&
+  const uint32_t cmax = lowd ? sd : sd;  // high-d: one tile walk per group
+  while (c < cmax && (child_min >> (c + 1)) >= (lowd ? kSubMin : kChunkMin) &&
          (uint64_t(total_blocks) << (c + 1)) < target_items &&
-         (uint64_t(E) << (c + 2)) <= kMaxPartials &&
-         lv.level + 2 + c <= t.depth)
+         (uint64_t(E) << (c + 2)) <= kMaxPartials)
     ++c;
   const uint32_t K = 1u << c;
   ws.partials.ensure(size_t(E) * 2 * K * sizeof(double), s);
@@ -771,10 +825,12 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     FSGG_CUDA(cudaEventCreate(&ws.ev0));
     FSGG_CUDA(cudaEventCreate(&ws.ev1));
   }
+  unsigned long long* d_perf = d_evals + 1;
+  FSGG_CUDA(cudaMemsetAsync(d_perf, 0, 8, s));
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
   if (lowd) {
     with_lowd(ks.family, d, [&](auto op) {
-      op.tiled(grid, s, pts, lv, nb, c, t, ks.scale, partials);
+      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf);
     });
   } else {
     with_family(ks.family, [&](auto fam) {
@@ -792,11 +848,15 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
       t.last.as<uint32_t>(), g1, g2, groot);
   FSGG_LAUNCH_CHECK();
   ds.launches += 2;
-  FSGG_CUDA(cudaEventSynchronize(ws.ev1));
+  unsigned long long perf = ev;
+  if (lowd) FSGG_CUDA(cudaMemcpyAsync(&perf, d_perf, 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
   float ms = 0.f;
   FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
   stats.tiled_seconds += ms * 1e-3;
   stats.tiled_evals += ev;
+  stats.tiled_performed += perf;
+  stats.performed += perf - ev;  // stats.performed was credited with ev above
   stats.tiled_launches += 1;
 }
 

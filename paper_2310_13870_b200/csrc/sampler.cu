@@ -149,6 +149,8 @@ __device__ __forceinline__ uint32_t low(unsigned long long x) {
 // Stable placement: slot g's left children occupy [A[s]+B[s], A[e]+B[s]),
 // its right children [A[e]+B[s], A[e]+B[e]), where A/B are the exclusive
 // prefix counts of left/right children and [s, e) = goff[g], goff[g+1].
+// Each child entry also carries log2 of its node's mass (the child sum just
+// computed), the lower bound the next level's pruning is certified against.
 __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                const uint32_t* __restrict__ et,
                                const uint32_t* __restrict__ eg,
@@ -156,9 +158,12 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                const unsigned long long* __restrict__ flags,
                                const uint32_t* __restrict__ goff,
                                const unsigned long long* __restrict__ P,
+                               const double* __restrict__ g1,
+                               const double* __restrict__ g2,
                                uint32_t* __restrict__ neq,
                                uint32_t* __restrict__ net,
-                               uint32_t* __restrict__ neg) {
+                               uint32_t* __restrict__ neg,
+                               float* __restrict__ nelm) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E) return;
   const unsigned long long fl = flags[i];
@@ -170,12 +175,14 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
     neq[pos] = q;
     net[pos] = l;
     neg[pos] = 2 * g;
+    nelm[pos] = static_cast<float>(log2(g1[i]));
   }
   if (low(fl)) {
     const uint32_t pos = hiw(P[goff[g + 1]]) + low(Pi);
     neq[pos] = q;
     net[pos] = t - l;
     neg[pos] = 2 * g + 1;
+    nelm[pos] = static_cast<float>(log2(g2[i]));
   }
 }
 
@@ -235,11 +242,12 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
 
   // double-buffered entry lists, capacity = total tickets (>= entries)
   const uint64_t cap = std::max<uint64_t>(total, 1);
-  DevBuf eq[2], et[2], eg[2];
+  DevBuf eq[2], et[2], eg[2], elm[2];
   for (int b = 0; b < 2; ++b) {
     eq[b].alloc(cap * 4, s);
     et[b].alloc(cap * 4, s);
     eg[b].alloc(cap * 4, s);
+    elm[b].alloc(cap * 4, s);
   }
   DevBuf g1(cap * 8, s), g2(cap * 8, s), tl(cap * 4, s), flags((cap + 1) * 8, s),
       P((cap + 1) * 8, s);
@@ -276,6 +284,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     lv.num_entries = E;
     lv.eq = eq[cur].as<uint32_t>();
     lv.eg = eg[cur].as<uint32_t>();
+    lv.elm = level == 0 ? nullptr : elm[cur].as<float>();
+    lv.prune = req.prune;
     lv.goff = goff[cur].as<uint32_t>();
     kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
               level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr,
@@ -304,8 +314,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     scatter_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
         E, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(), eg[cur].as<uint32_t>(),
         tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur].as<uint32_t>(),
-        P.as<unsigned long long>(), eq[nxt].as<uint32_t>(), et[nxt].as<uint32_t>(),
-        eg[nxt].as<uint32_t>());
+        P.as<unsigned long long>(), g1.as<double>(), g2.as<double>(), eq[nxt].as<uint32_t>(),
+        et[nxt].as<uint32_t>(), eg[nxt].as<uint32_t>(), elm[nxt].as<float>());
     FSGG_LAUNCH_CHECK();
     if (level < t.depth) {
       goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(

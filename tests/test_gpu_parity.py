@@ -65,11 +65,12 @@ def test_per_node_sums_match_reference(golden):
     assert worst <= SUM_RTOL
 
 
-def test_sampled_triples_edge_for_edge(golden):
+@pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
+def test_sampled_triples_edge_for_edge(golden, dense):
     n = golden["points"].shape[0]
     tri, diag = F.sample_neighbors_counted(golden["ds"], golden["kernel"], np.arange(n),
                                            int(golden["rounds"]), int(golden["seed"]),
-                                           diagnostics=True)
+                                           diagnostics=True, dense_kde=dense)
     ref = golden["triples"]
     assert tri.shape == ref.shape
     diff = np.nonzero(np.any(tri != ref, axis=1))[0]
