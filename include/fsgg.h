@@ -105,6 +105,7 @@ typedef struct fsgg_report {
   uint32_t gpu_launches;      /* kernels launched by this call */
   uint64_t kernel_evals_performed;    /* evaluations actually executed */
   uint64_t kde_tiled_performed_evals; /* of which in the tiled kernel */
+  uint64_t tie_verified_entries; /* entries re-decided on fp64 sums (tie guard) */
 } fsgg_report;
 
 /* Per-edge quantities of the weighting step (sparsifier.hpp:29-38). */

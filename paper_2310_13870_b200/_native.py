@@ -47,7 +47,8 @@ class fsgg_report(C.Structure):
                 ("kde_tiled_seconds", C.c_double), ("kde_tiled_launches", C.c_uint32),
                 ("levels", C.c_uint32), ("peak_entries", C.c_uint64),
                 ("gpu_launches", C.c_uint32), ("kernel_evals_performed", C.c_uint64),
-                ("kde_tiled_performed_evals", C.c_uint64)]
+                ("kde_tiled_performed_evals", C.c_uint64),
+                ("tie_verified_entries", C.c_uint64)]
 
 
 class fsgg_edge_estimate(C.Structure):

@@ -247,6 +247,7 @@ class BuildReport:
     gpu_launches: int = 0
     kernel_evals_performed: int = 0
     kde_tiled_performed_evals: int = 0
+    tie_verified_entries: int = 0
 
     @classmethod
     def _from_c(cls, r):
@@ -314,8 +315,12 @@ def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig
     est_arr = None
     if estimates:
         m = int(g.num_edges) if g.num_edges else graph.num_edges()
-        raw = C.string_at(est, m * C.sizeof(N.fsgg_edge_estimate)) if m else b""
-        est_arr = np.frombuffer(raw, dtype=EDGE_ESTIMATE_DTYPE).copy()
+        nbytes = m * C.sizeof(N.fsgg_edge_estimate)
+        if m:
+            raw = np.ctypeslib.as_array(C.cast(est, C.POINTER(C.c_uint8)), shape=(nbytes,))
+            est_arr = raw.view(EDGE_ESTIMATE_DTYPE).copy()
+        else:
+            est_arr = np.zeros(0, EDGE_ESTIMATE_DTYPE)
         lib.fsgg_free(C.cast(est, C.c_void_p))
     if report or estimates:
         return graph, BuildReport._from_c(rep), est_arr

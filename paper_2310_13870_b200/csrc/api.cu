@@ -164,6 +164,7 @@ struct BuildOut {
   fsgg::KdeStats kde;
   uint32_t levels = 0;
   uint64_t peak = 0;
+  uint64_t tie_verified = 0;
 };
 
 // Descent over the configured query shard; fills res (and optionally keys).
@@ -197,6 +198,7 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   bo.kde = res.kde;
   bo.levels = static_cast<uint32_t>(res.entries_per_level.size());
   bo.peak = res.peak_entries;
+  bo.tie_verified = res.tie_verified;
 }
 
 void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
@@ -220,6 +222,7 @@ void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
   r->kernel_evals = bo.kde.evals;
   r->kernel_evals_performed = bo.kde.performed;
   r->kde_tiled_performed_evals = bo.kde.tiled_performed;
+  r->tie_verified_entries = bo.tie_verified;
   r->kde_tiled_evals = bo.kde.tiled_evals;
   r->kde_tiled_seconds = bo.kde.tiled_seconds;
   r->kde_tiled_launches = bo.kde.tiled_launches;

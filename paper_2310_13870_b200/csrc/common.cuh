@@ -68,6 +68,34 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+#ifdef __CUDACC__
+// fp64 kernel value, same operation order as proj/include/fsg/kernel.hpp:28-53.
+__device__ __forceinline__ double kernel_f64(int family, double sigma,
+                                             const float* x, const float* y,
+                                             uint32_t d) {
+  double s = 0.0;
+  if (family == 2) {
+    for (uint32_t k = 0; k < d; ++k)
+      s = __dadd_rn(s, fabs(__dsub_rn(double(x[k]), double(y[k]))));
+    return exp(-s / sigma);
+  }
+  // Products rounded and added in order; the last coordinate of an odd d is
+  // fused, as the reference binary's vectorised loop does (see
+  // oracle/fsg_oracle.c: sq_dist_ref).
+  const uint32_t even = d & ~1u;
+  for (uint32_t k = 0; k < even; ++k) {
+    const double t = __dsub_rn(double(x[k]), double(y[k]));
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  if (d & 1u) {
+    const double t = __dsub_rn(double(x[d - 1]), double(y[d - 1]));
+    s = __fma_rn(t, t, s);
+  }
+  if (family == 1) return exp(-sqrt(s) / sigma);
+  return exp(-s / __dmul_rn(sigma, sigma));
+}
+#endif
+
 inline uint32_t ceil_div_u32(uint64_t a, uint64_t b) {
   return static_cast<uint32_t>((a + b - 1) / b);
 }

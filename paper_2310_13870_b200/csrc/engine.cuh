@@ -149,6 +149,7 @@ struct SampleRequest {
   uint64_t seed = 1;
   int rng_mode = 0;
   int prune = 1;
+  bool verify_ties = true;  // reference RNG mode: re-decide near-ties on fp64 sums
   bool want_root_sums = false;
 };
 
@@ -161,6 +162,7 @@ struct SampleResult {
   DevBuf leaf_src, leaf_cnt;  // u32 total_tickets
   DevBuf groot;    // f64 nq: g_full of each query (root sum), if requested
   uint64_t degenerate_draws = 0;
+  uint64_t tie_verified = 0;  // entries re-decided on fp64 sums
   std::vector<uint64_t> entries_per_level, tickets_per_level;
   uint64_t peak_entries = 0;
   KdeStats kde;

@@ -25,6 +25,10 @@ namespace fsgg {
 
 namespace {
 
+// Relative half-width (of min(p, 1-p)) of the tie guard: 5x the worst p
+// error implied by the fp32 child sums' measured relative error (~1e-5).
+constexpr double kTieMargin = 1e-4;
+
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
                                  uint32_t* __restrict__ eq,
@@ -69,7 +73,10 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
                              uint32_t* __restrict__ leaf_cnt,
                              uint32_t* __restrict__ tl,
                              unsigned long long* __restrict__ flags,
-                             unsigned long long* __restrict__ counters) {
+                             unsigned long long* __restrict__ counters,
+                             const float* __restrict__ elm,
+                             uint32_t* __restrict__ vlist,
+                             uint32_t* __restrict__ vcount) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long tsum = 0, degen = 0;
   if (i < E) {
@@ -89,9 +96,13 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
     } else {
       const double a = g1[i], b = g2[i];
       double p;
+      bool verify = false;
       if (a <= kSumFloor && b <= kSumFloor) {  // :207-209
         p = 0.5;
-        degen = t;
+        if (vlist)
+          verify = true;  // degenerate by fp32 sums: decided on exact sums
+        else
+          degen = t;
       } else {
         p = a / (a + b);  // :211
       }
@@ -102,14 +113,33 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
         left = t;
       } else {
         // u_c = (x_c >> 11) * 2^-53 < p  <=>  (x_c >> 11) < ceil(p * 2^53)
-        const uint64_t thr = static_cast<uint64_t>(ceil(p * 9007199254740992.0));
+        const double P = p * 9007199254740992.0;
+        const uint64_t thr = static_cast<uint64_t>(ceil(P));
         left = 0;
         if (rng_mode == 0) {
           // RngStream::keyed(seed, kRouteTag, (first<<32)|last, query)
           const uint64_t key =
               route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
-          for (uint32_t c = 0; c < t; ++c)
-            left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+          if (vlist) {
+            // Tie guard: a draw within the fp32 sums' error bound of p is
+            // re-decided on fp64 sums (exact_sums_kernel), which makes the
+            // output match the reference's exact backend edge for edge.
+            const float deficit = elm ? fmaxf(0.f, -elm[i]) : 0.f;
+            const double rel = kTieMargin * (1.0 + deficit / 32.0);
+            const double M = rel * fmin(p, 1.0 - p) * 9007199254740992.0 + 1.0;
+            const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
+            const uint64_t hi = static_cast<uint64_t>(P + M);
+            bool near = false;
+            for (uint32_t c = 0; c < t; ++c) {
+              const uint64_t m = splitmix64(key + c) >> 11;
+              left += m < thr ? 1u : 0u;
+              near |= (m >= lo) & (m <= hi);
+            }
+            verify |= near;
+          } else {
+            for (uint32_t c = 0; c < t; ++c)
+              left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+          }
         } else {
           const uint2 k = make_uint2(uint32_t(seed), uint32_t(seed >> 32));
           for (uint32_t c = 0; c < t; c += 2) {
@@ -124,6 +154,7 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
       tl[i] = left;
       fl = (static_cast<unsigned long long>(left > 0) << 32) |
            static_cast<unsigned long long>(left < t);
+      if (verify) vlist[atomicAdd(vcount, 1u)] = i;
     }
     flags[i] = fl;
   } else if (i == E) {
@@ -136,6 +167,93 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
   if ((threadIdx.x & 31) == 0) {
     if (tsum) atomicAdd(counters + 0, tsum);
     if (degen) atomicAdd(counters + 1, degen);
+  }
+}
+
+// fp64 child sums for the entries the tie guard flagged: one CTA per entry,
+// every term in fp64 with the reference's operation order
+// (kernel_f64), fixed-order block reduction. Grid-strided over the device
+// count, so no host synchronisation is needed.
+__global__ void __launch_bounds__(256)
+    exact_sums_kernel(const float* __restrict__ pts, uint32_t d, int family,
+                      double sigma, uint32_t level, const uint32_t* __restrict__ eq,
+                      const uint32_t* __restrict__ eg,
+                      const uint32_t* __restrict__ tfirst,
+                      const uint32_t* __restrict__ tlast,
+                      const uint32_t* __restrict__ vlist,
+                      const uint32_t* __restrict__ vcount, double* __restrict__ g1,
+                      double* __restrict__ g2) {
+  __shared__ double red[2][256];
+  const uint32_t cnt = *vcount;
+  for (uint32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+    const uint32_t i = vlist[b];
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
+    const float* xq = pts + size_t(eq[i]) * d;
+    double s0 = 0.0, s1 = 0.0;
+    for (uint32_t j = f + threadIdx.x; j < mid; j += blockDim.x)
+      s0 += kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
+    for (uint32_t j = mid + threadIdx.x; j < l; j += blockDim.x)
+      s1 += kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    __syncthreads();
+    for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+        red[0][threadIdx.x] += red[0][threadIdx.x + w];
+        red[1][threadIdx.x] += red[1][threadIdx.x + w];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      g1[i] = fmax(red[0][0], kSumFloor);
+      g2[i] = fmax(red[1][0], kSumFloor);
+    }
+    __syncthreads();
+  }
+}
+
+// Re-decide the flagged entries on the fp64 sums (reference stream).
+__global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
+                               const uint32_t* __restrict__ et,
+                               const uint32_t* __restrict__ eg,
+                               const double* __restrict__ g1,
+                               const double* __restrict__ g2,
+                               const uint32_t* __restrict__ tfirst,
+                               const uint32_t* __restrict__ tlast, uint64_t key_prefix,
+                               const uint32_t* __restrict__ vlist,
+                               const uint32_t* __restrict__ vcount,
+                               uint32_t* __restrict__ tl,
+                               unsigned long long* __restrict__ flags,
+                               unsigned long long* __restrict__ counters) {
+  const uint32_t cnt = *vcount;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < cnt;
+       b += gridDim.x * blockDim.x) {
+    const uint32_t i = vlist[b];
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h], q = eq[i], t = et[i];
+    const double a = g1[i], bb = g2[i];
+    double p;
+    if (a <= kSumFloor && bb <= kSumFloor) {
+      p = 0.5;
+      atomicAdd(counters + 1, static_cast<unsigned long long>(t));
+    } else {
+      p = a / (a + bb);
+    }
+    uint32_t left;
+    if (p <= 0.0) {
+      left = 0;
+    } else if (p >= 1.0) {
+      left = t;
+    } else {
+      const uint64_t thr = static_cast<uint64_t>(ceil(p * 9007199254740992.0));
+      const uint64_t key = route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
+      left = 0;
+      for (uint32_t c = 0; c < t; ++c) left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+    }
+    tl[i] = left;
+    flags[i] = (static_cast<unsigned long long>(left > 0) << 32) |
+               static_cast<unsigned long long>(left < t);
   }
 }
 
@@ -256,6 +374,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   goff[0].alloc((max_slots + 1) * 4, s);
   goff[1].alloc((max_slots + 1) * 4, s);
   DevBuf counters(64, s), cub_tmp;
+  const bool verify = req.rng_mode == 0 && req.verify_ties;
+  DevBuf vlist(verify ? cap * 4 : 4, s);
   KdeWorkspace ws;
 
   init_rows_kernel<<<ceil_div_u32(std::max<uint32_t>(nq, 1), 256), 256, 0, s>>>(
@@ -272,6 +392,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   out.entries_per_level.clear();
   out.tickets_per_level.clear();
   out.degenerate_draws = 0;
+  out.tie_verified = 0;
   out.peak_entries = 0;
   for (uint32_t level = 0; E > 0; ++level) {
     if (level > t.depth) throw NumericError("descent exceeded tree depth");
@@ -291,7 +412,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
               level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr,
               ws, out.kde);
 
-    FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
+    FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
+    uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
     route_kernel<<<ceil_div_u32(uint64_t(E) + 1, 256), 256, 0, s>>>(
         E, level, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(),
         eg[cur].as<uint32_t>(), g1.as<double>(), g2.as<double>(),
@@ -299,8 +421,24 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         req.seed, qrow.as<uint32_t>(), out.row_off.as<uint64_t>(),
         out.row_cnt.as<uint32_t>(), out.leaf_src.as<uint32_t>(),
         out.leaf_cnt.as<uint32_t>(), tl.as<uint32_t>(),
-        flags.as<unsigned long long>(), counters.as<unsigned long long>());
+        flags.as<unsigned long long>(), counters.as<unsigned long long>(),
+        level == 0 ? nullptr : elm[cur].as<float>(),
+        verify ? vlist.as<uint32_t>() : nullptr, vcount);
     FSGG_LAUNCH_CHECK();
+    if (verify) {
+      exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
+          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, level, eq[cur].as<uint32_t>(),
+          eg[cur].as<uint32_t>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+          vlist.as<uint32_t>(), vcount, g1.as<double>(), g2.as<double>());
+      FSGG_LAUNCH_CHECK();
+      reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
+          level, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(), eg[cur].as<uint32_t>(),
+          g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+          prefix, vlist.as<uint32_t>(), vcount, tl.as<uint32_t>(),
+          flags.as<unsigned long long>(), counters.as<unsigned long long>());
+      FSGG_LAUNCH_CHECK();
+      ds.launches += 2;
+    }
 
     size_t tmp_bytes = 0;
     FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
@@ -326,14 +464,15 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     }
     ds.launches += 3;
 
-    unsigned long long host[3];
-    FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 16, cudaMemcpyDeviceToHost, s));
-    FSGG_CUDA(cudaMemcpyAsync(host + 2, P.as<unsigned long long>() + E, 8,
+    unsigned long long host[4];
+    FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 24, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaMemcpyAsync(host + 3, P.as<unsigned long long>() + E, 8,
                               cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
     out.tickets_per_level.push_back(host[0]);
     out.degenerate_draws += host[1];
-    const uint64_t next = uint64_t(host[2] >> 32) + uint64_t(host[2] & 0xffffffffull);
+    out.tie_verified += host[2] & 0xffffffffull;
+    const uint64_t next = uint64_t(host[3] >> 32) + uint64_t(host[3] & 0xffffffffull);
     if (next > cap) throw NumericError("entry list overflow");
     if (next > 0 && level >= t.depth)
       throw NumericError("tickets remain below the deepest level");

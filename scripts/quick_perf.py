@@ -19,4 +19,4 @@ for name in sys.argv[1:] or ["C2"]:
               f"({rep.kde_tiled_performed_evals/max(rep.kde_tiled_seconds,1e-9)/1e12:.3f} Tperf/s) "
               f"sample_s={rep.sampling_seconds:.3f} graph_s={rep.weighting_seconds:.3f} "
               f"tree_s={rep.estimator_build_seconds:.3f} levels={rep.levels} peak={rep.peak_entries} "
-              f"launches={rep.gpu_launches}", flush=True)
+              f"launches={rep.gpu_launches} ties={rep.tie_verified_entries}", flush=True)

@@ -107,7 +107,8 @@ def test_c2_ticket_conservation():
     ds = F.Dataset(w.points)
     tri, diag = F.sample_neighbors_counted(ds, F.Kernel(F.KernelFamily.gaussian, w.sigma),
                                            np.arange(w.n), w.rounds, 1, diagnostics=True)
-    assert all(t == w.n * w.rounds for t in diag.tickets_per_level)
+    assert all(t == w.n * w.rounds for t in diag.tickets_per_level), diag.tickets_per_level
     assert int(tri[:, 2].astype(np.int64).sum()) == w.n * w.rounds
-    assert diag.entries_per_level[0] == w.n and len(diag.entries_per_level) == 18
+    assert diag.entries_per_level[0] == w.n and len(diag.entries_per_level) == 18, \
+        diag.entries_per_level
     assert diag.degenerate_draws == 0
