@@ -18,6 +18,9 @@
 #include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "engine.cuh"
 
@@ -394,9 +397,18 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   out.degenerate_draws = 0;
   out.tie_verified = 0;
   out.peak_entries = 0;
+  // FSGG_TRACE=1: per-level phase times (CUDA events on the launch stream)
+  // and host wall time to stderr.
+  const bool trace = std::getenv("FSGG_TRACE") != nullptr;
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (trace)
+    for (auto& e : tev) FSGG_CUDA(cudaEventCreate(&e));
   for (uint32_t level = 0; E > 0; ++level) {
     if (level > t.depth) throw NumericError("descent exceeded tree depth");
     const uint32_t G = 1u << level;
+    const auto wall0 = std::chrono::steady_clock::now();
+    const KdeStats kde0 = out.kde;
+    if (trace) FSGG_CUDA(cudaEventRecord(tev[0], s));
     out.entries_per_level.push_back(E);
     out.peak_entries = std::max<uint64_t>(out.peak_entries, E);
     LevelView lv;
@@ -412,6 +424,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
               level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr,
               ws, out.kde);
 
+    if (trace) FSGG_CUDA(cudaEventRecord(tev[1], s));
     FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
     uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
     route_kernel<<<ceil_div_u32(uint64_t(E) + 1, 256), 256, 0, s>>>(
@@ -440,6 +453,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       ds.launches += 2;
     }
 
+    if (trace) FSGG_CUDA(cudaEventRecord(tev[2], s));
     size_t tmp_bytes = 0;
     FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
         nullptr, tmp_bytes, flags.as<unsigned long long>(),
@@ -464,6 +478,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     }
     ds.launches += 3;
 
+    if (trace) FSGG_CUDA(cudaEventRecord(tev[3], s));
     unsigned long long host[4];
     FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 24, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaMemcpyAsync(host + 3, P.as<unsigned long long>() + E, 8,
@@ -476,9 +491,24 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     if (next > cap) throw NumericError("entry list overflow");
     if (next > 0 && level >= t.depth)
       throw NumericError("tickets remain below the deepest level");
+    if (trace) {
+      float ms[3];
+      for (int k = 0; k < 3; ++k) FSGG_CUDA(cudaEventElapsedTime(&ms[k], tev[k], tev[k + 1]));
+      const double wall = std::chrono::duration<double, std::milli>(
+                              std::chrono::steady_clock::now() - wall0).count();
+      const uint32_t smax = uint32_t((uint64_t(ds.n) + (1ull << level) - 1) >> level);
+      std::fprintf(stderr,
+                   "fsgg level %2u: entries=%10u node<=%8u evals=%.3e performed=%.3e "
+                   "kde=%8.3fms route=%7.3fms scan+scatter=%7.3fms wall=%8.3fms ties=%llu\n",
+                   level, E, smax, double(out.kde.evals - kde0.evals),
+                   double(out.kde.performed - kde0.performed), ms[0], ms[1], ms[2], wall,
+                   (unsigned long long)(host[2] & 0xffffffffull));
+    }
     E = static_cast<uint32_t>(next);
     cur = nxt;
   }
+  if (trace)
+    for (auto& e : tev) cudaEventDestroy(e);
 }
 
 void sampled_triples_to_host(Dataset& ds, SampleResult& res,

@@ -107,7 +107,10 @@ def test_c2_ticket_conservation():
     ds = F.Dataset(w.points)
     tri, diag = F.sample_neighbors_counted(ds, F.Kernel(F.KernelFamily.gaussian, w.sigma),
                                            np.arange(w.n), w.rounds, 1, diagnostics=True)
-    assert all(t == w.n * w.rounds for t in diag.tickets_per_level), diag.tickets_per_level
+    # n is not a power of two: leaves sit at depths 16 and 17, so only the
+    # last level holds fewer tickets (those not yet emitted at depth 16)
+    assert all(t == w.n * w.rounds for t in diag.tickets_per_level[:-1]), diag.tickets_per_level
+    assert 0 < diag.tickets_per_level[-1] < w.n * w.rounds
     assert int(tri[:, 2].astype(np.int64).sum()) == w.n * w.rounds
     assert diag.entries_per_level[0] == w.n and len(diag.entries_per_level) == 18, \
         diag.entries_per_level
