@@ -18,20 +18,21 @@
 
 struct fsgg_dataset {
   fsgg::Dataset ds;
-  // Results kept alive for the device-pointer APIs.
+  // Results kept alive for the device-pointer APIs; reused (grow-only)
+  // across calls so repeated builds never go back to the allocator.
   std::unique_ptr<fsgg::GraphResult> graph;
+  std::unique_ptr<fsgg::SampleResult> sample;
   std::unique_ptr<fsgg::SampleResult> shard;
+  fsgg::DevBuf keys;
   fsgg::DevBuf shard_keys;
   uint64_t shard_npairs = 0;
   ~fsgg_dataset() {
     graph.reset();
+    sample.reset();
     shard.reset();
+    keys.release();
     shard_keys.release();
-    ds.tree.first.release();
-    ds.tree.last.release();
-    ds.tree.lo.release();
-    ds.tree.hi.release();
-    ds.pts.release();
+    ds.release_all();
     if (ds.stream) {
       cudaStreamSynchronize(ds.stream);
       cudaStreamDestroy(ds.stream);
@@ -243,15 +244,15 @@ void build_device(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config*
   BuildOut bo;
   bo.L = rounds_for(cfg, ds.n);
   double t0 = now();
-  fsgg::SampleResult res;
-  fsgg::DevBuf keys;
+  if (!h->sample) h->sample = std::make_unique<fsgg::SampleResult>();
+  fsgg::SampleResult& res = *h->sample;
   uint64_t npairs = 0;
-  run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, keys, &npairs, bo);
+  run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, h->keys, &npairs, bo);
   double t1 = now();
   const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
-  h->graph = std::make_unique<fsgg::GraphResult>();
+  if (!h->graph) h->graph = std::make_unique<fsgg::GraphResult>();
   fsgg::finish_graph(ds, ks, bo.L, res.groot.as<double>(),
-                     keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph);
+                     h->keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph);
   double t2 = now();
   bo.t_graph += t2 - t1;
   if (report) finish_report(report, ds, bo, h->graph.get(), t2 - t0 + bo.t_tree * 0);
@@ -467,7 +468,11 @@ int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
     req.rng_mode = rng_mode;
     req.prune = dense_kde ? 0 : 1;
     std::vector<uint32_t> host;
-    fsgg::SampleResult res;
+    if (!h->sample) h->sample = std::make_unique<fsgg::SampleResult>();
+    fsgg::SampleResult& res = *h->sample;
+    res.entries_per_level.clear();
+    res.tickets_per_level.clear();
+    res.degenerate_draws = 0;
     if (!req.queries.empty()) {
       const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
       fsgg::sample_counted(ds, ks, req, res);
@@ -528,13 +533,14 @@ int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_con
     BuildOut bo;
     bo.L = rounds_for(cfg, ds.n);
     double t0 = now();
-    h->shard = std::make_unique<fsgg::SampleResult>();
+    if (!h->shard) h->shard = std::make_unique<fsgg::SampleResult>();
     uint64_t npairs = 0;
     if (qe > qb) {
       run_descent(h, kernel, cfg, bo.L, qb, qe, *h->shard, h->shard_keys, &npairs, bo);
     } else {
-      h->shard->groot.alloc(8, ds.stream);
-      h->shard_keys.alloc(8, ds.stream);
+      h->shard->groot.ensure(8, ds.stream);
+      h->shard_keys.ensure(8, ds.stream);
+      h->shard->nq = 0;
     }
     std::memset(out, 0, sizeof(*out));
     out->query_begin = qb;
@@ -578,7 +584,7 @@ int fsgg_finish_graph(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t round
     if (rounds == 0) throw fsgg::ConfigError("rounds must be positive");
     double t0 = now();
     const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
-    h->graph = std::make_unique<fsgg::GraphResult>();
+    if (!h->graph) h->graph = std::make_unique<fsgg::GraphResult>();
     fsgg::finish_graph(h->ds, ks, rounds, g_full_device, pairs_device, num_pairs, false,
                        false, *h->graph);
     to_device_graph(h, out);

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -85,6 +87,8 @@ struct TreeTable {
 };
 constexpr uint32_t kBoxMaxDim = 16;
 
+struct KdeWorkspace;
+
 struct Dataset {
   int device = 0;
   uint32_t n = 0, d = 0;
@@ -93,9 +97,18 @@ struct Dataset {
   DevBuf pts;  // f32 n*d
   TreeTable tree;
   bool tree_valid = false;
-  // Reusable work buffers owned by the handle.
-  DevBuf scratch_graph[12];
   uint32_t launches = 0;  // kernel launches issued (reset per API call)
+  // Grow-only work buffers owned by the handle: repeated builds on one
+  // dataset never go back to the allocator (a fresh multi-GB cudaMallocAsync
+  // costs hundreds of ms when the pool has to map new memory).
+  std::unordered_map<std::string, DevBuf> arena;
+  DevBuf& buf(const std::string& name, size_t bytes) {
+    DevBuf& b = arena[name];
+    b.ensure(bytes ? bytes : 8, stream);
+    return b;
+  }
+  std::unique_ptr<KdeWorkspace> kde_ws;
+  void release_all();
 };
 
 // ---- tree.cu --------------------------------------------------------------
@@ -130,12 +143,25 @@ struct KdeWorkspace {
   ~KdeWorkspace();
 };
 
+inline void Dataset::release_all() {
+  kde_ws.reset();
+  arena.clear();
+  tree.first.release();
+  tree.last.release();
+  tree.lo.release();
+  tree.hi.release();
+  pts.release();
+}
+
 // Child sums for every entry of the level: g1 = sum over [first, mid),
 // g2 = sum over [mid, last), floored at 1e-300 (kde.cpp:68). When groot is
 // non-null, also writes the unfloored root sum g1 + g2 (level 0 only).
+// Tiled levels keep per-entry partial sums over the node's descendants
+// *row_depth levels down in ws.partials (row stride 2^*row_depth), aiming
+// for serve_levels >= 1; *row_depth = 0 when no partial rows were kept.
 void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                double* g1, double* g2, double* groot, KdeWorkspace& ws,
-               KdeStats& stats);
+               KdeStats& stats, uint32_t serve_levels, uint32_t* row_depth);
 
 // KdeEstimator::eval seam: arbitrary range, arbitrary targets (device).
 void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,

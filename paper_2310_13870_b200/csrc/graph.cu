@@ -182,7 +182,9 @@ uint64_t sort_unique_compact(Dataset& ds, DevBuf& keys, uint64_t m,
                              uint32_t bits) {
   cudaStream_t s = ds.stream;
   if (m == 0) return 0;
-  DevBuf alt(m * 8, s), tmp, cnt(16, s);
+  DevBuf& alt = ds.buf("g.alt", m * 8);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  DevBuf& cnt = ds.buf("g.cnt", 16);
   cub::DoubleBuffer<unsigned long long> db(keys.as<unsigned long long>(),
                                            alt.as<unsigned long long>());
   cub_call(tmp, s, [&](void* t, size_t& b) {
@@ -214,8 +216,8 @@ uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
   cudaStream_t s = ds.stream;
   const uint64_t cap = res.total_tickets;
   const uint32_t bits = index_bits(ds.n);
-  keys.alloc(std::max<uint64_t>(cap, 1) * 8, s);
-  DevBuf counters(16, s);
+  keys.ensure(std::max<uint64_t>(cap, 1) * 8, s);
+  DevBuf& counters = ds.buf("g.counters", 16);
   FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
   rows_to_keys_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(
       res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(),
@@ -250,7 +252,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   out.n = n;
 
   // 1. canonical sorted unique public keys
-  DevBuf keys(std::max<uint64_t>(nkeys, 1) * 8, s);
+  DevBuf& keys = ds.buf("g.keys", std::max<uint64_t>(nkeys, 1) * 8);
   uint64_t m = nkeys;
   if (keys_sorted_unique) {
     if (m)
@@ -271,10 +273,11 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   }
 
   // 2. drop underflowing pairs (k_ij < 1e-300)
-  DevBuf tmp, cnt(16, s);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  DevBuf& cnt = ds.buf("g.cnt", 16);
   out.underflow = 0;
   if (m) {
-    DevBuf keep(m, s);
+    DevBuf& keep = ds.buf("g.keep", m);
     FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
     underflow_flags_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
         keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
@@ -285,7 +288,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
     FSGG_CUDA(cudaMemcpyAsync(&dropped, cnt.as<void>(), 8, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
     if (dropped) {
-      DevBuf kept(m * 8, s);
+      DevBuf& kept = ds.buf("g.kept", m * 8);
       cub_call(tmp, s, [&](void* t, size_t& b) {
         return cub::DeviceSelect::Flagged(t, b, keys.as<unsigned long long>(),
                                           keep.as<unsigned char>(),
@@ -304,10 +307,10 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   // 3. weights (+ estimates)
   out.m = m;
   const uint64_t mm = std::max<uint64_t>(m, 1);
-  out.u.alloc(mm * 4, s);
-  out.v.alloc(mm * 4, s);
-  out.w.alloc(mm * 8, s);
-  if (want_estimates) out.est.alloc(mm * sizeof(EdgeEstimateDev), s);
+  out.u.ensure(mm * 4, s);
+  out.v.ensure(mm * 4, s);
+  out.w.ensure(mm * 8, s);
+  if (want_estimates) out.est.ensure(mm * sizeof(EdgeEstimateDev), s);
   if (m) {
     weights_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
         keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
@@ -318,10 +321,14 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   }
 
   // 4. upper CSR, transposed CSR, degrees, total weight
-  out.row_ptr.alloc(size_t(n + 1) * 8, s);
-  out.degrees.alloc(size_t(n) * 8, s);
-  DevBuf rpt(size_t(n + 1) * 8, s), tkeys(mm * 8, s), tkeys2(mm * 8, s),
-      wt(mm * 8, s), wt2(mm * 8, s), trows(mm * 4, s);
+  out.row_ptr.ensure(size_t(n + 1) * 8, s);
+  out.degrees.ensure(size_t(n) * 8, s);
+  DevBuf& rpt = ds.buf("g.rpt", size_t(n + 1) * 8);
+  DevBuf& tkeys = ds.buf("g.tkeys", mm * 8);
+  DevBuf& tkeys2 = ds.buf("g.tkeys2", mm * 8);
+  DevBuf& wt = ds.buf("g.wt", mm * 8);
+  DevBuf& wt2 = ds.buf("g.wt2", mm * 8);
+  DevBuf& trows = ds.buf("g.trows", mm * 4);
   row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
       out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
   FSGG_LAUNCH_CHECK();

@@ -54,11 +54,11 @@ constexpr int kXBM = 64;             // entries per high-d work item
 constexpr int kXBN = 64;             // sources per high-d tile
 constexpr int kXBK = 16;             // dims per high-d k-step
 constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
-constexpr uint64_t kMaxPartials = 64ull << 20;  // doubles
+constexpr uint64_t kMaxPartials = 256ull << 20;  // doubles (2 GiB)
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
 constexpr float kPruneBits = 80.f;   // sub-chunk bound below 2^-80 of the node mass
-constexpr uint32_t kSubMin = 1024;   // smallest sub-chunk (pruning granularity)
+constexpr uint32_t kSubMin = 512;    // smallest sub-chunk (pruning granularity)
 
 template <int D>
 struct LowDTile {
@@ -734,8 +734,9 @@ uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
 
 void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                double* g1, double* g2, double* groot, KdeWorkspace& ws,
-               KdeStats& stats) {
+               KdeStats& stats, uint32_t serve_levels, uint32_t* row_depth) {
   const uint32_t E = lv.num_entries;
+  if (row_depth) *row_depth = 0;
   if (E == 0) return;
   const uint32_t n = ds.n, d = ds.d;
   const uint32_t s_max = uint32_t((uint64_t(n) + (1ull << lv.level) - 1) >> lv.level);
@@ -808,12 +809,16 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const uint64_t target_items = uint64_t(ds.num_sms) * 8 * 40;
   uint32_t sd = 0;
   while ((child_min >> (sd + 1)) >= kSubMin && lv.level + 2 + sd <= t.depth) ++sd;
+  // c >= serve_levels - 1 keeps per-entry partials at the granularity of
+  // the node's descendants c+1 levels down, so the next c levels' child sums
+  // are range sums of this row (lookup_sums_kernel, sampler.cu) instead of
+  // new kernel evaluations.
   uint32_t c = 0;
-  const uint32_t cmax = lowd ? sd : sd;  // high-d: one tile walk per group
-  while (c < cmax && (child_min >> (c + 1)) >= (lowd ? kSubMin : kChunkMin) &&
-         (uint64_t(total_blocks) << (c + 1)) < target_items &&
+  while (c < sd && (child_min >> (c + 1)) >= (lowd ? kSubMin : kChunkMin) &&
+         ((uint64_t(total_blocks) << (c + 1)) < target_items || c + 1 < serve_levels) &&
          (uint64_t(E) << (c + 2)) <= kMaxPartials)
     ++c;
+  if (row_depth) *row_depth = c + 1;
   const uint32_t K = 1u << c;
   ws.partials.ensure(size_t(E) * 2 * K * sizeof(double), s);
   double* partials = ws.partials.as<double>();

@@ -31,6 +31,8 @@ namespace {
 // Relative half-width (of min(p, 1-p)) of the tie guard: 5x the worst p
 // error implied by the fp32 child sums' measured relative error (~1e-5).
 constexpr double kTieMargin = 1e-4;
+// A compute level keeps partial rows deep enough to serve this many levels.
+constexpr uint32_t kServeLevels = 5;
 
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
@@ -78,6 +80,8 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
                              unsigned long long* __restrict__ flags,
                              unsigned long long* __restrict__ counters,
                              const float* __restrict__ elm,
+                             const uint32_t* __restrict__ eprow,
+                             const float* __restrict__ row_mass,
                              uint32_t* __restrict__ vlist,
                              uint32_t* __restrict__ vcount) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -127,9 +131,15 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
             // Tie guard: a draw within the fp32 sums' error bound of p is
             // re-decided on fp64 sums (exact_sums_kernel), which makes the
             // output match the reference's exact backend edge for edge.
-            const float deficit = elm ? fmaxf(0.f, -elm[i]) : 0.f;
-            const double rel = kTieMargin * (1.0 + deficit / 32.0);
-            const double M = rel * fmin(p, 1.0 - p) * 9007199254740992.0 + 1.0;
+            const float em = elm ? elm[i] : 0.f;
+            const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
+            // certified pruning at the compute level skipped < 2^-60 of the
+            // ancestor row's mass: an absolute error on p of at most this
+            const double pruned =
+                row_mass ? exp2(double(row_mass[eprow ? eprow[i] : i]) - 58.0 - double(em))
+                         : 0.0;
+            const double M =
+                (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
             const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
             const uint64_t hi = static_cast<uint64_t>(P + M);
             bool near = false;
@@ -260,6 +270,42 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
   }
 }
 
+// Child sums from the partial row of the entry's ancestor at the last
+// compute level (row_level = level - j): that row holds the ancestor's
+// descendants 2^rd wide; this entry's node is its descendant idx at depth j,
+// whose children own `span` consecutive buckets each. Sums in fixed order.
+__global__ void lookup_sums_kernel(uint32_t E, uint32_t level, uint32_t j, uint32_t rd,
+                                   const uint32_t* __restrict__ eg,
+                                   const uint32_t* __restrict__ eprow,
+                                   const double* __restrict__ rows,
+                                   const uint32_t* __restrict__ tfirst,
+                                   const uint32_t* __restrict__ tlast,
+                                   double* __restrict__ g1, double* __restrict__ g2,
+                                   unsigned long long* __restrict__ evals) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long ev = 0;
+  if (i < E) {
+    const uint32_t g = eg[i];
+    const uint64_t h = ((1ull << level) - 1) + g;
+    const uint32_t size = tlast[h] - tfirst[h];
+    if (size < 2) {
+      g1[i] = g2[i] = 0.0;
+    } else {
+      const uint32_t idx = g & ((1u << j) - 1u);
+      const uint32_t span = 1u << (rd - j - 1);
+      const double* row = rows + (size_t(eprow[i]) << rd) + size_t(2 * idx) * span;
+      double a = 0.0, b = 0.0;
+      for (uint32_t k = 0; k < span; ++k) a += row[k];
+      for (uint32_t k = 0; k < span; ++k) b += row[span + k];
+      g1[i] = fmax(a, kSumFloor);
+      g2[i] = fmax(b, kSumFloor);
+      ev = size;
+    }
+  }
+  for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+}
+
 __device__ __forceinline__ uint32_t hiw(unsigned long long x) {
   return uint32_t(x >> 32);
 }
@@ -284,19 +330,23 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                uint32_t* __restrict__ neq,
                                uint32_t* __restrict__ net,
                                uint32_t* __restrict__ neg,
-                               float* __restrict__ nelm) {
+                               float* __restrict__ nelm,
+                               const uint32_t* __restrict__ eprow,
+                               uint32_t* __restrict__ neprow, int self_rows) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E) return;
   const unsigned long long fl = flags[i];
   if (!fl) return;
   const uint32_t g = eg[i], q = eq[i], t = et[i], l = tl[i];
   const unsigned long long Pi = P[i];
+  const uint32_t prow = self_rows ? i : (eprow ? eprow[i] : 0u);
   if (hiw(fl)) {
     const uint32_t pos = hiw(Pi) + low(P[goff[g]]);
     neq[pos] = q;
     net[pos] = l;
     neg[pos] = 2 * g;
     nelm[pos] = static_cast<float>(log2(g1[i]));
+    neprow[pos] = prow;
   }
   if (low(fl)) {
     const uint32_t pos = hiw(P[goff[g + 1]]) + low(Pi);
@@ -304,6 +354,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
     net[pos] = t - l;
     neg[pos] = 2 * g + 1;
     nelm[pos] = static_cast<float>(log2(g2[i]));
+    neprow[pos] = prow;
   }
 }
 
@@ -346,12 +397,13 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   // host -> device: queries, tickets, leaf row offsets
   std::vector<uint64_t> row_off(nq + 1, 0);
   for (uint32_t i = 0; i < nq; ++i) row_off[i + 1] = row_off[i] + req.tickets[i];
-  out.uq.alloc(size_t(nq) * 4 + 4, s);
-  out.row_off.alloc(size_t(nq + 1) * 8, s);
-  out.row_cnt.alloc(size_t(nq) * 4 + 4, s);
-  out.leaf_src.alloc(total * 4 + 4, s);
-  out.leaf_cnt.alloc(total * 4 + 4, s);
-  DevBuf dtk(size_t(nq) * 4 + 4, s), qrow(size_t(ds.n) * 4, s);
+  out.uq.ensure(size_t(nq) * 4 + 4, s);
+  out.row_off.ensure(size_t(nq + 1) * 8, s);
+  out.row_cnt.ensure(size_t(nq) * 4 + 4, s);
+  out.leaf_src.ensure(total * 4 + 4, s);
+  out.leaf_cnt.ensure(total * 4 + 4, s);
+  DevBuf& dtk = ds.buf("s.tickets", size_t(nq) * 4 + 4);
+  DevBuf& qrow = ds.buf("s.qrow", size_t(ds.n) * 4);
   FSGG_CUDA(cudaMemcpyAsync(out.uq.as<void>(), req.queries.data(), size_t(nq) * 4,
                             cudaMemcpyHostToDevice, s));
   FSGG_CUDA(cudaMemcpyAsync(dtk.as<void>(), req.tickets.data(), size_t(nq) * 4,
@@ -359,35 +411,50 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   FSGG_CUDA(cudaMemcpyAsync(out.row_off.as<void>(), row_off.data(),
                             size_t(nq + 1) * 8, cudaMemcpyHostToDevice, s));
   FSGG_CUDA(cudaMemsetAsync(out.row_cnt.as<void>(), 0, size_t(nq) * 4 + 4, s));
-  if (req.want_root_sums) out.groot.alloc(size_t(nq) * 8 + 8, s);
+  if (req.want_root_sums) out.groot.ensure(size_t(nq) * 8 + 8, s);
 
   // double-buffered entry lists, capacity = total tickets (>= entries)
   const uint64_t cap = std::max<uint64_t>(total, 1);
-  DevBuf eq[2], et[2], eg[2], elm[2];
+  DevBuf* eq[2];
+  DevBuf* et[2];
+  DevBuf* eg[2];
+  DevBuf* elm[2];
+  DevBuf* eprow[2];
   for (int b = 0; b < 2; ++b) {
-    eq[b].alloc(cap * 4, s);
-    et[b].alloc(cap * 4, s);
-    eg[b].alloc(cap * 4, s);
-    elm[b].alloc(cap * 4, s);
+    const std::string k = std::to_string(b);
+    eq[b] = &ds.buf("s.eq" + k, cap * 4);
+    et[b] = &ds.buf("s.et" + k, cap * 4);
+    eg[b] = &ds.buf("s.eg" + k, cap * 4);
+    elm[b] = &ds.buf("s.elm" + k, cap * 4);
+    eprow[b] = &ds.buf("s.eprow" + k, cap * 4);
   }
-  DevBuf g1(cap * 8, s), g2(cap * 8, s), tl(cap * 4, s), flags((cap + 1) * 8, s),
-      P((cap + 1) * 8, s);
+  // Partial rows of the last compute level serve the following levels.
+  DevBuf& row_mass = ds.buf("s.row_mass", 8);
+  DevBuf& lookup_evals = ds.buf("s.lookup_evals", 8);
+  bool have_rows = false;
+  uint32_t row_level = 0, row_depth = 0;
+  DevBuf& g1 = ds.buf("s.g1", cap * 8);
+  DevBuf& g2 = ds.buf("s.g2", cap * 8);
+  DevBuf& tl = ds.buf("s.tl", cap * 4);
+  DevBuf& flags = ds.buf("s.flags", (cap + 1) * 8);
+  DevBuf& P = ds.buf("s.scan", (cap + 1) * 8);
   const uint64_t max_slots = 1ull << t.depth;
-  DevBuf goff[2];
-  goff[0].alloc((max_slots + 1) * 4, s);
-  goff[1].alloc((max_slots + 1) * 4, s);
-  DevBuf counters(64, s), cub_tmp;
+  DevBuf* goff[2] = {&ds.buf("s.goff0", (max_slots + 1) * 4),
+                     &ds.buf("s.goff1", (max_slots + 1) * 4)};
+  DevBuf& counters = ds.buf("s.counters", 64);
+  DevBuf& cub_tmp = ds.buf("s.cub_tmp", 8);
   const bool verify = req.rng_mode == 0 && req.verify_ties;
-  DevBuf vlist(verify ? cap * 4 : 4, s);
-  KdeWorkspace ws;
+  DevBuf& vlist = ds.buf("s.vlist", verify ? cap * 4 : 4);
+  if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
+  KdeWorkspace& ws = *ds.kde_ws;
 
   init_rows_kernel<<<ceil_div_u32(std::max<uint32_t>(nq, 1), 256), 256, 0, s>>>(
-      out.uq.as<uint32_t>(), nq, qrow.as<uint32_t>(), eq[0].as<uint32_t>(),
-      et[0].as<uint32_t>(), eg[0].as<uint32_t>(), dtk.as<uint32_t>());
+      out.uq.as<uint32_t>(), nq, qrow.as<uint32_t>(), eq[0]->as<uint32_t>(),
+      et[0]->as<uint32_t>(), eg[0]->as<uint32_t>(), dtk.as<uint32_t>());
   FSGG_LAUNCH_CHECK();
   ds.launches++;
   const uint32_t goff0[2] = {0, nq};
-  FSGG_CUDA(cudaMemcpyAsync(goff[0].as<void>(), goff0, 8, cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemcpyAsync(goff[0]->as<void>(), goff0, 8, cudaMemcpyHostToDevice, s));
 
   const uint64_t prefix = route_key_prefix(req.seed);
   uint32_t E = nq;
@@ -396,6 +463,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   out.tickets_per_level.clear();
   out.degenerate_draws = 0;
   out.tie_verified = 0;
+  out.kde = KdeStats{};
   out.peak_entries = 0;
   // FSGG_TRACE=1: per-level phase times (CUDA events on the launch stream)
   // and host wall time to stderr.
@@ -415,37 +483,71 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     lv.level = level;
     lv.num_slots = G;
     lv.num_entries = E;
-    lv.eq = eq[cur].as<uint32_t>();
-    lv.eg = eg[cur].as<uint32_t>();
-    lv.elm = level == 0 ? nullptr : elm[cur].as<float>();
+    lv.eq = eq[cur]->as<uint32_t>();
+    lv.eg = eg[cur]->as<uint32_t>();
+    lv.elm = level == 0 ? nullptr : elm[cur]->as<float>();
     lv.prune = req.prune;
-    lv.goff = goff[cur].as<uint32_t>();
-    kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
-              level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr,
-              ws, out.kde);
+    lv.goff = goff[cur]->as<uint32_t>();
+    const bool lookup = have_rows && level - row_level < row_depth;
+    bool self_rows = false;
+    if (lookup) {
+      FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
+      lookup_sums_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+          E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
+          eprow[cur]->as<uint32_t>(), ws.partials.as<double>(), t.first.as<uint32_t>(),
+          t.last.as<uint32_t>(), g1.as<double>(), g2.as<double>(),
+          lookup_evals.as<unsigned long long>());
+      FSGG_LAUNCH_CHECK();
+      ds.launches++;
+      unsigned long long ev = 0;
+      FSGG_CUDA(cudaMemcpyAsync(&ev, lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      out.kde.evals += ev;  // reference-equivalent work served from the rows
+    } else {
+      uint32_t rd = 0;
+      kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
+                level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr, ws,
+                out.kde, kServeLevels, &rd);
+      have_rows = rd > 1;
+      if (have_rows) {
+        self_rows = true;
+        row_level = level;
+        row_depth = rd;
+        if (req.prune && req.verify_ties && req.rng_mode == 0) {
+          row_mass.ensure(size_t(E) * 4, s);
+          if (level == 0)
+            FSGG_CUDA(cudaMemsetAsync(row_mass.as<void>(), 0, size_t(E) * 4, s));
+          else
+            FSGG_CUDA(cudaMemcpyAsync(row_mass.as<void>(), elm[cur]->as<void>(),
+                                      size_t(E) * 4, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    }
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[1], s));
     FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
     uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
     route_kernel<<<ceil_div_u32(uint64_t(E) + 1, 256), 256, 0, s>>>(
-        E, level, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(),
-        eg[cur].as<uint32_t>(), g1.as<double>(), g2.as<double>(),
+        E, level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(),
+        eg[cur]->as<uint32_t>(), g1.as<double>(), g2.as<double>(),
         t.first.as<uint32_t>(), t.last.as<uint32_t>(), prefix, req.rng_mode,
         req.seed, qrow.as<uint32_t>(), out.row_off.as<uint64_t>(),
         out.row_cnt.as<uint32_t>(), out.leaf_src.as<uint32_t>(),
         out.leaf_cnt.as<uint32_t>(), tl.as<uint32_t>(),
         flags.as<unsigned long long>(), counters.as<unsigned long long>(),
-        level == 0 ? nullptr : elm[cur].as<float>(),
+        level == 0 ? nullptr : elm[cur]->as<float>(),
+        self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
+        (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
         verify ? vlist.as<uint32_t>() : nullptr, vcount);
     FSGG_LAUNCH_CHECK();
     if (verify) {
       exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
-          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, level, eq[cur].as<uint32_t>(),
-          eg[cur].as<uint32_t>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, level, eq[cur]->as<uint32_t>(),
+          eg[cur]->as<uint32_t>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
           vlist.as<uint32_t>(), vcount, g1.as<double>(), g2.as<double>());
       FSGG_LAUNCH_CHECK();
       reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
-          level, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(), eg[cur].as<uint32_t>(),
+          level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
           g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
           prefix, vlist.as<uint32_t>(), vcount, tl.as<uint32_t>(),
           flags.as<unsigned long long>(), counters.as<unsigned long long>());
@@ -464,15 +566,16 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         P.as<unsigned long long>(), uint64_t(E) + 1, s));
     const int nxt = cur ^ 1;
     scatter_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
-        E, eq[cur].as<uint32_t>(), et[cur].as<uint32_t>(), eg[cur].as<uint32_t>(),
-        tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur].as<uint32_t>(),
-        P.as<unsigned long long>(), g1.as<double>(), g2.as<double>(), eq[nxt].as<uint32_t>(),
-        et[nxt].as<uint32_t>(), eg[nxt].as<uint32_t>(), elm[nxt].as<float>());
+        E, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+        tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur]->as<uint32_t>(),
+        P.as<unsigned long long>(), g1.as<double>(), g2.as<double>(), eq[nxt]->as<uint32_t>(),
+        et[nxt]->as<uint32_t>(), eg[nxt]->as<uint32_t>(), elm[nxt]->as<float>(),
+        eprow[cur]->as<uint32_t>(), eprow[nxt]->as<uint32_t>(), self_rows ? 1 : 0);
     FSGG_LAUNCH_CHECK();
     if (level < t.depth) {
       goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
-          G, goff[cur].as<uint32_t>(), P.as<unsigned long long>(),
-          goff[nxt].as<uint32_t>());
+          G, goff[cur]->as<uint32_t>(), P.as<unsigned long long>(),
+          goff[nxt]->as<uint32_t>());
       FSGG_LAUNCH_CHECK();
       ds.launches++;
     }
@@ -519,7 +622,10 @@ void sampled_triples_to_host(Dataset& ds, SampleResult& res,
   triples.clear();
   if (nq == 0 || total == 0) return;
   if (total > 0x7fffffffull) throw ConfigError("too many tickets for host output");
-  DevBuf ends(size_t(nq) * 8, s), src_out(total * 4, s), cnt_out(total * 4, s), tmp;
+  DevBuf& ends = ds.buf("t.ends", size_t(nq) * 8);
+  DevBuf& src_out = ds.buf("t.src", total * 4);
+  DevBuf& cnt_out = ds.buf("t.cnt", total * 4);
+  DevBuf& tmp = ds.buf("t.tmp", 8);
   row_ends_kernel<<<ceil_div_u32(nq, 256), 256, 0, s>>>(
       res.row_off.as<uint64_t>(), res.row_cnt.as<uint32_t>(), nq, ends.as<uint64_t>());
   FSGG_LAUNCH_CHECK();
@@ -528,7 +634,7 @@ void sampled_triples_to_host(Dataset& ds, SampleResult& res,
       nullptr, tmp_bytes, res.leaf_src.as<uint32_t>(), src_out.as<uint32_t>(),
       res.leaf_cnt.as<uint32_t>(), cnt_out.as<uint32_t>(), int(total), int(nq),
       res.row_off.as<uint64_t>(), ends.as<uint64_t>(), s));
-  tmp.alloc(tmp_bytes, s);
+  tmp.ensure(tmp_bytes, s);
   FSGG_CUDA(cub::DeviceSegmentedSort::SortPairs(
       tmp.as<void>(), tmp_bytes, res.leaf_src.as<uint32_t>(), src_out.as<uint32_t>(),
       res.leaf_cnt.as<uint32_t>(), cnt_out.as<uint32_t>(), int(total), int(nq),

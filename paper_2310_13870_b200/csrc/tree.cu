@@ -77,8 +77,8 @@ void build_tree(Dataset& ds) {
   t.depth = depth;
   t.slots = (2ull << depth) - 1;
   cudaStream_t s = ds.stream;
-  t.first.alloc(t.slots * 4, s);
-  t.last.alloc(t.slots * 4, s);
+  t.first.ensure(t.slots * 4, s);
+  t.last.ensure(t.slots * 4, s);
   const int tpb = 256;
   tree_ranges_kernel<<<ceil_div_u32(t.slots, tpb), tpb, 0, s>>>(
       ds.n, t.slots, t.first.as<uint32_t>(), t.last.as<uint32_t>());
@@ -86,8 +86,8 @@ void build_tree(Dataset& ds) {
   ds.launches++;
   t.has_boxes = ds.d <= kBoxMaxDim;
   if (t.has_boxes) {
-    t.lo.alloc(t.slots * ds.d * 4, s);
-    t.hi.alloc(t.slots * ds.d * 4, s);
+    t.lo.ensure(t.slots * ds.d * 4, s);
+    t.hi.ensure(t.slots * ds.d * 4, s);
     for (int level = int(depth); level >= 0; --level) {
       uint64_t cnt = 1ull << level;
       tree_boxes_kernel<<<ceil_div_u32(cnt, tpb), tpb, 0, s>>>(
