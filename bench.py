@@ -303,20 +303,20 @@ def main():
         pinned = torch.empty(w.points.shape, dtype=torch.float32, pin_memory=True)
         pinned.numpy()[:] = w.points
         host_ptr = pinned.data_ptr()
+        hostbufs = F.api.HostGraphBuffers()
         h2d = w.points.nbytes
         e2e_ms, d2h = 0.0, 0
         for i in range(args.warmup + K):
             torch.cuda.synchronize()
             barrier()
             t0 = time.perf_counter()
-            ds.upload_ptr(host_ptr)
+            ds.upload_ptr(host_ptr)  # pinned host -> device
             if world == 1:
-                g = F.build_similarity_graph(ds, kernel, cfg)
-                nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+                dg, _ = F.build_similarity_graph_device(ds, kernel, cfg)
             else:
-                parallel.build_similarity_graph_distributed(ds, kernel, cfg)
-                g = F.api.device_graph_to_host(ds)
-                nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+                dg = parallel.build_similarity_graph_distributed(ds, kernel, cfg).graph
+            g = hostbufs.fetch(ds, dg)  # device -> pinned host: edges, CSR, degrees
+            nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
             torch.cuda.synchronize()
             barrier()
             if i >= args.warmup:

@@ -203,6 +203,13 @@ int fsgg_build_similarity_graph_host(const float* points, uint32_t n,
  * or distributed build) into host memory (free with fsgg_graph_free). */
 int fsgg_device_graph_to_host(fsgg_dataset* ds, fsgg_graph* out);
 
+/* Copy the handle's current device graph into caller-owned host buffers
+ * (any may be NULL): u, v (num_edges u32), w (num_edges f64), row_ptr
+ * (n + 1 u64), degrees (n f64). With pinned (page-locked) buffers this runs
+ * at full PCIe/C2C bandwidth; completes before returning. */
+int fsgg_device_graph_copy(fsgg_dataset* ds, uint32_t* u, uint32_t* v,
+                           double* w, uint64_t* row_ptr, double* degrees);
+
 void fsgg_graph_free(fsgg_graph* g);
 void fsgg_free(void* p);
 

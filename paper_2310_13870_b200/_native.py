@@ -116,6 +116,7 @@ _SIGS = {
                                                    C.POINTER(fsgg_report)]),
     "fsgg_graph_free": (None, [C.POINTER(fsgg_graph)]),
     "fsgg_device_graph_to_host": (C.c_int, [_P, C.POINTER(fsgg_graph)]),
+    "fsgg_device_graph_copy": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "fsgg_free": (None, [_P]),
     "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
                                                 C.c_uint32, C.c_uint64, C.c_int, C.c_int,

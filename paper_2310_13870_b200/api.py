@@ -293,6 +293,37 @@ def device_graph_to_host(ds: Dataset) -> WeightedGraph:
         lib.fsgg_graph_free(C.byref(g))
 
 
+class HostGraphBuffers:
+    """Reusable page-locked host buffers for device graph read-back (the
+    e2e path): grown on demand, filled by fsgg_device_graph_copy."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def _get(self, name, count, dtype):
+        import torch
+        tdt = {np.uint32: torch.int32, np.float64: torch.float64, np.uint64: torch.int64}[dtype]
+        t = self._bufs.get(name)
+        if t is None or t.numel() < count:
+            t = torch.empty(max(count, 1) + max(count, 1) // 4, dtype=tdt, pin_memory=True)
+            self._bufs[name] = t
+        return t.numpy().view(dtype)[:count]
+
+    def fetch(self, ds: "Dataset", graph) -> "WeightedGraph":
+        m, n = int(graph.num_edges), int(graph.n)
+        u = self._get("u", m, np.uint32)
+        v = self._get("v", m, np.uint32)
+        w = self._get("w", m, np.float64)
+        rp = self._get("row_ptr", n + 1, np.uint64)
+        dg = self._get("degrees", n, np.float64)
+        N.check(N.lib().fsgg_device_graph_copy(
+            ds._h, u.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
+            w.ctypes.data_as(C.c_void_p), rp.ctypes.data_as(C.c_void_p),
+            dg.ctypes.data_as(C.c_void_p)))
+        return WeightedGraph(n=n, u=u, v=v, w=w, row_ptr=rp, degrees=dg,
+                             total_weight=float(graph.total_weight))
+
+
 def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig | None = None,
                            report: bool = False, estimates: bool = False):
     """FastSimilarityGraph (proj/src/sparsifier.cpp:51-142) on the device.

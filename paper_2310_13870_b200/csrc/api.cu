@@ -426,6 +426,26 @@ int fsgg_device_graph_to_host(fsgg_dataset* h, fsgg_graph* out) {
   });
 }
 
+int fsgg_device_graph_copy(fsgg_dataset* h, uint32_t* u, uint32_t* v, double* w,
+                           uint64_t* row_ptr, double* degrees) {
+  return guarded([&] {
+    activate(h);
+    if (!h->graph) throw fsgg::ConfigError("no graph built on this dataset");
+    const fsgg::GraphResult& g = *h->graph;
+    cudaStream_t s = h->ds.stream;
+    auto cp = [&](void* dst, const fsgg::DevBuf& src, size_t bytes) {
+      if (dst && bytes)
+        FSGG_CUDA(cudaMemcpyAsync(dst, src.as<void>(), bytes, cudaMemcpyDeviceToHost, s));
+    };
+    cp(u, g.u, g.m * 4);
+    cp(v, g.v, g.m * 4);
+    cp(w, g.w, g.m * 8);
+    cp(row_ptr, g.row_ptr, (uint64_t(g.n) + 1) * 8);
+    cp(degrees, g.degrees, uint64_t(g.n) * 8);
+    FSGG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 void fsgg_graph_free(fsgg_graph* g) {
   if (!g) return;
   std::free(g->u);
