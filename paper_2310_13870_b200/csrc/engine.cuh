@@ -176,6 +176,7 @@ struct SampleRequest {
   int rng_mode = 0;
   int prune = 1;
   bool verify_ties = true;  // reference RNG mode: re-decide near-ties on fp64 sums
+  bool dfs_finish = true;   // finish small-node levels depth-first (finish.cu)
   bool want_root_sums = false;
 };
 
@@ -200,6 +201,21 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
 // Sorted (query, source, count) triples copied to the host.
 void sampled_triples_to_host(Dataset& ds, SampleResult& res,
                              std::vector<uint32_t>& triples);
+
+// ---- finish.cu ------------------------------------------------------------
+constexpr uint32_t kDfsMaxNode = 128;  // levels whose nodes are all <= this
+struct DfsArgs {
+  uint32_t E = 0, level = 0;
+  const uint32_t *eq = nullptr, *et = nullptr, *eg = nullptr;
+  uint64_t key_prefix = 0, seed = 0;
+  int rng_mode = 0, verify = 1;
+  const uint32_t* qrow = nullptr;
+  const uint64_t* row_off = nullptr;
+  uint32_t *row_cnt = nullptr, *leaf_src = nullptr, *leaf_cnt = nullptr;
+  unsigned long long* stats = nullptr;  // [4][64] entries/tickets/evals/degen + ties
+};
+bool dfs_finish_supported(uint32_t d);
+void dfs_finish(Dataset& ds, const KernelSpec& ks, const DfsArgs& args);
 
 // ---- graph.cu -------------------------------------------------------------
 struct GraphResult {

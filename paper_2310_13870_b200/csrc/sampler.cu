@@ -474,6 +474,49 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   for (uint32_t level = 0; E > 0; ++level) {
     if (level > t.depth) throw NumericError("descent exceeded tree depth");
     const uint32_t G = 1u << level;
+    const uint32_t smax_level = uint32_t((uint64_t(ds.n) + (1ull << level) - 1) >> level);
+    if (req.dfs_finish && dfs_finish_supported(ds.d) && smax_level <= kDfsMaxNode) {
+      // every remaining level is finished depth-first per entry (finish.cu)
+      DevBuf& st = ds.buf("s.dfs_stats", (4 * 64 + 1) * 8);
+      FSGG_CUDA(cudaMemsetAsync(st.as<void>(), 0, (4 * 64 + 1) * 8, s));
+      DfsArgs a;
+      a.E = E;
+      a.level = level;
+      a.eq = eq[cur]->as<uint32_t>();
+      a.et = et[cur]->as<uint32_t>();
+      a.eg = eg[cur]->as<uint32_t>();
+      a.key_prefix = prefix;
+      a.seed = req.seed;
+      a.rng_mode = req.rng_mode;
+      a.verify = verify ? 1 : 0;
+      a.qrow = qrow.as<uint32_t>();
+      a.row_off = out.row_off.as<uint64_t>();
+      a.row_cnt = out.row_cnt.as<uint32_t>();
+      a.leaf_src = out.leaf_src.as<uint32_t>();
+      a.leaf_cnt = out.leaf_cnt.as<uint32_t>();
+      a.stats = st.as<unsigned long long>();
+      const auto w0 = std::chrono::steady_clock::now();
+      dfs_finish(ds, ks, a);
+      std::vector<unsigned long long> h(4 * 64 + 1);
+      FSGG_CUDA(cudaMemcpyAsync(h.data(), st.as<void>(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      for (uint32_t lv2 = level; lv2 < 64 && h[lv2]; ++lv2) {
+        out.entries_per_level.push_back(h[lv2]);
+        out.tickets_per_level.push_back(h[64 + lv2]);
+        out.kde.evals += h[128 + lv2];
+        out.kde.performed += h[128 + lv2];
+        out.degenerate_draws += h[192 + lv2];
+        out.peak_entries = std::max<uint64_t>(out.peak_entries, h[lv2]);
+      }
+      out.tie_verified += h[256];
+      if (trace)
+        std::fprintf(stderr, "fsgg levels %u..: depth-first finish of %u entries %.3fms\n",
+                     level, E,
+                     std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - w0).count());
+      E = 0;
+      break;
+    }
     const auto wall0 = std::chrono::steady_clock::now();
     const KdeStats kde0 = out.kde;
     if (trace) FSGG_CUDA(cudaEventRecord(tev[0], s));
