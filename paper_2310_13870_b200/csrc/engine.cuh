@@ -203,7 +203,7 @@ void sampled_triples_to_host(Dataset& ds, SampleResult& res,
                              std::vector<uint32_t>& triples);
 
 // ---- finish.cu ------------------------------------------------------------
-constexpr uint32_t kDfsMaxNode = 128;  // levels whose nodes are all <= this
+constexpr uint32_t kDfsMaxNode = 0;  // depth-first finish off by default (slower: divergent)
 struct DfsArgs {
   uint32_t E = 0, level = 0;
   const uint32_t *eq = nullptr, *et = nullptr, *eg = nullptr;

@@ -20,6 +20,7 @@ namespace {
 
 constexpr int kDfsThreads = 128;
 constexpr int kMaxLevels = 64;
+constexpr int kMaxDepth = 10;  // levels below the start level (nodes <= 512)
 constexpr double kTieMargin = 1e-4;  // as route_kernel (sampler.cu)
 
 __device__ __forceinline__ uint4 philox4x32_f(uint4 c, uint2 k) {
@@ -88,13 +89,18 @@ __global__ void __launch_bounds__(kDfsThreads)
     sh[sp] = ((1u << level0) - 1) + eg[i];
     st[sp++] = et[i];
     unsigned long long ties = 0;
+    // per-thread per-level tallies (flushed once: shared-memory atomics per
+    // visited node would serialise the block on a handful of addresses)
+    uint32_t c_ent[kMaxDepth] = {}, c_tik[kMaxDepth] = {}, c_ev[kMaxDepth] = {},
+             c_deg[kMaxDepth] = {};
     while (sp > 0) {
       --sp;
       const uint32_t h = sh[sp], t = st[sp];
       const uint32_t lev = 31 - __clz(h + 1);
+      const uint32_t rl = min(lev - level0, uint32_t(kMaxDepth - 1));
       const uint32_t f = tfirst[h], l = tlast[h];
-      atomicAdd(&s_stats[0][lev], 1ull);
-      atomicAdd(&s_stats[1][lev], static_cast<unsigned long long>(t));
+      c_ent[rl] += 1;
+      c_tik[rl] += t;
       if (l - f == 1) {  // proj/src/sampler.cpp:196-198
         const uint32_t slot = atomicAdd(row_cnt + row, 1u);
         const uint64_t at = row_off[row] + slot;
@@ -112,7 +118,7 @@ __global__ void __launch_bounds__(kDfsThreads)
                                    : 0.f;
       double a = fmax(range_sum_f32<D, FAM>(pts, qc, f, mid, scale, offl), kSumFloor);
       double b = fmax(range_sum_f32<D, FAM>(pts, qc, mid, l, scale, offr), kSumFloor);
-      atomicAdd(&s_stats[2][lev], static_cast<unsigned long long>(l - f));
+      c_ev[rl] += l - f;
       bool exact = false;
       uint32_t left = 0;
       for (int pass = 0; pass < 2; ++pass) {
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(kDfsThreads)
           ++ties;
           continue;
         }
-        if (degenerate) atomicAdd(&s_stats[3][lev], static_cast<unsigned long long>(t));
+        if (degenerate) c_deg[rl] += t;
         break;
       }
       // right pushed first so the left subtree is walked first
@@ -173,6 +179,13 @@ __global__ void __launch_bounds__(kDfsThreads)
       }
     }
     if (ties) atomicAdd(&s_ties, ties);
+    for (uint32_t r = 0; r < kMaxDepth && level0 + r < kMaxLevels; ++r) {
+      if (!c_ent[r]) break;
+      atomicAdd(&s_stats[0][level0 + r], static_cast<unsigned long long>(c_ent[r]));
+      atomicAdd(&s_stats[1][level0 + r], static_cast<unsigned long long>(c_tik[r]));
+      atomicAdd(&s_stats[2][level0 + r], static_cast<unsigned long long>(c_ev[r]));
+      if (c_deg[r]) atomicAdd(&s_stats[3][level0 + r], static_cast<unsigned long long>(c_deg[r]));
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < 4 * kMaxLevels; k += blockDim.x) {

@@ -34,6 +34,16 @@ constexpr double kTieMargin = 1e-4;
 // A compute level keeps partial rows deep enough to serve this many levels.
 constexpr uint32_t kServeLevels = 5;
 
+// Levels whose nodes all hold <= this many points are finished depth-first
+// (finish.cu); FSGG_DFS_MAX overrides (0 disables).
+uint32_t dfs_max_node() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("FSGG_DFS_MAX");
+    return e ? uint32_t(std::atoi(e)) : kDfsMaxNode;
+  }();
+  return v;
+}
+
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
                                  uint32_t* __restrict__ eq,
@@ -475,7 +485,21 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     if (level > t.depth) throw NumericError("descent exceeded tree depth");
     const uint32_t G = 1u << level;
     const uint32_t smax_level = uint32_t((uint64_t(ds.n) + (1ull << level) - 1) >> level);
-    if (req.dfs_finish && dfs_finish_supported(ds.d) && smax_level <= kDfsMaxNode) {
+    if (req.dfs_finish && dfs_finish_supported(ds.d) && smax_level <= dfs_max_node()) {
+      if (level == 0 && req.want_root_sums) {
+        // the root's sums are the degree KDE g_full: compute them first
+        LevelView lv0;
+        lv0.level = 0;
+        lv0.num_slots = 1;
+        lv0.num_entries = E;
+        lv0.eq = eq[cur]->as<uint32_t>();
+        lv0.eg = eg[cur]->as<uint32_t>();
+        lv0.goff = goff[cur]->as<uint32_t>();
+        lv0.prune = req.prune;
+        KdeStats scratch;
+        kde_level(ds, ks, lv0, g1.as<double>(), g2.as<double>(), out.groot.as<double>(), ws,
+                  scratch, 1, nullptr);
+      }
       // every remaining level is finished depth-first per entry (finish.cu)
       DevBuf& st = ds.buf("s.dfs_stats", (4 * 64 + 1) * 8);
       FSGG_CUDA(cudaMemsetAsync(st.as<void>(), 0, (4 * 64 + 1) * 8, s));

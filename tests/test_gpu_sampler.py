@@ -295,3 +295,32 @@ def test_philox_mode_graph_is_valid():
         estimates=True)
     assert rep.sampled_pairs > 0 and g.num_edges() <= 2000 * 32
     assert np.all(np.abs(g.w * est["p_hat"] - est["k_ij"]) <= 1e-12 * est["k_ij"])
+
+
+def test_depth_first_finish_matches_level_synchronous(tmp_path):
+    """The optional depth-first finish (FSGG_DFS_MAX, finish.cu) must give
+    the same samples and diagnostics as the level-synchronous path."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "dfs.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})\n"
+        "import paper_2310_13870_b200 as F\n"
+        "from paper_2310_13870_b200 import datasets\n"
+        "p, _ = datasets.make_moons(20000, 0.05, 3)\n"
+        "ds = F.Dataset(p)\n"
+        "k = F.Kernel(F.KernelFamily.gaussian, 0.1)\n"
+        "tri, d = F.sample_neighbors_counted(ds, k, np.arange(20000), 16, 5, diagnostics=True)\n"
+        "np.save(sys.argv[1], tri)\n"
+        "print(d.entries_per_level, d.tickets_per_level)\n")
+    outs = []
+    for dfs in ("0", "64"):
+        env = dict(os.environ, FSGG_DFS_MAX=dfs)
+        r = subprocess.run([sys.executable, str(script), str(tmp_path / f"t{dfs}.npy")], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        outs.append((np.load(tmp_path / f"t{dfs}.npy"), r.stdout))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
