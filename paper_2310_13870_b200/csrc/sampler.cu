@@ -72,7 +72,7 @@ __device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
 }
 
 // proj/src/sampler.cpp:186-225 per entry.
-__global__ void route_kernel(uint32_t E, uint32_t level,
+__global__ void __launch_bounds__(256, 6) route_kernel(uint32_t E, uint32_t level,
                              const uint32_t* __restrict__ eq,
                              const uint32_t* __restrict__ et,
                              const uint32_t* __restrict__ eg,
@@ -97,9 +97,14 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long tsum = 0, degen = 0;
   if (i < E) {
-    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    // every per-entry stream is loaded up front so the loads overlap (the
+    // kernel is latency-bound at deep levels: ~60M entries, little math)
+    const uint32_t gi = eg[i], q = eq[i], t = et[i];
+    const double a = g1[i], b = g2[i];
+    const float em = elm ? elm[i] : 0.f;
+    const uint32_t pr = eprow ? eprow[i] : i;
+    const uint64_t h = ((1ull << level) - 1) + gi;
     const uint32_t f = tfirst[h], l = tlast[h];
-    const uint32_t q = eq[i], t = et[i];
     tsum = t;
     unsigned long long fl = 0;
     if (l - f == 1) {
@@ -111,7 +116,6 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
       leaf_cnt[at] = t;
       tl[i] = 0;
     } else {
-      const double a = g1[i], b = g2[i];
       double p;
       bool verify = false;
       if (a <= kSumFloor && b <= kSumFloor) {  // :207-209
@@ -141,13 +145,10 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
             // Tie guard: a draw within the fp32 sums' error bound of p is
             // re-decided on fp64 sums (exact_sums_kernel), which makes the
             // output match the reference's exact backend edge for edge.
-            const float em = elm ? elm[i] : 0.f;
             const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
             // certified pruning at the compute level skipped < 2^-60 of the
             // ancestor row's mass: an absolute error on p of at most this
-            const double pruned =
-                row_mass ? exp2(double(row_mass[eprow ? eprow[i] : i]) - 58.0 - double(em))
-                         : 0.0;
+            const double pruned = row_mass ? double(exp2f(row_mass[pr] - 58.f - em)) : 0.0;
             const double M =
                 (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
             const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
@@ -194,30 +195,62 @@ __global__ void route_kernel(uint32_t E, uint32_t level,
 }
 
 // fp64 child sums for the entries the tie guard flagged: one CTA per entry,
-// every term in fp64 with the reference's operation order
-// (kernel_f64), fixed-order block reduction. Grid-strided over the device
-// count, so no host synchronisation is needed.
+// every term in fp64 with the reference's operation order (kernel_f64),
+// fixed-order block reduction. Sub-chunks (tree descendants of ~256+ points)
+// whose bounding-box bound is below 2^-80 of the entry's node mass are
+// skipped (total < 2^-70 of it: far below the 2^-53 resolution of the
+// decision). Grid-strided over the device count: no host synchronisation.
 __global__ void __launch_bounds__(256)
     exact_sums_kernel(const float* __restrict__ pts, uint32_t d, int family,
-                      double sigma, uint32_t level, const uint32_t* __restrict__ eq,
-                      const uint32_t* __restrict__ eg,
-                      const uint32_t* __restrict__ tfirst,
-                      const uint32_t* __restrict__ tlast,
+                      double sigma, float scale, uint32_t level, uint32_t depth,
+                      const uint32_t* __restrict__ eq, const uint32_t* __restrict__ eg,
+                      const float* __restrict__ elm, const uint32_t* __restrict__ tfirst,
+                      const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
+                      const float* __restrict__ thi, int has_boxes,
                       const uint32_t* __restrict__ vlist,
                       const uint32_t* __restrict__ vcount, double* __restrict__ g1,
                       double* __restrict__ g2) {
   __shared__ double red[2][256];
+  __shared__ unsigned char keep[1024];
   const uint32_t cnt = *vcount;
   for (uint32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
     const uint32_t i = vlist[b];
     const uint64_t h = ((1ull << level) - 1) + eg[i];
     const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
     const float* xq = pts + size_t(eq[i]) * d;
+    // sub-chunk depth below the node: >= 256 points each, <= 1024 of them
+    uint32_t kd = 0;
+    while (kd < 10 && level + kd + 1 <= depth && ((l - f) >> (kd + 1)) >= 256) ++kd;
+    const uint32_t nsub = 1u << kd;
+    const uint64_t hb = ((1ull << (level + kd)) - 1) + (uint64_t(eg[i]) << kd);
+    const float lim_base = (elm ? elm[i] : 0.f) - 1.f - 80.f;  // log2 of the skip bound
+    for (uint32_t c = threadIdx.x; c < nsub; c += blockDim.x) {
+      bool k = true;
+      if (has_boxes && kd > 0) {
+        float acc = 0.f;
+        for (uint32_t a = 0; a < d; ++a) {
+          const float v = fmaxf(fmaxf(tlo[(hb + c) * d + a] - xq[a], xq[a] - thi[(hb + c) * d + a]), 0.f);
+          acc = (family == 2) ? acc + v : fmaf(v, v, acc);
+        }
+        const float dist = family == 1 ? sqrtf(acc) : acc;
+        const float sz = float(tlast[hb + c] - tfirst[hb + c]);
+        k = __log2f(sz) - scale * dist >= lim_base;
+      }
+      keep[c] = k;
+    }
+    __syncthreads();
     double s0 = 0.0, s1 = 0.0;
-    for (uint32_t j = f + threadIdx.x; j < mid; j += blockDim.x)
-      s0 += kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
-    for (uint32_t j = mid + threadIdx.x; j < l; j += blockDim.x)
-      s1 += kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
+    for (uint32_t c = 0; c < nsub; ++c) {
+      if (!keep[c]) continue;
+      const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
+      for (uint32_t j = cf + threadIdx.x; j < cl; j += blockDim.x) {
+        const double v = kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
+        if (j < mid)
+          s0 += v;
+        else
+          s1 += v;
+      }
+    }
     red[0][threadIdx.x] = s0;
     red[1][threadIdx.x] = s1;
     __syncthreads();
@@ -609,9 +642,12 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     FSGG_LAUNCH_CHECK();
     if (verify) {
       exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
-          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, level, eq[cur]->as<uint32_t>(),
-          eg[cur]->as<uint32_t>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
-          vlist.as<uint32_t>(), vcount, g1.as<double>(), g2.as<double>());
+          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, ks.scale, level, t.depth,
+          eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+          level == 0 ? nullptr : elm[cur]->as<float>(), t.first.as<uint32_t>(),
+          t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+          t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
+          g2.as<double>());
       FSGG_LAUNCH_CHECK();
       reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
           level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
