@@ -71,118 +71,128 @@ __device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
   return c;
 }
 
-// proj/src/sampler.cpp:186-225 per entry.
-__global__ void __launch_bounds__(256, 6) route_kernel(uint32_t E, uint32_t level,
-                             const uint32_t* __restrict__ eq,
-                             const uint32_t* __restrict__ et,
-                             const uint32_t* __restrict__ eg,
-                             const double* __restrict__ g1,
-                             const double* __restrict__ g2,
-                             const uint32_t* __restrict__ tfirst,
-                             const uint32_t* __restrict__ tlast,
-                             uint64_t key_prefix, int rng_mode, uint64_t seed,
-                             const uint32_t* __restrict__ qrow,
-                             const uint64_t* __restrict__ row_off,
-                             uint32_t* __restrict__ row_cnt,
-                             uint32_t* __restrict__ leaf_src,
-                             uint32_t* __restrict__ leaf_cnt,
-                             uint32_t* __restrict__ tl,
-                             unsigned long long* __restrict__ flags,
-                             unsigned long long* __restrict__ counters,
-                             const float* __restrict__ elm,
-                             const uint32_t* __restrict__ eprow,
-                             const float* __restrict__ row_mass,
-                             uint32_t* __restrict__ vlist,
-                             uint32_t* __restrict__ vcount) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// proj/src/sampler.cpp:186-225 per entry. Each thread handles kRouteUnroll
+// entries (block-strided, coalesced) and issues every load of all of them
+// before using any: at deep levels the kernel is a latency-bound stream of
+// ~60M entries with little arithmetic.
+constexpr int kRouteThreads = 256;
+constexpr int kRouteUnroll = 4;
+
+__global__ void __launch_bounds__(kRouteThreads)
+    route_kernel(uint32_t E, uint32_t level, const uint32_t* __restrict__ eq,
+                 const uint32_t* __restrict__ et, const uint32_t* __restrict__ eg,
+                 const double* __restrict__ g1, const double* __restrict__ g2,
+                 const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                 uint64_t key_prefix, int rng_mode, uint64_t seed,
+                 const uint32_t* __restrict__ qrow, const uint64_t* __restrict__ row_off,
+                 uint32_t* __restrict__ row_cnt, uint32_t* __restrict__ leaf_src,
+                 uint32_t* __restrict__ leaf_cnt, uint32_t* __restrict__ tl,
+                 unsigned long long* __restrict__ flags,
+                 unsigned long long* __restrict__ counters, const float* __restrict__ elm,
+                 const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
+                 uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount) {
+  constexpr int U = kRouteUnroll;
+  const uint32_t base = blockIdx.x * (kRouteThreads * U) + threadIdx.x;
+  uint32_t gi[U], q[U], t[U], f[U], l[U];
+  double a[U], b[U];
+  float em[U], rm[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kRouteThreads;
+    const bool ok = i < E;
+    gi[u] = ok ? eg[i] : 0u;
+    q[u] = ok ? eq[i] : 0u;
+    t[u] = ok ? et[i] : 0u;
+    a[u] = ok ? g1[i] : 0.0;
+    b[u] = ok ? g2[i] : 0.0;
+    em[u] = (ok && elm) ? elm[i] : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kRouteThreads;
+    const uint64_t h = ((1ull << level) - 1) + gi[u];
+    f[u] = i < E ? tfirst[h] : 0u;
+    l[u] = i < E ? tlast[h] : 0u;
+    rm[u] = (i < E && row_mass) ? row_mass[eprow ? eprow[i] : i] : 0.f;
+  }
   unsigned long long tsum = 0, degen = 0;
-  if (i < E) {
-    // every per-entry stream is loaded up front so the loads overlap (the
-    // kernel is latency-bound at deep levels: ~60M entries, little math)
-    const uint32_t gi = eg[i], q = eq[i], t = et[i];
-    const double a = g1[i], b = g2[i];
-    const float em = elm ? elm[i] : 0.f;
-    const uint32_t pr = eprow ? eprow[i] : i;
-    const uint64_t h = ((1ull << level) - 1) + gi;
-    const uint32_t f = tfirst[h], l = tlast[h];
-    tsum = t;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kRouteThreads;
+    if (i == E) flags[i] = 0;  // scan sentinel
+    if (i >= E) continue;
+    tsum += t[u];
     unsigned long long fl = 0;
-    if (l - f == 1) {
+    if (l[u] - f[u] == 1) {
       // :196-198 leaf: (query, source = first, count = tickets)
-      const uint32_t row = qrow[q];
+      const uint32_t row = qrow[q[u]];
       const uint32_t slot = atomicAdd(row_cnt + row, 1u);
       const uint64_t at = row_off[row] + slot;
-      leaf_src[at] = f;
-      leaf_cnt[at] = t;
+      leaf_src[at] = f[u];
+      leaf_cnt[at] = t[u];
       tl[i] = 0;
     } else {
       double p;
       bool verify = false;
-      if (a <= kSumFloor && b <= kSumFloor) {  // :207-209
+      if (a[u] <= kSumFloor && b[u] <= kSumFloor) {  // :207-209
         p = 0.5;
         if (vlist)
           verify = true;  // degenerate by fp32 sums: decided on exact sums
         else
-          degen = t;
+          degen += t[u];
       } else {
-        p = a / (a + b);  // :211
+        p = a[u] / (a[u] + b[u]);  // :211
       }
-      uint32_t left;
-      if (p <= 0.0) {  // rng.hpp:66-67
-        left = 0;
-      } else if (p >= 1.0) {
-        left = t;
-      } else {
+      uint32_t left = 0;
+      if (p >= 1.0) {  // rng.hpp:66-67
+        left = t[u];
+      } else if (p > 0.0) {
         // u_c = (x_c >> 11) * 2^-53 < p  <=>  (x_c >> 11) < ceil(p * 2^53)
         const double P = p * 9007199254740992.0;
         const uint64_t thr = static_cast<uint64_t>(ceil(P));
-        left = 0;
         if (rng_mode == 0) {
           // RngStream::keyed(seed, kRouteTag, (first<<32)|last, query)
           const uint64_t key =
-              route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
+              route_key(key_prefix, (uint64_t(f[u]) << 32) | l[u], uint64_t(q[u]));
           if (vlist) {
             // Tie guard: a draw within the fp32 sums' error bound of p is
             // re-decided on fp64 sums (exact_sums_kernel), which makes the
             // output match the reference's exact backend edge for edge.
-            const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
+            const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em[u]) / 32.0);
             // certified pruning at the compute level skipped < 2^-60 of the
             // ancestor row's mass: an absolute error on p of at most this
-            const double pruned = row_mass ? double(exp2f(row_mass[pr] - 58.f - em)) : 0.0;
-            const double M =
-                (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
+            const double pruned = row_mass ? double(exp2f(rm[u] - 58.f - em[u])) : 0.0;
+            const double M = (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
             const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
             const uint64_t hi = static_cast<uint64_t>(P + M);
             bool near = false;
-            for (uint32_t c = 0; c < t; ++c) {
+            for (uint32_t c = 0; c < t[u]; ++c) {
               const uint64_t m = splitmix64(key + c) >> 11;
               left += m < thr ? 1u : 0u;
               near |= (m >= lo) & (m <= hi);
             }
             verify |= near;
           } else {
-            for (uint32_t c = 0; c < t; ++c)
+            for (uint32_t c = 0; c < t[u]; ++c)
               left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
           }
         } else {
           const uint2 k = make_uint2(uint32_t(seed), uint32_t(seed >> 32));
-          for (uint32_t c = 0; c < t; c += 2) {
-            const uint4 r = philox4x32(make_uint4(c >> 1, q, f, l), k);
+          for (uint32_t c = 0; c < t[u]; c += 2) {
+            const uint4 r = philox4x32(make_uint4(c >> 1, q[u], f[u], l[u]), k);
             const uint64_t x0 = (uint64_t(r.x) << 32) | r.y;
             const uint64_t x1 = (uint64_t(r.z) << 32) | r.w;
             left += (x0 >> 11) < thr ? 1u : 0u;
-            if (c + 1 < t) left += (x1 >> 11) < thr ? 1u : 0u;
+            if (c + 1 < t[u]) left += (x1 >> 11) < thr ? 1u : 0u;
           }
         }
       }
       tl[i] = left;
       fl = (static_cast<unsigned long long>(left > 0) << 32) |
-           static_cast<unsigned long long>(left < t);
+           static_cast<unsigned long long>(left < t[u]);
       if (verify) vlist[atomicAdd(vcount, 1u)] = i;
     }
     flags[i] = fl;
-  } else if (i == E) {
-    flags[i] = 0;
   }
   for (int o = 16; o; o >>= 1) {
     tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
@@ -627,7 +637,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     if (trace) FSGG_CUDA(cudaEventRecord(tev[1], s));
     FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
     uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
-    route_kernel<<<ceil_div_u32(uint64_t(E) + 1, 256), 256, 0, s>>>(
+    route_kernel<<<ceil_div_u32(uint64_t(E) + 1, kRouteThreads * kRouteUnroll),
+                   kRouteThreads, 0, s>>>(
         E, level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(),
         eg[cur]->as<uint32_t>(), g1.as<double>(), g2.as<double>(),
         t.first.as<uint32_t>(), t.last.as<uint32_t>(), prefix, req.rng_mode,
