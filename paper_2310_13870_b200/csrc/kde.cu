@@ -60,6 +60,7 @@ constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
 constexpr float kPruneBits = 80.f;   // sub-chunk bound below 2^-80 of the node mass
 constexpr uint32_t kSubMin = 512;    // smallest sub-chunk (pruning granularity)
+constexpr uint32_t kSubMinSmall = 64;  // ... for nodes below 8 * kSubMin points
 
 template <int D>
 struct LowDTile {
@@ -767,13 +768,16 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const uint32_t child_min = node_min / 2;
   const uint64_t target_items = uint64_t(ds.num_sms) * 8 * 40;
   uint32_t sd = 0;
-  while ((child_min >> (sd + 1)) >= kSubMin && lv.level + 2 + sd <= t.depth) ++sd;
+  // small nodes: finer sub-chunks so the partial rows can still serve the
+  // next levels (pruning rarely applies there anyway)
+  const uint32_t sub_min = child_min >= 8 * kSubMin ? kSubMin : kSubMinSmall;
+  while ((child_min >> (sd + 1)) >= sub_min && lv.level + 2 + sd <= t.depth) ++sd;
   // c >= serve_levels - 1 keeps per-entry partials at the granularity of
   // the node's descendants c+1 levels down, so the next c levels' child sums
   // are range sums of this row (lookup_sums_kernel, sampler.cu) instead of
   // new kernel evaluations.
   uint32_t c = 0;
-  while (c < sd && (child_min >> (c + 1)) >= (lowd ? kSubMin : kChunkMin) &&
+  while (c < sd && (child_min >> (c + 1)) >= (lowd ? sub_min : kChunkMin) &&
          ((uint64_t(total_blocks) << (c + 1)) < target_items || c + 1 < serve_levels) &&
          (uint64_t(E) << (c + 2)) <= kMaxPartials)
     ++c;
