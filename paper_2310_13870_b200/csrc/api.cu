@@ -363,6 +363,7 @@ int fsgg_dataset_upload(fsgg_dataset* h, const float* host_points) {
                               size_t(h->ds.n) * h->ds.d * 4, cudaMemcpyHostToDevice,
                               h->ds.stream));
     h->ds.tree_valid = false;  // bounding boxes depend on the coordinates
+    h->ds.tc_ready = false;    // so do the tf32 split copies
   });
 }
 

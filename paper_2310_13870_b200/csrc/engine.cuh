@@ -108,6 +108,9 @@ struct Dataset {
     return b;
   }
   std::unique_ptr<KdeWorkspace> kde_ws;
+  // tensor-core path (kde_tc.cu): split tf32 hi/lo copies + tensor maps
+  bool tc_ready = false;
+  alignas(64) unsigned char tc_blob[320];
   void release_all();
 };
 
@@ -162,6 +165,14 @@ inline void Dataset::release_all() {
 void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                double* g1, double* g2, double* groot, KdeWorkspace& ws,
                KdeStats& stats, uint32_t serve_levels, uint32_t* row_depth);
+
+// ---- kde_tc.cu (tcgen05 / TMEM / TMA, 3xTF32) -------------------------------
+constexpr uint32_t kTcMinDim = 64;
+bool kde_tc_supported(const Dataset& ds, int family);
+// Same work items / partial layout as the tiled kernels with 128 entries per
+// block; blk_off must have been computed with 128 entries per block.
+void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
+                  const uint32_t* blk_off, uint32_t cdepth, uint64_t items, double* partials);
 
 // KdeEstimator::eval seam: arbitrary range, arbitrary targets (device).
 void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,

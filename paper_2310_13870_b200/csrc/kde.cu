@@ -688,6 +688,7 @@ void with_family(int family, F&& f) {
 }
 
 constexpr uint32_t kLowDMax = 8;
+constexpr uint32_t kTcDirectMax = 8;  // tensor-core levels: direct only for tiny nodes
 uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
 
 }  // namespace
@@ -705,8 +706,9 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const TreeTable& t = ds.tree;
   const float* pts = ds.pts.as<float>();
   const bool lowd = d <= kLowDMax;
-  const bool direct = s_max <= direct_threshold(d);
-  const uint32_t be = lowd ? kBE : kXBM;
+  const bool tc = !lowd && kde_tc_supported(ds, ks.family);
+  const bool direct = s_max <= (tc ? kTcDirectMax : direct_threshold(d));
+  const uint32_t be = lowd ? kBE : (tc ? 128u : uint32_t(kXBM));
 
   // blocks per slot + exact evaluation count of the level
   const uint32_t G = lv.num_slots;
@@ -800,6 +802,8 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     with_lowd(ks.family, d, [&](auto op) {
       op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf);
     });
+  } else if (tc) {
+    kde_tc_tiled(ds, ks, lv, nb, c, items, partials);
   } else {
     with_family(ks.family, [&](auto fam) {
       constexpr int FAM = decltype(fam)::value;

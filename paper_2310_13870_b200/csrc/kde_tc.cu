@@ -1,0 +1,461 @@
+// Tensor-core child sums for high-dimensional data (d >= kTcMinDim):
+// tcgen05.mma kind::tf32 with TMEM accumulators, TMA-fed sources and
+// error-compensated 3xTF32, replacing the CUDA-core kde_xd_tiled_kernel.
+//
+// For a block of 128 entries (queries q_m, gathered) against a source range
+// (x_n, contiguous) the kernel forms S = Q X^T on the tensor cores,
+//   S ~= Qhi Xhi^T + Qhi Xlo^T + Qlo Xhi^T     (hi = tf32(x), lo = tf32(x - hi))
+// which keeps fp32-level accuracy (SURVEY.md §8a': 1.1e-8 vs 4.4e-5 for
+// 1xTF32), then in the epilogue d2 = |q|^2 + |x|^2 - 2 S, arg = -scale * d2
+// (gaussian) or -scale * sqrt(d2) (exponential), one MUFU.EX2 per element and
+// a per-row running sum — the n x n matrix never leaves TMEM/registers.
+//
+// CTA = 8 warps, warp-specialised:
+//   warp 0     TMA producer: source tiles Xhi/Xlo (128 rows x 32 fp32, SW128)
+//   warp 1     TMEM allocator + single-thread MMA issuer
+//   warps 2-3  query gather: cp.async of Qhi/Qlo rows into the SW128 layout
+//   warps 4-7  epilogue: tcgen05.ld of the 128 x 128 fp32 accumulator
+// Pipelines: 3-stage smem ring (full/empty mbarriers), double-buffered TMEM
+// accumulator (tfull/tempty) so the epilogue of N-tile t overlaps the MMAs of
+// N-tile t+1.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "engine.cuh"
+
+namespace fsgg {
+namespace {
+
+constexpr int kTcM = 128;       // entries per work item = TMEM lanes
+constexpr int kTcN = 128;       // sources per N-tile
+constexpr int kTcKB = 32;       // fp32 per K-block: one 128-byte SW128 row
+constexpr int kTcStages = 3;
+constexpr int kTcThreads = 256;
+constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or lo)
+constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
+constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 256;
+constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major, 128-byte-swizzled shared-memory matrix descriptor (sm100 UMMA):
+// start >> 4 [0,14), LBO >> 4 [16,30) (unused for SW128 K-major: 1),
+// SBO >> 4 [32,46) = 1024 B between 8-row groups, version 1 [46,48),
+// layout type SWIZZLE_128B = 2 [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3fff);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128.
+constexpr uint32_t kIdesc = (1u << 4)            // c_format F32
+                            | (2u << 7)          // a_format TF32
+                            | (2u << 10)         // b_format TF32
+                            | (uint32_t(kTcN >> 3) << 17) | (uint32_t(kTcM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// hi = tf32(x) (round to nearest), lo = tf32(x - hi); both stored as fp32
+// bit patterns in row-major n x d_pad arrays (padding columns are 0), plus
+// |x|^2 accumulated in fp64 and rounded once.
+__global__ void tc_split_kernel(const float* __restrict__ pts, uint32_t n, uint32_t d,
+                                uint32_t d_pad, float* __restrict__ hi, float* __restrict__ lo,
+                                float* __restrict__ norm) {
+  const uint32_t row = blockIdx.x;
+  if (row >= n) return;
+  double acc = 0.0;
+  for (uint32_t k = threadIdx.x; k < d_pad; k += blockDim.x) {
+    float h = 0.f, l = 0.f;
+    if (k < d) {
+      const float x = pts[size_t(row) * d + k];
+      uint32_t hb;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+      h = __uint_as_float(hb);
+      uint32_t lb;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(x - h));
+      l = __uint_as_float(lb);
+      acc += double(x) * double(x);
+    }
+    hi[size_t(row) * d_pad + k] = h;
+    lo[size_t(row) * d_pad + k] = l;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) norm[row] = float(red[0]);
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    kde_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
+                  const __grid_constant__ CUtensorMap map_lo, const float* __restrict__ qhi_g,
+                  const float* __restrict__ qlo_g, const float* __restrict__ norm,
+                  uint32_t d_pad, const uint32_t* __restrict__ eq,
+                  const uint32_t* __restrict__ goff, const uint32_t* __restrict__ blk_off,
+                  uint32_t num_slots, uint32_t level, uint32_t cdepth,
+                  const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                  float scale, double* __restrict__ partials) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kStageBytes);
+  uint64_t* full = bars;                   // [kTcStages]
+  uint64_t* empty = bars + kTcStages;      // [kTcStages]
+  uint64_t* tfull = bars + 2 * kTcStages;  // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- work item (same decomposition as the other tiled KDE kernels) ----
+  const uint32_t K = 1u << cdepth;
+  const uint32_t item = blockIdx.x;
+  const uint32_t blk = item >> (cdepth + 1);
+  const uint32_t side = (item >> cdepth) & 1u;
+  const uint32_t kk = item & (K - 1);
+  uint32_t g;
+  {
+    uint32_t lo_ = 0, hi_ = num_slots;
+    while (hi_ - lo_ > 1) {
+      const uint32_t mid = (lo_ + hi_) >> 1;
+      if (blk_off[mid] <= blk) lo_ = mid; else hi_ = mid;
+    }
+    g = lo_;
+  }
+  const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kTcM;
+  const uint32_t e1 = min(e0 + uint32_t(kTcM), goff[g + 1]);
+  const uint32_t lc = level + 1 + cdepth;
+  const uint64_t h = ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
+  const uint32_t cf = tfirst[h], cl = tlast[h];
+  const uint32_t ntiles = (cl - cf + kTcN - 1) / kTcN;
+  const uint32_t kblocks = d_pad / kTcKB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1 + 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t total = ntiles * kblocks;
+
+  if (warp == 0) {
+    // ---- TMA producer: source tiles --------------------------------------
+    if (lane == 0) {
+      for (uint32_t it = 0; it < total; ++it) {
+        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+        const uint32_t tile = it / kblocks, kb = it % kblocks;
+        mbar_wait(&empty[s], ph ^ 1u);
+        unsigned char* st = smem + s * kStageBytes;
+        mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+        const int row = int(cf + tile * kTcN), col = int(kb * kTcKB);
+        tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
+        tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer --------------------------------------------------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t tile = 0; tile < ntiles; ++tile) {
+        const uint32_t buf = tile & 1u;
+        mbar_wait(&tempty[buf], ((tile >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + buf * kTcN;
+        for (uint32_t kb = 0; kb < kblocks; ++kb, ++it) {
+          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + s * kStageBytes);
+#pragma unroll
+          for (int ks = 0; ks < kTcKB / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
+            const uint64_t a_hi = sw128_desc(base + off);
+            const uint64_t a_lo = sw128_desc(base + kTileBytes + off);
+            const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
+            const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
+            mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
+            mma_tf32(tacc, a_hi, b_lo, 1);
+            mma_tf32(tacc, a_lo, b_hi, 1);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp < 4) {
+    // ---- query gather (64 threads): rows t and t + 64 ----------------------
+    const uint32_t t = threadIdx.x - 64;
+    uint32_t qrow[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t e = e0 + t + 64 * r;
+      qrow[r] = eq[e < e1 ? e : e0];
+    }
+    for (uint32_t it = 0; it < total; ++it) {
+      const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+      const uint32_t kb = it % kblocks;
+      mbar_wait(&empty[s], ph ^ 1u);
+      unsigned char* st = smem + s * kStageBytes;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t row = t + 64 * r;
+        const size_t src = size_t(qrow[r]) * d_pad + kb * kTcKB;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t dst = row * 128 + ((c ^ (row & 7)) << 4);
+          cp_async16(st + dst, qhi_g + src + c * 4);
+          cp_async16(st + kTileBytes + dst, qlo_g + src + c * 4);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (it > 0) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full[(it - 1) % kTcStages]);
+      }
+    }
+    if (total > 0) {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[(total - 1) % kTcStages]);
+    }
+  } else {
+    // ---- epilogue (128 threads = TMEM lanes) -------------------------------
+    const uint32_t ew = warp & 3;               // TMEM lane group of this warp
+    const uint32_t row = ew * 32 + lane;        // accumulator row = entry
+    const uint32_t e = e0 + row;
+    const float qn = norm[eq[e < e1 ? e : e0]];
+    double racc = 0.0;
+    for (uint32_t tile = 0; tile < ntiles; ++tile) {
+      const uint32_t buf = tile & 1u;
+      mbar_wait(&tfull[buf], (tile >> 1) & 1u);
+      tc_fence_after();
+      const uint32_t n0 = cf + tile * kTcN;
+      const uint32_t valid = min(uint32_t(kTcN), cl - n0);
+      float acc = 0.f;
+#pragma unroll
+      for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
+        float v[32];
+        tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t col = chunk * 32 + k;
+          const float xn = __ldg(norm + n0 + min(col, valid - 1));
+          float d2 = fmaxf(fmaf(-2.f, v[k], qn + xn), 0.f);
+          if constexpr (FAM == 1) d2 = sqrtf(d2);
+          const float term = ex2_approx(-scale * d2);
+          acc += col < valid ? term : 0.f;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+      racc += acc;
+    }
+    if (e < e1) partials[size_t(e) * (2u * K) + side * K + kk] = racc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ---- host: tensor maps -------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (!fn) throw DeviceError("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad) {
+  const cuuint64_t dims[2] = {d_pad, n};
+  const cuuint64_t strides[1] = {cuuint64_t(d_pad) * 4};
+  const cuuint32_t box[2] = {uint32_t(kTcKB), uint32_t(kTcN)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+struct TcState {
+  uint32_t d_pad = 0;
+  CUtensorMap map_hi, map_lo;
+};
+
+TcState& tc_state(Dataset& ds) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ds.tc_ready) {
+    const uint32_t d_pad = (ds.d + kTcKB - 1) / kTcKB * kTcKB;
+    DevBuf& hi = ds.buf("tc.hi", size_t(ds.n) * d_pad * 4);
+    DevBuf& lo = ds.buf("tc.lo", size_t(ds.n) * d_pad * 4);
+    DevBuf& nrm = ds.buf("tc.norm", size_t(ds.n) * 4);
+    tc_split_kernel<<<ds.n, 256, 0, ds.stream>>>(ds.pts.as<float>(), ds.n, ds.d, d_pad,
+                                                 hi.as<float>(), lo.as<float>(), nrm.as<float>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+    auto* st = reinterpret_cast<TcState*>(ds.tc_blob);
+    st->d_pad = d_pad;
+    make_map(&st->map_hi, hi.as<float>(), ds.n, d_pad);
+    make_map(&st->map_lo, lo.as<float>(), ds.n, d_pad);
+    ds.tc_ready = true;
+  }
+  return *reinterpret_cast<TcState*>(ds.tc_blob);
+}
+
+}  // namespace
+
+static_assert(sizeof(TcState) <= sizeof(Dataset::tc_blob), "tc_blob too small");
+
+bool kde_tc_supported(const Dataset& ds, int family) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("FSGG_TC");
+    return !(e && e[0] == '0');
+  }();
+  return enabled && ds.d >= kTcMinDim && family != 2;
+}
+
+void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
+                  const uint32_t* blk_off, uint32_t cdepth, uint64_t items, double* partials) {
+  TcState& st = tc_state(ds);
+  const TreeTable& t = ds.tree;
+  static bool attr[64] = {};
+  auto kern = ks.family == 1 ? kde_tc_kernel<1> : kde_tc_kernel<0>;
+  if (ds.device < 64 && !attr[ds.device]) {
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemBytes));
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kSmemBytes));
+    attr[ds.device] = true;
+  }
+  kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
+      st.map_hi, st.map_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
+      ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
+      lv.level, cdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials);
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+}
+
+}  // namespace fsgg
