@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   const uint32_t* __restrict__ goff, const uint32_t* __restrict__ blk_off,
                   uint32_t num_slots, uint32_t level, uint32_t cdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
-                  float scale, double* __restrict__ partials) {
+                  float scale, double* __restrict__ partials, int terms) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
             const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
             mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
-            mma_tf32(tacc, a_hi, b_lo, 1);
-            mma_tf32(tacc, a_lo, b_hi, 1);
+            if (terms & 1) mma_tf32(tacc, a_hi, b_lo, 1);
+            if (terms & 2) mma_tf32(tacc, a_lo, b_hi, 1);
           }
           mma_commit(&empty[s]);
         }
@@ -429,6 +429,15 @@ TcState& tc_state(Dataset& ds) {
 
 static_assert(sizeof(TcState) <= sizeof(Dataset::tc_blob), "tc_blob too small");
 
+// FSGG_TC_TERMS (debug): bit 0 = Qhi*Xlo, bit 1 = Qlo*Xhi (default 3 = 3xTF32)
+int tc_terms() {
+  static const int v = [] {
+    const char* e = std::getenv("FSGG_TC_TERMS");
+    return e ? std::atoi(e) : 3;
+  }();
+  return v;
+}
+
 bool kde_tc_supported(const Dataset& ds, int family) {
   static const bool enabled = [] {
     const char* e = std::getenv("FSGG_TC");
@@ -453,7 +462,8 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
-      lv.level, cdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials);
+      lv.level, cdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
+      tc_terms());
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }
