@@ -171,8 +171,11 @@ constexpr uint32_t kTcMinDim = 64;
 bool kde_tc_supported(const Dataset& ds, int family);
 // Same work items / partial layout as the tiled kernels with 128 entries per
 // block; blk_off must have been computed with 128 entries per block.
+// Partials: one per (entry, sub-chunk at depth sdepth below each child),
+// row width 2^(sdepth+1).
 void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
-                  const uint32_t* blk_off, uint32_t cdepth, uint64_t items, double* partials);
+                  const uint32_t* blk_off, uint32_t cdepth, uint32_t sdepth, uint64_t items,
+                  double* partials);
 
 // KdeEstimator::eval seam: arbitrary range, arbitrary targets (device).
 void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,

@@ -689,6 +689,9 @@ void with_family(int family, F&& f) {
 
 constexpr uint32_t kLowDMax = 8;
 constexpr uint32_t kTcDirectMax = 8;  // tensor-core levels: direct only for tiny nodes
+constexpr uint32_t kTcSubMin = 16;    // tensor-core partial buckets: >= 16 sources
+constexpr uint32_t kTcChunkMin = 128; // ... work items: >= one 128-source N-tile
+constexpr uint32_t kTcMaxRowDepth = 7;
 uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
 
 }  // namespace
@@ -779,13 +782,29 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   // are range sums of this row (lookup_sums_kernel, sampler.cu) instead of
   // new kernel evaluations.
   uint32_t c = 0;
-  while (c < sd && (child_min >> (c + 1)) >= (lowd ? sub_min : kChunkMin) &&
-         ((uint64_t(total_blocks) << (c + 1)) < target_items || c + 1 < serve_levels) &&
-         (uint64_t(E) << (c + 2)) <= kMaxPartials)
-    ++c;
-  if (row_depth) *row_depth = c + 1;
+  // rl: log2 of the partial-row width. The CUDA-core kernels write one
+  // partial per work item (rl = c + 1); the tensor-core kernel splits its
+  // columns at sub-chunk boundaries and writes one per sub-chunk (rl = sd + 1).
+  uint32_t rl;
+  if (tc) {
+    sd = 0;
+    while ((child_min >> (sd + 1)) >= kTcSubMin && lv.level + 2 + sd <= t.depth &&
+           sd + 1 < kTcMaxRowDepth && (uint64_t(E) << (sd + 2)) <= kMaxPartials)
+      ++sd;
+    while (c < sd && (child_min >> (c + 1)) >= kTcChunkMin &&
+           (uint64_t(total_blocks) << (c + 1)) < target_items)
+      ++c;
+    rl = sd + 1;
+  } else {
+    while (c < sd && (child_min >> (c + 1)) >= (lowd ? sub_min : kChunkMin) &&
+           ((uint64_t(total_blocks) << (c + 1)) < target_items || c + 1 < serve_levels) &&
+           (uint64_t(E) << (c + 2)) <= kMaxPartials)
+      ++c;
+    rl = c + 1;
+  }
+  if (row_depth) *row_depth = rl;
   const uint32_t K = 1u << c;
-  ws.partials.ensure(size_t(E) * 2 * K * sizeof(double), s);
+  ws.partials.ensure(size_t(E) << rl << 3, s);
   double* partials = ws.partials.as<double>();
   const uint64_t items = uint64_t(total_blocks) * 2 * K;
   if (items > 0x7fffffffull) throw ConfigError("level too large for one launch");
@@ -803,7 +822,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
       op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf);
     });
   } else if (tc) {
-    kde_tc_tiled(ds, ks, lv, nb, c, items, partials);
+    kde_tc_tiled(ds, ks, lv, nb, c, sd, items, partials);
   } else {
     with_family(ks.family, [&](auto fam) {
       constexpr int FAM = decltype(fam)::value;
@@ -816,7 +835,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   FSGG_LAUNCH_CHECK();
   FSGG_CUDA(cudaEventRecord(ws.ev1, s));
   finalize_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
-      partials, K, lv.eg, E, lv.level, t.first.as<uint32_t>(),
+      partials, 1u << (rl - 1), lv.eg, E, lv.level, t.first.as<uint32_t>(),
       t.last.as<uint32_t>(), g1, g2, groot);
   FSGG_LAUNCH_CHECK();
   ds.launches += 2;

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   const float* __restrict__ qlo_g, const float* __restrict__ norm,
                   uint32_t d_pad, const uint32_t* __restrict__ eq,
                   const uint32_t* __restrict__ goff, const uint32_t* __restrict__ blk_off,
-                  uint32_t num_slots, uint32_t level, uint32_t cdepth,
+                  uint32_t num_slots, uint32_t level, uint32_t cdepth, uint32_t sdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
                   float scale, double* __restrict__ partials, int terms) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -345,10 +345,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---- epilogue (128 threads = TMEM lanes) -------------------------------
+    // Columns are split at the sub-chunk boundaries (tree descendants
+    // sdepth levels below the child); one fp64 partial per sub-chunk.
     const uint32_t ew = warp & 3;               // TMEM lane group of this warp
     const uint32_t row = ew * 32 + lane;        // accumulator row = entry
     const uint32_t e = e0 + row;
     const float qn = norm[eq[e < e1 ? e : e0]];
+    const uint32_t nsub = 1u << (sdepth - cdepth);
+    const uint64_t hs = ((1ull << (level + 1 + sdepth)) - 1) +
+                        ((uint64_t(2 * g + side)) << sdepth) + uint64_t(kk) * nsub;
+    double* prow = partials + (size_t(e) << (sdepth + 1)) + (side << sdepth) + kk * nsub;
+    uint32_t b = 0, bend = tlast[hs];
     double racc = 0.0;
     for (uint32_t tile = 0; tile < ntiles; ++tile) {
       const uint32_t buf = tile & 1u;
@@ -364,18 +371,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           const uint32_t col = chunk * 32 + k;
-          const float xn = __ldg(norm + n0 + min(col, valid - 1));
-          float d2 = fmaxf(fmaf(-2.f, v[k], qn + xn), 0.f);
-          if constexpr (FAM == 1) d2 = sqrtf(d2);
-          const float term = ex2_approx(-scale * d2);
-          acc += col < valid ? term : 0.f;
+          if (col < valid) {  // uniform across the warp
+            while (n0 + col >= bend) {  // next sub-chunk (uniform)
+              if (e < e1) prow[b] = racc + acc;
+              racc = 0.0;
+              acc = 0.f;
+              bend = tlast[hs + (++b)];
+            }
+            const float xn = __ldg(norm + n0 + col);
+            float d2 = fmaxf(fmaf(-2.f, v[k], qn + xn), 0.f);
+            if constexpr (FAM == 1) d2 = sqrtf(d2);
+            acc += ex2_approx(-scale * d2);
+          }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[buf]);
       racc += acc;
     }
-    if (e < e1) partials[size_t(e) * (2u * K) + side * K + kk] = racc;
+    if (e < e1) prow[b] = racc;
   }
   tc_fence_before();
   __syncthreads();
@@ -473,7 +487,8 @@ bool kde_tc_supported(const Dataset& ds, int family) {
 }
 
 void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
-                  const uint32_t* blk_off, uint32_t cdepth, uint64_t items, double* partials) {
+                  const uint32_t* blk_off, uint32_t cdepth, uint32_t sdepth, uint64_t items,
+                  double* partials) {
   TcState& st = tc_state(ds);
   const TreeTable& t = ds.tree;
   static bool attr[64] = {};
@@ -488,7 +503,7 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
-      lv.level, cdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
+      lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
       tc_terms());
   FSGG_LAUNCH_CHECK();
   ds.launches++;

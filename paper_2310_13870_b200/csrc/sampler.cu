@@ -250,15 +250,45 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     double s0 = 0.0, s1 = 0.0;
-    for (uint32_t c = 0; c < nsub; ++c) {
-      if (!keep[c]) continue;
-      const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
-      for (uint32_t j = cf + threadIdx.x; j < cl; j += blockDim.x) {
-        const double v = kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
-        if (j < mid)
-          s0 += v;
-        else
-          s1 += v;
+    if (d < 32) {
+      for (uint32_t c = 0; c < nsub; ++c) {
+        if (!keep[c]) continue;
+        const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
+        for (uint32_t j = cf + threadIdx.x; j < cl; j += blockDim.x) {
+          const double v = kernel_f64(family, sigma, xq, pts + size_t(j) * d, d);
+          if (j < mid)
+            s0 += v;
+          else
+            s1 += v;
+        }
+      }
+    } else {
+      // high d: a warp per source, lanes over coordinates (coalesced rows);
+      // the coordinate order of the fp64 distance differs from the
+      // reference's, which moves k by ~1 ulp — far below the 2^-53 grid
+      // the decision is taken on.
+      const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (uint32_t c = 0; c < nsub; ++c) {
+        if (!keep[c]) continue;
+        const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
+        for (uint32_t j = cf + warp; j < cl; j += blockDim.x >> 5) {
+          const float* xj = pts + size_t(j) * d;
+          double part = 0.0;
+          for (uint32_t a = lane; a < d; a += 32) {
+            const double t = double(xq[a]) - double(xj[a]);
+            part = family == 2 ? part + fabs(t) : fma(t, t, part);
+          }
+          for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+          if (lane == 0) {
+            const double v = family == 2   ? exp(-part / sigma)
+                             : family == 1 ? exp(-sqrt(part) / sigma)
+                                           : exp(-part / (sigma * sigma));
+            if (j < mid)
+              s0 += v;
+            else
+              s1 += v;
+          }
+        }
       }
     }
     red[0][threadIdx.x] = s0;
