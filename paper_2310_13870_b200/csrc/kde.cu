@@ -688,7 +688,7 @@ void with_family(int family, F&& f) {
 }
 
 constexpr uint32_t kLowDMax = 8;
-constexpr uint32_t kTcDirectMax = 8;  // tensor-core levels: direct only for tiny nodes
+constexpr uint32_t kTcDirectMax = 24;  // tensor-core levels: direct (warp per entry) for small nodes
 constexpr uint32_t kTcSubMin = 16;    // tensor-core partial buckets: >= 16 sources
 constexpr uint32_t kTcChunkMin = 128; // ... work items: >= one 128-source N-tile
 constexpr uint32_t kTcMaxRowDepth = 7;
