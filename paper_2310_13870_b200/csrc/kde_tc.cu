@@ -37,6 +37,7 @@ constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or
 constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
 constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 256;
 constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
+constexpr uint32_t kTcGroup = 16;                       // entry blocks per L2 group
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -196,7 +197,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   const float* __restrict__ qlo_g, const float* __restrict__ norm,
                   uint32_t d_pad, const uint32_t* __restrict__ eq,
                   const uint32_t* __restrict__ goff, const uint32_t* __restrict__ blk_off,
-                  uint32_t num_slots, uint32_t level, uint32_t cdepth, uint32_t sdepth,
+                  uint32_t num_slots, uint32_t total_blocks, uint32_t level, uint32_t cdepth,
+                  uint32_t sdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
                   float scale, double* __restrict__ partials, int terms) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -211,12 +213,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- work item (same decomposition as the other tiled KDE kernels) ----
+  // ---- work item: (entry block, side, chunk group), visited in groups of
+  // kTcGroup entry blocks x all source groups so the ~148 concurrent CTAs
+  // share their query and source tiles through L2 (the hi/lo copies of C5
+  // are 440 MB; with a block-major order every CTA streams its sources from
+  // DRAM) ----
   const uint32_t K = 1u << cdepth;
-  const uint32_t item = blockIdx.x;
-  const uint32_t blk = item >> (cdepth + 1);
-  const uint32_t side = (item >> cdepth) & 1u;
-  const uint32_t kk = item & (K - 1);
+  const uint32_t cols = 2u * K;
+  uint32_t blk, col;
+  {
+    const uint32_t grp = blockIdx.x / (kTcGroup * cols);
+    const uint32_t r = blockIdx.x - grp * (kTcGroup * cols);
+    const uint32_t gsize = min(uint32_t(kTcGroup), total_blocks - grp * kTcGroup);
+    blk = grp * kTcGroup + r % gsize;
+    col = r / gsize;
+  }
+  const uint32_t side = col >> cdepth;
+  const uint32_t kk = col & (K - 1);
   uint32_t g;
   {
     uint32_t lo_ = 0, hi_ = num_slots;
@@ -503,7 +516,7 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
-      lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
+      static_cast<uint32_t>(items >> (cdepth + 1)), lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
       tc_terms());
   FSGG_LAUNCH_CHECK();
   ds.launches++;
