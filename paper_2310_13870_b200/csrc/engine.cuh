@@ -110,7 +110,7 @@ struct Dataset {
   std::unique_ptr<KdeWorkspace> kde_ws;
   // tensor-core path (kde_tc.cu): split tf32 hi/lo copies + tensor maps
   bool tc_ready = false;
-  alignas(64) unsigned char tc_blob[320];
+  alignas(64) unsigned char tc_blob[576];
   void release_all();
 };
 

@@ -70,6 +70,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA row gather (sm_100a): four rows of a 2-D tensor (box {32 fp32, 1 row})
+// at arbitrary row indices land as four consecutive 128-byte rows at dst,
+// swizzled by their shared-memory address like a regular SW128 tile.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int col, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
@@ -193,7 +205,9 @@ __global__ void tc_split_kernel(const float* __restrict__ pts, uint32_t n, uint3
 template <int FAM>
 __global__ void __launch_bounds__(kTcThreads, 1)
     kde_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
-                  const __grid_constant__ CUtensorMap map_lo, const float* __restrict__ qhi_g,
+                  const __grid_constant__ CUtensorMap map_lo,
+                  const __grid_constant__ CUtensorMap gmap_hi,
+                  const __grid_constant__ CUtensorMap gmap_lo, const float* __restrict__ qhi_g,
                   const float* __restrict__ qlo_g, const float* __restrict__ norm,
                   uint32_t d_pad, const uint32_t* __restrict__ eq,
                   const uint32_t* __restrict__ goff, const uint32_t* __restrict__ blk_off,
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&full[s], 1 + 64);
+      mbar_init(&full[s], 2);  // producer (sources) + gather warp (queries)
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -268,6 +282,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&gmap_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&gmap_lo)) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -288,12 +304,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t tile = it / kblocks, kb = it % kblocks;
         mbar_wait(&empty[s], ph ^ 1u);
         unsigned char* st = smem + s * kStageBytes;
-        mbar_arrive_expect_tx(&full[s], (contig ? 4 : 2) * kTileBytes);
+        mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
         const int row = int(cf + tile * kTcN), col = int(kb * kTcKB);
-        if (contig) {
-          tma_load_2d(st, &map_hi, &full[s], col, int(q0));
-          tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(q0));
-        }
         tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
         tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
       }
@@ -329,45 +341,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp < 4) {
-    // ---- query gather (64 threads): rows t and t + 64 ----------------------
-    const uint32_t t = threadIdx.x - 64;
-    uint32_t qrow[2];
+    // ---- query tiles (warp 2): one TMA box when the block's queries are
+    // consecutive, else TMA gather4 — lane l brings rows 4l..4l+3 ----------
+    if (warp == 2) {
+      int rows[4];
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const uint32_t e = e0 + t + 64 * r;
-      qrow[r] = eq[e < e1 ? e : e0];
-    }
-    for (uint32_t it = 0; it < total; ++it) {
-      const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-      const uint32_t kb = it % kblocks;
-      mbar_wait(&empty[s], ph ^ 1u);
-      if (contig) {  // the producer's TMA brings the query tile
-        mbar_arrive(&full[s]);
-        continue;
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t e = e0 + 4 * lane + j;
+        rows[j] = int(eq[e < e1 ? e : e0]);
       }
-      unsigned char* st = smem + s * kStageBytes;
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t row = t + 64 * r;
-        const size_t src = size_t(qrow[r]) * d_pad + kb * kTcKB;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t dst = row * 128 + ((c ^ (row & 7)) << 4);
-          cp_async16(st + dst, qhi_g + src + c * 4);
-          cp_async16(st + kTileBytes + dst, qlo_g + src + c * 4);
+      for (uint32_t it = 0; it < total; ++it) {
+        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+        const int col = int((it % kblocks) * kTcKB);
+        mbar_wait(&empty[s], ph ^ 1u);
+        unsigned char* st = smem + s * kStageBytes;
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+        __syncwarp();
+        if (contig) {
+          if (lane == 0) {
+            tma_load_2d(st, &map_hi, &full[s], col, int(q0));
+            tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(q0));
+          }
+        } else {
+          tma_gather4(st + lane * 512, &gmap_hi, &full[s], col, rows[0], rows[1], rows[2],
+                      rows[3]);
+          tma_gather4(st + kTileBytes + lane * 512, &gmap_lo, &full[s], col, rows[0], rows[1],
+                      rows[2], rows[3]);
         }
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (it > 0) {
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&full[(it - 1) % kTcStages]);
-      }
-    }
-    if (total > 0 && !contig) {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full[(total - 1) % kTcStages]);
     }
   } else {
     // ---- epilogue (128 threads = TMEM lanes) -------------------------------
@@ -448,10 +449,10 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad) {
+void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad, uint32_t box_rows) {
   const cuuint64_t dims[2] = {d_pad, n};
   const cuuint64_t strides[1] = {cuuint64_t(d_pad) * 4};
-  const cuuint32_t box[2] = {uint32_t(kTcKB), uint32_t(kTcN)};
+  const cuuint32_t box[2] = {uint32_t(kTcKB), box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides,
                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -462,7 +463,8 @@ void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad) {
 
 struct TcState {
   uint32_t d_pad = 0;
-  CUtensorMap map_hi, map_lo;
+  CUtensorMap map_hi, map_lo;    // 128-row boxes (sources, contiguous queries)
+  CUtensorMap gmap_hi, gmap_lo;  // 1-row boxes for tile::gather4
 };
 
 TcState& tc_state(Dataset& ds) {
@@ -484,8 +486,10 @@ TcState& tc_state(Dataset& ds) {
     ds.launches += 2;
     auto* st = reinterpret_cast<TcState*>(ds.tc_blob);
     st->d_pad = d_pad;
-    make_map(&st->map_hi, hi.as<float>(), ds.n, d_pad);
-    make_map(&st->map_lo, lo.as<float>(), ds.n, d_pad);
+    make_map(&st->map_hi, hi.as<float>(), ds.n, d_pad, kTcN);
+    make_map(&st->map_lo, lo.as<float>(), ds.n, d_pad, kTcN);
+    make_map(&st->gmap_hi, hi.as<float>(), ds.n, d_pad, 1);
+    make_map(&st->gmap_lo, lo.as<float>(), ds.n, d_pad, 1);
     ds.tc_ready = true;
   }
   return *reinterpret_cast<TcState*>(ds.tc_blob);
@@ -527,7 +531,7 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     attr[ds.device] = true;
   }
   kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
-      st.map_hi, st.map_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
+      st.map_hi, st.map_lo, st.gmap_hi, st.gmap_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
       static_cast<uint32_t>(items >> (cdepth + 1)), lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
       tc_terms());
