@@ -263,31 +263,45 @@ __global__ void __launch_bounds__(256)
         }
       }
     } else {
-      // high d: a warp per source, lanes over coordinates (coalesced rows);
-      // the coordinate order of the fp64 distance differs from the
-      // reference's, which moves k by ~1 ulp — far below the 2^-53 grid
-      // the decision is taken on.
-      const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      // high d: a thread per source, float4 loads and four independent fp64
+      // accumulators (the per-tie work is a long dot-product stream; the
+      // coordinate order differs from the reference's, which moves k by
+      // ~1 ulp — far below the 2^-53 grid the decision is taken on)
+      const uint32_t d4 = d & ~3u;
       for (uint32_t c = 0; c < nsub; ++c) {
         if (!keep[c]) continue;
         const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
-        for (uint32_t j = cf + warp; j < cl; j += blockDim.x >> 5) {
+        for (uint32_t j = cf + threadIdx.x; j < cl; j += blockDim.x) {
           const float* xj = pts + size_t(j) * d;
-          double part = 0.0;
-          for (uint32_t a = lane; a < d; a += 32) {
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+          const bool al = ((reinterpret_cast<uintptr_t>(xj) | reinterpret_cast<uintptr_t>(xq)) & 15) == 0;
+          uint32_t a = 0;
+          if (al) {
+            for (; a < d4; a += 4) {
+              const float4 u = *reinterpret_cast<const float4*>(xq + a);
+              const float4 v = __ldg(reinterpret_cast<const float4*>(xj + a));
+              const double t0 = double(u.x) - double(v.x), t1 = double(u.y) - double(v.y);
+              const double t2 = double(u.z) - double(v.z), t3 = double(u.w) - double(v.w);
+              if (family == 2) {
+                acc[0] += fabs(t0); acc[1] += fabs(t1); acc[2] += fabs(t2); acc[3] += fabs(t3);
+              } else {
+                acc[0] = fma(t0, t0, acc[0]); acc[1] = fma(t1, t1, acc[1]);
+                acc[2] = fma(t2, t2, acc[2]); acc[3] = fma(t3, t3, acc[3]);
+              }
+            }
+          }
+          for (; a < d; ++a) {
             const double t = double(xq[a]) - double(xj[a]);
-            part = family == 2 ? part + fabs(t) : fma(t, t, part);
+            acc[a & 3] = family == 2 ? acc[a & 3] + fabs(t) : fma(t, t, acc[a & 3]);
           }
-          for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-          if (lane == 0) {
-            const double v = family == 2   ? exp(-part / sigma)
-                             : family == 1 ? exp(-sqrt(part) / sigma)
-                                           : exp(-part / (sigma * sigma));
-            if (j < mid)
-              s0 += v;
-            else
-              s1 += v;
-          }
+          const double part = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+          const double v = family == 2   ? exp(-part / sigma)
+                           : family == 1 ? exp(-sqrt(part) / sigma)
+                                         : exp(-part / (sigma * sigma));
+          if (j < mid)
+            s0 += v;
+          else
+            s1 += v;
         }
       }
     }
