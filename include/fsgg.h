@@ -213,6 +213,24 @@ int fsgg_device_graph_copy(fsgg_dataset* ds, uint32_t* u, uint32_t* v,
 void fsgg_graph_free(fsgg_graph* g);
 void fsgg_free(void* p);
 
+/* Graph files (host-only; no device needed).
+ * Text edge list, byte-identical to fsg::write_edge_list / save_edge_list
+ * (proj/src/graph.cpp:234-241, 265-270): "n m\n" then "u v %.17g\n" per
+ * edge in array order. threads = 0 uses every host core; the bytes do not
+ * depend on it. */
+int fsgg_graph_save_text(const char* path, uint32_t n, uint64_t num_edges,
+                         const uint32_t* u, const uint32_t* v, const double* w,
+                         uint32_t threads);
+/* fsg::read_edge_list / load_edge_list (graph.cpp:243-263, 272-276): swaps
+ * u > v, sorts unsorted input by (u, v), degrees and total weight summed in
+ * the reference's order. Returns FSGG_ERR_IO for unreadable or malformed
+ * files. Free with fsgg_graph_free. */
+int fsgg_graph_load_text(const char* path, uint32_t threads, fsgg_graph* out);
+/* Binary upper-triangular CSR ("FSGGCSR1", n, m, total weight, row_ptr,
+ * v, w, degrees; little-endian): no text conversion either way. */
+int fsgg_graph_save_csr(const char* path, const fsgg_graph* g);
+int fsgg_graph_load_csr(const char* path, fsgg_graph* out);
+
 /* fsg::SampleDiagnostics (proj/include/fsg/sampler.hpp:22-26). */
 typedef struct fsgg_sample_diag {
   uint32_t nlevels;

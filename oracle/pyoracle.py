@@ -145,6 +145,28 @@ class Ref:
         out["report"]["backend"] = name.value.decode()
         return out
 
+    # --- edge-list files (proj/src/graph.cpp:234-276) -----------------------
+    def save_edge_list(self, path, n, u, v, w):
+        u = np.ascontiguousarray(u, np.uint32)
+        v = np.ascontiguousarray(v, np.uint32)
+        w = np.ascontiguousarray(w, np.float64)
+        self._check(self.lib.fsgref_save_edge_list(
+            os.fsencode(path), C.c_uint32(n), C.c_size_t(u.size), u.ctypes.data_as(C.c_void_p),
+            v.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p)))
+
+    def load_edge_list(self, path):
+        n = C.c_uint32()
+        m = C.c_size_t()
+        tot = C.c_double()
+        u, v, w, deg = (C.c_void_p() for _ in range(4))
+        self._check(self.lib.fsgref_load_edge_list(os.fsencode(path), C.byref(n), C.byref(m),
+                                                   C.byref(u), C.byref(v), C.byref(w),
+                                                   C.byref(deg), C.byref(tot)))
+        M = m.value
+        return dict(n=n.value, u=_take(self.lib, u, M, np.uint32),
+                    v=_take(self.lib, v, M, np.uint32), w=_take(self.lib, w, M, np.float64),
+                    degrees=_take(self.lib, deg, n.value, np.float64), total_weight=tot.value)
+
 
 class RefEstimator:
     def __init__(self, ref: Ref, pts, family, sigma, backend, epsilon):

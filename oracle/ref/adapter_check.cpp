@@ -7,17 +7,7 @@
 
 #include "fsg/datasets.hpp"
 #include "fsg/sparsifier.hpp"
-#include "fsg/spectral.hpp"
 #include "fsgg/fsg_adapter.hpp"
-
-namespace fsg {
-EigenResult smallest_eigenpairs(const WeightedGraph&, uint32_t, const EigenOptions&) {
-  throw NumericError("no spectral module");
-}
-ClusterLabels spectral_cluster(const WeightedGraph&, uint32_t, uint64_t, const SpectralOptions&) {
-  throw NumericError("no spectral module");
-}
-}  // namespace fsg
 
 int main() {
   auto data = fsg::make_blobs(2000, {{-2.0, 0.0}, {2.0, 0.0}}, 0.5, 1);

@@ -27,6 +27,7 @@
 
 #include "fsg/common.hpp"
 #include "fsg/dataset.hpp"
+#include "fsg/graph.hpp"
 #include "fsg/datasets.hpp"
 #include "fsg/kde.hpp"
 #include "fsg/kernel.hpp"
@@ -34,19 +35,9 @@
 #include "fsg/sparsifier.hpp"
 #include "fsg/spectral.hpp"
 
-// The spectral module needs Eigen, which is absent from this image
-// (SURVEY.md §8c workaround 3). Only compare_sparsifiers() references these
-// two symbols (proj/src/sparsifier.cpp:214,217); the harness never calls it.
-namespace fsg {
-EigenResult smallest_eigenpairs(const WeightedGraph&, uint32_t,
-                                const EigenOptions&) {
-  throw NumericError("spectral module not built in the oracle harness");
-}
-ClusterLabels spectral_cluster(const WeightedGraph&, uint32_t, uint64_t,
-                               const SpectralOptions&) {
-  throw NumericError("spectral module not built in the oracle harness");
-}
-}  // namespace fsg
+// proj/src/spectral.cpp is compiled in place against oracle/ref/eigen_shim
+// (a stand-in for the absent Eigen headers), so the spectral pipeline below
+// is the reference's own code.
 
 namespace {
 
@@ -350,6 +341,100 @@ int fsgref_build_graph(const double* pts, uint32_t n, uint32_t d, int family,
       std::strncpy(backend_name, rep.backend.c_str(), name_cap - 1);
       backend_name[name_cap - 1] = 0;
     }
+  });
+}
+
+// fsg::save_edge_list on a graph adopted from sorted unique arrays
+// (GraphBuilder::adopt_sorted_unique, proj/src/graph.cpp:40-54).
+int fsgref_save_edge_list(const char* path, uint32_t n, size_t m, const uint32_t* u,
+                          const uint32_t* v, const double* w) {
+  return guarded([&] {
+    std::vector<fsg::Edge> e(m);
+    for (size_t i = 0; i < m; ++i) e[i] = {u[i], v[i], w[i]};
+    fsg::GraphBuilder b(n);
+    b.adopt_sorted_unique(std::move(e));
+    fsg::save_edge_list(path, b.build());
+  });
+}
+
+// fsg::load_edge_list: arrays, degrees and total weight of the read graph.
+int fsgref_load_edge_list(const char* path, uint32_t* n, size_t* m, uint32_t** u,
+                          uint32_t** v, double** w, double** degrees, double* total) {
+  return guarded([&] {
+    fsg::WeightedGraph g = fsg::load_edge_list(path);
+    const auto& e = g.edges();
+    std::vector<uint32_t> uu(e.size()), vv(e.size());
+    std::vector<double> ww(e.size());
+    for (size_t i = 0; i < e.size(); ++i) {
+      uu[i] = e[i].u;
+      vv[i] = e[i].v;
+      ww[i] = e[i].w;
+    }
+    *n = g.num_vertices();
+    *m = e.size();
+    *u = dup_vector(uu);
+    *v = dup_vector(vv);
+    *w = dup_vector(ww);
+    *degrees = dup_vector(g.degrees());
+    *total = g.total_weight();
+  });
+}
+
+namespace {
+fsg::WeightedGraph adopt_graph(uint32_t n, size_t m, const uint32_t* u, const uint32_t* v,
+                               const double* w) {
+  std::vector<fsg::Edge> e(m);
+  for (size_t i = 0; i < m; ++i) e[i] = {u[i], v[i], w[i]};
+  fsg::GraphBuilder b(n);
+  b.adopt_sorted_unique(std::move(e));
+  return b.build();
+}
+}  // namespace
+
+// fsg::smallest_eigenpairs (proj/src/spectral.cpp:40-222). vectors (n*q,
+// column-major) and residuals may be NULL.
+int fsgref_smallest_eigenpairs(uint32_t n, size_t m, const uint32_t* u, const uint32_t* v,
+                               const double* w, uint32_t q, double tol, uint64_t seed,
+                               double* values, double* vectors, double* residuals,
+                               uint64_t* matvecs) {
+  return guarded([&] {
+    fsg::WeightedGraph g = adopt_graph(n, m, u, v, w);
+    fsg::EigenOptions o;
+    o.tol = tol;
+    o.seed = seed;
+    fsg::EigenResult r = fsg::smallest_eigenpairs(g, q, o);
+    std::memcpy(values, r.eigenvalues.data(), q * sizeof(double));
+    if (vectors) std::memcpy(vectors, r.eigenvectors.data(), size_t(n) * q * sizeof(double));
+    if (residuals) std::memcpy(residuals, r.residuals.data(), q * sizeof(double));
+    if (matvecs) *matvecs = r.matvecs;
+  });
+}
+
+// fsg::kmeans (spectral.cpp:257-403) on caller rows (n x dim, row-major).
+int fsgref_kmeans(const double* pts, uint32_t n, uint32_t dim, uint32_t k, uint32_t restarts,
+                  uint32_t max_iters, double rel_tol, uint64_t seed, uint32_t* labels,
+                  double* cost, uint32_t* iterations) {
+  return guarded([&] {
+    fsg::KMeansOptions o;
+    o.restarts = restarts;
+    o.max_iters = max_iters;
+    o.rel_tol = rel_tol;
+    o.seed = seed;
+    fsg::KMeansResult r =
+        fsg::kmeans(std::vector<double>(pts, pts + size_t(n) * dim), n, dim, k, o);
+    std::memcpy(labels, r.labels.labels.data(), size_t(n) * sizeof(uint32_t));
+    if (cost) *cost = r.cost;
+    if (iterations) *iterations = r.iterations;
+  });
+}
+
+// fsg::spectral_cluster (spectral.cpp:405-419) with default options.
+int fsgref_spectral_cluster(uint32_t n, size_t m, const uint32_t* u, const uint32_t* v,
+                            const double* w, uint32_t k, uint64_t seed, uint32_t* labels) {
+  return guarded([&] {
+    fsg::WeightedGraph g = adopt_graph(n, m, u, v, w);
+    fsg::ClusterLabels l = fsg::spectral_cluster(g, k, seed);
+    std::memcpy(labels, l.labels.data(), size_t(n) * sizeof(uint32_t));
   });
 }
 

@@ -7,8 +7,8 @@ package is the host-side mirror of the reference interface over it.
 from .api import (BuildReport, Dataset, Kernel, KernelFamily, KdeEstimator, LogBase,
                   RngMode, SampleDiagnostics, SparsifierConfig, WeightedGraph,
                   build_similarity_graph, build_similarity_graph_device, default_epsilon,
-                  device_available, exact_kde, make_estimator, sample_neighbors,
-                  sample_neighbors_counted)
+                  device_available, exact_kde, load_csr, make_estimator,
+                  read_edge_list, sample_neighbors, sample_neighbors_counted)
 from .errors import (ConfigError, DeviceError, Error, InvalidConfig, IoError,
                      LengthMismatch, NumericError, TooFewPoints)
 
@@ -16,7 +16,7 @@ __all__ = [
     "BuildReport", "Dataset", "Kernel", "KernelFamily", "KdeEstimator", "LogBase", "RngMode",
     "SampleDiagnostics", "SparsifierConfig", "WeightedGraph", "build_similarity_graph",
     "build_similarity_graph_device", "default_epsilon", "device_available", "exact_kde",
-    "make_estimator", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
+    "load_csr", "make_estimator", "read_edge_list", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
     "DeviceError", "Error", "InvalidConfig", "IoError", "LengthMismatch", "NumericError",
     "TooFewPoints",
 ]

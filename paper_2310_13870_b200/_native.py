@@ -118,6 +118,11 @@ _SIGS = {
     "fsgg_device_graph_to_host": (C.c_int, [_P, C.POINTER(fsgg_graph)]),
     "fsgg_device_graph_copy": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "fsgg_free": (None, [_P]),
+    "fsgg_graph_save_text": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint64, _P, _P, _P,
+                                       C.c_uint32]),
+    "fsgg_graph_load_text": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(fsgg_graph)]),
+    "fsgg_graph_save_csr": (C.c_int, [C.c_char_p, C.POINTER(fsgg_graph)]),
+    "fsgg_graph_load_csr": (C.c_int, [C.c_char_p, C.POINTER(fsgg_graph)]),
     "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
                                                 C.c_uint32, C.c_uint64, C.c_int, C.c_int,
                                                 C.POINTER(_P), C.POINTER(C.c_size_t),

@@ -23,6 +23,7 @@ over points or edges.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 import math
 from dataclasses import dataclass, field
@@ -210,12 +211,48 @@ class WeightedGraph:
     def edges(self):
         return list(zip(self.u.tolist(), self.v.tolist(), self.w.tolist()))
 
-    def write_edge_list(self, path: str):
-        """Byte-compatible with proj/src/graph.cpp:234-241 ("n m", "u v %.17g")."""
-        with open(path, "w") as f:
-            f.write(f"{self.n} {self.num_edges()}\n")
-            for a, b, c in zip(self.u.tolist(), self.v.tolist(), self.w.tolist()):
-                f.write(f"{a} {b} {c:.17g}\n")
+    def write_edge_list(self, path: str, threads: int = 0):
+        """fsg::save_edge_list (proj/src/graph.cpp:234-241, 265-270): "n m"
+        then "u v %.17g" per edge, byte-identical to the reference's file."""
+        u = np.ascontiguousarray(self.u, np.uint32)
+        v = np.ascontiguousarray(self.v, np.uint32)
+        w = np.ascontiguousarray(self.w, np.float64)
+        N.check(N.lib().fsgg_graph_save_text(os.fsencode(path), self.n, u.size,
+                                             u.ctypes.data, v.ctypes.data, w.ctypes.data,
+                                             threads))
+
+    def save_csr(self, path: str):
+        """Binary upper-triangular CSR (include/fsgg.h: fsgg_graph_save_csr)."""
+        g = N.fsgg_graph()
+        keep = [np.ascontiguousarray(self.u, np.uint32), np.ascontiguousarray(self.v, np.uint32),
+                np.ascontiguousarray(self.w, np.float64),
+                np.ascontiguousarray(self.row_ptr, np.uint64),
+                np.ascontiguousarray(self.degrees, np.float64)]
+        g.n, g.num_edges, g.total_weight = self.n, keep[0].size, self.total_weight
+        g.u, g.v, g.w, g.row_ptr, g.degrees = (C.cast(a.ctypes.data, f) for a, f in zip(
+            keep, [C.POINTER(C.c_uint32)] * 2 + [C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                                                 C.POINTER(C.c_double)]))
+        N.check(N.lib().fsgg_graph_save_csr(os.fsencode(path), C.byref(g)))
+
+
+def _load_graph(fn, path, *extra) -> WeightedGraph:
+    g = N.fsgg_graph()
+    lib = N.lib()
+    N.check(getattr(lib, fn)(os.fsencode(path), *extra, C.byref(g)))
+    try:
+        return _graph_from_c(g)
+    finally:
+        lib.fsgg_graph_free(C.byref(g))
+
+
+def read_edge_list(path: str, threads: int = 0) -> WeightedGraph:
+    """fsg::load_edge_list (proj/src/graph.cpp:243-263, 272-276)."""
+    return _load_graph("fsgg_graph_load_text", path, threads)
+
+
+def load_csr(path: str) -> WeightedGraph:
+    """Inverse of WeightedGraph.save_csr."""
+    return _load_graph("fsgg_graph_load_csr", path)
 
 
 @dataclass

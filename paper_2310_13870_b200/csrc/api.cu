@@ -16,6 +16,15 @@
 #include "../../include/fsgg.h"
 #include "engine.cuh"
 
+namespace fsgg {
+// graph_io.cpp
+void graph_save_text(const char* path, uint32_t n, uint64_t m, const uint32_t* u,
+                     const uint32_t* v, const double* w, uint32_t threads);
+void graph_load_text(const char* path, uint32_t threads, fsgg_graph* g);
+void graph_save_csr(const char* path, const fsgg_graph* g);
+void graph_load_csr(const char* path, fsgg_graph* g);
+}  // namespace fsgg
+
 struct fsgg_dataset {
   fsgg::Dataset ds;
   // Results kept alive for the device-pointer APIs; reused (grow-only)
@@ -458,6 +467,23 @@ void fsgg_graph_free(fsgg_graph* g) {
 }
 
 void fsgg_free(void* p) { std::free(p); }
+
+int fsgg_graph_save_text(const char* path, uint32_t n, uint64_t num_edges, const uint32_t* u,
+                         const uint32_t* v, const double* w, uint32_t threads) {
+  return guarded([&] { fsgg::graph_save_text(path, n, num_edges, u, v, w, threads); });
+}
+
+int fsgg_graph_load_text(const char* path, uint32_t threads, fsgg_graph* out) {
+  return guarded([&] { fsgg::graph_load_text(path, threads, out); });
+}
+
+int fsgg_graph_save_csr(const char* path, const fsgg_graph* g) {
+  return guarded([&] { fsgg::graph_save_csr(path, g); });
+}
+
+int fsgg_graph_load_csr(const char* path, fsgg_graph* out) {
+  return guarded([&] { fsgg::graph_load_csr(path, out); });
+}
 
 int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
                                   const uint32_t* queries, size_t num_queries,

@@ -143,7 +143,8 @@ __device__ __forceinline__ void lowd_range_sum(
 // mass is < 2^-60 of the node mass: routing compares u < p on a 2^-53 grid,
 // so decisions are unchanged (the fp32 evaluation itself perturbs p ~2^40
 // times more). The whole CTA skips when all its entries agree; a warp skips
-// the arithmetic when all of its entries do.
+// the arithmetic when all of its entries do; a pruned sub-chunk is dropped
+// from an entry's sum whether or not its CTA evaluated it.
 template <int D, int FAM>
 __global__ void __launch_bounds__(kThreads)
     kde_lowd_tiled_kernel(const float* __restrict__ pts,
@@ -203,18 +204,23 @@ __global__ void __launch_bounds__(kThreads)
       offA = scale * box_dist<FAM>(qa_c, tlo + h * D, thi + h * D, D);
       offB = scale * box_dist<FAM>(qb_c, tlo + h * D, thi + h * D, D);
     }
-    bool skip = false;
+    bool skipA = false, skipB = false;
     if (prune) {
       const float lim = __log2f(float(cl - cf)) + kPruneBits;
-      skip = (!va || offA > lim - lbA) && (!vb || offB > lim - lbB);
+      skipA = !va || offA > lim - lbA;
+      skipB = !vb || offB > lim - lbB;
     }
+    const bool skip = skipA && skipB;
     if (__syncthreads_and(skip)) continue;
     const bool wskip = __all_sync(0xffffffffu, skip);
     double sA = 0.0, sB = 0.0;
     lowd_range_sum<D, FAM>(pts, sm, q2, make_float2(offA, offB), scale, cf, cl, sA, sB,
                            wskip);
-    accA += rescale(sA, offA);
-    accB += rescale(sB, offB);
+    // A pruned sub-chunk contributes nothing to that entry even when its CTA
+    // evaluates it for others: each sum depends on (node, query) alone, never
+    // on which entries share the CTA (so sharded and unsharded runs agree).
+    if (!skipA) accA += rescale(sA, offA);
+    if (!skipB) accB += rescale(sB, offB);
     if (!wskip) done += uint64_t(cl - cf) * nvalid_warp;
   }
   const uint32_t stride = 2u * K, col = side * K + kk;
