@@ -213,6 +213,60 @@ int fsgg_device_graph_copy(fsgg_dataset* ds, uint32_t* u, uint32_t* v,
 void fsgg_graph_free(fsgg_graph* g);
 void fsgg_free(void* p);
 
+/* Spectral clustering on the graph (proj/include/fsg/spectral.hpp), the
+ * consumer of the similarity graph, run on the device. */
+typedef struct fsgg_eigen_options { /* spectral.hpp:11-16 */
+  double tol;           /* 1e-6 */
+  uint64_t max_matvecs; /* 0 = 50 n + 1000 */
+  uint32_t max_basis;   /* 0 = auto */
+  uint64_t seed;        /* 7 */
+} fsgg_eigen_options;
+typedef struct fsgg_kmeans_options { /* spectral.hpp:44-49 */
+  uint32_t restarts;  /* 10 */
+  uint32_t max_iters; /* 300 */
+  double rel_tol;     /* 1e-8 */
+  uint64_t seed;      /* 7 */
+} fsgg_kmeans_options;
+typedef struct fsgg_spectral_options {
+  fsgg_eigen_options eigen;
+  fsgg_kmeans_options kmeans;
+} fsgg_spectral_options;
+typedef struct fsgg_spectral_report {
+  uint64_t matvecs;
+  uint32_t components;
+  uint32_t kmeans_iterations;
+  double kmeans_cost;
+  double eigen_seconds;
+  double kmeans_seconds;
+  uint64_t gpu_launches;
+} fsgg_spectral_report;
+void fsgg_spectral_options_init(fsgg_spectral_options* opts);
+
+/* fsg::smallest_eigenpairs (spectral.cpp:40-222) of the normalised Laplacian
+ * of the handle's current device graph (last build on `ds`): q eigenvalues
+ * ascending; vectors (n x q column-major) and residuals may be NULL.
+ * Isolated vertex -> FSGG_ERR_CONFIG; no convergence -> FSGG_ERR_NUMERIC. */
+int fsgg_smallest_eigenpairs(fsgg_dataset* ds, uint32_t q, const fsgg_eigen_options* opts,
+                             double* values, double* vectors, double* residuals,
+                             uint64_t* matvecs);
+/* fsg::spectral_cluster (spectral.cpp:405-419) on the handle's device graph;
+ * labels: n entries in [0, k). opts may be NULL (reference defaults). */
+int fsgg_spectral_cluster(fsgg_dataset* ds, uint32_t k, uint64_t seed,
+                          const fsgg_spectral_options* opts, uint32_t* labels,
+                          fsgg_spectral_report* report);
+/* Same for a host graph (e.g. from fsgg_graph_load_text), uploaded to
+ * `device` for the call. */
+int fsgg_spectral_cluster_graph(const fsgg_graph* g, int device, uint32_t k, uint64_t seed,
+                                const fsgg_spectral_options* opts, uint32_t* labels,
+                                fsgg_spectral_report* report);
+int fsgg_smallest_eigenpairs_graph(const fsgg_graph* g, int device, uint32_t q,
+                                   const fsgg_eigen_options* opts, double* values,
+                                   double* vectors, double* residuals, uint64_t* matvecs);
+/* fsg::kmeans (spectral.cpp:257-403) on host rows (n x dim, row-major). */
+int fsgg_kmeans(const double* points, uint32_t n, uint32_t dim, uint32_t k,
+                const fsgg_kmeans_options* opts, int device, uint32_t* labels,
+                double* cost, uint32_t* iterations);
+
 /* Graph files (host-only; no device needed).
  * Text edge list, byte-identical to fsg::write_edge_list / save_edge_list
  * (proj/src/graph.cpp:234-241, 265-270): "n m\n" then "u v %.17g\n" per

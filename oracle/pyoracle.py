@@ -145,6 +145,49 @@ class Ref:
         out["report"]["backend"] = name.value.decode()
         return out
 
+    # --- spectral module (proj/src/spectral.cpp, built on ref/eigen_shim) ----
+    @staticmethod
+    def _graph_args(u, v, w):
+        u = np.ascontiguousarray(u, np.uint32)
+        v = np.ascontiguousarray(v, np.uint32)
+        w = np.ascontiguousarray(w, np.float64)
+        return (u, v, w), (C.c_size_t(u.size), u.ctypes.data_as(C.c_void_p),
+                           v.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p))
+
+    def smallest_eigenpairs(self, n, u, v, w, q, tol=1e-6, seed=7, vectors=True):
+        keep, args = self._graph_args(u, v, w)
+        vals = np.zeros(q)
+        res = np.zeros(q)
+        vecs = np.zeros((q, n)) if vectors else None
+        mv = C.c_uint64()
+        self._check(self.lib.fsgref_smallest_eigenpairs(
+            C.c_uint32(n), *args, C.c_uint32(q), C.c_double(tol), C.c_uint64(seed),
+            vals.ctypes.data_as(C.c_void_p),
+            vecs.ctypes.data_as(C.c_void_p) if vectors else None,
+            res.ctypes.data_as(C.c_void_p), C.byref(mv)))
+        return dict(eigenvalues=vals, eigenvectors=vecs, residuals=res, matvecs=mv.value)
+
+    def spectral_cluster(self, n, u, v, w, k, seed=7):
+        keep, args = self._graph_args(u, v, w)
+        lab = np.zeros(n, np.uint32)
+        self._check(self.lib.fsgref_spectral_cluster(C.c_uint32(n), *args, C.c_uint32(k),
+                                                     C.c_uint64(seed),
+                                                     lab.ctypes.data_as(C.c_void_p)))
+        return lab
+
+    def kmeans(self, pts, k, restarts=10, max_iters=300, rel_tol=1e-8, seed=7):
+        pts = np.ascontiguousarray(pts, np.float64)
+        n, dim = pts.shape
+        lab = np.zeros(n, np.uint32)
+        cost = C.c_double()
+        iters = C.c_uint32()
+        self._check(self.lib.fsgref_kmeans(pts.ctypes.data_as(C.c_void_p), C.c_uint32(n),
+                                           C.c_uint32(dim), C.c_uint32(k), C.c_uint32(restarts),
+                                           C.c_uint32(max_iters), C.c_double(rel_tol),
+                                           C.c_uint64(seed), lab.ctypes.data_as(C.c_void_p),
+                                           C.byref(cost), C.byref(iters)))
+        return lab, cost.value, iters.value
+
     # --- edge-list files (proj/src/graph.cpp:234-276) -----------------------
     def save_edge_list(self, path, n, u, v, w):
         u = np.ascontiguousarray(u, np.uint32)

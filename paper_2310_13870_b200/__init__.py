@@ -4,15 +4,18 @@ Drop-in for the reference's ``fsg::build_similarity_graph`` path: the C ABI
 is ``include/fsgg.h`` (libfsgg.so, hand-written sm_100a kernels); this
 package is the host-side mirror of the reference interface over it.
 """
-from .api import (BuildReport, Dataset, Kernel, KernelFamily, KdeEstimator, LogBase,
+from .api import (BuildReport, Dataset, EigenOptions, EigenResult, KMeansOptions,
+                  SpectralOptions, kmeans, smallest_eigenpairs, spectral_cluster, Kernel, KernelFamily, KdeEstimator, LogBase,
                   RngMode, SampleDiagnostics, SparsifierConfig, WeightedGraph,
                   build_similarity_graph, build_similarity_graph_device, default_epsilon,
-                  device_available, exact_kde, load_csr, make_estimator,
+                  device_available, device_graph_to_host, exact_kde, load_csr, make_estimator,
                   read_edge_list, sample_neighbors, sample_neighbors_counted)
 from .errors import (ConfigError, DeviceError, Error, InvalidConfig, IoError,
                      LengthMismatch, NumericError, TooFewPoints)
 
 __all__ = [
+    "EigenOptions", "EigenResult", "KMeansOptions", "SpectralOptions", "kmeans",
+    "smallest_eigenpairs", "spectral_cluster", "device_graph_to_host",
     "BuildReport", "Dataset", "Kernel", "KernelFamily", "KdeEstimator", "LogBase", "RngMode",
     "SampleDiagnostics", "SparsifierConfig", "WeightedGraph", "build_similarity_graph",
     "build_similarity_graph_device", "default_epsilon", "device_available", "exact_kde",

@@ -64,6 +64,27 @@ class fsgg_graph(C.Structure):
                 ("degrees", C.POINTER(C.c_double)), ("total_weight", C.c_double)]
 
 
+class fsgg_eigen_options(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_matvecs", C.c_uint64), ("max_basis", C.c_uint32),
+                ("seed", C.c_uint64)]
+
+
+class fsgg_kmeans_options(C.Structure):
+    _fields_ = [("restarts", C.c_uint32), ("max_iters", C.c_uint32), ("rel_tol", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+class fsgg_spectral_options(C.Structure):
+    _fields_ = [("eigen", fsgg_eigen_options), ("kmeans", fsgg_kmeans_options)]
+
+
+class fsgg_spectral_report(C.Structure):
+    _fields_ = [("matvecs", C.c_uint64), ("components", C.c_uint32),
+                ("kmeans_iterations", C.c_uint32), ("kmeans_cost", C.c_double),
+                ("eigen_seconds", C.c_double), ("kmeans_seconds", C.c_double),
+                ("gpu_launches", C.c_uint64)]
+
+
 class fsgg_device_graph(C.Structure):
     _fields_ = [("n", C.c_uint32), ("num_edges", C.c_uint64), ("u", C.c_void_p),
                 ("v", C.c_void_p), ("w", C.c_void_p), ("row_ptr", C.c_void_p),
@@ -118,6 +139,21 @@ _SIGS = {
     "fsgg_device_graph_to_host": (C.c_int, [_P, C.POINTER(fsgg_graph)]),
     "fsgg_device_graph_copy": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "fsgg_free": (None, [_P]),
+    "fsgg_spectral_options_init": (None, [C.POINTER(fsgg_spectral_options)]),
+    "fsgg_smallest_eigenpairs": (C.c_int, [_P, C.c_uint32, C.POINTER(fsgg_eigen_options), _P, _P,
+                                           _P, C.POINTER(C.c_uint64)]),
+    "fsgg_spectral_cluster": (C.c_int, [_P, C.c_uint32, C.c_uint64,
+                                        C.POINTER(fsgg_spectral_options), _P,
+                                        C.POINTER(fsgg_spectral_report)]),
+    "fsgg_spectral_cluster_graph": (C.c_int, [C.POINTER(fsgg_graph), C.c_int, C.c_uint32,
+                                              C.c_uint64, C.POINTER(fsgg_spectral_options), _P,
+                                              C.POINTER(fsgg_spectral_report)]),
+    "fsgg_smallest_eigenpairs_graph": (C.c_int, [C.POINTER(fsgg_graph), C.c_int, C.c_uint32,
+                                                 C.POINTER(fsgg_eigen_options), _P, _P, _P,
+                                                 C.POINTER(C.c_uint64)]),
+    "fsgg_kmeans": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32,
+                              C.POINTER(fsgg_kmeans_options), C.c_int, _P,
+                              C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
     "fsgg_graph_save_text": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint64, _P, _P, _P,
                                        C.c_uint32]),
     "fsgg_graph_load_text": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(fsgg_graph)]),

@@ -221,8 +221,8 @@ class WeightedGraph:
                                              u.ctypes.data, v.ctypes.data, w.ctypes.data,
                                              threads))
 
-    def save_csr(self, path: str):
-        """Binary upper-triangular CSR (include/fsgg.h: fsgg_graph_save_csr)."""
+    def _c(self):
+        """fsgg_graph view of this graph's arrays (and the arrays keeping it alive)."""
         g = N.fsgg_graph()
         keep = [np.ascontiguousarray(self.u, np.uint32), np.ascontiguousarray(self.v, np.uint32),
                 np.ascontiguousarray(self.w, np.float64),
@@ -232,6 +232,11 @@ class WeightedGraph:
         g.u, g.v, g.w, g.row_ptr, g.degrees = (C.cast(a.ctypes.data, f) for a, f in zip(
             keep, [C.POINTER(C.c_uint32)] * 2 + [C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                                                  C.POINTER(C.c_double)]))
+        return g, keep
+
+    def save_csr(self, path: str):
+        """Binary upper-triangular CSR (include/fsgg.h: fsgg_graph_save_csr)."""
+        g, _keep = self._c()
         N.check(N.lib().fsgg_graph_save_csr(os.fsencode(path), C.byref(g)))
 
 
@@ -504,3 +509,110 @@ def device_available() -> bool:
 def _ensure_two_points(n):
     if n < 2:
         raise TooFewPoints("similarity graph needs n >= 2")
+
+
+# ---- spectral clustering (proj/include/fsg/spectral.hpp) on the device ----
+
+@dataclass
+class EigenOptions:
+    """proj/include/fsg/spectral.hpp:11-16"""
+    tol: float = 1e-6
+    max_matvecs: int = 0
+    max_basis: int = 0
+    seed: int = 7
+
+    def _c(self):
+        return N.fsgg_eigen_options(self.tol, self.max_matvecs, self.max_basis, self.seed)
+
+
+@dataclass
+class KMeansOptions:
+    """proj/include/fsg/spectral.hpp:44-49"""
+    restarts: int = 10
+    max_iters: int = 300
+    rel_tol: float = 1e-8
+    seed: int = 7
+
+    def _c(self):
+        return N.fsgg_kmeans_options(self.restarts, self.max_iters, self.rel_tol, self.seed)
+
+
+@dataclass
+class SpectralOptions:
+    eigen: EigenOptions = field(default_factory=EigenOptions)
+    kmeans: KMeansOptions = field(default_factory=KMeansOptions)
+
+    def _c(self):
+        return N.fsgg_spectral_options(self.eigen._c(), self.kmeans._c())
+
+
+@dataclass
+class EigenResult:
+    """fsg::EigenResult: eigenvalues ascending; eigenvectors[i] is pair i."""
+    eigenvalues: np.ndarray
+    eigenvectors: np.ndarray | None
+    residuals: np.ndarray
+    matvecs: int
+
+
+def smallest_eigenpairs(graph, q: int, options: EigenOptions | None = None,
+                        vectors: bool = True, device: int = 0) -> EigenResult:
+    """fsg::smallest_eigenpairs (proj/src/spectral.cpp:40-222) of the
+    normalised Laplacian, on the device. ``graph`` is a Dataset (its last
+    device-built graph) or a WeightedGraph (uploaded for the call)."""
+    opts = (options or EigenOptions())._c()
+    vals = np.zeros(q)
+    res = np.zeros(q)
+    mv = C.c_uint64()
+    lib = N.lib()
+    if isinstance(graph, Dataset):
+        n = graph.n
+        vecs = np.zeros((q, n)) if vectors else None
+        N.check(lib.fsgg_smallest_eigenpairs(graph._h, q, C.byref(opts), vals.ctypes.data,
+                                             vecs.ctypes.data if vectors else None,
+                                             res.ctypes.data, C.byref(mv)))
+    else:
+        g, keep = graph._c()
+        vecs = np.zeros((q, graph.n)) if vectors else None
+        N.check(lib.fsgg_smallest_eigenpairs_graph(C.byref(g), device, q, C.byref(opts),
+                                                   vals.ctypes.data,
+                                                   vecs.ctypes.data if vectors else None,
+                                                   res.ctypes.data, C.byref(mv)))
+    return EigenResult(vals, vecs, res, int(mv.value))
+
+
+def spectral_cluster(graph, k: int, seed: int = 7, options: SpectralOptions | None = None,
+                     device: int = 0, report: bool = False):
+    """fsg::spectral_cluster (proj/src/spectral.cpp:405-419) on the device:
+    labels (uint32, n) in [0, k); with report=True also a dict of counters."""
+    opts = (options or SpectralOptions())._c()
+    rep = N.fsgg_spectral_report()
+    lib = N.lib()
+    if isinstance(graph, Dataset):
+        labels = np.zeros(graph.n, np.uint32)
+        N.check(lib.fsgg_spectral_cluster(graph._h, k, seed, C.byref(opts), labels.ctypes.data,
+                                          C.byref(rep)))
+    else:
+        g, keep = graph._c()
+        labels = np.zeros(graph.n, np.uint32)
+        N.check(lib.fsgg_spectral_cluster_graph(C.byref(g), device, k, seed, C.byref(opts),
+                                                labels.ctypes.data, C.byref(rep)))
+    if report:
+        return labels, {f: getattr(rep, f) for f, _ in rep._fields_}
+    return labels
+
+
+def kmeans(points, k: int, options: KMeansOptions | None = None, device: int = 0):
+    """fsg::kmeans (proj/src/spectral.cpp:257-403) on the device:
+    (labels, cost, iterations) of the best restart."""
+    pts = np.ascontiguousarray(points, np.float64)
+    if pts.ndim != 2:
+        raise ValueError("points must be n x dim")
+    n, dim = pts.shape
+    labels = np.zeros(n, np.uint32)
+    cost = C.c_double()
+    iters = C.c_uint32()
+    opts = (options or KMeansOptions())._c()
+    N.check(N.lib().fsgg_kmeans(pts.ctypes.data, n, dim, k, C.byref(opts), device,
+                                labels.ctypes.data, C.byref(cost), C.byref(iters)))
+    return labels, float(cost.value), int(iters.value)

@@ -15,6 +15,7 @@
 
 #include "../../include/fsgg.h"
 #include "engine.cuh"
+#include "spectral.cuh"
 
 namespace fsgg {
 // graph_io.cpp
@@ -302,6 +303,123 @@ void to_device_graph(fsgg_dataset* h, fsgg_device_graph* out) {
   out->total_weight = g.total_weight;
 }
 
+fsgg::SpectralGraphView handle_graph_view(fsgg_dataset* h) {
+  if (!h) throw fsgg::ConfigError("dataset handle is null");
+  if (!h->graph) throw fsgg::ConfigError("no graph on this handle: build one first");
+  const fsgg::GraphResult& g = *h->graph;
+  FSGG_CUDA(cudaSetDevice(h->ds.device));
+  fsgg::SpectralGraphView v;
+  v.n = g.n;
+  v.m = g.m;
+  v.row_ptr = g.row_ptr.as<uint64_t>();
+  v.col = g.v.as<uint32_t>();
+  v.w = g.w.as<double>();
+  v.degrees = g.degrees.as<double>();
+  return v;
+}
+
+// A host graph uploaded for one call, on its own stream.
+struct UploadedGraph {
+  cudaStream_t s = nullptr;
+  fsgg::DevBuf rp, col, w, deg;
+  fsgg::SpectralGraphView view;
+  UploadedGraph(const fsgg_graph* g, int device) {
+    if (!g) throw fsgg::ConfigError("graph is null");
+    if (g->n == 0) throw fsgg::ConfigError("graph needs at least one vertex");
+    if (!g->row_ptr || !g->degrees || (g->num_edges && (!g->v || !g->w)))
+      throw fsgg::ConfigError("graph needs v, w, row_ptr and degrees");
+    require_device(device);
+    FSGG_CUDA(cudaSetDevice(device));
+    FSGG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const uint64_t m = g->num_edges;
+    rp.alloc(size_t(g->n + 1) * 8, s);
+    col.alloc(std::max<uint64_t>(m, 1) * 4, s);
+    w.alloc(std::max<uint64_t>(m, 1) * 8, s);
+    deg.alloc(size_t(g->n) * 8, s);
+    FSGG_CUDA(cudaMemcpyAsync(rp.as<void>(), g->row_ptr, size_t(g->n + 1) * 8,
+                              cudaMemcpyHostToDevice, s));
+    if (m) {
+      FSGG_CUDA(cudaMemcpyAsync(col.as<void>(), g->v, m * 4, cudaMemcpyHostToDevice, s));
+      FSGG_CUDA(cudaMemcpyAsync(w.as<void>(), g->w, m * 8, cudaMemcpyHostToDevice, s));
+    }
+    FSGG_CUDA(cudaMemcpyAsync(deg.as<void>(), g->degrees, size_t(g->n) * 8,
+                              cudaMemcpyHostToDevice, s));
+    view.n = g->n;
+    view.m = m;
+    view.row_ptr = rp.as<uint64_t>();
+    view.col = col.as<uint32_t>();
+    view.w = w.as<double>();
+    view.degrees = deg.as<double>();
+  }
+  ~UploadedGraph() {
+    rp.release();
+    col.release();
+    w.release();
+    deg.release();
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+fsgg::EigenOpts eigen_opts(const fsgg_eigen_options* o) {
+  fsgg::EigenOpts e;
+  if (o) {
+    e.tol = o->tol;
+    e.max_matvecs = o->max_matvecs;
+    e.max_basis = o->max_basis;
+    e.seed = o->seed;
+  }
+  return e;
+}
+
+fsgg::KmeansOpts kmeans_opts(const fsgg_kmeans_options* o) {
+  fsgg::KmeansOpts k;
+  if (o) {
+    k.restarts = o->restarts;
+    k.max_iters = o->max_iters;
+    k.rel_tol = o->rel_tol;
+    k.seed = o->seed;
+  }
+  return k;
+}
+
+void eigenpairs_out(const fsgg::SpectralGraphView& v, cudaStream_t s, uint32_t q,
+                    const fsgg_eigen_options* opts, double* values, double* vectors,
+                    double* residuals, uint64_t* matvecs) {
+  if (!values) throw fsgg::ConfigError("values is null");
+  std::vector<double> vals, res;
+  fsgg::DevBuf vecs;
+  fsgg::SpectralStats st;
+  fsgg::smallest_eigenpairs_dev(v, s, q, eigen_opts(opts), vals, res, vecs, st);
+  std::memcpy(values, vals.data(), q * sizeof(double));
+  if (residuals) std::memcpy(residuals, res.data(), q * sizeof(double));
+  if (vectors)
+    FSGG_CUDA(cudaMemcpyAsync(vectors, vecs.as<void>(), size_t(v.n) * q * 8,
+                              cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  if (matvecs) *matvecs = st.matvecs;
+}
+
+void spectral_out(const fsgg::SpectralGraphView& v, cudaStream_t s, uint32_t k, uint64_t seed,
+                  const fsgg_spectral_options* opts, uint32_t* labels,
+                  fsgg_spectral_report* rep) {
+  if (!labels) throw fsgg::ConfigError("labels is null");
+  fsgg::SpectralStats st;
+  fsgg::spectral_cluster_dev(v, s, k, seed, eigen_opts(opts ? &opts->eigen : nullptr),
+                             kmeans_opts(opts ? &opts->kmeans : nullptr), labels, nullptr, st);
+  if (rep) {
+    rep->matvecs = st.matvecs;
+    rep->components = st.ncomp;
+    rep->kmeans_iterations = st.kmeans_iterations;
+    rep->kmeans_cost = st.kmeans_cost;
+    rep->eigen_seconds = st.eigen_seconds;
+    rep->kmeans_seconds = st.kmeans_seconds;
+    rep->gpu_launches = st.launches;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -467,6 +585,83 @@ void fsgg_graph_free(fsgg_graph* g) {
 }
 
 void fsgg_free(void* p) { std::free(p); }
+
+void fsgg_spectral_options_init(fsgg_spectral_options* o) {
+  if (!o) return;
+  const fsgg::EigenOpts e;
+  const fsgg::KmeansOpts k;
+  o->eigen.tol = e.tol;
+  o->eigen.max_matvecs = e.max_matvecs;
+  o->eigen.max_basis = e.max_basis;
+  o->eigen.seed = e.seed;
+  o->kmeans.restarts = k.restarts;
+  o->kmeans.max_iters = k.max_iters;
+  o->kmeans.rel_tol = k.rel_tol;
+  o->kmeans.seed = k.seed;
+}
+
+int fsgg_smallest_eigenpairs(fsgg_dataset* h, uint32_t q, const fsgg_eigen_options* opts,
+                             double* values, double* vectors, double* residuals,
+                             uint64_t* matvecs) {
+  return guarded([&] {
+    const fsgg::SpectralGraphView v = handle_graph_view(h);
+    eigenpairs_out(v, h->ds.stream, q, opts, values, vectors, residuals, matvecs);
+  });
+}
+
+int fsgg_spectral_cluster(fsgg_dataset* h, uint32_t k, uint64_t seed,
+                          const fsgg_spectral_options* opts, uint32_t* labels,
+                          fsgg_spectral_report* report) {
+  return guarded([&] {
+    const fsgg::SpectralGraphView v = handle_graph_view(h);
+    spectral_out(v, h->ds.stream, k, seed, opts, labels, report);
+  });
+}
+
+int fsgg_spectral_cluster_graph(const fsgg_graph* g, int device, uint32_t k, uint64_t seed,
+                                const fsgg_spectral_options* opts, uint32_t* labels,
+                                fsgg_spectral_report* report) {
+  return guarded([&] {
+    UploadedGraph up(g, device);
+    spectral_out(up.view, up.s, k, seed, opts, labels, report);
+  });
+}
+
+int fsgg_smallest_eigenpairs_graph(const fsgg_graph* g, int device, uint32_t q,
+                                   const fsgg_eigen_options* opts, double* values,
+                                   double* vectors, double* residuals, uint64_t* matvecs) {
+  return guarded([&] {
+    UploadedGraph up(g, device);
+    eigenpairs_out(up.view, up.s, q, opts, values, vectors, residuals, matvecs);
+  });
+}
+
+int fsgg_kmeans(const double* points, uint32_t n, uint32_t dim, uint32_t k,
+                const fsgg_kmeans_options* opts, int device, uint32_t* labels, double* cost,
+                uint32_t* iterations) {
+  return guarded([&] {
+    if (!points || !labels) throw fsgg::ConfigError("null argument");
+    if (n == 0 || dim == 0) throw fsgg::ConfigError("empty k-means input");
+    require_device(device);
+    FSGG_CUDA(cudaSetDevice(device));
+    cudaStream_t s = nullptr;
+    FSGG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } guard{s};
+    fsgg::DevBuf pts(size_t(n) * dim * 8, s);
+    FSGG_CUDA(cudaMemcpyAsync(pts.as<void>(), points, size_t(n) * dim * 8,
+                              cudaMemcpyHostToDevice, s));
+    fsgg::SpectralStats st;
+    fsgg::kmeans_dev(pts.as<double>(), n, dim, k, kmeans_opts(opts), s, labels, cost,
+                     iterations, st);
+    pts.release();
+  });
+}
 
 int fsgg_graph_save_text(const char* path, uint32_t n, uint64_t num_edges, const uint32_t* u,
                          const uint32_t* v, const double* w, uint32_t threads) {

@@ -158,3 +158,27 @@ def test_oracle_rejects_invalid(oracle):
         oracle.kde_exact(p, 4, 2, [0], 1.0)
     with pytest.raises(OracleError):
         oracle.build_graph(p[:1], 1.0, 4)
+
+
+def test_reference_spectral_module_on_eigen_standin(ref):
+    """Pins the reference spectral module as built here (proj/src/spectral.cpp
+    on oracle/ref/eigen_shim): its eigenvalues agree with scipy's dense
+    solver on the same normalised Laplacian, and spectral_cluster recovers
+    the two moons."""
+    from paper_2310_13870_b200 import datasets
+    from sklearn.metrics import adjusted_rand_score
+    pts, truth = datasets.make_moons(3000, 0.05, 1)
+    g = ref.build_graph(pts.astype(np.float32).astype(np.float64), 0.15, 32, seed=1,
+                        want_estimates=False)
+    n = 3000
+    e = ref.smallest_eigenpairs(n, g["u"], g["v"], g["w"], 4)
+    a = np.zeros((n, n))
+    a[g["u"], g["v"]] = g["w"]
+    a[g["v"], g["u"]] = g["w"]
+    dinv = 1.0 / np.sqrt(a.sum(1))
+    lap = np.eye(n) - dinv[:, None] * a * dinv[None, :]
+    dense = np.linalg.eigvalsh(lap)[:4]
+    np.testing.assert_allclose(e["eigenvalues"], dense, atol=1e-6)
+    assert np.all(e["residuals"] < 1e-5)
+    lab = ref.spectral_cluster(n, g["u"], g["v"], g["w"], 2, seed=7)
+    assert adjusted_rand_score(truth, lab) > 0.99
