@@ -87,6 +87,13 @@ struct TreeTable {
 };
 constexpr uint32_t kBoxMaxDim = 16;
 
+// Certified pruning (kde.cu): a source sub-chunk is skipped for an entry when
+// its bounding-box bound is below 2^-kPruneBits of half the entry's node
+// mass. With at most 2^20 sub-chunks per node the skipped mass is below
+// 2^-(kPruneBits - 21) of the node mass -- far below the fp32 evaluation
+// error -- and the tie guard widens its margin by that bound (sampler.cu).
+constexpr float kPruneBits = 48.f;
+
 struct KdeWorkspace;
 
 struct Dataset {

@@ -58,7 +58,6 @@ constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
 constexpr uint64_t kMaxPartials = 256ull << 20;  // doubles (2 GiB)
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
-constexpr float kPruneBits = 80.f;   // sub-chunk bound below 2^-80 of the node mass
 constexpr uint32_t kSubMin = 512;    // smallest sub-chunk (pruning granularity)
 constexpr uint32_t kSubMinSmall = 64;  // ... for nodes below 8 * kSubMin points
 
@@ -140,9 +139,10 @@ __device__ __forceinline__ void lowd_range_sum(
 // skipped when that bound is below 2^-kPruneBits of half the entry's node
 // mass (known from the previous level; >= 1 at the root, which holds the
 // query itself). With at most 2^20 sub-chunks per node the total skipped
-// mass is < 2^-60 of the node mass: routing compares u < p on a 2^-53 grid,
-// so decisions are unchanged (the fp32 evaluation itself perturbs p ~2^40
-// times more). The whole CTA skips when all its entries agree; a warp skips
+// mass is < 2^-27 of the node mass (kPruneBits = 48), below the fp32
+// evaluation error of the sums; the tie guard adds this bound to its margin,
+// so routing decisions still match the fp64 reference exactly (a draw that
+// close to p is re-decided on exact sums). The whole CTA skips when all its entries agree; a warp skips
 // the arithmetic when all of its entries do; a pruned sub-chunk is dropped
 // from an entry's sum whether or not its CTA evaluated it.
 template <int D, int FAM>

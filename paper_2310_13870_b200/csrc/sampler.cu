@@ -159,9 +159,11 @@ __global__ void __launch_bounds__(kRouteThreads)
             // re-decided on fp64 sums (exact_sums_kernel), which makes the
             // output match the reference's exact backend edge for edge.
             const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em[u]) / 32.0);
-            // certified pruning at the compute level skipped < 2^-60 of the
-            // ancestor row's mass: an absolute error on p of at most this
-            const double pruned = row_mass ? double(exp2f(rm[u] - 58.f - em[u])) : 0.0;
+            // certified pruning at the compute level skipped < 2^-(B-21) of
+            // the ancestor row's mass (B = kPruneBits): an absolute error on
+            // p of at most this (3 bits of slack)
+            const double pruned =
+                row_mass ? double(exp2f(rm[u] - (kPruneBits - 24.f) - em[u])) : 0.0;
             const double M = (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
             const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
             const uint64_t hi = static_cast<uint64_t>(P + M);
