@@ -12,7 +12,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libfsgg.so")
+# FSGG_LIB_PATH: load an alternative in-tree build (development A/B runs)
+LIB_PATH = os.environ.get("FSGG_LIB_PATH") or os.path.join(HERE, "_lib", "libfsgg.so")
 INCLUDE_DIR = os.path.join(os.path.dirname(HERE), "include")
 
 FSGG_OK = 0

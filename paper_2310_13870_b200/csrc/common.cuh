@@ -69,6 +69,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 #ifdef __CUDACC__
+// 2^x for a pair of x <= 0 on the FP32 pipe instead of MUFU (FA4-style
+// offload): x = j + f with j = rint(x) (1.5*2^23 magic add), 2^f on
+// [-1/2, 1/2] by a degree-5 minimax polynomial (max rel. error 2.4e-7 in
+// fp32, the same order as ex2.approx), then j added to the exponent field.
+// Arguments are clamped at -125 (MUFU's .ftz result there is 0; this one is
+// < 2^-124: both negligible against the pruning bound).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-r.x, -r.y));
+  float2 p = make_float2(0.0013277226826176047f, 0.0013277226826176047f);
+  p = __ffma2_rn(p, f, make_float2(0.009675547480583191f, 0.009675547480583191f));
+  p = __ffma2_rn(p, f, make_float2(0.0555071085691452f, 0.0555071085691452f));
+  p = __ffma2_rn(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  // low bits of t hold j; (bits(t) << 23) == (j << 23) mod 2^32
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+#endif
+
+#ifdef __CUDACC__
 // fp64 kernel value, same operation order as proj/include/fsg/kernel.hpp:28-53.
 __device__ __forceinline__ double kernel_f64(int family, double sigma,
                                              const float* x, const float* y,

@@ -198,6 +198,7 @@ struct SampleRequest {
   int prune = 1;
   bool verify_ties = true;  // reference RNG mode: re-decide near-ties on fp64 sums
   bool dfs_finish = true;   // finish small-node levels depth-first (finish.cu)
+  bool walk = true;         // single-ticket entries below kWalkMaxNode walk (walk.cu)
   bool want_root_sums = false;
 };
 
@@ -237,6 +238,25 @@ struct DfsArgs {
 };
 bool dfs_finish_supported(uint32_t d);
 void dfs_finish(Dataset& ds, const KernelSpec& ks, const DfsArgs& args);
+
+// ---- walk.cu --------------------------------------------------------------
+// Entries holding a single ticket below nodes of kWalkMaxNode points leave
+// the level-synchronous lists and finish as one path walk each.
+constexpr uint32_t kWalkMaxNode = 64;
+struct WalkArgs {
+  uint32_t W = 0;  // walks
+  const uint32_t* wq = nullptr;  // query
+  const uint32_t* wh = nullptr;  // heap index of the start node
+  const float* welm = nullptr;   // log2 of the start node's sum
+  uint64_t key_prefix = 0, seed = 0;
+  int rng_mode = 0, verify = 1;
+  const uint32_t* qrow = nullptr;
+  const uint64_t* row_off = nullptr;
+  uint32_t *row_cnt = nullptr, *leaf_src = nullptr, *leaf_cnt = nullptr;
+  unsigned long long* stats = nullptr;  // [5][64]: entries, tickets, evals, degen, ties
+};
+bool walk_supported(uint32_t d);
+void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& args);
 
 // ---- graph.cu -------------------------------------------------------------
 struct GraphResult {

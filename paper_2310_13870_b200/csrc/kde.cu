@@ -58,6 +58,11 @@ constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
 constexpr uint64_t kMaxPartials = 256ull << 20;  // doubles (2 GiB)
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
+#ifndef FSGG_POLY_EVERY
+#define FSGG_POLY_EVERY 16
+#endif
+// 1 in kPolyEvery exp2 on the FP32 pipe (ex2_poly2); 0 = all on MUFU
+constexpr uint32_t kPolyEvery = FSGG_POLY_EVERY;
 constexpr uint32_t kSubMin = 512;    // smallest sub-chunk (pruning granularity)
 constexpr uint32_t kSubMinSmall = 64;  // ... for nodes below 8 * kSubMin points
 
@@ -110,14 +115,31 @@ __device__ __forceinline__ void lowd_range_sum(
     for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
       const uint32_t j1 = min(lenp, j0 + kFlush);
       float2 acc = make_float2(0.f, 0.f);
-#pragma unroll 4
-      for (uint32_t j = j0; j < j1; ++j) {
+      auto arg_of = [&](uint32_t j) {
         const float2* x = sm + j * D;
         float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
 #pragma unroll
         for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
         t = fam_finish<FAM>(t);
-        const float2 arg = __ffma2_rn(t, ms, off2);
+        return __ffma2_rn(t, ms, off2);
+      };
+      uint32_t j = j0;
+      // one source in kPolyEvery takes the FP32-pipe exp2, the rest MUFU:
+      // balances the two pipes (the loop is MUFU-bound otherwise)
+      if (kPolyEvery > 0)
+      for (; j + kPolyEvery <= j1; j += kPolyEvery) {
+#pragma unroll
+        for (uint32_t u = 0; u < kPolyEvery; ++u) {
+          const float2 arg = arg_of(j + u);
+          if (u == kPolyEvery - 1)
+            acc = __fadd2_rn(acc, ex2_poly2(arg));
+          else
+            acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+        }
+      }
+#pragma unroll 4
+      for (; j < j1; ++j) {
+        const float2 arg = arg_of(j);
         acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
       }
       accA += acc.x;
@@ -253,29 +275,12 @@ __global__ void __launch_bounds__(256)
     g1[i] = g2[i] = 0.0;
     return;
   }
-  const uint32_t mid = f + (l - f) / 2;
   const uint32_t q = eq[i];
   float qc[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
   double s[2];
-#pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    const uint64_t hc = 2 * h + 1 + side;
-    const uint32_t a = side ? mid : f, b = side ? l : mid;
-    const float off =
-        has_boxes ? scale * box_dist<FAM>(qc, tlo + hc * D, thi + hc * D, D) : 0.f;
-    float acc = 0.f;
-    for (uint32_t j = a; j < b; ++j) {
-      const float* x = pts + size_t(j) * D;
-      float t = 0.f;
-#pragma unroll
-      for (int k = 0; k < D; ++k) t = fam_acc1<FAM>(qc[k] - __ldg(x + k), t);
-      t = fam_finish1<FAM>(t);
-      acc += ex2_approx(fmaf(t, -scale, off));
-    }
-    s[side] = rescale(acc, off);
-  }
+  direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
   g1[i] = fmax(s[0], kSumFloor);
   g2[i] = fmax(s[1], kSumFloor);
   if (groot) groot[i] = fmax(s[0] + s[1], kSumFloor);

@@ -1,9 +1,11 @@
-// Kernel-family arithmetic shared by the KDE kernels (kde.cu) and the
-// depth-first finish kernel (finish.cu).
+// Kernel-family arithmetic shared by the KDE kernels (kde.cu), the
+// depth-first finish kernel (finish.cu) and the single-ticket walk (walk.cu).
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "common.cuh"
 
 namespace fsgg {
 
@@ -47,6 +49,55 @@ __device__ __forceinline__ float box_dist(const float* q, const float* lo,
     acc = (FAM == 2) ? acc + v : fmaf(v, v, acc);
   }
   return fam_finish1<FAM>(acc);
+}
+
+// Rescale an fp32 sum of offset terms 2^(off - scale*dist) back to k units.
+__device__ __forceinline__ double rescale_off(double acc, float off) {
+  return off > 0.f ? acc * exp2(-static_cast<double>(off)) : acc;
+}
+
+// Child sums of a small node (heap index h, points [f, l), l - f >= 2) for
+// one query, one thread: fp32 terms with the child's bounding-box exponent
+// offset, fp32 accumulation in index order, fp64 rescale. Shared by the
+// direct KDE kernel and the walk so both produce the same bits.
+template <int D, int FAM>
+__device__ __forceinline__ void direct_child_sums(const float* __restrict__ pts,
+                                                  const float (&qc)[D], uint64_t h,
+                                                  uint32_t f, uint32_t l,
+                                                  const float* __restrict__ tlo,
+                                                  const float* __restrict__ thi,
+                                                  int has_boxes, float scale, double (&s)[2]) {
+  const uint32_t mid = f + (l - f) / 2;
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const uint64_t hc = 2 * h + 1 + side;
+    const uint32_t a = side ? mid : f, b = side ? l : mid;
+    const float off =
+        has_boxes ? scale * box_dist<FAM>(qc, tlo + hc * D, thi + hc * D, D) : 0.f;
+    float acc = 0.f;
+    for (uint32_t j = a; j < b; ++j) {
+      const float* x = pts + size_t(j) * D;
+      float t = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) t = fam_acc1<FAM>(qc[k] - __ldg(x + k), t);
+      t = fam_finish1<FAM>(t);
+      acc += ex2_approx(fmaf(t, -scale, off));
+    }
+    s[side] = rescale_off(acc, off);
+  }
+}
+
+// Philox4x32-10 (Salmon et al. 2011), for rng_mode = PHILOX.
+__device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
 }
 
 

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "engine.cuh"
+#include "kde_math.cuh"
 
 namespace fsgg {
 
@@ -44,6 +45,13 @@ uint32_t dfs_max_node() {
   return v;
 }
 
+// Children below nodes of this many points that hold one ticket finish as
+// walks (walk.cu); FSGG_WALK_MAX overrides (0 disables).
+uint32_t walk_max_node() {
+  const char* e = std::getenv("FSGG_WALK_MAX");  // read per call: tests toggle it
+  return e ? uint32_t(std::atoi(e)) : kWalkMaxNode;
+}
+
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
                                  uint32_t* __restrict__ eq,
@@ -58,25 +66,22 @@ __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
   eg[i] = 0;
 }
 
-// Philox4x32-10 (Salmon et al. 2011), for rng_mode = PHILOX.
-__device__ __forceinline__ uint4 philox4x32(uint4 c, uint2 k) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-    k.x += 0x9E3779B9u;
-    k.y += 0xBB67AE85u;
-  }
-  return c;
-}
-
 // proj/src/sampler.cpp:186-225 per entry. Each thread handles kRouteUnroll
 // entries (block-strided, coalesced) and issues every load of all of them
 // before using any: at deep levels the kernel is a latency-bound stream of
 // ~60M entries with little arithmetic.
 constexpr int kRouteThreads = 256;
 constexpr int kRouteUnroll = 4;
+constexpr uint32_t kLeafMark = 0xffffffffu;  // tl of an entry that emitted a leaf
+
+// Packed (has_left, has_right) for the next level's list; with `walk`, a
+// child holding exactly one ticket leaves the lists for walk.cu instead.
+__device__ __forceinline__ unsigned long long child_flags(uint32_t left, uint32_t t, int walk) {
+  const uint32_t right = t - left;
+  const bool kl = left > 0 && !(walk && left == 1);
+  const bool kr = right > 0 && !(walk && right == 1);
+  return (static_cast<unsigned long long>(kl) << 32) | static_cast<unsigned long long>(kr);
+}
 
 __global__ void __launch_bounds__(kRouteThreads)
     route_kernel(uint32_t E, uint32_t level, const uint32_t* __restrict__ eq,
@@ -90,7 +95,7 @@ __global__ void __launch_bounds__(kRouteThreads)
                  unsigned long long* __restrict__ flags,
                  unsigned long long* __restrict__ counters, const float* __restrict__ elm,
                  const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
-                 uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount) {
+                 uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk) {
   constexpr int U = kRouteUnroll;
   const uint32_t base = blockIdx.x * (kRouteThreads * U) + threadIdx.x;
   uint32_t gi[U], q[U], t[U], f[U], l[U];
@@ -130,7 +135,7 @@ __global__ void __launch_bounds__(kRouteThreads)
       const uint64_t at = row_off[row] + slot;
       leaf_src[at] = f[u];
       leaf_cnt[at] = t[u];
-      tl[i] = 0;
+      tl[i] = kLeafMark;
     } else {
       double p;
       bool verify = false;
@@ -190,8 +195,7 @@ __global__ void __launch_bounds__(kRouteThreads)
         }
       }
       tl[i] = left;
-      fl = (static_cast<unsigned long long>(left > 0) << 32) |
-           static_cast<unsigned long long>(left < t[u]);
+      fl = child_flags(left, t[u], walk);
       if (verify) vlist[atomicAdd(vcount, 1u)] = i;
     }
     flags[i] = fl;
@@ -337,7 +341,7 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
                                const uint32_t* __restrict__ vcount,
                                uint32_t* __restrict__ tl,
                                unsigned long long* __restrict__ flags,
-                               unsigned long long* __restrict__ counters) {
+                               unsigned long long* __restrict__ counters, int walk) {
   const uint32_t cnt = *vcount;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < cnt;
        b += gridDim.x * blockDim.x) {
@@ -364,8 +368,7 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
       for (uint32_t c = 0; c < t; ++c) left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
     }
     tl[i] = left;
-    flags[i] = (static_cast<unsigned long long>(left > 0) << 32) |
-               static_cast<unsigned long long>(left < t);
+    flags[i] = child_flags(left, t, walk);
   }
 }
 
@@ -431,29 +434,70 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                uint32_t* __restrict__ neg,
                                float* __restrict__ nelm,
                                const uint32_t* __restrict__ eprow,
-                               uint32_t* __restrict__ neprow, int self_rows) {
+                               uint32_t* __restrict__ neprow, int self_rows,
+                               uint32_t level, uint32_t* __restrict__ wq,
+                               uint32_t* __restrict__ wh, float* __restrict__ welm,
+                               uint32_t* __restrict__ wcount) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= E) return;
-  const unsigned long long fl = flags[i];
-  if (!fl) return;
-  const uint32_t g = eg[i], q = eq[i], t = et[i], l = tl[i];
-  const unsigned long long Pi = P[i];
-  const uint32_t prow = self_rows ? i : (eprow ? eprow[i] : 0u);
-  if (hiw(fl)) {
-    const uint32_t pos = hiw(Pi) + low(P[goff[g]]);
-    neq[pos] = q;
-    net[pos] = l;
-    neg[pos] = 2 * g;
-    nelm[pos] = static_cast<float>(log2(g1[i]));
-    neprow[pos] = prow;
+  uint32_t nw = 0, wmask = 0;  // single-ticket children handed to the walk
+  uint32_t g = 0, q = 0;
+  if (i < E) {
+    const unsigned long long fl = flags[i];
+    const uint32_t t = et[i], l = tl[i];
+    g = eg[i];
+    q = eq[i];
+    if (wq && l != kLeafMark) {
+      wmask = (l == 1 ? 1u : 0u) | (t - l == 1 ? 2u : 0u);
+      nw = __popc(wmask);
+    }
+    if (fl) {
+      const unsigned long long Pi = P[i];
+      const uint32_t prow = self_rows ? i : (eprow ? eprow[i] : 0u);
+      if (hiw(fl)) {
+        const uint32_t pos = hiw(Pi) + low(P[goff[g]]);
+        neq[pos] = q;
+        net[pos] = l;
+        neg[pos] = 2 * g;
+        nelm[pos] = static_cast<float>(log2(g1[i]));
+        neprow[pos] = prow;
+      }
+      if (low(fl)) {
+        const uint32_t pos = hiw(P[goff[g + 1]]) + low(Pi);
+        neq[pos] = q;
+        net[pos] = t - l;
+        neg[pos] = 2 * g + 1;
+        nelm[pos] = static_cast<float>(log2(g2[i]));
+        neprow[pos] = prow;
+      }
+    }
   }
-  if (low(fl)) {
-    const uint32_t pos = hiw(P[goff[g + 1]]) + low(Pi);
-    neq[pos] = q;
-    net[pos] = t - l;
-    neg[pos] = 2 * g + 1;
-    nelm[pos] = static_cast<float>(log2(g2[i]));
-    neprow[pos] = prow;
+  if (!wq) return;
+  // warp-aggregated reservation in the walk list (order is irrelevant: each
+  // walk is independent and leaves land in per-query rows)
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t incl = nw;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= uint32_t(o)) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  uint32_t base = 0;
+  if (lane == 31) base = atomicAdd(wcount, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  uint32_t pos = base + incl - nw;
+  const uint32_t hbase = (1u << (level + 1)) - 1;
+  if (wmask & 1u) {
+    wq[pos] = q;
+    wh[pos] = hbase + 2 * g;
+    welm[pos] = static_cast<float>(log2(g1[i]));
+    ++pos;
+  }
+  if (wmask & 2u) {
+    wq[pos] = q;
+    wh[pos] = hbase + 2 * g + 1;
+    welm[pos] = static_cast<float>(log2(g2[i]));
   }
 }
 
@@ -546,6 +590,13 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   DevBuf& vlist = ds.buf("s.vlist", verify ? cap * 4 : 4);
   if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
   KdeWorkspace& ws = *ds.kde_ws;
+  // single-ticket walk list (walk.cu), filled by scatter_kernel
+  const bool walk_on = req.walk && walk_supported(ds.d) && walk_max_node() > 0;
+  DevBuf& wq = ds.buf("s.wq", walk_on ? cap * 4 : 4);
+  DevBuf& wh = ds.buf("s.wh", walk_on ? cap * 4 : 4);
+  DevBuf& welm = ds.buf("s.welm", walk_on ? cap * 4 : 4);
+  DevBuf& wcount = ds.buf("s.wcount", 8);
+  FSGG_CUDA(cudaMemsetAsync(wcount.as<void>(), 0, 8, s));
 
   init_rows_kernel<<<ceil_div_u32(std::max<uint32_t>(nq, 1), 256), 256, 0, s>>>(
       out.uq.as<uint32_t>(), nq, qrow.as<uint32_t>(), eq[0]->as<uint32_t>(),
@@ -681,6 +732,10 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     }
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[1], s));
+    // children (level + 1) below walk_max_node points with one ticket walk
+    const uint32_t smax_child =
+        uint32_t((uint64_t(ds.n) + (1ull << (level + 1)) - 1) >> (level + 1));
+    const int wk = walk_on && level < t.depth && smax_child <= walk_max_node() ? 1 : 0;
     FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
     uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
     route_kernel<<<ceil_div_u32(uint64_t(E) + 1, kRouteThreads * kRouteUnroll),
@@ -695,7 +750,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         level == 0 ? nullptr : elm[cur]->as<float>(),
         self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
-        verify ? vlist.as<uint32_t>() : nullptr, vcount);
+        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk);
     FSGG_LAUNCH_CHECK();
     if (verify) {
       exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
@@ -710,7 +765,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
           level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
           g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
           prefix, vlist.as<uint32_t>(), vcount, tl.as<uint32_t>(),
-          flags.as<unsigned long long>(), counters.as<unsigned long long>());
+          flags.as<unsigned long long>(), counters.as<unsigned long long>(), wk);
       FSGG_LAUNCH_CHECK();
       ds.launches += 2;
     }
@@ -730,7 +785,9 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur]->as<uint32_t>(),
         P.as<unsigned long long>(), g1.as<double>(), g2.as<double>(), eq[nxt]->as<uint32_t>(),
         et[nxt]->as<uint32_t>(), eg[nxt]->as<uint32_t>(), elm[nxt]->as<float>(),
-        eprow[cur]->as<uint32_t>(), eprow[nxt]->as<uint32_t>(), self_rows ? 1 : 0);
+        eprow[cur]->as<uint32_t>(), eprow[nxt]->as<uint32_t>(), self_rows ? 1 : 0, level,
+        wk ? wq.as<uint32_t>() : nullptr, wh.as<uint32_t>(), welm.as<float>(),
+        wcount.as<uint32_t>());
     FSGG_LAUNCH_CHECK();
     if (level < t.depth) {
       goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
@@ -769,6 +826,54 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     }
     E = static_cast<uint32_t>(next);
     cur = nxt;
+  }
+  if (walk_on) {
+    uint32_t W = 0;
+    FSGG_CUDA(cudaMemcpyAsync(&W, wcount.as<void>(), 4, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    if (W > 0) {
+      const auto w0 = std::chrono::steady_clock::now();
+      DevBuf& st = ds.buf("s.walk_stats", 4 * 64 * 8);
+      FSGG_CUDA(cudaMemsetAsync(st.as<void>(), 0, 4 * 64 * 8, s));
+      WalkArgs a;
+      a.W = W;
+      a.wq = wq.as<uint32_t>();
+      a.wh = wh.as<uint32_t>();
+      a.welm = welm.as<float>();
+      a.key_prefix = prefix;
+      a.seed = req.seed;
+      a.rng_mode = req.rng_mode;
+      a.verify = verify ? 1 : 0;
+      a.qrow = qrow.as<uint32_t>();
+      a.row_off = out.row_off.as<uint64_t>();
+      a.row_cnt = out.row_cnt.as<uint32_t>();
+      a.leaf_src = out.leaf_src.as<uint32_t>();
+      a.leaf_cnt = out.leaf_cnt.as<uint32_t>();
+      a.stats = st.as<unsigned long long>();
+      walk_finish(ds, ks, a);
+      std::vector<unsigned long long> h(4 * 64);
+      FSGG_CUDA(cudaMemcpyAsync(h.data(), st.as<void>(), h.size() * 8, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      // merge the walks' per-level tallies into the level diagnostics
+      for (uint32_t lv2 = 0; lv2 < 64; ++lv2) {
+        if (!h[lv2]) continue;
+        if (out.entries_per_level.size() <= lv2) {
+          out.entries_per_level.resize(lv2 + 1, 0);
+          out.tickets_per_level.resize(lv2 + 1, 0);
+        }
+        out.entries_per_level[lv2] += h[lv2];
+        out.tickets_per_level[lv2] += h[lv2];  // one ticket each
+        out.kde.evals += h[64 + lv2];
+        out.kde.performed += h[64 + lv2];
+        out.degenerate_draws += h[128 + lv2];
+        out.tie_verified += h[192 + lv2];
+      }
+      for (uint64_t e : out.entries_per_level) out.peak_entries = std::max(out.peak_entries, e);
+      if (trace)
+        std::fprintf(stderr, "fsgg walks: %u single-ticket walks %.3fms\n", W,
+                     std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - w0).count());
+    }
   }
   if (trace)
     for (auto& e : tev) cudaEventDestroy(e);

@@ -324,3 +324,33 @@ def test_depth_first_finish_matches_level_synchronous(tmp_path):
         outs.append((np.load(tmp_path / f"t{dfs}.npy"), r.stdout))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1]
+
+
+@pytest.mark.parametrize("rng", ["reference", "philox"])
+def test_single_ticket_walks_match_level_synchronous(rng):
+    """Single-ticket walks (walk.cu, FSGG_WALK_MAX) must give the same
+    samples and the same reference diagnostics as keeping every entry in the
+    level-synchronous lists, for both RNG modes and several thresholds."""
+    import os
+    p, _ = datasets.make_moons(30000, 0.05, 3)
+    ds = F.Dataset(p)
+    k = F.Kernel(F.KernelFamily.gaussian, 0.08)
+    mode = F.RngMode.reference if rng == "reference" else F.RngMode.philox
+    outs = []
+    old = os.environ.get("FSGG_WALK_MAX")
+    try:
+        for wmax in ("0", "64", "1024"):
+            os.environ["FSGG_WALK_MAX"] = wmax
+            tri, d = F.sample_neighbors_counted(ds, k, np.arange(30000), 24, 5, rng_mode=mode,
+                                                diagnostics=True)
+            outs.append((tri, d))
+    finally:
+        if old is None:
+            os.environ.pop("FSGG_WALK_MAX", None)
+        else:
+            os.environ["FSGG_WALK_MAX"] = old
+    for tri, d in outs[1:]:
+        assert np.array_equal(outs[0][0], tri)
+        assert list(outs[0][1].entries_per_level) == list(d.entries_per_level)
+        assert list(outs[0][1].tickets_per_level) == list(d.tickets_per_level)
+        assert outs[0][1].degenerate_draws == d.degenerate_draws
