@@ -55,7 +55,7 @@ constexpr int kXBM = 64;             // entries per high-d work item
 constexpr int kXBN = 64;             // sources per high-d tile
 constexpr int kXBK = 16;             // dims per high-d k-step
 constexpr uint32_t kChunkMin = 2048; // smallest source chunk of one item
-constexpr uint64_t kMaxPartials = 256ull << 20;  // doubles (2 GiB)
+constexpr uint64_t kMaxPartials = 2560ull << 20;  // doubles (20 GiB of the 180 GB HBM)
 constexpr float kPad = 3.0e18f;      // padding coordinate: term underflows to 0
 constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
 #ifndef FSGG_POLY_EVERY

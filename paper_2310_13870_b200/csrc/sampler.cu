@@ -34,6 +34,13 @@ namespace {
 constexpr double kTieMargin = 1e-4;
 // A compute level keeps partial rows deep enough to serve this many levels.
 constexpr uint32_t kServeLevels = 5;
+// The root's rows are kept deeper (one pass over all n^2 pairs then serves
+// every level down to nodes of ~n/2^10); FSGG_ROOT_SERVE overrides.
+constexpr uint32_t kServeLevelsRoot = 9;
+uint32_t root_serve_levels() {
+  const char* e = std::getenv("FSGG_ROOT_SERVE");
+  return e ? uint32_t(std::atoi(e)) : kServeLevelsRoot;
+}
 
 // Levels whose nodes all hold <= this many points are finished depth-first
 // (finish.cu); FSGG_DFS_MAX overrides (0 disables).
@@ -714,7 +721,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       uint32_t rd = 0;
       kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
                 level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr, ws,
-                out.kde, kServeLevels, &rd);
+                out.kde, level == 0 ? root_serve_levels() : kServeLevels, &rd);
       have_rows = rd > 1;
       if (have_rows) {
         self_rows = true;
