@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "kde_math.cuh"
@@ -700,9 +701,13 @@ void with_family(int family, F&& f) {
 
 constexpr uint32_t kLowDMax = 8;
 constexpr uint32_t kTcDirectMax = 24;  // tensor-core levels: direct (warp per entry) for small nodes
+uint32_t env_u32(const char* name, uint32_t dflt) {  // development overrides
+  const char* e = std::getenv(name);
+  return e ? uint32_t(std::atoi(e)) : dflt;
+}
 constexpr uint32_t kTcSubMin = 16;    // tensor-core partial buckets: >= 16 sources
 constexpr uint32_t kTcChunkMin = 128; // ... work items: >= one 128-source N-tile
-constexpr uint32_t kTcMaxRowDepth = 7;
+constexpr uint32_t kTcMaxRowDepth = 11;  // root rows serve ~10 levels (C5: 70k x 2^11 buckets)
 uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
 
 }  // namespace
@@ -721,7 +726,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const float* pts = ds.pts.as<float>();
   const bool lowd = d <= kLowDMax;
   const bool tc = !lowd && kde_tc_supported(ds, ks.family);
-  const bool direct = s_max <= (tc ? kTcDirectMax : direct_threshold(d));
+  const bool direct = s_max <= (tc ? env_u32("FSGG_TC_DIRECT", kTcDirectMax) : direct_threshold(d));
   const uint32_t be = lowd ? kBE : (tc ? 128u : uint32_t(kXBM));
 
   // blocks per slot + exact evaluation count of the level
@@ -800,7 +805,8 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   if (tc) {
     sd = 0;
     while ((child_min >> (sd + 1)) >= kTcSubMin && lv.level + 2 + sd <= t.depth &&
-           sd + 1 < kTcMaxRowDepth && (uint64_t(E) << (sd + 2)) <= kMaxPartials)
+           sd + 1 < env_u32("FSGG_TC_ROWDEPTH", kTcMaxRowDepth) &&
+           (uint64_t(E) << (sd + 2)) <= kMaxPartials)
       ++sd;
     while (c < sd && (child_min >> (c + 1)) >= kTcChunkMin &&
            (uint64_t(total_blocks) << (c + 1)) < target_items)

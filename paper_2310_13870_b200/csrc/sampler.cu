@@ -14,6 +14,7 @@
 //   3. one 64-bit exclusive scan of packed (has_left, has_right) flags;
 //   4. scatter_kernel / goff_kernel: deterministic stable placement, left
 //      children of a node before its right children (:217-222), no atomics.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
@@ -21,6 +22,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "engine.cuh"
 #include "kde_math.cuh"
@@ -336,6 +338,128 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// High-d tie guard, batched: the flagged entries of one node share its
+// sources, so instead of one full pass over the node per tie (C5: 70k rows x
+// 784 dims per tie at the root), ties are sorted by node, cut into batches of
+// kTieBatch, and each CTA streams one chunk of the node's sources once for a
+// whole batch: every source row is read once (float4) and its fp64 squared
+// distance to each batch query accumulated in index order over the dims
+// (kernel_f64's order), exp in fp64. Per-(tie, chunk) partials are combined
+// in chunk order by tie_reduce_kernel, so results are deterministic.
+constexpr uint32_t kTieBatchMinDim = 32;  // below: exact_sums_kernel (pruned sub-chunks)
+constexpr uint32_t kTieBatchMinNode = 16384;  // smaller nodes: one CTA per tie is cheaper
+constexpr int kTieBatch = 16;
+constexpr uint32_t kTieChunk = 1024;
+constexpr int kTieThreads = 128;
+
+struct TieItem {
+  uint32_t first;   // position of the batch's first tie in the sorted list
+  uint32_t count;   // ties in the batch (<= kTieBatch)
+  uint32_t src0, src1;  // source chunk [src0, src1)
+  uint32_t mid;     // node split point
+  uint32_t chunk;   // chunk index within the node
+  uint32_t nchunks; // chunks of the node
+  uint32_t pad;
+};
+
+__global__ void __launch_bounds__(kTieThreads)
+    tie_batch_kernel(const float* __restrict__ pts, uint32_t d, int family, double sigma,
+                     const uint32_t* __restrict__ eq, const uint32_t* __restrict__ sorted,
+                     const TieItem* __restrict__ items, uint32_t max_chunks,
+                     double* __restrict__ partials) {
+  extern __shared__ __align__(16) float tq[];  // [kTieBatch][d]
+  __shared__ double red[kTieThreads / 32][kTieBatch][2];
+  const TieItem it = items[blockIdx.x];
+  for (uint32_t idx = threadIdx.x; idx < it.count * d; idx += blockDim.x) {
+    const uint32_t t = idx / d, a = idx % d;
+    tq[idx] = pts[size_t(eq[sorted[it.first + t]]) * d + a];
+  }
+  __syncthreads();
+  double s0[kTieBatch], s1[kTieBatch];
+#pragma unroll
+  for (int t = 0; t < kTieBatch; ++t) s0[t] = s1[t] = 0.0;
+  const double inv = family == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  for (uint32_t j = it.src0 + threadIdx.x; j < it.src1; j += blockDim.x) {
+    const float* xj = pts + size_t(j) * d;
+    double acc[kTieBatch];
+#pragma unroll
+    for (int t = 0; t < kTieBatch; ++t) acc[t] = 0.0;
+    for (uint32_t a = 0; a < d; ++a) {
+      const double xv = double(__ldg(xj + a));
+#pragma unroll
+      for (int t = 0; t < kTieBatch; ++t) {
+        if (uint32_t(t) < it.count) {
+          const double df = double(tq[t * d + a]) - xv;
+          acc[t] = family == 2 ? acc[t] + fabs(df) : fma(df, df, acc[t]);
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kTieBatch; ++t) {
+      if (uint32_t(t) < it.count) {
+        const double v = family == 1 ? exp(-sqrt(acc[t]) * inv) : exp(-acc[t] * inv);
+        if (j < it.mid)
+          s0[t] += v;
+        else
+          s1[t] += v;
+      }
+    }
+  }
+  // fixed-order block reduction: warp butterflies, then warps in order
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = 0; t < kTieBatch; ++t) {
+    double a0 = s0[t], a1 = s1[t];
+    for (int o = 16; o; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane == 0) {
+      red[w][t][0] = a0;
+      red[w][t][1] = a1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < it.count * 2) {
+    const uint32_t t = threadIdx.x >> 1, side = threadIdx.x & 1;
+    double v = 0.0;
+    for (int k = 0; k < kTieThreads / 32; ++k) v += red[k][t][side];
+    partials[(size_t(it.first + t) * max_chunks + it.chunk) * 2 + side] = v;
+  }
+}
+
+__global__ void gather_u32_kernel(uint32_t n, const uint32_t* __restrict__ idx,
+                                  const uint32_t* __restrict__ src, uint32_t* __restrict__ out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n) out[b] = src[idx[b]];
+}
+
+__global__ void node_range_kernel(uint32_t n, const uint32_t* __restrict__ slot, uint64_t hbase,
+                                  const uint32_t* __restrict__ tfirst,
+                                  const uint32_t* __restrict__ tlast, uint32_t* __restrict__ out) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n) {
+    out[2 * b] = tfirst[hbase + slot[b]];
+    out[2 * b + 1] = tlast[hbase + slot[b]];
+  }
+}
+
+__global__ void tie_reduce_kernel(uint32_t count, const uint32_t* __restrict__ sorted,
+                                  const uint32_t* __restrict__ nchunks_of,
+                                  uint32_t max_chunks, const double* __restrict__ partials,
+                                  double* __restrict__ g1, double* __restrict__ g2) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  double a = 0.0, c = 0.0;
+  for (uint32_t k = 0; k < nchunks_of[b]; ++k) {
+    a += partials[(size_t(b) * max_chunks + k) * 2];
+    c += partials[(size_t(b) * max_chunks + k) * 2 + 1];
+  }
+  const uint32_t i = sorted[b];
+  g1[i] = fmax(a, kSumFloor);
+  g2[i] = fmax(c, kSumFloor);
+}
+
 // Re-decide the flagged entries on the fp64 sums (reference stream).
 __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
                                const uint32_t* __restrict__ et,
@@ -527,6 +651,94 @@ __global__ void row_ends_kernel(const uint64_t* __restrict__ row_off,
                                 uint32_t nq, uint64_t* __restrict__ ends) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nq) ends[i] = row_off[i] + row_cnt[i];
+}
+
+// Sort the flagged entries by node, cut node groups into batches, one work
+// item per (batch, source chunk); partial sums reduced per tie in chunk order.
+void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const uint32_t* eq,
+                      const uint32_t* eg, const uint32_t* vlist, uint32_t cnt, double* g1,
+                      double* g2) {
+  cudaStream_t s = ds.stream;
+  const TreeTable& t = ds.tree;
+  DevBuf& sorted = ds.buf("s.tie_sorted", size_t(cnt) * 4);
+  DevBuf& tmp = ds.buf("s.tie_tmp", 8);
+  const int bits = 32;
+  size_t tb = 0;
+  FSGG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, vlist, sorted.as<uint32_t>(), int(cnt), 0,
+                                           bits, s));
+  tmp.ensure(tb, s);
+  FSGG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.as<void>(), tb, vlist, sorted.as<uint32_t>(),
+                                           int(cnt), 0, bits, s));
+  // entries are grouped by node slot in index order, so sorted indices are
+  // grouped by node: read their slots back and build the batches on the host
+  std::vector<uint32_t> slot(cnt);
+  DevBuf& dslot = ds.buf("s.tie_slot", size_t(cnt) * 4);
+  gather_u32_kernel<<<ceil_div_u32(cnt, 256), 256, 0, s>>>(cnt, sorted.as<uint32_t>(), eg,
+                                                           dslot.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  FSGG_CUDA(cudaMemcpyAsync(slot.data(), dslot.as<void>(), size_t(cnt) * 4,
+                            cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> hf(cnt), hl(cnt);
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  // node ranges of the distinct slots
+  const uint64_t hbase = (1ull << level) - 1;
+  std::vector<TieItem> items;
+  std::vector<uint32_t> nch(cnt, 0);
+  uint32_t max_chunks = 1;
+  {
+    // fetch first/last for every tie's node (small: cnt entries)
+    DevBuf& df = ds.buf("s.tie_f", size_t(cnt) * 8);
+    node_range_kernel<<<ceil_div_u32(cnt, 256), 256, 0, s>>>(
+        cnt, dslot.as<uint32_t>(), hbase, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+        df.as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    std::vector<uint32_t> fl(size_t(cnt) * 2);
+    FSGG_CUDA(cudaMemcpyAsync(fl.data(), df.as<void>(), size_t(cnt) * 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t b = 0; b < cnt; ++b) {
+      hf[b] = fl[2 * b];
+      hl[b] = fl[2 * b + 1];
+    }
+  }
+  for (uint32_t b = 0; b < cnt;) {
+    uint32_t e = b + 1;
+    while (e < cnt && slot[e] == slot[b] && e - b < uint32_t(kTieBatch)) ++e;
+    const uint32_t f = hf[b], l = hl[b], mid = f + (l - f) / 2;
+    const uint32_t chunks = std::max<uint32_t>(1, (l - f + kTieChunk - 1) / kTieChunk);
+    max_chunks = std::max(max_chunks, chunks);
+    for (uint32_t c = 0; c < chunks; ++c) {
+      TieItem it;
+      it.first = b;
+      it.count = e - b;
+      it.src0 = f + c * kTieChunk;
+      it.src1 = std::min(l, it.src0 + kTieChunk);
+      it.mid = mid;
+      it.chunk = c;
+      it.nchunks = chunks;
+      it.pad = 0;
+      items.push_back(it);
+    }
+    for (uint32_t k = b; k < e; ++k) nch[k] = chunks;
+    b = e;
+  }
+  DevBuf& ditems = ds.buf("s.tie_items", items.size() * sizeof(TieItem));
+  DevBuf& dnch = ds.buf("s.tie_nch", size_t(cnt) * 4);
+  DevBuf& parts = ds.buf("s.tie_parts", size_t(cnt) * max_chunks * 16);
+  FSGG_CUDA(cudaMemcpyAsync(ditems.as<void>(), items.data(), items.size() * sizeof(TieItem),
+                            cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemcpyAsync(dnch.as<void>(), nch.data(), size_t(cnt) * 4, cudaMemcpyHostToDevice, s));
+  const size_t smem = size_t(kTieBatch) * ds.d * 4;
+  FSGG_CUDA(cudaFuncSetAttribute(tie_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(std::max<size_t>(smem, 48u << 10))));
+  tie_batch_kernel<<<uint32_t(items.size()), kTieThreads, smem, s>>>(
+      ds.pts.as<float>(), ds.d, ks.family, ks.sigma, eq, sorted.as<uint32_t>(),
+      ditems.as<TieItem>(), max_chunks, parts.as<double>());
+  FSGG_LAUNCH_CHECK();
+  tie_reduce_kernel<<<ceil_div_u32(cnt, 128), 128, 0, s>>>(cnt, sorted.as<uint32_t>(),
+                                                          dnch.as<uint32_t>(), max_chunks,
+                                                          parts.as<double>(), g1, g2);
+  FSGG_LAUNCH_CHECK();
+  ds.launches += 5;
 }
 
 }  // namespace
@@ -759,7 +971,23 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
         verify ? vlist.as<uint32_t>() : nullptr, vcount, wk);
     FSGG_LAUNCH_CHECK();
-    if (verify) {
+    if (verify && ds.d >= kTieBatchMinDim && smax_level >= kTieBatchMinNode) {
+      // high d: batched fp64 recomputation (tie_batch_kernel), then reroute
+      uint32_t cnt = 0;
+      FSGG_CUDA(cudaMemcpyAsync(&cnt, vcount, 4, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      if (cnt > 0) {
+        batched_tie_sums(ds, ks, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+                         vlist.as<uint32_t>(), cnt, g1.as<double>(), g2.as<double>());
+        reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
+            level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+            g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+            prefix, ds.buf("s.tie_sorted", 4).as<uint32_t>(), vcount, tl.as<uint32_t>(),
+            flags.as<unsigned long long>(), counters.as<unsigned long long>(), wk);
+        FSGG_LAUNCH_CHECK();
+        ds.launches += 1;
+      }
+    } else if (verify) {
       exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
           ds.pts.as<float>(), ds.d, ks.family, ks.sigma, ks.scale, level, t.depth,
           eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
