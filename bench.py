@@ -47,6 +47,7 @@ CONFIG_DOC = {
     "C4": "synthetic image pixels n=154401 d=5 sigma=0.2 L=32",
     "C5": "GMM n=70000 d=784 sigma=median dist L=32",
 }
+TC_MIN_DIM = 64  # kTcMinDim (engine.cuh): gaussian d >= 64 runs on tcgen05
 NOMINAL_EX2_PER_CLK_PER_SM = 16
 SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -352,20 +353,57 @@ def main():
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
-    roofline = {
-        "bound": "mufu", "kernel": "kde_lowd_tiled_kernel<2,gaussian>",
-        "achieved": achieved / 1e9, "peak": ex2.value / 1e9, "unit": "Gex2/s",
-        "frac": achieved / ex2.value if ex2.value else None,
-        "peak_source": "measured in this run: MUFU.EX2 microbenchmark (fsgg_probe_ex2_throughput)",
-        "nominal_peak": nominal / 1e9, "frac_of_nominal": achieved / nominal,
-        "algorithmic_unit": "one Gaussian kernel evaluation = one ex2 (SURVEY.md §8d)",
-        "evals_per_launch": tiled_perf / max(tiled_launches, 1),
-        "reference_equivalent_evals_per_launch": tiled_evals / max(tiled_launches, 1),
-        "reference_equivalent_rate": tiled_evals / max(tiled_s, 1e-12) / 1e9,
-        "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
-        "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
-        "traffic": traffic,
-    }
+    tensor = w.d >= TC_MIN_DIM
+    if tensor:
+        # tcgen05 kind::tf32 path (kde_tc.cu): algorithmic work is the fp32
+        # dot-product form, 2*d FLOPs per evaluation; the
+        # kernel executes it three times (3xTF32 error compensation).
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except (OSError, ValueError):
+            pass
+        bf16 = float(peaks.get("bf16_tflops", 2250.0))
+        tf32_peak = bf16 / 2.0
+        alg = tiled_perf * 2.0 * w.d / max(tiled_s, 1e-12) / 1e12
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "kde_tc_ncu.json")
+        if os.path.exists(prof):
+            try:
+                l0 = json.load(open(prof))["launches"][0]
+                mul = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
+                traffic = sum(float(l0[k][0]) * mul.get(l0[k][1], 1.0)
+                              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            except (OSError, ValueError, KeyError, IndexError):
+                traffic = None
+        roofline = {
+            "bound": "tensor", "kernel": "kde_tc_kernel<gaussian> (tcgen05.mma kind::tf32, 3xTF32)",
+            "achieved": alg, "peak": tf32_peak, "unit": "TFLOP/s",
+            "frac": alg / tf32_peak,
+            "executed_tflops": 3.0 * alg, "executed_frac": 3.0 * alg / tf32_peak,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS) / 2: dense TF32 is "
+                            "half the bf16 rate on Blackwell"),
+            "algorithmic_unit": "2*d FLOPs per Gaussian evaluation (dot-product form, SURVEY.md §8d)",
+            "evals_per_launch": tiled_perf / max(tiled_launches, 1),
+            "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
+            "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
+            "traffic": traffic,
+        }
+    else:
+        roofline = {
+            "bound": "mufu", "kernel": "kde_lowd_tiled_kernel<2,gaussian>",
+            "achieved": achieved / 1e9, "peak": ex2.value / 1e9, "unit": "Gex2/s",
+            "frac": achieved / ex2.value if ex2.value else None,
+            "peak_source": "measured in this run: MUFU.EX2 microbenchmark (fsgg_probe_ex2_throughput)",
+            "nominal_peak": nominal / 1e9, "frac_of_nominal": achieved / nominal,
+            "algorithmic_unit": "one Gaussian kernel evaluation = one ex2 (SURVEY.md §8d)",
+            "evals_per_launch": tiled_perf / max(tiled_launches, 1),
+            "reference_equivalent_evals_per_launch": tiled_evals / max(tiled_launches, 1),
+            "reference_equivalent_rate": tiled_evals / max(tiled_s, 1e-12) / 1e9,
+            "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
+            "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
+            "traffic": traffic,
+        }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
@@ -385,7 +423,7 @@ def main():
         "kernel_evals_note": ("reference-equivalent Gaussian evaluations (2.38 n^2 sampler + n^2 "
                               "degree KDE in the reference; here the degree KDE is fused, levels "
                               "reuse partial rows and certified pruning skips sub-chunks below "
-                              "2^-80 of the node mass, so far fewer are executed)"),
+                              "2^-48 of the node mass, so far fewer are executed)"),
         "undirected_edges": edges, "undirected_edges_per_s": edges * K / total_s,
         "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "clocks": clk,
