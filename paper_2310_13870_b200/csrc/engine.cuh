@@ -148,7 +148,11 @@ struct KdeStats {
 };
 
 struct KdeWorkspace {
-  DevBuf partials, blk_off, cub_tmp;
+  // partials: per entry a row of 2^rd fp64 bucket sums (the node's
+  // descendants rd levels down); pyr: the same row's pairwise-sum pyramid,
+  // depths 1..rd-1 at offsets 2^m - 2 (a lookup then reads two values).
+  DevBuf partials, pyr, blk_off, cub_tmp;
+  uint32_t pyr_depth = 0;  // row depth the pyramid was built for (0: none)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~KdeWorkspace();
 };

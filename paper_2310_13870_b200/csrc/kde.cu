@@ -519,6 +519,50 @@ __global__ void finalize_kernel(const double* __restrict__ partials,
   if (groot) groot[i] = fmax(a + b, kSumFloor);
 }
 
+// Pairwise-sum pyramid of each entry's partial row (rd >= 2): one warp per
+// entry stages the 2^rd buckets in shared memory, writes depths rd-1 .. 1
+// (fixed pairwise order) to pyr, and the two depth-1 sums as the entry's
+// child sums. Lookups at the next levels then read two values per entry.
+__global__ void pyramid_kernel(const double* __restrict__ partials, uint32_t rd,
+                               const uint32_t* __restrict__ eg, uint32_t E, uint32_t level,
+                               const uint32_t* __restrict__ tfirst,
+                               const uint32_t* __restrict__ tlast, double* __restrict__ pyr,
+                               double* __restrict__ g1, double* __restrict__ g2,
+                               double* __restrict__ groot) {
+  extern __shared__ double psm[];
+  const uint32_t W = 1u << rd;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t i = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (i >= E) return;
+  double* a = psm + size_t(warp) * 2 * W;  // level m+1 values
+  double* b = a + W;                        // level m values
+  const double* row = partials + (size_t(i) << rd);
+  double* out = pyr + (size_t(i) << rd);
+  for (uint32_t k = lane; k < W; k += 32) a[k] = row[k];
+  __syncwarp();
+  for (uint32_t m = rd - 1; m >= 1; --m) {
+    const uint32_t cnt = 1u << m;
+    for (uint32_t k = lane; k < cnt; k += 32) {
+      const double v = a[2 * k] + a[2 * k + 1];
+      b[k] = v;
+      out[(cnt - 2) + k] = v;
+    }
+    __syncwarp();
+    for (uint32_t k = lane; k < cnt; k += 32) a[k] = b[k];
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    if (tlast[h] - tfirst[h] < 2) {
+      g1[i] = g2[i] = 0.0;
+    } else {
+      g1[i] = fmax(a[0], kSumFloor);
+      g2[i] = fmax(a[1], kSumFloor);
+      if (groot) groot[i] = fmax(a[0] + a[1], kSumFloor);
+    }
+  }
+}
+
 // ---- arbitrary-range evaluation (KdeEstimator::eval seam) -----------------
 __global__ void range_box_kernel(const float* __restrict__ pts, uint32_t d,
                                  uint32_t first, uint32_t last, float* lo,
@@ -700,6 +744,7 @@ void with_family(int family, F&& f) {
 }
 
 constexpr uint32_t kLowDMax = 8;
+constexpr uint32_t kPyramidMinDepth = 6;  // rows of >= 64 buckets get a sum pyramid
 constexpr uint32_t kTcDirectMax = 24;  // tensor-core levels: direct (warp per entry) for small nodes
 uint32_t env_u32(const char* name, uint32_t dflt) {  // development overrides
   const char* e = std::getenv(name);
@@ -851,9 +896,22 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   }
   FSGG_LAUNCH_CHECK();
   FSGG_CUDA(cudaEventRecord(ws.ev1, s));
-  finalize_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
-      partials, 1u << (rl - 1), lv.eg, E, lv.level, t.first.as<uint32_t>(),
-      t.last.as<uint32_t>(), g1, g2, groot);
+  ws.pyr_depth = 0;
+  if (rl >= kPyramidMinDepth) {
+    ws.pyr_depth = rl;
+    ws.pyr.ensure(size_t(E) << rl << 3, s);
+    const size_t per_warp = size_t(2) << rl << 3;
+    const uint32_t warps = uint32_t(std::max<size_t>(1, std::min<size_t>(8, (96u << 10) / per_warp)));
+    FSGG_CUDA(cudaFuncSetAttribute(pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(std::max<size_t>(per_warp * warps, 48u << 10))));
+    pyramid_kernel<<<ceil_div_u32(E, warps), warps * 32, per_warp * warps, s>>>(
+        partials, rl, lv.eg, E, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+        ws.pyr.as<double>(), g1, g2, groot);
+  } else {
+    finalize_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+        partials, 1u << (rl - 1), lv.eg, E, lv.level, t.first.as<uint32_t>(),
+        t.last.as<uint32_t>(), g1, g2, groot);
+  }
   FSGG_LAUNCH_CHECK();
   ds.launches += 2;
   unsigned long long perf = ev;

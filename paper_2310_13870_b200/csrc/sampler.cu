@@ -505,12 +505,12 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
 
 // Child sums from the partial row of the entry's ancestor at the last
 // compute level (row_level = level - j): that row holds the ancestor's
-// descendants 2^rd wide; this entry's node is its descendant idx at depth j,
-// whose children own `span` consecutive buckets each. Sums in fixed order.
+// descendants 2^rd wide and its pairwise-sum pyramid.
 __global__ void lookup_sums_kernel(uint32_t E, uint32_t level, uint32_t j, uint32_t rd,
                                    const uint32_t* __restrict__ eg,
                                    const uint32_t* __restrict__ eprow,
                                    const double* __restrict__ rows,
+                                   const double* __restrict__ pyr,
                                    const uint32_t* __restrict__ tfirst,
                                    const uint32_t* __restrict__ tlast,
                                    double* __restrict__ g1, double* __restrict__ g2,
@@ -524,14 +524,25 @@ __global__ void lookup_sums_kernel(uint32_t E, uint32_t level, uint32_t j, uint3
     if (size < 2) {
       g1[i] = g2[i] = 0.0;
     } else {
+      // the node is descendant idx (depth j) of the row's node; its children
+      // are entries 2 idx, 2 idx + 1 at depth j + 1: the row itself at the
+      // deepest level, else the row's pairwise-sum pyramid (kde.cu)
       const uint32_t idx = g & ((1u << j) - 1u);
-      const uint32_t span = 1u << (rd - j - 1);
-      const double* row = rows + (size_t(eprow[i]) << rd) + size_t(2 * idx) * span;
-      double a = 0.0, b = 0.0;
-      for (uint32_t k = 0; k < span; ++k) a += row[k];
-      for (uint32_t k = 0; k < span; ++k) b += row[span + k];
-      g1[i] = fmax(a, kSumFloor);
-      g2[i] = fmax(b, kSumFloor);
+      if (pyr || j + 1 == rd) {
+        const double* src = j + 1 == rd
+                                ? rows + (size_t(eprow[i]) << rd)
+                                : pyr + (size_t(eprow[i]) << rd) + ((2u << j) - 2u);
+        g1[i] = fmax(src[2 * idx], kSumFloor);
+        g2[i] = fmax(src[2 * idx + 1], kSumFloor);
+      } else {  // short rows: the children own `span` consecutive buckets each
+        const uint32_t span = 1u << (rd - j - 1);
+        const double* row = rows + (size_t(eprow[i]) << rd) + size_t(2 * idx) * span;
+        double a = 0.0, b = 0.0;
+        for (uint32_t k = 0; k < span; ++k) a += row[k];
+        for (uint32_t k = 0; k < span; ++k) b += row[span + k];
+        g1[i] = fmax(a, kSumFloor);
+        g2[i] = fmax(b, kSumFloor);
+      }
       ev = size;
     }
   }
@@ -920,7 +931,9 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
       lookup_sums_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
           E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
-          eprow[cur]->as<uint32_t>(), ws.partials.as<double>(), t.first.as<uint32_t>(),
+          eprow[cur]->as<uint32_t>(), ws.partials.as<double>(),
+          ws.pyr_depth == row_depth ? ws.pyr.as<double>() : nullptr,
+          t.first.as<uint32_t>(),
           t.last.as<uint32_t>(), g1.as<double>(), g2.as<double>(),
           lookup_evals.as<unsigned long long>());
       FSGG_LAUNCH_CHECK();
