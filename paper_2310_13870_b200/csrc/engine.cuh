@@ -136,6 +136,7 @@ struct LevelView {
   int prune = 1;                   // certified pruning of negligible sub-chunks
   const uint32_t* eg = nullptr;    // level-local slot per entry
   const uint32_t* goff = nullptr;  // num_slots + 1
+  uint32_t qbase = 0xffffffffu;    // level 0: entries are points qbase.. in order (else ~0)
 };
 
 struct KdeStats {
@@ -242,6 +243,12 @@ struct DfsArgs {
 };
 bool dfs_finish_supported(uint32_t d);
 void dfs_finish(Dataset& ds, const KernelSpec& ks, const DfsArgs& args);
+
+// ---- kde_sym.cu -----------------------------------------------------------
+// Root level with every pair evaluated once (row + column sums of block
+// pairs); writes rows [E][2^rd] for the points [qb, qe). false: unsupported.
+bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
+                        uint32_t rd, double* rows, unsigned long long* d_performed);
 
 // ---- walk.cu --------------------------------------------------------------
 // Entries holding a single ticket below nodes of kWalkMaxNode points leave

@@ -879,7 +879,12 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   unsigned long long* d_perf = d_evals + 1;
   FSGG_CUDA(cudaMemsetAsync(d_perf, 0, 8, s));
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
-  if (lowd) {
+  const bool sym = lowd && lv.level == 0 && lv.qbase != 0xffffffffu && lv.prune &&
+                   env_u32("FSGG_SYM", 1) != 0 &&
+                   kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials, d_perf);
+  if (sym) {
+    // every pair evaluated once (kde_sym.cu)
+  } else if (lowd) {
     with_lowd(ks.family, d, [&](auto op) {
       op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf);
     });

@@ -1,0 +1,372 @@
+// Symmetric root level: the n^2 pass of the descent evaluates every pair once.
+//
+// At the root every query is also a source, and k(q, x) = k(x, q): the row
+// sums a query needs (its partial row over the root's descendants) and the
+// column sums its partner block needs come out of the same evaluations. The
+// point set is cut into tree-aligned blocks (nodes at depth Lb, <= 256
+// points); for every pair of blocks I <= J that is not prunable (bounding-box
+// distance) one CTA evaluates the |I| x |J| tile once and writes
+//   * the row sums of I's points over J  -> I's slot for partner J,
+//   * the column sums of J's points over I -> J's slot for partner I,
+// each as one fp32 value per point (a fixed-order sum of <= 256 terms).
+// sym_rows_kernel then folds every point's partner values, in ascending
+// partner order, into its fp64 bucket row (buckets = tree nodes at depth rd,
+// aligned with the blocks), which is exactly the row format of the tiled
+// kernels (kde.cu) — lookups and the pyramid are unchanged.
+//
+// Pruning per (point, partner block) keeps the tiled kernel's certified rule
+// (bound below 2^-kPruneBits of half the root mass, >= 1/2): a pruned
+// partner's value is dropped for that point only. Every value depends on the
+// two blocks alone, so a shard (a contiguous query range) computes the tiles
+// touching its blocks and gets bit-identical rows.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "engine.cuh"
+#include "kde_math.cuh"
+
+namespace fsgg {
+namespace {
+
+constexpr int kSymThreads = 128;  // 4 warps
+constexpr int kSymWarps = kSymThreads / 32;
+constexpr uint32_t kSymBlock = 256;  // max points per block
+constexpr int kSymRows = 8;          // rows per lane: 32 lanes x 8 = 256
+constexpr uint32_t kSymMinBlock = 192;
+
+struct SymTile {
+  uint32_t I, J, slotI, slotJ;
+};
+
+__device__ __forceinline__ float block_dist(const float* lo, const float* hi, uint32_t a,
+                                            uint32_t b, uint32_t d, int family) {
+  float acc = 0.f;
+  for (uint32_t k = 0; k < d; ++k) {
+    const float g = fmaxf(0.f, fmaxf(lo[size_t(b) * d + k] - hi[size_t(a) * d + k],
+                                     lo[size_t(a) * d + k] - hi[size_t(b) * d + k]));
+    acc = family == 2 ? acc + g : fmaf(g, g, acc);
+  }
+  return family == 1 ? sqrtf(acc) : acc;
+}
+
+// Block pair (a, b) can contribute to some point of either block.
+__device__ __forceinline__ bool pair_active(const float* lo, const float* hi,
+                                            const uint32_t* bf, const uint32_t* bl, uint32_t a,
+                                            uint32_t b, uint32_t d, int family, float scale,
+                                            float bits) {
+  const float off = scale * block_dist(lo, hi, a, b, d, family);
+  const float na = float(bl[a] - bf[a]), nb = float(bl[b] - bf[b]);
+  return off <= __log2f(fmaxf(na, nb)) + bits;
+}
+
+__global__ void sym_count_kernel(uint32_t B, const float* __restrict__ lo,
+                                 const float* __restrict__ hi, const uint32_t* __restrict__ bf,
+                                 const uint32_t* __restrict__ bl, uint32_t d, int family,
+                                 float scale, float bits, uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t red[8];
+  const uint32_t I = blockIdx.x;
+  uint32_t c = 0;
+  for (uint32_t J = threadIdx.x; J < B; J += blockDim.x)
+    c += pair_active(lo, hi, bf, bl, I, J, d, family, scale, bits) ? 1u : 0u;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) t += red[w];
+    cnt[I] = t;
+  }
+}
+
+// Ordered compaction of I's active partners (ascending J).
+__global__ void sym_fill_kernel(uint32_t B, const float* __restrict__ lo,
+                                const float* __restrict__ hi, const uint32_t* __restrict__ bf,
+                                const uint32_t* __restrict__ bl, uint32_t d, int family,
+                                float scale, float bits, const uint32_t* __restrict__ poff,
+                                uint32_t* __restrict__ plist) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t base;
+  const uint32_t I = blockIdx.x;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) base = poff[I];
+  __syncthreads();
+  for (uint32_t J0 = 0; J0 < B; J0 += blockDim.x) {
+    const uint32_t J = J0 + threadIdx.x;
+    const bool a = J < B && pair_active(lo, hi, bf, bl, I, J, d, family, scale, bits);
+    const unsigned m = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+    for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+      if (k < w) before += wsum[k];
+      total += wsum[k];
+    }
+    if (a) plist[base + before + __popc(m & ((1u << lane) - 1u))] = J;
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    __syncthreads();
+  }
+}
+
+// Tiles (I <= J) that touch the query blocks [b0, b1].
+__global__ void sym_tiles_kernel(uint32_t B, const uint32_t* __restrict__ poff,
+                                 const uint32_t* __restrict__ plist, uint32_t b0, uint32_t b1,
+                                 SymTile* __restrict__ tiles, uint32_t* __restrict__ ntiles) {
+  const uint32_t I = blockIdx.x;
+  for (uint32_t k = poff[I] + threadIdx.x; k < poff[I + 1]; k += blockDim.x) {
+    const uint32_t J = plist[k];
+    if (J < I) continue;
+    const bool touch = (I >= b0 && I <= b1) || (J >= b0 && J <= b1);
+    if (!touch) continue;
+    // position of I in J's (ascending) partner list
+    uint32_t lo = poff[J], hi = poff[J + 1];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (plist[mid] < I)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const uint32_t at = atomicAdd(ntiles, 1u);
+    tiles[at] = SymTile{I, J, k - poff[I], lo - poff[J]};
+  }
+}
+
+template <int D, int FAM>
+__global__ void __launch_bounds__(kSymThreads)
+    sym_tile_kernel(const float* __restrict__ pts, const SymTile* __restrict__ tiles,
+                    const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
+                    const float* __restrict__ lo, const float* __restrict__ hi, float scale,
+                    float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
+                    unsigned long long* __restrict__ performed) {
+  __shared__ __align__(16) float2 sx[kSymBlock * D];
+  __shared__ float rowred[kSymWarps][kSymBlock];
+  __shared__ float colv[kSymBlock];
+  const SymTile tl = tiles[blockIdx.x];
+  const uint32_t fi = bf[tl.I], ni = bl[tl.I] - fi;
+  const uint32_t fj = bf[tl.J], nj = bl[tl.J] - fj;
+  for (uint32_t idx = threadIdx.x; idx < nj * D; idx += blockDim.x) {
+    const float v = -__ldg(pts + size_t(fj) * D + idx);
+    sx[idx] = make_float2(v, v);
+  }
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // this lane's rows (points of I) as 4 packed pairs; absent rows far away
+  float2 q2[kSymRows / 2][D];
+#pragma unroll
+  for (int p = 0; p < kSymRows / 2; ++p) {
+    const uint32_t r0 = lane * kSymRows + 2 * p, r1 = r0 + 1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float a = r0 < ni ? __ldg(pts + size_t(fi + r0) * D + k) : 1e18f;
+      const float b = r1 < ni ? __ldg(pts + size_t(fi + r1) * D + k) : 1e18f;
+      q2[p][k] = make_float2(a, b);
+    }
+  }
+  __syncthreads();
+  const float2 ms = make_float2(-scale, -scale);
+  float2 racc[kSymRows / 2];
+#pragma unroll
+  for (int p = 0; p < kSymRows / 2; ++p) racc[p] = make_float2(0.f, 0.f);
+  float ccol0 = 0.f, ccol1 = 0.f;  // column sums of this warp's sources lane, lane + 32
+  const uint32_t j0 = w * 64, j1 = min(nj, j0 + 64);
+  for (uint32_t j = j0; j < j1; ++j) {
+    const float2* x = sx + j * D;
+    float2 es = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < kSymRows / 2; ++p) {
+      float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+#pragma unroll
+      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
+      t = fam_finish<FAM>(t);
+      const float2 arg = __fmul2_rn(t, ms);
+      const float2 e = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
+      racc[p] = __fadd2_rn(racc[p], e);
+      es = __fadd2_rn(es, e);
+    }
+    float c = es.x + es.y;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == ((j - j0) & 31)) {
+      if (j - j0 < 32)
+        ccol0 = c;
+      else
+        ccol1 = c;
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < kSymRows / 2; ++p) {
+    rowred[w][lane * kSymRows + 2 * p] = racc[p].x;
+    rowred[w][lane * kSymRows + 2 * p + 1] = racc[p].y;
+  }
+  if (j0 + lane < nj) colv[j0 + lane] = ccol0;
+  if (j0 + 32 + lane < nj) colv[j0 + 32 + lane] = ccol1;
+  __syncthreads();
+  // rows of I over J, columns of J over I (the diagonal tile has rows only);
+  // a point that prunes the partner block drops its value
+  for (uint32_t t = threadIdx.x; t < ni; t += blockDim.x) {
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSymWarps; ++k) v += rowred[k][t];
+    float q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = __ldg(pts + size_t(fi + t) * D + k);
+    const float off = scale * box_dist<FAM>(q, lo + size_t(tl.J) * D, hi + size_t(tl.J) * D, D);
+    if (off > __log2f(float(nj)) + bits) v = 0.f;
+    P[(size_t(poff[tl.I]) + tl.slotI) * kSymBlock + t] = v;
+  }
+  if (tl.I != tl.J) {
+    for (uint32_t t = threadIdx.x; t < nj; t += blockDim.x) {
+      float v = colv[t];
+      float x[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = __ldg(pts + size_t(fj + t) * D + k);
+      const float off = scale * box_dist<FAM>(x, lo + size_t(tl.I) * D, hi + size_t(tl.I) * D, D);
+      if (off > __log2f(float(ni)) + bits) v = 0.f;
+      P[(size_t(poff[tl.J]) + tl.slotJ) * kSymBlock + t] = v;
+    }
+  }
+  if (performed && threadIdx.x == 0) atomicAdd(performed, (unsigned long long)ni * nj);
+}
+
+// Fold each point's partner values, in ascending partner order, into its
+// fp64 bucket row (bucket of partner J = J >> shift).
+constexpr uint32_t kSymBucketChunk = 16;  // 16 x 256 fp64 = 32 KiB of shared memory
+__global__ void __launch_bounds__(kSymBlock)
+    sym_rows_kernel(const float* __restrict__ P, const uint32_t* __restrict__ poff,
+                    const uint32_t* __restrict__ plist, const uint32_t* __restrict__ bf,
+                    const uint32_t* __restrict__ bl, uint32_t blk0, uint32_t shift,
+                    uint32_t rd, uint32_t qb, uint32_t qe, double* __restrict__ rows) {
+  __shared__ double acc[kSymBucketChunk][kSymBlock];
+  const uint32_t I = blk0 + blockIdx.x;
+  const uint32_t f = bf[I], ni = bl[I] - f;
+  const uint32_t t = threadIdx.x;
+  const uint32_t W = 1u << rd;
+  const uint32_t p0 = poff[I], p1 = poff[I + 1];
+  const uint32_t pt = f + t;
+  const bool mine = t < ni && pt >= qb && pt < qe;
+  uint32_t k = p0;
+  for (uint32_t b0 = 0; b0 < W; b0 += kSymBucketChunk) {
+#pragma unroll
+    for (uint32_t c = 0; c < kSymBucketChunk; ++c) acc[c][t] = 0.0;
+    for (; k < p1 && (plist[k] >> shift) < b0 + kSymBucketChunk; ++k) {
+      const uint32_t c = (plist[k] >> shift) - b0;
+      if (t < ni) acc[c][t] += double(P[size_t(k) * kSymBlock + t]);
+    }
+    if (mine) {
+      double* out = rows + (size_t(pt - qb) << rd) + b0;
+      const uint32_t cmax = min(kSymBucketChunk, W - b0);
+      for (uint32_t c = 0; c < cmax; ++c) out[c] = acc[c][t];
+    }
+  }
+}
+
+template <class F>
+void sym_by_dim(uint32_t d, F&& f) {
+  switch (d) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 5: f(std::integral_constant<int, 5>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 7: f(std::integral_constant<int, 7>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    default: throw ConfigError("symmetric root supports d <= 8");
+  }
+}
+
+}  // namespace
+
+bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
+                        uint32_t rd, double* rows, unsigned long long* d_performed) {
+  const TreeTable& t = ds.tree;
+  if (ds.d < 1 || ds.d > 8 || !t.has_boxes) return false;
+  // blocks: tree nodes at depth Lb with <= 256 points, Lb >= rd
+  uint32_t Lb = 0;
+  while (((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > kSymBlock) ++Lb;
+  if (Lb > t.depth || Lb < rd || Lb > 20) return false;
+  // tiles are 256 x 256 in registers: smaller blocks leave lanes idle (C4's
+  // 151-point blocks measured slower than the one-sided tiled kernel)
+  if ((uint64_t(ds.n) >> Lb) < kSymMinBlock) return false;
+  cudaStream_t s = ds.stream;
+  const uint32_t B = 1u << Lb;
+  const uint64_t hb = uint64_t(B) - 1;
+  const uint32_t* bf = t.first.as<uint32_t>() + hb;
+  const uint32_t* bl = t.last.as<uint32_t>() + hb;
+  const float* lo = t.lo.as<float>() + hb * ds.d;
+  const float* hi = t.hi.as<float>() + hb * ds.d;
+  const float bits = kPruneBits + 1.f;  // half the root mass (>= 1/2)
+
+  DevBuf& cnt = ds.buf("sym.cnt", size_t(B + 1) * 4);
+  DevBuf& poff = ds.buf("sym.poff", size_t(B + 1) * 4);
+  DevBuf& tmp = ds.buf("sym.tmp", 8);
+  sym_count_kernel<<<B, 256, 0, s>>>(B, lo, hi, bf, bl, ds.d, ks.family, ks.scale, bits,
+                                     cnt.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  FSGG_CUDA(cudaMemsetAsync(cnt.as<uint32_t>() + B, 0, 4, s));
+  size_t tb = 0;
+  FSGG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<uint32_t>(), poff.as<uint32_t>(),
+                                          B + 1, s));
+  tmp.ensure(tb, s);
+  FSGG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.as<void>(), tb, cnt.as<uint32_t>(),
+                                          poff.as<uint32_t>(), B + 1, s));
+  uint32_t npart = 0;
+  FSGG_CUDA(cudaMemcpyAsync(&npart, poff.as<uint32_t>() + B, 4, cudaMemcpyDeviceToHost, s));
+  // query blocks: the blocks holding points qb and qe - 1
+  std::vector<uint32_t> hbf(B), hbl(B);
+  FSGG_CUDA(cudaMemcpyAsync(hbf.data(), bf, size_t(B) * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(hbl.data(), bl, size_t(B) * 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  uint32_t b0 = 0, b1 = B - 1;
+  while (b0 < B && hbl[b0] <= qb) ++b0;
+  while (b1 > 0 && hbf[b1] >= qe) --b1;
+  DevBuf& plist = ds.buf("sym.plist", size_t(npart) * 4 + 4);
+  sym_fill_kernel<<<B, 256, 0, s>>>(B, lo, hi, bf, bl, ds.d, ks.family, ks.scale, bits,
+                                    poff.as<uint32_t>(), plist.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  DevBuf& tiles = ds.buf("sym.tiles", size_t(npart) * sizeof(SymTile) + 16);
+  DevBuf& ntiles = ds.buf("sym.ntiles", 8);
+  FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 4, s));
+  sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1,
+                                     tiles.as<SymTile>(), ntiles.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  uint32_t nt = 0;
+  FSGG_CUDA(cudaMemcpyAsync(&nt, ntiles.as<void>(), 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  DevBuf& P = ds.buf("sym.P", size_t(npart) * kSymBlock * 4 + 4);
+  if (nt > 0) {
+    sym_by_dim(ds.d, [&](auto dim) {
+      constexpr int D = decltype(dim)::value;
+      switch (ks.family) {
+        case 0:
+          sym_tile_kernel<D, 0><<<nt, kSymThreads, 0, s>>>(
+              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
+              poff.as<uint32_t>(), P.as<float>(), d_performed);
+          break;
+        case 1:
+          sym_tile_kernel<D, 1><<<nt, kSymThreads, 0, s>>>(
+              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
+              poff.as<uint32_t>(), P.as<float>(), d_performed);
+          break;
+        default:
+          sym_tile_kernel<D, 2><<<nt, kSymThreads, 0, s>>>(
+              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
+              poff.as<uint32_t>(), P.as<float>(), d_performed);
+          break;
+      }
+    });
+    FSGG_LAUNCH_CHECK();
+  }
+  if (b0 <= b1) {
+    sym_rows_kernel<<<b1 - b0 + 1, kSymBlock, 0, s>>>(P.as<float>(), poff.as<uint32_t>(),
+                                                     plist.as<uint32_t>(), bf, bl, b0,
+                                                     Lb - rd, rd, qb, qe, rows);
+    FSGG_LAUNCH_CHECK();
+  }
+  ds.launches += 7;
+  return true;
+}
+
+}  // namespace fsgg

@@ -836,6 +836,9 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   const uint32_t goff0[2] = {0, nq};
   FSGG_CUDA(cudaMemcpyAsync(goff[0]->as<void>(), goff0, 8, cudaMemcpyHostToDevice, s));
 
+  // level-0 entries are a contiguous point range (full builds and shards)
+  const bool contiguous =
+      nq > 0 && uint64_t(req.queries.back()) - req.queries.front() + 1 == nq;
   const uint64_t prefix = route_key_prefix(req.seed);
   uint32_t E = nq;
   int cur = 0;
@@ -925,6 +928,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     lv.elm = level == 0 ? nullptr : elm[cur]->as<float>();
     lv.prune = req.prune;
     lv.goff = goff[cur]->as<uint32_t>();
+    if (level == 0 && contiguous) lv.qbase = req.queries.front();
     const bool lookup = have_rows && level - row_level < row_depth;
     bool self_rows = false;
     if (lookup) {

@@ -354,3 +354,32 @@ def test_single_ticket_walks_match_level_synchronous(rng):
         assert list(outs[0][1].entries_per_level) == list(d.entries_per_level)
         assert list(outs[0][1].tickets_per_level) == list(d.tickets_per_level)
         assert outs[0][1].degenerate_draws == d.degenerate_draws
+
+
+def test_symmetric_root_matches_one_sided():
+    """The symmetric root pass (kde_sym.cu, each pair evaluated once) and the
+    one-sided tiled pass give the same samples and edge set; g_full differs
+    only by fp32 summation order (weights within 1e-6)."""
+    import os
+    p, _ = datasets.make_moons(60000, 0.05, 11)
+    ds = F.Dataset(p.astype(np.float32))
+    k = F.Kernel(F.KernelFamily.gaussian, 0.06)
+    cfg = F.SparsifierConfig(rounds=16, seed=3)
+    outs = []
+    old = os.environ.get("FSGG_SYM")
+    try:
+        for sym in ("0", "1"):
+            os.environ["FSGG_SYM"] = sym
+            tri = F.sample_neighbors_counted(ds, k, np.arange(60000), 16, 3)
+            g, rep, _ = F.build_similarity_graph(ds, k, cfg, report=True)
+            outs.append((tri, g, rep))
+    finally:
+        if old is None:
+            os.environ.pop("FSGG_SYM", None)
+        else:
+            os.environ["FSGG_SYM"] = old
+    (t0, g0, r0), (t1, g1, r1) = outs
+    assert np.array_equal(t0, t1)
+    assert np.array_equal(g0.u, g1.u) and np.array_equal(g0.v, g1.v)
+    np.testing.assert_allclose(g1.w, g0.w, rtol=1e-6)
+    assert r1.kernel_evals_performed < r0.kernel_evals_performed
