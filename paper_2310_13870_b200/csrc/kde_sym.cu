@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(kSymThreads)
   const SymTile tl = tiles[blockIdx.x];
   const uint32_t fi = bf[tl.I], ni = bl[tl.I] - fi;
   const uint32_t fj = bf[tl.J], nj = bl[tl.J] - fj;
-  for (uint32_t idx = threadIdx.x; idx < nj * D; idx += blockDim.x) {
-    const float v = -__ldg(pts + size_t(fj) * D + idx);
+  // sources of J, negated and duplicated; slots past nj sit far away (their
+  // terms underflow to 0), so the unrolled source loop needs no guard
+  for (uint32_t idx = threadIdx.x; idx < kSymBlock * D; idx += blockDim.x) {
+    const float v = idx < nj * D ? -__ldg(pts + size_t(fj) * D + idx) : -1e18f;
     sx[idx] = make_float2(v, v);
   }
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -169,39 +171,45 @@ __global__ void __launch_bounds__(kSymThreads)
   float2 racc[kSymRows / 2];
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) racc[p] = make_float2(0.f, 0.f);
-  float ccol0 = 0.f, ccol1 = 0.f;  // column sums of this warp's sources lane, lane + 32
-  const uint32_t j0 = w * 64, j1 = min(nj, j0 + 64);
-  for (uint32_t j = j0; j < j1; ++j) {
-    const float2* x = sx + j * D;
-    float2 es = make_float2(0.f, 0.f);
+  // warp w: sources [64 w, 64 w + 64) in two batches of 32
+  for (uint32_t jb = w * 64; jb < w * 64 + 64 && jb < nj; jb += 32) {
+    float c[32];  // this lane's 8-row partial of each source's column sum
 #pragma unroll
-    for (int p = 0; p < kSymRows / 2; ++p) {
-      float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+    for (int jj = 0; jj < 32; ++jj) {
+      const float2* x = sx + (jb + jj) * D;
+      float2 es = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
-      t = fam_finish<FAM>(t);
-      const float2 arg = __fmul2_rn(t, ms);
-      const float2 e = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
-      racc[p] = __fadd2_rn(racc[p], e);
-      es = __fadd2_rn(es, e);
+      for (int p = 0; p < kSymRows / 2; ++p) {
+        float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+#pragma unroll
+        for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
+        t = fam_finish<FAM>(t);
+        const float2 arg = __fmul2_rn(t, ms);
+        const float2 e = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
+        racc[p] = __fadd2_rn(racc[p], e);
+        es = p == 0 ? e : __fadd2_rn(es, e);
+      }
+      c[jj] = es.x + es.y;
     }
-    float c = es.x + es.y;
+    // butterfly transpose-reduction: afterwards lane l holds the column sum
+    // of source jb + l over all 32 lanes (31 shuffles for 32 sources)
 #pragma unroll
-    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if (lane == ((j - j0) & 31)) {
-      if (j - j0 < 32)
-        ccol0 = c;
-      else
-        ccol1 = c;
+    for (int st = 16; st >= 1; st >>= 1) {
+      const bool up = (lane & st) != 0;
+#pragma unroll
+      for (int i = 0; i < st; ++i) {
+        const float keep = up ? c[i + st] : c[i];
+        const float send = up ? c[i] : c[i + st];
+        c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+      }
     }
+    if (jb + lane < nj) colv[jb + lane] = c[0];
   }
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) {
     rowred[w][lane * kSymRows + 2 * p] = racc[p].x;
     rowred[w][lane * kSymRows + 2 * p + 1] = racc[p].y;
   }
-  if (j0 + lane < nj) colv[j0 + lane] = ccol0;
-  if (j0 + 32 + lane < nj) colv[j0 + 32 + lane] = ccol1;
   __syncthreads();
   // rows of I over J, columns of J over I (the diagonal tile has rows only);
   // a point that prunes the partner block drops its value
