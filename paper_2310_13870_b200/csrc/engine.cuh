@@ -249,6 +249,8 @@ void dfs_finish(Dataset& ds, const KernelSpec& ks, const DfsArgs& args);
 // pairs); writes rows [E][2^rd] for the points [qb, qe). false: unsupported.
 bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
                         uint32_t rd, double* rows, unsigned long long* d_performed);
+// Depth of the symmetric pass's blocks (0: the pass does not apply).
+uint32_t sym_block_depth(const Dataset& ds);
 
 // ---- walk.cu --------------------------------------------------------------
 // Entries holding a single ticket below nodes of kWalkMaxNode points leave

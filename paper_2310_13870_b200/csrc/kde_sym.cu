@@ -287,17 +287,24 @@ void sym_by_dim(uint32_t d, F&& f) {
 
 }  // namespace
 
+uint32_t sym_block_depth(const Dataset& ds) {
+  const TreeTable& t = ds.tree;
+  if (ds.d < 1 || ds.d > 8 || !t.has_boxes) return 0;
+  // blocks: tree nodes at depth Lb with <= 256 points
+  uint32_t Lb = 0;
+  while (((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > kSymBlock) ++Lb;
+  if (Lb == 0 || Lb > t.depth || Lb > 20) return 0;
+  // tiles are 256 x 256 in registers: smaller blocks leave lanes idle (C4's
+  // 151-point blocks measured slower than the one-sided tiled kernel)
+  if ((uint64_t(ds.n) >> Lb) < kSymMinBlock) return 0;
+  return Lb;
+}
+
 bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
                         uint32_t rd, double* rows, unsigned long long* d_performed) {
   const TreeTable& t = ds.tree;
-  if (ds.d < 1 || ds.d > 8 || !t.has_boxes) return false;
-  // blocks: tree nodes at depth Lb with <= 256 points, Lb >= rd
-  uint32_t Lb = 0;
-  while (((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > kSymBlock) ++Lb;
-  if (Lb > t.depth || Lb < rd || Lb > 20) return false;
-  // tiles are 256 x 256 in registers: smaller blocks leave lanes idle (C4's
-  // 151-point blocks measured slower than the one-sided tiled kernel)
-  if ((uint64_t(ds.n) >> Lb) < kSymMinBlock) return false;
+  const uint32_t Lb = sym_block_depth(ds);
+  if (Lb == 0 || Lb < rd) return false;
   cudaStream_t s = ds.stream;
   const uint32_t B = 1u << Lb;
   const uint64_t hb = uint64_t(B) - 1;
