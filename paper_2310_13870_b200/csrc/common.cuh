@@ -61,6 +61,15 @@ __host__ __device__ __forceinline__ uint64_t route_key(uint64_t prefix,
   uint64_t k = splitmix64(prefix ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
   return splitmix64(k ^ splitmix64(b ^ 0x3c6ef372fe94f82bULL));
 }
+// Same key with the query's link splitmix64(b ^ ...) precomputed (a walk
+// keeps its query for every node it visits).
+__host__ __device__ __forceinline__ uint64_t query_link(uint64_t b) {
+  return splitmix64(b ^ 0x3c6ef372fe94f82bULL);
+}
+__host__ __device__ __forceinline__ uint64_t route_key_q(uint64_t prefix, uint64_t a,
+                                                         uint64_t qlink) {
+  return splitmix64(splitmix64(prefix ^ splitmix64(a ^ 0xbb67ae8584caa73bULL)) ^ qlink);
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

@@ -73,7 +73,7 @@ struct LowDTile {
 };
 
 __device__ __forceinline__ double rescale(double acc, float off) {
-  return off > 0.f ? acc * exp2(-static_cast<double>(off)) : acc;
+  return rescale_off(acc, off);  // kde_math.cuh
 }
 
 // Work-item -> node slot lookup: largest g with blk_off[g] <= blk.

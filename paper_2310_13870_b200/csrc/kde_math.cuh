@@ -52,8 +52,13 @@ __device__ __forceinline__ float box_dist(const float* q, const float* lo,
 }
 
 // Rescale an fp32 sum of offset terms 2^(off - scale*dist) back to k units.
+// 2^-off = 2^-j * 2^-(off - j) with j = floor(off): an exact power of two
+// times a MUFU ex2 of a value in (-1, 0] (rel. error ~1e-7, the order of the
+// fp32 terms themselves) instead of an fp64 exp2 per child.
 __device__ __forceinline__ double rescale_off(double acc, float off) {
-  return off > 0.f ? acc * exp2(-static_cast<double>(off)) : acc;
+  if (!(off > 0.f)) return acc;
+  const float j = floorf(off);
+  return ldexp(acc * static_cast<double>(ex2_approx(j - off)), -static_cast<int>(j));
 }
 
 // Child sums of a small node (heap index h, points [f, l), l - f >= 2) for

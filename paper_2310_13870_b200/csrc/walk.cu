@@ -31,8 +31,9 @@ struct Decision {
 };
 
 __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_t f,
-                                           uint32_t l, uint32_t q, uint64_t key_prefix,
-                                           int rng_mode, uint64_t seed, bool want_near) {
+                                           uint32_t l, uint32_t q, uint64_t qlink,
+                                           uint64_t key_prefix, int rng_mode, uint64_t seed,
+                                           bool want_near) {
   Decision d{false, false, false};
   double p;
   if (a <= kSumFloor && b <= kSumFloor) {
@@ -49,7 +50,7 @@ __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_
     const uint64_t thr = static_cast<uint64_t>(ceil(P));
     uint64_t m;
     if (rng_mode == 0) {
-      m = splitmix64(route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q))) >> 11;
+      m = splitmix64(route_key_q(key_prefix, (uint64_t(f) << 32) | l, qlink)) >> 11;
       if (want_near) {
         const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
         const double M = rel * fmin(p, 1.0 - p) * 9007199254740992.0 + 1.0;
@@ -88,8 +89,10 @@ __global__ void __launch_bounds__(kWalkThreads)
   uint64_t h = 0;
   float em = 0.f;
   float qc[D];
+  uint64_t qlink = 0;
   if (live) {
     q = wq[i];
+    qlink = query_link(q);
     h = wh[i];
     em = welm[i];
     lev = 31 - __clz(uint32_t(h) + 1);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(kWalkThreads)
         direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
         double a = fmax(s[0], kSumFloor), b = fmax(s[1], kSumFloor);
         ev = l - f;
-        Decision dc = decide(a, b, em, f, l, q, key_prefix, rng_mode, seed, check);
+        Decision dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, check);
         if (check && dc.near) {
           // tie guard: re-decide on fp64 sums (kernel_f64, index order)
           const uint32_t mid = f + (l - f) / 2;
@@ -125,11 +128,13 @@ __global__ void __launch_bounds__(kWalkThreads)
           for (uint32_t j = mid; j < l; ++j) e1 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
           a = fmax(e0, kSumFloor);
           b = fmax(e1, kSumFloor);
-          dc = decide(a, b, em, f, l, q, key_prefix, rng_mode, seed, false);
+          dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, false);
           tie = 1;
         }
         dg = dc.degenerate ? 1u : 0u;
-        em = static_cast<float>(log2(dc.left ? a : b));
+        // log2 of the chosen child's sum, to integer precision (only the tie
+        // margin's far-node widening reads it)
+        em = float(int((__double_as_longlong(dc.left ? a : b) >> 52) & 0x7ff) - 1023);
         h = dc.left ? 2 * h + 1 : 2 * h + 2;
         ++lev;
       }
