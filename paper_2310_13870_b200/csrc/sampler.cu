@@ -506,44 +506,65 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
 // Child sums from the partial row of the entry's ancestor at the last
 // compute level (row_level = level - j): that row holds the ancestor's
 // descendants 2^rd wide and its pairwise-sum pyramid.
-__global__ void lookup_sums_kernel(uint32_t E, uint32_t level, uint32_t j, uint32_t rd,
-                                   const uint32_t* __restrict__ eg,
-                                   const uint32_t* __restrict__ eprow,
-                                   const double* __restrict__ rows,
-                                   const double* __restrict__ pyr,
-                                   const uint32_t* __restrict__ tfirst,
-                                   const uint32_t* __restrict__ tlast,
-                                   double* __restrict__ g1, double* __restrict__ g2,
-                                   unsigned long long* __restrict__ evals) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int kLookupThreads = 256;
+constexpr int kLookupUnroll = 4;  // entries per thread, all loads issued first
+
+__global__ void __launch_bounds__(kLookupThreads)
+    lookup_sums_kernel(uint32_t E, uint32_t level, uint32_t j, uint32_t rd,
+                       const uint32_t* __restrict__ eg, const uint32_t* __restrict__ eprow,
+                       const double* __restrict__ rows, const double* __restrict__ pyr,
+                       const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                       double* __restrict__ g1, double* __restrict__ g2,
+                       unsigned long long* __restrict__ evals) {
+  constexpr int U = kLookupUnroll;
+  const uint32_t base = blockIdx.x * (kLookupThreads * U) + threadIdx.x;
+  uint32_t g[U], pr[U], size[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kLookupThreads;
+    g[u] = i < E ? eg[i] : 0u;
+    pr[u] = i < E ? eprow[i] : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t h = ((1ull << level) - 1) + g[u];
+    size[u] = base + u * kLookupThreads < E ? tlast[h] - tfirst[h] : 0u;
+  }
+  // the node is descendant idx (depth j) of the row's node; its children are
+  // entries 2 idx, 2 idx + 1 at depth j + 1: the row itself at the deepest
+  // level, else the row's pairwise-sum pyramid (kde.cu), else (short rows)
+  // `span` consecutive buckets each
+  const bool two = pyr || j + 1 == rd;
+  const uint32_t span = two ? 1u : 1u << (rd - j - 1);
+  double a[U], b[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a[u] = b[u] = 0.0;
+    if (size[u] >= 2) {
+      const uint32_t idx = g[u] & ((1u << j) - 1u);
+      const double* src = j + 1 == rd || !pyr
+                              ? rows + (size_t(pr[u]) << rd) + size_t(2 * idx) * span
+                              : pyr + (size_t(pr[u]) << rd) + ((2u << j) - 2u) + 2 * idx;
+      if (two) {
+        a[u] = src[0];
+        b[u] = src[1];
+      } else {
+        for (uint32_t k = 0; k < span; ++k) a[u] += src[k];
+        for (uint32_t k = 0; k < span; ++k) b[u] += src[span + k];
+      }
+    }
+  }
   unsigned long long ev = 0;
-  if (i < E) {
-    const uint32_t g = eg[i];
-    const uint64_t h = ((1ull << level) - 1) + g;
-    const uint32_t size = tlast[h] - tfirst[h];
-    if (size < 2) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kLookupThreads;
+    if (i >= E) continue;
+    if (size[u] < 2) {
       g1[i] = g2[i] = 0.0;
     } else {
-      // the node is descendant idx (depth j) of the row's node; its children
-      // are entries 2 idx, 2 idx + 1 at depth j + 1: the row itself at the
-      // deepest level, else the row's pairwise-sum pyramid (kde.cu)
-      const uint32_t idx = g & ((1u << j) - 1u);
-      if (pyr || j + 1 == rd) {
-        const double* src = j + 1 == rd
-                                ? rows + (size_t(eprow[i]) << rd)
-                                : pyr + (size_t(eprow[i]) << rd) + ((2u << j) - 2u);
-        g1[i] = fmax(src[2 * idx], kSumFloor);
-        g2[i] = fmax(src[2 * idx + 1], kSumFloor);
-      } else {  // short rows: the children own `span` consecutive buckets each
-        const uint32_t span = 1u << (rd - j - 1);
-        const double* row = rows + (size_t(eprow[i]) << rd) + size_t(2 * idx) * span;
-        double a = 0.0, b = 0.0;
-        for (uint32_t k = 0; k < span; ++k) a += row[k];
-        for (uint32_t k = 0; k < span; ++k) b += row[span + k];
-        g1[i] = fmax(a, kSumFloor);
-        g2[i] = fmax(b, kSumFloor);
-      }
-      ev = size;
+      g1[i] = fmax(a[u], kSumFloor);
+      g2[i] = fmax(b[u], kSumFloor);
+      ev += size[u];
     }
   }
   for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
@@ -614,32 +635,43 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
     }
   }
   if (!wq) return;
-  // warp-aggregated reservation in the walk list (order is irrelevant: each
-  // walk is independent and leaves land in per-query rows)
-  const uint32_t lane = threadIdx.x & 31;
+  // CTA-aggregated reservation in the walk list: one atomic per CTA (a
+  // per-warp atomic on the single counter serialised ~2M times a level).
+  // Order within the list is irrelevant: walks are independent and leaves
+  // land in per-query rows.
+  __shared__ uint32_t wtot[8], wbase;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = nw;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= uint32_t(o)) incl += y;
   }
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total == 0) return;
-  uint32_t base = 0;
-  if (lane == 31) base = atomicAdd(wcount, total);
-  base = __shfl_sync(0xffffffffu, base, 31);
-  uint32_t pos = base + incl - nw;
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+      const uint32_t c = wtot[k];
+      wtot[k] = t;
+      t += c;
+    }
+    wbase = t ? atomicAdd(wcount, t) : 0u;
+  }
+  __syncthreads();
+  if (nw == 0) return;
+  uint32_t pos = wbase + wtot[warp] + incl - nw;
   const uint32_t hbase = (1u << (level + 1)) - 1;
   if (wmask & 1u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g;
-    welm[pos] = static_cast<float>(log2(g1[i]));
+    welm[pos] = float(int((__double_as_longlong(g1[i]) >> 52) & 0x7ff) - 1023);
     ++pos;
   }
   if (wmask & 2u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g + 1;
-    welm[pos] = static_cast<float>(log2(g2[i]));
+    welm[pos] = float(int((__double_as_longlong(g2[i]) >> 52) & 0x7ff) - 1023);
   }
 }
 
@@ -933,7 +965,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     bool self_rows = false;
     if (lookup) {
       FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
-      lookup_sums_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+      lookup_sums_kernel<<<ceil_div_u32(E, kLookupThreads * kLookupUnroll), kLookupThreads, 0, s>>>(
           E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
           eprow[cur]->as<uint32_t>(), ws.partials.as<double>(),
           ws.pyr_depth == row_depth ? ws.pyr.as<double>() : nullptr,
