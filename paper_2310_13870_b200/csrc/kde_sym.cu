@@ -111,26 +111,59 @@ __global__ void sym_fill_kernel(uint32_t B, const float* __restrict__ lo,
 }
 
 // Tiles (I <= J) that touch the query blocks [b0, b1].
-__global__ void sym_tiles_kernel(uint32_t B, const uint32_t* __restrict__ poff,
-                                 const uint32_t* __restrict__ plist, uint32_t b0, uint32_t b1,
-                                 SymTile* __restrict__ tiles, uint32_t* __restrict__ ntiles) {
+__global__ void __launch_bounds__(128)
+    sym_tiles_kernel(uint32_t B, const uint32_t* __restrict__ poff,
+                     const uint32_t* __restrict__ plist, uint32_t b0, uint32_t b1,
+                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
+                     SymTile* __restrict__ tiles, uint32_t* __restrict__ ntiles,
+                     unsigned long long* __restrict__ performed) {
+  __shared__ unsigned long long red[4];
+  __shared__ uint32_t wcnt[4], cbase;
   const uint32_t I = blockIdx.x;
-  for (uint32_t k = poff[I] + threadIdx.x; k < poff[I + 1]; k += blockDim.x) {
-    const uint32_t J = plist[k];
-    if (J < I) continue;
-    const bool touch = (I >= b0 && I <= b1) || (J >= b0 && J <= b1);
-    if (!touch) continue;
-    // position of I in J's (ascending) partner list
-    uint32_t lo = poff[J], hi = poff[J + 1];
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (plist[mid] < I)
-        lo = mid + 1;
-      else
-        hi = mid;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long ev = 0;  // evaluations of this row's tiles
+  for (uint32_t k0 = poff[I]; k0 < poff[I + 1]; k0 += blockDim.x) {
+    const uint32_t k = k0 + threadIdx.x;
+    const uint32_t J = k < poff[I + 1] ? plist[k] : 0u;
+    const bool take = k < poff[I + 1] && J >= I &&
+                      ((I >= b0 && I <= b1) || (J >= b0 && J <= b1));
+    // one reservation per CTA chunk (a per-tile atomic on one counter
+    // serialises ~1.7M times at C3)
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (lane == 0) wcnt[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t c = wcnt[q];
+        wcnt[q] = t;
+        t += c;
+      }
+      cbase = t ? atomicAdd(ntiles, t) : 0u;
     }
-    const uint32_t at = atomicAdd(ntiles, 1u);
-    tiles[at] = SymTile{I, J, k - poff[I], lo - poff[J]};
+    __syncthreads();
+    if (take) {
+      ev += (unsigned long long)(bl[I] - bf[I]) * (bl[J] - bf[J]);
+      // position of I in J's (ascending) partner list
+      uint32_t lo = poff[J], hi = poff[J + 1];
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (plist[mid] < I)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      tiles[cbase + wcnt[w] + __popc(m & ((1u << lane) - 1u))] =
+          SymTile{I, J, k - poff[I], lo - poff[J]};
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if (lane == 0) red[w] = ev;
+  __syncthreads();
+  if (threadIdx.x == 0 && performed) {
+    const unsigned long long t = red[0] + red[1] + red[2] + red[3];
+    if (t) atomicAdd(performed, t);
   }
 }
 
@@ -235,7 +268,6 @@ __global__ void __launch_bounds__(kSymThreads)
       P[(size_t(poff[tl.J]) + tl.slotJ) * kSymBlock + t] = v;
     }
   }
-  if (performed && threadIdx.x == 0) atomicAdd(performed, (unsigned long long)ni * nj);
 }
 
 // Fold each point's partner values, in ascending partner order, into its
@@ -344,8 +376,9 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   DevBuf& tiles = ds.buf("sym.tiles", size_t(npart) * sizeof(SymTile) + 16);
   DevBuf& ntiles = ds.buf("sym.ntiles", 8);
   FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 4, s));
-  sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1,
-                                     tiles.as<SymTile>(), ntiles.as<uint32_t>());
+  sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1, bf,
+                                     bl, tiles.as<SymTile>(), ntiles.as<uint32_t>(),
+                                     d_performed);
   FSGG_LAUNCH_CHECK();
   uint32_t nt = 0;
   FSGG_CUDA(cudaMemcpyAsync(&nt, ntiles.as<void>(), 4, cudaMemcpyDeviceToHost, s));

@@ -209,13 +209,26 @@ __global__ void __launch_bounds__(kRouteThreads)
     }
     flags[i] = fl;
   }
+  // one atomic per CTA per counter (per-warp atomics on two addresses
+  // serialise ~0.5M times a level at 60M entries)
+  __shared__ unsigned long long red_t[kRouteThreads / 32], red_d[kRouteThreads / 32];
   for (int o = 16; o; o >>= 1) {
     tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
     degen += __shfl_xor_sync(0xffffffffu, degen, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    if (tsum) atomicAdd(counters + 0, tsum);
-    if (degen) atomicAdd(counters + 1, degen);
+    red_t[threadIdx.x >> 5] = tsum;
+    red_d[threadIdx.x >> 5] = degen;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a = 0, b = 0;
+    for (int k = 0; k < kRouteThreads / 32; ++k) {
+      a += red_t[k];
+      b += red_d[k];
+    }
+    if (a) atomicAdd(counters + 0, a);
+    if (b) atomicAdd(counters + 1, b);
   }
 }
 
@@ -567,8 +580,15 @@ __global__ void __launch_bounds__(kLookupThreads)
       ev += size[u];
     }
   }
+  __shared__ unsigned long long red_ev[kLookupThreads / 32];
   for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
-  if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+  if ((threadIdx.x & 31) == 0) red_ev[threadIdx.x >> 5] = ev;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < kLookupThreads / 32; ++k) t += red_ev[k];
+    if (t) atomicAdd(evals, t);
+  }
 }
 
 __device__ __forceinline__ uint32_t hiw(unsigned long long x) {
