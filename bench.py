@@ -294,6 +294,8 @@ def main():
     performed = sum(r.kernel_evals_performed for r in reps)
     tiled_s = sum(r.kde_tiled_seconds for r in reps)
     tiled_launches = sum(r.kde_tiled_launches for r in reps)
+    root_perf = sum(getattr(r, "kde_root_performed_evals", 0) for r in reps)
+    root_s = sum(getattr(r, "kde_root_seconds", 0.0) for r in reps)
     launches = sum(r.gpu_launches for r in reps)
     if world > 1:
         agg = torch.tensor([evals, tiled_evals], dtype=torch.float64, device=f"cuda:{local}")
@@ -347,7 +349,7 @@ def main():
     nominal = NOMINAL_EX2_PER_CLK_PER_SM * props.multi_processor_count * 1965e6
     achieved = tiled_perf / max(tiled_s, 1e-12)  # evaluations the kernel executed
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "kde_tiled_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "kde_sym_ncu.json" if root_s > 0 else "kde_tiled_ncu.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -388,6 +390,30 @@ def main():
             "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
             "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
             "traffic": traffic,
+        }
+    elif root_s > 0:
+        # the dominant kernel is the symmetric root pass (kde_sym.cu): every
+        # pair (q, x) of non-pruned block pairs evaluated once, one ex2 each,
+        # serving both q's and x's rows; timed around the tile kernel alone
+        root_rate = root_perf / root_s
+        roofline = {
+            "bound": "mufu", "kernel": "sym_tile_kernel<2,gaussian> (root level, each pair once)",
+            "achieved": root_rate / 1e9, "peak": ex2.value / 1e9, "unit": "Gex2/s",
+            "frac": root_rate / ex2.value if ex2.value else None,
+            "peak_source": "measured in this run: MUFU.EX2 microbenchmark (fsgg_probe_ex2_throughput)",
+            "nominal_peak": nominal / 1e9, "frac_of_nominal": root_rate / nominal,
+            "algorithmic_unit": ("one Gaussian kernel evaluation = one ex2 (SURVEY.md §8d); here "
+                                 "each executed ex2 is a pair serving two row sums"),
+            "evals_per_launch": root_perf / K,
+            "reference_equivalent_evals_per_launch": (n * n) ,
+            "reference_equivalent_rate": n * n * K / root_s / 1e9,
+            "mean_launch_ms": root_s / K * 1e3,
+            "share_of_step": root_s / max(total_s, 1e-12) if world == 1 else None,
+            "traffic": traffic,
+            "all_tile_kernels": {"executed_evals_per_step": tiled_perf / K,
+                                 "seconds_per_step": tiled_s / K,
+                                 "rate_gex2_s": achieved / 1e9,
+                                 "launches_per_step": tiled_launches / K},
         }
     else:
         roofline = {

@@ -106,6 +106,8 @@ typedef struct fsgg_report {
   uint64_t kernel_evals_performed;    /* evaluations actually executed */
   uint64_t kde_tiled_performed_evals; /* of which in the tiled kernel */
   uint64_t tie_verified_entries; /* entries re-decided on fp64 sums (tie guard) */
+  uint64_t kde_root_performed_evals; /* pair evaluations of the symmetric root kernel */
+  double kde_root_seconds;           /* its device time (0: one-sided root pass) */
 } fsgg_report;
 
 /* Per-edge quantities of the weighting step (sparsifier.hpp:29-38). */

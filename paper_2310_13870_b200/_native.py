@@ -49,7 +49,8 @@ class fsgg_report(C.Structure):
                 ("levels", C.c_uint32), ("peak_entries", C.c_uint64),
                 ("gpu_launches", C.c_uint32), ("kernel_evals_performed", C.c_uint64),
                 ("kde_tiled_performed_evals", C.c_uint64),
-                ("tie_verified_entries", C.c_uint64)]
+                ("tie_verified_entries", C.c_uint64),
+                ("kde_root_performed_evals", C.c_uint64), ("kde_root_seconds", C.c_double)]
 
 
 class fsgg_edge_estimate(C.Structure):

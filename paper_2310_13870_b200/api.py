@@ -290,6 +290,8 @@ class BuildReport:
     kernel_evals_performed: int = 0
     kde_tiled_performed_evals: int = 0
     tie_verified_entries: int = 0
+    kde_root_performed_evals: int = 0
+    kde_root_seconds: float = 0.0
 
     @classmethod
     def _from_c(cls, r):

@@ -234,6 +234,8 @@ void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
   r->kernel_evals_performed = bo.kde.performed;
   r->kde_tiled_performed_evals = bo.kde.tiled_performed;
   r->tie_verified_entries = bo.tie_verified;
+  r->kde_root_performed_evals = bo.kde.root_performed;
+  r->kde_root_seconds = bo.kde.root_seconds;
   r->kde_tiled_evals = bo.kde.tiled_evals;
   r->kde_tiled_seconds = bo.kde.tiled_seconds;
   r->kde_tiled_launches = bo.kde.tiled_launches;

@@ -146,6 +146,8 @@ struct KdeStats {
   uint64_t tiled_performed = 0;
   double tiled_seconds = 0.0;
   uint32_t tiled_launches = 0;
+  uint64_t root_performed = 0;   // symmetric root kernel (kde_sym.cu): pair evaluations
+  double root_seconds = 0.0;     // ... and its device time (tile kernel only)
 };
 
 struct KdeWorkspace {
@@ -247,8 +249,10 @@ void dfs_finish(Dataset& ds, const KernelSpec& ks, const DfsArgs& args);
 // ---- kde_sym.cu -----------------------------------------------------------
 // Root level with every pair evaluated once (row + column sums of block
 // pairs); writes rows [E][2^rd] for the points [qb, qe). false: unsupported.
+// ev0/ev1 (nullable) are recorded around the tile kernel alone.
 bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
-                        uint32_t rd, double* rows, unsigned long long* d_performed);
+                        uint32_t rd, double* rows, unsigned long long* d_performed,
+                        cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 // Depth of the symmetric pass's blocks (0: the pass does not apply).
 uint32_t sym_block_depth(const Dataset& ds);
 

@@ -881,7 +881,8 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
   const bool sym = lowd && lv.level == 0 && lv.qbase != 0xffffffffu && lv.prune &&
                    env_u32("FSGG_SYM", 1) != 0 &&
-                   kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials, d_perf);
+                   kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials, d_perf,
+                                      ws.ev0, ws.ev1);
   if (sym) {
     // every pair evaluated once (kde_sym.cu)
   } else if (lowd) {
@@ -900,7 +901,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     });
   }
   FSGG_LAUNCH_CHECK();
-  FSGG_CUDA(cudaEventRecord(ws.ev1, s));
+  if (!sym) FSGG_CUDA(cudaEventRecord(ws.ev1, s));  // sym: around its tile kernel
   ws.pyr_depth = 0;
   if (rl >= kPyramidMinDepth) {
     ws.pyr_depth = rl;
@@ -925,6 +926,10 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   float ms = 0.f;
   FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
   stats.tiled_seconds += ms * 1e-3;
+  if (sym) {
+    stats.root_seconds += ms * 1e-3;
+    stats.root_performed += perf;
+  }
   stats.tiled_evals += ev;
   stats.tiled_performed += perf;
   stats.performed += perf - ev;  // stats.performed was credited with ev above

@@ -272,20 +272,23 @@ __global__ void __launch_bounds__(kSymThreads)
 
 // Fold each point's partner values, in ascending partner order, into its
 // fp64 bucket row (bucket of partner J = J >> shift).
-constexpr uint32_t kSymBucketChunk = 16;  // 16 x 256 fp64 = 32 KiB of shared memory
+constexpr uint32_t kSymBucketChunk = 16;  // 16 x 257 fp64 = 32 KiB of shared memory
 __global__ void __launch_bounds__(kSymBlock)
     sym_rows_kernel(const float* __restrict__ P, const uint32_t* __restrict__ poff,
                     const uint32_t* __restrict__ plist, const uint32_t* __restrict__ bf,
                     const uint32_t* __restrict__ bl, uint32_t blk0, uint32_t shift,
                     uint32_t rd, uint32_t qb, uint32_t qe, double* __restrict__ rows) {
-  __shared__ double acc[kSymBucketChunk][kSymBlock];
+  // acc[c][t]: point t's sum for bucket b0 + c (row stride 257: conflict-free
+  // when the store pass below reads it column-wise)
+  __shared__ double acc[kSymBucketChunk][kSymBlock + 1];
   const uint32_t I = blk0 + blockIdx.x;
   const uint32_t f = bf[I], ni = bl[I] - f;
   const uint32_t t = threadIdx.x;
   const uint32_t W = 1u << rd;
   const uint32_t p0 = poff[I], p1 = poff[I + 1];
-  const uint32_t pt = f + t;
-  const bool mine = t < ni && pt >= qb && pt < qe;
+  // points of this block that are queries of this call
+  const uint32_t t0 = qb > f ? min(qb - f, ni) : 0u;
+  const uint32_t t1 = qe > f ? min(qe - f, ni) : 0u;
   uint32_t k = p0;
   for (uint32_t b0 = 0; b0 < W; b0 += kSymBucketChunk) {
 #pragma unroll
@@ -294,11 +297,14 @@ __global__ void __launch_bounds__(kSymBlock)
       const uint32_t c = (plist[k] >> shift) - b0;
       if (t < ni) acc[c][t] += double(P[size_t(k) * kSymBlock + t]);
     }
-    if (mine) {
-      double* out = rows + (size_t(pt - qb) << rd) + b0;
-      const uint32_t cmax = min(kSymBucketChunk, W - b0);
-      for (uint32_t c = 0; c < cmax; ++c) out[c] = acc[c][t];
+    __syncthreads();
+    // coalesced store: consecutive threads write consecutive buckets of a point
+    const uint32_t cmax = min(kSymBucketChunk, W - b0);
+    for (uint32_t idx = t; idx < (t1 - t0) * cmax; idx += blockDim.x) {
+      const uint32_t pt = t0 + idx / cmax, c = idx % cmax;
+      rows[(size_t(f + pt - qb) << rd) + b0 + c] = acc[c][pt];
     }
+    __syncthreads();
   }
 }
 
@@ -333,7 +339,8 @@ uint32_t sym_block_depth(const Dataset& ds) {
 }
 
 bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
-                        uint32_t rd, double* rows, unsigned long long* d_performed) {
+                        uint32_t rd, double* rows, unsigned long long* d_performed,
+                        cudaEvent_t ev0, cudaEvent_t ev1) {
   const TreeTable& t = ds.tree;
   const uint32_t Lb = sym_block_depth(ds);
   if (Lb == 0 || Lb < rd) return false;
@@ -384,6 +391,7 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   FSGG_CUDA(cudaMemcpyAsync(&nt, ntiles.as<void>(), 4, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
   DevBuf& P = ds.buf("sym.P", size_t(npart) * kSymBlock * 4 + 4);
+  if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
   if (nt > 0) {
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
@@ -407,6 +415,7 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
     });
     FSGG_LAUNCH_CHECK();
   }
+  if (ev1) FSGG_CUDA(cudaEventRecord(ev1, s));
   if (b0 <= b1) {
     sym_rows_kernel<<<b1 - b0 + 1, kSymBlock, 0, s>>>(P.as<float>(), poff.as<uint32_t>(),
                                                      plist.as<uint32_t>(), bf, bl, b0,
