@@ -87,38 +87,42 @@ __global__ void public_to_compact_kernel(const unsigned long long* in,
   out[i] = ((k >> 32) << bits) | (k & 0xffffffffull);
 }
 
-__global__ void underflow_flags_kernel(const unsigned long long* __restrict__ keys,
-                                       uint64_t m, const float* __restrict__ pts,
-                                       uint32_t d, int family, double sigma,
-                                       unsigned char* __restrict__ keep,
-                                       unsigned long long* __restrict__ dropped) {
+// Steps 2 + 3 in one pass: k_ij once per pair, the underflow flag
+// (sparsifier.cpp:105-109) and the weight (:110-113); dropped pairs are
+// compacted afterwards (rare).
+__global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64_t m,
+                             const float* __restrict__ pts, uint32_t d, int family,
+                             double sigma, double L, const double* __restrict__ g_full,
+                             uint32_t* __restrict__ u, uint32_t* __restrict__ v,
+                             double* __restrict__ w, EdgeEstimateDev* est,
+                             unsigned char* __restrict__ keep,
+                             unsigned long long* __restrict__ dropped) {
+  __shared__ unsigned long long red[8];
   const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (e >= m) return;
-  const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
-  const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
-  const bool ok = k >= 1e-300;
-  keep[e] = ok;
-  if (!ok) atomicAdd(dropped, 1ull);
-}
-
-__global__ void weights_kernel(const unsigned long long* __restrict__ keys,
-                               uint64_t m, const float* __restrict__ pts,
-                               uint32_t d, int family, double sigma, double L,
-                               const double* __restrict__ g_full,
-                               uint32_t* __restrict__ u, uint32_t* __restrict__ v,
-                               double* __restrict__ w, EdgeEstimateDev* est) {
-  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (e >= m) return;
-  const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
-  const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
-  const double gi = g_full[i], gj = g_full[j];
-  const double pi = fmin(__ddiv_rn(__dmul_rn(L, k), gi), 1.0);
-  const double pj = fmin(__ddiv_rn(__dmul_rn(L, k), gj), 1.0);
-  const double ph = __dsub_rn(__dadd_rn(pi, pj), __dmul_rn(pi, pj));
-  u[e] = i;
-  v[e] = j;
-  w[e] = __ddiv_rn(k, ph);
-  if (est) est[e] = EdgeEstimateDev{i, j, k, gi, gj, pi, pj, ph};
+  unsigned long long drop = 0;
+  if (e < m) {
+    const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
+    const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
+    const bool ok = k >= 1e-300;
+    keep[e] = ok;
+    drop = ok ? 0 : 1;
+    const double gi = g_full[i], gj = g_full[j];
+    const double pi = fmin(__ddiv_rn(__dmul_rn(L, k), gi), 1.0);
+    const double pj = fmin(__ddiv_rn(__dmul_rn(L, k), gj), 1.0);
+    const double ph = __dsub_rn(__dadd_rn(pi, pj), __dmul_rn(pi, pj));
+    u[e] = i;
+    v[e] = j;
+    w[e] = __ddiv_rn(k, ph);
+    if (est) est[e] = EdgeEstimateDev{i, j, k, gi, gj, pi, pj, ph};
+  }
+  for (int o = 16; o; o >>= 1) drop += __shfl_xor_sync(0xffffffffu, drop, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = drop;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (uint32_t k = 0; k < blockDim.x / 32; ++k) t += red[k];
+    if (t) atomicAdd(dropped, t);
+  }
 }
 
 // row_ptr[x] = first edge index with key-row >= x (keys sorted).
@@ -135,22 +139,6 @@ __global__ void row_ptr_kernel(const uint32_t* __restrict__ rows, uint64_t m,
       hi = mid;
   }
   row_ptr[x] = lo;
-}
-
-__global__ void transpose_keys_kernel(const uint32_t* __restrict__ u,
-                                      const uint32_t* __restrict__ v, uint64_t m,
-                                      uint32_t bits,
-                                      unsigned long long* __restrict__ keys) {
-  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (e >= m) return;
-  keys[e] = (static_cast<unsigned long long>(v[e]) << bits) | u[e];
-}
-
-__global__ void key_rows_kernel(const unsigned long long* __restrict__ keys,
-                                uint64_t m, uint32_t bits, uint32_t* __restrict__ rows) {
-  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (e >= m) return;
-  rows[e] = uint32_t(keys[e] >> bits);
 }
 
 // Degree of x in the reference's accumulation order (graph.cpp:14-21):
@@ -272,84 +260,93 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
     ds.launches += 2;
   }
 
-  // 2. drop underflowing pairs (k_ij < 1e-300)
+  // 2 + 3. k_ij once: underflow drop (k_ij < 1e-300) and weights (+ estimates)
   DevBuf& tmp = ds.buf("g.tmp", 8);
   DevBuf& cnt = ds.buf("g.cnt", 16);
   out.underflow = 0;
+  {
+    const uint64_t mm0 = std::max<uint64_t>(m, 1);
+    out.u.ensure(mm0 * 4, s);
+    out.v.ensure(mm0 * 4, s);
+    out.w.ensure(mm0 * 8, s);
+    if (want_estimates) out.est.ensure(mm0 * sizeof(EdgeEstimateDev), s);
+  }
   if (m) {
     DevBuf& keep = ds.buf("g.keep", m);
     FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
-    underflow_flags_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
-        keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
-        keep.as<unsigned char>(), cnt.as<unsigned long long>());
+    edges_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma, double(rounds), g_full,
+        out.u.as<uint32_t>(), out.v.as<uint32_t>(), out.w.as<double>(),
+        want_estimates ? out.est.as<EdgeEstimateDev>() : nullptr, keep.as<unsigned char>(),
+        cnt.as<unsigned long long>());
     FSGG_LAUNCH_CHECK();
     ds.launches++;
     unsigned long long dropped = 0;
     FSGG_CUDA(cudaMemcpyAsync(&dropped, cnt.as<void>(), 8, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
     if (dropped) {
-      DevBuf& kept = ds.buf("g.kept", m * 8);
-      cub_call(tmp, s, [&](void* t, size_t& b) {
-        return cub::DeviceSelect::Flagged(t, b, keys.as<unsigned long long>(),
-                                          keep.as<unsigned char>(),
-                                          kept.as<unsigned long long>(),
-                                          cnt.as<uint64_t>() + 1, m, s);
-      });
-      ds.launches++;
-      std::swap(keys, kept);
+      // compact every per-edge array by the keep flags (stable)
+      auto compact = [&](DevBuf& arr, size_t elem, const char* name) {
+        DevBuf& o = ds.buf(name, m * elem);
+        if (elem == 4) {
+          cub_call(tmp, s, [&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, arr.as<uint32_t>(), keep.as<unsigned char>(),
+                                              o.as<uint32_t>(), cnt.as<uint64_t>() + 1, m, s);
+          });
+        } else if (elem == 8) {
+          cub_call(tmp, s, [&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, arr.as<double>(), keep.as<unsigned char>(),
+                                              o.as<double>(), cnt.as<uint64_t>() + 1, m, s);
+          });
+        } else {
+          cub_call(tmp, s, [&](void* t, size_t& b) {
+            return cub::DeviceSelect::Flagged(t, b, arr.as<EdgeEstimateDev>(),
+                                              keep.as<unsigned char>(),
+                                              o.as<EdgeEstimateDev>(), cnt.as<uint64_t>() + 1,
+                                              m, s);
+          });
+        }
+        FSGG_CUDA(cudaMemcpyAsync(arr.as<void>(), o.as<void>(), (m - dropped) * elem,
+                                  cudaMemcpyDeviceToDevice, s));
+      };
+      compact(out.u, 4, "g.cu");
+      compact(out.v, 4, "g.cv");
+      compact(out.w, 8, "g.cw");
+      if (want_estimates) compact(out.est, sizeof(EdgeEstimateDev), "g.ce");
+      ds.launches += 4;
       m -= dropped;
       out.underflow = dropped;
     }
   }
   if (m > uint64_t(n) * rounds)
     throw NumericError("sparsity invariant violated: more than n*L edges");
-
-  // 3. weights (+ estimates)
   out.m = m;
   const uint64_t mm = std::max<uint64_t>(m, 1);
-  out.u.ensure(mm * 4, s);
-  out.v.ensure(mm * 4, s);
-  out.w.ensure(mm * 8, s);
-  if (want_estimates) out.est.ensure(mm * sizeof(EdgeEstimateDev), s);
-  if (m) {
-    weights_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
-        keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma,
-        double(rounds), g_full, out.u.as<uint32_t>(), out.v.as<uint32_t>(),
-        out.w.as<double>(), want_estimates ? out.est.as<EdgeEstimateDev>() : nullptr);
-    FSGG_LAUNCH_CHECK();
-    ds.launches++;
-  }
 
-  // 4. upper CSR, transposed CSR, degrees, total weight
+  // 4. upper CSR, transposed CSR, degrees, total weight. The transpose is a
+  // stable radix sort on v alone (ceil(log2 n) bits): edges arrive in (u, v)
+  // order, so each vertex's lower neighbours stay in ascending u.
   out.row_ptr.ensure(size_t(n + 1) * 8, s);
   out.degrees.ensure(size_t(n) * 8, s);
   DevBuf& rpt = ds.buf("g.rpt", size_t(n + 1) * 8);
-  DevBuf& tkeys = ds.buf("g.tkeys", mm * 8);
-  DevBuf& tkeys2 = ds.buf("g.tkeys2", mm * 8);
+  DevBuf& tv = ds.buf("g.tv", mm * 4);
+  DevBuf& tv2 = ds.buf("g.tv2", mm * 4);
   DevBuf& wt = ds.buf("g.wt", mm * 8);
   DevBuf& wt2 = ds.buf("g.wt2", mm * 8);
-  DevBuf& trows = ds.buf("g.trows", mm * 4);
   row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
       out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
   FSGG_LAUNCH_CHECK();
   if (m) {
-    transpose_keys_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
-        out.u.as<uint32_t>(), out.v.as<uint32_t>(), m, bits,
-        tkeys.as<unsigned long long>());
-    FSGG_LAUNCH_CHECK();
-    cub::DoubleBuffer<unsigned long long> dk(tkeys.as<unsigned long long>(),
-                                             tkeys2.as<unsigned long long>());
+    FSGG_CUDA(cudaMemcpyAsync(tv.as<void>(), out.v.as<void>(), m * 4, cudaMemcpyDeviceToDevice, s));
     FSGG_CUDA(cudaMemcpyAsync(wt.as<void>(), out.w.as<void>(), m * 8,
                               cudaMemcpyDeviceToDevice, s));
+    cub::DoubleBuffer<uint32_t> dk(tv.as<uint32_t>(), tv2.as<uint32_t>());
     cub::DoubleBuffer<double> dv(wt.as<double>(), wt2.as<double>());
     cub_call(tmp, s, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(2 * bits), s);
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(bits), s);
     });
-    key_rows_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(dk.Current(), m, bits,
-                                                         trows.as<uint32_t>());
-    FSGG_LAUNCH_CHECK();
     row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
-        trows.as<uint32_t>(), m, n, rpt.as<uint64_t>());
+        dk.Current(), m, n, rpt.as<uint64_t>());
     FSGG_LAUNCH_CHECK();
     degrees_kernel<<<ceil_div_u32(n, 256), 256, 0, s>>>(
         n, rpt.as<uint64_t>(), dv.Current(), out.row_ptr.as<uint64_t>(),
