@@ -864,6 +864,18 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
       ++c;
     rl = c + 1;
   }
+  // the symmetric root pass (kde_sym.cu) writes rows at any depth up to its
+  // block depth Lb (not tied to sub-chunks): as deep as serve_levels asks,
+  // capped by Lb and by HBM
+  const uint32_t Lb = (lowd && lv.level == 0 && lv.qbase != 0xffffffffu && lv.prune &&
+                       env_u32("FSGG_SYM", 1) != 0)
+                          ? sym_block_depth(ds)
+                          : 0;
+  if (Lb > 0) {
+    uint32_t want = std::min(std::max(rl, std::min(serve_levels, Lb)), Lb);
+    while (want > 1 && (uint64_t(E) << (want + 1)) > kMaxPartials) --want;
+    rl = want;
+  }
   if (row_depth) *row_depth = rl;
   const uint32_t K = 1u << c;
   ws.partials.ensure(size_t(E) << rl << 3, s);
@@ -879,10 +891,9 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   unsigned long long* d_perf = d_evals + 1;
   FSGG_CUDA(cudaMemsetAsync(d_perf, 0, 8, s));
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
-  const bool sym = lowd && lv.level == 0 && lv.qbase != 0xffffffffu && lv.prune &&
-                   env_u32("FSGG_SYM", 1) != 0 &&
-                   kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials, d_perf,
-                                      ws.ev0, ws.ev1);
+  const bool sym = Lb > 0 && kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials,
+                                                d_perf, ws.ev0, ws.ev1);
+  if (Lb > 0 && !sym) throw NumericError("symmetric root pass rejected its row depth");
   if (sym) {
     // every pair evaluated once (kde_sym.cu)
   } else if (lowd) {

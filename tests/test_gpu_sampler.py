@@ -223,6 +223,27 @@ def test_graph_vs_oracle(oracle, d, fam, sigma, L):
     assert rep.sampled_pairs == ref["report"]["sampled_pairs"]
 
 
+@pytest.mark.parametrize("d,fam,sigma,n", [(1, G, 0.02, 3500), (2, G, 0.08, 3500),
+                                           (2, E, 0.05, 3300), (3, LAP, 0.1, 3500),
+                                           (2, G, 0.03, 7000)])
+def test_graph_vs_oracle_symmetric_root(oracle, d, fam, sigma, n):
+    """Sizes whose root blocks hold >= 192 points, so the root level runs on
+    the symmetric pass (kde_sym.cu) and the deep levels on walks: the graph
+    still equals the exact reference's edge for edge."""
+    rng = np.random.default_rng(7 * n + d)
+    p = (rng.random((n, d)) * np.linspace(1.0, 0.4, d)).astype(np.float32)
+    p = p[np.argsort(p[:, 0], kind="stable")]  # spatially coherent order, like the generators
+    L = 8
+    g, rep, est = F.build_similarity_graph(F.Dataset(p), F.Kernel(fam, sigma),
+                                           F.SparsifierConfig(rounds=L, seed=9), report=True,
+                                           estimates=True)
+    assert rep.kde_root_performed_evals > 0  # the symmetric pass ran
+    ref = oracle.build_graph(p.astype(np.float64), sigma, L, seed=9, family=int(fam))
+    assert np.array_equal(g.u, ref["u"]) and np.array_equal(g.v, ref["v"])
+    assert rel(g.w, ref["w"]).max() <= 1e-5
+    assert rel(g.degrees, ref["degrees"]).max() <= 1e-5
+
+
 def test_degree_ratio_vs_full_graph():
     # proj/tests/test_sparsifier.cpp:103-114
     p, _ = datasets.make_blobs(200, [[0.0, 0.0], [6.0, 0.0]], 0.6, 5)
