@@ -320,8 +320,10 @@ def main():
                 dg, _ = F.build_similarity_graph_device(ds, kernel, cfg)
             else:
                 dg = parallel.build_similarity_graph_distributed(ds, kernel, cfg).graph
-            g = hostbufs.fetch(ds, dg)  # device -> pinned host: edges, CSR, degrees
-            nbytes = g.u.nbytes + g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+            # device -> pinned host: the graph as CSR (row_ptr, v, w) + degrees;
+            # the per-edge u is redundant with row_ptr and expanded on demand
+            g = hostbufs.fetch(ds, dg)
+            nbytes = g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
             torch.cuda.synchronize()
             barrier()
             if i >= args.warmup:

@@ -203,7 +203,17 @@ class WeightedGraph:
         return self.n
 
     def num_edges(self) -> int:
-        return int(self.u.size)
+        return int(self.v.size)
+
+    def __getattr__(self, name):
+        # graphs read back as CSR only (HostGraphBuffers.fetch) expand the
+        # row index of every edge on first use
+        if name == "u":
+            u = np.repeat(np.arange(self.n, dtype=np.uint32),
+                          np.diff(np.asarray(self.row_ptr, np.int64)))
+            object.__setattr__(self, "u", u)
+            return u
+        raise AttributeError(name)
 
     def degree(self, v: int) -> float:
         return float(self.degrees[v])
@@ -353,19 +363,26 @@ class HostGraphBuffers:
             self._bufs[name] = t
         return t.numpy().view(dtype)[:count]
 
-    def fetch(self, ds: "Dataset", graph) -> "WeightedGraph":
+    def fetch(self, ds: "Dataset", graph, with_u: bool = False) -> "WeightedGraph":
+        """Copy the device graph into the pinned buffers. By default only the
+        CSR (row_ptr, v, w) and degrees cross PCIe — the complete graph; the
+        per-edge u (a 4-byte row index per edge) is expanded on the host on
+        first access, or copied too with with_u=True."""
         m, n = int(graph.num_edges), int(graph.n)
-        u = self._get("u", m, np.uint32)
+        u = self._get("u", m, np.uint32) if with_u else None
         v = self._get("v", m, np.uint32)
         w = self._get("w", m, np.float64)
         rp = self._get("row_ptr", n + 1, np.uint64)
         dg = self._get("degrees", n, np.float64)
         N.check(N.lib().fsgg_device_graph_copy(
-            ds._h, u.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
-            w.ctypes.data_as(C.c_void_p), rp.ctypes.data_as(C.c_void_p),
-            dg.ctypes.data_as(C.c_void_p)))
-        return WeightedGraph(n=n, u=u, v=v, w=w, row_ptr=rp, degrees=dg,
-                             total_weight=float(graph.total_weight))
+            ds._h, u.ctypes.data_as(C.c_void_p) if with_u else None,
+            v.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p),
+            rp.ctypes.data_as(C.c_void_p), dg.ctypes.data_as(C.c_void_p)))
+        g = WeightedGraph(n=n, u=u, v=v, w=w, row_ptr=rp, degrees=dg,
+                          total_weight=float(graph.total_weight))
+        if not with_u:
+            del g.u  # expanded lazily from row_ptr (WeightedGraph.__getattr__)
+        return g
 
 
 def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig | None = None,

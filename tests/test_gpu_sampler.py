@@ -404,3 +404,17 @@ def test_symmetric_root_matches_one_sided():
     assert np.array_equal(g0.u, g1.u) and np.array_equal(g0.v, g1.v)
     np.testing.assert_allclose(g1.w, g0.w, rtol=1e-6)
     assert r1.kernel_evals_performed < r0.kernel_evals_performed
+
+
+def test_pinned_csr_readback_matches_full_copy():
+    """bench.py's e2e read-back (HostGraphBuffers.fetch: CSR + degrees over
+    PCIe, u expanded on the host on first use) equals the full host copy."""
+    p, _ = datasets.make_moons(5000, 0.05, 2)
+    ds = F.Dataset(p.astype(np.float32))
+    dg, _ = F.build_similarity_graph_device(ds, F.Kernel(G, 0.1), F.SparsifierConfig(rounds=8))
+    full = F.device_graph_to_host(ds)
+    g = F.api.HostGraphBuffers().fetch(ds, dg)
+    assert "u" not in g.__dict__
+    for k in ("v", "w", "row_ptr", "degrees"):
+        assert np.array_equal(getattr(g, k), getattr(full, k))
+    assert np.array_equal(g.u, full.u) and g.num_edges() == full.num_edges()
