@@ -51,6 +51,22 @@ __device__ __forceinline__ float box_dist(const float* q, const float* lo,
   return fam_finish1<FAM>(acc);
 }
 
+// box_dist with a compile-time dimension (8-byte box loads for d = 2).
+template <int D, int FAM>
+__device__ __forceinline__ float box_dist_d(const float (&q)[D], const float* lo,
+                                            const float* hi) {
+  if constexpr (D == 2) {
+    const float2 l = __ldg(reinterpret_cast<const float2*>(lo));
+    const float2 h = __ldg(reinterpret_cast<const float2*>(hi));
+    const float v0 = fmaxf(fmaxf(l.x - q[0], q[0] - h.x), 0.f);
+    const float v1 = fmaxf(fmaxf(l.y - q[1], q[1] - h.y), 0.f);
+    const float acc = (FAM == 2) ? v0 + v1 : fmaf(v1, v1, v0 * v0);
+    return fam_finish1<FAM>(acc);
+  } else {
+    return box_dist<FAM>(q, lo, hi, D);
+  }
+}
+
 // Rescale an fp32 sum of offset terms 2^(off - scale*dist) back to k units.
 // 2^-off = 2^-j * 2^-(off - j) with j = floor(off): an exact power of two
 // times a MUFU ex2 of a value in (-1, 0] (rel. error ~1e-7, the order of the
@@ -77,14 +93,19 @@ __device__ __forceinline__ void direct_child_sums(const float* __restrict__ pts,
   for (int side = 0; side < 2; ++side) {
     const uint64_t hc = 2 * h + 1 + side;
     const uint32_t a = side ? mid : f, b = side ? l : mid;
-    const float off =
-        has_boxes ? scale * box_dist<FAM>(qc, tlo + hc * D, thi + hc * D, D) : 0.f;
+    const float off = has_boxes ? scale * box_dist_d<D, FAM>(qc, tlo + hc * D, thi + hc * D) : 0.f;
     float acc = 0.f;
     for (uint32_t j = a; j < b; ++j) {
-      const float* x = pts + size_t(j) * D;
       float t = 0.f;
+      if constexpr (D == 2) {  // one 8-byte load per point
+        const float2 x = __ldg(reinterpret_cast<const float2*>(pts) + j);
+        t = fam_acc1<FAM>(qc[0] - x.x, t);
+        t = fam_acc1<FAM>(qc[1] - x.y, t);
+      } else {
+        const float* x = pts + size_t(j) * D;
 #pragma unroll
-      for (int k = 0; k < D; ++k) t = fam_acc1<FAM>(qc[k] - __ldg(x + k), t);
+        for (int k = 0; k < D; ++k) t = fam_acc1<FAM>(qc[k] - __ldg(x + k), t);
+      }
       t = fam_finish1<FAM>(t);
       acc += ex2_approx(fmaf(t, -scale, off));
     }
