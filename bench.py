@@ -369,7 +369,10 @@ def main():
             pass
         bf16 = float(peaks.get("bf16_tflops", 2250.0))
         tf32_peak = bf16 / 2.0
-        alg = tiled_perf * 2.0 * w.d / max(tiled_s, 1e-12) / 1e12
+        # the root launch (n x n, contiguous query tiles) is the dominant one;
+        # deeper tensor-core levels (gathered query blocks) are reported beside
+        r_perf, r_s = (root_perf, root_s) if root_s > 0 else (tiled_perf, tiled_s)
+        alg = r_perf * 2.0 * w.d / max(r_s, 1e-12) / 1e12
         traffic = None
         prof = os.path.join(ROOT, "profiles", "kde_tc_ncu.json")
         if os.path.exists(prof):
@@ -388,10 +391,14 @@ def main():
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS) / 2: dense TF32 is "
                             "half the bf16 rate on Blackwell"),
             "algorithmic_unit": "2*d FLOPs per Gaussian evaluation (dot-product form, SURVEY.md §8d)",
-            "evals_per_launch": tiled_perf / max(tiled_launches, 1),
-            "mean_launch_ms": tiled_s / max(tiled_launches, 1) * 1e3,
-            "share_of_step": tiled_s / max(total_s, 1e-12) if world == 1 else None,
+            "evals_per_launch": r_perf / K if root_s > 0 else tiled_perf / max(tiled_launches, 1),
+            "mean_launch_ms": (r_s / K if root_s > 0 else tiled_s / max(tiled_launches, 1)) * 1e3,
+            "share_of_step": r_s / max(total_s, 1e-12) if world == 1 else None,
             "traffic": traffic,
+            "all_tensor_launches": {"executed_evals_per_step": tiled_perf / K,
+                                    "seconds_per_step": tiled_s / K,
+                                    "algorithmic_tflops": tiled_perf * 2.0 * w.d / max(tiled_s, 1e-12) / 1e12,
+                                    "launches_per_step": tiled_launches / K},
         }
     elif root_s > 0:
         # the dominant kernel is the symmetric root pass (kde_sym.cu): every

@@ -937,7 +937,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   float ms = 0.f;
   FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
   stats.tiled_seconds += ms * 1e-3;
-  if (sym) {
+  if (sym || (tc && lv.level == 0)) {  // the root launch: the dominant kernel
     stats.root_seconds += ms * 1e-3;
     stats.root_performed += perf;
   }
