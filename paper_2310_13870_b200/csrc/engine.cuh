@@ -259,7 +259,7 @@ uint32_t sym_block_depth(const Dataset& ds);
 // ---- walk.cu --------------------------------------------------------------
 // Entries holding a single ticket below nodes of kWalkMaxNode points leave
 // the level-synchronous lists and finish as one path walk each.
-constexpr uint32_t kWalkMaxNode = 64;
+constexpr uint32_t kWalkMaxNode = 128;
 struct WalkArgs {
   uint32_t W = 0;  // walks
   const uint32_t* wq = nullptr;  // query
