@@ -351,6 +351,126 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Low-d tie guard (d <= 8): exact_sums_kernel specialised on (D, family):
+// unrolled coordinates, 8-byte loads for d = 2, and the exponent scaled by
+// a precomputed 1/sigma^2 (1/sigma) instead of a per-term fp64 division —
+// the values move by <= 1 ulp, far below the 2^-53 grid the re-decision is
+// taken on.
+template <int D, int FAM>
+__global__ void __launch_bounds__(256)
+    exact_sums_lowd_kernel(const float* __restrict__ pts, double sigma, float scale,
+                           uint32_t level, uint32_t depth, const uint32_t* __restrict__ eq,
+                           const uint32_t* __restrict__ eg, const float* __restrict__ elm,
+                           const uint32_t* __restrict__ tfirst,
+                           const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
+                           const float* __restrict__ thi, int has_boxes,
+                           const uint32_t* __restrict__ vlist,
+                           const uint32_t* __restrict__ vcount, double* __restrict__ g1,
+                           double* __restrict__ g2) {
+  __shared__ double red[2][256];
+  __shared__ unsigned char keep[1024];
+  const uint32_t cnt = *vcount;
+  const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  for (uint32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+    const uint32_t i = vlist[b];
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
+    const float* xq = pts + size_t(eq[i]) * D;
+    double q[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) q[k] = double(xq[k]);
+    uint32_t kd = 0;
+    while (kd < 10 && level + kd + 1 <= depth && ((l - f) >> (kd + 1)) >= 256) ++kd;
+    const uint32_t nsub = 1u << kd;
+    const uint64_t hb = ((1ull << (level + kd)) - 1) + (uint64_t(eg[i]) << kd);
+    const float lim_base = (elm ? elm[i] : 0.f) - 1.f - 80.f;  // log2 of the skip bound
+    for (uint32_t c = threadIdx.x; c < nsub; c += blockDim.x) {
+      bool k = true;
+      if (has_boxes && kd > 0) {
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const float v = fmaxf(fmaxf(tlo[(hb + c) * D + a] - xq[a], xq[a] - thi[(hb + c) * D + a]), 0.f);
+          acc = (FAM == 2) ? acc + v : fmaf(v, v, acc);
+        }
+        const float dist = FAM == 1 ? sqrtf(acc) : acc;
+        const float sz = float(tlast[hb + c] - tfirst[hb + c]);
+        k = __log2f(sz) - scale * dist >= lim_base;
+      }
+      keep[c] = k;
+    }
+    __syncthreads();
+    double s0 = 0.0, s1 = 0.0;
+    for (uint32_t c = 0; c < nsub; ++c) {
+      if (!keep[c]) continue;
+      const uint32_t cf = kd ? tfirst[hb + c] : f, cl = kd ? tlast[hb + c] : l;
+      for (uint32_t j = cf + threadIdx.x; j < cl; j += blockDim.x) {
+        double x[D];
+        if constexpr (D == 2) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(pts) + j);
+          x[0] = double(v.x);
+          x[1] = double(v.y);
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) x[a] = double(__ldg(pts + size_t(j) * D + a));
+        }
+        double t = 0.0;
+        if constexpr (FAM == 2) {
+#pragma unroll
+          for (int a = 0; a < D; ++a) t += fabs(q[a] - x[a]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < D; ++a) t = fma(q[a] - x[a], q[a] - x[a], t);
+          if constexpr (FAM == 1) t = sqrt(t);
+        }
+        const double v = exp(-t * inv);
+        if (j < mid)
+          s0 += v;
+        else
+          s1 += v;
+      }
+    }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    __syncthreads();
+    for (uint32_t w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+        red[0][threadIdx.x] += red[0][threadIdx.x + w];
+        red[1][threadIdx.x] += red[1][threadIdx.x + w];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      g1[i] = fmax(red[0][0], kSumFloor);
+      g2[i] = fmax(red[1][0], kSumFloor);
+    }
+    __syncthreads();
+  }
+}
+
+template <class F>
+bool lowd_exact_dispatch(uint32_t d, int family, F&& f) {
+  auto by_fam = [&](auto dim) {
+    switch (family) {
+      case 0: f(dim, std::integral_constant<int, 0>{}); return true;
+      case 1: f(dim, std::integral_constant<int, 1>{}); return true;
+      case 2: f(dim, std::integral_constant<int, 2>{}); return true;
+      default: return false;
+    }
+  };
+  switch (d) {
+    case 1: return by_fam(std::integral_constant<int, 1>{});
+    case 2: return by_fam(std::integral_constant<int, 2>{});
+    case 3: return by_fam(std::integral_constant<int, 3>{});
+    case 4: return by_fam(std::integral_constant<int, 4>{});
+    case 5: return by_fam(std::integral_constant<int, 5>{});
+    case 6: return by_fam(std::integral_constant<int, 6>{});
+    case 7: return by_fam(std::integral_constant<int, 7>{});
+    case 8: return by_fam(std::integral_constant<int, 8>{});
+    default: return false;
+  }
+}
+
 // High-d tie guard, batched: the flagged entries of one node share its
 // sources, so instead of one full pass over the node per tie (C5: 70k rows x
 // 784 dims per tie at the root), ties are sorted by node, cut into batches of
@@ -1057,13 +1177,24 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         ds.launches += 1;
       }
     } else if (verify) {
-      exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
-          ds.pts.as<float>(), ds.d, ks.family, ks.sigma, ks.scale, level, t.depth,
-          eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
-          level == 0 ? nullptr : elm[cur]->as<float>(), t.first.as<uint32_t>(),
-          t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
-          t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
-          g2.as<double>());
+      const bool lowd_done = lowd_exact_dispatch(ds.d, ks.family, [&](auto dim, auto fam) {
+        constexpr int D = decltype(dim)::value;
+        constexpr int FAM = decltype(fam)::value;
+        exact_sums_lowd_kernel<D, FAM><<<ds.num_sms * 4, 256, 0, s>>>(
+            ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
+            eg[cur]->as<uint32_t>(), level == 0 ? nullptr : elm[cur]->as<float>(),
+            t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+            t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
+            g2.as<double>());
+      });
+      if (!lowd_done)
+        exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
+            ds.pts.as<float>(), ds.d, ks.family, ks.sigma, ks.scale, level, t.depth,
+            eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+            level == 0 ? nullptr : elm[cur]->as<float>(), t.first.as<uint32_t>(),
+            t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+            t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
+            g2.as<double>());
       FSGG_LAUNCH_CHECK();
       reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
           level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
