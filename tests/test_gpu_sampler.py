@@ -284,20 +284,25 @@ def test_p_hat_band(oracle):
     assert np.all(est["p_hat"] >= 6 / 7 * pref) and np.all(est["p_hat"] <= 36 / 5 * pref)
 
 
-def test_sharded_build_is_bit_identical(oracle):
+@pytest.mark.parametrize("n", [3000, 3500, 14000])
+def test_sharded_build_is_bit_identical(oracle, n):
     """Query shards processed separately (as on N GPUs) and merged through
-    fsgg_finish_graph reproduce the 1-GPU graph bit for bit."""
+    fsgg_finish_graph reproduce the 1-GPU graph bit for bit — with the
+    one-sided root (n = 3000) and the symmetric root pass (3500, 14000: root
+    blocks of >= 192 points; a shard computes the block-pair tiles touching
+    its blocks)."""
     import torch
     from paper_2310_13870_b200 import parallel
-    p, _ = datasets.make_moons(3000, 0.05, 2)
+    p, _ = datasets.make_moons(n, 0.05, 2)
     ds = F.Dataset(p)
     k = F.Kernel(G, 0.1)
     cfg = F.SparsifierConfig(rounds=16, seed=3)
-    full = F.build_similarity_graph(ds, k, cfg)
-    for world in (2, 3):
+    full, rep, _ = F.build_similarity_graph(ds, k, cfg, report=True)
+    assert (rep.kde_root_performed_evals > 0) == (n != 3000)
+    for world in (2, 3, 5):
         pairs, gs = [], []
         for r in range(world):
-            qb, qe = parallel.shard_range(3000, r, world)
+            qb, qe = parallel.shard_range(n, r, world)
             sh, _, pr, g = parallel.sample_shard(
                 ds, k, F.SparsifierConfig(rounds=16, seed=3, query_begin=qb, query_end=qe))
             pairs.append(pr)
