@@ -517,7 +517,36 @@ __global__ void __launch_bounds__(kTieThreads)
     double acc[kTieBatch];
 #pragma unroll
     for (int t = 0; t < kTieBatch; ++t) acc[t] = 0.0;
-    for (uint32_t a = 0; a < d; ++a) {
+    // four dimensions per step: one 16-byte load of the source and one
+    // 16-byte (broadcast) shared-memory load per tie, then 4 fp64 terms
+    // each — the scalar loop was bound by shared-memory wavefronts
+    uint32_t a = 0;
+    if ((d & 3u) == 0) {
+      for (; a < d; a += 4) {
+        const float4 x4 = __ldg(reinterpret_cast<const float4*>(xj + a));
+        const double x0 = x4.x, x1 = x4.y, x2 = x4.z, x3 = x4.w;
+#pragma unroll
+        for (int t = 0; t < kTieBatch; ++t) {
+          if (uint32_t(t) < it.count) {
+            const float4 q4 = *reinterpret_cast<const float4*>(tq + t * d + a);
+            const double d0 = double(q4.x) - x0, d1 = double(q4.y) - x1;
+            const double d2 = double(q4.z) - x2, d3 = double(q4.w) - x3;
+            if (family == 2) {
+              acc[t] = acc[t] + fabs(d0);
+              acc[t] = acc[t] + fabs(d1);
+              acc[t] = acc[t] + fabs(d2);
+              acc[t] = acc[t] + fabs(d3);
+            } else {
+              acc[t] = fma(d0, d0, acc[t]);
+              acc[t] = fma(d1, d1, acc[t]);
+              acc[t] = fma(d2, d2, acc[t]);
+              acc[t] = fma(d3, d3, acc[t]);
+            }
+          }
+        }
+      }
+    }
+    for (; a < d; ++a) {
       const double xv = double(__ldg(xj + a));
 #pragma unroll
       for (int t = 0; t < kTieBatch; ++t) {
