@@ -258,7 +258,7 @@ def main():
             g, rep = F.build_similarity_graph_device(ds, kernel, cfg)
             return g, rep
         res = parallel.build_similarity_graph_distributed(ds, kernel, cfg)
-        return res.graph, res.report
+        return res, res.report
 
     for _ in range(args.warmup):
         step()
@@ -318,12 +318,23 @@ def main():
             ds.upload_ptr(host_ptr)  # pinned host -> device
             if world == 1:
                 dg, _ = F.build_similarity_graph_device(ds, kernel, cfg)
+                # device -> pinned host: the graph as CSR (row_ptr, v, w) +
+                # degrees; the per-edge u is redundant with row_ptr and
+                # expanded on demand
+                g = hostbufs.fetch(ds, dg)
+                nbytes = g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
             else:
-                dg = parallel.build_similarity_graph_distributed(ds, kernel, cfg).graph
-            # device -> pinned host: the graph as CSR (row_ptr, v, w) + degrees;
-            # the per-edge u is redundant with row_ptr and expanded on demand
-            g = hostbufs.fetch(ds, dg)
-            nbytes = g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
+                # each rank reads back the all-gathered graph (CSR + degrees)
+                res = parallel.build_similarity_graph_distributed(ds, kernel, cfg)
+                nbytes = 0
+                for name in ("v", "w", "row_ptr", "degrees"):
+                    t_dev = getattr(res, name)
+                    pin = hostbufs._bufs.get(name)
+                    if pin is None or pin.numel() < t_dev.numel() or pin.dtype != t_dev.dtype:
+                        pin = torch.empty(t_dev.numel(), dtype=t_dev.dtype, pin_memory=True)
+                        hostbufs._bufs[name] = pin
+                    pin[: t_dev.numel()].copy_(t_dev, non_blocking=True)
+                    nbytes += t_dev.numel() * t_dev.element_size()
             torch.cuda.synchronize()
             barrier()
             if i >= args.warmup:

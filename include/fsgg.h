@@ -205,10 +205,10 @@ int fsgg_build_similarity_graph_host(const float* points, uint32_t n,
  * or distributed build) into host memory (free with fsgg_graph_free). */
 int fsgg_device_graph_to_host(fsgg_dataset* ds, fsgg_graph* out);
 
-/* Copy the handle's current device graph into caller-owned host buffers
- * (any may be NULL): u, v (num_edges u32), w (num_edges f64), row_ptr
- * (n + 1 u64), degrees (n f64). With pinned (page-locked) buffers this runs
- * at full PCIe/C2C bandwidth; completes before returning. */
+/* Copy the handle's current device graph into caller-owned buffers (host
+ * or device memory; any may be NULL): u, v (num_edges u32), w (num_edges
+ * f64), row_ptr (n + 1 u64), degrees (n f64). With pinned (page-locked) host
+ * buffers this runs at full PCIe/C2C bandwidth; completes before returning. */
 int fsgg_device_graph_copy(fsgg_dataset* ds, uint32_t* u, uint32_t* v,
                            double* w, uint64_t* row_ptr, double* degrees);
 
@@ -361,6 +361,22 @@ int fsgg_finish_graph(fsgg_dataset* ds, const fsgg_kernel* kernel,
                       uint32_t rounds, const double* g_full_device,
                       const uint64_t* pairs_device, uint64_t num_pairs,
                       fsgg_device_graph* out, fsgg_report* report);
+
+/* Row-sharded phase 2 (each rank owns the rows [row_begin, row_end) of the
+ * upper-triangular graph; parallel.py routes every pair key (u << 32 | v,
+ * u < v) to the owner of u first). Call sequence per rank:
+ *   fsgg_finish_graph(ds, ..., routed pairs, ...)   dedupe + weights of the
+ *       rank's rows (degrees in `out` are partial: use the next two calls);
+ *   fsgg_rows_transposed(ds, v, w)   the rows' (v, w), m entries, stable-sorted
+ *       by v, to be routed to the owners of v;
+ *   fsgg_rows_degrees(ds, v, w, n, row_begin, row_end, deg)   degrees of the
+ *       rank's rows from the received (v, w) (concatenated in rank order) and
+ *       its own rows — summed in exactly the 1-GPU order.
+ * All pointers are device pointers on the handle's device. */
+int fsgg_rows_transposed(fsgg_dataset* ds, uint32_t* v_device, double* w_device);
+int fsgg_rows_degrees(fsgg_dataset* ds, const uint32_t* lower_v_device,
+                      const double* lower_w_device, uint64_t num_lower, uint32_t row_begin,
+                      uint32_t row_end, double* degrees_device);
 
 #ifdef __cplusplus
 }

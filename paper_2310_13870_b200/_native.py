@@ -156,6 +156,8 @@ _SIGS = {
     "fsgg_kmeans": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32,
                               C.POINTER(fsgg_kmeans_options), C.c_int, _P,
                               C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
+    "fsgg_rows_transposed": (C.c_int, [_P, _P, _P]),
+    "fsgg_rows_degrees": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_uint32, C.c_uint32, _P]),
     "fsgg_graph_save_text": (C.c_int, [C.c_char_p, C.c_uint32, C.c_uint64, _P, _P, _P,
                                        C.c_uint32]),
     "fsgg_graph_load_text": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(fsgg_graph)]),

@@ -565,7 +565,7 @@ int fsgg_device_graph_copy(fsgg_dataset* h, uint32_t* u, uint32_t* v, double* w,
     cudaStream_t s = h->ds.stream;
     auto cp = [&](void* dst, const fsgg::DevBuf& src, size_t bytes) {
       if (dst && bytes)
-        FSGG_CUDA(cudaMemcpyAsync(dst, src.as<void>(), bytes, cudaMemcpyDeviceToHost, s));
+        FSGG_CUDA(cudaMemcpyAsync(dst, src.as<void>(), bytes, cudaMemcpyDefault, s));
     };
     cp(u, g.u, g.m * 4);
     cp(v, g.v, g.m * 4);
@@ -838,6 +838,30 @@ int fsgg_finish_graph(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t round
       bo.t_graph = now() - t0;
       finish_report(report, h->ds, bo, h->graph.get(), bo.t_graph);
     }
+  });
+}
+
+int fsgg_rows_transposed(fsgg_dataset* h, uint32_t* v_device, double* w_device) {
+  return guarded([&] {
+    activate(h);
+    if (!h->graph) throw fsgg::ConfigError("no graph on this handle: finish one first");
+    if (h->graph->m && (!v_device || !w_device)) throw fsgg::ConfigError("null argument");
+    fsgg::rows_transposed(h->ds, *h->graph, v_device, w_device);
+  });
+}
+
+int fsgg_rows_degrees(fsgg_dataset* h, const uint32_t* lower_v_device,
+                      const double* lower_w_device, uint64_t num_lower, uint32_t row_begin,
+                      uint32_t row_end, double* degrees_device) {
+  return guarded([&] {
+    activate(h);
+    if (!h->graph) throw fsgg::ConfigError("no graph on this handle: finish one first");
+    if (row_begin > row_end || row_end > h->ds.n) throw fsgg::ConfigError("invalid row range");
+    if ((num_lower && (!lower_v_device || !lower_w_device)) ||
+        (row_end > row_begin && !degrees_device))
+      throw fsgg::ConfigError("null argument");
+    fsgg::rows_degrees(h->ds, *h->graph, lower_v_device, lower_w_device, num_lower, row_begin,
+                       row_end, degrees_device);
   });
 }
 

@@ -290,6 +290,14 @@ struct GraphResult {
 uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
                         uint64_t* self_pairs, uint64_t* sampled_pairs);
 
+// Row-sharded finish (multi-GPU): the graph's (v, w) stable-sorted by v
+// (the degree contributions the owner of v needs), and the degrees of rows
+// [rb, re) from the routed lower contributions plus the local rows.
+void rows_transposed(Dataset& ds, const GraphResult& g, uint32_t* v_out, double* w_out);
+void rows_degrees(Dataset& ds, const GraphResult& g, const uint32_t* lower_v,
+                  const double* lower_w, uint64_t nlower, uint32_t rb, uint32_t re,
+                  double* deg_out);
+
 // Dedupe (keys may repeat across shards), weight, CSR, degrees.
 void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
                   const double* g_full, const uint64_t* keys, uint64_t nkeys,

@@ -156,6 +156,41 @@ __global__ void degrees_kernel(uint32_t n, const uint64_t* __restrict__ rpt,
   deg[x] = s;
 }
 
+// Degrees of rows [rb, re) of a row-sharded graph: the lower contributions
+// (edges (u, x), u < x, routed here from their owners and stable-sorted by
+// x: u ascending) first, then the rank's own row x — exactly the
+// accumulation order of degrees_kernel on one GPU.
+__global__ void rows_degrees_kernel(uint32_t rb, uint32_t re,
+                                    const uint64_t* __restrict__ lrp,  // re - rb + 1
+                                    const double* __restrict__ lw,
+                                    const uint64_t* __restrict__ rp,   // global upper CSR
+                                    const double* __restrict__ w,
+                                    double* __restrict__ deg) {
+  const uint32_t x = rb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= re) return;
+  double s = 0.0;
+  for (uint64_t e = lrp[x - rb]; e < lrp[x - rb + 1]; ++e) s = __dadd_rn(s, lw[e]);
+  for (uint64_t e = rp[x]; e < rp[x + 1]; ++e) s = __dadd_rn(s, w[e]);
+  deg[x - rb] = s;
+}
+
+// lrp[i] = first index of sorted keys with key >= rb + i (i <= re - rb)
+__global__ void range_ptr_kernel(const uint32_t* __restrict__ keys, uint64_t m, uint32_t rb,
+                                 uint32_t re, uint64_t* __restrict__ lrp) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > re - rb) return;
+  const uint32_t x = rb + i;
+  uint64_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < x)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  lrp[i] = lo;
+}
+
 template <class F>
 void cub_call(DevBuf& tmp, cudaStream_t s, F&& f) {
   size_t bytes = 0;
@@ -363,6 +398,68 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
     out.total_weight = 0.0;
   }
   FSGG_CUDA(cudaStreamSynchronize(s));
+}
+
+// ---- row-sharded finish (multi-GPU, parallel.py) ----------------------------
+
+void rows_transposed(Dataset& ds, const GraphResult& g, uint32_t* v_out, double* w_out) {
+  cudaStream_t s = ds.stream;
+  const uint64_t m = g.m;
+  if (m == 0) return;
+  const uint32_t bits = index_bits(ds.n);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  DevBuf& k2 = ds.buf("rt.k2", m * 4);
+  DevBuf& w2 = ds.buf("rt.w2", m * 8);
+  FSGG_CUDA(cudaMemcpyAsync(v_out, g.v.as<void>(), m * 4, cudaMemcpyDeviceToDevice, s));
+  FSGG_CUDA(cudaMemcpyAsync(w_out, g.w.as<void>(), m * 8, cudaMemcpyDeviceToDevice, s));
+  cub::DoubleBuffer<uint32_t> dk(v_out, k2.as<uint32_t>());
+  cub::DoubleBuffer<double> dv(w_out, w2.as<double>());
+  cub_call(tmp, s, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(bits), s);
+  });
+  if (dk.Current() != v_out)
+    FSGG_CUDA(cudaMemcpyAsync(v_out, dk.Current(), m * 4, cudaMemcpyDeviceToDevice, s));
+  if (dv.Current() != w_out)
+    FSGG_CUDA(cudaMemcpyAsync(w_out, dv.Current(), m * 8, cudaMemcpyDeviceToDevice, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  ds.launches += 4;
+}
+
+void rows_degrees(Dataset& ds, const GraphResult& g, const uint32_t* lower_v,
+                  const double* lower_w, uint64_t nlower, uint32_t rb, uint32_t re,
+                  double* deg_out) {
+  cudaStream_t s = ds.stream;
+  if (re <= rb) return;
+  const uint32_t bits = index_bits(ds.n);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  const uint64_t nl = std::max<uint64_t>(nlower, 1);
+  DevBuf& k1 = ds.buf("rd.k1", nl * 4);
+  DevBuf& k2 = ds.buf("rd.k2", nl * 4);
+  DevBuf& w1 = ds.buf("rd.w1", nl * 8);
+  DevBuf& w2 = ds.buf("rd.w2", nl * 8);
+  DevBuf& lrp = ds.buf("rd.lrp", size_t(re - rb + 1) * 8);
+  const uint32_t* keys = k1.as<uint32_t>();
+  const double* vals = w1.as<double>();
+  if (nlower) {
+    FSGG_CUDA(cudaMemcpyAsync(k1.as<void>(), lower_v, nlower * 4, cudaMemcpyDeviceToDevice, s));
+    FSGG_CUDA(cudaMemcpyAsync(w1.as<void>(), lower_w, nlower * 8, cudaMemcpyDeviceToDevice, s));
+    // stable: rank order (u ranges ascending) survives within each vertex
+    cub::DoubleBuffer<uint32_t> dk(k1.as<uint32_t>(), k2.as<uint32_t>());
+    cub::DoubleBuffer<double> dv(w1.as<double>(), w2.as<double>());
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, nlower, 0, int(bits), s);
+    });
+    keys = dk.Current();
+    vals = dv.Current();
+  }
+  range_ptr_kernel<<<ceil_div_u32(uint64_t(re - rb) + 1, 256), 256, 0, s>>>(
+      keys, nlower, rb, re, lrp.as<uint64_t>());
+  FSGG_LAUNCH_CHECK();
+  rows_degrees_kernel<<<ceil_div_u32(re - rb, 256), 256, 0, s>>>(
+      rb, re, lrp.as<uint64_t>(), vals, g.row_ptr.as<uint64_t>(), g.w.as<double>(), deg_out);
+  FSGG_LAUNCH_CHECK();
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  ds.launches += 4;
 }
 
 }  // namespace fsgg

@@ -4,16 +4,23 @@ A query's descent reads only the replicated points and its own keyed RNG
 stream (proj/src/sampler.cpp:213-214), and every child sum is reduced over
 node-aligned source chunks in a fixed order, so partitioning the queries
 changes nothing observable: the sharded graph is bit-identical to the
-1-GPU graph. The only data exchange is at the end (north star: "NCCL over
-NVLink is used only for the final edge-list all-gather"):
+1-GPU graph. There is no collective during the descent; the exchanges are
+at the end, all over NCCL:
 
   1. all-gather of the degree KDE slices g_full (n fp64), needed because
      p_j uses the other endpoint's estimate (proj/src/sparsifier.cpp:110-111);
-  2. all-gather of the shards' sorted unique pair keys (variable length:
-     counts all-gather + padded all-gather);
-then every rank runs the same dedupe/weight/CSR/degree kernels
-(fsgg_finish_graph) on the concatenation. The exchange helpers below are
-device-agnostic so the CPU suite exercises them with ``gloo``.
+  2. all-to-all of the pair keys (u << 32 | v, u < v) to the rank owning
+     row u (rows are sharded like the queries) — every rank then dedupes and
+     weights only its own rows (fsgg_finish_graph);
+  3. all-to-all of the rows' (v, w) to the rank owning v, which sums each
+     vertex's degree in exactly the 1-GPU order (fsgg_rows_transposed,
+     fsgg_rows_degrees);
+  4. optionally the final all-gather of the edge lists and degrees (the
+     north star's "final edge-list all-gather"), concatenated in rank order
+     = the global (u, v) order.
+The graph finish is thus split N ways instead of repeated on every rank.
+The exchange helpers are device-agnostic so the CPU suite exercises them
+with ``gloo``.
 """
 from __future__ import annotations
 
@@ -32,6 +39,10 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
+def shard_bounds(n: int, world: int) -> list[int]:
+    return [shard_range(n, r, world)[0] for r in range(world)] + [n]
+
+
 def allgather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather 1-D tensors of different lengths, concatenated in rank order."""
     world = dist.get_world_size(group)
@@ -47,15 +58,35 @@ def allgather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat([b[:s] for b, s in zip(bufs, sizes)])
 
 
-class DistributedResult:
-    """Device graph of the sharded build (valid until the next build on ds)."""
+def owner_splits(keys: torch.Tensor, bounds: list[int]) -> list[int]:
+    """Per-destination counts of a sorted key array cut at ``bounds``."""
+    b = torch.tensor(bounds[1:-1], dtype=keys.dtype, device=keys.device)
+    cuts = torch.searchsorted(keys, b).tolist() if b.numel() else []
+    edges = [0] + cuts + [keys.numel()]
+    return [edges[i + 1] - edges[i] for i in range(len(edges) - 1)]
 
-    def __init__(self, graph, report: BuildReport, shard_report: BuildReport,
-                 exchange_bytes: int):
-        self.graph = graph
-        self.report = report
-        self.shard_report = shard_report
-        self.exchange_bytes = exchange_bytes
+
+def alltoall_varlen(t: torch.Tensor, send_counts: list[int], group=None) -> torch.Tensor:
+    """Send t[sum(send_counts[:r]) : ...] to rank r; received slices are
+    concatenated in source-rank order."""
+    world = dist.get_world_size(group)
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=t.device)
+    rc = torch.empty(world, dtype=torch.int64, device=t.device)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv = rc.tolist()
+    out = torch.empty(sum(recv), dtype=t.dtype, device=t.device)
+    dist.all_to_all_single(out, t.contiguous(), output_split_sizes=recv,
+                           input_split_sizes=list(send_counts), group=group)
+    return out
+
+
+class DistributedResult:
+    """Sharded build: this rank's rows [row_begin, row_end) of the graph
+    (u, v, w sorted by (u, v)) and their degrees; with ``gathered`` the
+    full graph (edge arrays, row_ptr, degrees) on every rank."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
 
 
 def sample_shard(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig):
@@ -85,17 +116,52 @@ def finish_graph(ds: Dataset, kernel: Kernel, rounds: int, g_full: torch.Tensor,
     return out, BuildReport._from_c(rep)
 
 
+def finish_rows(ds: Dataset, kernel: Kernel, rounds: int, g_full: torch.Tensor,
+                pairs: torch.Tensor, row_begin: int, row_end: int, bounds: list[int],
+                group=None):
+    """Phase 2 of the row-sharded finish on one rank: `pairs` are this
+    shard's sorted unique keys; returns (rows graph tensors, degrees of the
+    rank's rows, report)."""
+    dev = torch.device("cuda", ds.device)
+    routed = alltoall_varlen(pairs, owner_splits(pairs >> 32, bounds), group)
+    graph, frep = finish_graph(ds, kernel, rounds, g_full, routed)
+    m = int(graph.num_edges)
+    v = torch.empty(m, dtype=torch.int32, device=dev)
+    w = torch.empty(m, dtype=torch.float64, device=dev)
+    N.check(N.lib().fsgg_rows_transposed(ds._h, C.c_void_p(v.data_ptr() if m else 0),
+                                         C.c_void_p(w.data_ptr() if m else 0)))
+    splits = owner_splits(v.to(torch.int64), bounds)
+    lower_v = alltoall_varlen(v, splits, group)
+    lower_w = alltoall_varlen(w, splits, group)
+    torch.cuda.synchronize(dev)
+    deg = torch.empty(row_end - row_begin, dtype=torch.float64, device=dev)
+    N.check(N.lib().fsgg_rows_degrees(
+        ds._h, C.c_void_p(lower_v.data_ptr() if lower_v.numel() else 0),
+        C.c_void_p(lower_w.data_ptr() if lower_w.numel() else 0), lower_v.numel(), row_begin,
+        row_end, C.c_void_p(deg.data_ptr() if deg.numel() else 0)))
+    rows = dict(u=torch.empty(m, dtype=torch.int32, device=dev),
+                v=torch.empty(m, dtype=torch.int32, device=dev),
+                w=torch.empty(m, dtype=torch.float64, device=dev))
+    if m:  # device-to-device copy of the rank's rows out of the library
+        N.check(N.lib().fsgg_device_graph_copy(
+            ds._h, C.c_void_p(rows["u"].data_ptr()), C.c_void_p(rows["v"].data_ptr()),
+            C.c_void_p(rows["w"].data_ptr()), None, None))
+    return rows, deg, frep, routed.numel() * 8 + (lower_v.numel() * 12)
+
+
 def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
                                        config: SparsifierConfig | None = None,
-                                       group=None) -> DistributedResult:
+                                       group=None, gather: bool = True) -> DistributedResult:
     """build_similarity_graph over all ranks of ``group`` (one GPU each)."""
     cfg = config or SparsifierConfig()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    qb, qe = shard_range(ds.n, rank, world)
+    n = ds.n
+    qb, qe = shard_range(n, rank, world)
+    bounds = shard_bounds(n, world)
     sh, srep, pairs, g = sample_shard(ds, kernel, replace(cfg, query_begin=qb, query_end=qe))
     g_full = allgather_varlen(g, group)
-    all_pairs = allgather_varlen(pairs, group)
-    graph, frep = finish_graph(ds, kernel, int(sh.rounds), g_full, all_pairs)
+    rows, deg, frep, moved = finish_rows(ds, kernel, int(sh.rounds), g_full, pairs, qb, qe,
+                                         bounds, group)
     frep.sampled_pairs = srep.sampled_pairs
     frep.self_pairs_discarded = srep.self_pairs_discarded
     frep.degenerate_draws = srep.degenerate_draws
@@ -105,5 +171,18 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
     frep.kde_tiled_launches = srep.kde_tiled_launches
     frep.sampling_seconds = srep.sampling_seconds
     frep.gpu_launches += srep.gpu_launches
-    exchange = (g_full.numel() * 8 + all_pairs.numel() * 8)
-    return DistributedResult(graph, frep, srep, exchange)
+    res = DistributedResult(row_begin=qb, row_end=qe, u=rows["u"], v=rows["v"], w=rows["w"],
+                            degrees=deg, report=frep, shard_report=srep,
+                            exchange_bytes=g_full.numel() * 8 + moved, gathered=False)
+    if gather:
+        res.u = allgather_varlen(rows["u"], group)
+        res.v = allgather_varlen(rows["v"], group)
+        res.w = allgather_varlen(rows["w"], group)
+        res.degrees = allgather_varlen(deg, group)
+        counts = torch.bincount(res.u.to(torch.int64), minlength=n)
+        res.row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=res.u.device)
+        res.row_ptr[1:] = torch.cumsum(counts, 0)
+        res.gathered = True
+        res.exchange_bytes += res.u.numel() * 16 + n * 8
+    res.num_edges = int(res.v.numel())
+    return res

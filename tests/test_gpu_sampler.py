@@ -313,6 +313,75 @@ def test_sharded_build_is_bit_identical(oracle, n):
         assert np.array_equal(g.w, full.w) and np.array_equal(g.degrees, full.degrees)
 
 
+@pytest.mark.parametrize("n,world", [(3000, 2), (3500, 3), (14000, 5)])
+def test_row_sharded_finish_is_bit_identical(n, world):
+    """The multi-GPU finish split by rows (parallel.finish_rows' exchanges
+    emulated in-process, one dataset handle per rank): pairs routed to the
+    owner of u, rows deduped and weighted there, (v, w) routed to the owner
+    of v for the degrees — the concatenated rank outputs equal the 1-GPU
+    graph and degrees bit for bit."""
+    import torch
+    from paper_2310_13870_b200 import _native as N
+    from paper_2310_13870_b200 import parallel
+    import ctypes as C
+    p, _ = datasets.make_moons(n, 0.05, 2)
+    k = F.Kernel(G, 0.1)
+    L = 16
+    full = F.build_similarity_graph(F.Dataset(p), k, F.SparsifierConfig(rounds=L, seed=3))
+    bounds = parallel.shard_bounds(n, world)
+    handles = [F.Dataset(p) for _ in range(world)]
+    pairs, gs = [], []
+    for r in range(world):
+        sh, _, pr, g = parallel.sample_shard(
+            handles[r], k, F.SparsifierConfig(rounds=L, seed=3, query_begin=bounds[r],
+                                              query_end=bounds[r + 1]))
+        pairs.append(pr)
+        gs.append(g)
+    g_full = torch.cat(gs)
+
+    def route(chunks, keyfn):  # emulated all_to_all: dest d gets slices in source order
+        out = [[] for _ in range(world)]
+        for t in chunks:
+            splits = parallel.owner_splits(keyfn(t), bounds)
+            for d, piece in enumerate(torch.split(t, splits)):
+                out[d].append(piece)
+        return out
+
+    routed = [torch.cat(x) for x in route(pairs, lambda t: t >> 32)]
+    vs, ws, rows = [], [], []
+    for d in range(world):
+        graph, _ = parallel.finish_graph(handles[d], k, L, g_full, routed[d])
+        m = int(graph.num_edges)
+        v = torch.empty(m, dtype=torch.int32, device="cuda")
+        w = torch.empty(m, dtype=torch.float64, device="cuda")
+        N.check(N.lib().fsgg_rows_transposed(handles[d]._h, C.c_void_p(v.data_ptr()),
+                                             C.c_void_p(w.data_ptr())))
+        vs.append(v)
+        ws.append(w)
+        rows.append(F.device_graph_to_host(handles[d]))
+    lv = route(vs, lambda t: t.to(torch.int64))
+    lw_splits = [parallel.owner_splits(v.to(torch.int64), bounds) for v in vs]
+    lw = [[] for _ in range(world)]
+    for src, w in enumerate(ws):
+        for d, piece in enumerate(torch.split(w, lw_splits[src])):
+            lw[d].append(piece)
+    degs = []
+    for d in range(world):
+        lower_v, lower_w = torch.cat(lv[d]), torch.cat(lw[d])
+        deg = torch.empty(bounds[d + 1] - bounds[d], dtype=torch.float64, device="cuda")
+        N.check(N.lib().fsgg_rows_degrees(
+            handles[d]._h, C.c_void_p(lower_v.data_ptr() if lower_v.numel() else 0),
+            C.c_void_p(lower_w.data_ptr() if lower_w.numel() else 0), lower_v.numel(),
+            bounds[d], bounds[d + 1], C.c_void_p(deg.data_ptr())))
+        degs.append(deg.cpu().numpy())
+    u = np.concatenate([r.u for r in rows])
+    v = np.concatenate([r.v for r in rows])
+    w = np.concatenate([r.w for r in rows])
+    assert np.array_equal(u, full.u) and np.array_equal(v, full.v)
+    assert w.tobytes() == full.w.tobytes()
+    assert np.concatenate(degs).tobytes() == full.degrees.tobytes()
+
+
 def test_philox_mode_graph_is_valid():
     p, _ = datasets.make_moons(2000, 0.05, 1)
     g, rep, est = F.build_similarity_graph(

@@ -76,3 +76,57 @@ def test_shard_ranges_partition():
             spans = [shard_range(n, r, world) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def _route_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle.pyoracle import Oracle
+    from paper_2310_13870_b200.parallel import (alltoall_varlen, owner_splits, shard_bounds,
+                                                shard_range)
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle()
+    n, sigma, L, seed = 301, 0.2, 6, 5
+    pts = orc.random_dataset(n, 2, 7)
+    qb, qe = shard_range(n, rank, world)
+    tri = orc.sample_counted(pts, np.arange(qb, qe), L, seed, sigma)["triples"]
+    q, s = tri[:, 0].astype(np.int64), tri[:, 1].astype(np.int64)
+    keep = q != s
+    keys = np.unique((np.minimum(q, s)[keep] << 32) | np.maximum(q, s)[keep])
+    bounds = shard_bounds(n, world)
+    t = torch.from_numpy(keys)
+    # step 2 of parallel.py: pair keys to the owner of row u
+    routed = alltoall_varlen(t, owner_splits(t >> 32, bounds))
+    mine = np.unique(routed.numpy())
+    assert np.all((mine >> 32) >= qb) and np.all((mine >> 32) < qe)
+    np.save(os.path.join(out_dir, f"rows{rank}.npy"), mine)
+    # step 3: (v, w) of the rows to the owner of v, concatenated in rank order
+    v = np.sort((mine & 0xffffffff).astype(np.int64), kind="stable")
+    tv = torch.from_numpy(v)
+    lower = alltoall_varlen(tv, owner_splits(tv, bounds)).numpy()
+    assert np.all(lower >= qb) and np.all(lower < qe)
+    np.save(os.path.join(out_dir, f"lower{rank}.npy"), lower)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_routing_matches_single_process(tmp_path, world):
+    """parallel.py's all-to-all routing over gloo: every rank ends with
+    exactly the edges of its rows, and with the degree contributions
+    (edges (u, x), u < x) of its vertices."""
+    from oracle.pyoracle import Oracle
+    from paper_2310_13870_b200.parallel import shard_range
+    mp.spawn(_route_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    orc = Oracle()
+    full = orc.build_graph(orc.random_dataset(301, 2, 7), 0.2, 6, seed=5)
+    u, v = full["u"].astype(np.int64), full["v"].astype(np.int64)
+    got = np.concatenate([np.load(tmp_path / f"rows{r}.npy") for r in range(world)])
+    assert np.array_equal(got, (u << 32) | v)
+    for r in range(world):
+        qb, qe = shard_range(301, r, world)
+        lower = np.load(tmp_path / f"lower{r}.npy")
+        assert np.array_equal(np.sort(lower), np.sort(v[(v >= qb) & (v < qe)]))
