@@ -4,6 +4,8 @@ seeded random problems spanning every code path — dimension class (low-d
 tiled/direct, mid-d CUDA-core, high-d tensor cores), kernel family, sizes on
 either side of the symmetric-root and walk thresholds, clustered and uniform
 data, index orders, L, seeds."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -66,3 +68,45 @@ def test_random_graph_matches_oracle(oracle, i):
     assert rep.sampled_pairs == ref["report"]["sampled_pairs"], info
     assert rep.self_pairs_discarded == ref["report"]["self_pairs_discarded"], info
     assert rep.degenerate_draws == ref["report"]["degenerate_draws"], info
+
+
+def _edge_case(name):
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    if name == "identical-points":
+        p = np.zeros((600, 2), np.float32)
+        return p, F.KernelFamily.gaussian, 0.1, 8
+    if name == "far-clusters":  # cross-cluster terms underflow: degenerate draws
+        p = np.concatenate([rng.normal(0, 0.01, (400, 2)), rng.normal(50, 0.01, (400, 2))])
+        return p.astype(np.float32), F.KernelFamily.gaussian, 0.05, 16
+    if name == "tiny-sigma":  # almost every sum at the 1e-300 floor
+        p = rng.random((3500, 2)).astype(np.float32)
+        return p, F.KernelFamily.gaussian, 1e-4, 4
+    if name == "huge-sigma":  # flat kernel: tickets spread uniformly
+        p = rng.random((3500, 3)).astype(np.float32)
+        return p, F.KernelFamily.gaussian, 1e3, 8
+    if name == "duplicates":  # many exact duplicates among distinct points
+        base = rng.random((50, 2))
+        p = base[rng.integers(0, 50, 3400)].astype(np.float32)
+        return p, F.KernelFamily.laplacian, 0.2, 8
+    if name == "line-1d-large":
+        p = np.sort(rng.random((20000, 1)), axis=0).astype(np.float32)
+        return p, F.KernelFamily.exponential, 0.002, 8
+    raise ValueError(name)
+
+
+@pytest.mark.parametrize("name", ["identical-points", "far-clusters", "tiny-sigma", "huge-sigma",
+                                  "duplicates", "line-1d-large"])
+def test_edge_cases_match_oracle(oracle, name):
+    p, fam, sigma, L = _edge_case(name)
+    seed = 17
+    g, rep, _ = F.build_similarity_graph(F.Dataset(p), F.Kernel(fam, sigma),
+                                         F.SparsifierConfig(rounds=L, seed=seed), report=True,
+                                         estimates=True)
+    ref = oracle.build_graph(p.astype(np.float64), sigma, L, seed=seed, family=int(fam))
+    assert np.array_equal(g.u, ref["u"]) and np.array_equal(g.v, ref["v"])
+    if g.w.size:
+        assert (np.abs(g.w - ref["w"]) / ref["w"]).max() <= 1e-5
+    assert rep.sampled_pairs == ref["report"]["sampled_pairs"]
+    assert rep.self_pairs_discarded == ref["report"]["self_pairs_discarded"]
+    assert rep.degenerate_draws == ref["report"]["degenerate_draws"]
+    assert rep.underflow_edges_discarded == ref["report"]["underflow_edges_discarded"]
