@@ -37,7 +37,7 @@ constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or
 constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
 constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 256;
 constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
-constexpr uint32_t kTcGroup = 16;                       // entry blocks per L2 group
+constexpr uint32_t kTcGroup = 64;                       // entry blocks per L2 group
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
