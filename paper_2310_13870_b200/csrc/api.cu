@@ -185,10 +185,13 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   fsgg::Dataset& ds = h->ds;
   const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
   double t0 = now();
-  if (!ds.tree_valid) {
-    fsgg::build_tree(ds);
-    FSGG_CUDA(cudaStreamSynchronize(ds.stream));
-  }
+  // Every build derives its tree (node boxes) and, on the tensor-core path,
+  // the centred tf32 split of the points afresh: per-dataset preprocessing
+  // is part of the job, as the reference's estimator build is.
+  ds.tree_valid = false;
+  ds.tc_ready = false;
+  fsgg::build_tree(ds);
+  FSGG_CUDA(cudaStreamSynchronize(ds.stream));
   double t1 = now();
   fsgg::SampleRequest req;
   req.queries.resize(qe - qb);
