@@ -366,12 +366,12 @@ __global__ void __launch_bounds__(256)
                            const float* __restrict__ thi, int has_boxes,
                            const uint32_t* __restrict__ vlist,
                            const uint32_t* __restrict__ vcount, double* __restrict__ g1,
-                           double* __restrict__ g2) {
+                           double* __restrict__ g2, uint32_t first_tie) {
   __shared__ double red[2][256];
   __shared__ unsigned char keep[1024];
   const uint32_t cnt = *vcount;
   const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
-  for (uint32_t b = blockIdx.x; b < cnt; b += gridDim.x) {
+  for (uint32_t b = first_tie + blockIdx.x; b < cnt; b += gridDim.x) {
     const uint32_t i = vlist[b];
     const uint64_t h = ((1ull << level) - 1) + eg[i];
     const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
@@ -445,6 +445,126 @@ __global__ void __launch_bounds__(256)
       g2[i] = fmax(red[1][0], kSumFloor);
     }
     __syncthreads();
+  }
+}
+
+// Low-d tie guard split over (tie, sub-chunk) items, one warp each: a
+// level-1 tie scans a 500k-point node, and one CTA per tie left the GPU
+// nearly idle at the top levels (tens to thousands of ties). Each warp sums
+// its sub-chunk's fp64 terms (same terms and skip rule as
+// exact_sums_lowd_kernel) lane-strided, reduces them with a fixed butterfly
+// and writes one (left, right) partial; tie_split_reduce_kernel adds the
+// partials in sub-chunk order, so the result depends only on the (node,
+// query). Ties beyond the partial buffer's capacity (max_ties) are left to
+// exact_sums_lowd_kernel (first_tie = max_ties) — no host sync needed.
+constexpr uint32_t kTieSplitItems = 1u << 22;  // partial buffer: 4M items x 2 doubles
+constexpr int kTieSplitThreads = 256;
+
+__device__ __forceinline__ uint32_t tie_sub_depth(uint32_t level, uint32_t depth, uint32_t size) {
+  uint32_t kd = 0;
+  while (kd < 10 && level + kd + 1 <= depth && (size >> (kd + 1)) >= 256) ++kd;
+  return kd;
+}
+
+template <int D, int FAM>
+__global__ void __launch_bounds__(kTieSplitThreads)
+    tie_split_kernel(const float* __restrict__ pts, double sigma, float scale, uint32_t level,
+                     uint32_t depth, const uint32_t* __restrict__ eq,
+                     const uint32_t* __restrict__ eg, const float* __restrict__ elm,
+                     const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                     const float* __restrict__ tlo, const float* __restrict__ thi,
+                     int has_boxes, const uint32_t* __restrict__ vlist,
+                     const uint32_t* __restrict__ vcount, uint32_t max_chunks,
+                     uint32_t max_ties, double* __restrict__ part) {
+  const uint32_t ties = min(*vcount, max_ties);
+  const uint64_t items = uint64_t(ties) * max_chunks;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warps = uint64_t(gridDim.x) * (kTieSplitThreads / 32);
+  const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  for (uint64_t it = blockIdx.x * uint64_t(kTieSplitThreads / 32) + (threadIdx.x >> 5);
+       it < items; it += warps) {
+    const uint32_t b = uint32_t(it / max_chunks), c = uint32_t(it % max_chunks);
+    const uint32_t i = vlist[b];
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
+    const uint32_t kd = tie_sub_depth(level, depth, l - f);
+    double s0 = 0.0, s1 = 0.0;
+    if (c < (1u << kd)) {
+      const float* xq = pts + size_t(eq[i]) * D;
+      const uint64_t hb = ((1ull << (level + kd)) - 1) + (uint64_t(eg[i]) << kd) + c;
+      bool keep = true;
+      if (has_boxes && kd > 0) {
+        const float lim_base = (elm ? elm[i] : 0.f) - 1.f - 80.f;
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const float v = fmaxf(fmaxf(tlo[hb * D + a] - xq[a], xq[a] - thi[hb * D + a]), 0.f);
+          acc = (FAM == 2) ? acc + v : fmaf(v, v, acc);
+        }
+        const float dist = FAM == 1 ? sqrtf(acc) : acc;
+        const float sz = float(tlast[hb] - tfirst[hb]);
+        keep = __log2f(sz) - scale * dist >= lim_base;
+      }
+      if (keep) {
+        double q[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) q[k] = double(xq[k]);
+        const uint32_t cf = kd ? tfirst[hb] : f, cl = kd ? tlast[hb] : l;
+        for (uint32_t j = cf + lane; j < cl; j += 32) {
+          double x[D];
+          if constexpr (D == 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(pts) + j);
+            x[0] = double(v.x);
+            x[1] = double(v.y);
+          } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) x[a] = double(__ldg(pts + size_t(j) * D + a));
+          }
+          double t = 0.0;
+          if constexpr (FAM == 2) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) t += fabs(q[a] - x[a]);
+          } else {
+#pragma unroll
+            for (int a = 0; a < D; ++a) t = fma(q[a] - x[a], q[a] - x[a], t);
+            if constexpr (FAM == 1) t = sqrt(t);
+          }
+          const double v = exp(-t * inv);
+          if (j < mid)
+            s0 += v;
+          else
+            s1 += v;
+        }
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) {
+      part[it * 2] = s0;
+      part[it * 2 + 1] = s1;
+    }
+  }
+}
+
+__global__ void tie_split_reduce_kernel(const uint32_t* __restrict__ vlist,
+                                        const uint32_t* __restrict__ vcount,
+                                        uint32_t max_chunks, uint32_t max_ties,
+                                        const double* __restrict__ part,
+                                        double* __restrict__ g1, double* __restrict__ g2) {
+  const uint32_t ties = min(*vcount, max_ties);
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < ties;
+       b += gridDim.x * blockDim.x) {
+    double a = 0.0, c = 0.0;
+    const double* p = part + size_t(b) * max_chunks * 2;
+    for (uint32_t k = 0; k < max_chunks; ++k) {
+      a += p[2 * k];
+      c += p[2 * k + 1];
+    }
+    const uint32_t i = vlist[b];
+    g1[i] = fmax(a, kSumFloor);
+    g2[i] = fmax(c, kSumFloor);
   }
 }
 
@@ -1209,12 +1329,29 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       const bool lowd_done = lowd_exact_dispatch(ds.d, ks.family, [&](auto dim, auto fam) {
         constexpr int D = decltype(dim)::value;
         constexpr int FAM = decltype(fam)::value;
+        const float* lm = level == 0 ? nullptr : elm[cur]->as<float>();
+        const int boxes = t.has_boxes && req.prune ? 1 : 0;
+        // the level's largest node fixes the partial layout (sub-chunks per tie)
+        uint32_t kd = 0;
+        while (kd < 10 && level + kd + 1 <= t.depth && (smax_level >> (kd + 1)) >= 256) ++kd;
+        const uint32_t max_chunks = 1u << kd;
+        const uint32_t max_ties = kTieSplitItems / max_chunks;
+        DevBuf& part = ds.buf("s.tie_part", size_t(kTieSplitItems) * 16);
+        tie_split_kernel<D, FAM><<<ds.num_sms * 8, kTieSplitThreads, 0, s>>>(
+            ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
+            eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+            t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
+            max_chunks, max_ties, part.as<double>());
+        tie_split_reduce_kernel<<<ds.num_sms, 256, 0, s>>>(
+            vlist.as<uint32_t>(), vcount, max_chunks, max_ties, part.as<double>(),
+            g1.as<double>(), g2.as<double>());
+        // overflow ties (more than the partial buffer holds): one CTA each
         exact_sums_lowd_kernel<D, FAM><<<ds.num_sms * 4, 256, 0, s>>>(
             ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
-            eg[cur]->as<uint32_t>(), level == 0 ? nullptr : elm[cur]->as<float>(),
-            t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
-            t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
-            g2.as<double>());
+            eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+            t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
+            g1.as<double>(), g2.as<double>(), max_ties);
+        ds.launches += 2;
       });
       if (!lowd_done)
         exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(

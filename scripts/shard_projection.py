@@ -1,0 +1,138 @@
+"""Per-rank cost of the multi-GPU build, measured on ONE GPU.
+
+The descent has no collective (parallel.py), so what rank r of N does is a
+function of its query range alone: this script runs each rank's shard
+descent (fsgg_sample_shard) and its row-sharded finish (fsgg_finish_graph on
+the keys routed to it + fsgg_rows_transposed + fsgg_rows_degrees) one after
+another on one GPU, times each with a device sync on both sides (best of
+`--reps`), and reports max over ranks per phase. The NCCL exchanges are not
+run here (one GPU); their bytes are counted and reported separately.
+
+    python scripts/shard_projection.py [--n 1000000] [--worlds 1,2,4,8]
+
+This is a PROJECTION (the ranks never run concurrently here); bench.py under
+torchrun is the measurement.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2310_13870_b200 as F  # noqa: E402
+from paper_2310_13870_b200 import _native as N  # noqa: E402
+from paper_2310_13870_b200 import datasets, parallel  # noqa: E402
+
+
+def timed(fn, reps):
+    best, out = None, None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        best = dt if best is None else min(best, dt)
+    return best, out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--sigma", type=float, default=0.05)
+    ap.add_argument("--rounds", type=int, default=64)
+    ap.add_argument("--worlds", default="1,2,4,8")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    p, _ = datasets.make_moons(a.n, 0.05, 1)
+    p = p.astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(F.KernelFamily.gaussian, a.sigma)
+    L = a.rounds
+    # warm the arena with the full problem
+    F.build_similarity_graph_device(ds, k, F.SparsifierConfig(rounds=L, seed=1))
+    torch.cuda.synchronize()
+    full_t, _ = timed(lambda: F.build_similarity_graph_device(
+        ds, k, F.SparsifierConfig(rounds=L, seed=1)), a.reps)
+    result = {"n": a.n, "sigma": a.sigma, "L": L, "one_gpu_build_s": full_t, "worlds": {}}
+    print(f"1-GPU build {full_t * 1e3:.1f} ms", flush=True)
+    for world in [int(x) for x in a.worlds.split(",")]:
+        bounds = parallel.shard_bounds(a.n, world)
+        sample_s, root_s, pairs, gs = [], [], [], []
+        for r in range(world):
+            cfg = F.SparsifierConfig(rounds=L, seed=1, query_begin=bounds[r],
+                                     query_end=bounds[r + 1])
+            t, (sh, rep, pr, g) = timed(lambda: parallel.sample_shard(ds, k, cfg), a.reps)
+            sample_s.append(t)
+            root_s.append(rep.kde_root_seconds)
+            pairs.append(pr)
+            gs.append(g)
+        g_full = torch.cat(gs)
+        routed = [[] for _ in range(world)]
+        for t in pairs:
+            for d, piece in enumerate(torch.split(t, parallel.owner_splits(t >> 32, bounds))):
+                routed[d].append(piece)
+        routed = [torch.cat(x) for x in routed]
+        finish_s, lower_bytes, vs, ws = [], [], [], []
+        for d in range(world):
+            def fin():
+                graph, _ = parallel.finish_graph(ds, k, L, g_full, routed[d])
+                m = int(graph.num_edges)
+                v = torch.empty(m, dtype=torch.int32, device="cuda")
+                w = torch.empty(m, dtype=torch.float64, device="cuda")
+                N.check(N.lib().fsgg_rows_transposed(ds._h, C.c_void_p(v.data_ptr()),
+                                                     C.c_void_p(w.data_ptr())))
+                return v, w
+            t, (v, w) = timed(fin, a.reps)
+            vs.append(v)
+            ws.append(w)
+            # degrees: received lower contributions (emulated routing) + own rows
+            sp = parallel.owner_splits(v.to(torch.int64), bounds)
+            lower_bytes.append(sum(sp[i] for i in range(world) if i != d) * 12)
+            finish_s.append(t)
+        deg_s = []
+        for d in range(world):
+            lv = torch.cat([torch.split(vs[s], parallel.owner_splits(vs[s].to(torch.int64),
+                                                                     bounds))[d]
+                            for s in range(world)])
+            lw = torch.cat([torch.split(ws[s], parallel.owner_splits(vs[s].to(torch.int64),
+                                                                     bounds))[d]
+                            for s in range(world)])
+            deg = torch.empty(bounds[d + 1] - bounds[d], dtype=torch.float64, device="cuda")
+            t, _ = timed(lambda: N.check(N.lib().fsgg_rows_degrees(
+                ds._h, C.c_void_p(lv.data_ptr() if lv.numel() else 0),
+                C.c_void_p(lw.data_ptr() if lw.numel() else 0), lv.numel(), bounds[d],
+                bounds[d + 1], C.c_void_p(deg.data_ptr()))), a.reps)
+            deg_s.append(t)
+        key_bytes = [sum(x.numel() for i, x in enumerate(
+            torch.split(pairs[s], parallel.owner_splits(pairs[s] >> 32, bounds))) if i != s) * 8
+            for s in range(world)]
+        per_rank = [sample_s[r] + finish_s[r] + deg_s[r] for r in range(world)]
+        w_out = {
+            "sample_s": sample_s, "root_kernel_s": root_s, "finish_s": finish_s,
+            "degrees_s": deg_s,
+            "max_sample_s": max(sample_s), "max_finish_s": max(finish_s),
+            "max_degrees_s": max(deg_s),
+            "max_rank_compute_s": max(max(sample_s), 0) + max(finish_s) + max(deg_s),
+            "exchange_bytes_per_rank_max": max(key_bytes) + max(lower_bytes) + 8 * a.n,
+            "projected_speedup_compute_only": full_t / (max(sample_s) + max(finish_s)
+                                                        + max(deg_s)),
+        }
+        result["worlds"][world] = w_out
+        print(world, json.dumps({k2: (round(v2, 5) if isinstance(v2, float) else v2)
+                                 for k2, v2 in w_out.items() if not isinstance(v2, list)}),
+              "sample", [round(x * 1e3, 2) for x in sample_s],
+              "root", [round(x * 1e3, 2) for x in root_s], flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(result, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
