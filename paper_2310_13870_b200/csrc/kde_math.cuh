@@ -74,7 +74,11 @@ __device__ __forceinline__ float box_dist_d(const float (&q)[D], const float* lo
 __device__ __forceinline__ double rescale_off(double acc, float off) {
   if (!(off > 0.f)) return acc;
   const float j = floorf(off);
-  return ldexp(acc * static_cast<double>(ex2_approx(j - off)), -static_cast<int>(j));
+  const double m = acc * static_cast<double>(ex2_approx(j - off));
+  // 2^-j built from its exponent bits: the same bits as ldexp(m, -j) (an
+  // exact power-of-two scaling), without the library call
+  if (j > 1022.f) return ldexp(m, -static_cast<int>(j));
+  return m * __hiloint2double((1023 - static_cast<int>(j)) << 20, 0);
 }
 
 // Child sums of a small node (heap index h, points [f, l), l - f >= 2) for

@@ -138,12 +138,16 @@ __global__ void __launch_bounds__(kWalkThreads)
         h = dc.left ? 2 * h + 1 : 2 * h + 2;
         ++lev;
       }
-      // per-level tallies, one shared-memory update per level group of the warp
-      const unsigned grp = __match_any_sync(live_mask, at);
+      // per-level tallies, one shared-memory update per level group of the
+      // warp; lanes of a warp almost always share the level (fast path)
+      const uint32_t lead_at = __shfl_sync(live_mask, at, __ffs(live_mask) - 1);
+      const unsigned grp = __all_sync(live_mask, at == lead_at) ? live_mask
+                                                                : __match_any_sync(live_mask, at);
       const uint32_t n_ent = __popc(grp);
       const uint32_t n_ev = __reduce_add_sync(grp, ev);
-      const uint32_t n_dg = __reduce_add_sync(grp, dg);
-      const uint32_t n_tie = __reduce_add_sync(grp, tie);
+      const bool rare = __any_sync(grp, dg | tie);
+      const uint32_t n_dg = rare ? __reduce_add_sync(grp, dg) : 0u;
+      const uint32_t n_tie = rare ? __reduce_add_sync(grp, tie) : 0u;
       if ((threadIdx.x & 31) == uint32_t(__ffs(grp) - 1) && at < kMaxLevels) {
         atomicAdd(&s_stats[0][at], static_cast<unsigned long long>(n_ent));
         if (n_ev) atomicAdd(&s_stats[1][at], static_cast<unsigned long long>(n_ev));
