@@ -156,6 +156,11 @@ struct KdeWorkspace {
   // depths 1..rd-1 at offsets 2^m - 2 (a lookup then reads two values).
   DevBuf partials, pyr, blk_off, cub_tmp;
   uint32_t pyr_depth = 0;  // row depth the pyramid was built for (0: none)
+  // symmetric root (kde_sym.cu): block depth Lb of the last root pass (0: the
+  // root was not symmetric). Its per-(point, partner block) values stay in
+  // the arena ("sym.*") and serve levels whose children are unions of
+  // blocks (block_lookup_sums, kde_sym.cu).
+  uint32_t sym_Lb = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~KdeWorkspace();
 };
@@ -255,6 +260,14 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
                         cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 // Depth of the symmetric pass's blocks (0: the pass does not apply).
 uint32_t sym_block_depth(const Dataset& ds);
+// Child sums of level `level` (1 <= level, level + 1 <= ws.sym_Lb) from the
+// symmetric root's per-(point, partner block) values: each child of a node
+// at this level is a run of whole blocks, so its sum for query q is the sum,
+// in ascending partner order, of q's values for the partners in that run.
+// Adds the reference-equivalent evaluations to *evals (device counter).
+void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,
+                       const uint32_t* eg, double* g1, double* g2,
+                       unsigned long long* evals);
 
 // ---- walk.cu --------------------------------------------------------------
 // Entries holding a single ticket below nodes of kWalkMaxNode points leave

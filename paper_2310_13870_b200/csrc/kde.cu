@@ -894,6 +894,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const bool sym = Lb > 0 && kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials,
                                                 d_perf, ws.ev0, ws.ev1);
   if (Lb > 0 && !sym) throw NumericError("symmetric root pass rejected its row depth");
+  if (lv.level == 0) ws.sym_Lb = sym ? Lb : 0;
   if (sym) {
     // every pair evaluated once (kde_sym.cu)
   } else if (lowd) {

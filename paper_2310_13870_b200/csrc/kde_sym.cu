@@ -308,6 +308,93 @@ __global__ void __launch_bounds__(kSymBlock)
   }
 }
 
+// Block index of every point (blocks are the depth-Lb tree nodes).
+__global__ void sym_qblock_kernel(const uint32_t* __restrict__ bf,
+                                  const uint32_t* __restrict__ bl,
+                                  uint32_t* __restrict__ qblk) {
+  const uint32_t I = blockIdx.x;
+  for (uint32_t p = bf[I] + threadIdx.x; p < bl[I]; p += blockDim.x) qblk[p] = I;
+}
+
+// One thread per entry, kBlkUnroll entries per thread (all loads first). The
+// node's blocks are [B0, B1) (heap slot g at `level` covers blocks
+// g << (Lb - level) ...); q's partners in that run are a contiguous range of
+// its block's ascending partner list: one lower_bound for B0, then a forward
+// scan that sums the values of the left half [B0, Bm) and the right half
+// [Bm, B1) in partner order (fp64), exactly the values the root rows fold.
+constexpr int kBlkThreads = 256;
+constexpr int kBlkUnroll = 2;
+__global__ void __launch_bounds__(kBlkThreads)
+    block_lookup_kernel(uint32_t E, uint32_t level, uint32_t Lb,
+                        const uint32_t* __restrict__ eq, const uint32_t* __restrict__ eg,
+                        const uint32_t* __restrict__ qblk, const uint32_t* __restrict__ bf,
+                        const uint32_t* __restrict__ poff, const uint32_t* __restrict__ plist,
+                        const float* __restrict__ P, const uint32_t* __restrict__ tfirst,
+                        const uint32_t* __restrict__ tlast, double* __restrict__ g1,
+                        double* __restrict__ g2, unsigned long long* __restrict__ evals) {
+  constexpr int U = kBlkUnroll;
+  const uint32_t base = blockIdx.x * (kBlkThreads * U) + threadIdx.x;
+  const uint32_t sh = Lb - level;
+  uint32_t q[U], g[U], I[U], size[U], k[U], k1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kBlkThreads;
+    q[u] = i < E ? eq[i] : 0u;
+    g[u] = i < E ? eg[i] : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t h = ((1ull << level) - 1) + g[u];
+    size[u] = base + u * kBlkThreads < E ? tlast[h] - tfirst[h] : 0u;
+    I[u] = qblk[q[u]];
+    k[u] = poff[I[u]];
+    k1[u] = poff[I[u] + 1];
+  }
+  double a[U], b[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a[u] = b[u] = 0.0;
+    const uint32_t B0 = g[u] << sh, Bm = B0 + (1u << (sh - 1)), B1 = B0 + (1u << sh);
+    // lower_bound(B0) in plist[k, k1)
+    uint32_t lo = k[u], hi = k1[u];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(plist + mid) < B0)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const uint32_t t = q[u] - bf[I[u]];
+    for (uint32_t kk = lo; kk < k1[u]; ++kk) {
+      const uint32_t J = __ldg(plist + kk);
+      if (J >= B1) break;
+      const double v = double(__ldg(P + size_t(kk) * 256 + t));
+      if (J < Bm)
+        a[u] += v;
+      else
+        b[u] += v;
+    }
+  }
+  unsigned long long ev = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t i = base + u * kBlkThreads;
+    if (i >= E) continue;
+    g1[i] = fmax(a[u], kSumFloor);
+    g2[i] = fmax(b[u], kSumFloor);
+    ev += size[u];
+  }
+  __shared__ unsigned long long red[kBlkThreads / 32];
+  for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ev;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tot = 0;
+    for (int w = 0; w < kBlkThreads / 32; ++w) tot += red[w];
+    if (tot) atomicAdd(evals, tot);
+  }
+}
+
 template <class F>
 void sym_by_dim(uint32_t d, F&& f) {
   switch (d) {
@@ -416,6 +503,10 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
     FSGG_LAUNCH_CHECK();
   }
   if (ev1) FSGG_CUDA(cudaEventRecord(ev1, s));
+  DevBuf& qblk = ds.buf("sym.qblk", size_t(ds.n) * 4);
+  sym_qblock_kernel<<<B, 256, 0, s>>>(bf, bl, qblk.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
   if (b0 <= b1) {
     sym_rows_kernel<<<b1 - b0 + 1, kSymBlock, 0, s>>>(P.as<float>(), poff.as<uint32_t>(),
                                                      plist.as<uint32_t>(), bf, bl, b0,
@@ -424,6 +515,24 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   }
   ds.launches += 7;
   return true;
+}
+
+void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,
+                       const uint32_t* eg, double* g1, double* g2,
+                       unsigned long long* evals) {
+  const uint32_t Lb = ds.kde_ws ? ds.kde_ws->sym_Lb : 0;
+  if (Lb == 0 || level == 0 || level + 1 > Lb) throw NumericError("no symmetric block values");
+  if (E == 0) return;
+  const TreeTable& t = ds.tree;
+  const uint64_t hb = (uint64_t(1) << Lb) - 1;
+  cudaStream_t s = ds.stream;
+  block_lookup_kernel<<<ceil_div_u32(E, kBlkThreads * kBlkUnroll), kBlkThreads, 0, s>>>(
+      E, level, Lb, eq, eg, ds.buf("sym.qblk", 4).as<uint32_t>(), t.first.as<uint32_t>() + hb,
+      ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
+      ds.buf("sym.P", 4).as<float>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(), g1, g2,
+      evals);
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
 }
 
 }  // namespace fsgg

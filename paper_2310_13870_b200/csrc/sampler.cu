@@ -44,6 +44,12 @@ uint32_t root_serve_levels() {
   return e ? uint32_t(std::atoi(e)) : kServeLevelsRoot;
 }
 
+// Block-value lookups below the root rows (FSGG_BLK_LOOKUP=0 disables).
+bool blk_lookup_on() {
+  const char* e = std::getenv("FSGG_BLK_LOOKUP");  // read per call: tests toggle it
+  return !e || std::atoi(e) != 0;
+}
+
 // Levels whose nodes all hold <= this many points are finished depth-first
 // (finish.cu); FSGG_DFS_MAX overrides (0 disables).
 uint32_t dfs_max_node() {
@@ -1251,8 +1257,20 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     lv.goff = goff[cur]->as<uint32_t>();
     if (level == 0 && contiguous) lv.qbase = req.queries.front();
     const bool lookup = have_rows && level - row_level < row_depth;
+    // below the root rows' reach, the symmetric root's block values still
+    // hold every child sum while children are unions of its blocks
+    const bool blk_lookup = !lookup && have_rows && row_level == 0 && level > 0 &&
+                            ws.sym_Lb > 0 && level + 1 <= ws.sym_Lb && blk_lookup_on();
     bool self_rows = false;
-    if (lookup) {
+    if (blk_lookup) {
+      FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
+      block_lookup_sums(ds, E, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+                        g1.as<double>(), g2.as<double>(), lookup_evals.as<unsigned long long>());
+      unsigned long long ev = 0;
+      FSGG_CUDA(cudaMemcpyAsync(&ev, lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      out.kde.evals += ev;
+    } else if (lookup) {
       FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
       lookup_sums_kernel<<<ceil_div_u32(E, kLookupThreads * kLookupUnroll), kLookupThreads, 0, s>>>(
           E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),

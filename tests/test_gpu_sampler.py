@@ -451,6 +451,40 @@ def test_single_ticket_walks_match_level_synchronous(rng):
         assert outs[0][1].degenerate_draws == d.degenerate_draws
 
 
+def test_block_lookups_match_computed_levels():
+    """Levels served from the symmetric root's per-(point, partner block)
+    values (block_lookup_sums, FSGG_BLK_LOOKUP) give the same samples and
+    diagnostics as computing those levels; shallow root rows
+    (FSGG_ROOT_SERVE=4) make levels 4-7 block lookups at this n."""
+    import os
+    p, _ = datasets.make_moons(60000, 0.05, 11)
+    ds = F.Dataset(p.astype(np.float32))
+    k = F.Kernel(F.KernelFamily.gaussian, 0.06)
+    outs = []
+    saved = {v: os.environ.get(v) for v in ("FSGG_BLK_LOOKUP", "FSGG_ROOT_SERVE")}
+    try:
+        for serve, blk in (("4", "0"), ("4", "1"), (None, "1")):
+            if serve is None:
+                os.environ.pop("FSGG_ROOT_SERVE", None)
+            else:
+                os.environ["FSGG_ROOT_SERVE"] = serve
+            os.environ["FSGG_BLK_LOOKUP"] = blk
+            tri, d = F.sample_neighbors_counted(ds, k, np.arange(60000), 16, 5,
+                                                diagnostics=True)
+            outs.append((tri, d))
+    finally:
+        for v, old in saved.items():
+            if old is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = old
+    for tri, d in outs[1:]:
+        assert np.array_equal(outs[0][0], tri)
+        assert list(outs[0][1].entries_per_level) == list(d.entries_per_level)
+        assert list(outs[0][1].tickets_per_level) == list(d.tickets_per_level)
+        assert outs[0][1].degenerate_draws == d.degenerate_draws
+
+
 def test_symmetric_root_matches_one_sided():
     """The symmetric root pass (kde_sym.cu, each pair evaluated once) and the
     one-sided tiled pass give the same samples and edge set; g_full differs
