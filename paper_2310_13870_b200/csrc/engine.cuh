@@ -161,6 +161,8 @@ struct KdeWorkspace {
   // the arena ("sym.*") and serve levels whose children are unions of
   // blocks (block_lookup_sums, kde_sym.cu).
   uint32_t sym_Lb = 0;
+  uint32_t sym_b0 = 0;       // first query block of that pass
+  bool sym_pos = false;      // "sym.pos" holds the partner-position table
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~KdeWorkspace();
 };
@@ -260,6 +262,7 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
                         cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
 // Depth of the symmetric pass's blocks (0: the pass does not apply).
 uint32_t sym_block_depth(const Dataset& ds);
+constexpr uint32_t kSymRootServe = 7;  // symmetric root: fp64 rows serve levels 1..6
 // Child sums of level `level` (1 <= level, level + 1 <= ws.sym_Lb) from the
 // symmetric root's per-(point, partner block) values: each child of a node
 // at this level is a run of whole blocks, so its sum for query q is the sum,

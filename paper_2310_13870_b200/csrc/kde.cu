@@ -872,6 +872,14 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                           ? sym_block_depth(ds)
                           : 0;
   if (Lb > 0) {
+    // the block values (block_lookup_sums) serve every level whose children
+    // are unions of blocks, so the fp64 rows only need to reach the levels
+    // where a block lookup would sum many partners: kSymRootServe (measured
+    // at C3: rows for levels 1-6 + block lookups for 7-11 beat rows to 8)
+    if (!std::getenv("FSGG_ROOT_SERVE")) {
+      serve_levels = std::min(serve_levels, kSymRootServe);
+      rl = std::min(rl, serve_levels);
+    }
     uint32_t want = std::min(std::max(rl, std::min(serve_levels, Lb)), Lb);
     while (want > 1 && (uint64_t(E) << (want + 1)) > kMaxPartials) --want;
     rl = want;

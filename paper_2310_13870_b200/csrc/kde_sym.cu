@@ -316,6 +316,24 @@ __global__ void sym_qblock_kernel(const uint32_t* __restrict__ bf,
   for (uint32_t p = bf[I] + threadIdx.x; p < bl[I]; p += blockDim.x) qblk[p] = I;
 }
 
+// pos[I - b0][J] = position of the first partner >= J in I's ascending
+// partner list (J = 0..B), for the query blocks I in [b0, b0 + gridDim.x):
+// a lookup then finds the partner run of any block range with three
+// independent loads instead of a binary search.
+constexpr uint32_t kSymPosMaxBlocks = 8192;  // table (B + 1)^2 x 4 bytes <= 256 MiB
+__global__ void sym_pos_kernel(uint32_t B, uint32_t b0, const uint32_t* __restrict__ poff,
+                               const uint32_t* __restrict__ plist, uint32_t* __restrict__ pos) {
+  const uint32_t I = b0 + blockIdx.x;
+  uint32_t* row = pos + size_t(blockIdx.x) * (B + 1);
+  const uint32_t p0 = poff[I], p1 = poff[I + 1];
+  for (uint32_t k = p0 + threadIdx.x; k < p1; k += blockDim.x) {
+    const uint32_t from = k == p0 ? 0u : plist[k - 1] + 1;
+    for (uint32_t J = from; J <= plist[k]; ++J) row[J] = k;
+  }
+  const uint32_t tail = p1 > p0 ? plist[p1 - 1] + 1 : 0u;
+  for (uint32_t J = tail + threadIdx.x; J <= B; J += blockDim.x) row[J] = p1;
+}
+
 // One thread per entry, kBlkUnroll entries per thread (all loads first). The
 // node's blocks are [B0, B1) (heap slot g at `level` covers blocks
 // g << (Lb - level) ...); q's partners in that run are a contiguous range of
@@ -330,7 +348,8 @@ __global__ void __launch_bounds__(kBlkThreads)
                         const uint32_t* __restrict__ qblk, const uint32_t* __restrict__ bf,
                         const uint32_t* __restrict__ poff, const uint32_t* __restrict__ plist,
                         const float* __restrict__ P, const uint32_t* __restrict__ tfirst,
-                        const uint32_t* __restrict__ tlast, double* __restrict__ g1,
+                        const uint32_t* __restrict__ tlast, const uint32_t* __restrict__ pos,
+                        uint32_t b0, double* __restrict__ g1,
                         double* __restrict__ g2, unsigned long long* __restrict__ evals) {
   constexpr int U = kBlkUnroll;
   const uint32_t base = blockIdx.x * (kBlkThreads * U) + threadIdx.x;
@@ -351,6 +370,28 @@ __global__ void __launch_bounds__(kBlkThreads)
     k1[u] = poff[I[u] + 1];
   }
   double a[U], b[U];
+  if (pos) {  // partner runs from the position table
+    const uint32_t W = (1u << Lb) + 1;
+    uint32_t km[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      k[u] = km[u] = k1[u] = 0;
+      if (base + u * kBlkThreads < E) {  // (a padding lane's query 0 may precede b0)
+        const uint32_t* row = pos + size_t(I[u] - b0) * W;
+        const uint32_t B0 = g[u] << sh;
+        k[u] = row[B0];
+        km[u] = row[B0 + (1u << (sh - 1))];
+        k1[u] = row[B0 + (1u << sh)];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = b[u] = 0.0;
+      const float* pv = P + (q[u] - bf[I[u]]);
+      for (uint32_t kk = k[u]; kk < km[u]; ++kk) a[u] += double(__ldg(pv + size_t(kk) * 256));
+      for (uint32_t kk = km[u]; kk < k1[u]; ++kk) b[u] += double(__ldg(pv + size_t(kk) * 256));
+    }
+  } else
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     a[u] = b[u] = 0.0;
@@ -503,6 +544,15 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
     FSGG_LAUNCH_CHECK();
   }
   if (ev1) FSGG_CUDA(cudaEventRecord(ev1, s));
+  ds.kde_ws->sym_b0 = b0;
+  ds.kde_ws->sym_pos = B <= kSymPosMaxBlocks && b0 <= b1;
+  if (ds.kde_ws->sym_pos) {
+    DevBuf& pos = ds.buf("sym.pos", size_t(b1 - b0 + 1) * (B + 1) * 4);
+    sym_pos_kernel<<<b1 - b0 + 1, 256, 0, s>>>(B, b0, poff.as<uint32_t>(), plist.as<uint32_t>(),
+                                              pos.as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
   DevBuf& qblk = ds.buf("sym.qblk", size_t(ds.n) * 4);
   sym_qblock_kernel<<<B, 256, 0, s>>>(bf, bl, qblk.as<uint32_t>());
   FSGG_LAUNCH_CHECK();
@@ -529,8 +579,9 @@ void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* 
   block_lookup_kernel<<<ceil_div_u32(E, kBlkThreads * kBlkUnroll), kBlkThreads, 0, s>>>(
       E, level, Lb, eq, eg, ds.buf("sym.qblk", 4).as<uint32_t>(), t.first.as<uint32_t>() + hb,
       ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
-      ds.buf("sym.P", 4).as<float>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(), g1, g2,
-      evals);
+      ds.buf("sym.P", 4).as<float>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+      ds.kde_ws->sym_pos ? ds.buf("sym.pos", 4).as<uint32_t>() : nullptr, ds.kde_ws->sym_b0, g1,
+      g2, evals);
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }

@@ -284,13 +284,13 @@ def test_p_hat_band(oracle):
     assert np.all(est["p_hat"] >= 6 / 7 * pref) and np.all(est["p_hat"] <= 36 / 5 * pref)
 
 
-@pytest.mark.parametrize("n", [3000, 3500, 14000])
+@pytest.mark.parametrize("n", [3000, 3500, 14000, 60000])
 def test_sharded_build_is_bit_identical(oracle, n):
     """Query shards processed separately (as on N GPUs) and merged through
     fsgg_finish_graph reproduce the 1-GPU graph bit for bit — with the
     one-sided root (n = 3000) and the symmetric root pass (3500, 14000: root
     blocks of >= 192 points; a shard computes the block-pair tiles touching
-    its blocks)."""
+    its blocks; 60000: level 7 is served from the shard's block values)."""
     import torch
     from paper_2310_13870_b200 import parallel
     p, _ = datasets.make_moons(n, 0.05, 2)
