@@ -849,7 +849,11 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   uint32_t rl;
   if (tc) {
     sd = 0;
-    while ((child_min >> (sd + 1)) >= kTcSubMin && lv.level + 2 + sd <= t.depth &&
+    // small nodes: buckets down to single points, so one tensor-core pass
+    // serves every remaining level by lookups (C5 levels 12-15: the direct
+    // warp-per-entry kernel re-read each 784-d query once per level)
+    const uint32_t tc_sub_min = child_min >= 8 * kTcSubMin ? kTcSubMin : 1u;
+    while ((child_min >> (sd + 1)) >= tc_sub_min && lv.level + 2 + sd <= t.depth &&
            sd + 1 < env_u32("FSGG_TC_ROWDEPTH", kTcMaxRowDepth) &&
            (uint64_t(E) << (sd + 2)) <= kMaxPartials)
       ++sd;

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   uint32_t num_slots, uint32_t total_blocks, uint32_t level, uint32_t cdepth,
                   uint32_t sdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
-                  float scale, double* __restrict__ partials, int terms) {
+                  float scale, double* __restrict__ partials, int terms, int whole) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   // share their query and source tiles through L2 (the hi/lo copies of C5
   // are 440 MB; with a block-major order every CTA streams its sources from
   // DRAM) ----
+  // whole: nodes of <= kTcN points take one item per (entry block, node),
+  // both children in one N tile (each query tile gathered once, not twice)
   const uint32_t K = 1u << cdepth;
-  const uint32_t cols = 2u * K;
+  const uint32_t cols = whole ? 1u : 2u * K;
   uint32_t blk, col;
   {
     const uint32_t grp = blockIdx.x / (kTcGroup * cols);
@@ -242,8 +244,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     blk = grp * kTcGroup + r % gsize;
     col = r / gsize;
   }
-  const uint32_t side = col >> cdepth;
-  const uint32_t kk = col & (K - 1);
+  const uint32_t side = whole ? 0u : col >> cdepth;
+  const uint32_t kk = whole ? 0u : col & (K - 1);
   uint32_t g;
   {
     uint32_t lo_ = 0, hi_ = num_slots;
@@ -256,7 +258,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kTcM;
   const uint32_t e1 = min(e0 + uint32_t(kTcM), goff[g + 1]);
   const uint32_t lc = level + 1 + cdepth;
-  const uint64_t h = ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
+  const uint64_t h = whole ? ((1ull << level) - 1) + g
+                           : ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
   const uint32_t cf = tfirst[h], cl = tlast[h];
   const uint32_t ntiles = (cl - cf + kTcN - 1) / kTcN;
   const uint32_t kblocks = d_pad / kTcKB;
@@ -530,11 +533,14 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                                    kSmemBytes));
     attr[ds.device] = true;
   }
-  kern<<<dim3(static_cast<uint32_t>(items)), kTcThreads, kSmemBytes, ds.stream>>>(
+  const uint32_t s_max = uint32_t((uint64_t(ds.n) + (1ull << lv.level) - 1) >> lv.level);
+  const int whole = cdepth == 0 && s_max <= uint32_t(kTcN) ? 1 : 0;
+  const uint64_t launch = whole ? items / 2 : items;
+  kern<<<dim3(static_cast<uint32_t>(launch)), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, st.gmap_hi, st.gmap_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
       static_cast<uint32_t>(items >> (cdepth + 1)), lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
-      tc_terms());
+      tc_terms(), whole);
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }

@@ -559,18 +559,26 @@ __global__ void tie_split_reduce_kernel(const uint32_t* __restrict__ vlist,
                                         uint32_t max_chunks, uint32_t max_ties,
                                         const double* __restrict__ part,
                                         double* __restrict__ g1, double* __restrict__ g2) {
+  // one warp per tie: lane-strided partial sums, then a fixed butterfly
   const uint32_t ties = min(*vcount, max_ties);
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < ties;
-       b += gridDim.x * blockDim.x) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < ties;
+       b += (gridDim.x * blockDim.x) >> 5) {
     double a = 0.0, c = 0.0;
     const double* p = part + size_t(b) * max_chunks * 2;
-    for (uint32_t k = 0; k < max_chunks; ++k) {
+    for (uint32_t k = lane; k < max_chunks; k += 32) {
       a += p[2 * k];
       c += p[2 * k + 1];
     }
-    const uint32_t i = vlist[b];
-    g1[i] = fmax(a, kSumFloor);
-    g2[i] = fmax(c, kSumFloor);
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      const uint32_t i = vlist[b];
+      g1[i] = fmax(a, kSumFloor);
+      g2[i] = fmax(c, kSumFloor);
+    }
   }
 }
 
@@ -1360,7 +1368,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
             eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
             t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
             max_chunks, max_ties, part.as<double>());
-        tie_split_reduce_kernel<<<ds.num_sms, 256, 0, s>>>(
+        tie_split_reduce_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
             vlist.as<uint32_t>(), vcount, max_chunks, max_ties, part.as<double>(),
             g1.as<double>(), g2.as<double>());
         // overflow ties (more than the partial buffer holds): one CTA each
