@@ -614,8 +614,9 @@ bool lowd_exact_dispatch(uint32_t d, int family, F&& f) {
 // (kernel_f64's order), exp in fp64. Per-(tie, chunk) partials are combined
 // in chunk order by tie_reduce_kernel, so results are deterministic.
 constexpr uint32_t kTieBatchMinDim = 32;  // below: exact_sums_kernel (pruned sub-chunks)
-constexpr uint32_t kTieBatchMinNode = 16384;  // smaller nodes: one CTA per tie is cheaper
-constexpr int kTieBatch = 16;
+constexpr uint32_t kTieBatchMinNode = 1024;  // smaller nodes: one CTA per tie is cheaper
+constexpr uint32_t kTieBatchMaxDim = 3200;    // fp64 batch queries in shared memory (<= 200 KiB)
+constexpr int kTieBatch = 8;
 constexpr uint32_t kTieChunk = 1024;
 constexpr int kTieThreads = 128;
 
@@ -634,12 +635,14 @@ __global__ void __launch_bounds__(kTieThreads)
                      const uint32_t* __restrict__ eq, const uint32_t* __restrict__ sorted,
                      const TieItem* __restrict__ items, uint32_t max_chunks,
                      double* __restrict__ partials) {
-  extern __shared__ __align__(16) float tq[];  // [kTieBatch][d]
+  // the batch's queries, converted to fp64 once (a per-term F2F of every
+  // batch query kept the conversion (XU) pipe saturated)
+  extern __shared__ __align__(16) double tq[];  // [kTieBatch][d]
   __shared__ double red[kTieThreads / 32][kTieBatch][2];
   const TieItem it = items[blockIdx.x];
   for (uint32_t idx = threadIdx.x; idx < it.count * d; idx += blockDim.x) {
     const uint32_t t = idx / d, a = idx % d;
-    tq[idx] = pts[size_t(eq[sorted[it.first + t]]) * d + a];
+    tq[idx] = double(pts[size_t(eq[sorted[it.first + t]]) * d + a]);
   }
   __syncthreads();
   double s0[kTieBatch], s1[kTieBatch];
@@ -662,9 +665,10 @@ __global__ void __launch_bounds__(kTieThreads)
 #pragma unroll
         for (int t = 0; t < kTieBatch; ++t) {
           if (uint32_t(t) < it.count) {
-            const float4 q4 = *reinterpret_cast<const float4*>(tq + t * d + a);
-            const double d0 = double(q4.x) - x0, d1 = double(q4.y) - x1;
-            const double d2 = double(q4.z) - x2, d3 = double(q4.w) - x3;
+            const double2 qa = *reinterpret_cast<const double2*>(tq + t * d + a);
+            const double2 qb = *reinterpret_cast<const double2*>(tq + t * d + a + 2);
+            const double d0 = qa.x - x0, d1 = qa.y - x1;
+            const double d2 = qb.x - x2, d3 = qb.y - x3;
             if (family == 2) {
               acc[t] = acc[t] + fabs(d0);
               acc[t] = acc[t] + fabs(d1);
@@ -685,7 +689,7 @@ __global__ void __launch_bounds__(kTieThreads)
 #pragma unroll
       for (int t = 0; t < kTieBatch; ++t) {
         if (uint32_t(t) < it.count) {
-          const double df = double(tq[t * d + a]) - xv;
+          const double df = tq[t * d + a] - xv;
           acc[t] = family == 2 ? acc[t] + fabs(df) : fma(df, df, acc[t]);
         }
       }
@@ -1046,18 +1050,30 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
       hl[b] = fl[2 * b + 1];
     }
   }
+  // source chunk: kTieChunk, shortened (to >= 128 sources) when the level's
+  // batches x chunks would not give every SM several CTAs
+  uint64_t batch_sources = 0;
+  for (uint32_t b = 0; b < cnt;) {
+    uint32_t e = b + 1;
+    while (e < cnt && slot[e] == slot[b] && e - b < uint32_t(kTieBatch)) ++e;
+    batch_sources += hl[b] - hf[b];
+    b = e;
+  }
+  const uint64_t want_items = uint64_t(ds.num_sms) * 16;
+  uint32_t chunk_len = kTieChunk;
+  while (chunk_len > 128 && batch_sources / chunk_len < want_items) chunk_len >>= 1;
   for (uint32_t b = 0; b < cnt;) {
     uint32_t e = b + 1;
     while (e < cnt && slot[e] == slot[b] && e - b < uint32_t(kTieBatch)) ++e;
     const uint32_t f = hf[b], l = hl[b], mid = f + (l - f) / 2;
-    const uint32_t chunks = std::max<uint32_t>(1, (l - f + kTieChunk - 1) / kTieChunk);
+    const uint32_t chunks = std::max<uint32_t>(1, (l - f + chunk_len - 1) / chunk_len);
     max_chunks = std::max(max_chunks, chunks);
     for (uint32_t c = 0; c < chunks; ++c) {
       TieItem it;
       it.first = b;
       it.count = e - b;
-      it.src0 = f + c * kTieChunk;
-      it.src1 = std::min(l, it.src0 + kTieChunk);
+      it.src0 = f + c * chunk_len;
+      it.src1 = std::min(l, it.src0 + chunk_len);
       it.mid = mid;
       it.chunk = c;
       it.nchunks = chunks;
@@ -1073,7 +1089,7 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
   FSGG_CUDA(cudaMemcpyAsync(ditems.as<void>(), items.data(), items.size() * sizeof(TieItem),
                             cudaMemcpyHostToDevice, s));
   FSGG_CUDA(cudaMemcpyAsync(dnch.as<void>(), nch.data(), size_t(cnt) * 4, cudaMemcpyHostToDevice, s));
-  const size_t smem = size_t(kTieBatch) * ds.d * 4;
+  const size_t smem = size_t(kTieBatch) * ds.d * 8;
   FSGG_CUDA(cudaFuncSetAttribute(tie_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(std::max<size_t>(smem, 48u << 10))));
   tie_batch_kernel<<<uint32_t(items.size()), kTieThreads, smem, s>>>(
@@ -1335,7 +1351,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
         verify ? vlist.as<uint32_t>() : nullptr, vcount, wk);
     FSGG_LAUNCH_CHECK();
-    if (verify && ds.d >= kTieBatchMinDim && smax_level >= kTieBatchMinNode) {
+    if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
+        smax_level >= kTieBatchMinNode) {
       // high d: batched fp64 recomputation (tie_batch_kernel), then reroute
       uint32_t cnt = 0;
       FSGG_CUDA(cudaMemcpyAsync(&cnt, vcount, 4, cudaMemcpyDeviceToHost, s));
