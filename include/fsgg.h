@@ -354,6 +354,31 @@ int fsgg_sample_shard(fsgg_dataset* ds, const fsgg_kernel* kernel,
  * may be NULL); completes before returning. */
 int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
                       double* g_full_device);
+/* Owner mode of the symmetric root pass (low d, multi-GPU). At the root
+ * every query is a source, and the block-pair tiles between two shards
+ * serve both: instead of both ranks evaluating such a tile, one computes it
+ * and sends the other rank's side as a record. Sequence per rank:
+ *   fsgg_shard_bounds(ds, world, bounds)        block-aligned query ranges
+ *   fsgg_shard_root_prepare(ds, k, cfg, &n)   this shard's tiles, and n
+ *       records owed to other ranks
+ *   fsgg_shard_root_export(ds, dst)             copy them to a caller device
+ *       buffer: 260 32-bit words each (X, Y, first point of X, |X|, 256 fp32
+ *       values of X's points over partner block Y), for the rank whose range
+ *       holds point word[2]
+ *   (caller: all-to-all of the records)
+ *   fsgg_shard_root_receive(ds, recv, m)        store the m received records
+ *   fsgg_sample_shard(ds, k, cfg, ...)          the descent, root tiles reused
+ * Results are bit-identical to the 1-GPU build. prepare returns 0 records
+ * (and the descent computes its root alone) when the root pass is not
+ * symmetric for this data or the range is not block-aligned. Replaces no
+ * reference interface: the reference has no multi-device path
+ * (SURVEY.md §2). */
+int fsgg_shard_bounds(fsgg_dataset* ds, uint32_t world, uint32_t* bounds_host);
+int fsgg_shard_root_prepare(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                            const fsgg_config* cfg, uint64_t* num_records);
+int fsgg_shard_root_export(fsgg_dataset* ds, uint32_t* records_device);
+int fsgg_shard_root_receive(fsgg_dataset* ds, const uint32_t* records_device,
+                            uint64_t num_records);
 /* Phase 2 after the caller all-gathers g_full (n doubles, device) and the
  * shards' pair keys (concatenated, device, any order, duplicates allowed):
  * dedupe, weight, CSR and degrees exactly as the 1-GPU path. */

@@ -35,6 +35,7 @@ struct fsgg_dataset {
   std::unique_ptr<fsgg::SampleResult> shard;
   fsgg::DevBuf keys;
   fsgg::DevBuf shard_keys;
+  uint64_t root_records = 0;  // owner-mode root records of the last prepare
   uint64_t shard_npairs = 0;
   ~fsgg_dataset() {
     graph.reset();
@@ -801,6 +802,65 @@ int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_con
     out->self_pairs = bo.self;
     out->degenerate_draws = bo.degenerate;
     if (report) finish_report(report, ds, bo, nullptr, now() - t0);
+  });
+}
+
+int fsgg_shard_bounds(fsgg_dataset* h, uint32_t world, uint32_t* bounds) {
+  return guarded([&] {
+    activate(h);
+    if (world == 0 || !bounds) throw fsgg::ConfigError("invalid world size");
+    fsgg::Dataset& ds = h->ds;
+    if (!ds.tree_valid) fsgg::build_tree(ds);
+    fsgg::sym_shard_bounds(ds, world, bounds);
+  });
+}
+
+int fsgg_shard_root_prepare(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config* cfgp,
+                            uint64_t* num_records) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    if (!num_records) throw fsgg::ConfigError("null output");
+    *num_records = 0;
+    h->root_records = 0;
+    fsgg_config cfg = cfgp ? *cfgp : default_config();
+    fsgg::Dataset& ds = h->ds;
+    uint32_t qb = cfg.query_begin, qe = cfg.query_end;
+    if (qb == 0 && qe == 0) qe = ds.n;
+    if (qb > qe || qe > ds.n) throw fsgg::ConfigError("invalid query shard");
+    const char* e = std::getenv("FSGG_SYM");
+    if (cfg.dense_kde || (e && std::atoi(e) == 0)) return;  // no symmetric root
+    const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+    ds.tree_valid = false;  // the descent rebuilds it too (same table)
+    fsgg::build_tree(ds);
+    uint32_t n = 0;
+    const uint32_t* recs = nullptr;
+    fsgg::sym_shard_prepare(ds, ks, qb, qe, &n, &recs);
+    h->root_records = n;
+    *num_records = n;
+  });
+}
+
+int fsgg_shard_root_export(fsgg_dataset* h, uint32_t* records_device) {
+  return guarded([&] {
+    activate(h);
+    if (h->root_records == 0) return;
+    if (!records_device) throw fsgg::ConfigError("null records");
+    fsgg::Dataset& ds = h->ds;
+    FSGG_CUDA(cudaMemcpyAsync(records_device, ds.buf("sym.rec", 4).as<void>(),
+                              size_t(h->root_records) * fsgg::kSymRecordWords * 4,
+                              cudaMemcpyDeviceToDevice, ds.stream));
+    FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  });
+}
+
+int fsgg_shard_root_receive(fsgg_dataset* h, const uint32_t* records, uint64_t num_records) {
+  return guarded([&] {
+    activate(h);
+    if (num_records && !records) throw fsgg::ConfigError("null records");
+    if (num_records > 0xffffffffull) throw fsgg::ConfigError("too many records");
+    fsgg::sym_shard_receive(h->ds, records, uint32_t(num_records));
+    FSGG_CUDA(cudaStreamSynchronize(h->ds.stream));
   });
 }
 

@@ -163,6 +163,14 @@ struct KdeWorkspace {
   uint32_t sym_Lb = 0;
   uint32_t sym_b0 = 0;       // first query block of that pass
   bool sym_pos = false;      // "sym.pos" holds the partner-position table
+  // multi-GPU owner mode: tiles of shard [sym_ready_qb, sym_ready_qe)
+  // computed (and remote records received) ahead of the descent
+  bool sym_ready = false;
+  uint32_t sym_ready_qb = 0, sym_ready_qe = 0, sym_ready_b0 = 0, sym_ready_b1 = 0;
+  float sym_ready_scale = 0.f;
+  int sym_ready_family = -1;
+  double sym_ready_seconds = 0.0;     // device time of that tile kernel
+  double sym_prepared_seconds = 0.0;  // ... credited to the root level that used it
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ~KdeWorkspace();
 };
@@ -263,6 +271,18 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
 // Depth of the symmetric pass's blocks (0: the pass does not apply).
 uint32_t sym_block_depth(const Dataset& ds);
 constexpr uint32_t kSymRootServe = 7;  // symmetric root: fp64 rows serve levels 1..6
+// Multi-GPU owner mode of the symmetric root (shard bounds on block
+// boundaries): compute this shard's tiles, returning the records of values
+// owed to other ranks (device, kSymRecordWords 32-bit words each: X, Y,
+// first point of X, |X|, 256 values). false (no records) when the root is
+// not symmetric or the bounds are not block-aligned.
+constexpr uint32_t kSymRecordWords = 260;
+bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
+                       uint32_t* num_records, const uint32_t** records);
+// Store records received from other ranks (device) into this shard's values.
+void sym_shard_receive(Dataset& ds, const uint32_t* records, uint32_t num_records);
+// Block-aligned shard bounds (world + 1 entries) for owner mode.
+void sym_shard_bounds(Dataset& ds, uint32_t world, uint32_t* bounds);
 // Child sums of level `level` (1 <= level, level + 1 <= ws.sym_Lb) from the
 // symmetric root's per-(point, partner block) values: each child of a node
 // at this level is a run of whole blocks, so its sum for query q is the sum,

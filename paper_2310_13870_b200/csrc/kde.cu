@@ -949,6 +949,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   FSGG_CUDA(cudaStreamSynchronize(s));
   float ms = 0.f;
   FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
+  if (sym) ms += float(ws.sym_prepared_seconds * 1e3);  // tiles run ahead (owner mode)
   stats.tiled_seconds += ms * 1e-3;
   if (sym || (tc && lv.level == 0)) {  // the root launch: the dominant kernel
     stats.root_seconds += ms * 1e-3;

@@ -36,9 +36,15 @@ constexpr uint32_t kSymBlock = 256;  // max points per block
 constexpr int kSymRows = 8;          // rows per lane: 32 lanes x 8 = 256
 constexpr uint32_t kSymMinBlock = 192;
 
+// rec/remote: in a multi-GPU shard (owner mode) one side of a cross-shard
+// tile may belong to another rank; its values then go to exchange record
+// `rec` instead of P (remote bit 1: I's rows, bit 2: J's columns).
 struct SymTile {
-  uint32_t I, J, slotI, slotJ;
+  uint32_t I, J, slotI, slotJ, rec, remote;
 };
+// Exchange record: [X, Y, first point of X, |X|, 256 values of X's points
+// over partner block Y], 32-bit words.
+constexpr uint32_t kSymRecWords = kSymRecordWords;  // 4 + 256
 
 __device__ __forceinline__ float block_dist(const float* lo, const float* hi, uint32_t a,
                                             uint32_t b, uint32_t d, int family) {
@@ -111,12 +117,17 @@ __global__ void sym_fill_kernel(uint32_t B, const float* __restrict__ lo,
 }
 
 // Tiles (I <= J) that touch the query blocks [b0, b1].
+// Owner mode (multi-GPU, shard bounds on block boundaries): every tile is
+// computed by exactly one rank — a tile inside the shard by it, a cross tile
+// (I, J) by the owner of I when I + J is even, else by the owner of J — and
+// the other rank's side travels as an exchange record.
 __global__ void __launch_bounds__(128)
     sym_tiles_kernel(uint32_t B, const uint32_t* __restrict__ poff,
                      const uint32_t* __restrict__ plist, uint32_t b0, uint32_t b1,
                      const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
                      SymTile* __restrict__ tiles, uint32_t* __restrict__ ntiles,
-                     unsigned long long* __restrict__ performed) {
+                     unsigned long long* __restrict__ performed, int own,
+                     uint32_t* __restrict__ nrec, uint32_t* __restrict__ records) {
   __shared__ unsigned long long red[4];
   __shared__ uint32_t wcnt[4], cbase;
   const uint32_t I = blockIdx.x;
@@ -125,8 +136,11 @@ __global__ void __launch_bounds__(128)
   for (uint32_t k0 = poff[I]; k0 < poff[I + 1]; k0 += blockDim.x) {
     const uint32_t k = k0 + threadIdx.x;
     const uint32_t J = k < poff[I + 1] ? plist[k] : 0u;
+    const bool mineI = I >= b0 && I <= b1, mineJ = J >= b0 && J <= b1;
     const bool take = k < poff[I + 1] && J >= I &&
-                      ((I >= b0 && I <= b1) || (J >= b0 && J <= b1));
+                      (own ? (mineI && mineJ) || (mineI && ((I + J) & 1u) == 0u) ||
+                                 (mineJ && ((I + J) & 1u) == 1u)
+                           : mineI || mineJ);
     // one reservation per CTA chunk (a per-tile atomic on one counter
     // serialises ~1.7M times at C3)
     const unsigned m = __ballot_sync(0xffffffffu, take);
@@ -153,8 +167,19 @@ __global__ void __launch_bounds__(128)
         else
           hi = mid;
       }
+      uint32_t rec = 0, remote = 0;
+      if (own && !(mineI && mineJ)) {  // the other block's values are exported
+        remote = mineI ? 2u : 1u;
+        rec = atomicAdd(nrec, 1u);
+        const uint32_t X = mineI ? J : I, Y = mineI ? I : J;
+        uint32_t* hdr = records + size_t(rec) * kSymRecWords;
+        hdr[0] = X;
+        hdr[1] = Y;
+        hdr[2] = bf[X];
+        hdr[3] = bl[X] - bf[X];
+      }
       tiles[cbase + wcnt[w] + __popc(m & ((1u << lane) - 1u))] =
-          SymTile{I, J, k - poff[I], lo - poff[J]};
+          SymTile{I, J, k - poff[I], lo - poff[J], rec, remote};
     }
     __syncthreads();
   }
@@ -173,7 +198,7 @@ __global__ void __launch_bounds__(kSymThreads)
                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
                     const float* __restrict__ lo, const float* __restrict__ hi, float scale,
                     float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
-                    unsigned long long* __restrict__ performed) {
+                    unsigned long long* __restrict__ performed, float* __restrict__ records) {
   __shared__ __align__(16) float2 sx[kSymBlock * D];
   __shared__ float rowred[kSymWarps][kSymBlock];
   __shared__ float colv[kSymBlock];
@@ -255,7 +280,10 @@ __global__ void __launch_bounds__(kSymThreads)
     for (int k = 0; k < D; ++k) q[k] = __ldg(pts + size_t(fi + t) * D + k);
     const float off = scale * box_dist<FAM>(q, lo + size_t(tl.J) * D, hi + size_t(tl.J) * D, D);
     if (off > __log2f(float(nj)) + bits) v = 0.f;
-    P[(size_t(poff[tl.I]) + tl.slotI) * kSymBlock + t] = v;
+    if (tl.remote & 1u)
+      records[size_t(tl.rec) * kSymRecWords + 4 + t] = v;
+    else
+      P[(size_t(poff[tl.I]) + tl.slotI) * kSymBlock + t] = v;
   }
   if (tl.I != tl.J) {
     for (uint32_t t = threadIdx.x; t < nj; t += blockDim.x) {
@@ -265,7 +293,10 @@ __global__ void __launch_bounds__(kSymThreads)
       for (int k = 0; k < D; ++k) x[k] = __ldg(pts + size_t(fj + t) * D + k);
       const float off = scale * box_dist<FAM>(x, lo + size_t(tl.I) * D, hi + size_t(tl.I) * D, D);
       if (off > __log2f(float(ni)) + bits) v = 0.f;
-      P[(size_t(poff[tl.J]) + tl.slotJ) * kSymBlock + t] = v;
+      if (tl.remote & 2u)
+        records[size_t(tl.rec) * kSymRecWords + 4 + t] = v;
+      else
+        P[(size_t(poff[tl.J]) + tl.slotJ) * kSymBlock + t] = v;
     }
   }
 }
@@ -306,6 +337,24 @@ __global__ void __launch_bounds__(kSymBlock)
     }
     __syncthreads();
   }
+}
+
+// Received exchange records into P: X's slot for partner Y.
+__global__ void sym_receive_kernel(const uint32_t* __restrict__ records,
+                                   const uint32_t* __restrict__ poff,
+                                   const uint32_t* __restrict__ plist, float* __restrict__ P) {
+  const uint32_t* r = records + size_t(blockIdx.x) * kSymRecWords;
+  const uint32_t X = r[0], Y = r[1], nx = r[3];
+  uint32_t lo = poff[X], hi = poff[X + 1];
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (plist[mid] < Y)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  for (uint32_t t = threadIdx.x; t < nx; t += blockDim.x)
+    P[size_t(lo) * kSymBlock + t] = __uint_as_float(r[4 + t]);
 }
 
 // Block index of every point (blocks are the depth-Lb tree nodes).
@@ -466,12 +515,16 @@ uint32_t sym_block_depth(const Dataset& ds) {
   return Lb;
 }
 
-bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
-                        uint32_t rd, double* rows, unsigned long long* d_performed,
-                        cudaEvent_t ev0, cudaEvent_t ev1) {
+namespace {
+
+// Count / fill the partner lists, build the tile list of the query blocks
+// [b0, b1] and run the tile kernel. own: owner mode (multi-GPU exchange);
+// remote sides go to "sym.rec" records (*nrec of them).
+void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, bool own,
+                   unsigned long long* d_performed, cudaEvent_t ev0, cudaEvent_t ev1,
+                   uint32_t* b0_out, uint32_t* b1_out, uint32_t* nrec_out) {
   const TreeTable& t = ds.tree;
   const uint32_t Lb = sym_block_depth(ds);
-  if (Lb == 0 || Lb < rd) return false;
   cudaStream_t s = ds.stream;
   const uint32_t B = 1u << Lb;
   const uint64_t hb = uint64_t(B) - 1;
@@ -510,40 +563,130 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   FSGG_LAUNCH_CHECK();
   DevBuf& tiles = ds.buf("sym.tiles", size_t(npart) * sizeof(SymTile) + 16);
   DevBuf& ntiles = ds.buf("sym.ntiles", 8);
-  FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 4, s));
+  FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 8, s));
+  // a cross tile has one remote side: at most half the partner slots
+  DevBuf& rec = ds.buf("sym.rec", own ? (size_t(npart) / 2 + 1) * kSymRecWords * 4 : 4);
   sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1, bf,
                                      bl, tiles.as<SymTile>(), ntiles.as<uint32_t>(),
-                                     d_performed);
+                                     d_performed, own ? 1 : 0, ntiles.as<uint32_t>() + 1,
+                                     rec.as<uint32_t>());
   FSGG_LAUNCH_CHECK();
-  uint32_t nt = 0;
-  FSGG_CUDA(cudaMemcpyAsync(&nt, ntiles.as<void>(), 4, cudaMemcpyDeviceToHost, s));
+  uint32_t nt2[2] = {0, 0};
+  FSGG_CUDA(cudaMemcpyAsync(nt2, ntiles.as<void>(), 8, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
+  const uint32_t nt = nt2[0];
   DevBuf& P = ds.buf("sym.P", size_t(npart) * kSymBlock * 4 + 4);
   if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
   if (nt > 0) {
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
+      auto launch = [&](auto kern) {
+        kern<<<nt, kSymThreads, 0, s>>>(ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi,
+                                        ks.scale, bits, poff.as<uint32_t>(), P.as<float>(),
+                                        d_performed, rec.as<float>());
+      };
       switch (ks.family) {
-        case 0:
-          sym_tile_kernel<D, 0><<<nt, kSymThreads, 0, s>>>(
-              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
-              poff.as<uint32_t>(), P.as<float>(), d_performed);
-          break;
-        case 1:
-          sym_tile_kernel<D, 1><<<nt, kSymThreads, 0, s>>>(
-              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
-              poff.as<uint32_t>(), P.as<float>(), d_performed);
-          break;
-        default:
-          sym_tile_kernel<D, 2><<<nt, kSymThreads, 0, s>>>(
-              ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi, ks.scale, bits,
-              poff.as<uint32_t>(), P.as<float>(), d_performed);
-          break;
+        case 0: launch(sym_tile_kernel<D, 0>); break;
+        case 1: launch(sym_tile_kernel<D, 1>); break;
+        default: launch(sym_tile_kernel<D, 2>); break;
       }
     });
     FSGG_LAUNCH_CHECK();
   }
   if (ev1) FSGG_CUDA(cudaEventRecord(ev1, s));
+  ds.launches += 4;
+  *b0_out = b0;
+  *b1_out = b1;
+  *nrec_out = own ? nt2[1] : 0;
+}
+
+}  // namespace
+
+bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
+                       uint32_t* num_records, const uint32_t** records) {
+  *num_records = 0;
+  *records = nullptr;
+  if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
+  KdeWorkspace& ws = *ds.kde_ws;
+  ws.sym_ready = false;
+  const uint32_t Lb = sym_block_depth(ds);
+  if (Lb == 0 || qe <= qb) return false;
+  // owner mode needs block-aligned shard bounds (every block on one rank)
+  const TreeTable& t = ds.tree;
+  const uint64_t hb = (uint64_t(1) << Lb) - 1;
+  std::vector<uint32_t> hbf(size_t(1) << Lb);
+  FSGG_CUDA(cudaMemcpyAsync(hbf.data(), t.first.as<uint32_t>() + hb, hbf.size() * 4,
+                            cudaMemcpyDeviceToHost, ds.stream));
+  FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  const bool qb_ok = std::binary_search(hbf.begin(), hbf.end(), qb);
+  const bool qe_ok = qe == ds.n || std::binary_search(hbf.begin(), hbf.end(), qe);
+  if (!qb_ok || !qe_ok) return false;
+  if (!ws.ev0) {
+    FSGG_CUDA(cudaEventCreate(&ws.ev0));
+    FSGG_CUDA(cudaEventCreate(&ws.ev1));
+  }
+  DevBuf& perf = ds.buf("sym.perf", 8);
+  FSGG_CUDA(cudaMemsetAsync(perf.as<void>(), 0, 8, ds.stream));
+  uint32_t b0 = 0, b1 = 0, nrec = 0;
+  sym_tile_pass(ds, ks, qb, qe, true, perf.as<unsigned long long>(), ws.ev0, ws.ev1, &b0, &b1,
+                &nrec);
+  FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  float ms = 0.f;
+  FSGG_CUDA(cudaEventElapsedTime(&ms, ws.ev0, ws.ev1));
+  ws.sym_ready = true;
+  ws.sym_ready_qb = qb;
+  ws.sym_ready_qe = qe;
+  ws.sym_ready_scale = ks.scale;
+  ws.sym_ready_family = ks.family;
+  ws.sym_ready_b0 = b0;
+  ws.sym_ready_b1 = b1;
+  ws.sym_ready_seconds = ms * 1e-3;
+  *num_records = nrec;
+  *records = ds.buf("sym.rec", 4).as<uint32_t>();
+  return true;
+}
+
+void sym_shard_receive(Dataset& ds, const uint32_t* records, uint32_t num_records) {
+  if (!ds.kde_ws || !ds.kde_ws->sym_ready) throw ConfigError("no prepared symmetric root");
+  if (num_records == 0) return;
+  sym_receive_kernel<<<num_records, 256, 0, ds.stream>>>(
+      records, ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
+      ds.buf("sym.P", 4).as<float>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+}
+
+bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
+                        uint32_t rd, double* rows, unsigned long long* d_performed,
+                        cudaEvent_t ev0, cudaEvent_t ev1) {
+  const TreeTable& t = ds.tree;
+  const uint32_t Lb = sym_block_depth(ds);
+  if (Lb == 0 || Lb < rd) return false;
+  cudaStream_t s = ds.stream;
+  const uint32_t B = 1u << Lb;
+  const uint64_t hb = uint64_t(B) - 1;
+  const uint32_t* bf = t.first.as<uint32_t>() + hb;
+  const uint32_t* bl = t.last.as<uint32_t>() + hb;
+  KdeWorkspace& ws = *ds.kde_ws;
+  uint32_t b0 = 0, b1 = 0, nrec = 0;
+  ws.sym_prepared_seconds = 0.0;
+  if (ws.sym_ready && ws.sym_ready_qb == qb && ws.sym_ready_qe == qe &&
+      ws.sym_ready_scale == ks.scale && ws.sym_ready_family == ks.family) {
+    // tiles already computed by sym_shard_prepare (+ received records)
+    b0 = ws.sym_ready_b0;
+    b1 = ws.sym_ready_b1;
+    FSGG_CUDA(cudaMemcpyAsync(d_performed, ds.buf("sym.perf", 8).as<void>(), 8,
+                              cudaMemcpyDeviceToDevice, s));
+    if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
+    if (ev1) FSGG_CUDA(cudaEventRecord(ev1, s));
+    ws.sym_prepared_seconds = ws.sym_ready_seconds;
+  } else {
+    sym_tile_pass(ds, ks, qb, qe, false, d_performed, ev0, ev1, &b0, &b1, &nrec);
+  }
+  ws.sym_ready = false;
+  DevBuf& poff = ds.buf("sym.poff", 4);
+  DevBuf& plist = ds.buf("sym.plist", 4);
+  DevBuf& P = ds.buf("sym.P", 4);
   ds.kde_ws->sym_b0 = b0;
   ds.kde_ws->sym_pos = B <= kSymPosMaxBlocks && b0 <= b1;
   if (ds.kde_ws->sym_pos) {
@@ -562,9 +705,25 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
                                                      plist.as<uint32_t>(), bf, bl, b0,
                                                      Lb - rd, rd, qb, qe, rows);
     FSGG_LAUNCH_CHECK();
+    ds.launches++;
   }
-  ds.launches += 7;
   return true;
+}
+
+void sym_shard_bounds(Dataset& ds, uint32_t world, uint32_t* bounds) {
+  const uint32_t Lb = sym_block_depth(ds);
+  for (uint32_t r = 0; r <= world; ++r) bounds[r] = uint32_t(uint64_t(ds.n) * r / world);
+  if (Lb == 0) return;
+  const uint32_t B = 1u << Lb;
+  std::vector<uint32_t> hbf(B);
+  FSGG_CUDA(cudaMemcpyAsync(hbf.data(), ds.tree.first.as<uint32_t>() + (B - 1), size_t(B) * 4,
+                            cudaMemcpyDeviceToHost, ds.stream));
+  FSGG_CUDA(cudaStreamSynchronize(ds.stream));
+  // rank r starts at block round(r B / world): equal block counts
+  for (uint32_t r = 1; r < world; ++r)
+    bounds[r] = hbf[std::min<uint64_t>(B - 1, (uint64_t(B) * r + world / 2) / world)];
+  bounds[0] = 0;
+  bounds[world] = ds.n;
 }
 
 void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,

@@ -19,6 +19,14 @@ at the end, all over NCCL:
      north star's "final edge-list all-gather"), concatenated in rank order
      = the global (u, v) order.
 The graph finish is thus split N ways instead of repeated on every rank.
+
+With the symmetric root pass (low d) there is one exchange before the
+descent: shard bounds sit on the root's block boundaries
+(fsgg_shard_bounds), every block-pair tile is evaluated by exactly one rank,
+and the other rank's side (256 fp32 values per tile) is sent to it as a
+record with one all-to-all (exchange_root) — the root's n^2 work is split
+N ways instead of each rank also evaluating the tiles it shares with its
+neighbours.
 The exchange helpers are device-agnostic so the CPU suite exercises them
 with ``gloo``.
 """
@@ -41,6 +49,69 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 
 def shard_bounds(n: int, world: int) -> list[int]:
     return [shard_range(n, r, world)[0] for r in range(world)] + [n]
+
+
+def block_shard_bounds(ds: Dataset, world: int) -> list[int]:
+    """Query bounds on the symmetric root's block boundaries (plain
+    shard_bounds when the root pass is not symmetric for this data)."""
+    b = (C.c_uint32 * (world + 1))()
+    N.check(N.lib().fsgg_shard_bounds(ds._h, world, b))
+    return [int(x) for x in b]
+
+
+RECORD_WORDS = 260  # X, Y, first point of X, |X|, 256 values (include/fsgg.h)
+
+
+def record_destinations(records: torch.Tensor, bounds: list[int]) -> torch.Tensor:
+    """Rank owning each record's block (word 2 = the block's first point)."""
+    first = records[:, 2].to(torch.int64)
+    b = torch.tensor(bounds[1:-1], dtype=torch.int64, device=records.device)
+    return torch.searchsorted(b, first, right=True)
+
+
+def route_records(records: torch.Tensor, bounds: list[int], group=None) -> torch.Tensor:
+    """All-to-all of exchange records (int32 [m, RECORD_WORDS]) to the ranks
+    owning their blocks; returns the records this rank received."""
+    world = dist.get_world_size(group)
+    dest = record_destinations(records, bounds)
+    order = torch.argsort(dest, stable=True)
+    counts = torch.bincount(dest, minlength=world).tolist()
+    flat = records.index_select(0, order).reshape(-1)
+    recv = alltoall_varlen(flat, [c * RECORD_WORDS for c in counts], group)
+    return recv.reshape(-1, RECORD_WORDS)
+
+
+def prepare_root(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig) -> torch.Tensor:
+    """fsgg_shard_root_prepare: this shard's root tiles; returns the records
+    owed to other ranks (a device copy, int32 [m, RECORD_WORDS])."""
+    k = kernel._c()
+    c = cfg._c()
+    n = C.c_uint64(0)
+    N.check(N.lib().fsgg_shard_root_prepare(ds._h, C.byref(k), C.byref(c), C.byref(n)))
+    dev = torch.device("cuda", ds.device)
+    m = int(n.value)
+    out = torch.empty((m, RECORD_WORDS), dtype=torch.int32, device=dev)
+    if m:
+        N.check(N.lib().fsgg_shard_root_export(ds._h, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def receive_root(ds: Dataset, records: torch.Tensor):
+    torch.cuda.synchronize(ds.device)  # the all-to-all ran on torch's stream
+    N.check(N.lib().fsgg_shard_root_receive(
+        ds._h, C.c_void_p(records.data_ptr() if records.numel() else 0), records.shape[0]))
+
+
+def exchange_root(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig, bounds: list[int],
+                  group=None) -> int:
+    """Owner-mode symmetric root for this rank's shard (cfg.query_begin/end
+    must be its entry of `bounds`): compute, exchange, store. Returns the
+    bytes this rank sent."""
+    recs = prepare_root(ds, kernel, cfg)
+    # every rank joins the collective, also with nothing to send
+    recv = route_records(recs, bounds, group)
+    receive_root(ds, recv)
+    return recs.numel() * 4
 
 
 def allgather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
@@ -156,9 +227,11 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
     cfg = config or SparsifierConfig()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = ds.n
-    qb, qe = shard_range(n, rank, world)
-    bounds = shard_bounds(n, world)
-    sh, srep, pairs, g = sample_shard(ds, kernel, replace(cfg, query_begin=qb, query_end=qe))
+    bounds = block_shard_bounds(ds, world)
+    qb, qe = bounds[rank], bounds[rank + 1]
+    shard_cfg = replace(cfg, query_begin=qb, query_end=qe)
+    root_bytes = exchange_root(ds, kernel, shard_cfg, bounds, group)
+    sh, srep, pairs, g = sample_shard(ds, kernel, shard_cfg)
     g_full = allgather_varlen(g, group)
     rows, deg, frep, moved = finish_rows(ds, kernel, int(sh.rounds), g_full, pairs, qb, qe,
                                          bounds, group)
@@ -173,7 +246,8 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
     frep.gpu_launches += srep.gpu_launches
     res = DistributedResult(row_begin=qb, row_end=qe, u=rows["u"], v=rows["v"], w=rows["w"],
                             degrees=deg, report=frep, shard_report=srep,
-                            exchange_bytes=g_full.numel() * 8 + moved, gathered=False)
+                            exchange_bytes=g_full.numel() * 8 + moved + root_bytes,
+                            gathered=False)
     if gather:
         res.u = allgather_varlen(rows["u"], group)
         res.v = allgather_varlen(rows["v"], group)

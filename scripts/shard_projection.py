@@ -2,7 +2,8 @@
 
 The descent has no collective (parallel.py), so what rank r of N does is a
 function of its query range alone: this script runs each rank's shard
-descent (fsgg_sample_shard) and its row-sharded finish (fsgg_finish_graph on
+descent (owner-mode root: fsgg_shard_root_prepare + the records the other
+ranks owe it + fsgg_sample_shard) and its row-sharded finish (fsgg_finish_graph on
 the keys routed to it + fsgg_rows_transposed + fsgg_rows_degrees) one after
 another on one GPU, times each with a device sync on both sides (best of
 `--reps`), and reports max over ranks per phase. The NCCL exchanges are not
@@ -49,6 +50,8 @@ def main():
     ap.add_argument("--worlds", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default="")
+    ap.add_argument("--no-owner", action="store_true",
+                    help="plain query shards (each rank evaluates every root tile it touches)")
     a = ap.parse_args()
     p, _ = datasets.make_moons(a.n, 0.05, 1)
     p = p.astype(np.float32)
@@ -63,16 +66,50 @@ def main():
     result = {"n": a.n, "sigma": a.sigma, "L": L, "one_gpu_build_s": full_t, "worlds": {}}
     print(f"1-GPU build {full_t * 1e3:.1f} ms", flush=True)
     for world in [int(x) for x in a.worlds.split(",")]:
-        bounds = parallel.shard_bounds(a.n, world)
-        sample_s, root_s, pairs, gs = [], [], [], []
-        for r in range(world):
-            cfg = F.SparsifierConfig(rounds=L, seed=1, query_begin=bounds[r],
-                                     query_end=bounds[r + 1])
-            t, (sh, rep, pr, g) = timed(lambda: parallel.sample_shard(ds, k, cfg), a.reps)
-            sample_s.append(t)
-            root_s.append(rep.kde_root_seconds)
-            pairs.append(pr)
-            gs.append(g)
+        # owner mode (default): block-aligned bounds, each root tile on one
+        # rank, one handle per rank (their root values must coexist for the
+        # emulated record exchange)
+        if a.no_owner:
+            bounds = parallel.shard_bounds(a.n, world)
+            handles = [ds] * world
+        else:
+            bounds = parallel.block_shard_bounds(ds, world)
+            handles = [ds] + [F.Dataset(p) for _ in range(world - 1)]
+        cfgs = [F.SparsifierConfig(rounds=L, seed=1, query_begin=bounds[r],
+                                   query_end=bounds[r + 1]) for r in range(world)]
+        sample_s, root_s, pairs, gs, prep_s, recv_s, rec_bytes = [], [], [], [], [], [], []
+        for rep_i in range(a.reps):
+            recs = []
+            for r in range(world):
+                if a.no_owner:
+                    prep_s.append(0.0)
+                    recs.append(None)
+                    continue
+                t, x = timed(lambda: parallel.prepare_root(handles[r], k, cfgs[r]), 1)
+                prep_s.append(t)
+                recs.append(x)
+            for d in range(world):
+                if a.no_owner:
+                    recv_s.append(0.0)
+                    rec_bytes.append(0)
+                    continue
+                inbox = torch.cat([x[parallel.record_destinations(x, bounds) == d] for x in recs])
+                rec_bytes.append(int(inbox.numel()) * 4)
+                t, _ = timed(lambda: parallel.receive_root(handles[d], inbox), 1)
+                recv_s.append(t)
+            for r in range(world):
+                t, (sh, rep, pr, g) = timed(lambda: parallel.sample_shard(handles[r], k, cfgs[r]),
+                                            1)
+                if rep_i == 0:
+                    sample_s.append(t)
+                    root_s.append(rep.kde_root_seconds)
+                    pairs.append(pr)
+                    gs.append(g)
+                else:
+                    sample_s[r] = min(sample_s[r], t)
+        prep_s = [min(prep_s[r::world]) for r in range(world)]
+        recv_s = [min(recv_s[r::world]) for r in range(world)]
+        sample_s = [sample_s[r] + prep_s[r] + recv_s[r] for r in range(world)]
         g_full = torch.cat(gs)
         routed = [[] for _ in range(world)]
         for t in pairs:
@@ -110,6 +147,7 @@ def main():
                 C.c_void_p(lw.data_ptr() if lw.numel() else 0), lv.numel(), bounds[d],
                 bounds[d + 1], C.c_void_p(deg.data_ptr()))), a.reps)
             deg_s.append(t)
+        ds = handles[0]
         key_bytes = [sum(x.numel() for i, x in enumerate(
             torch.split(pairs[s], parallel.owner_splits(pairs[s] >> 32, bounds))) if i != s) * 8
             for s in range(world)]
@@ -120,7 +158,10 @@ def main():
             "max_sample_s": max(sample_s), "max_finish_s": max(finish_s),
             "max_degrees_s": max(deg_s),
             "max_rank_compute_s": max(max(sample_s), 0) + max(finish_s) + max(deg_s),
-            "exchange_bytes_per_rank_max": max(key_bytes) + max(lower_bytes) + 8 * a.n,
+            "root_prepare_s": prep_s, "root_receive_s": recv_s,
+            "root_record_bytes_received": rec_bytes[:world],
+            "exchange_bytes_per_rank_max": max(key_bytes) + max(lower_bytes) + 8 * a.n
+            + max(rec_bytes[:world] or [0]),
             "projected_speedup_compute_only": full_t / (max(sample_s) + max(finish_s)
                                                         + max(deg_s)),
         }

@@ -313,6 +313,45 @@ def test_sharded_build_is_bit_identical(oracle, n):
         assert np.array_equal(g.w, full.w) and np.array_equal(g.degrees, full.degrees)
 
 
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_owner_mode_root_is_bit_identical(world):
+    """Multi-GPU symmetric root in owner mode (one handle per emulated rank on
+    one GPU): block-aligned bounds, every block-pair tile evaluated by one
+    rank only (the ranks' root evaluations add up to the 1-GPU count), the
+    other side's values routed as records — the merged graph equals the
+    1-GPU graph bit for bit."""
+    import torch
+    from paper_2310_13870_b200 import parallel
+    n = 60000
+    p, _ = datasets.make_moons(n, 0.05, 2)
+    k = F.Kernel(G, 0.06)
+    cfg = F.SparsifierConfig(rounds=16, seed=3)
+    ds0 = F.Dataset(p)
+    full, rep, _ = F.build_similarity_graph(ds0, k, cfg, report=True)
+    assert rep.kde_root_performed_evals > 0
+    handles = [F.Dataset(p) for _ in range(world)]
+    bounds = parallel.block_shard_bounds(handles[0], world)
+    assert bounds[0] == 0 and bounds[-1] == n
+    cfgs = [F.SparsifierConfig(rounds=16, seed=3, query_begin=bounds[r], query_end=bounds[r + 1])
+            for r in range(world)]
+    recs = [parallel.prepare_root(handles[r], k, cfgs[r]) for r in range(world)]
+    assert sum(int(x.shape[0]) for x in recs) > 0
+    for d in range(world):
+        inbox = [x[parallel.record_destinations(x, bounds) == d] for x in recs]
+        parallel.receive_root(handles[d], torch.cat(inbox))
+    pairs, gs, performed = [], [], 0
+    for r in range(world):
+        sh, srep, pr, g = parallel.sample_shard(handles[r], k, cfgs[r])
+        pairs.append(pr)
+        gs.append(g)
+        performed += srep.kde_root_performed_evals
+    assert performed == rep.kde_root_performed_evals
+    parallel.finish_graph(ds0, k, 16, torch.cat(gs), torch.cat(pairs))
+    g = F.api.device_graph_to_host(ds0)
+    assert np.array_equal(g.u, full.u) and np.array_equal(g.v, full.v)
+    assert np.array_equal(g.w, full.w) and np.array_equal(g.degrees, full.degrees)
+
+
 @pytest.mark.parametrize("n,world", [(3000, 2), (3500, 3), (14000, 5)])
 def test_row_sharded_finish_is_bit_identical(n, world):
     """The multi-GPU finish split by rows (parallel.finish_rows' exchanges

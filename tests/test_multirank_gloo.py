@@ -130,3 +130,43 @@ def test_row_routing_matches_single_process(tmp_path, world):
         qb, qe = shard_range(301, r, world)
         lower = np.load(tmp_path / f"lower{r}.npy")
         assert np.array_equal(np.sort(lower), np.sort(v[(v >= qb) & (v < qe)]))
+
+
+def _record_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2310_13870_b200.parallel import RECORD_WORDS, route_records
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bounds = [0, 1000, 2500, 4000][: world] + [4000]
+    rng = np.random.default_rng(rank)
+    m = 50 + 10 * rank
+    recs = np.zeros((m, RECORD_WORDS), dtype=np.int32)
+    recs[:, 0] = rng.integers(0, 64, m)             # block X
+    recs[:, 1] = rank                                # sender tag (stands for Y)
+    recs[:, 2] = rng.integers(0, bounds[-1], m)      # first point of X
+    recs[:, 3] = 7
+    recs[:, 4:] = rng.integers(0, 1 << 30, (m, RECORD_WORDS - 4))
+    np.save(os.path.join(out_dir, f"sent{rank}.npy"), recs)
+    got = route_records(torch.from_numpy(recs), bounds).numpy()
+    np.save(os.path.join(out_dir, f"got{rank}.npy"), got)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_root_record_routing(tmp_path, world):
+    """Owner-mode symmetric root (parallel.route_records): every record
+    reaches the rank whose query range holds its block's first point, intact,
+    with sender order preserved."""
+    mp.spawn(_record_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+             join=True)
+    bounds = [0, 1000, 2500, 4000][: world] + [4000]
+    sent = [np.load(tmp_path / f"sent{r}.npy") for r in range(world)]
+    for d in range(world):
+        got = np.load(tmp_path / f"got{d}.npy")
+        expect = np.concatenate([s[(s[:, 2] >= bounds[d]) & (s[:, 2] < bounds[d + 1])]
+                                 for s in sent])
+        assert np.array_equal(got, expect)
