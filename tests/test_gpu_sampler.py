@@ -565,3 +565,32 @@ def test_pinned_csr_readback_matches_full_copy():
     for k in ("v", "w", "row_ptr", "degrees"):
         assert np.array_equal(getattr(g, k), getattr(full, k))
     assert np.array_equal(g.u, full.u) and g.num_edges() == full.num_edges()
+
+
+def test_distributed_build_over_nccl_world1():
+    """parallel.build_similarity_graph_distributed end to end over a real NCCL
+    process group (world size 1 on this one-GPU box: every collective of the
+    multi-GPU path runs, owner-mode root included) equals the 1-GPU build."""
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2310_13870_b200 import parallel
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p, _ = datasets.make_moons(60000, 0.05, 2)
+        ds = F.Dataset(p)
+        k = F.Kernel(G, 0.06)
+        cfg = F.SparsifierConfig(rounds=16, seed=3)
+        full = F.build_similarity_graph(ds, k, cfg)
+        res = parallel.build_similarity_graph_distributed(ds, k, cfg)
+        assert np.array_equal(res.u.cpu().numpy(), full.u)
+        assert np.array_equal(res.v.cpu().numpy(), full.v)
+        assert np.array_equal(res.w.cpu().numpy(), full.w)
+        assert np.array_equal(res.degrees.cpu().numpy(), full.degrees)
+    finally:
+        dist.destroy_process_group()
