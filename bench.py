@@ -365,7 +365,10 @@ def main():
     prof = os.path.join(ROOT, "profiles", "kde_sym_ncu.json" if root_s > 0 else "kde_tiled_ncu.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            cap = json.load(open(prof))
+            # only a capture of this workload's launch says anything about it
+            if str(cap.get("config", "")).startswith(args.config):
+                traffic = cap.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
     tensor = w.d >= TC_MIN_DIM
@@ -388,10 +391,12 @@ def main():
         prof = os.path.join(ROOT, "profiles", "kde_tc_ncu.json")
         if os.path.exists(prof):
             try:
-                l0 = json.load(open(prof))["launches"][0]
+                cap = json.load(open(prof))
+                l0 = cap["launches"][0]
                 mul = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}
-                traffic = sum(float(l0[k][0]) * mul.get(l0[k][1], 1.0)
-                              for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+                if str(cap.get("config", "")).startswith(args.config):
+                    traffic = sum(float(l0[k][0]) * mul.get(l0[k][1], 1.0)
+                                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             except (OSError, ValueError, KeyError, IndexError):
                 traffic = None
         roofline = {

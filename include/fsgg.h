@@ -362,9 +362,9 @@ int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
  *   fsgg_shard_root_prepare(ds, k, cfg, &n)   this shard's tiles, and n
  *       records owed to other ranks
  *   fsgg_shard_root_export(ds, dst)             copy them to a caller device
- *       buffer: 260 32-bit words each (X, Y, first point of X, |X|, 256 fp32
- *       values of X's points over partner block Y), for the rank whose range
- *       holds point word[2]
+ *       buffer: 324 32-bit words each (X, Y, first point of X, |X|, then
+ *       |X| <= 320 fp32 values of X's points over partner block Y), for the
+ *       rank whose range holds point word[2]
  *   (caller: all-to-all of the records)
  *   fsgg_shard_root_receive(ds, recv, m)        store the m received records
  *   fsgg_sample_shard(ds, k, cfg, ...)          the descent, root tiles reused

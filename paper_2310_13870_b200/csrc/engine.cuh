@@ -274,9 +274,10 @@ constexpr uint32_t kSymRootServe = 7;  // symmetric root: fp64 rows serve levels
 // Multi-GPU owner mode of the symmetric root (shard bounds on block
 // boundaries): compute this shard's tiles, returning the records of values
 // owed to other ranks (device, kSymRecordWords 32-bit words each: X, Y,
-// first point of X, |X|, 256 values). false (no records) when the root is
+// first point of X, |X|, kSymStride values). false (no records) when the root is
 // not symmetric or the bounds are not block-aligned.
-constexpr uint32_t kSymRecordWords = 260;
+constexpr uint32_t kSymStride = 320;  // values per (block, partner) slot: max block size
+constexpr uint32_t kSymRecordWords = 4 + kSymStride;
 bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe,
                        uint32_t* num_records, const uint32_t** records);
 // Store records received from other ranks (device) into this shard's values.

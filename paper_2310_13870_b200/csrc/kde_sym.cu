@@ -30,10 +30,12 @@
 namespace fsgg {
 namespace {
 
-constexpr int kSymThreads = 128;  // 4 warps
-constexpr int kSymWarps = kSymThreads / 32;
-constexpr uint32_t kSymBlock = 256;  // max points per block
-constexpr int kSymRows = 8;          // rows per lane: 32 lanes x 8 = 256
+// A tile holds up to 32 * ROWS rows in registers (ROWS per lane, 8 or 10)
+// and as many sources (ROWS / 2 warps x 64). Blocks of <= 256 points take
+// ROWS = 8, blocks of 257..320 points ROWS = 10 (C4: 302-point blocks at 94%
+// lane use, where 256-capacity tiles of its 151-point blocks left 65% of the
+// lanes on padding). P rows and records have the 320-value stride.
+constexpr uint32_t kSymBlock = kSymStride;  // max points per block (320)
 constexpr uint32_t kSymMinBlock = 192;
 
 // rec/remote: in a multi-GPU shard (owner mode) one side of a cross-shard
@@ -44,7 +46,7 @@ struct SymTile {
 };
 // Exchange record: [X, Y, first point of X, |X|, 256 values of X's points
 // over partner block Y], 32-bit words.
-constexpr uint32_t kSymRecWords = kSymRecordWords;  // 4 + 256
+constexpr uint32_t kSymRecWords = kSymRecordWords;  // 4 + kSymStride
 
 __device__ __forceinline__ float block_dist(const float* lo, const float* hi, uint32_t a,
                                             uint32_t b, uint32_t d, int family) {
@@ -192,22 +194,25 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-template <int D, int FAM>
-__global__ void __launch_bounds__(kSymThreads)
+template <int D, int FAM, int ROWS, bool OWN>
+__global__ void __launch_bounds__(ROWS * 16)
     sym_tile_kernel(const float* __restrict__ pts, const SymTile* __restrict__ tiles,
                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
                     const float* __restrict__ lo, const float* __restrict__ hi, float scale,
                     float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
                     unsigned long long* __restrict__ performed, float* __restrict__ records) {
-  __shared__ __align__(16) float2 sx[kSymBlock * D];
-  __shared__ float rowred[kSymWarps][kSymBlock];
-  __shared__ float colv[kSymBlock];
+  constexpr int kSymRows = ROWS;
+  constexpr int kSymWarps = ROWS / 2;
+  constexpr uint32_t kCap = 32u * ROWS;
+  __shared__ __align__(16) float2 sx[kCap * D];
+  __shared__ float rowred[kSymWarps][kCap];
+  __shared__ float colv[kCap];
   const SymTile tl = tiles[blockIdx.x];
   const uint32_t fi = bf[tl.I], ni = bl[tl.I] - fi;
   const uint32_t fj = bf[tl.J], nj = bl[tl.J] - fj;
   // sources of J, negated and duplicated; slots past nj sit far away (their
   // terms underflow to 0), so the unrolled source loop needs no guard
-  for (uint32_t idx = threadIdx.x; idx < kSymBlock * D; idx += blockDim.x) {
+  for (uint32_t idx = threadIdx.x; idx < kCap * D; idx += blockDim.x) {
     const float v = idx < nj * D ? -__ldg(pts + size_t(fj) * D + idx) : -1e18f;
     sx[idx] = make_float2(v, v);
   }
@@ -269,6 +274,14 @@ __global__ void __launch_bounds__(kSymThreads)
     rowred[w][lane * kSymRows + 2 * p + 1] = racc[p].y;
   }
   __syncthreads();
+  // destinations: this shard's P slots, or an exchange record (owner mode;
+  // a separate instantiation: the single-GPU kernel keeps its 80 registers)
+  float* rdst = P + (size_t(poff[tl.I]) + tl.slotI) * kCap;
+  float* cdst = P + (size_t(poff[tl.J]) + tl.slotJ) * kCap;
+  if constexpr (OWN) {
+    if (tl.remote & 1u) rdst = records + size_t(tl.rec) * kSymRecWords + 4;
+    if (tl.remote & 2u) cdst = records + size_t(tl.rec) * kSymRecWords + 4;
+  }
   // rows of I over J, columns of J over I (the diagonal tile has rows only);
   // a point that prunes the partner block drops its value
   for (uint32_t t = threadIdx.x; t < ni; t += blockDim.x) {
@@ -280,10 +293,7 @@ __global__ void __launch_bounds__(kSymThreads)
     for (int k = 0; k < D; ++k) q[k] = __ldg(pts + size_t(fi + t) * D + k);
     const float off = scale * box_dist<FAM>(q, lo + size_t(tl.J) * D, hi + size_t(tl.J) * D, D);
     if (off > __log2f(float(nj)) + bits) v = 0.f;
-    if (tl.remote & 1u)
-      records[size_t(tl.rec) * kSymRecWords + 4 + t] = v;
-    else
-      P[(size_t(poff[tl.I]) + tl.slotI) * kSymBlock + t] = v;
+    rdst[t] = v;
   }
   if (tl.I != tl.J) {
     for (uint32_t t = threadIdx.x; t < nj; t += blockDim.x) {
@@ -293,10 +303,7 @@ __global__ void __launch_bounds__(kSymThreads)
       for (int k = 0; k < D; ++k) x[k] = __ldg(pts + size_t(fj + t) * D + k);
       const float off = scale * box_dist<FAM>(x, lo + size_t(tl.I) * D, hi + size_t(tl.I) * D, D);
       if (off > __log2f(float(ni)) + bits) v = 0.f;
-      if (tl.remote & 2u)
-        records[size_t(tl.rec) * kSymRecWords + 4 + t] = v;
-      else
-        P[(size_t(poff[tl.J]) + tl.slotJ) * kSymBlock + t] = v;
+      cdst[t] = v;
     }
   }
 }
@@ -308,7 +315,8 @@ __global__ void __launch_bounds__(kSymBlock)
     sym_rows_kernel(const float* __restrict__ P, const uint32_t* __restrict__ poff,
                     const uint32_t* __restrict__ plist, const uint32_t* __restrict__ bf,
                     const uint32_t* __restrict__ bl, uint32_t blk0, uint32_t shift,
-                    uint32_t rd, uint32_t qb, uint32_t qe, double* __restrict__ rows) {
+                    uint32_t rd, uint32_t qb, uint32_t qe, double* __restrict__ rows,
+                    uint32_t ps) {
   // acc[c][t]: point t's sum for bucket b0 + c (row stride 257: conflict-free
   // when the store pass below reads it column-wise)
   __shared__ double acc[kSymBucketChunk][kSymBlock + 1];
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(kSymBlock)
     for (uint32_t c = 0; c < kSymBucketChunk; ++c) acc[c][t] = 0.0;
     for (; k < p1 && (plist[k] >> shift) < b0 + kSymBucketChunk; ++k) {
       const uint32_t c = (plist[k] >> shift) - b0;
-      if (t < ni) acc[c][t] += double(P[size_t(k) * kSymBlock + t]);
+      if (t < ni) acc[c][t] += double(P[size_t(k) * ps + t]);
     }
     __syncthreads();
     // coalesced store: consecutive threads write consecutive buckets of a point
@@ -342,7 +350,8 @@ __global__ void __launch_bounds__(kSymBlock)
 // Received exchange records into P: X's slot for partner Y.
 __global__ void sym_receive_kernel(const uint32_t* __restrict__ records,
                                    const uint32_t* __restrict__ poff,
-                                   const uint32_t* __restrict__ plist, float* __restrict__ P) {
+                                   const uint32_t* __restrict__ plist, float* __restrict__ P,
+                                   uint32_t ps) {
   const uint32_t* r = records + size_t(blockIdx.x) * kSymRecWords;
   const uint32_t X = r[0], Y = r[1], nx = r[3];
   uint32_t lo = poff[X], hi = poff[X + 1];
@@ -354,7 +363,7 @@ __global__ void sym_receive_kernel(const uint32_t* __restrict__ records,
       hi = mid;
   }
   for (uint32_t t = threadIdx.x; t < nx; t += blockDim.x)
-    P[size_t(lo) * kSymBlock + t] = __uint_as_float(r[4 + t]);
+    P[size_t(lo) * ps + t] = __uint_as_float(r[4 + t]);
 }
 
 // Block index of every point (blocks are the depth-Lb tree nodes).
@@ -398,7 +407,7 @@ __global__ void __launch_bounds__(kBlkThreads)
                         const uint32_t* __restrict__ poff, const uint32_t* __restrict__ plist,
                         const float* __restrict__ P, const uint32_t* __restrict__ tfirst,
                         const uint32_t* __restrict__ tlast, const uint32_t* __restrict__ pos,
-                        uint32_t b0, double* __restrict__ g1,
+                        uint32_t b0, uint32_t ps, double* __restrict__ g1,
                         double* __restrict__ g2, unsigned long long* __restrict__ evals) {
   constexpr int U = kBlkUnroll;
   const uint32_t base = blockIdx.x * (kBlkThreads * U) + threadIdx.x;
@@ -437,8 +446,8 @@ __global__ void __launch_bounds__(kBlkThreads)
     for (int u = 0; u < U; ++u) {
       a[u] = b[u] = 0.0;
       const float* pv = P + (q[u] - bf[I[u]]);
-      for (uint32_t kk = k[u]; kk < km[u]; ++kk) a[u] += double(__ldg(pv + size_t(kk) * 256));
-      for (uint32_t kk = km[u]; kk < k1[u]; ++kk) b[u] += double(__ldg(pv + size_t(kk) * 256));
+      for (uint32_t kk = k[u]; kk < km[u]; ++kk) a[u] += double(__ldg(pv + size_t(kk) * ps));
+      for (uint32_t kk = km[u]; kk < k1[u]; ++kk) b[u] += double(__ldg(pv + size_t(kk) * ps));
     }
   } else
 #pragma unroll
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kBlkThreads)
     for (uint32_t kk = lo; kk < k1[u]; ++kk) {
       const uint32_t J = __ldg(plist + kk);
       if (J >= B1) break;
-      const double v = double(__ldg(P + size_t(kk) * 256 + t));
+      const double v = double(__ldg(P + size_t(kk) * ps + t));
       if (J < Bm)
         a[u] += v;
       else
@@ -505,15 +514,24 @@ void sym_by_dim(uint32_t d, F&& f) {
 uint32_t sym_block_depth(const Dataset& ds) {
   const TreeTable& t = ds.tree;
   if (ds.d < 1 || ds.d > 8 || !t.has_boxes) return 0;
-  // blocks: tree nodes at depth Lb with <= 256 points
+  // blocks: tree nodes at depth Lb with <= 320 points (<= 256 for d > 6:
+  // 10-row lanes would spill)
+  const uint32_t cap = ds.d <= 6 ? kSymBlock : 256u;
   uint32_t Lb = 0;
-  while (((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > kSymBlock) ++Lb;
+  while (((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > cap) ++Lb;
   if (Lb == 0 || Lb > t.depth || Lb > 20) return 0;
-  // tiles are 256 x 256 in registers: smaller blocks leave lanes idle (C4's
-  // 151-point blocks measured slower than the one-sided tiled kernel)
+  // tiles hold 256 (or 320) rows in registers: smaller blocks leave lanes
+  // idle (151-point blocks measured slower than the one-sided tiled kernel)
   if ((uint64_t(ds.n) >> Lb) < kSymMinBlock) return 0;
   return Lb;
 }
+
+// Rows per lane of the tile kernel for this dataset's blocks.
+int sym_rows_per_lane(const Dataset& ds, uint32_t Lb) {
+  return ((uint64_t(ds.n) + (1ull << Lb) - 1) >> Lb) > 256 ? 10 : 8;
+}
+// Values per (block, partner) slot of P: the tile capacity.
+uint32_t sym_pstride(const Dataset& ds, uint32_t Lb) { return 32u * sym_rows_per_lane(ds, Lb); }
 
 namespace {
 
@@ -575,20 +593,31 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   FSGG_CUDA(cudaMemcpyAsync(nt2, ntiles.as<void>(), 8, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
   const uint32_t nt = nt2[0];
-  DevBuf& P = ds.buf("sym.P", size_t(npart) * kSymBlock * 4 + 4);
+  DevBuf& P = ds.buf("sym.P", size_t(npart) * sym_pstride(ds, Lb) * 4 + 4);
   if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
   if (nt > 0) {
+    const int rows = sym_rows_per_lane(ds, Lb);
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
-      auto launch = [&](auto kern) {
-        kern<<<nt, kSymThreads, 0, s>>>(ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi,
-                                        ks.scale, bits, poff.as<uint32_t>(), P.as<float>(),
-                                        d_performed, rec.as<float>());
+      auto launch = [&](auto kern, int threads) {
+        kern<<<nt, threads, 0, s>>>(ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi,
+                                    ks.scale, bits, poff.as<uint32_t>(), P.as<float>(),
+                                    d_performed, rec.as<float>());
+      };
+      auto by_rows = [&](auto fam) {
+        constexpr int FAM = decltype(fam)::value;
+        if constexpr (D <= 6) {
+          if (rows == 10)
+            return own ? launch(sym_tile_kernel<D, FAM, 10, true>, 160)
+                       : launch(sym_tile_kernel<D, FAM, 10, false>, 160);
+        }
+        own ? launch(sym_tile_kernel<D, FAM, 8, true>, 128)
+            : launch(sym_tile_kernel<D, FAM, 8, false>, 128);
       };
       switch (ks.family) {
-        case 0: launch(sym_tile_kernel<D, 0>); break;
-        case 1: launch(sym_tile_kernel<D, 1>); break;
-        default: launch(sym_tile_kernel<D, 2>); break;
+        case 0: by_rows(std::integral_constant<int, 0>{}); break;
+        case 1: by_rows(std::integral_constant<int, 1>{}); break;
+        default: by_rows(std::integral_constant<int, 2>{}); break;
       }
     });
     FSGG_LAUNCH_CHECK();
@@ -651,7 +680,7 @@ void sym_shard_receive(Dataset& ds, const uint32_t* records, uint32_t num_record
   if (num_records == 0) return;
   sym_receive_kernel<<<num_records, 256, 0, ds.stream>>>(
       records, ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
-      ds.buf("sym.P", 4).as<float>());
+      ds.buf("sym.P", 4).as<float>(), sym_pstride(ds, sym_block_depth(ds)));
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }
@@ -703,7 +732,8 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   if (b0 <= b1) {
     sym_rows_kernel<<<b1 - b0 + 1, kSymBlock, 0, s>>>(P.as<float>(), poff.as<uint32_t>(),
                                                      plist.as<uint32_t>(), bf, bl, b0,
-                                                     Lb - rd, rd, qb, qe, rows);
+                                                     Lb - rd, rd, qb, qe, rows,
+                                                     sym_pstride(ds, Lb));
     FSGG_LAUNCH_CHECK();
     ds.launches++;
   }
@@ -739,7 +769,8 @@ void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* 
       E, level, Lb, eq, eg, ds.buf("sym.qblk", 4).as<uint32_t>(), t.first.as<uint32_t>() + hb,
       ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
       ds.buf("sym.P", 4).as<float>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
-      ds.kde_ws->sym_pos ? ds.buf("sym.pos", 4).as<uint32_t>() : nullptr, ds.kde_ws->sym_b0, g1,
+      ds.kde_ws->sym_pos ? ds.buf("sym.pos", 4).as<uint32_t>() : nullptr, ds.kde_ws->sym_b0,
+      sym_pstride(ds, Lb), g1,
       g2, evals);
   FSGG_LAUNCH_CHECK();
   ds.launches++;

@@ -23,7 +23,7 @@ The graph finish is thus split N ways instead of repeated on every rank.
 With the symmetric root pass (low d) there is one exchange before the
 descent: shard bounds sit on the root's block boundaries
 (fsgg_shard_bounds), every block-pair tile is evaluated by exactly one rank,
-and the other rank's side (256 fp32 values per tile) is sent to it as a
+and the other rank's side (one fp32 value per point of its block) is sent to it as a
 record with one all-to-all (exchange_root) — the root's n^2 work is split
 N ways instead of each rank also evaluating the tiles it shares with its
 neighbours.
@@ -59,7 +59,7 @@ def block_shard_bounds(ds: Dataset, world: int) -> list[int]:
     return [int(x) for x in b]
 
 
-RECORD_WORDS = 260  # X, Y, first point of X, |X|, 256 values (include/fsgg.h)
+RECORD_WORDS = 324  # X, Y, first point of X, |X|, 320 values (include/fsgg.h)
 
 
 def record_destinations(records: torch.Tensor, bounds: list[int]) -> torch.Tensor:
