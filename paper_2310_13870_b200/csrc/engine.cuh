@@ -155,6 +155,7 @@ struct KdeWorkspace {
   // descendants rd levels down); pyr: the same row's pairwise-sum pyramid,
   // depths 1..rd-1 at offsets 2^m - 2 (a lookup then reads two values).
   DevBuf partials, pyr, blk_off, cub_tmp;
+  DevBuf direct_evals;  // u64: evaluations of the direct levels (caller resets/reads)
   uint32_t pyr_depth = 0;  // row depth the pyramid was built for (0: none)
   // symmetric root (kde_sym.cu): block depth Lb of the last root pass (0: the
   // root was not symmetric). Its per-(point, partner block) values stay in

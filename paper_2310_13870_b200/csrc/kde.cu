@@ -781,9 +781,12 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   unsigned long long* d_evals =
       reinterpret_cast<unsigned long long*>(nb + G + 2 + (G & 1));
   FSGG_CUDA(cudaMemsetAsync(d_evals, 0, 16, s));
+  // direct levels add their evaluation count to ws.direct_evals (read once
+  // by the caller after the descent: no host sync per small level)
+  if (direct) ws.direct_evals.ensure(8, s);
   slot_blocks_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
       lv.goff, G, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(), be,
-      direct ? nullptr : nb, d_evals);
+      direct ? nullptr : nb, direct ? ws.direct_evals.as<unsigned long long>() : d_evals);
   FSGG_LAUNCH_CHECK();
   ds.launches += 1;
 
@@ -803,11 +806,6 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     }
     FSGG_LAUNCH_CHECK();
     ds.launches += 1;
-    unsigned long long ev = 0;
-    FSGG_CUDA(cudaMemcpyAsync(&ev, d_evals, 8, cudaMemcpyDeviceToHost, s));
-    FSGG_CUDA(cudaStreamSynchronize(s));
-    stats.evals += ev;
-    stats.performed += ev;
     return;
   }
 

@@ -1155,6 +1155,10 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   // Partial rows of the last compute level serve the following levels.
   DevBuf& row_mass = ds.buf("s.row_mass", 8);
   DevBuf& lookup_evals = ds.buf("s.lookup_evals", 8);
+  FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
+  if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
+  ds.kde_ws->direct_evals.ensure(8, s);
+  FSGG_CUDA(cudaMemsetAsync(ds.kde_ws->direct_evals.as<void>(), 0, 8, s));
   bool have_rows = false;
   uint32_t row_level = 0, row_depth = 0;
   DevBuf& g1 = ds.buf("s.g1", cap * 8);
@@ -1286,16 +1290,12 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     const bool blk_lookup = !lookup && have_rows && row_level == 0 && level > 0 &&
                             ws.sym_Lb > 0 && level + 1 <= ws.sym_Lb && blk_lookup_on();
     bool self_rows = false;
+    // (lookup levels accumulate their reference-equivalent evaluations on the
+    // device; read once after the descent — no host sync per level)
     if (blk_lookup) {
-      FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
       block_lookup_sums(ds, E, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
                         g1.as<double>(), g2.as<double>(), lookup_evals.as<unsigned long long>());
-      unsigned long long ev = 0;
-      FSGG_CUDA(cudaMemcpyAsync(&ev, lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
-      FSGG_CUDA(cudaStreamSynchronize(s));
-      out.kde.evals += ev;
     } else if (lookup) {
-      FSGG_CUDA(cudaMemsetAsync(lookup_evals.as<void>(), 0, 8, s));
       lookup_sums_kernel<<<ceil_div_u32(E, kLookupThreads * kLookupUnroll), kLookupThreads, 0, s>>>(
           E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
           eprow[cur]->as<uint32_t>(), ws.partials.as<double>(),
@@ -1305,10 +1305,6 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
           lookup_evals.as<unsigned long long>());
       FSGG_LAUNCH_CHECK();
       ds.launches++;
-      unsigned long long ev = 0;
-      FSGG_CUDA(cudaMemcpyAsync(&ev, lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
-      FSGG_CUDA(cudaStreamSynchronize(s));
-      out.kde.evals += ev;  // reference-equivalent work served from the rows
     } else {
       uint32_t rd = 0;
       kde_level(ds, ks, lv, g1.as<double>(), g2.as<double>(),
@@ -1470,6 +1466,16 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     }
     E = static_cast<uint32_t>(next);
     cur = nxt;
+  }
+  {
+    // reference-equivalent work served by lookups; direct-level evaluations
+    unsigned long long ev[2] = {0, 0};
+    FSGG_CUDA(cudaMemcpyAsync(&ev[0], lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaMemcpyAsync(&ev[1], ds.kde_ws->direct_evals.as<void>(), 8,
+                              cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    out.kde.evals += ev[0] + ev[1];
+    out.kde.performed += ev[1];
   }
   if (walk_on) {
     uint32_t W = 0;
