@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(128)
                      const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
                      SymTile* __restrict__ tiles, uint32_t* __restrict__ ntiles,
                      unsigned long long* __restrict__ performed, int own,
-                     uint32_t* __restrict__ nrec, uint32_t* __restrict__ records) {
+                     uint32_t* __restrict__ nrec, uint32_t* __restrict__ records,
+                     SymTile* __restrict__ xtiles) {
   __shared__ unsigned long long red[4];
   __shared__ uint32_t wcnt[4], cbase;
   const uint32_t I = blockIdx.x;
@@ -139,10 +140,13 @@ __global__ void __launch_bounds__(128)
     const uint32_t k = k0 + threadIdx.x;
     const uint32_t J = k < poff[I + 1] ? plist[k] : 0u;
     const bool mineI = I >= b0 && I <= b1, mineJ = J >= b0 && J <= b1;
-    const bool take = k < poff[I + 1] && J >= I &&
-                      (own ? (mineI && mineJ) || (mineI && ((I + J) & 1u) == 0u) ||
-                                 (mineJ && ((I + J) & 1u) == 1u)
-                           : mineI || mineJ);
+    const bool take_any = k < poff[I + 1] && J >= I &&
+                          (own ? (mineI && mineJ) || (mineI && ((I + J) & 1u) == 0u) ||
+                                     (mineJ && ((I + J) & 1u) == 1u)
+                               : mineI || mineJ);
+    // owner mode: cross-shard tiles go to their own list (record = index)
+    const bool cross = take_any && own && !(mineI && mineJ);
+    const bool take = take_any && !cross;
     // one reservation per CTA chunk (a per-tile atomic on one counter
     // serialises ~1.7M times at C3)
     const unsigned m = __ballot_sync(0xffffffffu, take);
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(128)
       cbase = t ? atomicAdd(ntiles, t) : 0u;
     }
     __syncthreads();
-    if (take) {
+    if (take_any) {
       ev += (unsigned long long)(bl[I] - bf[I]) * (bl[J] - bf[J]);
       // position of I in J's (ascending) partner list
       uint32_t lo = poff[J], hi = poff[J + 1];
@@ -169,19 +173,20 @@ __global__ void __launch_bounds__(128)
         else
           hi = mid;
       }
-      uint32_t rec = 0, remote = 0;
-      if (own && !(mineI && mineJ)) {  // the other block's values are exported
-        remote = mineI ? 2u : 1u;
-        rec = atomicAdd(nrec, 1u);
+      if (cross) {  // the other block's values are exported as record `rec`
+        const uint32_t remote = mineI ? 2u : 1u;
+        const uint32_t rec = atomicAdd(nrec, 1u);
         const uint32_t X = mineI ? J : I, Y = mineI ? I : J;
         uint32_t* hdr = records + size_t(rec) * kSymRecWords;
         hdr[0] = X;
         hdr[1] = Y;
         hdr[2] = bf[X];
         hdr[3] = bl[X] - bf[X];
+        xtiles[rec] = SymTile{I, J, k - poff[I], lo - poff[J], rec, remote};
+      } else {
+        tiles[cbase + wcnt[w] + __popc(m & ((1u << lane) - 1u))] =
+            SymTile{I, J, k - poff[I], lo - poff[J], 0u, 0u};
       }
-      tiles[cbase + wcnt[w] + __popc(m & ((1u << lane) - 1u))] =
-          SymTile{I, J, k - poff[I], lo - poff[J], rec, remote};
     }
     __syncthreads();
   }
@@ -195,12 +200,12 @@ __global__ void __launch_bounds__(128)
 }
 
 template <int D, int FAM, int ROWS, bool OWN>
-__global__ void __launch_bounds__(ROWS * 16)
-    sym_tile_kernel(const float* __restrict__ pts, const SymTile* __restrict__ tiles,
-                    const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
-                    const float* __restrict__ lo, const float* __restrict__ hi, float scale,
-                    float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
-                    unsigned long long* __restrict__ performed, float* __restrict__ records) {
+__device__ __forceinline__ void sym_tile_body(
+    const float* __restrict__ pts, const SymTile* __restrict__ tiles,
+    const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
+    const float* __restrict__ lo, const float* __restrict__ hi, float scale, float bits,
+    const uint32_t* __restrict__ poff, float* __restrict__ P,
+    unsigned long long* __restrict__ performed, float* __restrict__ records) {
   constexpr int kSymRows = ROWS;
   constexpr int kSymWarps = ROWS / 2;
   constexpr uint32_t kCap = 32u * ROWS;
@@ -306,6 +311,30 @@ __global__ void __launch_bounds__(ROWS * 16)
       cdst[t] = v;
     }
   }
+}
+
+// The kernel for a shard's own tiles (80 registers at d = 2, 6 CTAs per SM)
+// and the one for owner-mode cross-shard tiles (one side exported).
+template <int D, int FAM, int ROWS>
+__global__ void __launch_bounds__(ROWS * 16)
+    sym_tile_kernel(const float* __restrict__ pts, const SymTile* __restrict__ tiles,
+                    const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
+                    const float* __restrict__ lo, const float* __restrict__ hi, float scale,
+                    float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
+                    unsigned long long* __restrict__ performed, float* __restrict__ records) {
+  sym_tile_body<D, FAM, ROWS, false>(pts, tiles, bf, bl, lo, hi, scale, bits, poff, P,
+                                     performed, records);
+}
+template <int D, int FAM, int ROWS>
+__global__ void __launch_bounds__(ROWS * 16)
+    sym_tile_own_kernel(const float* __restrict__ pts, const SymTile* __restrict__ tiles,
+                        const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
+                        const float* __restrict__ lo, const float* __restrict__ hi,
+                        float scale, float bits, const uint32_t* __restrict__ poff,
+                        float* __restrict__ P, unsigned long long* __restrict__ performed,
+                        float* __restrict__ records) {
+  sym_tile_body<D, FAM, ROWS, true>(pts, tiles, bf, bl, lo, hi, scale, bits, poff, P,
+                                    performed, records);
 }
 
 // Fold each point's partner values, in ascending partner order, into its
@@ -584,35 +613,41 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 8, s));
   // a cross tile has one remote side: at most half the partner slots
   DevBuf& rec = ds.buf("sym.rec", own ? (size_t(npart) / 2 + 1) * kSymRecWords * 4 : 4);
+  DevBuf& xtiles = ds.buf("sym.xtiles", own ? (size_t(npart) / 2 + 1) * sizeof(SymTile) : 16);
   sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1, bf,
                                      bl, tiles.as<SymTile>(), ntiles.as<uint32_t>(),
                                      d_performed, own ? 1 : 0, ntiles.as<uint32_t>() + 1,
-                                     rec.as<uint32_t>());
+                                     rec.as<uint32_t>(), xtiles.as<SymTile>());
   FSGG_LAUNCH_CHECK();
   uint32_t nt2[2] = {0, 0};
   FSGG_CUDA(cudaMemcpyAsync(nt2, ntiles.as<void>(), 8, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
-  const uint32_t nt = nt2[0];
+  const uint32_t nt = nt2[0], nx = own ? nt2[1] : 0;
   DevBuf& P = ds.buf("sym.P", size_t(npart) * sym_pstride(ds, Lb) * 4 + 4);
   if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
-  if (nt > 0) {
-    const int rows = sym_rows_per_lane(ds, Lb);
+  // the shard's own tiles with the single-GPU kernel, then (owner mode) the
+  // cross-shard tiles with the kernel that exports one side
+  const int rows = sym_rows_per_lane(ds, Lb);
+  for (int pass = 0; pass < 2; ++pass) {
+    const uint32_t cnt = pass == 0 ? nt : nx;
+    if (cnt == 0) continue;
+    const SymTile* tl = pass == 0 ? tiles.as<SymTile>() : xtiles.as<SymTile>();
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
       auto launch = [&](auto kern, int threads) {
-        kern<<<nt, threads, 0, s>>>(ds.pts.as<float>(), tiles.as<SymTile>(), bf, bl, lo, hi,
-                                    ks.scale, bits, poff.as<uint32_t>(), P.as<float>(),
-                                    d_performed, rec.as<float>());
+        kern<<<cnt, threads, 0, s>>>(ds.pts.as<float>(), tl, bf, bl, lo, hi, ks.scale, bits,
+                                     poff.as<uint32_t>(), P.as<float>(), d_performed,
+                                     rec.as<float>());
       };
       auto by_rows = [&](auto fam) {
         constexpr int FAM = decltype(fam)::value;
         if constexpr (D <= 6) {
           if (rows == 10)
-            return own ? launch(sym_tile_kernel<D, FAM, 10, true>, 160)
-                       : launch(sym_tile_kernel<D, FAM, 10, false>, 160);
+            return pass ? launch(sym_tile_own_kernel<D, FAM, 10>, 160)
+                        : launch(sym_tile_kernel<D, FAM, 10>, 160);
         }
-        own ? launch(sym_tile_kernel<D, FAM, 8, true>, 128)
-            : launch(sym_tile_kernel<D, FAM, 8, false>, 128);
+        pass ? launch(sym_tile_own_kernel<D, FAM, 8>, 128)
+             : launch(sym_tile_kernel<D, FAM, 8>, 128);
       };
       switch (ks.family) {
         case 0: by_rows(std::integral_constant<int, 0>{}); break;
