@@ -594,3 +594,35 @@ def test_distributed_build_over_nccl_world1():
         assert np.array_equal(res.degrees.cpu().numpy(), full.degrees)
     finally:
         dist.destroy_process_group()
+
+
+def test_edge_inclusion_frequency_tracks_reference_probability(oracle):
+    """proj/tests/test_sparsifier.cpp:249-279 restated: over 1000 builds
+    (seeds 9000..9999, default rounds = 42 at n = 128) the frequency of every
+    pair with p(i, j) >= 0.03 lies in [0.9, 12] p(i, j), where p comes from
+    the full graph's degrees (p_i = min(log2 n k / deg_i, 1))."""
+    n = 128
+    pts = oracle.random_dataset(n, 2, 66).astype(np.float32)
+    ds = F.Dataset(pts)
+    k = F.Kernel(G, 0.3)
+    x = pts.astype(np.float64)
+    d2 = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1)
+    K = np.exp(-d2 / (0.3 * 0.3))
+    np.fill_diagonal(K, 0.0)
+    deg = K.sum(1)
+    hits = np.zeros((n, n), dtype=np.int64)
+    builds = 1000
+    for b in range(builds):
+        g = F.build_similarity_graph(ds, k, F.SparsifierConfig(seed=9000 + b))
+        hits[g.u, g.v] += 1
+    logn = math.log2(n)
+    iu, iv = np.triu_indices(n, 1)
+    kij = K[iu, iv]
+    pi = np.minimum(logn * kij / deg[iu], 1.0)
+    pj = np.minimum(logn * kij / deg[iv], 1.0)
+    p = pi + pj - pi * pj
+    sel = (p >= 0.03) & (kij >= 1e-300)
+    freq = hits[iu, iv][sel] / builds
+    assert sel.sum() >= 50
+    assert np.all(freq >= 0.9 * p[sel]), (freq / p[sel]).min()
+    assert np.all(freq <= 12.0 * p[sel]), (freq / p[sel]).max()
