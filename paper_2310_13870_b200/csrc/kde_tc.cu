@@ -20,6 +20,7 @@
 // N-tile t+1.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -202,6 +203,53 @@ __global__ void tc_split_kernel(const float* __restrict__ pts, uint32_t n, uint3
   if (threadIdx.x == 0) norm[row] = float(red[0]);
 }
 
+// Work item: (entry block, side, chunk group), visited in groups of
+// kTcGroup entry blocks x all source groups so the concurrent CTAs share
+// their query and source tiles through L2 (the hi/lo copies of C5 are
+// 440 MB; with a block-major order every CTA streams its sources from
+// DRAM). whole: nodes of <= kTcN points take one item per (entry block,
+// node), both children in one N tile (each query tile gathered once).
+struct TcItem {
+  uint32_t g, side, kk, e0, e1, cf, cl, ntiles;
+};
+
+__device__ __forceinline__ TcItem tc_item(uint32_t item, uint32_t cdepth, int whole,
+                                          uint32_t total_blocks, uint32_t num_slots,
+                                          uint32_t level, const uint32_t* __restrict__ goff,
+                                          const uint32_t* __restrict__ blk_off,
+                                          const uint32_t* __restrict__ tfirst,
+                                          const uint32_t* __restrict__ tlast) {
+  TcItem it;
+  const uint32_t K = 1u << cdepth;
+  const uint32_t cols = whole ? 1u : 2u * K;
+  const uint32_t grp = item / (kTcGroup * cols);
+  const uint32_t r = item - grp * (kTcGroup * cols);
+  const uint32_t gsize = min(uint32_t(kTcGroup), total_blocks - grp * kTcGroup);
+  const uint32_t blk = grp * kTcGroup + r % gsize;
+  const uint32_t col = r / gsize;
+  it.side = whole ? 0u : col >> cdepth;
+  it.kk = whole ? 0u : col & (K - 1);
+  uint32_t lo_ = 0, hi_ = num_slots;
+  while (hi_ - lo_ > 1) {
+    const uint32_t mid = (lo_ + hi_) >> 1;
+    if (blk_off[mid] <= blk) lo_ = mid; else hi_ = mid;
+  }
+  it.g = lo_;
+  it.e0 = goff[it.g] + (blk - blk_off[it.g]) * kTcM;
+  it.e1 = min(it.e0 + uint32_t(kTcM), goff[it.g + 1]);
+  const uint32_t lc = level + 1 + cdepth;
+  const uint64_t h = whole ? ((1ull << level) - 1) + it.g
+                           : ((1ull << lc) - 1) + ((uint64_t(2 * it.g + it.side)) << cdepth) + it.kk;
+  it.cf = tfirst[h];
+  it.cl = tlast[h];
+  it.ntiles = (it.cl - it.cf + kTcN - 1) / kTcN;
+  return it;
+}
+
+// Persistent: one CTA per SM walks the items blockIdx.x, + gridDim.x, ...;
+// the smem ring, the TMEM double buffer and their barrier phases run on
+// across items, so the next item's loads and MMAs overlap this item's
+// epilogue (one CTA per item left a pipeline fill and drain per ~4 N-tiles).
 template <int FAM>
 __global__ void __launch_bounds__(kTcThreads, 1)
     kde_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
@@ -214,7 +262,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   uint32_t num_slots, uint32_t total_blocks, uint32_t level, uint32_t cdepth,
                   uint32_t sdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
-                  float scale, double* __restrict__ partials, int terms, int whole) {
+                  float scale, double* __restrict__ partials, int terms, int whole,
+                  uint32_t items) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -226,43 +275,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- work item: (entry block, side, chunk group), visited in groups of
-  // kTcGroup entry blocks x all source groups so the ~148 concurrent CTAs
-  // share their query and source tiles through L2 (the hi/lo copies of C5
-  // are 440 MB; with a block-major order every CTA streams its sources from
-  // DRAM) ----
-  // whole: nodes of <= kTcN points take one item per (entry block, node),
-  // both children in one N tile (each query tile gathered once, not twice)
-  const uint32_t K = 1u << cdepth;
-  const uint32_t cols = whole ? 1u : 2u * K;
-  uint32_t blk, col;
-  {
-    const uint32_t grp = blockIdx.x / (kTcGroup * cols);
-    const uint32_t r = blockIdx.x - grp * (kTcGroup * cols);
-    const uint32_t gsize = min(uint32_t(kTcGroup), total_blocks - grp * kTcGroup);
-    blk = grp * kTcGroup + r % gsize;
-    col = r / gsize;
-  }
-  const uint32_t side = whole ? 0u : col >> cdepth;
-  const uint32_t kk = whole ? 0u : col & (K - 1);
-  uint32_t g;
-  {
-    uint32_t lo_ = 0, hi_ = num_slots;
-    while (hi_ - lo_ > 1) {
-      const uint32_t mid = (lo_ + hi_) >> 1;
-      if (blk_off[mid] <= blk) lo_ = mid; else hi_ = mid;
-    }
-    g = lo_;
-  }
-  const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kTcM;
-  const uint32_t e1 = min(e0 + uint32_t(kTcM), goff[g + 1]);
-  const uint32_t lc = level + 1 + cdepth;
-  const uint64_t h = whole ? ((1ull << level) - 1) + g
-                           : ((1ull << lc) - 1) + ((uint64_t(2 * g + side)) << cdepth) + kk;
-  const uint32_t cf = tfirst[h], cl = tlast[h];
-  const uint32_t ntiles = (cl - cf + kTcN - 1) / kTcN;
   const uint32_t kblocks = d_pad / kTcKB;
+  auto item_at = [&](uint32_t item) {
+    return tc_item(item, cdepth, whole, total_blocks, num_slots, level, goff, blk_off, tfirst,
+                   tlast);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -292,84 +309,96 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const uint32_t total = ntiles * kblocks;
 
-  // Queries of a block are sorted and distinct; when they are also
-  // consecutive point indices (always at the root of a full build) the
-  // query tiles are plain TMA boxes too and the gather warps stand by.
-  const uint32_t q0 = eq[e0];
-  const bool contig = eq[e1 - 1] == q0 + (e1 - 1 - e0);
   if (warp == 0) {
-    // ---- TMA producer: source (and contiguous query) tiles ---------------
+    // ---- TMA producer: source tiles ------------------------------------
     if (lane == 0) {
-      for (uint32_t it = 0; it < total; ++it) {
-        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-        const uint32_t tile = it / kblocks, kb = it % kblocks;
-        mbar_wait(&empty[s], ph ^ 1u);
-        unsigned char* st = smem + s * kStageBytes;
-        mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
-        const int row = int(cf + tile * kTcN), col = int(kb * kTcKB);
-        tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
-        tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
+      uint32_t it = 0;
+      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const TcItem w = item_at(item);
+        const uint32_t total = w.ntiles * kblocks;
+        for (uint32_t j = 0; j < total; ++j, ++it) {
+          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+          const uint32_t tile = j / kblocks, kb = j % kblocks;
+          mbar_wait(&empty[s], ph ^ 1u);
+          unsigned char* st = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+          const int row = int(w.cf + tile * kTcN), col = int(kb * kTcKB);
+          tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
+          tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
+        }
       }
     }
   } else if (warp == 1) {
     // ---- MMA issuer --------------------------------------------------------
     if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t tile = 0; tile < ntiles; ++tile) {
-        const uint32_t buf = tile & 1u;
-        mbar_wait(&tempty[buf], ((tile >> 1) & 1u) ^ 1u);
-        tc_fence_after();
-        const uint32_t tacc = tmem_base + buf * kTcN;
-        for (uint32_t kb = 0; kb < kblocks; ++kb, ++it) {
-          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-          mbar_wait(&full[s], ph);
+      uint32_t it = 0, tg = 0;
+      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const TcItem w = item_at(item);
+        for (uint32_t tile = 0; tile < w.ntiles; ++tile, ++tg) {
+          const uint32_t buf = tg & 1u;
+          mbar_wait(&tempty[buf], ((tg >> 1) & 1u) ^ 1u);
           tc_fence_after();
-          const uint32_t base = smem_u32(smem + s * kStageBytes);
+          const uint32_t tacc = tmem_base + buf * kTcN;
+          for (uint32_t kb = 0; kb < kblocks; ++kb, ++it) {
+            const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * kStageBytes);
 #pragma unroll
-          for (int ks = 0; ks < kTcKB / 8; ++ks) {
-            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
-            const uint64_t a_hi = sw128_desc(base + off);
-            const uint64_t a_lo = sw128_desc(base + kTileBytes + off);
-            const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
-            const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
-            mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
-            if (terms & 1) mma_tf32(tacc, a_hi, b_lo, 1);
-            if (terms & 2) mma_tf32(tacc, a_lo, b_hi, 1);
+            for (int ks = 0; ks < kTcKB / 8; ++ks) {
+              const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
+              const uint64_t a_hi = sw128_desc(base + off);
+              const uint64_t a_lo = sw128_desc(base + kTileBytes + off);
+              const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
+              const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
+              mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
+              if (terms & 1) mma_tf32(tacc, a_hi, b_lo, 1);
+              if (terms & 2) mma_tf32(tacc, a_lo, b_hi, 1);
+            }
+            mma_commit(&empty[s]);
           }
-          mma_commit(&empty[s]);
+          mma_commit(&tfull[buf]);
         }
-        mma_commit(&tfull[buf]);
       }
     }
   } else if (warp < 4) {
     // ---- query tiles (warp 2): one TMA box when the block's queries are
-    // consecutive, else TMA gather4 — lane l brings rows 4l..4l+3 ----------
+    // consecutive (always at the root of a full build), else TMA gather4 —
+    // lane l brings rows 4l..4l+3 ----------------------------------------
     if (warp == 2) {
-      int rows[4];
+      uint32_t it = 0;
+      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+        const TcItem w = item_at(item);
+        const uint32_t total = w.ntiles * kblocks;
+        int rows[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t e = e0 + 4 * lane + j;
-        rows[j] = int(eq[e < e1 ? e : e0]);
-      }
-      for (uint32_t it = 0; it < total; ++it) {
-        const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-        const int col = int((it % kblocks) * kTcKB);
-        mbar_wait(&empty[s], ph ^ 1u);
-        unsigned char* st = smem + s * kStageBytes;
-        if (lane == 0) mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
-        __syncwarp();
-        if (contig) {
-          if (lane == 0) {
-            tma_load_2d(st, &map_hi, &full[s], col, int(q0));
-            tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(q0));
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t e = w.e0 + 4 * lane + j;
+          rows[j] = int(eq[e < w.e1 ? e : w.e0]);
+        }
+        // queries of a block are sorted and distinct; consecutive point
+        // indices make the tile a plain box
+        const uint32_t q0 = eq[w.e0];
+        const bool contig = eq[w.e1 - 1] == q0 + (w.e1 - 1 - w.e0);
+        for (uint32_t j = 0; j < total; ++j, ++it) {
+          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+          const int col = int((j % kblocks) * kTcKB);
+          mbar_wait(&empty[s], ph ^ 1u);
+          unsigned char* st = smem + s * kStageBytes;
+          if (lane == 0) mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+          __syncwarp();
+          if (contig) {
+            if (lane == 0) {
+              tma_load_2d(st, &map_hi, &full[s], col, int(q0));
+              tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(q0));
+            }
+          } else {
+            tma_gather4(st + lane * 512, &gmap_hi, &full[s], col, rows[0], rows[1], rows[2],
+                        rows[3]);
+            tma_gather4(st + kTileBytes + lane * 512, &gmap_lo, &full[s], col, rows[0], rows[1],
+                        rows[2], rows[3]);
           }
-        } else {
-          tma_gather4(st + lane * 512, &gmap_hi, &full[s], col, rows[0], rows[1], rows[2],
-                      rows[3]);
-          tma_gather4(st + kTileBytes + lane * 512, &gmap_lo, &full[s], col, rows[0], rows[1],
-                      rows[2], rows[3]);
         }
       }
     }
@@ -379,47 +408,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // sdepth levels below the child); one fp64 partial per sub-chunk.
     const uint32_t ew = warp & 3;               // TMEM lane group of this warp
     const uint32_t row = ew * 32 + lane;        // accumulator row = entry
-    const uint32_t e = e0 + row;
-    const float qn = norm[eq[e < e1 ? e : e0]];
-    const uint32_t nsub = 1u << (sdepth - cdepth);
-    const uint64_t hs = ((1ull << (level + 1 + sdepth)) - 1) +
-                        ((uint64_t(2 * g + side)) << sdepth) + uint64_t(kk) * nsub;
-    double* prow = partials + (size_t(e) << (sdepth + 1)) + (side << sdepth) + kk * nsub;
-    uint32_t b = 0, bend = tlast[hs];
-    double racc = 0.0;
-    for (uint32_t tile = 0; tile < ntiles; ++tile) {
-      const uint32_t buf = tile & 1u;
-      mbar_wait(&tfull[buf], (tile >> 1) & 1u);
-      tc_fence_after();
-      const uint32_t n0 = cf + tile * kTcN;
-      const uint32_t valid = min(uint32_t(kTcN), cl - n0);
-      float acc = 0.f;
+    uint32_t tg = 0;
+    for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+      const TcItem w = item_at(item);
+      const uint32_t e = w.e0 + row;
+      const float qn = norm[eq[e < w.e1 ? e : w.e0]];
+      const uint32_t nsub = 1u << (sdepth - cdepth);
+      const uint64_t hs = ((1ull << (level + 1 + sdepth)) - 1) +
+                          ((uint64_t(2 * w.g + w.side)) << sdepth) + uint64_t(w.kk) * nsub;
+      double* prow =
+          partials + (size_t(e) << (sdepth + 1)) + (w.side << sdepth) + w.kk * nsub;
+      uint32_t b = 0, bend = tlast[hs];
+      double racc = 0.0;
+      for (uint32_t tile = 0; tile < w.ntiles; ++tile, ++tg) {
+        const uint32_t buf = tg & 1u;
+        mbar_wait(&tfull[buf], (tg >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t n0 = w.cf + tile * kTcN;
+        const uint32_t valid = min(uint32_t(kTcN), w.cl - n0);
+        float acc = 0.f;
 #pragma unroll
-      for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
-        float v[32];
-        tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+        for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
+          float v[32];
+          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const uint32_t col = chunk * 32 + k;
-          if (col < valid) {  // uniform across the warp
-            while (n0 + col >= bend) {  // next sub-chunk (uniform)
-              if (e < e1) prow[b] = racc + acc;
-              racc = 0.0;
-              acc = 0.f;
-              bend = tlast[hs + (++b)];
+          for (int k = 0; k < 32; ++k) {
+            const uint32_t col = chunk * 32 + k;
+            if (col < valid) {  // uniform across the warp
+              while (n0 + col >= bend) {  // next sub-chunk (uniform)
+                if (e < w.e1) prow[b] = racc + acc;
+                racc = 0.0;
+                acc = 0.f;
+                bend = tlast[hs + (++b)];
+              }
+              const float xn = __ldg(norm + n0 + col);
+              float d2 = fmaxf(fmaf(-2.f, v[k], qn + xn), 0.f);
+              if constexpr (FAM == 1) d2 = sqrtf(d2);
+              acc += ex2_approx(-scale * d2);
             }
-            const float xn = __ldg(norm + n0 + col);
-            float d2 = fmaxf(fmaf(-2.f, v[k], qn + xn), 0.f);
-            if constexpr (FAM == 1) d2 = sqrtf(d2);
-            acc += ex2_approx(-scale * d2);
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+        racc += acc;
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[buf]);
-      racc += acc;
+      if (e < w.e1) prow[b] = racc;
     }
-    if (e < e1) prow[b] = racc;
   }
   tc_fence_before();
   __syncthreads();
@@ -535,12 +569,13 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   }
   const uint32_t s_max = uint32_t((uint64_t(ds.n) + (1ull << lv.level) - 1) >> lv.level);
   const int whole = cdepth == 0 && s_max <= uint32_t(kTcN) ? 1 : 0;
-  const uint64_t launch = whole ? items / 2 : items;
-  kern<<<dim3(static_cast<uint32_t>(launch)), kTcThreads, kSmemBytes, ds.stream>>>(
+  const uint64_t nitems = whole ? items / 2 : items;
+  const uint32_t grid = uint32_t(std::min<uint64_t>(nitems, uint64_t(ds.num_sms)));
+  kern<<<dim3(grid), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, st.gmap_hi, st.gmap_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
       static_cast<uint32_t>(items >> (cdepth + 1)), lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
-      tc_terms(), whole);
+      tc_terms(), whole, static_cast<uint32_t>(nitems));
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }
