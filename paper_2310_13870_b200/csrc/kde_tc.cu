@@ -36,9 +36,11 @@ constexpr int kTcStages = 3;
 constexpr int kTcThreads = 256;
 constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or lo)
 constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
-constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 256;
+constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 512;
 constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
 constexpr uint32_t kTcGroup = 64;                       // entry blocks per L2 group
+constexpr int kRing = 8;          // work-item ring (persistent kernel)
+constexpr int kRingReaders = 6;   // MMA thread, query warp, 4 epilogue warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   uint32_t sdepth,
                   const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
                   float scale, double* __restrict__ partials, int terms, int whole,
-                  uint32_t items) {
+                  uint32_t items, uint32_t* __restrict__ next_item) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -272,10 +274,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* empty = bars + kTcStages;      // [kTcStages]
   uint64_t* tfull = bars + 2 * kTcStages;  // [2]
   uint64_t* tempty = tfull + 2;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ring_full = tempty + 2;           // [kRing]
+  uint64_t* ring_empty = ring_full + kRing;   // [kRing]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(ring_empty + kRing);  // [kRing]
+  uint32_t* tmem_slot = ring + kRing;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t kblocks = d_pad / kTcKB;
+  // Items are handed out in order by a global counter (the producer thread
+  // fetches, the other roles read them from a small smem ring): the active
+  // items of all CTAs stay a compact window, which is what lets them share
+  // query and source tiles in L2 (a static stride let CTAs drift apart:
+  // 4x the DRAM reads).
+  auto next = [&](uint32_t k) -> uint32_t {  // consumers: k-th item of this CTA
+    const uint32_t slot = k % kRing;
+    mbar_wait(&ring_full[slot], (k / kRing) & 1u);
+    return ring[slot];
+  };
+  auto release = [&](uint32_t k) { mbar_arrive(&ring_empty[k % kRing]); };
   auto item_at = [&](uint32_t item) {
     return tc_item(item, cdepth, whole, total_blocks, num_slots, level, goff, blk_off, tfirst,
                    tlast);
@@ -289,6 +305,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128);
+    }
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&ring_full[r], 1);
+      mbar_init(&ring_empty[r], kRingReaders);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -314,7 +334,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---- TMA producer: source tiles ------------------------------------
     if (lane == 0) {
       uint32_t it = 0;
-      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t slot = k % kRing;
+        mbar_wait(&ring_empty[slot], ((k / kRing) & 1u) ^ 1u);
+        const uint32_t item = atomicAdd(next_item, 1u);
+        ring[slot] = item;
+        mbar_arrive(&ring_full[slot]);  // release: the ring write is visible
+        if (item >= items) break;
         const TcItem w = item_at(item);
         const uint32_t total = w.ntiles * kblocks;
         for (uint32_t j = 0; j < total; ++j, ++it) {
@@ -333,7 +359,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---- MMA issuer --------------------------------------------------------
     if (lane == 0) {
       uint32_t it = 0, tg = 0;
-      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t item = next(k);
+        release(k);
+        if (item >= items) break;
         const TcItem w = item_at(item);
         for (uint32_t tile = 0; tile < w.ntiles; ++tile, ++tg) {
           const uint32_t buf = tg & 1u;
@@ -368,7 +397,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // lane l brings rows 4l..4l+3 ----------------------------------------
     if (warp == 2) {
       uint32_t it = 0;
-      for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t item = next(k);
+        __syncwarp();
+        if (lane == 0) release(k);
+        if (item >= items) break;
         const TcItem w = item_at(item);
         const uint32_t total = w.ntiles * kblocks;
         int rows[4];
@@ -409,7 +442,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t ew = warp & 3;               // TMEM lane group of this warp
     const uint32_t row = ew * 32 + lane;        // accumulator row = entry
     uint32_t tg = 0;
-    for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t item = next(k);
+      __syncwarp();
+      if (lane == 0) release(k);
+      if (item >= items) break;
       const TcItem w = item_at(item);
       const uint32_t e = w.e0 + row;
       const float qn = norm[eq[e < w.e1 ? e : w.e0]];
@@ -571,11 +608,13 @@ void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   const int whole = cdepth == 0 && s_max <= uint32_t(kTcN) ? 1 : 0;
   const uint64_t nitems = whole ? items / 2 : items;
   const uint32_t grid = uint32_t(std::min<uint64_t>(nitems, uint64_t(ds.num_sms)));
+  DevBuf& counter = ds.buf("tc.next_item", 8);
+  FSGG_CUDA(cudaMemsetAsync(counter.as<void>(), 0, 4, ds.stream));
   kern<<<dim3(grid), kTcThreads, kSmemBytes, ds.stream>>>(
       st.map_hi, st.map_lo, st.gmap_hi, st.gmap_lo, ds.buf("tc.hi", 8).as<float>(), ds.buf("tc.lo", 8).as<float>(),
       ds.buf("tc.norm", 8).as<float>(), st.d_pad, lv.eq, lv.goff, blk_off, lv.num_slots,
       static_cast<uint32_t>(items >> (cdepth + 1)), lv.level, cdepth, sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), ks.scale, partials,
-      tc_terms(), whole, static_cast<uint32_t>(nitems));
+      tc_terms(), whole, static_cast<uint32_t>(nitems), counter.as<uint32_t>());
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }
