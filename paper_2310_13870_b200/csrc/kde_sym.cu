@@ -361,9 +361,27 @@ __global__ void __launch_bounds__(kSymBlock)
   for (uint32_t b0 = 0; b0 < W; b0 += kSymBucketChunk) {
 #pragma unroll
     for (uint32_t c = 0; c < kSymBucketChunk; ++c) acc[c][t] = 0.0;
-    for (; k < p1 && (plist[k] >> shift) < b0 + kSymBucketChunk; ++k) {
-      const uint32_t c = (plist[k] >> shift) - b0;
-      if (t < ni) acc[c][t] += double(P[size_t(k) * ps + t]);
+    // partners in ascending order, 8 loads in flight per thread (one
+    // dependent load per partner left the kernel latency-bound)
+    const uint32_t bend = b0 + kSymBucketChunk;
+    while (k < p1) {
+      constexpr int kB = 8;
+      uint32_t cb[kB];
+      float v[kB];
+      uint32_t take = 0;
+#pragma unroll
+      for (int j = 0; j < kB; ++j) {
+        cb[j] = k + j < p1 ? (__ldg(plist + k + j) >> shift) : 0xffffffffu;
+        take += cb[j] < bend ? 1u : 0u;  // a prefix: partners are sorted
+      }
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        v[j] = (cb[j] < bend && t < ni) ? __ldg(P + size_t(k + j) * ps + t) : 0.f;
+#pragma unroll
+      for (int j = 0; j < kB; ++j)
+        if (cb[j] < bend && t < ni) acc[cb[j] - b0][t] += double(v[j]);
+      k += take;
+      if (take < uint32_t(kB)) break;
     }
     __syncthreads();
     // coalesced store: consecutive threads write consecutive buckets of a point
