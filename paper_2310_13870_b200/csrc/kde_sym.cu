@@ -493,8 +493,21 @@ __global__ void __launch_bounds__(kBlkThreads)
     for (int u = 0; u < U; ++u) {
       a[u] = b[u] = 0.0;
       const float* pv = P + (q[u] - bf[I[u]]);
-      for (uint32_t kk = k[u]; kk < km[u]; ++kk) a[u] += double(__ldg(pv + size_t(kk) * ps));
-      for (uint32_t kk = km[u]; kk < k1[u]; ++kk) b[u] += double(__ldg(pv + size_t(kk) * ps));
+      // 4 loads in flight; absent ones add +0 (the sums keep their bits)
+      for (uint32_t kk = k[u]; kk < km[u]; kk += 4) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = kk + j < km[u] ? __ldg(pv + size_t(kk + j) * ps) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[u] += double(v[j]);
+      }
+      for (uint32_t kk = km[u]; kk < k1[u]; kk += 4) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = kk + j < k1[u] ? __ldg(pv + size_t(kk + j) * ps) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[u] += double(v[j]);
+      }
     }
   } else
 #pragma unroll
