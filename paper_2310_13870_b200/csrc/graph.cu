@@ -39,16 +39,13 @@ __global__ void rows_to_keys_kernel(uint32_t nq, const uint32_t* __restrict__ uq
                                     const uint32_t* __restrict__ leaf_cnt,
                                     uint32_t bits, unsigned long long* __restrict__ keys,
                                     unsigned long long* __restrict__ counters) {
-  // one warp per row, lanes over its slots (coalesced; a thread per row
-  // strided 32 rows apart in every load)
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long self = 0, sampled = 0;
   if (r < nq) {
     const uint32_t q = uq[r], cnt = row_cnt[r];
     const uint64_t a = row_off[r], b = row_off[r + 1];
-    if (lane == 0) sampled = cnt;
-    for (uint64_t k = a + lane; k < b; k += 32) {
+    sampled = cnt;
+    for (uint64_t k = a; k < b; ++k) {
       unsigned long long key = ~0ull;
       if (k - a < cnt) {
         const uint32_t s = leaf_src[k];
@@ -245,8 +242,7 @@ uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
   keys.ensure(std::max<uint64_t>(cap, 1) * 8, s);
   DevBuf& counters = ds.buf("g.counters", 16);
   FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
-  rows_to_keys_kernel<<<ceil_div_u32(uint64_t(std::max<uint32_t>(res.nq, 1)) * 32, 256), 256,
-                        0, s>>>(
+  rows_to_keys_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(
       res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(),
       res.row_cnt.as<uint32_t>(), res.leaf_src.as<uint32_t>(),
       res.leaf_cnt.as<uint32_t>(), bits, keys.as<unsigned long long>(),
