@@ -66,6 +66,13 @@ __host__ __device__ __forceinline__ uint64_t route_key(uint64_t prefix,
 __host__ __device__ __forceinline__ uint64_t query_link(uint64_t b) {
   return splitmix64(b ^ 0x3c6ef372fe94f82bULL);
 }
+// The node's link splitmix64(prefix ^ splitmix64(a ^ ...)) of route_key: a
+// function of (seed, node) alone, tabulated once per build per tree slot
+// (node_link_kernel, sampler.cu), so an entry's key is
+// splitmix64(node_link ^ query_link).
+__host__ __device__ __forceinline__ uint64_t node_link(uint64_t prefix, uint64_t a) {
+  return splitmix64(prefix ^ splitmix64(a ^ 0xbb67ae8584caa73bULL));
+}
 __host__ __device__ __forceinline__ uint64_t route_key_q(uint64_t prefix, uint64_t a,
                                                          uint64_t qlink) {
   return splitmix64(splitmix64(prefix ^ splitmix64(a ^ 0xbb67ae8584caa73bULL)) ^ qlink);

@@ -309,6 +309,7 @@ struct WalkArgs {
   const uint64_t* row_off = nullptr;
   uint32_t *row_cnt = nullptr, *leaf_src = nullptr, *leaf_cnt = nullptr;
   unsigned long long* stats = nullptr;  // [5][64]: entries, tickets, evals, degen, ties
+  const uint64_t* nlink = nullptr;      // node_link per heap slot (reference RNG)
 };
 bool walk_supported(uint32_t d);
 void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& args);

@@ -67,6 +67,14 @@ uint32_t walk_max_node() {
   return e ? uint32_t(std::atoi(e)) : kWalkMaxNode;
 }
 
+// node_link (common.cuh) for every heap slot of the tree (reference RNG).
+__global__ void node_link_kernel(uint64_t nslots, const uint32_t* __restrict__ tfirst,
+                                 const uint32_t* __restrict__ tlast, uint64_t prefix,
+                                 uint64_t* __restrict__ out) {
+  const uint64_t h = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (h < nslots) out[h] = node_link(prefix, (uint64_t(tfirst[h]) << 32) | tlast[h]);
+}
+
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
                                  uint32_t* __restrict__ eq,
@@ -110,12 +118,14 @@ __global__ void __launch_bounds__(kRouteThreads)
                  unsigned long long* __restrict__ flags,
                  unsigned long long* __restrict__ counters, const float* __restrict__ elm,
                  const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
-                 uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk) {
+                 uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk,
+                 const uint64_t* __restrict__ nlink) {
   constexpr int U = kRouteUnroll;
   const uint32_t base = blockIdx.x * (kRouteThreads * U) + threadIdx.x;
   uint32_t gi[U], q[U], t[U], f[U], l[U];
   double a[U], b[U];
   float em[U], rm[U];
+  uint64_t nl[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * kRouteThreads;
@@ -133,6 +143,7 @@ __global__ void __launch_bounds__(kRouteThreads)
     const uint64_t h = ((1ull << level) - 1) + gi[u];
     f[u] = i < E ? tfirst[h] : 0u;
     l[u] = i < E ? tlast[h] : 0u;
+    nl[u] = (i < E && nlink) ? nlink[h] : 0ull;
     rm[u] = (i < E && row_mass) ? row_mass[eprow ? eprow[i] : i] : 0.f;
   }
   unsigned long long tsum = 0, degen = 0;
@@ -173,7 +184,8 @@ __global__ void __launch_bounds__(kRouteThreads)
         if (rng_mode == 0) {
           // RngStream::keyed(seed, kRouteTag, (first<<32)|last, query)
           const uint64_t key =
-              route_key(key_prefix, (uint64_t(f[u]) << 32) | l[u], uint64_t(q[u]));
+              nlink ? splitmix64(nl[u] ^ query_link(q[u]))
+                    : route_key(key_prefix, (uint64_t(f[u]) << 32) | l[u], uint64_t(q[u]));
           if (vlist) {
             // Tie guard: a draw within the fp32 sums' error bound of p is
             // re-decided on fp64 sums (exact_sums_kernel), which makes the
@@ -1195,6 +1207,17 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   const bool contiguous =
       nq > 0 && uint64_t(req.queries.back()) - req.queries.front() + 1 == nq;
   const uint64_t prefix = route_key_prefix(req.seed);
+  // per-slot node links of the keyed stream: an entry's key is then one
+  // splitmix64 of (node link ^ query link) instead of three
+  const uint64_t nslots = (uint64_t(2) << t.depth) - 1;
+  DevBuf& nlink = ds.buf("s.nlink", req.rng_mode == 0 ? nslots * 8 : 8);
+  if (req.rng_mode == 0) {
+    node_link_kernel<<<ceil_div_u32(nslots, 256), 256, 0, s>>>(
+        nslots, t.first.as<uint32_t>(), t.last.as<uint32_t>(), prefix, nlink.as<uint64_t>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
+  const uint64_t* nlink_p = req.rng_mode == 0 ? nlink.as<uint64_t>() : nullptr;
   uint32_t E = nq;
   int cur = 0;
   out.entries_per_level.clear();
@@ -1345,7 +1368,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         level == 0 ? nullptr : elm[cur]->as<float>(),
         self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
-        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk);
+        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p);
     FSGG_LAUNCH_CHECK();
     if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
         smax_level >= kTieBatchMinNode) {
@@ -1500,6 +1523,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       a.leaf_src = out.leaf_src.as<uint32_t>();
       a.leaf_cnt = out.leaf_cnt.as<uint32_t>();
       a.stats = st.as<unsigned long long>();
+      a.nlink = nlink_p;
       walk_finish(ds, ks, a);
       std::vector<unsigned long long> h(4 * 64);
       FSGG_CUDA(cudaMemcpyAsync(h.data(), st.as<void>(), h.size() * 8, cudaMemcpyDeviceToHost, s));

@@ -33,7 +33,7 @@ struct Decision {
 __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_t f,
                                            uint32_t l, uint32_t q, uint64_t qlink,
                                            uint64_t key_prefix, int rng_mode, uint64_t seed,
-                                           bool want_near) {
+                                           bool want_near, const uint64_t* nlink, uint64_t h) {
   Decision d{false, false, false};
   double p;
   if (a <= kSumFloor && b <= kSumFloor) {
@@ -50,7 +50,9 @@ __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_
     const uint64_t thr = static_cast<uint64_t>(ceil(P));
     uint64_t m;
     if (rng_mode == 0) {
-      m = splitmix64(route_key_q(key_prefix, (uint64_t(f) << 32) | l, qlink)) >> 11;
+      const uint64_t key = nlink ? splitmix64(__ldg(nlink + h) ^ qlink)
+                                 : route_key_q(key_prefix, (uint64_t(f) << 32) | l, qlink);
+      m = splitmix64(key) >> 11;
       if (want_near) {
         const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
         const double M = rel * fmin(p, 1.0 - p) * 9007199254740992.0 + 1.0;
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(kWalkThreads)
                 uint64_t seed, int verify, const uint32_t* __restrict__ qrow,
                 const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_cnt,
                 uint32_t* __restrict__ leaf_src, uint32_t* __restrict__ leaf_cnt,
-                unsigned long long* __restrict__ stats) {
+                unsigned long long* __restrict__ stats, const uint64_t* __restrict__ nlink) {
   __shared__ unsigned long long s_stats[4][kMaxLevels];  // entries, evals, degen, ties
   for (int k = threadIdx.x; k < 4 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
   __syncthreads();
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kWalkThreads)
         direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
         double a = fmax(s[0], kSumFloor), b = fmax(s[1], kSumFloor);
         ev = l - f;
-        Decision dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, check);
+        Decision dc =
+            decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, check, nlink, h);
         if (check && dc.near) {
           // tie guard: re-decide on fp64 sums (kernel_f64, index order)
           const uint32_t mid = f + (l - f) / 2;
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(kWalkThreads)
           for (uint32_t j = mid; j < l; ++j) e1 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
           a = fmax(e0, kSumFloor);
           b = fmax(e1, kSumFloor);
-          dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, false);
+          dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, false, nlink, h);
           tie = 1;
         }
         dg = dc.degenerate ? 1u : 0u;
@@ -193,7 +196,7 @@ void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& a) {
         ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
         ks.family, ks.sigma, a.key_prefix, a.rng_mode, a.seed, a.verify, a.qrow, a.row_off,
-        a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats);
+        a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats, a.nlink);
   };
   switch (ks.family) {
     case 0: walk_by_dim(ds.d, [&](auto dim) { launch(dim, std::integral_constant<int, 0>{}); }); break;
