@@ -94,7 +94,7 @@ __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
 // before using any: at deep levels the kernel is a latency-bound stream of
 // ~60M entries with little arithmetic.
 constexpr int kRouteThreads = 256;
-constexpr int kRouteUnroll = 4;
+constexpr int kRouteUnroll = 2;
 constexpr uint32_t kLeafMark = 0xffffffffu;  // tl of an entry that emitted a leaf
 
 // Packed (has_left, has_right) for the next level's list; with `walk`, a
