@@ -310,6 +310,12 @@ struct WalkArgs {
   uint32_t *row_cnt = nullptr, *leaf_src = nullptr, *leaf_cnt = nullptr;
   unsigned long long* stats = nullptr;  // [5][64]: entries, tickets, evals, degen, ties
   const uint64_t* nlink = nullptr;      // node_link per heap slot (reference RNG)
+  // first step from two-deep partial rows: walks whose start node lies one
+  // level below rows_level read row wrow (stride 4) instead of evaluating
+  const uint32_t* wrow = nullptr;
+  const float* wrm = nullptr;           // log2 node mass the rows were pruned against
+  const double* rows = nullptr;
+  uint32_t rows_level = 0;
 };
 bool walk_supported(uint32_t d);
 void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& args);

@@ -66,6 +66,7 @@ constexpr uint32_t kFlush = 256;     // fp32 run length before the fp64 flush
 constexpr uint32_t kPolyEvery = FSGG_POLY_EVERY;
 constexpr uint32_t kSubMin = 512;    // smallest sub-chunk (pruning granularity)
 constexpr uint32_t kSubMinSmall = 64;  // ... for nodes below 8 * kSubMin points
+constexpr uint32_t kSubMinRow = 32;    // per-sub-chunk rows: sub-chunks of >= 32 points
 
 template <int D>
 struct LowDTile {
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kThreads)
                           const float* __restrict__ tlo,
                           const float* __restrict__ thi, int has_boxes,
                           float scale, int prune, double* __restrict__ partials,
-                          unsigned long long* __restrict__ performed) {
+                          unsigned long long* __restrict__ performed, int per_sub) {
   constexpr int T = LowDTile<D>::T;
   __shared__ __align__(16) float2 sm[T * D];
   __shared__ unsigned long long s_done;
@@ -242,13 +243,22 @@ __global__ void __launch_bounds__(kThreads)
     // A pruned sub-chunk contributes nothing to that entry even when its CTA
     // evaluates it for others: each sum depends on (node, query) alone, never
     // on which entries share the CTA (so sharded and unsharded runs agree).
-    if (!skipA) accA += rescale(sA, offA);
-    if (!skipB) accB += rescale(sB, offB);
+    const double rA = skipA ? 0.0 : rescale(sA, offA);
+    const double rB = skipB ? 0.0 : rescale(sB, offB);
+    if (per_sub) {  // one partial per sub-chunk: rows sdepth + 1 deep (c == 0)
+      const uint32_t stride = 2u * nsub, col = side * nsub + sc;
+      if (va) partials[size_t(ia) * stride + col] = rA;
+      if (vb) partials[size_t(ib) * stride + col] = rB;
+    }
+    accA += rA;
+    accB += rB;
     if (!wskip) done += uint64_t(cl - cf) * nvalid_warp;
   }
-  const uint32_t stride = 2u * K, col = side * K + kk;
-  if (va) partials[size_t(ia) * stride + col] = accA;
-  if (vb) partials[size_t(ib) * stride + col] = accB;
+  if (!per_sub) {
+    const uint32_t stride = 2u * K, col = side * K + kk;
+    if (va) partials[size_t(ia) * stride + col] = accA;
+    if (vb) partials[size_t(ib) * stride + col] = accB;
+  }
   if (performed) {
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_done, done);
     __syncthreads();
@@ -680,12 +690,12 @@ struct LowD {
                     const LevelView& lv, const uint32_t* blk_off,
                     uint32_t cdepth, uint32_t sdepth, const TreeTable& t,
                     float scale, double* partials,
-                    unsigned long long* performed) {
+                    unsigned long long* performed, int per_sub) {
     kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
         pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
         sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
         t.hi.as<float>(), t.has_boxes, scale, lv.prune && t.has_boxes, partials,
-        performed);
+        performed, per_sub);
   }
   static void direct(cudaStream_t s, const float* pts, const LevelView& lv,
                      const TreeTable& t, float scale, double* g1, double* g2,
@@ -841,6 +851,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   // are range sums of this row (lookup_sums_kernel, sampler.cu) instead of
   // new kernel evaluations.
   uint32_t c = 0;
+  int per_sub = 0;
   // rl: log2 of the partial-row width. The CUDA-core kernels write one
   // partial per work item (rl = c + 1); the tensor-core kernel splits its
   // columns at sub-chunk boundaries and writes one per sub-chunk (rl = sd + 1).
@@ -865,6 +876,17 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
            (uint64_t(E) << (c + 2)) <= kMaxPartials)
       ++c;
     rl = c + 1;
+    // children of 64..127 points (C3 level 12): split each into two
+    // sub-chunks and keep both partials per child (rows two levels deep,
+    // same work items): the next level's child sums become lookups and a
+    // walk starting below reads its first child sums from the row
+    if (lowd && sd == 0 && c == 0 && child_min >= 2 * kSubMinRow &&
+        child_min < 2 * kSubMinSmall && lv.level + 2 <= t.depth &&
+        (uint64_t(E) << 2) <= kMaxPartials && env_u32("FSGG_SUBROWS", 1) != 0) {
+      sd = 1;
+      rl = 2;
+      per_sub = 1;
+    }
   }
   // the symmetric root pass (kde_sym.cu) writes rows at any depth up to its
   // block depth Lb (not tied to sub-chunks): as deep as serve_levels asks,
@@ -909,7 +931,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     // every pair evaluated once (kde_sym.cu)
   } else if (lowd) {
     with_lowd(ks.family, d, [&](auto op) {
-      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf);
+      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub);
     });
   } else if (tc) {
     kde_tc_tiled(ds, ks, lv, nb, c, sd, items, partials);

@@ -919,7 +919,9 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                uint32_t* __restrict__ neprow, int self_rows,
                                uint32_t level, uint32_t* __restrict__ wq,
                                uint32_t* __restrict__ wh, float* __restrict__ welm,
-                               uint32_t* __restrict__ wcount) {
+                               uint32_t* __restrict__ wcount, uint32_t* __restrict__ wrow,
+                               float* __restrict__ wrm, const float* __restrict__ elm,
+                               int rows2) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t nw = 0, wmask = 0;  // single-ticket children handed to the walk
   uint32_t g = 0, q = 0;
@@ -981,16 +983,26 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
   if (nw == 0) return;
   uint32_t pos = wbase + wtot[warp] + incl - nw;
   const uint32_t hbase = (1u << (level + 1)) - 1;
+  // rows2: this level kept two-deep partial rows (kde.cu, per-sub-chunk
+  // rows), so the walk's first child sums are in row i (walk.cu reads them
+  // if no later compute level reused the rows); wrm = log2 of this entry's
+  // node mass, the pruning scale of those partials
+  const uint32_t rw = rows2 ? i : 0xffffffffu;
+  const float rm = rows2 && elm ? elm[i] : 0.f;
   if (wmask & 1u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g;
     welm[pos] = float(int((__double_as_longlong(g1[i]) >> 52) & 0x7ff) - 1023);
+    wrow[pos] = rw;
+    wrm[pos] = rm;
     ++pos;
   }
   if (wmask & 2u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g + 1;
     welm[pos] = float(int((__double_as_longlong(g2[i]) >> 52) & 0x7ff) - 1023);
+    wrow[pos] = rw;
+    wrm[pos] = rm;
   }
 }
 
@@ -1172,6 +1184,9 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   ds.kde_ws->direct_evals.ensure(8, s);
   FSGG_CUDA(cudaMemsetAsync(ds.kde_ws->direct_evals.as<void>(), 0, 8, s));
   bool have_rows = false;
+  // the last level that wrote ws.partials (and their depth): the walks read
+  // two-deep rows only if nothing overwrote them after
+  uint32_t part_level = 0, part_depth = 0;
   uint32_t row_level = 0, row_depth = 0;
   DevBuf& g1 = ds.buf("s.g1", cap * 8);
   DevBuf& g2 = ds.buf("s.g2", cap * 8);
@@ -1192,6 +1207,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   DevBuf& wq = ds.buf("s.wq", walk_on ? cap * 4 : 4);
   DevBuf& wh = ds.buf("s.wh", walk_on ? cap * 4 : 4);
   DevBuf& welm = ds.buf("s.welm", walk_on ? cap * 4 : 4);
+  DevBuf& wrow = ds.buf("s.wrow", walk_on ? cap * 4 : 4);
+  DevBuf& wrm = ds.buf("s.wrm", walk_on ? cap * 4 : 4);
   DevBuf& wcount = ds.buf("s.wcount", 8);
   FSGG_CUDA(cudaMemsetAsync(wcount.as<void>(), 0, 8, s));
 
@@ -1334,6 +1351,10 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
                 level == 0 && req.want_root_sums ? out.groot.as<double>() : nullptr, ws,
                 out.kde, level == 0 ? root_serve_levels() : kServeLevels, &rd);
       have_rows = rd > 1;
+      if (rd > 0) {
+        part_level = level;
+        part_depth = rd;
+      }
       if (have_rows) {
         self_rows = true;
         row_level = level;
@@ -1450,7 +1471,9 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         et[nxt]->as<uint32_t>(), eg[nxt]->as<uint32_t>(), elm[nxt]->as<float>(),
         eprow[cur]->as<uint32_t>(), eprow[nxt]->as<uint32_t>(), self_rows ? 1 : 0, level,
         wk ? wq.as<uint32_t>() : nullptr, wh.as<uint32_t>(), welm.as<float>(),
-        wcount.as<uint32_t>());
+        wcount.as<uint32_t>(), wrow.as<uint32_t>(), wrm.as<float>(),
+        level == 0 ? nullptr : elm[cur]->as<float>(),
+        self_rows && row_depth == 2 ? 1 : 0);
     FSGG_LAUNCH_CHECK();
     if (level < t.depth) {
       goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
@@ -1506,13 +1529,18 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     FSGG_CUDA(cudaStreamSynchronize(s));
     if (W > 0) {
       const auto w0 = std::chrono::steady_clock::now();
-      DevBuf& st = ds.buf("s.walk_stats", 4 * 64 * 8);
-      FSGG_CUDA(cudaMemsetAsync(st.as<void>(), 0, 4 * 64 * 8, s));
+      DevBuf& st = ds.buf("s.walk_stats", 5 * 64 * 8);
+      FSGG_CUDA(cudaMemsetAsync(st.as<void>(), 0, 5 * 64 * 8, s));
       WalkArgs a;
       a.W = W;
       a.wq = wq.as<uint32_t>();
       a.wh = wh.as<uint32_t>();
       a.welm = welm.as<float>();
+      a.wrow = wrow.as<uint32_t>();
+      a.wrm = wrm.as<float>();
+      // the last compute level's two-deep rows, if no later level reused them
+      a.rows = part_depth == 2 ? ws.partials.as<double>() : nullptr;
+      a.rows_level = part_level;
       a.key_prefix = prefix;
       a.seed = req.seed;
       a.rng_mode = req.rng_mode;
@@ -1525,7 +1553,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       a.stats = st.as<unsigned long long>();
       a.nlink = nlink_p;
       walk_finish(ds, ks, a);
-      std::vector<unsigned long long> h(4 * 64);
+      std::vector<unsigned long long> h(5 * 64);
       FSGG_CUDA(cudaMemcpyAsync(h.data(), st.as<void>(), h.size() * 8, cudaMemcpyDeviceToHost, s));
       FSGG_CUDA(cudaStreamSynchronize(s));
       // merge the walks' per-level tallies into the level diagnostics
@@ -1538,7 +1566,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
         out.entries_per_level[lv2] += h[lv2];
         out.tickets_per_level[lv2] += h[lv2];  // one ticket each
         out.kde.evals += h[64 + lv2];
-        out.kde.performed += h[64 + lv2];
+        out.kde.performed += h[64 + lv2] - h[256 + lv2];  // minus steps read from rows
         out.degenerate_draws += h[128 + lv2];
         out.tie_verified += h[192 + lv2];
       }

@@ -33,7 +33,8 @@ struct Decision {
 __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_t f,
                                            uint32_t l, uint32_t q, uint64_t qlink,
                                            uint64_t key_prefix, int rng_mode, uint64_t seed,
-                                           bool want_near, const uint64_t* nlink, uint64_t h) {
+                                           bool want_near, const uint64_t* nlink, uint64_t h,
+                                           double pruned) {
   Decision d{false, false, false};
   double p;
   if (a <= kSumFloor && b <= kSumFloor) {
@@ -55,7 +56,7 @@ __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_
       m = splitmix64(key) >> 11;
       if (want_near) {
         const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em) / 32.0);
-        const double M = rel * fmin(p, 1.0 - p) * 9007199254740992.0 + 1.0;
+        const double M = (rel * fmin(p, 1.0 - p) + pruned) * 9007199254740992.0 + 1.0;
         const uint64_t lo = P > M ? static_cast<uint64_t>(P - M) : 0ull;
         const uint64_t hi = static_cast<uint64_t>(P + M);
         d.near |= (m >= lo) & (m <= hi);
@@ -80,9 +81,12 @@ __global__ void __launch_bounds__(kWalkThreads)
                 uint64_t seed, int verify, const uint32_t* __restrict__ qrow,
                 const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_cnt,
                 uint32_t* __restrict__ leaf_src, uint32_t* __restrict__ leaf_cnt,
-                unsigned long long* __restrict__ stats, const uint64_t* __restrict__ nlink) {
-  __shared__ unsigned long long s_stats[4][kMaxLevels];  // entries, evals, degen, ties
-  for (int k = threadIdx.x; k < 4 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
+                unsigned long long* __restrict__ stats, const uint64_t* __restrict__ nlink,
+                const uint32_t* __restrict__ wrow, const float* __restrict__ wrm,
+                const double* __restrict__ rows, uint32_t rows_level) {
+  // entries, evals, degen, ties, evals read from rows
+  __shared__ unsigned long long s_stats[5][kMaxLevels];
+  for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
   __syncthreads();
 
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -92,12 +96,18 @@ __global__ void __launch_bounds__(kWalkThreads)
   float em = 0.f;
   float qc[D];
   uint64_t qlink = 0;
+  uint32_t row = 0xffffffffu;  // first step read from the row (see WalkArgs)
+  float rmass = 0.f;
   if (live) {
     q = wq[i];
     qlink = query_link(q);
     h = wh[i];
     em = welm[i];
     lev = 31 - __clz(uint32_t(h) + 1);
+    if (rows && lev == rows_level + 1) {
+      row = wrow[i];
+      rmass = wrm[i];
+    }
 #pragma unroll
     for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
   }
@@ -106,7 +116,7 @@ __global__ void __launch_bounds__(kWalkThreads)
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     if (live) {
       const uint32_t f = tfirst[h], l = tlast[h];
-      uint32_t ev = 0, dg = 0, tie = 0;
+      uint32_t ev = 0, dg = 0, tie = 0, sv = 0;
       const uint32_t at = lev;
       if (l - f == 1) {  // sampler.cpp:196-198: leaf (query, source, 1)
         const uint32_t row = qrow[q];
@@ -117,11 +127,25 @@ __global__ void __launch_bounds__(kWalkThreads)
         live = false;
       } else {
         double s[2];
-        direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
-        double a = fmax(s[0], kSumFloor), b = fmax(s[1], kSumFloor);
+        double pruned = 0.0;
         ev = l - f;
+        if (row != 0xffffffffu) {
+          // the node's children are buckets 2 side, 2 side + 1 of the row
+          // (h odd: left child of its parent); the partials skipped
+          // sub-chunks below 2^-48 of half the row's node mass: the tie
+          // margin takes that bound (as route_kernel's row_mass term)
+          const double* r = rows + (size_t(row) << 2) + ((h & 1u) ? 0u : 2u);
+          s[0] = r[0];
+          s[1] = r[1];
+          pruned = check ? double(exp2f(rmass - (kPruneBits - 24.f) - em)) : 0.0;
+          sv = ev;
+          row = 0xffffffffu;  // later steps evaluate
+        } else {
+          direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
+        }
+        double a = fmax(s[0], kSumFloor), b = fmax(s[1], kSumFloor);
         Decision dc =
-            decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, check, nlink, h);
+            decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, check, nlink, h, pruned);
         if (check && dc.near) {
           // tie guard: re-decide on fp64 sums (kernel_f64, index order)
           const uint32_t mid = f + (l - f) / 2;
@@ -131,7 +155,7 @@ __global__ void __launch_bounds__(kWalkThreads)
           for (uint32_t j = mid; j < l; ++j) e1 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
           a = fmax(e0, kSumFloor);
           b = fmax(e1, kSumFloor);
-          dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, false, nlink, h);
+          dc = decide(a, b, em, f, l, q, qlink, key_prefix, rng_mode, seed, false, nlink, h, 0.0);
           tie = 1;
         }
         dg = dc.degenerate ? 1u : 0u;
@@ -148,6 +172,7 @@ __global__ void __launch_bounds__(kWalkThreads)
                                                                 : __match_any_sync(live_mask, at);
       const uint32_t n_ent = __popc(grp);
       const uint32_t n_ev = __reduce_add_sync(grp, ev);
+      const uint32_t n_sv = __reduce_add_sync(grp, sv);
       const bool rare = __any_sync(grp, dg | tie);
       const uint32_t n_dg = rare ? __reduce_add_sync(grp, dg) : 0u;
       const uint32_t n_tie = rare ? __reduce_add_sync(grp, tie) : 0u;
@@ -156,11 +181,12 @@ __global__ void __launch_bounds__(kWalkThreads)
         if (n_ev) atomicAdd(&s_stats[1][at], static_cast<unsigned long long>(n_ev));
         if (n_dg) atomicAdd(&s_stats[2][at], static_cast<unsigned long long>(n_dg));
         if (n_tie) atomicAdd(&s_stats[3][at], static_cast<unsigned long long>(n_tie));
+        if (n_sv) atomicAdd(&s_stats[4][at], static_cast<unsigned long long>(n_sv));
       }
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < 4 * kMaxLevels; k += blockDim.x) {
+  for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) {
     const unsigned long long v = (&s_stats[0][0])[k];
     if (v) atomicAdd(stats + k, v);
   }
@@ -196,7 +222,8 @@ void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& a) {
         ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
         ks.family, ks.sigma, a.key_prefix, a.rng_mode, a.seed, a.verify, a.qrow, a.row_off,
-        a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats, a.nlink);
+        a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats, a.nlink, a.wrow, a.wrm, a.rows,
+        a.rows_level);
   };
   switch (ks.family) {
     case 0: walk_by_dim(ds.d, [&](auto dim) { launch(dim, std::integral_constant<int, 0>{}); }); break;

@@ -464,25 +464,30 @@ def test_depth_first_finish_matches_level_synchronous(tmp_path):
 def test_single_ticket_walks_match_level_synchronous(rng):
     """Single-ticket walks (walk.cu, FSGG_WALK_MAX) must give the same
     samples and the same reference diagnostics as keeping every entry in the
-    level-synchronous lists, for both RNG modes and several thresholds."""
+    level-synchronous lists, for both RNG modes and several thresholds —
+    also with walks whose first step reads the two-deep partial rows of the
+    level above (FSGG_SUBROWS, n = 30000: rows at level 7, walks from 8)."""
     import os
     p, _ = datasets.make_moons(30000, 0.05, 3)
     ds = F.Dataset(p)
     k = F.Kernel(F.KernelFamily.gaussian, 0.08)
     mode = F.RngMode.reference if rng == "reference" else F.RngMode.philox
     outs = []
-    old = os.environ.get("FSGG_WALK_MAX")
+    saved = {v: os.environ.get(v) for v in ("FSGG_WALK_MAX", "FSGG_SUBROWS")}
     try:
-        for wmax in ("0", "64", "1024"):
+        for wmax, sub in (("0", "1"), ("64", "1"), ("1024", "1"), ("128", "1"),
+                          ("128", "0")):
             os.environ["FSGG_WALK_MAX"] = wmax
+            os.environ["FSGG_SUBROWS"] = sub
             tri, d = F.sample_neighbors_counted(ds, k, np.arange(30000), 24, 5, rng_mode=mode,
                                                 diagnostics=True)
             outs.append((tri, d))
     finally:
-        if old is None:
-            os.environ.pop("FSGG_WALK_MAX", None)
-        else:
-            os.environ["FSGG_WALK_MAX"] = old
+        for v, old in saved.items():
+            if old is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = old
     for tri, d in outs[1:]:
         assert np.array_equal(outs[0][0], tri)
         assert list(outs[0][1].entries_per_level) == list(d.entries_per_level)
