@@ -358,7 +358,7 @@ int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
  * every query is a source, and the block-pair tiles between two shards
  * serve both: instead of both ranks evaluating such a tile, one computes it
  * and sends the other rank's side as a record. Sequence per rank:
- *   fsgg_shard_bounds(ds, world, bounds)        block-aligned query ranges
+ *   fsgg_shard_bounds(ds, k, world, bounds)     block-aligned query ranges
  *   fsgg_shard_root_prepare(ds, k, cfg, &n)   this shard's tiles, and n
  *       records owed to other ranks
  *   fsgg_shard_root_export(ds, dst)             copy them to a caller device
@@ -373,7 +373,10 @@ int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
  * symmetric for this data or the range is not block-aligned. Replaces no
  * reference interface: the reference has no multi-device path
  * (SURVEY.md §2). */
-int fsgg_shard_bounds(fsgg_dataset* ds, uint32_t world, uint32_t* bounds_host);
+/* kernel may be NULL: equal block counts; else block-aligned bounds that
+ * balance a per-block cost model (root pair evaluations + descent work). */
+int fsgg_shard_bounds(fsgg_dataset* ds, const fsgg_kernel* kernel, uint32_t world,
+                      uint32_t* bounds_host);
 int fsgg_shard_root_prepare(fsgg_dataset* ds, const fsgg_kernel* kernel,
                             const fsgg_config* cfg, uint64_t* num_records);
 int fsgg_shard_root_export(fsgg_dataset* ds, uint32_t* records_device);

@@ -180,7 +180,8 @@ _SIGS = {
                                     C.POINTER(fsgg_shard), C.POINTER(fsgg_report)]),
     "fsgg_probe_ex2_throughput": (C.c_int, [C.c_int, C.POINTER(C.c_double),
                                             C.POINTER(C.c_double)]),
-    "fsgg_shard_bounds": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "fsgg_shard_bounds": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32,
+                                    C.POINTER(C.c_uint32)]),
     "fsgg_shard_root_prepare": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.POINTER(fsgg_config),
                                           C.POINTER(C.c_uint64)]),
     "fsgg_shard_root_export": (C.c_int, [_P, _P]),

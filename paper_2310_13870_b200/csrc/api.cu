@@ -805,13 +805,20 @@ int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_con
   });
 }
 
-int fsgg_shard_bounds(fsgg_dataset* h, uint32_t world, uint32_t* bounds) {
+int fsgg_shard_bounds(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t world,
+                      uint32_t* bounds) {
   return guarded([&] {
     activate(h);
     if (world == 0 || !bounds) throw fsgg::ConfigError("invalid world size");
     fsgg::Dataset& ds = h->ds;
     if (!ds.tree_valid) fsgg::build_tree(ds);
-    fsgg::sym_shard_bounds(ds, world, bounds);
+    if (kernel) {
+      validate_kernel(kernel);
+      const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
+      fsgg::sym_shard_bounds(ds, &ks, world, bounds);
+    } else {
+      fsgg::sym_shard_bounds(ds, nullptr, world, bounds);
+    }
   });
 }
 

@@ -283,8 +283,9 @@ bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t 
                        uint32_t* num_records, const uint32_t** records);
 // Store records received from other ranks (device) into this shard's values.
 void sym_shard_receive(Dataset& ds, const uint32_t* records, uint32_t num_records);
-// Block-aligned shard bounds (world + 1 entries) for owner mode.
-void sym_shard_bounds(Dataset& ds, uint32_t world, uint32_t* bounds);
+// Block-aligned shard bounds (world + 1 entries) for owner mode, balanced
+// by a per-block cost model when the kernel is given (else equal blocks).
+void sym_shard_bounds(Dataset& ds, const KernelSpec* ks, uint32_t world, uint32_t* bounds);
 // Child sums of level `level` (1 <= level, level + 1 <= ws.sym_Lb) from the
 // symmetric root's per-(point, partner block) values: each child of a node
 // at this level is a run of whole blocks, so its sum for query q is the sum,

@@ -818,20 +818,52 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   return true;
 }
 
-void sym_shard_bounds(Dataset& ds, uint32_t world, uint32_t* bounds) {
+// Cost model of a shard (measured on C3): a root pair evaluation costs
+// ~6.6e-6 of the descent work of one query; a block's root cost is half its
+// pair evaluations (cross tiles are split between the two owners).
+constexpr double kRootPairPerQuery = 6.6e-6;
+
+void sym_shard_bounds(Dataset& ds, const KernelSpec* ks, uint32_t world, uint32_t* bounds) {
   const uint32_t Lb = sym_block_depth(ds);
   for (uint32_t r = 0; r <= world; ++r) bounds[r] = uint32_t(uint64_t(ds.n) * r / world);
   if (Lb == 0) return;
   const uint32_t B = 1u << Lb;
-  std::vector<uint32_t> hbf(B);
-  FSGG_CUDA(cudaMemcpyAsync(hbf.data(), ds.tree.first.as<uint32_t>() + (B - 1), size_t(B) * 4,
+  const uint64_t hb = uint64_t(B) - 1;
+  std::vector<uint32_t> hbf(B), hbl(B), cnt(B, 0);
+  FSGG_CUDA(cudaMemcpyAsync(hbf.data(), ds.tree.first.as<uint32_t>() + hb, size_t(B) * 4,
                             cudaMemcpyDeviceToHost, ds.stream));
+  FSGG_CUDA(cudaMemcpyAsync(hbl.data(), ds.tree.last.as<uint32_t>() + hb, size_t(B) * 4,
+                            cudaMemcpyDeviceToHost, ds.stream));
+  if (ks) {  // active partners per block (the root pass's own count kernel)
+    DevBuf& c = ds.buf("sym.cnt", size_t(B + 1) * 4);
+    sym_count_kernel<<<B, 256, 0, ds.stream>>>(
+        B, ds.tree.lo.as<float>() + hb * ds.d, ds.tree.hi.as<float>() + hb * ds.d,
+        ds.tree.first.as<uint32_t>() + hb, ds.tree.last.as<uint32_t>() + hb, ds.d, ks->family,
+        ks->scale, kPruneBits + 1.f, c.as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    FSGG_CUDA(cudaMemcpyAsync(cnt.data(), c.as<void>(), size_t(B) * 4, cudaMemcpyDeviceToHost,
+                              ds.stream));
+  }
   FSGG_CUDA(cudaStreamSynchronize(ds.stream));
-  // rank r starts at block round(r B / world): equal block counts
-  for (uint32_t r = 1; r < world; ++r)
-    bounds[r] = hbf[std::min<uint64_t>(B - 1, (uint64_t(B) * r + world / 2) / world)];
+  // cumulative cost over blocks; rank r starts at the first block whose
+  // prefix reaches r/world of the total (equal block counts without ks)
+  const double per_block = double(ds.n) / B;
+  std::vector<double> pre(B + 1, 0.0);
+  for (uint32_t I = 0; I < B; ++I) {
+    const double sz = double(hbl[I] - hbf[I]);
+    pre[I + 1] = pre[I] + sz * (1.0 + kRootPairPerQuery * 0.5 * cnt[I] * per_block);
+  }
+  uint32_t I = 0;
+  for (uint32_t r = 1; r < world; ++r) {
+    const double target = pre[B] * r / world;
+    while (I < B && pre[I + 1] <= target) ++I;
+    // nearer of the two block boundaries around the target
+    const uint32_t cut = (I < B && target - pre[I] > pre[I + 1] - target) ? I + 1 : I;
+    bounds[r] = cut < B ? hbf[cut] : ds.n;
+  }
   bounds[0] = 0;
   bounds[world] = ds.n;
+  for (uint32_t r = 1; r <= world; ++r) bounds[r] = std::max(bounds[r], bounds[r - 1]);
 }
 
 void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,

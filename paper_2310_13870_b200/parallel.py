@@ -51,11 +51,13 @@ def shard_bounds(n: int, world: int) -> list[int]:
     return [shard_range(n, r, world)[0] for r in range(world)] + [n]
 
 
-def block_shard_bounds(ds: Dataset, world: int) -> list[int]:
+def block_shard_bounds(ds: Dataset, world: int, kernel: Kernel | None = None) -> list[int]:
     """Query bounds on the symmetric root's block boundaries (plain
-    shard_bounds when the root pass is not symmetric for this data)."""
+    shard_bounds when the root pass is not symmetric for this data); with
+    ``kernel``, balanced by the library's per-block cost model."""
     b = (C.c_uint32 * (world + 1))()
-    N.check(N.lib().fsgg_shard_bounds(ds._h, world, b))
+    k = kernel._c() if kernel is not None else None
+    N.check(N.lib().fsgg_shard_bounds(ds._h, C.byref(k) if k is not None else None, world, b))
     return [int(x) for x in b]
 
 
@@ -227,7 +229,7 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
     cfg = config or SparsifierConfig()
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     n = ds.n
-    bounds = block_shard_bounds(ds, world)
+    bounds = block_shard_bounds(ds, world, kernel)
     qb, qe = bounds[rank], bounds[rank + 1]
     shard_cfg = replace(cfg, query_begin=qb, query_end=qe)
     root_bytes = exchange_root(ds, kernel, shard_cfg, bounds, group)

@@ -73,7 +73,7 @@ def main():
             bounds = parallel.shard_bounds(a.n, world)
             handles = [ds] * world
         else:
-            bounds = parallel.block_shard_bounds(ds, world)
+            bounds = parallel.block_shard_bounds(ds, world, k)
             handles = [ds] + [F.Dataset(p) for _ in range(world - 1)]
         cfgs = [F.SparsifierConfig(rounds=L, seed=1, query_begin=bounds[r],
                                    query_end=bounds[r + 1]) for r in range(world)]

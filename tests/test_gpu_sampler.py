@@ -330,7 +330,7 @@ def test_owner_mode_root_is_bit_identical(world):
     full, rep, _ = F.build_similarity_graph(ds0, k, cfg, report=True)
     assert rep.kde_root_performed_evals > 0
     handles = [F.Dataset(p) for _ in range(world)]
-    bounds = parallel.block_shard_bounds(handles[0], world)
+    bounds = parallel.block_shard_bounds(handles[0], world, k)
     assert bounds[0] == 0 and bounds[-1] == n
     cfgs = [F.SparsifierConfig(rounds=16, seed=3, query_begin=bounds[r], query_end=bounds[r + 1])
             for r in range(world)]
