@@ -282,6 +282,19 @@ int fsgg_graph_save_text(const char* path, uint32_t n, uint64_t num_edges,
  * the reference's order. Returns FSGG_ERR_IO for unreadable or malformed
  * files. Free with fsgg_graph_free. */
 int fsgg_graph_load_text(const char* path, uint32_t threads, fsgg_graph* out);
+/* Point files, fsg::load_csv / save_csv (proj/src/dataset.cpp:54-130): an
+ * optional header row (first field not a number; a trailing "label" column
+ * marks integer labels), comma-separated values parsed as doubles; saving
+ * writes "x0,...,x{d-1}[,label]" and "%.17g" values. Rows are parsed and
+ * formatted in parallel (threads = 0: every host core); files and errors do
+ * not depend on the thread count. load: *points (n x d, row-major) and
+ * *labels (NULL when the file has none; pass labels = NULL to skip them)
+ * are freed with fsgg_free. Malformed files return FSGG_ERR_IO, non-finite
+ * values FSGG_ERR_CONFIG, as the reference. */
+int fsgg_csv_load(const char* path, uint32_t threads, double** points, uint32_t* n,
+                  uint32_t* d, uint32_t** labels);
+int fsgg_csv_save(const char* path, const double* points, uint32_t n, uint32_t d,
+                  const uint32_t* labels, uint32_t threads);
 /* Binary upper-triangular CSR ("FSGGCSR1", n, m, total weight, row_ptr,
  * v, w, degrees; little-endian): no text conversion either way. */
 int fsgg_graph_save_csr(const char* path, const fsgg_graph* g);

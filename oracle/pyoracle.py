@@ -63,6 +63,11 @@ class Ref:
         lib.fsgref_kde_eval.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, _u32p,
                                         C.c_size_t, _f64p]
         lib.fsgref_set_threads.argtypes = [C.c_uint]
+        lib.fsgref_load_csv.argtypes = [C.c_char_p, C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                        C.POINTER(C.c_void_p)]
+        lib.fsgref_save_csv.argtypes = [C.c_char_p, C.c_void_p, C.c_uint32, C.c_uint32,
+                                        C.c_void_p]
         lib.fsgref_worker_count.restype = C.c_uint
 
     def _check(self, rc):
@@ -71,6 +76,31 @@ class Ref:
 
     def set_threads(self, n: int):
         self.lib.fsgref_set_threads(n)
+
+    def load_csv(self, path: str):
+        """fsg::load_csv: (points n x d float64, labels uint32 or None)."""
+        pts, lab = C.c_void_p(), C.c_void_p()
+        n, d = C.c_uint32(), C.c_uint32()
+        self._check(self.lib.fsgref_load_csv(os.fsencode(path), C.byref(pts), C.byref(n),
+                                             C.byref(d), C.byref(lab)))
+        try:
+            x = np.ctypeslib.as_array(C.cast(pts, C.POINTER(C.c_double)),
+                                      shape=(n.value * d.value,)).copy()
+            labels = None
+            if lab.value:
+                labels = np.ctypeslib.as_array(C.cast(lab, C.POINTER(C.c_uint32)),
+                                               shape=(n.value,)).copy()
+            return x.reshape(n.value, d.value), labels
+        finally:
+            self.lib.fsgref_free(pts)
+            self.lib.fsgref_free(lab)
+
+    def save_csv(self, path: str, points, labels=None):
+        x = np.ascontiguousarray(points, np.float64)
+        lab = None if labels is None else np.ascontiguousarray(labels, np.uint32)
+        self._check(self.lib.fsgref_save_csv(os.fsencode(path), x.ctypes.data, x.shape[0],
+                                             x.shape[1],
+                                             lab.ctypes.data if lab is not None else None))
 
     def worker_count(self) -> int:
         return int(self.lib.fsgref_worker_count())

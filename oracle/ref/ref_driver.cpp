@@ -128,6 +128,30 @@ void fsgref_free(void* p) { std::free(p); }
 void fsgref_set_threads(unsigned n) { fsg::set_worker_count(n); }
 unsigned fsgref_worker_count(void) { return fsg::worker_count(); }
 
+// fsg::load_csv / save_csv (proj/src/dataset.cpp:54-130), called as is.
+int fsgref_load_csv(const char* path, double** pts, uint32_t* n, uint32_t* d,
+                    uint32_t** labels) {
+  *pts = nullptr;
+  *labels = nullptr;
+  return guarded([&] {
+    auto cd = fsg::load_csv(path);
+    *n = cd.data.size();
+    *d = cd.data.dim();
+    *pts = dup_vector(cd.data.raw());
+    if (cd.labels) *labels = dup_vector(*cd.labels);
+  });
+}
+
+int fsgref_save_csv(const char* path, const double* pts, uint32_t n, uint32_t d,
+                    const uint32_t* labels) {
+  return guarded([&] {
+    fsg::Dataset ds(std::vector<double>(pts, pts + size_t(n) * d), n, d);
+    std::vector<uint32_t> lab;
+    if (labels) lab.assign(labels, labels + n);
+    fsg::save_csv(path, ds, labels ? &lab : nullptr);
+  });
+}
+
 int fsgref_make_moons(uint32_t n, double noise, uint64_t seed, double* pts,
                       uint32_t* labels) {
   return guarded([&] {

@@ -8,8 +8,8 @@ from .api import (BuildReport, Dataset, EigenOptions, EigenResult, KMeansOptions
                   SpectralOptions, kmeans, smallest_eigenpairs, spectral_cluster, Kernel, KernelFamily, KdeEstimator, LogBase,
                   RngMode, SampleDiagnostics, SparsifierConfig, WeightedGraph,
                   build_similarity_graph, build_similarity_graph_device, default_epsilon,
-                  device_available, device_graph_to_host, exact_kde, load_csr, make_estimator,
-                  read_edge_list, sample_neighbors, sample_neighbors_counted)
+                  device_available, device_graph_to_host, exact_kde, load_csr, load_csv, make_estimator,
+                  read_edge_list, sample_neighbors, sample_neighbors_counted, save_csv)
 from .errors import (ConfigError, DeviceError, Error, InvalidConfig, IoError,
                      LengthMismatch, NumericError, TooFewPoints)
 
@@ -19,7 +19,7 @@ __all__ = [
     "BuildReport", "Dataset", "Kernel", "KernelFamily", "KdeEstimator", "LogBase", "RngMode",
     "SampleDiagnostics", "SparsifierConfig", "WeightedGraph", "build_similarity_graph",
     "build_similarity_graph_device", "default_epsilon", "device_available", "exact_kde",
-    "load_csr", "make_estimator", "read_edge_list", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
+    "load_csr", "load_csv", "save_csv", "make_estimator", "read_edge_list", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
     "DeviceError", "Error", "InvalidConfig", "IoError", "LengthMismatch", "NumericError",
     "TooFewPoints",
 ]

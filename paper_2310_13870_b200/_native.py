@@ -163,6 +163,9 @@ _SIGS = {
     "fsgg_graph_load_text": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(fsgg_graph)]),
     "fsgg_graph_save_csr": (C.c_int, [C.c_char_p, C.POINTER(fsgg_graph)]),
     "fsgg_graph_load_csr": (C.c_int, [C.c_char_p, C.POINTER(fsgg_graph)]),
+    "fsgg_csv_load": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(_P), C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint32), C.POINTER(_P)]),
+    "fsgg_csv_save": (C.c_int, [C.c_char_p, _P, C.c_uint32, C.c_uint32, _P, C.c_uint32]),
     "fsgg_sample_neighbors_counted": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
                                                 C.c_uint32, C.c_uint64, C.c_int, C.c_int,
                                                 C.POINTER(_P), C.POINTER(C.c_size_t),

@@ -270,6 +270,44 @@ def load_csr(path: str) -> WeightedGraph:
     return _load_graph("fsgg_graph_load_csr", path)
 
 
+def load_csv(path: str, threads: int = 0):
+    """fsg::load_csv (proj/src/dataset.cpp:54-102): returns (points as an
+    n x d float64 array, labels as uint32 or None)."""
+    lib = N.lib()
+    pts, lab = C.c_void_p(), C.c_void_p()
+    n, d = C.c_uint32(), C.c_uint32()
+    N.check(lib.fsgg_csv_load(os.fsencode(path), threads, C.byref(pts), C.byref(n),
+                              C.byref(d), C.byref(lab)))
+    try:
+        x = np.ctypeslib.as_array(C.cast(pts, C.POINTER(C.c_double)),
+                                  shape=(n.value * d.value,)).copy().reshape(n.value, d.value)
+        labels = None
+        if lab.value:
+            labels = np.ctypeslib.as_array(C.cast(lab, C.POINTER(C.c_uint32)),
+                                           shape=(n.value,)).copy()
+        return x, labels
+    finally:
+        lib.fsgg_free(pts)
+        lib.fsgg_free(lab)
+
+
+def save_csv(path: str, points, labels=None, threads: int = 0):
+    """fsg::save_csv (proj/src/dataset.cpp:104-130): "x0,...[,label]" header,
+    "%.17g" values."""
+    x = np.ascontiguousarray(points, np.float64)
+    if x.ndim != 2:
+        raise ValueError("points must be n x d")
+    n, d = x.shape
+    lab = None
+    if labels is not None:
+        lab = np.ascontiguousarray(labels, np.uint32)
+        if lab.size != n:
+            from .errors import LengthMismatch
+            raise LengthMismatch("label count does not match dataset size")
+    N.check(N.lib().fsgg_csv_save(os.fsencode(path), x.ctypes.data, n, d,
+                                  lab.ctypes.data if lab is not None else None, threads))
+
+
 @dataclass
 class BuildReport:
     """proj/include/fsg/sparsifier.hpp:40-58 plus device counters."""

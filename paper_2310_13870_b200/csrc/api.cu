@@ -24,6 +24,10 @@ void graph_save_text(const char* path, uint32_t n, uint64_t m, const uint32_t* u
 void graph_load_text(const char* path, uint32_t threads, fsgg_graph* g);
 void graph_save_csr(const char* path, const fsgg_graph* g);
 void graph_load_csr(const char* path, fsgg_graph* g);
+void csv_load(const char* path, uint32_t threads, double** points, uint32_t* n, uint32_t* d,
+              uint32_t** labels);
+void csv_save(const char* path, const double* pts, uint32_t n, uint32_t d,
+              const uint32_t* labels, uint32_t threads);
 }  // namespace fsgg
 
 struct fsgg_dataset {
@@ -680,6 +684,16 @@ int fsgg_graph_load_text(const char* path, uint32_t threads, fsgg_graph* out) {
 
 int fsgg_graph_save_csr(const char* path, const fsgg_graph* g) {
   return guarded([&] { fsgg::graph_save_csr(path, g); });
+}
+
+int fsgg_csv_load(const char* path, uint32_t threads, double** points, uint32_t* n,
+                  uint32_t* d, uint32_t** labels) {
+  return guarded([&] { fsgg::csv_load(path, threads, points, n, d, labels); });
+}
+
+int fsgg_csv_save(const char* path, const double* points, uint32_t n, uint32_t d,
+                  const uint32_t* labels, uint32_t threads) {
+  return guarded([&] { fsgg::csv_save(path, points, n, d, labels, threads); });
 }
 
 int fsgg_graph_load_csr(const char* path, fsgg_graph* out) {

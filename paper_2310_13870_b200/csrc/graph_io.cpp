@@ -12,7 +12,9 @@
 // not depend on the thread count.
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <charconv>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -357,6 +359,214 @@ void graph_load_csr(const char* path, fsgg_graph* g) {
     fsgg_graph_free(g);
     throw IoError(std::string("corrupt CSR file: ") + path);
   }
+}
+
+// ---- point files (proj/src/dataset.cpp:54-130) ------------------------------
+// load_csv: lines split at '\n' (empty lines skipped), fields at ',', '\r'
+// dropped; a first row whose first field is not a number is a header, and
+// a trailing "label" header column marks integer labels. Values parse as
+// std::from_chars doubles with surrounding whitespace allowed; any other
+// field, a wrong field count, a negative label or no data rows is an I/O
+// error (code 3), a non-finite value a config error (the Dataset
+// constructor's check, code 2). Rows are parsed in parallel chunks; the
+// error reported is the first one in file order, as sequentially.
+namespace {
+
+bool csv_double(const char* b, const char* e, double& out) {
+  while (b < e && std::isspace(static_cast<unsigned char>(*b))) ++b;
+  while (e > b && std::isspace(static_cast<unsigned char>(e[-1]))) --e;
+  if (b == e) return false;
+  const auto r = std::from_chars(b, e, out);
+  return r.ec == std::errc() && r.ptr == e;
+}
+
+// fields of [b, e) (one line) with '\r' removed, as split_fields does
+void csv_fields(const char* b, const char* e, std::vector<std::string>& out) {
+  out.clear();
+  std::string cur;
+  for (const char* p = b; p < e; ++p) {
+    if (*p == ',') {
+      out.push_back(cur);
+      cur.clear();
+    } else if (*p != '\r') {
+      cur += *p;
+    }
+  }
+  out.push_back(cur);
+}
+
+struct CsvChunk {
+  std::vector<double> values;
+  std::vector<uint32_t> labels;
+  std::string error;  // first error in this chunk ("" = none)
+};
+
+}  // namespace
+
+void csv_load(const char* path, uint32_t threads, double** points, uint32_t* n_out,
+              uint32_t* d_out, uint32_t** labels_out) {
+  if (!path || !points || !n_out || !d_out) throw ConfigError("null argument");
+  *points = nullptr;
+  if (labels_out) *labels_out = nullptr;
+  File in(path, "rb");
+  if (!in.f) throw IoError(std::string("cannot open ") + path);
+  std::fseek(in.f, 0, SEEK_END);
+  const long size = std::ftell(in.f);
+  std::fseek(in.f, 0, SEEK_SET);
+  if (size < 0) throw IoError(std::string("cannot read ") + path);
+  std::vector<char> text(size_t(size) + 1);
+  if (size && std::fread(text.data(), 1, size_t(size), in.f) != size_t(size))
+    throw IoError(std::string("cannot read ") + path);
+  const char* s = text.data();
+  const char* end = s + size;
+  auto line_end = [&](const char* p) {
+    const void* q = std::memchr(p, '\n', size_t(end - p));
+    return q ? static_cast<const char*>(q) : end;
+  };
+  // first non-empty line: header or the first data row
+  const char* p = s;
+  std::vector<std::string> f;
+  bool has_labels = false, header = false;
+  uint32_t d = 0;
+  while (p < end) {
+    const char* le = line_end(p);
+    if (le > p) {
+      csv_fields(p, le, f);
+      double probe;
+      if (!csv_double(f[0].data(), f[0].data() + f[0].size(), probe)) {
+        has_labels = !f.empty() && f.back() == "label";
+        d = static_cast<uint32_t>(f.size() - (has_labels ? 1 : 0));
+        header = true;
+        p = le < end ? le + 1 : end;
+      } else {
+        d = static_cast<uint32_t>(f.size());
+      }
+      break;
+    }
+    p = le < end ? le + 1 : end;
+  }
+  (void)header;
+  const uint32_t expect = d + (has_labels ? 1u : 0u);
+  // line-aligned chunks of the body, parsed in parallel
+  const uint64_t target = 1u << 22;
+  std::vector<const char*> cut{p};
+  while (cut.back() < end) {
+    const char* c = cut.back() + std::min<uint64_t>(target, uint64_t(end - cut.back()));
+    c = c < end ? line_end(c) : end;
+    cut.push_back(c < end ? c + 1 : end);
+  }
+  const uint64_t nch = cut.size() - 1;
+  std::vector<CsvChunk> chunks(nch);
+  const uint32_t t = resolve_threads(threads, uint64_t(end - p), 1u << 20);
+  parallel_for(t, nch, [&](uint64_t c) {
+    CsvChunk& ch = chunks[c];
+    std::vector<std::string> fl;
+    for (const char* q = cut[c]; q < cut[c + 1];) {
+      const char* le = line_end(q);
+      if (le > q) {
+        csv_fields(q, le, fl);
+        if (fl.size() != expect) {
+          ch.error = std::string(path) + ": row with " + std::to_string(fl.size()) +
+                     " fields, expected " + std::to_string(expect);
+          return;
+        }
+        for (uint32_t k = 0; k < d; ++k) {
+          double v;
+          if (!csv_double(fl[k].data(), fl[k].data() + fl[k].size(), v)) {
+            ch.error = std::string(path) + ": cannot parse value '" + fl[k] + "'";
+            return;
+          }
+          ch.values.push_back(v);
+        }
+        if (has_labels) {
+          double v;
+          if (!csv_double(fl[d].data(), fl[d].data() + fl[d].size(), v) || v < 0) {
+            ch.error = std::string(path) + ": cannot parse label '" + fl[d] + "'";
+            return;
+          }
+          ch.labels.push_back(static_cast<uint32_t>(v));
+        }
+      }
+      q = le < end ? le + 1 : end;
+    }
+  });
+  uint64_t nv = 0;
+  for (const CsvChunk& ch : chunks) {
+    if (!ch.error.empty()) throw IoError(ch.error);
+    nv += ch.values.size();
+  }
+  if (nv == 0) throw IoError(std::string(path) + ": no data rows");
+  if (d < 1) throw ConfigError("dataset needs n >= 1 and d >= 1");
+  const uint64_t n = nv / d;
+  if (n > UINT32_MAX) throw ConfigError("too many points");
+  double* pts = host_array<double>(nv);
+  uint32_t* lab = has_labels && labels_out ? host_array<uint32_t>(n) : nullptr;
+  uint64_t at = 0, la = 0;
+  for (const CsvChunk& ch : chunks) {
+    std::copy(ch.values.begin(), ch.values.end(), pts + at);
+    at += ch.values.size();
+    if (lab) {
+      std::copy(ch.labels.begin(), ch.labels.end(), lab + la);
+      la += ch.labels.size();
+    }
+  }
+  for (uint64_t i = 0; i < nv; ++i)
+    if (!std::isfinite(pts[i])) {  // Dataset::Dataset (dataset.cpp:19-22)
+      std::free(pts);
+      std::free(lab);
+      throw ConfigError("dataset coordinates must be finite");
+    }
+  *points = pts;
+  *n_out = static_cast<uint32_t>(n);
+  *d_out = d;
+  if (labels_out) *labels_out = lab;
+}
+
+// save_csv: header "x0,...,x{d-1}[,label]", values "%.17g" (std::to_chars
+// with precision 17), rows formatted in parallel chunks, written in order.
+void csv_save(const char* path, const double* pts, uint32_t n, uint32_t d,
+              const uint32_t* labels, uint32_t threads) {
+  if (!path || (n && !pts)) throw ConfigError("null argument");
+  if (d < 1 || n < 1) throw ConfigError("dataset needs n >= 1 and d >= 1");
+  File out(path, "wb");
+  if (!out.f) throw IoError(std::string("cannot write ") + path);
+  std::string head;
+  for (uint32_t c = 0; c < d; ++c) {
+    if (c) head += ',';
+    head += 'x';
+    head += std::to_string(c);
+  }
+  if (labels) head += ",label";
+  head += '\n';
+  bool ok = std::fwrite(head.data(), 1, head.size(), out.f) == head.size();
+  const uint64_t rows_per = std::max<uint64_t>(1, (1u << 18) / d);
+  const uint64_t chunks = (uint64_t(n) + rows_per - 1) / rows_per;
+  const uint32_t t = resolve_threads(threads, chunks, 1);
+  std::vector<std::vector<char>> buf(t);
+  std::vector<uint64_t> len(t);
+  for (uint64_t c0 = 0; ok && c0 < chunks; c0 += t) {
+    const uint64_t batch = std::min<uint64_t>(t, chunks - c0);
+    parallel_for(t, batch, [&](uint64_t b) {
+      const uint64_t r0 = (c0 + b) * rows_per, r1 = std::min<uint64_t>(n, r0 + rows_per);
+      buf[b].resize((r1 - r0) * (uint64_t(d) * 33 + 12));
+      char* q = buf[b].data();
+      for (uint64_t r = r0; r < r1; ++r) {
+        for (uint32_t c = 0; c < d; ++c) {
+          if (c) *q++ = ',';
+          q = std::to_chars(q, q + 32, pts[r * d + c], std::chars_format::general, 17).ptr;
+        }
+        if (labels) {
+          *q++ = ',';
+          q = put_u64(q, labels[r]);
+        }
+        *q++ = '\n';
+      }
+      len[b] = q - buf[b].data();
+    });
+    for (uint64_t b = 0; ok && b < batch; ++b)
+      ok = std::fwrite(buf[b].data(), 1, len[b], out.f) == len[b];
+  }
+  if (!ok || std::fflush(out.f) != 0) throw IoError(std::string("failed writing ") + path);
 }
 
 }  // namespace fsgg

@@ -119,3 +119,81 @@ def test_csr_round_trip(graph, tmp_path):
     (tmp_path / "magic.csr").write_bytes(b"X" + data[1:])
     with pytest.raises(F.IoError):
         F.load_csr(str(tmp_path / "magic.csr"))
+
+
+# ---- point files: fsg::load_csv / save_csv (proj/src/dataset.cpp:54-130) ----
+
+def _points(n, d, seed):
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0, 3, (n, d)) * np.exp(rng.normal(0, 4, (n, d)))
+    special = [0.0, -0.0, 1.0, 0.1, 1e-300, 5e-324, -1.7976931348623157e308, 2.0 ** 53 + 2,
+               1 / 3, -2.5e-308]
+    x.flat[:len(special)] = special
+    return x
+
+
+@pytest.mark.parametrize("labels", [False, True])
+def test_csv_save_bytes_match_reference(ref, tmp_path, labels):
+    x = _points(5000, 3, 1)
+    lab = (np.arange(5000) * 7 % 11).astype(np.uint32) if labels else None
+    ours, theirs = tmp_path / "ours.csv", tmp_path / "ref.csv"
+    F.save_csv(str(ours), x, lab, threads=3)
+    ref.save_csv(str(theirs), x, lab)
+    assert ours.read_bytes() == theirs.read_bytes()
+
+
+CSV_CASES = {
+    "header_labels": "x0,x1,label\n1,2,0\n3.5,-4e-3,1\n",
+    "no_header": "1,2\n3,4\n\n5,6\n",
+    "crlf_spaces": "x0,x1\r\n 1 , 2\r\n3,\t4 \r\n",
+    "header_no_label": "a,b,c\n1,2,3\n",
+    "label_fraction": "x0,label\n1.5,2.9\n2.5,0\n",
+    "trailing_no_newline": "x0\n1\n2",
+    "blank_lines": "\n\nx0,x1\n\n1,2\n\n",
+    "exponents": "1e300,-2.5E-308\n0x1p3,inf\n",
+    "bad_count": "x0,x1\n1,2\n3\n",
+    "bad_value": "x0,x1\n1,2\n3,abc\n",
+    "negative_label": "x0,label\n1,-1\n",
+    "empty_field": "x0,x1\n1,\n",
+    "no_rows": "x0,x1\n\n",
+    "nonfinite": "x0\nnan\n",
+    "header_only_label": "label\n1\n",
+}
+
+
+@pytest.mark.parametrize("case", sorted(CSV_CASES))
+def test_csv_load_matches_reference(ref, tmp_path, case):
+    path = tmp_path / f"{case}.csv"
+    path.write_bytes(CSV_CASES[case].encode())
+    from oracle.pyoracle import OracleError
+    try:
+        want = ref.load_csv(str(path))
+        want_err = None
+    except OracleError as e:  # the reference's exit code decides ours
+        want, want_err = None, e.code
+    try:
+        got = F.load_csv(str(path), threads=2)
+        got_err = None
+    except F.Error as e:
+        got, got_err = None, e
+    if want is None:
+        assert got is None, f"reference failed ({want_err}) but we parsed {case}"
+        assert got_err.exit_code == want_err, (got_err, want_err)
+    else:
+        assert got_err is None, got_err
+        assert np.array_equal(got[0], want[0]) and got[0].shape == want[0].shape
+        assert (got[1] is None) == (want[1] is None)
+        if want[1] is not None:
+            assert np.array_equal(got[1], want[1])
+
+
+def test_csv_large_parallel_round_trip(ref, tmp_path):
+    x = _points(200_000, 5, 2)
+    lab = (np.arange(200_000) % 7).astype(np.uint32)
+    path = tmp_path / "big.csv"
+    F.save_csv(str(path), x, lab)
+    for t in (1, 4, 0):
+        y, l = F.load_csv(str(path), threads=t)
+        assert np.array_equal(y, x) and np.array_equal(l, lab)
+    y2, l2 = ref.load_csv(str(path))
+    assert np.array_equal(y2, x) and np.array_equal(l2, lab)
