@@ -317,11 +317,11 @@ def main():
             t0 = time.perf_counter()
             ds.upload_ptr(host_ptr)  # pinned host -> device
             if world == 1:
-                dg, _ = F.build_similarity_graph_device(ds, kernel, cfg)
                 # device -> pinned host: the graph as CSR (row_ptr, v, w) +
-                # degrees; the per-edge u is redundant with row_ptr and
-                # expanded on demand
-                g = hostbufs.fetch(ds, dg)
+                # degrees, each array's copy started as soon as it is final
+                # (fsgg_build_similarity_graph_into); the per-edge u is
+                # redundant with row_ptr and expanded on demand
+                g = hostbufs.build_into(ds, kernel, cfg, L)
                 nbytes = g.v.nbytes + g.w.nbytes + g.row_ptr.nbytes + g.degrees.nbytes
             else:
                 # each rank reads back the all-gathered graph (CSR + degrees)

@@ -195,6 +195,18 @@ int fsgg_build_similarity_graph_device(fsgg_dataset* ds,
                                        fsgg_device_graph* out,
                                        fsgg_report* report);
 
+/* fsg::build_similarity_graph into caller host buffers (pinned memory for
+ * full speed): the upper CSR (v, w: `capacity` >= edge count entries, n*L
+ * always suffices; row_ptr: n+1; degrees: n) is copied out array by array
+ * while the rest of the graph is still being finished, so the transfer
+ * overlaps the device work. Any buffer pointer may be NULL (not copied);
+ * total_weight (nullable) receives the graph's total weight. Edge u of
+ * entry e is the row r with row_ptr[r] <= e < row_ptr[r+1]. */
+int fsgg_build_similarity_graph_into(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                                     const fsgg_config* cfg, uint64_t capacity,
+                                     uint32_t* v, double* w, uint64_t* row_ptr,
+                                     double* degrees, uint64_t* num_edges,
+                                     double* total_weight, fsgg_report* report);
 /* One-call drop-in from host fp32 points to a host graph. */
 int fsgg_build_similarity_graph_host(const float* points, uint32_t n,
                                      uint32_t d, const fsgg_kernel* kernel,

@@ -132,6 +132,11 @@ _SIGS = {
                                                      C.POINTER(fsgg_config),
                                                      C.POINTER(fsgg_device_graph),
                                                      C.POINTER(fsgg_report)]),
+    "fsgg_build_similarity_graph_into": (C.c_int, [_P, C.POINTER(fsgg_kernel),
+                                                   C.POINTER(fsgg_config), C.c_uint64, _P, _P,
+                                                   _P, _P, C.POINTER(C.c_uint64),
+                                                   C.POINTER(C.c_double),
+                                                   C.POINTER(fsgg_report)]),
     "fsgg_build_similarity_graph_host": (C.c_int, [_P, C.c_uint32, C.c_uint32,
                                                    C.POINTER(fsgg_kernel),
                                                    C.POINTER(fsgg_config), C.c_int,

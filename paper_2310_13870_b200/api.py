@@ -422,6 +422,32 @@ class HostGraphBuffers:
             del g.u  # expanded lazily from row_ptr (WeightedGraph.__getattr__)
         return g
 
+    def build_into(self, ds: "Dataset", kernel: "Kernel", config: "SparsifierConfig",
+                   rounds: int) -> "WeightedGraph":
+        """build_similarity_graph straight into the pinned buffers
+        (fsgg_build_similarity_graph_into): each CSR array's device-to-host
+        copy starts as soon as it is final, overlapping the rest of the
+        finish. ``rounds`` sizes the edge buffers (n * L bounds the edges)."""
+        n = ds.n
+        cap = n * rounds
+        v = self._get("v", cap, np.uint32)
+        w = self._get("w", cap, np.float64)
+        rp = self._get("row_ptr", n + 1, np.uint64)
+        dg = self._get("degrees", n, np.float64)
+        m = C.c_uint64()
+        tw = C.c_double()
+        rep = N.fsgg_report()
+        N.check(N.lib().fsgg_build_similarity_graph_into(
+            ds._h, C.byref(kernel._c()), C.byref(config._c()), cap,
+            v.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p),
+            rp.ctypes.data_as(C.c_void_p), dg.ctypes.data_as(C.c_void_p), C.byref(m),
+            C.byref(tw), C.byref(rep)))
+        mm = int(m.value)
+        g = WeightedGraph(n=n, u=None, v=v[:mm], w=w[:mm], row_ptr=rp, degrees=dg,
+                          total_weight=float(tw.value))
+        del g.u  # expanded lazily from row_ptr
+        return g
+
 
 def build_similarity_graph(ds: Dataset, kernel: Kernel, config: SparsifierConfig | None = None,
                            report: bool = False, estimates: bool = False):

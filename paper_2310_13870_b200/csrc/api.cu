@@ -253,7 +253,8 @@ void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
 }
 
 void build_device(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config* cfgp,
-                  fsgg_report* report, bool want_estimates) {
+                  fsgg_report* report, bool want_estimates,
+                  const fsgg::HostSink* sink = nullptr) {
   activate(h);
   validate_kernel(kernel);
   fsgg_config cfg = cfgp ? *cfgp : default_config();
@@ -272,7 +273,7 @@ void build_device(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config*
   const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
   if (!h->graph) h->graph = std::make_unique<fsgg::GraphResult>();
   fsgg::finish_graph(ds, ks, bo.L, res.groot.as<double>(),
-                     h->keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph);
+                     h->keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph, sink);
   double t2 = now();
   bo.t_graph += t2 - t1;
   if (report) finish_report(report, ds, bo, h->graph.get(), t2 - t0 + bo.t_tree * 0);
@@ -541,6 +542,25 @@ int fsgg_build_similarity_graph_device(fsgg_dataset* h, const fsgg_kernel* kerne
     if (!out) throw fsgg::ConfigError("null output");
     build_device(h, kernel, cfg, report, false);
     to_device_graph(h, out);
+  });
+}
+
+int fsgg_build_similarity_graph_into(fsgg_dataset* h, const fsgg_kernel* kernel,
+                                     const fsgg_config* cfg, uint64_t capacity,
+                                     uint32_t* v, double* w, uint64_t* row_ptr,
+                                     double* degrees, uint64_t* num_edges,
+                                     double* total_weight, fsgg_report* report) {
+  return guarded([&] {
+    if (!num_edges) throw fsgg::ConfigError("null output");
+    fsgg::HostSink sink;
+    sink.v = v;
+    sink.w = w;
+    sink.row_ptr = row_ptr;
+    sink.degrees = degrees;
+    sink.capacity = capacity;
+    build_device(h, kernel, cfg, report, false, &sink);
+    *num_edges = h->graph->m;
+    if (total_weight) *total_weight = h->graph->total_weight;
   });
 }
 

@@ -344,10 +344,22 @@ void rows_degrees(Dataset& ds, const GraphResult& g, const uint32_t* lower_v,
                   const double* lower_w, uint64_t nlower, uint32_t rb, uint32_t re,
                   double* deg_out);
 
+// Host destination of a graph streamed out while it is finished: each
+// array's device-to-host copy starts (on its own stream) as soon as the
+// array is final, overlapping the rest of the finish. Buffers should be
+// pinned; capacity bounds the edge arrays (n * L suffices).
+struct HostSink {
+  uint32_t* v = nullptr;
+  double* w = nullptr;
+  uint64_t* row_ptr = nullptr;
+  double* degrees = nullptr;
+  uint64_t capacity = 0;
+};
+
 // Dedupe (keys may repeat across shards), weight, CSR, degrees.
 void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
                   const double* g_full, const uint64_t* keys, uint64_t nkeys,
                   bool keys_sorted_unique, bool want_estimates,
-                  GraphResult& out);
+                  GraphResult& out, const HostSink* sink = nullptr);
 
 }  // namespace fsgg

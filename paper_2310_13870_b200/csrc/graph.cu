@@ -267,7 +267,7 @@ uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
 void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
                   const double* g_full, const uint64_t* keys_in, uint64_t nkeys,
                   bool keys_sorted_unique, bool want_estimates,
-                  GraphResult& out) {
+                  GraphResult& out, const HostSink* sink) {
   cudaStream_t s = ds.stream;
   const uint32_t n = ds.n, d = ds.d;
   const uint32_t bits = index_bits(n);
@@ -358,6 +358,24 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   out.m = m;
   const uint64_t mm = std::max<uint64_t>(m, 1);
 
+  // streamed host output: v and w are final here; their copies overlap the
+  // CSR, the transposed sort and the degrees below
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  auto after = [&](void* dst, const void* src, size_t bytes) {
+    if (!dst || !bytes) return;
+    FSGG_CUDA(cudaEventRecord(ev, s));
+    FSGG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+    FSGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
+  };
+  if (sink) {
+    if (m > sink->capacity) throw ConfigError("host output capacity below the edge count");
+    FSGG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    FSGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    after(sink->v, out.v.as<void>(), m * 4);
+    after(sink->w, out.w.as<void>(), m * 8);
+  }
+
   // 4. upper CSR, transposed CSR, degrees, total weight. The transpose is a
   // stable radix sort on v alone (ceil(log2 n) bits): edges arrive in (u, v)
   // order, so each vertex's lower neighbours stay in ascending u.
@@ -371,6 +389,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
       out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
   FSGG_LAUNCH_CHECK();
+  if (sink) after(sink->row_ptr, out.row_ptr.as<void>(), (uint64_t(n) + 1) * 8);
   if (m) {
     FSGG_CUDA(cudaMemcpyAsync(tv.as<void>(), out.v.as<void>(), m * 4, cudaMemcpyDeviceToDevice, s));
     FSGG_CUDA(cudaMemcpyAsync(wt.as<void>(), out.w.as<void>(), m * 8,
@@ -396,6 +415,12 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   } else {
     FSGG_CUDA(cudaMemsetAsync(out.degrees.as<void>(), 0, size_t(n) * 8, s));
     out.total_weight = 0.0;
+  }
+  if (sink) {
+    after(sink->degrees, out.degrees.as<void>(), size_t(n) * 8);
+    FSGG_CUDA(cudaStreamSynchronize(cs));
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(cs);
   }
   FSGG_CUDA(cudaStreamSynchronize(s));
 }

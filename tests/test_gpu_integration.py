@@ -49,3 +49,22 @@ def test_gpu_graph_file_round_trips_through_reference_reader(ref, tmp_path):
        total_weight=0.0).write_edge_list(str(ours))
     ref.save_edge_list(str(theirs), 2000, r["u"], r["v"], r["w"])
     assert ours.read_bytes() == theirs.read_bytes()
+
+
+def test_build_into_pinned_buffers_matches_device_build():
+    """fsgg_build_similarity_graph_into (host buffers filled while the graph
+    is finished) returns exactly the device build's CSR, weights, degrees
+    and total weight."""
+    import numpy as np
+    import paper_2310_13870_b200 as F
+    from paper_2310_13870_b200 import datasets
+    p, _ = datasets.make_moons(20000, 0.05, 4)
+    ds = F.Dataset(p)
+    k = F.Kernel(F.KernelFamily.gaussian, 0.08)
+    cfg = F.SparsifierConfig(rounds=16, seed=2)
+    full = F.build_similarity_graph(ds, k, cfg)
+    g = F.api.HostGraphBuffers().build_into(ds, k, cfg, 16)
+    assert np.array_equal(g.v, full.v) and np.array_equal(g.w, full.w)
+    assert np.array_equal(g.row_ptr, full.row_ptr) and np.array_equal(g.u, full.u)
+    assert np.array_equal(g.degrees, full.degrees)
+    assert g.total_weight == full.total_weight
