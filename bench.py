@@ -15,12 +15,15 @@ sigma = 0.05, 64 samples/point (it fits one GPU). Prints ONE JSON line.
              flushed (512 MiB write) between steps outside the timed events;
              max over ranks.
 * e2e        same metric through the public API with HOST buffers: each step
-             uploads the points from pinned memory and copies the whole graph
-             (u, v, w, row_ptr, degrees) back to host.
-* roofline   the tiled low-d KDE kernel (MUFU-bound): algorithmic Gaussian
-             evaluations (one ex2 each) per launch / its mean launch time
-             (CUDA events around each launch on its stream), against the
-             MUFU.EX2 throughput measured on this GPU in this run.
+             uploads the points from pinned memory and receives the whole
+             graph (upper CSR v, w, row_ptr + degrees) in pinned host
+             buffers (fsgg_build_similarity_graph_into).
+* roofline   the dominant kernel: for low d the symmetric root tile kernel
+             (MUFU-bound): Gaussian evaluations (one ex2 each) per launch /
+             its mean launch time (CUDA events around the launch on its
+             stream), against the MUFU.EX2 throughput measured on this GPU in
+             this run; for d >= 64 the tensor-core root launch against the
+             TF32 peak.
 * cpu_baseline  the reference's own code (oracle/_ref, compiled in place from
              /root/reference) on the host cores, default (auto = FGT for this
              config) backend, bounded sample: a contiguous block of queries.
