@@ -248,12 +248,14 @@ __device__ __forceinline__ void sym_tile_body(
   float2 racc[kSymRows / 2];
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) racc[p] = make_float2(0.f, 0.f);
-  // warp w: sources [64 w, 64 w + 64) in batches of 16 (16 column partials
-  // per lane instead of 32 keep the kernel at 6 CTAs per SM)
-  for (uint32_t jb = w * 64; jb < w * 64 + 64 && jb < nj; jb += 16) {
-    float c[16];  // this lane's 8-row partial of each source's column sum
+  // warp w: sources [64 w, 64 w + 64) in batches of 8: 8 column partials
+  // per lane (not 32) keep the kernel at 62 registers, 8 CTAs per SM — the
+  // extra shuffles cost less than the occupancy buys (32: 30.0 ms, 16: 29.6,
+  // 8: 28.9, 4: 30.1 on C3)
+  for (uint32_t jb = w * 64; jb < w * 64 + 64 && jb < nj; jb += 8) {
+    float c[8];  // this lane's 8-row partial of each source's column sum
 #pragma unroll
-    for (int jj = 0; jj < 16; ++jj) {
+    for (int jj = 0; jj < 8; ++jj) {
       const float2* x = sx + (jb + jj) * D;
       float2 es = make_float2(0.f, 0.f);
 #pragma unroll
@@ -268,13 +270,15 @@ __device__ __forceinline__ void sym_tile_body(
       }
       c[jj] = es.x + es.y;
     }
-    // fold the lane halves, then a butterfly transpose-reduction over 16
-    // lanes: afterwards lane l holds the column sum of source jb + (l & 15)
-    // over all 32 lanes (31 shuffles for 16 sources)
+    // fold lanes l ^ 16 and l ^ 8, then a butterfly transpose-reduction over
+    // 8 lanes: afterwards lane l holds the column sum of source jb + (l & 7)
+    // over all 32 lanes (23 shuffles for 8 sources)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
+    for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
 #pragma unroll
-    for (int st = 8; st >= 1; st >>= 1) {
+    for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 8);
+#pragma unroll
+    for (int st = 4; st >= 1; st >>= 1) {
       const bool up = (lane & st) != 0;
 #pragma unroll
       for (int i = 0; i < st; ++i) {
@@ -283,7 +287,7 @@ __device__ __forceinline__ void sym_tile_body(
         c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
       }
     }
-    if (lane < 16 && jb + lane < nj) colv[jb + lane] = c[0];
+    if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
   }
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) {
