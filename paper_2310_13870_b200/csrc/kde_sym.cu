@@ -332,7 +332,7 @@ __device__ __forceinline__ void sym_tile_body(
 // The kernel for a shard's own tiles (80 registers at d = 2, 6 CTAs per SM)
 // and the one for owner-mode cross-shard tiles (one side exported).
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(ROWS * 16)
+__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? 4 : 0)
     sym_tile_kernel(const float* __restrict__ pts, float cs,
                     const SymTile* __restrict__ tiles,
                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(ROWS * 16)
                                      performed, records);
 }
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(ROWS * 16)
+__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? 4 : 0)
     sym_tile_own_kernel(const float* __restrict__ pts, float cs,
                         const SymTile* __restrict__ tiles,
                         const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
