@@ -71,8 +71,10 @@ __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_
   return d;
 }
 
+// d <= 2: capped at 40 registers (12 CTAs per SM; a few spills) — the
+// kernel is issue/latency-bound and the extra warps measured 6% faster
 template <int D, int FAM>
-__global__ void __launch_bounds__(kWalkThreads)
+__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
     walk_kernel(const float* __restrict__ pts, uint32_t W, const uint32_t* __restrict__ wq,
                 const uint32_t* __restrict__ wh, const float* __restrict__ welm,
                 const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
