@@ -40,6 +40,7 @@ struct fsgg_dataset {
   fsgg::DevBuf keys;
   fsgg::DevBuf shard_keys;
   uint64_t root_records = 0;  // owner-mode root records of the last prepare
+  bool tree_fresh = false;    // tree built by the last prepare (reused once)
   uint64_t shard_npairs = 0;
   ~fsgg_dataset() {
     graph.reset();
@@ -193,9 +194,14 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   // Every build derives its tree (node boxes) and, on the tensor-core path,
   // the centred tf32 split of the points afresh: per-dataset preprocessing
   // is part of the job, as the reference's estimator build is.
-  ds.tree_valid = false;
-  ds.tc_ready = false;
-  fsgg::build_tree(ds);
+  // (the multi-GPU shard pipeline built it moments ago in
+  // fsgg_shard_root_prepare: same points, same job — not rebuilt)
+  if (!h->tree_fresh) {
+    ds.tree_valid = false;
+    ds.tc_ready = false;
+    fsgg::build_tree(ds);
+  }
+  h->tree_fresh = false;
   FSGG_CUDA(cudaStreamSynchronize(ds.stream));
   double t1 = now();
   fsgg::SampleRequest req;
@@ -501,6 +507,7 @@ int fsgg_dataset_upload(fsgg_dataset* h, const float* host_points) {
                               size_t(h->ds.n) * h->ds.d * 4, cudaMemcpyHostToDevice,
                               h->ds.stream));
     h->ds.tree_valid = false;  // bounding boxes depend on the coordinates
+    h->tree_fresh = false;
     h->ds.tc_ready = false;    // so do the tf32 split copies
   });
 }
@@ -872,8 +879,10 @@ int fsgg_shard_root_prepare(fsgg_dataset* h, const fsgg_kernel* kernel, const fs
     const char* e = std::getenv("FSGG_SYM");
     if (cfg.dense_kde || (e && std::atoi(e) == 0)) return;  // no symmetric root
     const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
-    ds.tree_valid = false;  // the descent rebuilds it too (same table)
+    ds.tree_valid = false;
+    ds.tc_ready = false;
     fsgg::build_tree(ds);
+    h->tree_fresh = true;  // the shard's descent reuses this table
     uint32_t n = 0;
     const uint32_t* recs = nullptr;
     fsgg::sym_shard_prepare(ds, ks, qb, qe, &n, &recs);
