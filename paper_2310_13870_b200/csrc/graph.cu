@@ -96,7 +96,7 @@ __global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64
                              uint32_t* __restrict__ u, uint32_t* __restrict__ v,
                              double* __restrict__ w, EdgeEstimateDev* est,
                              unsigned char* __restrict__ keep,
-                             unsigned long long* __restrict__ dropped) {
+                             unsigned long long* __restrict__ dropped, int write_v) {
   __shared__ unsigned long long red[8];
   const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   unsigned long long drop = 0;
@@ -111,7 +111,7 @@ __global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64
     const double pj = fmin(__ddiv_rn(__dmul_rn(L, k), gj), 1.0);
     const double ph = __dsub_rn(__dadd_rn(pi, pj), __dmul_rn(pi, pj));
     u[e] = i;
-    v[e] = j;
+    if (write_v) v[e] = j;
     w[e] = __ddiv_rn(k, ph);
     if (est) est[e] = EdgeEstimateDev{i, j, k, gi, gj, pi, pj, ph};
   }
@@ -123,6 +123,14 @@ __global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64
     for (uint32_t k = 0; k < blockDim.x / 32; ++k) t += red[k];
     if (t) atomicAdd(dropped, t);
   }
+}
+
+// v of every edge from the sorted unique public keys (streamed output: its
+// copy to the host can start before the weights exist).
+__global__ void keys_to_v_kernel(const unsigned long long* __restrict__ keys, uint64_t m,
+                                 uint32_t* __restrict__ v) {
+  const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (e < m) v[e] = uint32_t(keys[e]);
 }
 
 // row_ptr[x] = first edge index with key-row >= x (keys sorted).
@@ -306,6 +314,31 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
     out.w.ensure(mm0 * 8, s);
     if (want_estimates) out.est.ensure(mm0 * sizeof(EdgeEstimateDev), s);
   }
+  // streamed host output (HostSink): each array's device-to-host copy runs
+  // on its own stream as soon as the array is final — v right away (it is
+  // the keys' low word), w after the weights, row_ptr and degrees after
+  // theirs — overlapping the rest of the finish
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  auto after = [&](void* dst, const void* src, size_t bytes) {
+    if (!dst || !bytes) return;
+    FSGG_CUDA(cudaEventRecord(ev, s));
+    FSGG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+    FSGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
+  };
+  const bool early_v = sink && sink->v && m && m <= sink->capacity;
+  if (sink) {
+    if (m > sink->capacity) throw ConfigError("host output capacity below the edge count");
+    FSGG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    FSGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (early_v) {
+      keys_to_v_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(keys.as<unsigned long long>(), m,
+                                                            out.v.as<uint32_t>());
+      FSGG_LAUNCH_CHECK();
+      ds.launches++;
+      after(sink->v, out.v.as<void>(), m * 4);
+    }
+  }
   if (m) {
     DevBuf& keep = ds.buf("g.keep", m);
     FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
@@ -313,7 +346,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
         keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma, double(rounds), g_full,
         out.u.as<uint32_t>(), out.v.as<uint32_t>(), out.w.as<double>(),
         want_estimates ? out.est.as<EdgeEstimateDev>() : nullptr, keep.as<unsigned char>(),
-        cnt.as<unsigned long long>());
+        cnt.as<unsigned long long>(), early_v ? 0 : 1);
     FSGG_LAUNCH_CHECK();
     ds.launches++;
     unsigned long long dropped = 0;
@@ -358,21 +391,10 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   out.m = m;
   const uint64_t mm = std::max<uint64_t>(m, 1);
 
-  // streamed host output: v and w are final here; their copies overlap the
-  // CSR, the transposed sort and the degrees below
-  cudaStream_t cs = nullptr;
-  cudaEvent_t ev = nullptr;
-  auto after = [&](void* dst, const void* src, size_t bytes) {
-    if (!dst || !bytes) return;
-    FSGG_CUDA(cudaEventRecord(ev, s));
-    FSGG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-    FSGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
-  };
   if (sink) {
-    if (m > sink->capacity) throw ConfigError("host output capacity below the edge count");
-    FSGG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    FSGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    after(sink->v, out.v.as<void>(), m * 4);
+    // dropped underflow pairs compacted v: copy it again (after the first
+    // copy on the same stream); the weights are final here
+    if (!early_v || out.underflow) after(sink->v, out.v.as<void>(), m * 4);
     after(sink->w, out.w.as<void>(), m * 8);
   }
 
