@@ -115,6 +115,20 @@ struct Dataset {
     return b;
   }
   std::unique_ptr<KdeWorkspace> kde_ws;
+  // Pinned host words for the per-level counter readbacks: a D2H copy into
+  // pageable memory is staged by the driver and costs several microseconds
+  // more per level than a DMA straight into page-locked memory.
+  struct PinnedWords {
+    unsigned long long* p = nullptr;
+    ~PinnedWords() {
+      if (p) cudaFreeHost(p);
+    }
+  } pinned;
+  unsigned long long* host_words() {
+    if (!pinned.p) FSGG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pinned.p), 64 * 8,
+                                           cudaHostAllocDefault));
+    return pinned.p;
+  }
   // tensor-core path (kde_tc.cu): split tf32 hi/lo copies + tensor maps
   bool tc_ready = false;
   alignas(64) unsigned char tc_blob[576];

@@ -825,11 +825,12 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   ws.cub_tmp.ensure(tmp_bytes, s);
   FSGG_CUDA(cub::DeviceScan::ExclusiveSum(ws.cub_tmp.as<void>(), tmp_bytes, nb,
                                           nb, G + 1, s));
-  uint32_t total_blocks = 0;
-  unsigned long long ev = 0;
-  FSGG_CUDA(cudaMemcpyAsync(&total_blocks, nb + G, 4, cudaMemcpyDeviceToHost, s));
-  FSGG_CUDA(cudaMemcpyAsync(&ev, d_evals, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long* hw = ds.host_words();
+  FSGG_CUDA(cudaMemcpyAsync(hw, d_evals, 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(hw + 1, nb + G, 4, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
+  const unsigned long long ev = hw[0];
+  const uint32_t total_blocks = *reinterpret_cast<const uint32_t*>(hw + 1);
   ds.launches += 1;
   stats.evals += ev;
   stats.performed += ev;

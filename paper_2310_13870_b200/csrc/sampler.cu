@@ -1396,9 +1396,10 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
         smax_level >= kTieBatchMinNode) {
       // high d: batched fp64 recomputation (tie_batch_kernel), then reroute
-      uint32_t cnt = 0;
-      FSGG_CUDA(cudaMemcpyAsync(&cnt, vcount, 4, cudaMemcpyDeviceToHost, s));
+      uint32_t* hc = reinterpret_cast<uint32_t*>(ds.host_words());
+      FSGG_CUDA(cudaMemcpyAsync(hc, vcount, 4, cudaMemcpyDeviceToHost, s));
       FSGG_CUDA(cudaStreamSynchronize(s));
+      const uint32_t cnt = *hc;
       if (cnt > 0) {
         batched_tie_sums(ds, ks, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
                          vlist.as<uint32_t>(), cnt, g1.as<double>(), g2.as<double>());
@@ -1487,7 +1488,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     ds.launches += 3;
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[3], s));
-    unsigned long long host[4];
+    unsigned long long* host = ds.host_words();
     FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 24, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaMemcpyAsync(host + 3, P.as<unsigned long long>() + E, 8,
                               cudaMemcpyDeviceToHost, s));
@@ -1517,7 +1518,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
   }
   {
     // reference-equivalent work served by lookups; direct-level evaluations
-    unsigned long long ev[2] = {0, 0};
+    unsigned long long* ev = ds.host_words();
     FSGG_CUDA(cudaMemcpyAsync(&ev[0], lookup_evals.as<void>(), 8, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaMemcpyAsync(&ev[1], ds.kde_ws->direct_evals.as<void>(), 8,
                               cudaMemcpyDeviceToHost, s));
@@ -1526,9 +1527,10 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
     out.kde.performed += ev[1];
   }
   if (walk_on) {
-    uint32_t W = 0;
-    FSGG_CUDA(cudaMemcpyAsync(&W, wcount.as<void>(), 4, cudaMemcpyDeviceToHost, s));
+    uint32_t* hw = reinterpret_cast<uint32_t*>(ds.host_words());
+    FSGG_CUDA(cudaMemcpyAsync(hw, wcount.as<void>(), 4, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
+    const uint32_t W = *hw;
     if (W > 0) {
       const auto w0 = std::chrono::steady_clock::now();
       DevBuf& st = ds.buf("s.walk_stats", 5 * 64 * 8);
