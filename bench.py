@@ -127,109 +127,229 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- reference ----
-def reference_sample(points64, sigma, rounds, seed, target_s, threads):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_inputs(cfg: str):
+    """(fp32-rounded fp64 points, sigma, rounds, source) for the reference arm.
+
+    C1-C3 come from the REFERENCE's own generators (oracle/_ref make_blobs /
+    make_moons, proj/src/datasets.cpp:32-124), bit-identical to the points
+    the GPU arm builds from (tests/test_oracle.py pins them), so this arm never
+    loads libfsgg.so. C4/C5 are harness-defined (the reference has no
+    generator for them): their points come from the package's host generator."""
+    from oracle.pyoracle import Ref
+    if cfg in ("C1", "C2", "C3") and Ref.available:
+        ref = Ref()
+        if cfg == "C1":
+            p, _ = ref.make_blobs(2000, [[-2.0, 0.0], [2.0, 0.0]], 0.5, 1)
+            sigma, L = 0.5, 32
+        elif cfg == "C2":
+            p, _ = ref.make_moons(100_000, 0.05, 1)
+            sigma, L = 0.1, 64
+        else:
+            p, _ = ref.make_moons(1_000_000, 0.05, 1)
+            sigma, L = 0.05, 64
+        return p.astype(np.float32).astype(np.float64), sigma, L, "reference make_moons/make_blobs"
+    from paper_2310_13870_b200 import datasets
+    w = datasets.config(cfg)
+    return (w.points.astype(np.float64), w.sigma, w.rounds,
+            "harness generator (libfsgg.so host code; no reference generator for this config)")
+
+
+def bench_config(cfg: str, n: int, d: int, sigma: float, L: int, world: int) -> dict:
+    """The ONE config dict both arms print (same keys and values)."""
+    return {"workload": f"{cfg}: {CONFIG_DOC[cfg]}", "n": n, "d": d, "sigma": sigma,
+            "samples_per_point": L, "seed": 1, "rng": "reference (splitmix64)",
+            "parallelism": f"query shards x{world}",
+            "l2": "GPU arm: flushed (512 MiB write) between steps"}
+
+
+class RefSample:
     """The reference's own CPU path on a bounded sample of the workload.
 
-    Builds the reference's default estimator (make_estimator, auto backend:
-    FGT for d<=3, n>=4096, else exact; proj/src/kde.cpp:104-129) once, then
-    times sample_neighbors_counted (proj/src/sampler.cpp:77) plus the degree
-    KDE for a contiguous block of queries (their descent is exactly the one
-    the full job performs for them). The block size is calibrated to
-    ~target_s of CPU time."""
-    from oracle.pyoracle import Oracle, Ref
-    n = points64.shape[0]
-    if Ref.available:
-        ref = Ref()
-        ref.set_threads(threads)
+    Builds the reference's estimator (make_estimator, proj/src/kde.cpp:104-129;
+    backend 2 = auto: FGT for d <= 3, n >= 4096, else exact) once, then runs
+    sample_neighbors_counted (proj/src/sampler.cpp:77) plus the degree KDE
+    (sparsifier.cpp:74-75) for a contiguous block of queries: their descent is
+    exactly the one the full job performs for them. The block is calibrated
+    to ~target_s of CPU time. Falls back to the C restatement (exact, single
+    thread) when oracle/_ref was not built."""
+
+    def __init__(self, points64, sigma, rounds, seed, target_s, threads, backend=2):
+        from oracle.pyoracle import Oracle, Ref
+        self.n = points64.shape[0]
+        self.rounds, self.seed = rounds, seed
+        self.threads = threads
+        self.points64, self.sigma = points64, sigma
+        if Ref.available:
+            self.ref = Ref()
+            self.ref.set_threads(threads)
+            t0 = time.perf_counter()
+            self.est = self.ref.estimator(points64, 0, sigma, backend)
+            self.t_build = time.perf_counter() - t0
+            self.kind, self.backend = "reference", self.est.backend
+        else:
+            self.ref, self.est = None, None
+            self.orc = Oracle()
+            self.t_build, self.kind, self.backend, self.threads = 0.0, "port", "exact (oracle restatement)", 1
+        self.start = self.n // 4
+        s = 64
+        while True:  # calibrate: fixed per-call overheads make tiny probes pessimistic
+            t = sum(self.run(np.arange(self.start, self.start + s, dtype=np.uint32)))
+            t = max(t, 1e-6)
+            if t >= target_s / 4 or s >= self.n - self.start:
+                break
+            s = int(min(self.n - self.start, s * min(8.0, 0.5 * target_s / t)))
+        self.block = int(min(self.n - self.start, max(64, s * target_s / t)))
+        self.qs = np.arange(self.start, self.start + self.block, dtype=np.uint32)
+
+    def run(self, qs=None):
+        """(sampling seconds, degree-KDE seconds) for one pass over the block."""
+        qs = self.qs if qs is None else qs
         t0 = time.perf_counter()
-        est = ref.estimator(points64, 0, sigma, 2)
-        t_build = time.perf_counter() - t0
-        kind, backend = "reference", est.backend
-
-        def run(qs):
-            est.sample_counted(qs, rounds, seed)
-            est.eval(0, n, qs)
-    else:  # C restatement (exact backend), single thread
-        orc = Oracle()
-        t_build, kind, backend, threads = 0.0, "port", "exact (oracle restatement)", 1
-
-        def run(qs):
-            orc.sample_counted(points64, qs, rounds, seed, sigma)
-            orc.kde_exact(points64, 0, n, qs, sigma)
-    start = n // 4
-    s = 64
-    while True:  # calibrate: fixed per-call overheads make tiny probes pessimistic
-        t0 = time.perf_counter()
-        run(np.arange(start, start + s, dtype=np.uint32))
-        t = max(time.perf_counter() - t0, 1e-6)
-        if t >= target_s / 4 or s >= n - start:
-            break
-        s = int(min(n - start, s * min(8.0, 0.5 * target_s / t)))
-    s = int(min(n - start, max(64, s * target_s / t)))
-    return dict(run=run, start=start, block=s, t_build=t_build, kind=kind, backend=backend,
-                threads=threads)
+        if self.est is not None:
+            self.est.sample_counted(qs, self.rounds, self.seed)
+            t1 = time.perf_counter()
+            self.est.eval(0, self.n, qs)
+        else:
+            self.orc.sample_counted(self.points64, qs, self.rounds, self.seed, self.sigma)
+            t1 = time.perf_counter()
+            self.orc.kde_exact(self.points64, 0, self.n, qs, self.sigma)
+        return t1 - t0, time.perf_counter() - t1
 
 
-def cpu_baseline(points64, sigma, rounds, seed, target_s):
+def reduced_full_build(points64_fn, sigma, rounds, threads):
+    """BuildReport phases (proj/src/sparsifier.cpp:123-140) of one complete
+    reference build_similarity_graph at a reduced n (default backend)."""
+    from oracle.pyoracle import Ref
+    if not Ref.available:
+        return None
+    ref = Ref()
+    ref.set_threads(threads)
+    p64, label = points64_fn()
+    g = ref.build_graph(p64, sigma, rounds, seed=1, backend=2, want_estimates=False)
+    rep = g["report"]
+    keys = ("estimator_build_seconds", "sampling_seconds", "degree_kde_seconds",
+            "weighting_seconds", "total_seconds")
+    return {"points": label, "n": int(p64.shape[0]), "backend": rep["backend"],
+            "edge_count": int(rep["edge_count"]),
+            "phases": {k: rep[k] for k in keys},
+            "sampled_edges_per_s": p64.shape[0] * rounds / max(rep["total_seconds"], 1e-9)}
+
+
+def cpu_baseline(cfg, points64, sigma, rounds, seed, target_s):
     threads = os.cpu_count() or 1
-    rs = reference_sample(points64, sigma, rounds, seed, target_s, threads)
-    qs = np.arange(rs["start"], rs["start"] + rs["block"], dtype=np.uint32)
-    t0 = time.perf_counter()
-    rs["run"](qs)
-    dt = time.perf_counter() - t0
+    rs = RefSample(points64, sigma, rounds, seed, target_s, threads)
+    ts, tk = rs.run()
+    dt = ts + tk
     n = points64.shape[0]
-    value = rs["block"] * rounds / dt
-    return {
-        "value": value, "unit": "sampled edges/s", "cores": rs["threads"], "kind": rs["kind"],
-        "sample": (f"{rs['backend']} backend; sample_neighbors_counted + degree KDE for a "
-                   f"contiguous block of {rs['block']} of {n} queries (L={rounds}) on the full "
-                   f"point set; estimator build {rs['t_build']:.2f}s excluded"),
-        "sample_seconds": dt, "estimator_build_seconds": rs["t_build"],
-        "extrapolated_full_job_seconds": rs["t_build"] + dt * n / rs["block"],
+    value = rs.block * rounds / dt
+    out = {
+        "value": value, "unit": "sampled edges/s", "cores": rs.threads, "kind": rs.kind,
+        "cpu_model": cpu_model(),
+        "sample": (f"{rs.backend} backend; sample_neighbors_counted + degree KDE for a "
+                   f"contiguous block of {rs.block} of {n} queries (L={rounds}) on the full "
+                   f"point set; estimator build {rs.t_build:.2f}s excluded"),
+        "sample_seconds": dt, "estimator_build_seconds": rs.t_build,
+        "phases_on_sample": {"estimator_build_seconds": rs.t_build, "sampling_seconds": ts,
+                             "degree_kde_seconds": tk},
+        "extrapolated_full_job_seconds": rs.t_build + dt * n / rs.block,
     }
+    if rs.kind == "reference":
+        # the exact backend (the one the device path reproduces) on a smaller block
+        try:
+            ex = RefSample(points64, sigma, rounds, seed, target_s / 3, threads, backend=0)
+            es, ek = ex.run()
+            out["exact_backend"] = {
+                "value": ex.block * rounds / (es + ek), "unit": "sampled edges/s",
+                "sample": f"exact backend; contiguous block of {ex.block} queries",
+                "sample_seconds": es + ek,
+                "extrapolated_full_job_seconds": (es + ek) * n / ex.block}
+        except Exception as exc:  # reported, never fatal
+            out["exact_backend"] = {"error": repr(exc)}
+        if cfg in ("C2", "C3"):
+            try:
+                def pts():
+                    from oracle.pyoracle import Ref
+                    p, _ = Ref().make_moons(20_000, 0.05, 1)
+                    return p.astype(np.float32).astype(np.float64), "reference make_moons(20000)"
+                out["build_report_reduced"] = reduced_full_build(pts, sigma, rounds, threads)
+            except Exception as exc:
+                out["build_report_reduced"] = {"error": repr(exc)}
+    return out
 
 
 def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU code (oracle/_ref, compiled
+    in place from /root/reference by oracle/Makefile) on the host cores. Never
+    loads libfsgg.so for C1-C3."""
     if rank != 0:
         return
-    from paper_2310_13870_b200 import datasets
-    w = datasets.config(args.config)
-    p64 = w.points.astype(np.float64)
+    p64, sigma, L, source = reference_inputs(args.config)
+    n, d = p64.shape
     threads = os.cpu_count() or 1
-    rs = reference_sample(p64, w.sigma, w.rounds, 1, 6.0, threads)
-    qs = np.arange(rs["start"], rs["start"] + rs["block"], dtype=np.uint32)
+    rs = RefSample(p64, sigma, L, 1, 6.0, threads)
     for _ in range(args.warmup):
-        rs["run"](qs)
-    times = []
+        rs.run()
+    times, ts_sum, tk_sum = [], 0.0, 0.0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        rs["run"](qs)
-        times.append(time.perf_counter() - t0)
+        ts, tk = rs.run()
+        times.append(ts + tk)
+        ts_sum += ts
+        tk_sum += tk
     step = float(np.mean(times))
-    value = rs["block"] * w.rounds / step
-    sample = (f"{rs['backend']} backend; each step = sample_neighbors_counted + degree KDE "
-              f"for a contiguous block of {rs['block']} of {w.n} queries (L={w.rounds}); "
-              f"estimator build {rs['t_build']:.2f}s once, untimed")
+    value = rs.block * L / step
+    sample = (f"{rs.backend} backend; each step = sample_neighbors_counted + degree KDE "
+              f"for a contiguous block of {rs.block} of {n} queries (L={L}); "
+              f"estimator build {rs.t_build:.2f}s once, untimed; points: {source}")
     print(json.dumps({
         "impl": "reference", "metric": metric_name(args.config),
         "value": value, "unit": "sampled edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {CONFIG_DOC[args.config]}",
-                   "query_block": rs["block"], "backend": rs["backend"]},
-        "cpu_baseline": {"value": value, "unit": "sampled edges/s", "cores": rs["threads"],
-                         "kind": rs["kind"], "sample": sample},
+        "config": bench_config(args.config, n, d, sigma, L, world),
+        "cpu_baseline": {"value": value, "unit": "sampled edges/s", "cores": rs.threads,
+                         "kind": rs.kind, "cpu_model": cpu_model(), "sample": sample,
+                         "phases_per_step": {"sampling_seconds": ts_sum / args.steps,
+                                             "degree_kde_seconds": tk_sum / args.steps},
+                         "estimator_build_seconds": rs.t_build,
+                         "extrapolated_full_job_seconds": rs.t_build + step * n / rs.block},
         "e2e": {"value": value, "unit": "sampled edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
+def relaunch_under_torchrun(args):
+    """--gpus N without a torchrun environment: re-exec as N ranks (one per
+    GPU, rendezvous on 127.0.0.1), as the driver's own launch would."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 # ------------------------------------------------------------------ ours ----
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
@@ -461,7 +581,8 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(w.points.astype(np.float64), w.sigma, L, 1, args.cpu_seconds)
+            cpu = cpu_baseline(args.config, w.points.astype(np.float64), w.sigma, L, 1,
+                               args.cpu_seconds)
         except Exception as exc:  # reported, never fatal
             cpu = {"value": None, "error": repr(exc)}
     line = {
@@ -469,9 +590,7 @@ def main():
         "value": value, "unit": "sampled edges/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_s * 1e3 / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {CONFIG_DOC[args.config]}", "n": n, "d": w.d,
-                   "sigma": w.sigma, "samples_per_point": L, "rng": "reference (splitmix64)",
-                   "parallelism": f"query shards x{world}", "l2": "flushed (512 MiB) between steps"},
+        "config": bench_config(args.config, n, w.d, w.sigma, L, world),
         "kernel_evals_per_s": evals / total_s, "kernel_evals_per_step": evals / K / max(world, 1),
         "kernel_evals_performed_per_step": performed / K,
         "kernel_evals_note": ("reference-equivalent Gaussian evaluations (2.38 n^2 sampler + n^2 "

@@ -70,9 +70,12 @@ typedef struct fsgg_config {
   uint32_t query_begin;
   uint32_t query_end;
   /* 0 (default): certified pruning — a source sub-chunk whose bounding-box
-   * bound is below 2^-80 of the entry's node mass is skipped (total skipped
-   * mass < 2^-60 of the node mass; routing decisions unchanged).
-   * 1: evaluate every kernel term (dense). */
+   * bound is below 2^-48 of half the entry's node mass is skipped
+   * (engine.cuh kPruneBits); with at most 2^20 sub-chunks per node the
+   * skipped mass is below 2^-27 of the node mass, which the tie guard adds to
+   * its margin, so routing decisions are unchanged. Per child sum:
+   * |g - g_exact| <= (fp32 evaluation error) + 2^-27 * (node mass)
+   * (tests/test_gpu_node_sums.py). 1: evaluate every kernel term (dense). */
   int dense_kde;
 } fsgg_config;
 
@@ -196,8 +199,9 @@ int fsgg_build_similarity_graph_device(fsgg_dataset* ds,
                                        fsgg_report* report);
 
 /* fsg::build_similarity_graph into caller host buffers (pinned memory for
- * full speed): the upper CSR (v, w: `capacity` >= edge count entries, n*L
- * always suffices; row_ptr: n+1; degrees: n) is copied out array by array
+ * full speed): the upper CSR (v, w: `capacity` entries, at least the number
+ * of sampled unique pairs BEFORE underflow drops -- n*L always suffices --;
+ * row_ptr: n+1; degrees: n) is copied out array by array
  * while the rest of the graph is still being finished, so the transfer
  * overlaps the device work. Any buffer pointer may be NULL (not copied);
  * total_weight (nullable) receives the graph's total weight. Edge u of
@@ -330,6 +334,49 @@ int fsgg_sample_neighbors_counted(fsgg_dataset* ds, const fsgg_kernel* kernel,
                                   int dense_kde, uint32_t** triples,
                                   size_t* count, fsgg_sample_diag* diag);
 
+/* Same descent with options and a richer report (test / diagnostics
+ * entry point; the reference's closest equivalent is the recording
+ * KdeEstimator wrapper its tests put around ExactKdeEstimator::eval,
+ * proj/src/sampler.cpp:146-149 -> kde.cpp:38-49).
+ *
+ * record_sums = 1 exports, for every (node, query) entry of every level, the
+ * two child sums exactly as the level's KDE kernels produced them (symmetric
+ * root, root-row / block lookups, tiled or tensor-core passes, direct
+ * kernels), BEFORE the tie guard re-decides near-ties on fp64 sums. It forces
+ * the level-synchronous path (single-ticket walks off, which use the same
+ * direct_child_sums device function as the direct kernel). Records are
+ * malloc'd (free with fsgg_free); children of node [first, last) are
+ * [first, first + (last - first) / 2) and [that, last) (sampler.cpp:141,200);
+ * nodes of one point carry left = right = 0. */
+typedef struct fsgg_entry_record {
+  uint32_t level, query, first, last;
+  double left, right;
+} fsgg_entry_record;
+
+typedef struct fsgg_sample_options {
+  int rng_mode;      /* FSGG_RNG_REFERENCE | FSGG_RNG_PHILOX */
+  int dense_kde;     /* 1: no certified pruning */
+  int record_sums;   /* 1: export every entry's child sums (see above) */
+  int walks;         /* 0: no single-ticket walks (1 default) */
+} fsgg_sample_options;
+
+typedef struct fsgg_sample_report {
+  fsgg_sample_diag diag;
+  uint64_t kernel_evals;            /* reference-equivalent Gaussian evaluations */
+  uint64_t kernel_evals_performed;  /* evaluations executed on the device */
+  uint64_t root_evals_performed;    /* symmetric root pass (0: it did not run) */
+  uint64_t tie_verified;            /* entries re-decided on fp64 sums */
+  fsgg_entry_record* records;       /* record_sums only, else NULL */
+  size_t num_records;
+} fsgg_sample_report;
+
+void fsgg_sample_options_init(fsgg_sample_options* opt);
+int fsgg_sample_neighbors_counted_ex(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                                     const uint32_t* queries, size_t num_queries,
+                                     uint32_t rounds, uint64_t seed,
+                                     const fsgg_sample_options* opt, uint32_t** triples,
+                                     size_t* count, fsgg_sample_report* rep);
+
 /* fsg::KdeEstimator::eval (proj/include/fsg/kde.hpp:54-58, exact backend
  * proj/src/kde.cpp:57-71): out[t] = max(sum_{j in [first,last)} k(x_t, x_j),
  * 1e-300) for a non-empty range, 0 for an empty one. Host arrays. */
@@ -394,8 +441,10 @@ int fsgg_shard_export(fsgg_dataset* ds, uint64_t* pairs_device,
  *   fsgg_shard_root_receive(ds, recv, m)        store the m received records
  *   fsgg_sample_shard(ds, k, cfg, ...)          the descent, root tiles reused
  * Results are bit-identical to the 1-GPU build. prepare returns 0 records
- * (and the descent computes its root alone) when the root pass is not
- * symmetric for this data or the range is not block-aligned. Replaces no
+ * (and every rank's descent computes its root alone) when the root pass is
+ * not symmetric for this data -- a property of the dataset, so all ranks
+ * agree. A range that is not block-aligned is FSGG_ERR_CONFIG (a silent
+ * per-rank fallback would leave an aligned peer waiting for records). Replaces no
  * reference interface: the reference has no multi-device path
  * (SURVEY.md §2). */
 /* kernel may be NULL: equal block counts; else block-aligned bounds that

@@ -9,7 +9,8 @@ from .api import (BuildReport, Dataset, EigenOptions, EigenResult, KMeansOptions
                   RngMode, SampleDiagnostics, SparsifierConfig, WeightedGraph,
                   build_similarity_graph, build_similarity_graph_device, default_epsilon,
                   device_available, device_graph_to_host, exact_kde, load_csr, load_csv, make_estimator,
-                  read_edge_list, sample_neighbors, sample_neighbors_counted, save_csv)
+                  read_edge_list, sample_neighbors, sample_neighbors_counted,
+                  sample_neighbors_counted_ex, SampleReport, RECORD_DTYPE, save_csv)
 from .errors import (ConfigError, DeviceError, Error, InvalidConfig, IoError,
                      LengthMismatch, NumericError, TooFewPoints)
 
@@ -19,7 +20,8 @@ __all__ = [
     "BuildReport", "Dataset", "Kernel", "KernelFamily", "KdeEstimator", "LogBase", "RngMode",
     "SampleDiagnostics", "SparsifierConfig", "WeightedGraph", "build_similarity_graph",
     "build_similarity_graph_device", "default_epsilon", "device_available", "exact_kde",
-    "load_csr", "load_csv", "save_csv", "make_estimator", "read_edge_list", "sample_neighbors", "sample_neighbors_counted", "ConfigError",
+    "load_csr", "load_csv", "save_csv", "make_estimator", "read_edge_list", "sample_neighbors", "sample_neighbors_counted",
+    "sample_neighbors_counted_ex", "SampleReport", "RECORD_DTYPE", "ConfigError",
     "DeviceError", "Error", "InvalidConfig", "IoError", "LengthMismatch", "NumericError",
     "TooFewPoints",
 ]

@@ -98,6 +98,23 @@ class fsgg_sample_diag(C.Structure):
                 ("tickets_per_level", C.c_uint64 * 64), ("degenerate_draws", C.c_uint64)]
 
 
+class fsgg_entry_record(C.Structure):
+    _fields_ = [("level", C.c_uint32), ("query", C.c_uint32), ("first", C.c_uint32),
+                ("last", C.c_uint32), ("left", C.c_double), ("right", C.c_double)]
+
+
+class fsgg_sample_options(C.Structure):
+    _fields_ = [("rng_mode", C.c_int), ("dense_kde", C.c_int), ("record_sums", C.c_int),
+                ("walks", C.c_int)]
+
+
+class fsgg_sample_report(C.Structure):
+    _fields_ = [("diag", fsgg_sample_diag), ("kernel_evals", C.c_uint64),
+                ("kernel_evals_performed", C.c_uint64), ("root_evals_performed", C.c_uint64),
+                ("tie_verified", C.c_uint64), ("records", C.c_void_p),
+                ("num_records", C.c_size_t)]
+
+
 class fsgg_shard(C.Structure):
     _fields_ = [("query_begin", C.c_uint32), ("query_end", C.c_uint32),
                 ("rounds", C.c_uint32), ("num_pairs", C.c_uint64), ("pairs", C.c_void_p),
@@ -175,6 +192,12 @@ _SIGS = {
                                                 C.c_uint32, C.c_uint64, C.c_int, C.c_int,
                                                 C.POINTER(_P), C.POINTER(C.c_size_t),
                                                 C.POINTER(fsgg_sample_diag)]),
+    "fsgg_sample_options_init": (None, [C.POINTER(fsgg_sample_options)]),
+    "fsgg_sample_neighbors_counted_ex": (C.c_int, [_P, C.POINTER(fsgg_kernel), _P, C.c_size_t,
+                                                   C.c_uint32, C.c_uint64,
+                                                   C.POINTER(fsgg_sample_options),
+                                                   C.POINTER(_P), C.POINTER(C.c_size_t),
+                                                   C.POINTER(fsgg_sample_report)]),
     "fsgg_kde_eval": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.c_uint32, C.c_uint32, _P,
                                 C.c_size_t, _P]),
     "fsgg_make_moons": (C.c_int, [C.c_uint32, C.c_double, C.c_uint64, _P, _P]),

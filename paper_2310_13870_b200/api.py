@@ -138,8 +138,12 @@ class Dataset:
                 raise InvalidConfig("device points must be a 2-D float32 tensor")
             pts = points.contiguous()
             n, d = pts.shape
+            # the library copies on its own stream, which does not wait for
+            # torch's: finish whatever is still writing the tensor first
+            torch.cuda.current_stream(pts.device).synchronize()
+            device = pts.device.index if pts.device.index is not None else torch.cuda.current_device()
             N.check(lib.fsgg_dataset_create(C.c_void_p(pts.data_ptr()), n, d, 1,
-                                            pts.device.index or 0, C.byref(h)))
+                                            device, C.byref(h)))
         else:
             arr = np.asarray(points)
             if arr.ndim != 2:
@@ -532,6 +536,65 @@ def sample_neighbors_counted(ds: Dataset, kernel: Kernel, queries, rounds: int, 
                               int(diag.degenerate_draws))
         return tri, d
     return tri
+
+
+@dataclass
+class SampleReport:
+    """fsgg_sample_report: diagnostics, evaluation counters and (with
+    ``record_sums``) every entry's child sums as the level kernels produced
+    them. ``records`` is a numpy structured array with fields level, query,
+    first, last, left, right (children [first, mid) and [mid, last),
+    mid = first + (last - first) // 2)."""
+
+    diagnostics: SampleDiagnostics
+    kernel_evals: int
+    kernel_evals_performed: int
+    root_evals_performed: int
+    tie_verified: int
+    records: np.ndarray | None
+
+
+RECORD_DTYPE = np.dtype([("level", "<u4"), ("query", "<u4"), ("first", "<u4"), ("last", "<u4"),
+                         ("left", "<f8"), ("right", "<f8")])
+
+
+def sample_neighbors_counted_ex(ds: Dataset, kernel: Kernel, queries, rounds: int, seed: int,
+                                rng_mode: RngMode = RngMode.reference, dense_kde: bool = False,
+                                record_sums: bool = False, walks: bool = True):
+    """fsgg_sample_neighbors_counted_ex: the descent with options; returns
+    (triples, SampleReport)."""
+    q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64))
+    if q.size and (q.min() < 0):
+        raise InvalidConfig("query index out of range")
+    q = q.astype(np.uint32)
+    k = kernel._c()
+    opt = N.fsgg_sample_options()
+    lib = N.lib()
+    lib.fsgg_sample_options_init(C.byref(opt))
+    opt.rng_mode = int(rng_mode)
+    opt.dense_kde = int(dense_kde)
+    opt.record_sums = int(record_sums)
+    opt.walks = int(walks)
+    out = C.c_void_p()
+    cnt = C.c_size_t()
+    rep = N.fsgg_sample_report()
+    N.check(lib.fsgg_sample_neighbors_counted_ex(ds._h, C.byref(k), q.ctypes.data_as(C.c_void_p),
+                                                 q.size, rounds, seed, C.byref(opt), C.byref(out),
+                                                 C.byref(cnt), C.byref(rep)))
+    m = cnt.value
+    tri = _as_numpy(out, 3 * m, C.c_uint32, np.uint32).reshape(m, 3)
+    lib.fsgg_free(out)
+    recs = None
+    if rep.records:
+        nr = rep.num_records
+        buf = (C.c_char * (nr * RECORD_DTYPE.itemsize)).from_address(rep.records)
+        recs = np.frombuffer(bytes(buf), dtype=RECORD_DTYPE).copy()
+        lib.fsgg_free(C.c_void_p(rep.records))
+    d = rep.diag
+    diag = SampleDiagnostics(list(d.entries_per_level)[: d.nlevels],
+                             list(d.tickets_per_level)[: d.nlevels], int(d.degenerate_draws))
+    return tri, SampleReport(diag, int(rep.kernel_evals), int(rep.kernel_evals_performed),
+                             int(rep.root_evals_performed), int(rep.tie_verified), recs)
 
 
 def sample_neighbors(ds: Dataset, kernel: Kernel, queries, seed: int,

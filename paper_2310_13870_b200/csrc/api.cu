@@ -506,6 +506,7 @@ int fsgg_dataset_upload(fsgg_dataset* h, const float* host_points) {
     FSGG_CUDA(cudaMemcpyAsync(h->ds.pts.as<void>(), host_points,
                               size_t(h->ds.n) * h->ds.d * 4, cudaMemcpyHostToDevice,
                               h->ds.stream));
+    check_finite(h->ds);       // same validation as fsgg_dataset_create (dataset.cpp:19-21)
     h->ds.tree_valid = false;  // bounding boxes depend on the coordinates
     h->tree_fresh = false;
     h->ds.tc_ready = false;    // so do the tf32 split copies
@@ -727,11 +728,41 @@ int fsgg_graph_load_csr(const char* path, fsgg_graph* out) {
   return guarded([&] { fsgg::graph_load_csr(path, out); });
 }
 
+void fsgg_sample_options_init(fsgg_sample_options* opt) {
+  if (!opt) return;
+  opt->rng_mode = FSGG_RNG_REFERENCE;
+  opt->dense_kde = 0;
+  opt->record_sums = 0;
+  opt->walks = 1;
+}
+
 int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
                                   const uint32_t* queries, size_t num_queries,
                                   uint32_t rounds, uint64_t seed, int rng_mode,
                                   int dense_kde, uint32_t** triples, size_t* count,
                                   fsgg_sample_diag* diag) {
+  fsgg_sample_options opt;
+  fsgg_sample_options_init(&opt);
+  opt.rng_mode = rng_mode;
+  opt.dense_kde = dense_kde;
+  fsgg_sample_report rep;
+  const int rc = fsgg_sample_neighbors_counted_ex(h, kernel, queries, num_queries, rounds, seed,
+                                                  &opt, triples, count, diag ? &rep : nullptr);
+  if (rc == FSGG_OK && diag) *diag = rep.diag;
+  return rc;
+}
+
+int fsgg_sample_neighbors_counted_ex(fsgg_dataset* h, const fsgg_kernel* kernel,
+                                     const uint32_t* queries, size_t num_queries,
+                                     uint32_t rounds, uint64_t seed,
+                                     const fsgg_sample_options* opt, uint32_t** triples,
+                                     size_t* count, fsgg_sample_report* rep) {
+  fsgg_sample_options defaults;
+  fsgg_sample_options_init(&defaults);
+  if (!opt) opt = &defaults;
+  const int rng_mode = opt->rng_mode;
+  const int dense_kde = opt->dense_kde;
+  if (rep) std::memset(rep, 0, sizeof(*rep));
   return guarded([&] {
     activate(h);
     validate_kernel(kernel);
@@ -753,9 +784,13 @@ int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
       req.tickets.push_back(static_cast<uint32_t>(t));
       i = j;
     }
+    if (rng_mode != FSGG_RNG_REFERENCE && rng_mode != FSGG_RNG_PHILOX)
+      throw fsgg::ConfigError("unknown rng_mode");
     req.seed = seed;
     req.rng_mode = rng_mode;
     req.prune = dense_kde ? 0 : 1;
+    req.walk = opt->walks != 0;
+    req.record_sums = opt->record_sums != 0;
     std::vector<uint32_t> host;
     if (!h->sample) h->sample = std::make_unique<fsgg::SampleResult>();
     fsgg::SampleResult& res = *h->sample;
@@ -771,14 +806,27 @@ int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
     *triples = static_cast<uint32_t*>(std::malloc(std::max<size_t>(host.size(), 1) * 4));
     if (!*triples) throw std::bad_alloc();
     std::memcpy(*triples, host.data(), host.size() * 4);
-    if (diag) {
-      std::memset(diag, 0, sizeof(*diag));
+    if (rep) {
+      fsgg_sample_diag* diag = &rep->diag;
       diag->nlevels = static_cast<uint32_t>(std::min<size_t>(res.entries_per_level.size(), 64));
       for (uint32_t i = 0; i < diag->nlevels; ++i) {
         diag->entries_per_level[i] = res.entries_per_level[i];
         diag->tickets_per_level[i] = res.tickets_per_level[i];
       }
       diag->degenerate_draws = res.degenerate_draws;
+      rep->kernel_evals = res.kde.evals;
+      rep->kernel_evals_performed = res.kde.performed;
+      rep->root_evals_performed = res.kde.root_performed;
+      rep->tie_verified = res.tie_verified;
+      if (req.record_sums && !req.queries.empty()) {
+        static_assert(sizeof(fsgg_entry_record) == sizeof(fsgg::EntryRecord), "record layout");
+        const size_t m = res.records.size();
+        rep->records = static_cast<fsgg_entry_record*>(
+            std::malloc(std::max<size_t>(m, 1) * sizeof(fsgg_entry_record)));
+        if (!rep->records) throw std::bad_alloc();
+        std::memcpy(rep->records, res.records.data(), m * sizeof(fsgg_entry_record));
+        rep->num_records = m;
+      }
     }
   });
 }

@@ -237,6 +237,17 @@ struct SampleRequest {
   bool dfs_finish = true;   // finish small-node levels depth-first (finish.cu)
   bool walk = true;         // single-ticket entries below kWalkMaxNode walk (walk.cu)
   bool want_root_sums = false;
+  // Debug export (fsgg_sample_neighbors_counted_ex): every (node, query)
+  // entry's two child sums as the level's KDE kernels produced them, before
+  // the tie guard; forces the level-synchronous path (no walks / DFS).
+  bool record_sums = false;
+};
+
+// One recorded entry: node [first, last) at `level`, children
+// [first, first + (last - first) / 2) and [mid, last) (sampler.cpp:141, :200).
+struct EntryRecord {
+  uint32_t level, query, first, last;
+  double left, right;
 };
 
 struct SampleResult {
@@ -252,6 +263,7 @@ struct SampleResult {
   std::vector<uint64_t> entries_per_level, tickets_per_level;
   uint64_t peak_entries = 0;
   KdeStats kde;
+  std::vector<EntryRecord> records;  // record_sums only
 };
 
 void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,

@@ -318,8 +318,21 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   // on its own stream as soon as the array is final — v right away (it is
   // the keys' low word), w after the weights, row_ptr and degrees after
   // theirs — overlapping the rest of the finish
-  cudaStream_t cs = nullptr;
-  cudaEvent_t ev = nullptr;
+  // RAII: on any throw below, the side stream's copies into the caller's
+  // buffers are finished and the stream/event released before unwinding
+  struct SideStream {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev = nullptr;
+    ~SideStream() {
+      if (cs) {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+      }
+      if (ev) cudaEventDestroy(ev);
+    }
+  } side;
+  cudaStream_t& cs = side.cs;
+  cudaEvent_t& ev = side.ev;
   auto after = [&](void* dst, const void* src, size_t bytes) {
     if (!dst || !bytes) return;
     FSGG_CUDA(cudaEventRecord(ev, s));
@@ -328,7 +341,10 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   };
   const bool early_v = sink && sink->v && m && m <= sink->capacity;
   if (sink) {
-    if (m > sink->capacity) throw ConfigError("host output capacity below the edge count");
+    // checked before underflow drops: the capacity must hold the sampled
+    // unique pairs (n * L always does; fsgg.h)
+    if (m > sink->capacity)
+      throw ConfigError("host output capacity below the sampled unique pair count");
     FSGG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     FSGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     if (early_v) {
@@ -441,8 +457,6 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   if (sink) {
     after(sink->degrees, out.degrees.as<void>(), size_t(n) * 8);
     FSGG_CUDA(cudaStreamSynchronize(cs));
-    cudaEventDestroy(ev);
-    cudaStreamDestroy(cs);
   }
   FSGG_CUDA(cudaStreamSynchronize(s));
 }

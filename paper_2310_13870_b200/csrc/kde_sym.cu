@@ -735,7 +735,12 @@ bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t 
   FSGG_CUDA(cudaStreamSynchronize(ds.stream));
   const bool qb_ok = std::binary_search(hbf.begin(), hbf.end(), qb);
   const bool qe_ok = qe == ds.n || std::binary_search(hbf.begin(), hbf.end(), qe);
-  if (!qb_ok || !qe_ok) return false;
+  // Not a silent fallback: a peer whose bounds are aligned would run owner
+  // mode and wait for records this rank never sends (its sym.P slots would
+  // keep an earlier build's values).
+  if (!qb_ok || !qe_ok)
+    throw ConfigError("shard bounds must sit on symmetric-root block boundaries "
+                      "(use fsgg_shard_bounds)");
   if (!ws.ev0) {
     FSGG_CUDA(cudaEventCreate(&ws.ev0));
     FSGG_CUDA(cudaEventCreate(&ws.ev1));

@@ -1131,8 +1131,37 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
 
 }  // namespace
 
-void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
+// record_sums: one EntryRecord per entry of nodes with >= 2 points.
+__global__ void record_entries_kernel(uint32_t E, uint32_t level, const uint32_t* __restrict__ eq,
+                                      const uint32_t* __restrict__ eg,
+                                      const uint32_t* __restrict__ tfirst,
+                                      const uint32_t* __restrict__ tlast,
+                                      const double* __restrict__ g1,
+                                      const double* __restrict__ g2, EntryRecord* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const uint64_t slot = (uint64_t(1) << level) - 1 + eg[i];
+  EntryRecord r;
+  r.level = level;
+  r.query = eq[i];
+  r.first = tfirst[slot];
+  r.last = tlast[slot];
+  const bool split = r.last - r.first >= 2;
+  r.left = split ? g1[i] : 0.0;
+  r.right = split ? g2[i] : 0.0;
+  out[i] = r;
+}
+
+void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_in,
                     SampleResult& out) {
+  SampleRequest req_rec;
+  if (req_in.record_sums) {
+    req_rec = req_in;
+    req_rec.walk = false;
+    req_rec.dfs_finish = false;
+  }
+  const SampleRequest& req = req_in.record_sums ? req_rec : req_in;
+  out.records.clear();
   cudaStream_t s = ds.stream;
   if (!ds.tree_valid) build_tree(ds);
   const TreeTable& t = ds.tree;
@@ -1372,6 +1401,18 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
       }
     }
 
+    if (req.record_sums) {
+      DevBuf& rb = ds.buf("s.records", size_t(E) * sizeof(EntryRecord));
+      record_entries_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
+          E, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(), t.first.as<uint32_t>(),
+          t.last.as<uint32_t>(), g1.as<double>(), g2.as<double>(), rb.as<EntryRecord>());
+      FSGG_LAUNCH_CHECK();
+      const size_t o = out.records.size();
+      out.records.resize(o + E);
+      FSGG_CUDA(cudaMemcpyAsync(out.records.data() + o, rb.as<void>(),
+                                size_t(E) * sizeof(EntryRecord), cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+    }
     if (trace) FSGG_CUDA(cudaEventRecord(tev[1], s));
     // children (level + 1) below walk_max_node points with one ticket walk
     const uint32_t smax_child =

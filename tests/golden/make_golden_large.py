@@ -5,7 +5,9 @@ sizes where that is affordable on the build host, and stores compact
 fingerprints (counts, SHA-256 of the sorted edge arrays, weight samples)
 plus query-subset triples for C3, whose full exact run would take hours.
 
-    python tests/golden/make_golden_large.py [C2] [C3] [C4]
+    python tests/golden/make_golden_large.py [C2] [C3] [C4] [C5]
+
+FSG_GOLDEN_THREADS overrides the worker count (default: all host cores).
 """
 from __future__ import annotations
 
@@ -65,7 +67,7 @@ def query_subset(ref, name, count=256):
 
 def main():
     ref = Ref()
-    ref.set_threads(os.cpu_count() or 1)
+    ref.set_threads(int(os.environ.get("FSG_GOLDEN_THREADS", os.cpu_count() or 1)))
     which = sys.argv[1:] or ["C2", "C3"]
     path = os.path.join(OUT, "golden_large.json")
     meta = json.load(open(path)) if os.path.exists(path) else {}

@@ -78,6 +78,26 @@ def test_c3_query_rows_match_reference(c3, dense):
     assert rel(g, z["g_full"]).max() <= 2e-5
 
 
+@pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
+def test_c3_full_descent_rows_match_reference(c3, dense):
+    """The benchmarked path: ALL n queries (contiguous, as in the full build),
+    so the symmetric root over 4,096 blocks, block lookups at levels 7-11,
+    two-deep rows at level 12 and the walks from level 13 run. The 256 golden
+    queries' rows must equal the reference's."""
+    w, ds, k = c3
+    z = np.load(os.path.join(GOLDEN, "c3_queries.npz"))
+    tri, rep = F.sample_neighbors_counted_ex(ds, k, np.arange(w.n), w.rounds, 1,
+                                            dense_kde=dense)
+    if not dense:
+        assert rep.root_evals_performed > 0, "symmetric root did not run"
+    q = z["queries"].astype(np.int64)
+    lo = np.searchsorted(tri[:, 0], q, side="left")
+    hi = np.searchsorted(tri[:, 0], q, side="right")
+    rows = np.concatenate([tri[a:b] for a, b in zip(lo, hi)])
+    assert np.array_equal(rows, z["triples"])
+    assert int(tri[:, 2].astype(np.int64).sum()) == w.n * w.rounds
+
+
 def test_c3_full_graph_properties(c3):
     w, ds, k = c3
     n, L = w.n, w.rounds
