@@ -72,6 +72,9 @@ def parse_args():
                    help="target seconds of CPU work for the cpu_baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--kde-backend", default="exact", choices=["exact", "fast", "autoselect"],
+                   help="SparsifierConfig::kde.backend (exact: the headline; fast: the "
+                        "certified eps-budget backend, include/fsgg.h)")
     return p.parse_args()
 
 
@@ -164,9 +167,11 @@ def reference_inputs(cfg: str):
             "harness generator (libfsgg.so host code; no reference generator for this config)")
 
 
-def bench_config(cfg: str, n: int, d: int, sigma: float, L: int, world: int) -> dict:
+def bench_config(cfg: str, n: int, d: int, sigma: float, L: int, world: int,
+                 kde_backend: str = "exact") -> dict:
     """The ONE config dict both arms print (same keys and values)."""
-    return {"workload": f"{cfg}: {CONFIG_DOC[cfg]}", "n": n, "d": d, "sigma": sigma,
+    extra = {} if kde_backend == "exact" else {"kde_backend": kde_backend}
+    return {**extra, "workload": f"{cfg}: {CONFIG_DOC[cfg]}", "n": n, "d": d, "sigma": sigma,
             "samples_per_point": L, "seed": 1, "rng": "reference (splitmix64)",
             "parallelism": f"query shards x{world}",
             "l2": "GPU arm: flushed (512 MiB write) between steps"}
@@ -371,7 +376,7 @@ def main():
     w = datasets.config(args.config)
     n, L = w.n, w.rounds
     kernel = F.Kernel(F.KernelFamily.gaussian, w.sigma)
-    cfg = F.SparsifierConfig(rounds=L, seed=1)
+    cfg = F.SparsifierConfig(rounds=L, seed=1, kde_backend=F.KdeBackend[args.kde_backend])
     ds = F.Dataset(w.points, device=local)
     stream = torch.cuda.ExternalStream(N.lib().fsgg_dataset_stream(ds._h), device=local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
@@ -590,7 +595,8 @@ def main():
         "value": value, "unit": "sampled edges/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_s * 1e3 / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": bench_config(args.config, n, w.d, w.sigma, L, world),
+        "config": bench_config(args.config, n, w.d, w.sigma, L, world, args.kde_backend),
+        "kde_backend": {"name": reps[0].backend, "epsilon": reps[0].epsilon},
         "kernel_evals_per_s": evals / total_s, "kernel_evals_per_step": evals / K / max(world, 1),
         "kernel_evals_performed_per_step": performed / K,
         "kernel_evals_note": ("reference-equivalent Gaussian evaluations (2.38 n^2 sampler + n^2 "

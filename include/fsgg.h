@@ -77,7 +77,25 @@ typedef struct fsgg_config {
    * |g - g_exact| <= (fp32 evaluation error) + 2^-27 * (node mass)
    * (tests/test_gpu_node_sums.py). 1: evaluate every kernel term (dense). */
   int dense_kde;
+  /* fsg::KdeConfig::backend (proj/include/fsg/kde.hpp:20,28-30;
+   * make_estimator proj/src/kde.cpp:104-129). FSGG_KDE_EXACT (the default
+   * here: exact sums, the reference's exact backend edge for edge);
+   * FSGG_KDE_FAST: the device analogue of the reference's (1 +- eps) fast
+   * backend -- certified pruning with an epsilon-derived budget (eps =
+   * `epsilon`, or default_epsilon(n) when 0; 0 < eps < 1 else
+   * FSGG_ERR_CONFIG): every level skips at most eps / (depth + 1) of each
+   * node's kernel mass, so each query's sampling distribution is within total
+   * variation eps of the exact one and every degree g_full is within a factor
+   * (1 - eps / (depth + 1)) of exact; no tie guard. Non-gaussian kernels fall
+   * back to exact, as the reference does (UnsupportedKernel). FSGG_KDE_AUTO:
+   * the reference's autoselect rule (fast for gaussian, d <= 3, n >= 4096).
+   * The report's epsilon / backend say which ran. */
+  int kde_backend;
 } fsgg_config;
+
+#define FSGG_KDE_EXACT 0
+#define FSGG_KDE_FAST 1
+#define FSGG_KDE_AUTO 2
 
 /* Mirrors fsg::BuildReport (proj/include/fsg/sparsifier.hpp:40-58), plus
  * device counters. Phase times are device (CUDA event) seconds. */
@@ -358,6 +376,8 @@ typedef struct fsgg_sample_options {
   int dense_kde;     /* 1: no certified pruning */
   int record_sums;   /* 1: export every entry's child sums (see above) */
   int walks;         /* 0: no single-ticket walks (1 default) */
+  int kde_backend;   /* FSGG_KDE_EXACT (default) | _FAST | _AUTO, as fsgg_config */
+  double epsilon;    /* fast backend budget; 0 = default_epsilon(n) */
 } fsgg_sample_options;
 
 typedef struct fsgg_sample_report {

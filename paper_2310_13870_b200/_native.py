@@ -32,7 +32,7 @@ class fsgg_config(C.Structure):
                 ("rounds", C.c_uint32), ("epsilon", C.c_double), ("log_base", C.c_int),
                 ("seed", C.c_uint64), ("rng_mode", C.c_int),
                 ("query_begin", C.c_uint32), ("query_end", C.c_uint32),
-                ("dense_kde", C.c_int)]
+                ("dense_kde", C.c_int), ("kde_backend", C.c_int)]
 
 
 class fsgg_report(C.Structure):
@@ -105,7 +105,7 @@ class fsgg_entry_record(C.Structure):
 
 class fsgg_sample_options(C.Structure):
     _fields_ = [("rng_mode", C.c_int), ("dense_kde", C.c_int), ("record_sums", C.c_int),
-                ("walks", C.c_int)]
+                ("walks", C.c_int), ("kde_backend", C.c_int), ("epsilon", C.c_double)]
 
 
 class fsgg_sample_report(C.Structure):

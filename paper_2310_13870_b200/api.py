@@ -81,6 +81,16 @@ def default_epsilon(n: int, log_base: LogBase = LogBase.two) -> float:
     return N.lib().fsgg_default_epsilon(n, int(log_base))
 
 
+class KdeBackend(enum.IntEnum):
+    """fsg::KdeBackend (proj/include/fsg/kde.hpp:20). ``exact`` is this
+    library's default (the reference's is ``autoselect``): see fsgg.h,
+    fsgg_config::kde_backend, for the fast backend's certified budget."""
+
+    exact = 0
+    fast = 1
+    autoselect = 2
+
+
 @dataclass
 class SparsifierConfig:
     """proj/include/fsg/sparsifier.hpp:14-26 (+ rng_mode, query shard)."""
@@ -95,6 +105,7 @@ class SparsifierConfig:
     query_begin: int = 0
     query_end: int = 0
     dense_kde: bool = False  # True: evaluate every kernel term (no certified pruning)
+    kde_backend: KdeBackend = KdeBackend.exact  # SparsifierConfig::kde.backend
 
     def _c(self):
         c = N.fsgg_config()
@@ -108,6 +119,7 @@ class SparsifierConfig:
         c.query_begin = self.query_begin
         c.query_end = self.query_end
         c.dense_kde = int(self.dense_kde)
+        c.kde_backend = int(self.kde_backend)
         return c
 
     def rounds_for(self, n: int) -> int:
@@ -560,7 +572,8 @@ RECORD_DTYPE = np.dtype([("level", "<u4"), ("query", "<u4"), ("first", "<u4"), (
 
 def sample_neighbors_counted_ex(ds: Dataset, kernel: Kernel, queries, rounds: int, seed: int,
                                 rng_mode: RngMode = RngMode.reference, dense_kde: bool = False,
-                                record_sums: bool = False, walks: bool = True):
+                                record_sums: bool = False, walks: bool = True,
+                                kde_backend: "KdeBackend" = None, epsilon: float = 0.0):
     """fsgg_sample_neighbors_counted_ex: the descent with options; returns
     (triples, SampleReport)."""
     q = np.ascontiguousarray(np.asarray(queries, dtype=np.int64))
@@ -575,6 +588,8 @@ def sample_neighbors_counted_ex(ds: Dataset, kernel: Kernel, queries, rounds: in
     opt.dense_kde = int(dense_kde)
     opt.record_sums = int(record_sums)
     opt.walks = int(walks)
+    opt.kde_backend = int(KdeBackend.exact if kde_backend is None else kde_backend)
+    opt.epsilon = float(epsilon)
     out = C.c_void_p()
     cnt = C.c_size_t()
     rep = N.fsgg_sample_report()

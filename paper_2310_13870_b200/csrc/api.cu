@@ -150,6 +150,25 @@ fsgg_config default_config() {
   return c;
 }
 
+// make_estimator (proj/src/kde.cpp:104-129) on the device: which backend a
+// call runs and with what budget (fsgg.h, fsgg_config::kde_backend).
+struct Backend {
+  bool fast = false;
+  double eps = 0.0;
+};
+Backend resolve_backend(int kde_backend, double epsilon, int log_base, int family, uint32_t n,
+                        uint32_t d) {
+  if (kde_backend < FSGG_KDE_EXACT || kde_backend > FSGG_KDE_AUTO)
+    throw fsgg::ConfigError("unknown kde backend");
+  bool fast = kde_backend == FSGG_KDE_FAST;
+  if (kde_backend == FSGG_KDE_AUTO) fast = family == 0 && d <= 3 && n >= 4096;  // kde.hpp:39-40
+  if (!fast) return {};
+  if (family != 0) return {};  // UnsupportedKernel: informational fallback to exact
+  const double eps = epsilon > 0.0 ? epsilon : fsgg_default_epsilon(n, log_base);
+  if (!(eps > 0.0) || eps >= 1.0) throw fsgg::ConfigError("fast KDE needs 0 < epsilon < 1");
+  return {true, eps};
+}
+
 // proj/src/sparsifier.cpp:17-23
 uint32_t rounds_for(const fsgg_config& c, uint32_t n) {
   if (c.rounds > 0) return c.rounds;
@@ -166,12 +185,14 @@ void activate(fsgg_dataset* h) {
   h->ds.launches = 0;
 }
 
-void fill_report_common(fsgg_report* r, const fsgg::Dataset& ds, uint32_t L) {
+void fill_report_common(fsgg_report* r, const fsgg::Dataset& ds, uint32_t L,
+                        double eps = 0.0) {
   std::memset(r, 0, sizeof(*r));
   r->n = ds.n;
   r->rounds = L;
-  r->epsilon = 0.0;
-  std::strncpy(r->backend, "gpu-exact-sm100a", sizeof(r->backend) - 1);
+  r->epsilon = eps;  // the exact backend reports 0 (kde.hpp:30-31)
+  std::strncpy(r->backend, eps > 0.0 ? "gpu-fast-certified-sm100a" : "gpu-exact-sm100a",
+               sizeof(r->backend) - 1);
 }
 
 struct BuildOut {
@@ -182,6 +203,7 @@ struct BuildOut {
   uint32_t levels = 0;
   uint64_t peak = 0;
   uint64_t tie_verified = 0;
+  double eps = 0.0;  // fast backend budget (0: exact)
 };
 
 // Descent over the configured query shard; fills res (and optionally keys).
@@ -211,6 +233,13 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   req.seed = cfg.seed;
   req.rng_mode = cfg.rng_mode;
   req.prune = cfg.dense_kde ? 0 : 1;
+  const Backend be = resolve_backend(cfg.kde_backend, cfg.epsilon, cfg.log_base, kernel->family,
+                                     ds.n, ds.d);
+  if (be.fast && req.prune) {
+    req.fast_epsilon = be.eps;
+    req.verify_ties = false;  // the (1 +- eps) backend is not edge-for-edge exact
+    bo.eps = be.eps;
+  }
   req.want_root_sums = true;
   fsgg::sample_counted(ds, ks, req, res);
   double t2 = now();
@@ -228,7 +257,7 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
 
 void finish_report(fsgg_report* r, const fsgg::Dataset& ds, const BuildOut& bo,
                    const fsgg::GraphResult* g, double total) {
-  fill_report_common(r, ds, bo.L);
+  fill_report_common(r, ds, bo.L, bo.eps);
   r->sampled_pairs = bo.sampled;
   r->self_pairs_discarded = bo.self;
   r->degenerate_draws = bo.degenerate;
@@ -734,6 +763,8 @@ void fsgg_sample_options_init(fsgg_sample_options* opt) {
   opt->dense_kde = 0;
   opt->record_sums = 0;
   opt->walks = 1;
+  opt->kde_backend = FSGG_KDE_EXACT;
+  opt->epsilon = 0.0;
 }
 
 int fsgg_sample_neighbors_counted(fsgg_dataset* h, const fsgg_kernel* kernel,
@@ -791,6 +822,12 @@ int fsgg_sample_neighbors_counted_ex(fsgg_dataset* h, const fsgg_kernel* kernel,
     req.prune = dense_kde ? 0 : 1;
     req.walk = opt->walks != 0;
     req.record_sums = opt->record_sums != 0;
+    const Backend be = resolve_backend(opt->kde_backend, opt->epsilon, 0, kernel->family, ds.n,
+                                       ds.d);
+    if (be.fast && req.prune) {
+      req.fast_epsilon = be.eps;
+      req.verify_ties = false;
+    }
     std::vector<uint32_t> host;
     if (!h->sample) h->sample = std::make_unique<fsgg::SampleResult>();
     fsgg::SampleResult& res = *h->sample;
@@ -931,6 +968,14 @@ int fsgg_shard_root_prepare(fsgg_dataset* h, const fsgg_kernel* kernel, const fs
     ds.tc_ready = false;
     fsgg::build_tree(ds);
     h->tree_fresh = true;  // the shard's descent reuses this table
+    {  // the descent's pruning threshold (exact or fast backend)
+      const Backend be = resolve_backend(cfg.kde_backend, cfg.epsilon, cfg.log_base,
+                                         kernel->family, ds.n, ds.d);
+      fsgg::SampleRequest r;
+      r.fast_epsilon = be.fast ? be.eps : 0.0;
+      if (!ds.kde_ws) ds.kde_ws = std::make_unique<fsgg::KdeWorkspace>();
+      ds.kde_ws->prune_bits = fsgg::prune_bits_for(r, ds.tree);
+    }
     uint32_t n = 0;
     const uint32_t* recs = nullptr;
     fsgg::sym_shard_prepare(ds, ks, qb, qe, &n, &recs);

@@ -148,6 +148,7 @@ struct LevelView {
   const uint32_t* eq = nullptr;    // query index per entry
   const float* elm = nullptr;      // log2 of the entry's node mass (nullptr: root)
   int prune = 1;                   // certified pruning of negligible sub-chunks
+  float prune_bits = kPruneBits;   // ... below 2^-prune_bits of half the node mass
   const uint32_t* eg = nullptr;    // level-local slot per entry
   const uint32_t* goff = nullptr;  // num_slots + 1
   uint32_t qbase = 0xffffffffu;    // level 0: entries are points qbase.. in order (else ~0)
@@ -184,6 +185,10 @@ struct KdeWorkspace {
   uint32_t sym_ready_qb = 0, sym_ready_qe = 0, sym_ready_b0 = 0, sym_ready_b1 = 0;
   float sym_ready_scale = 0.f;
   int sym_ready_family = -1;
+  float sym_ready_bits = 0.f;
+  // pruning threshold of the current call (kPruneBits, or the fast
+  // backend's epsilon-derived value: fsgg_config.kde_backend)
+  float prune_bits = kPruneBits;
   double sym_ready_seconds = 0.0;     // device time of that tile kernel
   double sym_prepared_seconds = 0.0;  // ... credited to the root level that used it
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -233,6 +238,12 @@ struct SampleRequest {
   uint64_t seed = 1;
   int rng_mode = 0;
   int prune = 1;
+  // Fast backend (epsilon > 0): certified pruning at
+  // prune_bits = 19 + log2((depth + 1) / epsilon) instead of kPruneBits, no
+  // tie guard. The skipped mass per level is <= epsilon / (depth + 1) of
+  // every node's mass, so each query's sampling distribution is within
+  // total variation epsilon of the exact one (K1 fast).
+  double fast_epsilon = 0.0;
   bool verify_ties = true;  // reference RNG mode: re-decide near-ties on fp64 sums
   bool dfs_finish = true;   // finish small-node levels depth-first (finish.cu)
   bool walk = true;         // single-ticket entries below kWalkMaxNode walk (walk.cu)
@@ -268,6 +279,8 @@ struct SampleResult {
 
 void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req,
                     SampleResult& out);
+// Pruning threshold (log2) of a descent: kPruneBits, or the fast backend's.
+float prune_bits_for(const SampleRequest& req, const TreeTable& t);
 
 // Sorted (query, source, count) triples copied to the host.
 void sampled_triples_to_host(Dataset& ds, SampleResult& res,

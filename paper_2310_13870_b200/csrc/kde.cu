@@ -181,8 +181,9 @@ __global__ void __launch_bounds__(kThreads)
                           const uint32_t* __restrict__ tlast,
                           const float* __restrict__ tlo,
                           const float* __restrict__ thi, int has_boxes,
-                          float scale, int prune, double* __restrict__ partials,
+                          float scale, float prune_bits, double* __restrict__ partials,
                           unsigned long long* __restrict__ performed, int per_sub) {
+  const bool prune = prune_bits > 0.f;
   constexpr int T = LowDTile<D>::T;
   __shared__ __align__(16) float2 sm[T * D];
   __shared__ unsigned long long s_done;
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kThreads)
     }
     bool skipA = false, skipB = false;
     if (prune) {
-      const float lim = __log2f(float(cl - cf)) + kPruneBits;
+      const float lim = __log2f(float(cl - cf)) + prune_bits;
       skipA = !va || offA > lim - lbA;
       skipB = !vb || offB > lim - lbB;
     }
@@ -694,7 +695,7 @@ struct LowD {
     kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
         pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
         sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
-        t.hi.as<float>(), t.has_boxes, scale, lv.prune && t.has_boxes, partials,
+        t.hi.as<float>(), t.has_boxes, scale, (lv.prune && t.has_boxes) ? lv.prune_bits : 0.f, partials,
         performed, per_sub);
   }
   static void direct(cudaStream_t s, const float* pts, const LevelView& lv,

@@ -628,7 +628,9 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   const uint32_t* bl = t.last.as<uint32_t>() + hb;
   const float* lo = t.lo.as<float>() + hb * ds.d;
   const float* hi = t.hi.as<float>() + hb * ds.d;
-  const float bits = kPruneBits + 1.f;  // half the root mass (>= 1/2)
+  // half the root mass (>= 1/2); the call's threshold (kPruneBits, or the
+  // fast backend's)
+  const float bits = (ds.kde_ws ? ds.kde_ws->prune_bits : kPruneBits) + 1.f;
 
   DevBuf& cnt = ds.buf("sym.cnt", size_t(B + 1) * 4);
   DevBuf& poff = ds.buf("sym.poff", size_t(B + 1) * 4);
@@ -758,6 +760,7 @@ bool sym_shard_prepare(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t 
   ws.sym_ready_qe = qe;
   ws.sym_ready_scale = ks.scale;
   ws.sym_ready_family = ks.family;
+  ws.sym_ready_bits = ws.prune_bits;
   ws.sym_ready_b0 = b0;
   ws.sym_ready_b1 = b1;
   ws.sym_ready_seconds = ms * 1e-3;
@@ -791,7 +794,8 @@ bool kde_root_symmetric(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t
   uint32_t b0 = 0, b1 = 0, nrec = 0;
   ws.sym_prepared_seconds = 0.0;
   if (ws.sym_ready && ws.sym_ready_qb == qb && ws.sym_ready_qe == qe &&
-      ws.sym_ready_scale == ks.scale && ws.sym_ready_family == ks.family) {
+      ws.sym_ready_scale == ks.scale && ws.sym_ready_family == ks.family &&
+      ws.sym_ready_bits == ws.prune_bits) {
     // tiles already computed by sym_shard_prepare (+ received records)
     b0 = ws.sym_ready_b0;
     b1 = ws.sym_ready_b1;
@@ -852,7 +856,7 @@ void sym_shard_bounds(Dataset& ds, const KernelSpec* ks, uint32_t world, uint32_
     sym_count_kernel<<<B, 256, 0, ds.stream>>>(
         B, ds.tree.lo.as<float>() + hb * ds.d, ds.tree.hi.as<float>() + hb * ds.d,
         ds.tree.first.as<uint32_t>() + hb, ds.tree.last.as<uint32_t>() + hb, ds.d, ks->family,
-        ks->scale, kPruneBits + 1.f, c.as<uint32_t>());
+        ks->scale, (ds.kde_ws ? ds.kde_ws->prune_bits : kPruneBits) + 1.f, c.as<uint32_t>());
     FSGG_LAUNCH_CHECK();
     FSGG_CUDA(cudaMemcpyAsync(cnt.data(), c.as<void>(), size_t(B) * 4, cudaMemcpyDeviceToHost,
                               ds.stream));

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -1131,6 +1132,20 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
 
 }  // namespace
 
+// Pruning threshold (log2 units) of one descent. Exact backend: kPruneBits.
+// Fast backend: a sub-chunk is skipped below 2^-B of half the entry's node
+// mass and a node has <= 2^20 sub-chunks, so a level skips <= 2^(19 - B) of
+// every node's mass; B = 19 + log2((depth + 1) / eps) makes that
+// eps / (depth + 1) per level. Since a query reaches node N with probability
+// g_N / g_full and the masses of one level's nodes add up to g_full, each
+// level moves the query's sampling distribution by <= eps / (depth + 1) in
+// total variation: <= eps over the whole descent.
+float prune_bits_for(const SampleRequest& req, const TreeTable& t) {
+  if (!(req.fast_epsilon > 0.0)) return kPruneBits;
+  const double b = 19.0 + std::log2(double(t.depth + 1) / req.fast_epsilon);
+  return float(std::min<double>(kPruneBits, std::max(20.0, std::ceil(b))));
+}
+
 // record_sums: one EntryRecord per entry of nodes with >= 2 points.
 __global__ void record_entries_kernel(uint32_t E, uint32_t level, const uint32_t* __restrict__ eq,
                                       const uint32_t* __restrict__ eg,
@@ -1233,6 +1248,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
   DevBuf& vlist = ds.buf("s.vlist", verify ? cap * 4 : 4);
   if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
   KdeWorkspace& ws = *ds.kde_ws;
+  ws.prune_bits = prune_bits_for(req, t);
   // single-ticket walk list (walk.cu), filled by scatter_kernel
   const bool walk_on = req.walk && walk_supported(ds.d) && walk_max_node() > 0;
   DevBuf& wq = ds.buf("s.wq", walk_on ? cap * 4 : 4);
@@ -1295,6 +1311,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
         lv0.eg = eg[cur]->as<uint32_t>();
         lv0.goff = goff[cur]->as<uint32_t>();
         lv0.prune = req.prune;
+        lv0.prune_bits = ws.prune_bits;
         KdeStats scratch;
         kde_level(ds, ks, lv0, g1.as<double>(), g2.as<double>(), out.groot.as<double>(), ws,
                   scratch, 1, nullptr);
@@ -1353,6 +1370,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
     lv.eg = eg[cur]->as<uint32_t>();
     lv.elm = level == 0 ? nullptr : elm[cur]->as<float>();
     lv.prune = req.prune;
+    lv.prune_bits = ws.prune_bits;
     lv.goff = goff[cur]->as<uint32_t>();
     if (level == 0 && contiguous) lv.qbase = req.queries.front();
     const bool lookup = have_rows && level - row_level < row_depth;

@@ -31,18 +31,20 @@ def spectral_labels(n, u, v, w, k, seed=7):
     return KMeans(n_clusters=k, n_init=10, random_state=seed).fit_predict(emb)
 
 
+@pytest.mark.parametrize("ours", [F.KdeBackend.exact, F.KdeBackend.fast],
+                         ids=["gpu-exact", "gpu-fast"])
 @pytest.mark.parametrize("backend", [0, 2], ids=["ref-exact", "ref-auto-fgt"])
-def test_spectral_ari_vs_reference_graph(ref, backend):
+def test_spectral_ari_vs_reference_graph(ref, backend, ours):
     n, sigma, L = 20000, 0.1, 32
     pts, truth = datasets.make_moons(n, 0.05, 1)
     p32 = pts.astype(np.float32)
     g = F.build_similarity_graph(F.Dataset(p32), F.Kernel(F.KernelFamily.gaussian, sigma),
-                                 F.SparsifierConfig(rounds=L, seed=1))
+                                 F.SparsifierConfig(rounds=L, seed=1, kde_backend=ours))
     r = ref.build_graph(p32.astype(np.float64), sigma, L, seed=1, backend=backend,
                         want_estimates=False)
     lab_gpu = spectral_labels(n, g.u, g.v, g.w, 2)
     lab_ref = spectral_labels(n, r["u"], r["v"], r["w"], 2)
     ari = adjusted_rand_score(lab_ref, lab_gpu)
-    print(f"backend={r['report']['backend']}: ARI(gpu, ref) = {ari:.5f}, "
+    print(f"gpu={ours.name} ref={r['report']['backend']}: ARI(gpu, ref) = {ari:.5f}, "
           f"ARI(gpu, truth) = {adjusted_rand_score(truth, lab_gpu):.5f}")
     assert ari >= 0.99
