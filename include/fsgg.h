@@ -423,6 +423,27 @@ int fsgg_make_image_features(uint32_t height, uint32_t width,
 int fsgg_make_gmm(uint32_t n, uint32_t d, uint32_t k, double stddev,
                   uint64_t seed, double* points, uint32_t* labels);
 
+/* ---- input side on the device (same generators, GPU `device`) -------- */
+/* Each writes the points of the host generator above straight into device
+ * memory: fp64 (points64, n x d) and/or rounded to fp32 (points32, the
+ * precision the descent consumes) and/or labels — any of the three may be
+ * NULL; all are device pointers on `device`. log/sin/cos are correctly
+ * rounded (double-double); glibc's are within 0.502 ulp, so a fp64
+ * coordinate may differ from the host generator's in its last bit (~0.1% of
+ * values); the fp32 arrays are identical. Blocking. Errors as the host
+ * generators (2 for invalid arguments), 5 without an sm_100 device. */
+int fsgg_make_moons_device(uint32_t n, double noise, uint64_t seed, int device,
+                           double* points64, float* points32, uint32_t* labels);
+/* centers: HOST array k x d */
+int fsgg_make_blobs_device(uint32_t n, const double* centers, uint32_t k, uint32_t d,
+                           double stddev, uint64_t seed, int device, double* points64,
+                           float* points32, uint32_t* labels);
+int fsgg_make_image_features_device(uint32_t height, uint32_t width, uint32_t regions,
+                                    double noise, uint64_t seed, int device,
+                                    double* points64, float* points32, uint32_t* labels);
+int fsgg_make_gmm_device(uint32_t n, uint32_t d, uint32_t k, double stddev, uint64_t seed,
+                         int device, double* points64, float* points32, uint32_t* labels);
+
 /* ---- multi-GPU shard pipeline (one process per GPU) ------------------ */
 /* Phase 1 on every rank: descent for queries [query_begin, query_end) of
  * cfg, producing the shard's sorted unique undirected pair keys and its

@@ -468,6 +468,27 @@ void spectral_out(const fsgg::SpectralGraphView& v, cudaStream_t s, uint32_t k, 
 
 }  // namespace
 
+namespace {
+// device generators: validate, select the device, run, restore the device
+template <class F>
+int on_device(int device, bool valid, F&& f) {
+  return guarded([&] {
+    if (!valid) throw fsgg::ConfigError("invalid generator arguments");
+    require_device(device);
+    int prev = 0;
+    FSGG_CUDA(cudaGetDevice(&prev));
+    FSGG_CUDA(cudaSetDevice(device));
+    try {
+      f();
+    } catch (...) {
+      cudaSetDevice(prev);
+      throw;
+    }
+    FSGG_CUDA(cudaSetDevice(prev));
+  });
+}
+}  // namespace
+
 extern "C" {
 
 const char* fsgg_version(void) { return "fsgg 0.1.0 (sm_100a)"; }
@@ -889,6 +910,43 @@ int fsgg_kde_eval(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t first,
     fsgg::kde_range(ds, ks, first, last, dt.as<uint32_t>(), uint32_t(m), dout.as<double>());
     FSGG_CUDA(cudaMemcpyAsync(out, dout.as<void>(), m * 8, cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ---- device generators (datasets_dev.cu); argument checks as the host
+// generators (datasets.cpp), which follow proj/src/datasets.cpp:33-80
+
+int fsgg_make_moons_device(uint32_t n, double noise, uint64_t seed, int device,
+                           double* points64, float* points32, uint32_t* labels) {
+  return on_device(device, n >= 2 && noise >= 0.0, [&] {
+    fsgg::make_moons_device(n, noise, seed, points64, points32, labels);
+  });
+}
+
+int fsgg_make_blobs_device(uint32_t n, const double* centers, uint32_t k, uint32_t d,
+                           double stddev, uint64_t seed, int device, double* points64,
+                           float* points32, uint32_t* labels) {
+  return on_device(device, k > 0 && n >= k && stddev >= 0.0 && d > 0 && centers, [&] {
+    fsgg::make_blobs_device(n, centers, k, d, stddev, seed, points64, points32, labels);
+  });
+}
+
+int fsgg_make_image_features_device(uint32_t height, uint32_t width, uint32_t regions,
+                                    double noise, uint64_t seed, int device,
+                                    double* points64, float* points32, uint32_t* labels) {
+  return on_device(device,
+                   height > 0 && width > 0 && regions > 0 && noise >= 0.0 &&
+                       uint64_t(height) * width <= 0xffffffffull,
+                   [&] {
+                     fsgg::make_image_features_device(height, width, regions, noise, seed,
+                                                      points64, points32, labels);
+                   });
+}
+
+int fsgg_make_gmm_device(uint32_t n, uint32_t d, uint32_t k, double stddev, uint64_t seed,
+                         int device, double* points64, float* points32, uint32_t* labels) {
+  return on_device(device, k > 0 && n >= k && d > 0 && stddev >= 0.0, [&] {
+    fsgg::make_gmm_device(n, d, k, stddev, seed, points64, points32, labels);
   });
 }
 

@@ -360,6 +360,17 @@ struct WalkArgs {
 bool walk_supported(uint32_t d);
 void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& args);
 
+// datasets_dev.cu: device generators (blocking, current device); any of
+// p64 / p32 / labels may be null
+void make_moons_device(uint32_t n, double noise, uint64_t seed, double* p64, float* p32,
+                       uint32_t* labels);
+void make_blobs_device(uint32_t n, const double* centers_host, uint32_t k, uint32_t d,
+                       double stddev, uint64_t seed, double* p64, float* p32, uint32_t* labels);
+void make_image_features_device(uint32_t height, uint32_t width, uint32_t regions, double noise,
+                                uint64_t seed, double* p64, float* p32, uint32_t* labels);
+void make_gmm_device(uint32_t n, uint32_t d, uint32_t k, double stddev, uint64_t seed,
+                     double* p64, float* p32, uint32_t* labels);
+
 // ---- graph.cu -------------------------------------------------------------
 struct GraphResult {
   uint32_t n = 0;
