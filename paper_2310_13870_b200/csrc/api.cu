@@ -227,9 +227,10 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   FSGG_CUDA(cudaStreamSynchronize(ds.stream));
   double t1 = now();
   fsgg::SampleRequest req;
-  req.queries.resize(qe - qb);
-  for (uint32_t i = qb; i < qe; ++i) req.queries[i - qb] = i;
-  req.tickets.assign(qe - qb, L);
+  req.range = true;
+  req.range_begin = qb;
+  req.range_count = qe - qb;
+  req.range_tickets = L;
   req.seed = cfg.seed;
   req.rng_mode = cfg.rng_mode;
   req.prune = cfg.dense_kde ? 0 : 1;

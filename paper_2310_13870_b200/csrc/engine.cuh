@@ -152,6 +152,9 @@ struct LevelView {
   const uint32_t* eg = nullptr;    // level-local slot per entry
   const uint32_t* goff = nullptr;  // num_slots + 1
   uint32_t qbase = 0xffffffffu;    // level 0: entries are points qbase.. in order (else ~0)
+  // sync-free levels (sampler.cu): the entry count lives on the device and
+  // num_entries is only its upper bound; only direct levels accept this
+  const uint32_t* dE = nullptr;
 };
 
 struct KdeStats {
@@ -211,6 +214,9 @@ inline void Dataset::release_all() {
 // Tiled levels keep per-entry partial sums over the node's descendants
 // *row_depth levels down in ws.partials (row stride 2^*row_depth), aiming
 // for serve_levels >= 1; *row_depth = 0 when no partial rows were kept.
+// True when kde_level at `level` runs the low-d direct kernel (or nothing):
+// it then accepts a device-resident entry count (LevelView::dE).
+bool kde_level_sync_free(const Dataset& ds, const KernelSpec& ks, uint32_t level);
 void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                double* g1, double* g2, double* groot, KdeWorkspace& ws,
                KdeStats& stats, uint32_t serve_levels, uint32_t* row_depth);
@@ -235,6 +241,11 @@ void kde_range(Dataset& ds, const KernelSpec& ks, uint32_t first,
 struct SampleRequest {
   std::vector<uint32_t> queries;  // sorted unique query ids
   std::vector<uint32_t> tickets;  // tickets per query (rounds * multiplicity)
+  // Range request (builds and shards): queries [range_begin, range_begin +
+  // range_count), range_tickets each; `queries`/`tickets` stay empty and the
+  // device lists are generated in place (no host vectors, no upload).
+  bool range = false;
+  uint32_t range_begin = 0, range_count = 0, range_tickets = 0;
   uint64_t seed = 1;
   int rng_mode = 0;
   int prune = 1;
@@ -330,9 +341,10 @@ void sym_shard_bounds(Dataset& ds, const KernelSpec* ks, uint32_t world, uint32_
 // at this level is a run of whole blocks, so its sum for query q is the sum,
 // in ascending partner order, of q's values for the partners in that run.
 // Adds the reference-equivalent evaluations to *evals (device counter).
+// With dE, E is only an upper bound (the grid) and the count is *dE.
 void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,
                        const uint32_t* eg, double* g1, double* g2,
-                       unsigned long long* evals);
+                       unsigned long long* evals, const uint32_t* dE = nullptr);
 
 // ---- walk.cu --------------------------------------------------------------
 // Entries holding a single ticket below nodes of kWalkMaxNode points leave

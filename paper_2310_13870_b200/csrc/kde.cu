@@ -278,24 +278,35 @@ __global__ void __launch_bounds__(256)
                            const float* __restrict__ tlo,
                            const float* __restrict__ thi, int has_boxes,
                            float scale, double* __restrict__ g1,
-                           double* __restrict__ g2, double* __restrict__ groot) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= E) return;
-  const uint64_t h = ((1ull << level) - 1) + eg[i];
-  const uint32_t f = tfirst[h], l = tlast[h];
-  if (l - f < 2) {
-    g1[i] = g2[i] = 0.0;
-    return;
-  }
-  const uint32_t q = eq[i];
-  float qc[D];
+                           double* __restrict__ g2, double* __restrict__ groot,
+                           const uint32_t* __restrict__ dE,
+                           unsigned long long* __restrict__ evals) {
+  // dE: the entry count on the device (E is then the grid's upper bound,
+  // grid-strided) and the reference-equivalent evaluations are tallied here
+  if (dE) E = *dE;
+  unsigned long long ev = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x) {
+    const uint64_t h = ((1ull << level) - 1) + eg[i];
+    const uint32_t f = tfirst[h], l = tlast[h];
+    if (l - f < 2) {
+      g1[i] = g2[i] = 0.0;
+      continue;
+    }
+    ev += l - f;
+    const uint32_t q = eq[i];
+    float qc[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
-  double s[2];
-  direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
-  g1[i] = fmax(s[0], kSumFloor);
-  g2[i] = fmax(s[1], kSumFloor);
-  if (groot) groot[i] = fmax(s[0] + s[1], kSumFloor);
+    for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
+    double s[2];
+    direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
+    g1[i] = fmax(s[0], kSumFloor);
+    g2[i] = fmax(s[1], kSumFloor);
+    if (groot) groot[i] = fmax(s[0] + s[1], kSumFloor);
+  }
+  if (evals) {
+    for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if ((threadIdx.x & 31) == 0 && ev) atomicAdd(evals, ev);
+  }
 }
 
 // ---- high-d tiled kernel (CUDA-core micro-tiles, direct differences) ------
@@ -700,11 +711,13 @@ struct LowD {
   }
   static void direct(cudaStream_t s, const float* pts, const LevelView& lv,
                      const TreeTable& t, float scale, double* g1, double* g2,
-                     double* groot) {
-    kde_lowd_direct_kernel<D, FAM><<<ceil_div_u32(lv.num_entries, 256), 256, 0, s>>>(
+                     double* groot, uint32_t max_grid, unsigned long long* evals) {
+    const uint32_t grid = lv.dE ? std::min(ceil_div_u32(lv.num_entries, 256), max_grid)
+                                : ceil_div_u32(lv.num_entries, 256);
+    kde_lowd_direct_kernel<D, FAM><<<grid, 256, 0, s>>>(
         pts, lv.eq, lv.eg, lv.num_entries, lv.level, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
-        t.has_boxes, scale, g1, g2, groot);
+        t.has_boxes, scale, g1, g2, groot, lv.dE, evals);
   }
   static void range(dim3 grid, cudaStream_t s, const float* pts,
                     const uint32_t* targets, uint32_t m, uint32_t first,
@@ -768,6 +781,12 @@ uint32_t direct_threshold(uint32_t d) { return d <= kLowDMax ? 192u : 96u; }
 
 }  // namespace
 
+bool kde_level_sync_free(const Dataset& ds, const KernelSpec& ks, uint32_t level) {
+  (void)ks;
+  const uint32_t s_max = uint32_t((uint64_t(ds.n) + (1ull << level) - 1) >> level);
+  return s_max < 2 || (ds.d <= kLowDMax && s_max <= direct_threshold(ds.d));
+}
+
 void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                double* g1, double* g2, double* groot, KdeWorkspace& ws,
                KdeStats& stats, uint32_t serve_levels, uint32_t* row_depth) {
@@ -793,18 +812,24 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
       reinterpret_cast<unsigned long long*>(nb + G + 2 + (G & 1));
   FSGG_CUDA(cudaMemsetAsync(d_evals, 0, 16, s));
   // direct levels add their evaluation count to ws.direct_evals (read once
-  // by the caller after the descent: no host sync per small level)
+  // by the caller after the descent: no host sync per small level); the
+  // low-d direct kernel tallies it itself
+  if (lv.dE && !(direct && lowd))
+    throw ConfigError("device entry counts are only supported on low-d direct levels");
   if (direct) ws.direct_evals.ensure(8, s);
-  slot_blocks_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
-      lv.goff, G, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(), be,
-      direct ? nullptr : nb, direct ? ws.direct_evals.as<unsigned long long>() : d_evals);
-  FSGG_LAUNCH_CHECK();
-  ds.launches += 1;
+  if (!(direct && lowd)) {
+    slot_blocks_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
+        lv.goff, G, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(), be,
+        direct ? nullptr : nb, direct ? ws.direct_evals.as<unsigned long long>() : d_evals);
+    FSGG_LAUNCH_CHECK();
+    ds.launches += 1;
+  }
 
   if (direct) {
     if (lowd) {
       with_lowd(ks.family, d, [&](auto op) {
-        op.direct(s, pts, lv, t, ks.scale, g1, g2, groot);
+        op.direct(s, pts, lv, t, ks.scale, g1, g2, groot, uint32_t(ds.num_sms) * 16,
+                  ws.direct_evals.as<unsigned long long>());
       });
     } else {
       with_family(ks.family, [&](auto fam) {

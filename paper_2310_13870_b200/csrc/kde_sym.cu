@@ -473,10 +473,14 @@ __global__ void __launch_bounds__(kBlkThreads)
                         const float* __restrict__ P, const uint32_t* __restrict__ tfirst,
                         const uint32_t* __restrict__ tlast, const uint32_t* __restrict__ pos,
                         uint32_t b0, uint32_t ps, double* __restrict__ g1,
-                        double* __restrict__ g2, unsigned long long* __restrict__ evals) {
+                        double* __restrict__ g2, unsigned long long* __restrict__ evals,
+                        const uint32_t* __restrict__ dE) {
   constexpr int U = kBlkUnroll;
-  const uint32_t base = blockIdx.x * (kBlkThreads * U) + threadIdx.x;
+  if (dE) E = *dE;  // sync-free levels: the count is on the device
   const uint32_t sh = Lb - level;
+  unsigned long long ev = 0;
+  for (uint32_t tile = blockIdx.x; uint64_t(tile) * (kBlkThreads * U) < E; tile += gridDim.x) {
+  const uint32_t base = tile * (kBlkThreads * U) + threadIdx.x;
   uint32_t q[U], g[U], I[U], size[U], k[U], k1[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -552,7 +556,6 @@ __global__ void __launch_bounds__(kBlkThreads)
         b[u] += v;
     }
   }
-  unsigned long long ev = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * kBlkThreads;
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(kBlkThreads)
     g2[i] = fmax(b[u], kSumFloor);
     ev += size[u];
   }
+  }  // tiles
   __shared__ unsigned long long red[kBlkThreads / 32];
   for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ev;
@@ -885,20 +889,23 @@ void sym_shard_bounds(Dataset& ds, const KernelSpec* ks, uint32_t world, uint32_
 
 void block_lookup_sums(Dataset& ds, uint32_t E, uint32_t level, const uint32_t* eq,
                        const uint32_t* eg, double* g1, double* g2,
-                       unsigned long long* evals) {
+                       unsigned long long* evals, const uint32_t* dE) {
   const uint32_t Lb = ds.kde_ws ? ds.kde_ws->sym_Lb : 0;
   if (Lb == 0 || level == 0 || level + 1 > Lb) throw NumericError("no symmetric block values");
   if (E == 0) return;
   const TreeTable& t = ds.tree;
   const uint64_t hb = (uint64_t(1) << Lb) - 1;
   cudaStream_t s = ds.stream;
-  block_lookup_kernel<<<ceil_div_u32(E, kBlkThreads * kBlkUnroll), kBlkThreads, 0, s>>>(
+  // E: the entry count, or with dE its upper bound (grid-strided)
+  const uint32_t grid = std::min<uint32_t>(ceil_div_u32(E, kBlkThreads * kBlkUnroll),
+                                           uint32_t(ds.num_sms) * 16);
+  block_lookup_kernel<<<grid, kBlkThreads, 0, s>>>(
       E, level, Lb, eq, eg, ds.buf("sym.qblk", 4).as<uint32_t>(), t.first.as<uint32_t>() + hb,
       ds.buf("sym.poff", 4).as<uint32_t>(), ds.buf("sym.plist", 4).as<uint32_t>(),
       ds.buf("sym.P", 4).as<float>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
       ds.kde_ws->sym_pos ? ds.buf("sym.pos", 4).as<uint32_t>() : nullptr, ds.kde_ws->sym_b0,
       sym_pstride(ds, Lb), g1,
-      g2, evals);
+      g2, evals, dE);
   FSGG_LAUNCH_CHECK();
   ds.launches++;
 }

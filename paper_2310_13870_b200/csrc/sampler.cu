@@ -14,6 +14,9 @@
 //   3. one 64-bit exclusive scan of packed (has_left, has_right) flags;
 //   4. scatter_kernel / goff_kernel: deterministic stable placement, left
 //      children of a node before its right children (:217-222), no atomics.
+#include <cub/block/block_load.cuh>
+#include <cub/block/block_scan.cuh>
+#include <cub/block/block_store.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -76,6 +79,18 @@ __global__ void node_link_kernel(uint64_t nslots, const uint32_t* __restrict__ t
   if (h < nslots) out[h] = node_link(prefix, (uint64_t(tfirst[h]) << 32) | tlast[h]);
 }
 
+// Range request: queries qb.., `tickets` each, leaf rows of that size.
+__global__ void range_request_kernel(uint32_t qb, uint32_t nq, uint32_t tickets,
+                                     uint32_t* __restrict__ uq, uint32_t* __restrict__ tk,
+                                     uint64_t* __restrict__ row_off) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nq) {
+    uq[i] = qb + i;
+    tk[i] = tickets;
+  }
+  if (i <= nq) row_off[i] = uint64_t(i) * tickets;
+}
+
 __global__ void init_rows_kernel(const uint32_t* __restrict__ uq,
                                  uint32_t nq, uint32_t* __restrict__ qrow,
                                  uint32_t* __restrict__ eq,
@@ -122,9 +137,14 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
                  unsigned long long* __restrict__ counters, const float* __restrict__ elm,
                  const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
                  uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk,
-                 const uint64_t* __restrict__ nlink) {
+                 const uint64_t* __restrict__ nlink, const uint32_t* __restrict__ dE) {
   constexpr int U = kRouteUnroll;
-  const uint32_t base = blockIdx.x * (kRouteThreads * U) + threadIdx.x;
+  if (dE) E = *dE;  // the level's entry count on the device (sync-free levels)
+  unsigned long long tsum = 0, degen = 0;
+  // grid-stride over tiles of kRouteThreads * U entries (index E: sentinel)
+  for (uint32_t tile = blockIdx.x; uint64_t(tile) * (kRouteThreads * U) <= E;
+       tile += gridDim.x) {
+  const uint32_t base = tile * (kRouteThreads * U) + threadIdx.x;
   uint32_t gi[U], q[U], t[U], f[U], l[U];
   double a[U], b[U];
   float em[U], rm[U];
@@ -149,7 +169,6 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
     nl[u] = (i < E && nlink) ? nlink[h] : 0ull;
     rm[u] = (i < E && row_mass) ? row_mass[eprow ? eprow[i] : i] : 0.f;
   }
-  unsigned long long tsum = 0, degen = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * kRouteThreads;
@@ -230,6 +249,7 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
     }
     flags[i] = fl;
   }
+  }  // tiles
   // one atomic per CTA per counter (per-warp atomics on two addresses
   // serialise ~0.5M times a level at 60M entries)
   __shared__ unsigned long long red_t[kRouteThreads / 32], red_d[kRouteThreads / 32];
@@ -474,7 +494,7 @@ __global__ void __launch_bounds__(256)
 // nearly idle at the top levels (tens to thousands of ties). Each warp sums
 // its sub-chunk's fp64 terms (same terms and skip rule as
 // exact_sums_lowd_kernel) lane-strided, reduces them with a fixed butterfly
-// and writes one (left, right) partial; tie_split_reduce_kernel adds the
+// and writes one (left, right) partial; tie_finish_kernel adds the
 // partials in sub-chunk order, so the result depends only on the (node,
 // query). Ties beyond the partial buffer's capacity (max_ties) are left to
 // exact_sums_lowd_kernel (first_tie = max_ties) — no host sync needed.
@@ -487,25 +507,18 @@ __device__ __forceinline__ uint32_t tie_sub_depth(uint32_t level, uint32_t depth
   return kd;
 }
 
+// One warp's fp64 (left, right) sums of entry i over sub-chunk c of its
+// node (all lanes return the butterfly-reduced totals).
 template <int D, int FAM>
-__global__ void __launch_bounds__(kTieSplitThreads)
-    tie_split_kernel(const float* __restrict__ pts, double sigma, float scale, uint32_t level,
-                     uint32_t depth, const uint32_t* __restrict__ eq,
-                     const uint32_t* __restrict__ eg, const float* __restrict__ elm,
-                     const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
-                     const float* __restrict__ tlo, const float* __restrict__ thi,
-                     int has_boxes, const uint32_t* __restrict__ vlist,
-                     const uint32_t* __restrict__ vcount, uint32_t max_chunks,
-                     uint32_t max_ties, double* __restrict__ part) {
-  const uint32_t ties = min(*vcount, max_ties);
-  const uint64_t items = uint64_t(ties) * max_chunks;
+__device__ __forceinline__ void tie_chunk_sums(
+    const float* __restrict__ pts, double inv, float scale, uint32_t level, uint32_t depth,
+    const uint32_t* __restrict__ eq, const uint32_t* __restrict__ eg,
+    const float* __restrict__ elm, const uint32_t* __restrict__ tfirst,
+    const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
+    const float* __restrict__ thi, int has_boxes, uint32_t i, uint32_t c, double& r0,
+    double& r1) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warps = uint64_t(gridDim.x) * (kTieSplitThreads / 32);
-  const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
-  for (uint64_t it = blockIdx.x * uint64_t(kTieSplitThreads / 32) + (threadIdx.x >> 5);
-       it < items; it += warps) {
-    const uint32_t b = uint32_t(it / max_chunks), c = uint32_t(it % max_chunks);
-    const uint32_t i = vlist[b];
+  {
     const uint64_t h = ((1ull << level) - 1) + eg[i];
     const uint32_t f = tfirst[h], l = tlast[h], mid = f + (l - f) / 2;
     const uint32_t kd = tie_sub_depth(level, depth, l - f);
@@ -562,37 +575,35 @@ __global__ void __launch_bounds__(kTieSplitThreads)
       s0 += __shfl_xor_sync(0xffffffffu, s0, o);
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     }
-    if (lane == 0) {
-      part[it * 2] = s0;
-      part[it * 2 + 1] = s1;
-    }
+    r0 = s0;
+    r1 = s1;
   }
 }
 
-__global__ void tie_split_reduce_kernel(const uint32_t* __restrict__ vlist,
-                                        const uint32_t* __restrict__ vcount,
-                                        uint32_t max_chunks, uint32_t max_ties,
-                                        const double* __restrict__ part,
-                                        double* __restrict__ g1, double* __restrict__ g2) {
-  // one warp per tie: lane-strided partial sums, then a fixed butterfly
+template <int D, int FAM>
+__global__ void __launch_bounds__(kTieSplitThreads)
+    tie_split_kernel(const float* __restrict__ pts, double sigma, float scale, uint32_t level,
+                     uint32_t depth, const uint32_t* __restrict__ eq,
+                     const uint32_t* __restrict__ eg, const float* __restrict__ elm,
+                     const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                     const float* __restrict__ tlo, const float* __restrict__ thi,
+                     int has_boxes, const uint32_t* __restrict__ vlist,
+                     const uint32_t* __restrict__ vcount, uint32_t max_chunks,
+                     uint32_t max_ties, double* __restrict__ part) {
   const uint32_t ties = min(*vcount, max_ties);
+  const uint64_t items = uint64_t(ties) * max_chunks;
   const uint32_t lane = threadIdx.x & 31;
-  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < ties;
-       b += (gridDim.x * blockDim.x) >> 5) {
-    double a = 0.0, c = 0.0;
-    const double* p = part + size_t(b) * max_chunks * 2;
-    for (uint32_t k = lane; k < max_chunks; k += 32) {
-      a += p[2 * k];
-      c += p[2 * k + 1];
-    }
-    for (int o = 16; o; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      c += __shfl_xor_sync(0xffffffffu, c, o);
-    }
+  const uint64_t warps = uint64_t(gridDim.x) * (kTieSplitThreads / 32);
+  const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  for (uint64_t it = blockIdx.x * uint64_t(kTieSplitThreads / 32) + (threadIdx.x >> 5);
+       it < items; it += warps) {
+    const uint32_t b = uint32_t(it / max_chunks), c = uint32_t(it % max_chunks);
+    double s0, s1;
+    tie_chunk_sums<D, FAM>(pts, inv, scale, level, depth, eq, eg, elm, tfirst, tlast, tlo, thi,
+                           has_boxes, vlist[b], c, s0, s1);
     if (lane == 0) {
-      const uint32_t i = vlist[b];
-      g1[i] = fmax(a, kSumFloor);
-      g2[i] = fmax(c, kSumFloor);
+      part[it * 2] = s0;
+      part[it * 2 + 1] = s1;
     }
   }
 }
@@ -776,6 +787,42 @@ __global__ void tie_reduce_kernel(uint32_t count, const uint32_t* __restrict__ s
 }
 
 // Re-decide the flagged entries on the fp64 sums (reference stream).
+// The tie guard's re-decision of entry i on its (now fp64) child sums
+// a = g1[i], b = g2[i] (sampler.cpp:205-222 on the keyed stream).
+__device__ __forceinline__ void reroute_entry(uint32_t i, uint32_t level,
+                                              const uint32_t* __restrict__ eq,
+                                              const uint32_t* __restrict__ et,
+                                              const uint32_t* __restrict__ eg, double a,
+                                              double bb, const uint32_t* __restrict__ tfirst,
+                                              const uint32_t* __restrict__ tlast,
+                                              uint64_t key_prefix, uint32_t* __restrict__ tl,
+                                              unsigned long long* __restrict__ flags,
+                                              unsigned long long* __restrict__ counters,
+                                              int walk) {
+  const uint64_t h = ((1ull << level) - 1) + eg[i];
+  const uint32_t f = tfirst[h], l = tlast[h], q = eq[i], t = et[i];
+  double p;
+  if (a <= kSumFloor && bb <= kSumFloor) {
+    p = 0.5;
+    atomicAdd(counters + 1, static_cast<unsigned long long>(t));
+  } else {
+    p = a / (a + bb);
+  }
+  uint32_t left;
+  if (p <= 0.0) {
+    left = 0;
+  } else if (p >= 1.0) {
+    left = t;
+  } else {
+    const uint64_t thr = static_cast<uint64_t>(ceil(p * 9007199254740992.0));
+    const uint64_t key = route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
+    left = 0;
+    for (uint32_t c = 0; c < t; ++c) left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+  }
+  tl[i] = left;
+  flags[i] = child_flags(left, t, walk);
+}
+
 __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
                                const uint32_t* __restrict__ et,
                                const uint32_t* __restrict__ eg,
@@ -792,29 +839,91 @@ __global__ void reroute_kernel(uint32_t level, const uint32_t* __restrict__ eq,
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < cnt;
        b += gridDim.x * blockDim.x) {
     const uint32_t i = vlist[b];
-    const uint64_t h = ((1ull << level) - 1) + eg[i];
-    const uint32_t f = tfirst[h], l = tlast[h], q = eq[i], t = et[i];
-    const double a = g1[i], bb = g2[i];
-    double p;
-    if (a <= kSumFloor && bb <= kSumFloor) {
-      p = 0.5;
-      atomicAdd(counters + 1, static_cast<unsigned long long>(t));
+    reroute_entry(i, level, eq, et, eg, g1[i], g2[i], tfirst, tlast, key_prefix, tl, flags,
+                  counters, walk);
+  }
+}
+
+// Low-d tie guard, second half (replaces tie_split_reduce_kernel +
+// reroute_kernel): one warp per tie adds its sub-chunk partials in
+// tie_split_reduce order (lane-strided, fixed butterfly), stores the sums
+// and re-decides the entry; ties past the partial buffer (max_ties) already
+// hold exact_sums_lowd_kernel's sums.
+__global__ void __launch_bounds__(256)
+    tie_finish_kernel(uint32_t level, const uint32_t* __restrict__ eq,
+                      const uint32_t* __restrict__ et, const uint32_t* __restrict__ eg,
+                      double* __restrict__ g1, double* __restrict__ g2,
+                      const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                      uint64_t key_prefix, const uint32_t* __restrict__ vlist,
+                      const uint32_t* __restrict__ vcount, uint32_t max_chunks,
+                      uint32_t max_ties, const double* __restrict__ part,
+                      uint32_t* __restrict__ tl, unsigned long long* __restrict__ flags,
+                      unsigned long long* __restrict__ counters, int walk) {
+  const uint32_t ties = *vcount;
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < ties;
+       b += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t i = vlist[b];
+    double a, c;
+    if (b < max_ties) {
+      a = 0.0;
+      c = 0.0;
+      const double* p = part + size_t(b) * max_chunks * 2;
+      for (uint32_t k = lane; k < max_chunks; k += 32) {
+        a += p[2 * k];
+        c += p[2 * k + 1];
+      }
+      for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+      }
+      a = fmax(a, kSumFloor);
+      c = fmax(c, kSumFloor);
+      if (lane == 0) {
+        g1[i] = a;
+        g2[i] = c;
+      }
     } else {
-      p = a / (a + bb);
+      a = g1[i];
+      c = g2[i];
     }
-    uint32_t left;
-    if (p <= 0.0) {
-      left = 0;
-    } else if (p >= 1.0) {
-      left = t;
-    } else {
-      const uint64_t thr = static_cast<uint64_t>(ceil(p * 9007199254740992.0));
-      const uint64_t key = route_key(key_prefix, (uint64_t(f) << 32) | l, uint64_t(q));
-      left = 0;
-      for (uint32_t c = 0; c < t; ++c) left += (splitmix64(key + c) >> 11) < thr ? 1u : 0u;
+    if (lane == 0)
+      reroute_entry(i, level, eq, et, eg, a, c, tfirst, tlast, key_prefix, tl, flags, counters,
+                    walk);
+  }
+}
+
+// Low-d tie guard for levels whose nodes are one sub-chunk (< 512 points):
+// split, reduce and re-decision in one pass, one warp per tie. The sums are
+// bit-identical to tie_split_kernel + tie_finish_kernel with one chunk (a
+// single partial added to zeros).
+template <int D, int FAM>
+__global__ void __launch_bounds__(kTieSplitThreads)
+    tie_onepass_kernel(const float* __restrict__ pts, double sigma, float scale, uint32_t level,
+                       uint32_t depth, const uint32_t* __restrict__ eq,
+                       const uint32_t* __restrict__ et, const uint32_t* __restrict__ eg,
+                       const float* __restrict__ elm, const uint32_t* __restrict__ tfirst,
+                       const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
+                       const float* __restrict__ thi, int has_boxes,
+                       const uint32_t* __restrict__ vlist, const uint32_t* __restrict__ vcount,
+                       double* __restrict__ g1, double* __restrict__ g2, uint64_t key_prefix,
+                       uint32_t* __restrict__ tl, unsigned long long* __restrict__ flags,
+                       unsigned long long* __restrict__ counters, int walk) {
+  const uint32_t ties = *vcount;
+  const double inv = FAM == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  for (uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < ties;
+       b += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t i = vlist[b];
+    double s0, s1;
+    tie_chunk_sums<D, FAM>(pts, inv, scale, level, depth, eq, eg, elm, tfirst, tlast, tlo, thi,
+                           has_boxes, i, 0, s0, s1);
+    if ((threadIdx.x & 31) == 0) {
+      const double a = fmax(s0, kSumFloor), c = fmax(s1, kSumFloor);
+      g1[i] = a;
+      g2[i] = c;
+      reroute_entry(i, level, eq, et, eg, a, c, tfirst, tlast, key_prefix, tl, flags, counters,
+                    walk);
     }
-    tl[i] = left;
-    flags[i] = child_flags(left, t, walk);
   }
 }
 
@@ -830,9 +939,13 @@ __global__ void __launch_bounds__(kLookupThreads)
                        const double* __restrict__ rows, const double* __restrict__ pyr,
                        const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
                        double* __restrict__ g1, double* __restrict__ g2,
-                       unsigned long long* __restrict__ evals) {
+                       unsigned long long* __restrict__ evals, const uint32_t* __restrict__ dE) {
   constexpr int U = kLookupUnroll;
-  const uint32_t base = blockIdx.x * (kLookupThreads * U) + threadIdx.x;
+  if (dE) E = *dE;
+  unsigned long long ev = 0;
+  for (uint32_t tile = blockIdx.x; uint64_t(tile) * (kLookupThreads * U) < E;
+       tile += gridDim.x) {
+  const uint32_t base = tile * (kLookupThreads * U) + threadIdx.x;
   uint32_t g[U], pr[U], size[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -869,7 +982,6 @@ __global__ void __launch_bounds__(kLookupThreads)
       }
     }
   }
-  unsigned long long ev = 0;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * kLookupThreads;
@@ -882,6 +994,7 @@ __global__ void __launch_bounds__(kLookupThreads)
       ev += size[u];
     }
   }
+  }  // tiles
   __shared__ unsigned long long red_ev[kLookupThreads / 32];
   for (int o = 16; o; o >>= 1) ev += __shfl_xor_sync(0xffffffffu, ev, o);
   if ((threadIdx.x & 31) == 0) red_ev[threadIdx.x >> 5] = ev;
@@ -924,8 +1037,11 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
                                uint32_t* __restrict__ wh, float* __restrict__ welm,
                                uint32_t* __restrict__ wcount, uint32_t* __restrict__ wrow,
                                float* __restrict__ wrm, const float* __restrict__ elm,
-                               int rows2) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                               int rows2, const uint32_t* __restrict__ dE) {
+  if (dE) E = *dE;
+  __shared__ uint32_t wtot[8], wbase;
+  for (uint32_t tile = blockIdx.x; uint64_t(tile) * blockDim.x < E; tile += gridDim.x) {
+  const uint32_t i = tile * blockDim.x + threadIdx.x;
   uint32_t nw = 0, wmask = 0;  // single-ticket children handed to the walk
   uint32_t g = 0, q = 0;
   if (i < E) {
@@ -958,12 +1074,11 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
       }
     }
   }
-  if (!wq) return;
+  if (!wq) continue;
   // CTA-aggregated reservation in the walk list: one atomic per CTA (a
   // per-warp atomic on the single counter serialised ~2M times a level).
   // Order within the list is irrelevant: walks are independent and leaves
   // land in per-query rows.
-  __shared__ uint32_t wtot[8], wbase;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = nw;
 #pragma unroll
@@ -983,8 +1098,11 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
     wbase = t ? atomicAdd(wcount, t) : 0u;
   }
   __syncthreads();
-  if (nw == 0) return;
-  uint32_t pos = wbase + wtot[warp] + incl - nw;
+  const uint32_t cta_base = wbase;
+  const uint32_t warp_off = wtot[warp];
+  __syncthreads();  // wtot / wbase are rewritten by the next tile
+  if (nw == 0) continue;
+  uint32_t pos = cta_base + warp_off + incl - nw;
   const uint32_t hbase = (1u << (level + 1)) - 1;
   // rows2: this level kept two-deep partial rows (kde.cu, per-sub-chunk
   // rows), so the walk's first child sums are in row i (walk.cu reads them
@@ -1006,6 +1124,120 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
     welm[pos] = float(int((__double_as_longlong(g2[i]) >> 52) & 0x7ff) - 1023);
     wrow[pos] = rw;
     wrm[pos] = rm;
+  }
+  }  // tiles
+}
+
+// Exclusive scan of the E + 1 packed child flags (the last one is route's
+// zero sentinel, so P[E] = the next level's (left, right) totals) with the
+// entry count read on the device: one pass, decoupled look-back. Tiles are
+// taken in order from a per-level counter, so every predecessor a tile waits
+// on belongs to a running CTA. Tile states are (epoch << 2 | kind) words
+// written after their value (kind 1: the tile's aggregate, 2: its inclusive
+// prefix) with a fence in between; the epoch (level + 1) makes the words of
+// earlier levels invisible, so the state array is cleared once per descent.
+// The thread holding index E also writes the next level's entry count.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr uint32_t kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    flags_scan_kernel(const uint32_t* __restrict__ dE, const unsigned long long* __restrict__ flags,
+                      unsigned long long* __restrict__ P, uint32_t* __restrict__ tstate,
+                      unsigned long long* __restrict__ tagg, unsigned long long* __restrict__ tinc,
+                      uint32_t* __restrict__ tctr, uint32_t epoch, uint32_t* __restrict__ e_next) {
+  using Load = cub::BlockLoad<unsigned long long, kScanThreads, kScanItems,
+                              cub::BLOCK_LOAD_WARP_TRANSPOSE>;
+  using Store = cub::BlockStore<unsigned long long, kScanThreads, kScanItems,
+                                cub::BLOCK_STORE_WARP_TRANSPOSE>;
+  using Scan = cub::BlockScan<unsigned long long, kScanThreads>;
+  __shared__ union {
+    typename Load::TempStorage load;
+    typename Store::TempStorage store;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_prefix;
+  const uint32_t n = *dE + 1;
+  const uint32_t ntiles = (n + kScanTile - 1) / kScanTile;
+  const uint32_t lane = threadIdx.x & 31;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t base = tile * kScanTile;
+    const uint32_t valid = min(kScanTile, n - base);
+    unsigned long long v[kScanItems];
+    Load(tmp.load).Load(flags + base, v, int(valid), 0ull);
+    __syncthreads();
+    unsigned long long agg;
+    Scan(tmp.scan).ExclusiveSum(v, v, agg);
+    if (threadIdx.x < 32) {
+      unsigned long long excl = 0;
+      if (tile == 0) {
+        if (lane == 0) {
+          tinc[0] = agg;
+          __threadfence();
+          atomicExch(tstate, (epoch << 2) | 2u);
+        }
+      } else {
+        if (lane == 0) {
+          tagg[tile] = agg;
+          __threadfence();
+          atomicExch(tstate + tile, (epoch << 2) | 1u);
+        }
+        int pred = int(tile) - 1;
+        for (;;) {
+          const int tt = pred - int(lane);
+          uint32_t st = (epoch << 2) | 2u;
+          unsigned long long val = 0;
+          if (tt >= 0) {
+            do {
+              st = ld_volatile(tstate + tt);
+            } while ((st >> 2) != epoch);
+            __threadfence();
+            val = (st & 3u) == 2u ? ld_volatile(tinc + tt) : ld_volatile(tagg + tt);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, (st & 3u) == 2u);
+          const int stop = inc ? __ffs(inc) - 1 : 31;
+          unsigned long long c = int(lane) <= stop ? val : 0ull;
+          for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+          excl += c;
+          if (inc) break;
+          pred -= 32;
+        }
+        if (lane == 0) {
+          tinc[tile] = excl + agg;
+          __threadfence();
+          atomicExch(tstate + tile, (epoch << 2) | 2u);
+        }
+      }
+      if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    const unsigned long long pre = s_prefix;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] += pre;
+    // the sentinel (index n - 1 = E): its exclusive prefix is the level total
+    const uint32_t last = n - 1 - base;
+    if (last < kScanTile && threadIdx.x == last / kScanItems) {
+      unsigned long long tot = 0;
+#pragma unroll
+      for (int k = 0; k < kScanItems; ++k)
+        if (uint32_t(k) == last % kScanItems) tot = v[k];
+      *e_next = uint32_t(tot >> 32) + uint32_t(tot);
+    }
+    __syncthreads();
+    Store(tmp.store).Store(P + base, v, int(valid));
+    __syncthreads();
   }
 }
 
@@ -1180,17 +1412,22 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
   cudaStream_t s = ds.stream;
   if (!ds.tree_valid) build_tree(ds);
   const TreeTable& t = ds.tree;
-  const uint32_t nq = static_cast<uint32_t>(req.queries.size());
+  const uint32_t nq =
+      req.range ? req.range_count : static_cast<uint32_t>(req.queries.size());
   out.nq = nq;
   uint64_t total = 0;
-  for (uint32_t x : req.tickets) total += x;
+  if (req.range) {
+    if (uint64_t(req.range_begin) + nq > ds.n) throw ConfigError("query range out of bounds");
+    total = uint64_t(nq) * req.range_tickets;
+  } else {
+    for (uint32_t x : req.tickets) total += x;
+  }
   out.total_tickets = total;
   if (total > 0xffffffffull)
     throw ConfigError("total tickets exceed 2^32 - 1 (entries are 32-bit)");
 
-  // host -> device: queries, tickets, leaf row offsets
-  std::vector<uint64_t> row_off(nq + 1, 0);
-  for (uint32_t i = 0; i < nq; ++i) row_off[i + 1] = row_off[i] + req.tickets[i];
+  // queries, tickets, leaf row offsets: generated on the device for a range
+  // request, else uploaded
   out.uq.ensure(size_t(nq) * 4 + 4, s);
   out.row_off.ensure(size_t(nq + 1) * 8, s);
   out.row_cnt.ensure(size_t(nq) * 4 + 4, s);
@@ -1198,12 +1435,22 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
   out.leaf_cnt.ensure(total * 4 + 4, s);
   DevBuf& dtk = ds.buf("s.tickets", size_t(nq) * 4 + 4);
   DevBuf& qrow = ds.buf("s.qrow", size_t(ds.n) * 4);
-  FSGG_CUDA(cudaMemcpyAsync(out.uq.as<void>(), req.queries.data(), size_t(nq) * 4,
-                            cudaMemcpyHostToDevice, s));
-  FSGG_CUDA(cudaMemcpyAsync(dtk.as<void>(), req.tickets.data(), size_t(nq) * 4,
-                            cudaMemcpyHostToDevice, s));
-  FSGG_CUDA(cudaMemcpyAsync(out.row_off.as<void>(), row_off.data(),
-                            size_t(nq + 1) * 8, cudaMemcpyHostToDevice, s));
+  if (req.range) {
+    range_request_kernel<<<ceil_div_u32(uint64_t(nq) + 1, 256), 256, 0, s>>>(
+        req.range_begin, nq, req.range_tickets, out.uq.as<uint32_t>(), dtk.as<uint32_t>(),
+        out.row_off.as<uint64_t>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  } else {
+    std::vector<uint64_t> row_off(nq + 1, 0);
+    for (uint32_t i = 0; i < nq; ++i) row_off[i + 1] = row_off[i] + req.tickets[i];
+    FSGG_CUDA(cudaMemcpyAsync(out.uq.as<void>(), req.queries.data(), size_t(nq) * 4,
+                              cudaMemcpyHostToDevice, s));
+    FSGG_CUDA(cudaMemcpyAsync(dtk.as<void>(), req.tickets.data(), size_t(nq) * 4,
+                              cudaMemcpyHostToDevice, s));
+    FSGG_CUDA(cudaMemcpyAsync(out.row_off.as<void>(), row_off.data(),
+                              size_t(nq + 1) * 8, cudaMemcpyHostToDevice, s));
+  }
   FSGG_CUDA(cudaMemsetAsync(out.row_cnt.as<void>(), 0, size_t(nq) * 4 + 4, s));
   if (req.want_root_sums) out.groot.ensure(size_t(nq) * 8 + 8, s);
 
@@ -1242,8 +1489,22 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
   const uint64_t max_slots = 1ull << t.depth;
   DevBuf* goff[2] = {&ds.buf("s.goff0", (max_slots + 1) * 4),
                      &ds.buf("s.goff1", (max_slots + 1) * 4)};
-  DevBuf& counters = ds.buf("s.counters", 64);
-  DevBuf& cub_tmp = ds.buf("s.cub_tmp", 8);
+  // per-level counters (tickets, degenerate draws, tie count, spare) and the
+  // entry count of every level (elog[0] = nq; the scan writes elog[l + 1]):
+  // read once after the descent
+  constexpr uint32_t kMaxLevelsLog = 64;
+  DevBuf& lvc = ds.buf("s.lvc", kMaxLevelsLog * 4 * 8);
+  DevBuf& elog = ds.buf("s.elog", (kMaxLevelsLog + 2) * 4);
+  FSGG_CUDA(cudaMemsetAsync(lvc.as<void>(), 0, kMaxLevelsLog * 4 * 8, s));
+  FSGG_CUDA(cudaMemsetAsync(elog.as<void>(), 0, (kMaxLevelsLog + 2) * 4, s));
+  FSGG_CUDA(cudaMemcpyAsync(elog.as<void>(), &nq, 4, cudaMemcpyHostToDevice, s));
+  // decoupled look-back scan state (flags_scan_kernel), cleared per descent
+  const uint64_t max_tiles = (cap + 1 + kScanTile - 1) / kScanTile;
+  DevBuf& tstate = ds.buf("s.scan_state", max_tiles * 4 + kMaxLevelsLog * 4);
+  DevBuf& tagg = ds.buf("s.scan_agg", max_tiles * 8);
+  DevBuf& tinc = ds.buf("s.scan_inc", max_tiles * 8);
+  FSGG_CUDA(cudaMemsetAsync(tstate.as<void>(), 0, max_tiles * 4 + kMaxLevelsLog * 4, s));
+  uint32_t* tctr = tstate.as<uint32_t>() + max_tiles;
   const bool verify = req.rng_mode == 0 && req.verify_ties;
   DevBuf& vlist = ds.buf("s.vlist", verify ? cap * 4 : 4);
   if (!ds.kde_ws) ds.kde_ws = std::make_unique<KdeWorkspace>();
@@ -1269,7 +1530,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
 
   // level-0 entries are a contiguous point range (full builds and shards)
   const bool contiguous =
-      nq > 0 && uint64_t(req.queries.back()) - req.queries.front() + 1 == nq;
+      nq > 0 && (req.range || uint64_t(req.queries.back()) - req.queries.front() + 1 == nq);
+  const uint32_t first_query = req.range ? req.range_begin : (nq ? req.queries.front() : 0u);
   const uint64_t prefix = route_key_prefix(req.seed);
   // per-slot node links of the keyed stream: an entry's key is then one
   // splitmix64 of (node link ^ query link) instead of three
@@ -1282,7 +1544,14 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
     ds.launches++;
   }
   const uint64_t* nlink_p = req.rng_mode == 0 ? nlink.as<uint64_t>() : nullptr;
+  // E: the current level's entry count when known on the host (E_known);
+  // E_hi: an upper bound otherwise. Sync-free descent (low d): a level's
+  // kernels read the count from elog on the device and grid-stride, so the
+  // host only synchronises before the levels whose launch geometry needs the
+  // exact count (tiled KDE levels); statistics are read once at the end.
   uint32_t E = nq;
+  bool E_known = true;
+  uint64_t E_hi = nq;
   int cur = 0;
   out.entries_per_level.clear();
   out.tickets_per_level.clear();
@@ -1296,9 +1565,35 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
   if (trace)
     for (auto& e : tev) FSGG_CUDA(cudaEventCreate(&e));
-  for (uint32_t level = 0; E > 0; ++level) {
-    if (level > t.depth) throw NumericError("descent exceeded tree depth");
+  const char* sf_env = std::getenv("FSGG_SYNC_FREE");
+  const bool lite = ds.d <= 8 && !trace && !req.record_sums &&
+                    !(req.dfs_finish && dfs_finish_supported(ds.d) && dfs_max_node() > 0) &&
+                    !(sf_env && std::atoi(sf_env) == 0);
+  const uint32_t nsm = uint32_t(ds.num_sms);
+  // grid of a grid-strided kernel over n items, span items per CTA
+  auto grid_of = [&](uint64_t n, uint32_t span, uint32_t per_sm) {
+    return uint32_t(std::max<uint64_t>(
+        1, std::min<uint64_t>((n + span - 1) / span, uint64_t(nsm) * per_sm)));
+  };
+  uint32_t levels_run = 0;
+  for (uint32_t level = 0;; ++level) {
+    if (E_known && E == 0) break;
+    if (level > t.depth) {
+      if (E_known) throw NumericError("descent exceeded tree depth");
+      break;  // sync-free: checked on the level counts below
+    }
     const uint32_t G = 1u << level;
+    const uint32_t* dE = elog.as<uint32_t>() + level;
+    // the exact count, when the next launch needs it
+    auto sync_E = [&] {
+      if (E_known) return;
+      uint32_t* hw = reinterpret_cast<uint32_t*>(ds.host_words());
+      FSGG_CUDA(cudaMemcpyAsync(hw, dE, 4, cudaMemcpyDeviceToHost, s));
+      FSGG_CUDA(cudaStreamSynchronize(s));
+      E = *hw;
+      E_known = true;
+      E_hi = E;
+    };
     const uint32_t smax_level = uint32_t((uint64_t(ds.n) + (1ull << level) - 1) >> level);
     if (req.dfs_finish && dfs_finish_supported(ds.d) && smax_level <= dfs_max_node()) {
       if (level == 0 && req.want_root_sums) {
@@ -1359,39 +1654,48 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
     }
     const auto wall0 = std::chrono::steady_clock::now();
     const KdeStats kde0 = out.kde;
+    const bool lookup = have_rows && level - row_level < row_depth;
+    // below the root rows' reach, the symmetric root's block values still
+    // hold every child sum while children are unions of its blocks
+    const bool blk_lookup = !lookup && have_rows && row_level == 0 && level > 0 &&
+                            ws.sym_Lb > 0 && level + 1 <= ws.sym_Lb && blk_lookup_on();
+    if (!lite || (!lookup && !blk_lookup && !kde_level_sync_free(ds, ks, level))) sync_E();
+    if (E_known && E == 0) break;
+    ++levels_run;
+    const uint32_t En = E_known ? E : uint32_t(E_hi);  // grid bound
+    const uint32_t* dEp = E_known ? nullptr : dE;
     if (trace) FSGG_CUDA(cudaEventRecord(tev[0], s));
-    out.entries_per_level.push_back(E);
-    out.peak_entries = std::max<uint64_t>(out.peak_entries, E);
+    if (!lite) {
+      out.entries_per_level.push_back(E);
+      out.peak_entries = std::max<uint64_t>(out.peak_entries, E);
+    }
     LevelView lv;
     lv.level = level;
     lv.num_slots = G;
-    lv.num_entries = E;
+    lv.num_entries = En;
+    lv.dE = dEp;
     lv.eq = eq[cur]->as<uint32_t>();
     lv.eg = eg[cur]->as<uint32_t>();
     lv.elm = level == 0 ? nullptr : elm[cur]->as<float>();
     lv.prune = req.prune;
     lv.prune_bits = ws.prune_bits;
     lv.goff = goff[cur]->as<uint32_t>();
-    if (level == 0 && contiguous) lv.qbase = req.queries.front();
-    const bool lookup = have_rows && level - row_level < row_depth;
-    // below the root rows' reach, the symmetric root's block values still
-    // hold every child sum while children are unions of its blocks
-    const bool blk_lookup = !lookup && have_rows && row_level == 0 && level > 0 &&
-                            ws.sym_Lb > 0 && level + 1 <= ws.sym_Lb && blk_lookup_on();
+    if (level == 0 && contiguous) lv.qbase = first_query;
     bool self_rows = false;
     // (lookup levels accumulate their reference-equivalent evaluations on the
     // device; read once after the descent — no host sync per level)
     if (blk_lookup) {
-      block_lookup_sums(ds, E, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
-                        g1.as<double>(), g2.as<double>(), lookup_evals.as<unsigned long long>());
+      block_lookup_sums(ds, En, level, eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+                        g1.as<double>(), g2.as<double>(), lookup_evals.as<unsigned long long>(),
+                        dEp);
     } else if (lookup) {
-      lookup_sums_kernel<<<ceil_div_u32(E, kLookupThreads * kLookupUnroll), kLookupThreads, 0, s>>>(
-          E, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
+      lookup_sums_kernel<<<grid_of(En, kLookupThreads * kLookupUnroll, 16), kLookupThreads, 0, s>>>(
+          En, level, level - row_level, row_depth, eg[cur]->as<uint32_t>(),
           eprow[cur]->as<uint32_t>(), ws.partials.as<double>(),
           ws.pyr_depth == row_depth ? ws.pyr.as<double>() : nullptr,
           t.first.as<uint32_t>(),
           t.last.as<uint32_t>(), g1.as<double>(), g2.as<double>(),
-          lookup_evals.as<unsigned long long>());
+          lookup_evals.as<unsigned long long>(), dEp);
       FSGG_LAUNCH_CHECK();
       ds.launches++;
     } else {
@@ -1436,21 +1740,21 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
     const uint32_t smax_child =
         uint32_t((uint64_t(ds.n) + (1ull << (level + 1)) - 1) >> (level + 1));
     const int wk = walk_on && level < t.depth && smax_child <= walk_max_node() ? 1 : 0;
-    FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
-    uint32_t* vcount = reinterpret_cast<uint32_t*>(counters.as<unsigned long long>() + 2);
-    route_kernel<<<ceil_div_u32(uint64_t(E) + 1, kRouteThreads * kRouteUnroll),
+    unsigned long long* counters = lvc.as<unsigned long long>() + 4 * size_t(level);
+    uint32_t* vcount = reinterpret_cast<uint32_t*>(counters + 2);
+    route_kernel<<<grid_of(uint64_t(En) + 1, kRouteThreads * kRouteUnroll, 12),
                    kRouteThreads, 0, s>>>(
-        E, level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(),
+        En, level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(),
         eg[cur]->as<uint32_t>(), g1.as<double>(), g2.as<double>(),
         t.first.as<uint32_t>(), t.last.as<uint32_t>(), prefix, req.rng_mode,
         req.seed, qrow.as<uint32_t>(), out.row_off.as<uint64_t>(),
         out.row_cnt.as<uint32_t>(), out.leaf_src.as<uint32_t>(),
         out.leaf_cnt.as<uint32_t>(), tl.as<uint32_t>(),
-        flags.as<unsigned long long>(), counters.as<unsigned long long>(),
+        flags.as<unsigned long long>(), counters,
         level == 0 ? nullptr : elm[cur]->as<float>(),
         self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
-        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p);
+        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p, dEp);
     FSGG_LAUNCH_CHECK();
     if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
         smax_level >= kTieBatchMinNode) {
@@ -1466,7 +1770,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
             level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
             g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
             prefix, ds.buf("s.tie_sorted", 4).as<uint32_t>(), vcount, tl.as<uint32_t>(),
-            flags.as<unsigned long long>(), counters.as<unsigned long long>(), wk);
+            flags.as<unsigned long long>(), counters, wk);
         FSGG_LAUNCH_CHECK();
         ds.launches += 1;
       }
@@ -1481,24 +1785,40 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
         while (kd < 10 && level + kd + 1 <= t.depth && (smax_level >> (kd + 1)) >= 256) ++kd;
         const uint32_t max_chunks = 1u << kd;
         const uint32_t max_ties = kTieSplitItems / max_chunks;
+        if (max_chunks == 1) {  // one pass: sums, re-decision (no partial buffer)
+          tie_onepass_kernel<D, FAM><<<ds.num_sms * 8, kTieSplitThreads, 0, s>>>(
+              ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
+              et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(),
+              t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), boxes,
+              vlist.as<uint32_t>(), vcount, g1.as<double>(), g2.as<double>(), prefix,
+              tl.as<uint32_t>(), flags.as<unsigned long long>(), counters, wk);
+          ds.launches += 1;
+          return;
+        }
         DevBuf& part = ds.buf("s.tie_part", size_t(kTieSplitItems) * 16);
         tie_split_kernel<D, FAM><<<ds.num_sms * 8, kTieSplitThreads, 0, s>>>(
             ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
             eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
             t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
             max_chunks, max_ties, part.as<double>());
-        tie_split_reduce_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
-            vlist.as<uint32_t>(), vcount, max_chunks, max_ties, part.as<double>(),
-            g1.as<double>(), g2.as<double>());
-        // overflow ties (more than the partial buffer holds): one CTA each
-        exact_sums_lowd_kernel<D, FAM><<<ds.num_sms * 4, 256, 0, s>>>(
-            ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
-            eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
-            t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
-            g1.as<double>(), g2.as<double>(), max_ties);
+        // overflow ties (more than the partial buffer holds): one CTA each,
+        // launched only when the level can have that many
+        if (uint64_t(En) > max_ties) {
+          exact_sums_lowd_kernel<D, FAM><<<ds.num_sms * 4, 256, 0, s>>>(
+              ds.pts.as<float>(), ks.sigma, ks.scale, level, t.depth, eq[cur]->as<uint32_t>(),
+              eg[cur]->as<uint32_t>(), lm, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+              t.lo.as<float>(), t.hi.as<float>(), boxes, vlist.as<uint32_t>(), vcount,
+              g1.as<double>(), g2.as<double>(), max_ties);
+          ds.launches += 1;
+        }
+        tie_finish_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
+            level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+            g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+            prefix, vlist.as<uint32_t>(), vcount, max_chunks, max_ties, part.as<double>(),
+            tl.as<uint32_t>(), flags.as<unsigned long long>(), counters, wk);
         ds.launches += 2;
       });
-      if (!lowd_done)
+      if (!lowd_done) {
         exact_sums_kernel<<<ds.num_sms * 4, 256, 0, s>>>(
             ds.pts.as<float>(), ds.d, ks.family, ks.sigma, ks.scale, level, t.depth,
             eq[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
@@ -1506,28 +1826,27 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
             t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
             t.has_boxes && req.prune ? 1 : 0, vlist.as<uint32_t>(), vcount, g1.as<double>(),
             g2.as<double>());
+        FSGG_LAUNCH_CHECK();
+        reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
+            level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+            g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
+            prefix, vlist.as<uint32_t>(), vcount, tl.as<uint32_t>(),
+            flags.as<unsigned long long>(), counters, wk);
+        ds.launches += 2;
+      }
       FSGG_LAUNCH_CHECK();
-      reroute_kernel<<<ds.num_sms, 256, 0, s>>>(
-          level, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
-          g1.as<double>(), g2.as<double>(), t.first.as<uint32_t>(), t.last.as<uint32_t>(),
-          prefix, vlist.as<uint32_t>(), vcount, tl.as<uint32_t>(),
-          flags.as<unsigned long long>(), counters.as<unsigned long long>(), wk);
-      FSGG_LAUNCH_CHECK();
-      ds.launches += 2;
     }
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[2], s));
-    size_t tmp_bytes = 0;
-    FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
-        nullptr, tmp_bytes, flags.as<unsigned long long>(),
-        P.as<unsigned long long>(), uint64_t(E) + 1, s));
-    cub_tmp.ensure(tmp_bytes, s);
-    FSGG_CUDA(cub::DeviceScan::ExclusiveSum(
-        cub_tmp.as<void>(), tmp_bytes, flags.as<unsigned long long>(),
-        P.as<unsigned long long>(), uint64_t(E) + 1, s));
+    if (level + 1 > kMaxLevelsLog) throw NumericError("descent exceeded the level log");
+    flags_scan_kernel<<<grid_of(uint64_t(En) + 1, kScanTile, 4), kScanThreads, 0, s>>>(
+        dE, flags.as<unsigned long long>(), P.as<unsigned long long>(), tstate.as<uint32_t>(),
+        tagg.as<unsigned long long>(), tinc.as<unsigned long long>(), tctr + level, level + 1,
+        elog.as<uint32_t>() + level + 1);
+    FSGG_LAUNCH_CHECK();
     const int nxt = cur ^ 1;
-    scatter_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
-        E, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
+    scatter_kernel<<<grid_of(En, 256, 16), 256, 0, s>>>(
+        En, eq[cur]->as<uint32_t>(), et[cur]->as<uint32_t>(), eg[cur]->as<uint32_t>(),
         tl.as<uint32_t>(), flags.as<unsigned long long>(), goff[cur]->as<uint32_t>(),
         P.as<unsigned long long>(), g1.as<double>(), g2.as<double>(), eq[nxt]->as<uint32_t>(),
         et[nxt]->as<uint32_t>(), eg[nxt]->as<uint32_t>(), elm[nxt]->as<float>(),
@@ -1535,7 +1854,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
         wk ? wq.as<uint32_t>() : nullptr, wh.as<uint32_t>(), welm.as<float>(),
         wcount.as<uint32_t>(), wrow.as<uint32_t>(), wrm.as<float>(),
         level == 0 ? nullptr : elm[cur]->as<float>(),
-        self_rows && row_depth == 2 ? 1 : 0);
+        self_rows && row_depth == 2 ? 1 : 0, dEp);
     FSGG_LAUNCH_CHECK();
     if (level < t.depth) {
       goff_kernel<<<ceil_div_u32(uint64_t(G) + 1, 256), 256, 0, s>>>(
@@ -1545,17 +1864,23 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
       ds.launches++;
     }
     ds.launches += 3;
+    cur = nxt;
+    if (lite) {  // next level: count on the device, bounded by 2 E and the tickets
+      E_known = false;
+      E_hi = std::min<uint64_t>(2 * E_hi, cap);
+      continue;
+    }
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[3], s));
     unsigned long long* host = ds.host_words();
-    FSGG_CUDA(cudaMemcpyAsync(host, counters.as<void>(), 24, cudaMemcpyDeviceToHost, s));
-    FSGG_CUDA(cudaMemcpyAsync(host + 3, P.as<unsigned long long>() + E, 8,
+    FSGG_CUDA(cudaMemcpyAsync(host, counters, 24, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(host + 3), dE + 1, 4,
                               cudaMemcpyDeviceToHost, s));
     FSGG_CUDA(cudaStreamSynchronize(s));
     out.tickets_per_level.push_back(host[0]);
     out.degenerate_draws += host[1];
     out.tie_verified += host[2] & 0xffffffffull;
-    const uint64_t next = uint64_t(host[3] >> 32) + uint64_t(host[3] & 0xffffffffull);
+    const uint64_t next = *reinterpret_cast<const uint32_t*>(host + 3);
     if (next > cap) throw NumericError("entry list overflow");
     if (next > 0 && level >= t.depth)
       throw NumericError("tickets remain below the deepest level");
@@ -1573,7 +1898,27 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
                    (unsigned long long)(host[2] & 0xffffffffull));
     }
     E = static_cast<uint32_t>(next);
-    cur = nxt;
+    E_hi = E;
+  }
+  if (lite) {
+    // per-level statistics of the sync-free descent (one read)
+    std::vector<uint32_t> hE(kMaxLevelsLog + 2);
+    std::vector<unsigned long long> hc(size_t(kMaxLevelsLog) * 4);
+    FSGG_CUDA(cudaMemcpyAsync(hE.data(), elog.as<void>(), hE.size() * 4, cudaMemcpyDeviceToHost,
+                              s));
+    FSGG_CUDA(cudaMemcpyAsync(hc.data(), lvc.as<void>(), hc.size() * 8, cudaMemcpyDeviceToHost,
+                              s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    for (uint32_t l = 0; l < levels_run; ++l) {
+      if (hE[l] == 0) break;
+      if (hE[l] > cap) throw NumericError("entry list overflow");
+      out.entries_per_level.push_back(hE[l]);
+      out.peak_entries = std::max<uint64_t>(out.peak_entries, hE[l]);
+      out.tickets_per_level.push_back(hc[4 * l]);
+      out.degenerate_draws += hc[4 * l + 1];
+      out.tie_verified += hc[4 * l + 2] & 0xffffffffull;
+    }
+    if (hE[levels_run] > 0) throw NumericError("tickets remain below the deepest level");
   }
   {
     // reference-equivalent work served by lookups; direct-level evaluations
