@@ -55,13 +55,13 @@ typedef struct fsgg_kernel {
 } fsgg_kernel;
 
 /* Mirrors fsg::SparsifierConfig (proj/include/fsg/sparsifier.hpp:14-26).
- * `epsilon` and the KDE backend selection are accepted for ABI parity but
- * the device always computes exact kernel sums (epsilon() == 0). */
+ * `epsilon` is read by the fast backend only (kde_backend below); the exact
+ * backend, the default, reports epsilon 0 as the reference's does. */
 typedef struct fsgg_config {
   double C;                  /* default 1 */
   double lambda_k1_estimate; /* default 1 */
   uint32_t rounds;           /* 0 = ceil(6 C log(n) / lambda) */
-  double epsilon;            /* ignored by the exact device path */
+  double epsilon;            /* FSGG_KDE_FAST budget (0 = default_epsilon(n)) */
   int log_base;              /* 0 = log2 (default), 1 = natural */
   uint64_t seed;             /* default 1 */
   int rng_mode;              /* FSGG_RNG_REFERENCE (default) | FSGG_RNG_PHILOX */
@@ -497,6 +497,17 @@ int fsgg_shard_root_prepare(fsgg_dataset* ds, const fsgg_kernel* kernel,
 int fsgg_shard_root_export(fsgg_dataset* ds, uint32_t* records_device);
 int fsgg_shard_root_receive(fsgg_dataset* ds, const uint32_t* records_device,
                             uint64_t num_records);
+/* Phase 1 for the row-sharded finish: the descent of fsgg_sample_shard,
+ * then the shard's pair keys (u << 32 | v, u < v, self samples dropped,
+ * duplicates kept, unsorted) grouped by the rank owning row u under
+ * `bounds` (world + 1 entries, 0 .. n, host; world <= 64): counts[r] keys for
+ * rank r, in rank order, at out->pairs — ready for one all-to-all, no sort
+ * on the sending side (the owner's fsgg_finish_graph sorts and dedupes).
+ * out->num_pairs is their total. */
+int fsgg_sample_shard_routed(fsgg_dataset* ds, const fsgg_kernel* kernel,
+                             const fsgg_config* cfg, uint32_t world, const uint32_t* bounds,
+                             uint64_t* counts, fsgg_shard* out, fsgg_report* report);
+
 /* Phase 2 after the caller all-gathers g_full (n doubles, device) and the
  * shards' pair keys (concatenated, device, any order, duplicates allowed):
  * dedupe, weight, CSR and degrees exactly as the 1-GPU path. */
@@ -517,6 +528,12 @@ int fsgg_finish_graph(fsgg_dataset* ds, const fsgg_kernel* kernel,
  *       its own rows — summed in exactly the 1-GPU order.
  * All pointers are device pointers on the handle's device. */
 int fsgg_rows_transposed(fsgg_dataset* ds, uint32_t* v_device, double* w_device);
+/* The rank's slice of the gathered graph's row_ptr: row_ptr[row_begin ..
+ * row_end) of its rows plus edge_offset (the edges of the ranks before it),
+ * row_end - row_begin entries (device); concatenated in rank order plus the
+ * total edge count they form the global upper CSR row_ptr. */
+int fsgg_rows_row_ptr(fsgg_dataset* ds, uint32_t row_begin, uint32_t row_end,
+                      uint64_t edge_offset, uint64_t* row_ptr_device);
 int fsgg_rows_degrees(fsgg_dataset* ds, const uint32_t* lower_v_device,
                       const double* lower_w_device, uint64_t num_lower, uint32_t row_begin,
                       uint32_t row_end, double* degrees_device);

@@ -215,6 +215,11 @@ _SIGS = {
                                                   C.c_double, C.c_uint64, C.c_int, _P, _P, _P]),
     "fsgg_make_gmm_device": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_double,
                                        C.c_uint64, C.c_int, _P, _P, _P]),
+    "fsgg_sample_shard_routed": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.POINTER(fsgg_config),
+                                           C.c_uint32, C.POINTER(C.c_uint32),
+                                           C.POINTER(C.c_uint64), C.POINTER(fsgg_shard),
+                                           C.POINTER(fsgg_report)]),
+    "fsgg_rows_row_ptr": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint64, _P]),
     "fsgg_sample_shard": (C.c_int, [_P, C.POINTER(fsgg_kernel), C.POINTER(fsgg_config),
                                     C.POINTER(fsgg_shard), C.POINTER(fsgg_report)]),
     "fsgg_probe_ex2_throughput": (C.c_int, [C.c_int, C.POINTER(C.c_double),

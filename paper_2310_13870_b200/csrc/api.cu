@@ -207,9 +207,12 @@ struct BuildOut {
 };
 
 // Descent over the configured query shard; fills res (and optionally keys).
+// route_world > 0: the pair keys are grouped by the owner of row u under
+// route_bounds (fsgg_sample_shard_routed) instead of sorted and deduplicated.
 void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& cfg,
                  uint32_t L, uint32_t qb, uint32_t qe, fsgg::SampleResult& res,
-                 fsgg::DevBuf& keys, uint64_t* npairs, BuildOut& bo) {
+                 fsgg::DevBuf& keys, uint64_t* npairs, BuildOut& bo, uint32_t route_world = 0,
+                 const uint32_t* route_bounds = nullptr, uint64_t* route_counts = nullptr) {
   fsgg::Dataset& ds = h->ds;
   const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
   double t0 = now();
@@ -244,7 +247,9 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   req.want_root_sums = true;
   fsgg::sample_counted(ds, ks, req, res);
   double t2 = now();
-  *npairs = fsgg::collapse_pairs(ds, res, keys, &bo.self, &bo.sampled);
+  *npairs = route_world ? fsgg::collapse_pairs_routed(ds, res, keys, route_world, route_bounds,
+                                                      route_counts, &bo.self, &bo.sampled)
+                       : fsgg::collapse_pairs(ds, res, keys, &bo.self, &bo.sampled);
   double t3 = now();
   bo.t_tree = t1 - t0;
   bo.t_sample = t2 - t1;
@@ -990,6 +995,53 @@ int fsgg_sample_shard(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_con
   });
 }
 
+int fsgg_sample_shard_routed(fsgg_dataset* h, const fsgg_kernel* kernel,
+                             const fsgg_config* cfgp, uint32_t world, const uint32_t* bounds,
+                             uint64_t* counts, fsgg_shard* out, fsgg_report* report) {
+  return guarded([&] {
+    activate(h);
+    validate_kernel(kernel);
+    if (!out || !bounds || !counts) throw fsgg::ConfigError("null argument");
+    if (world == 0 || world > 64) throw fsgg::ConfigError("world size must be 1..64");
+    fsgg_config cfg = cfgp ? *cfgp : default_config();
+    fsgg::Dataset& ds = h->ds;
+    if (ds.n < 2) throw fsgg::ConfigError("similarity graph needs n >= 2");
+    if (bounds[0] != 0 || bounds[world] != ds.n)
+      throw fsgg::ConfigError("shard bounds must cover [0, n)");
+    for (uint32_t r = 0; r < world; ++r)
+      if (bounds[r] > bounds[r + 1]) throw fsgg::ConfigError("shard bounds must be sorted");
+    uint32_t qb = cfg.query_begin, qe = cfg.query_end;
+    if (qb == 0 && qe == 0) qe = ds.n;
+    if (qb > qe || qe > ds.n) throw fsgg::ConfigError("invalid query shard");
+    BuildOut bo;
+    bo.L = rounds_for(cfg, ds.n);
+    double t0 = now();
+    if (!h->shard) h->shard = std::make_unique<fsgg::SampleResult>();
+    uint64_t npairs = 0;
+    for (uint32_t r = 0; r < world; ++r) counts[r] = 0;
+    if (qe > qb) {
+      run_descent(h, kernel, cfg, bo.L, qb, qe, *h->shard, h->shard_keys, &npairs, bo, world,
+                  bounds, counts);
+    } else {
+      h->shard->groot.ensure(8, ds.stream);
+      h->shard_keys.ensure(8, ds.stream);
+      h->shard->nq = 0;
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->query_begin = qb;
+    out->query_end = qe;
+    out->rounds = bo.L;
+    out->num_pairs = npairs;
+    h->shard_npairs = npairs;
+    out->pairs = h->shard_keys.as<uint64_t>();
+    out->g_full = h->shard->groot.as<double>();
+    out->sampled_pairs = bo.sampled;
+    out->self_pairs = bo.self;
+    out->degenerate_draws = bo.degenerate;
+    if (report) finish_report(report, ds, bo, nullptr, now() - t0);
+  });
+}
+
 int fsgg_shard_bounds(fsgg_dataset* h, const fsgg_kernel* kernel, uint32_t world,
                       uint32_t* bounds) {
   return guarded([&] {
@@ -1112,6 +1164,17 @@ int fsgg_rows_transposed(fsgg_dataset* h, uint32_t* v_device, double* w_device) 
     if (!h->graph) throw fsgg::ConfigError("no graph on this handle: finish one first");
     if (h->graph->m && (!v_device || !w_device)) throw fsgg::ConfigError("null argument");
     fsgg::rows_transposed(h->ds, *h->graph, v_device, w_device);
+  });
+}
+
+int fsgg_rows_row_ptr(fsgg_dataset* h, uint32_t row_begin, uint32_t row_end,
+                      uint64_t edge_offset, uint64_t* row_ptr_device) {
+  return guarded([&] {
+    activate(h);
+    if (!h->graph) throw fsgg::ConfigError("no graph on this handle: finish one first");
+    if (row_begin > row_end || row_end > h->ds.n) throw fsgg::ConfigError("invalid row range");
+    if (row_end > row_begin && !row_ptr_device) throw fsgg::ConfigError("null argument");
+    fsgg::rows_row_ptr(h->ds, *h->graph, row_begin, row_end, edge_offset, row_ptr_device);
   });
 }
 

@@ -397,6 +397,13 @@ struct GraphResult {
 // self samples counted into *self_pairs. Returns count.
 uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
                         uint64_t* self_pairs, uint64_t* sampled_pairs);
+// Multi-GPU variant: the shard's pair keys ((u << 32) | v, u < v, self
+// samples dropped, duplicates kept, unsorted) grouped by the rank owning row
+// u under bounds (world + 1 entries, host): counts[r] keys for rank r, in
+// rank order. Returns the total. The owner sorts and dedupes what it gets.
+uint64_t collapse_pairs_routed(Dataset& ds, SampleResult& res, DevBuf& keys, uint32_t world,
+                               const uint32_t* bounds_host, uint64_t* counts,
+                               uint64_t* self_pairs, uint64_t* sampled_pairs);
 
 // Row-sharded finish (multi-GPU): the graph's (v, w) stable-sorted by v
 // (the degree contributions the owner of v needs), and the degrees of rows
@@ -405,6 +412,10 @@ void rows_transposed(Dataset& ds, const GraphResult& g, uint32_t* v_out, double*
 void rows_degrees(Dataset& ds, const GraphResult& g, const uint32_t* lower_v,
                   const double* lower_w, uint64_t nlower, uint32_t rb, uint32_t re,
                   double* deg_out);
+// row_ptr[rb .. re) of the rank's rows shifted by the edges of the ranks
+// before it: the rank's slice of the gathered graph's global row_ptr.
+void rows_row_ptr(Dataset& ds, const GraphResult& g, uint32_t rb, uint32_t re,
+                  uint64_t edge_offset, uint64_t* out);
 
 // Host destination of a graph streamed out while it is finished: each
 // array's device-to-host copy starts (on its own stream) as soon as the

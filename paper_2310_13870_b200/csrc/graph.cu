@@ -15,6 +15,8 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <vector>
+
 #include "engine.cuh"
 
 namespace fsgg {
@@ -240,7 +242,161 @@ uint64_t sort_unique_compact(Dataset& ds, DevBuf& keys, uint64_t m,
   return u;
 }
 
+// Shard keys by the owner of row u (multi-GPU finish): destination of a
+// compact key = the rank whose [bounds[r], bounds[r+1]) holds its u.
+constexpr int kRouteKeyThreads = 256;
+constexpr int kRouteKeyItems = 8;
+constexpr uint32_t kMaxWorld = 64;
+
+__device__ __forceinline__ uint32_t key_dest(uint32_t u, const uint32_t* sb, uint32_t world) {
+  uint32_t r = 0;
+  while (r + 1 < world && u >= sb[r + 1]) ++r;
+  return r;
+}
+
+__global__ void __launch_bounds__(kRouteKeyThreads)
+    key_dest_count_kernel(const unsigned long long* __restrict__ keys, uint64_t m, uint32_t bits,
+                          const uint32_t* __restrict__ bounds, uint32_t world,
+                          unsigned long long* __restrict__ counts) {
+  __shared__ uint32_t sb[kMaxWorld + 1];
+  __shared__ unsigned long long hist[kMaxWorld];
+  for (uint32_t k = threadIdx.x; k <= world; k += blockDim.x) sb[k] = bounds[k];
+  for (uint32_t k = threadIdx.x; k < world; k += blockDim.x) hist[k] = 0;
+  __syncthreads();
+  // warp-aggregated: lanes with the same destination add once (most keys of
+  // a tile share one, and same-address shared atomics serialise)
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint64_t e0 = blockIdx.x * uint64_t(blockDim.x); e0 < m;
+       e0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t e = e0 + threadIdx.x;
+    const unsigned long long k = e < m ? keys[e] : ~0ull;
+    const uint32_t dst = k != ~0ull ? key_dest(uint32_t(k >> bits), sb, world) : kMaxWorld;
+    const unsigned grp = __match_any_sync(0xffffffffu, dst);
+    if (dst < kMaxWorld && lane == uint32_t(__ffs(grp) - 1))
+      atomicAdd(&hist[dst], static_cast<unsigned long long>(__popc(grp)));
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < world; k += blockDim.x)
+    if (hist[k]) atomicAdd(counts + k, hist[k]);
+}
+
+// One tile per CTA: per-destination counts in shared memory, one global
+// reservation per destination, then the public keys (u << 32 | v) written
+// into their destination's range (order within it is irrelevant: the owner
+// sorts what it receives).
+__global__ void __launch_bounds__(kRouteKeyThreads)
+    key_dest_scatter_kernel(const unsigned long long* __restrict__ keys, uint64_t m,
+                            uint32_t bits, const uint32_t* __restrict__ bounds, uint32_t world,
+                            unsigned long long* __restrict__ cursor,
+                            unsigned long long* __restrict__ out) {
+  __shared__ uint32_t sb[kMaxWorld + 1];
+  __shared__ uint32_t cnt[kMaxWorld];
+  __shared__ unsigned long long base[kMaxWorld];
+  for (uint32_t k = threadIdx.x; k <= world; k += blockDim.x) sb[k] = bounds[k];
+  const uint64_t tile = uint64_t(kRouteKeyThreads) * kRouteKeyItems;
+  const unsigned long long mask = (1ull << bits) - 1;
+  for (uint64_t t0 = blockIdx.x * tile; t0 < m; t0 += uint64_t(gridDim.x) * tile) {
+    for (uint32_t k = threadIdx.x; k < world; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
+    unsigned long long key[kRouteKeyItems];
+    uint32_t dst[kRouteKeyItems], slot[kRouteKeyItems];
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < kRouteKeyItems; ++j) {
+      const uint64_t e = t0 + uint64_t(j) * kRouteKeyThreads + threadIdx.x;
+      key[j] = e < m ? keys[e] : ~0ull;
+      dst[j] = key[j] != ~0ull ? key_dest(uint32_t(key[j] >> bits), sb, world) : kMaxWorld;
+      // warp-aggregated slot reservation per destination
+      const unsigned grp = __match_any_sync(0xffffffffu, dst[j]);
+      const uint32_t leader = __ffs(grp) - 1;
+      uint32_t b0 = 0;
+      if (dst[j] < kMaxWorld && lane == leader) b0 = atomicAdd(&cnt[dst[j]], uint32_t(__popc(grp)));
+      b0 = __shfl_sync(0xffffffffu, b0, leader);
+      slot[j] = b0 + __popc(grp & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < world; k += blockDim.x)
+      base[k] = cnt[k] ? atomicAdd(cursor + k, static_cast<unsigned long long>(cnt[k])) : 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRouteKeyItems; ++j)
+      if (dst[j] < kMaxWorld)
+        out[base[dst[j]] + slot[j]] = ((key[j] >> bits) << 32) | (key[j] & mask);
+    __syncthreads();
+  }
+}
+
 }  // namespace
+
+__global__ void shifted_slice_kernel(const uint64_t* __restrict__ in, uint32_t count,
+                                     uint64_t shift, uint64_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = in[i] + shift;
+}
+
+void rows_row_ptr(Dataset& ds, const GraphResult& g, uint32_t rb, uint32_t re,
+                  uint64_t edge_offset, uint64_t* out) {
+  if (re <= rb) return;
+  cudaStream_t s = ds.stream;
+  shifted_slice_kernel<<<ceil_div_u32(re - rb, 256), 256, 0, s>>>(
+      g.row_ptr.as<uint64_t>() + rb, re - rb, edge_offset, out);
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+  FSGG_CUDA(cudaStreamSynchronize(s));
+}
+
+uint64_t collapse_pairs_routed(Dataset& ds, SampleResult& res, DevBuf& keys, uint32_t world,
+                               const uint32_t* bounds_host, uint64_t* counts,
+                               uint64_t* self_pairs, uint64_t* sampled_pairs) {
+  if (world == 0 || world > kMaxWorld) throw ConfigError("world size must be 1..64");
+  cudaStream_t s = ds.stream;
+  const uint64_t cap = std::max<uint64_t>(res.total_tickets, 1);
+  const uint32_t bits = index_bits(ds.n);
+  DevBuf& raw = ds.buf("g.raw_keys", cap * 8);
+  keys.ensure(cap * 8, s);
+  DevBuf& aux = ds.buf("g.route_aux", (kMaxWorld + 2) * 4 + 2 * kMaxWorld * 8);
+  uint32_t* dbounds = aux.as<uint32_t>();
+  unsigned long long* dcounts =
+      reinterpret_cast<unsigned long long*>(aux.as<char>() + (kMaxWorld + 1) * 4 + 4);
+  unsigned long long* dcursor = dcounts + kMaxWorld;
+  DevBuf& counters = ds.buf("g.counters", 16);
+  FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
+  FSGG_CUDA(cudaMemsetAsync(dcounts, 0, kMaxWorld * 8, s));
+  FSGG_CUDA(cudaMemcpyAsync(dbounds, bounds_host, size_t(world + 1) * 4, cudaMemcpyHostToDevice,
+                            s));
+  rows_to_keys_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(
+      res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(),
+      res.row_cnt.as<uint32_t>(), res.leaf_src.as<uint32_t>(),
+      res.leaf_cnt.as<uint32_t>(), bits, raw.as<unsigned long long>(),
+      counters.as<unsigned long long>());
+  const uint64_t m = res.total_tickets;
+  const uint32_t grid = std::max<uint32_t>(
+      1, std::min<uint32_t>(ceil_div_u32(m, uint64_t(kRouteKeyThreads) * kRouteKeyItems),
+                            uint32_t(ds.num_sms) * 8));
+  key_dest_count_kernel<<<grid, kRouteKeyThreads, 0, s>>>(raw.as<unsigned long long>(), m, bits,
+                                                          dbounds, world, dcounts);
+  FSGG_LAUNCH_CHECK();
+  unsigned long long hc[2 + kMaxWorld];
+  FSGG_CUDA(cudaMemcpyAsync(hc, counters.as<void>(), 16, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(hc + 2, dcounts, size_t(world) * 8, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  *self_pairs = hc[0];
+  *sampled_pairs = hc[1];
+  std::vector<unsigned long long> off(world);
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < world; ++r) {
+    counts[r] = hc[2 + r];
+    off[r] = total;
+    total += hc[2 + r];
+  }
+  FSGG_CUDA(cudaMemcpyAsync(dcursor, off.data(), size_t(world) * 8, cudaMemcpyHostToDevice, s));
+  key_dest_scatter_kernel<<<grid, kRouteKeyThreads, 0, s>>>(
+      raw.as<unsigned long long>(), m, bits, dbounds, world, dcursor,
+      keys.as<unsigned long long>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches += 3;
+  return total;
+}
 
 uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
                         uint64_t* self_pairs, uint64_t* sampled_pairs) {

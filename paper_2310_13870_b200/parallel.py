@@ -116,13 +116,25 @@ def exchange_root(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig, bounds: li
     return recs.numel() * 4
 
 
-def allgather_varlen(t: torch.Tensor, group=None) -> torch.Tensor:
-    """All-gather 1-D tensors of different lengths, concatenated in rank order."""
+def gather_sizes(n: int, device, group=None) -> list[int]:
     world = dist.get_world_size(group)
-    cnt = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    cnt = torch.tensor([n], dtype=torch.int64, device=device)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
-    sizes = [int(c.item()) for c in counts]
+    return [int(c.item()) for c in counts]
+
+
+def allgather_varlen(t: torch.Tensor, group=None, sizes: list[int] | None = None) -> torch.Tensor:
+    """All-gather 1-D tensors of different lengths, concatenated in rank order.
+    NCCL gathers the uneven pieces directly into one buffer; gloo (CPU
+    tests) needs equal sizes, so pieces are padded there."""
+    world = dist.get_world_size(group)
+    if sizes is None:
+        sizes = gather_sizes(t.numel(), t.device, group)
+    out = torch.empty(sum(sizes), dtype=t.dtype, device=t.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather(list(torch.split(out, sizes)), t.contiguous(), group=group)
+        return out
     cap = max(max(sizes), 1)
     padded = torch.zeros(cap, dtype=t.dtype, device=t.device)
     padded[: t.numel()] = t
@@ -177,6 +189,27 @@ def sample_shard(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig):
     return sh, BuildReport._from_c(rep), pairs, g
 
 
+def sample_shard_routed(ds: Dataset, kernel: Kernel, cfg: SparsifierConfig, bounds: list[int]):
+    """fsgg_sample_shard_routed: the shard's descent and its pair keys grouped
+    by the owner of row u (unsorted, no dedup on the sending side); returns
+    (shard, report, pairs, per-destination counts, g_full slice)."""
+    k = kernel._c()
+    c = cfg._c()
+    world = len(bounds) - 1
+    b = (C.c_uint32 * (world + 1))(*bounds)
+    counts = (C.c_uint64 * world)()
+    sh = N.fsgg_shard()
+    rep = N.fsgg_report()
+    N.check(N.lib().fsgg_sample_shard_routed(ds._h, C.byref(k), C.byref(c), world, b, counts,
+                                             C.byref(sh), C.byref(rep)))
+    dev = torch.device("cuda", ds.device)
+    pairs = torch.empty(int(sh.num_pairs), dtype=torch.int64, device=dev)
+    g = torch.empty(int(sh.query_end - sh.query_begin), dtype=torch.float64, device=dev)
+    N.check(N.lib().fsgg_shard_export(ds._h, C.c_void_p(pairs.data_ptr() if pairs.numel() else 0),
+                                      C.c_void_p(g.data_ptr() if g.numel() else 0)))
+    return sh, BuildReport._from_c(rep), pairs, [int(x) for x in counts], g
+
+
 def finish_graph(ds: Dataset, kernel: Kernel, rounds: int, g_full: torch.Tensor,
                  pairs: torch.Tensor):
     k = kernel._c()
@@ -191,12 +224,14 @@ def finish_graph(ds: Dataset, kernel: Kernel, rounds: int, g_full: torch.Tensor,
 
 def finish_rows(ds: Dataset, kernel: Kernel, rounds: int, g_full: torch.Tensor,
                 pairs: torch.Tensor, row_begin: int, row_end: int, bounds: list[int],
-                group=None):
+                group=None, counts: list[int] | None = None):
     """Phase 2 of the row-sharded finish on one rank: `pairs` are this
-    shard's sorted unique keys; returns (rows graph tensors, degrees of the
-    rank's rows, report)."""
+    shard's keys grouped by destination (`counts` per rank, from
+    sample_shard_routed) or sorted (then split at the bounds); returns (rows
+    graph tensors, degrees of the rank's rows, report)."""
     dev = torch.device("cuda", ds.device)
-    routed = alltoall_varlen(pairs, owner_splits(pairs >> 32, bounds), group)
+    splits = counts if counts is not None else owner_splits(pairs >> 32, bounds)
+    routed = alltoall_varlen(pairs, splits, group)
     graph, frep = finish_graph(ds, kernel, rounds, g_full, routed)
     m = int(graph.num_edges)
     v = torch.empty(m, dtype=torch.int32, device=dev)
@@ -233,10 +268,10 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
     qb, qe = bounds[rank], bounds[rank + 1]
     shard_cfg = replace(cfg, query_begin=qb, query_end=qe)
     root_bytes = exchange_root(ds, kernel, shard_cfg, bounds, group)
-    sh, srep, pairs, g = sample_shard(ds, kernel, shard_cfg)
-    g_full = allgather_varlen(g, group)
+    sh, srep, pairs, counts, g = sample_shard_routed(ds, kernel, shard_cfg, bounds)
+    g_full = allgather_varlen(g, group, [bounds[r + 1] - bounds[r] for r in range(world)])
     rows, deg, frep, moved = finish_rows(ds, kernel, int(sh.rounds), g_full, pairs, qb, qe,
-                                         bounds, group)
+                                         bounds, group, counts)
     frep.sampled_pairs = srep.sampled_pairs
     frep.self_pairs_discarded = srep.self_pairs_discarded
     frep.degenerate_draws = srep.degenerate_draws
@@ -251,14 +286,20 @@ def build_similarity_graph_distributed(ds: Dataset, kernel: Kernel,
                             exchange_bytes=g_full.numel() * 8 + moved + root_bytes,
                             gathered=False)
     if gather:
-        res.u = allgather_varlen(rows["u"], group)
-        res.v = allgather_varlen(rows["v"], group)
-        res.w = allgather_varlen(rows["w"], group)
-        res.degrees = allgather_varlen(deg, group)
-        counts = torch.bincount(res.u.to(torch.int64), minlength=n)
-        res.row_ptr = torch.zeros(n + 1, dtype=torch.int64, device=res.u.device)
-        res.row_ptr[1:] = torch.cumsum(counts, 0)
+        m_all = gather_sizes(rows["u"].numel(), rows["u"].device, group)
+        res.u = allgather_varlen(rows["u"], group, m_all)
+        res.v = allgather_varlen(rows["v"], group, m_all)
+        res.w = allgather_varlen(rows["w"], group, m_all)
+        row_sizes = [bounds[r + 1] - bounds[r] for r in range(world)]
+        res.degrees = allgather_varlen(deg, group, row_sizes)
+        # global upper CSR: each rank's row_ptr slice shifted by the edges of
+        # the ranks before it (fsgg_rows_row_ptr), gathered in rank order
+        rp = torch.empty(qe - qb, dtype=torch.int64, device=res.u.device)
+        N.check(N.lib().fsgg_rows_row_ptr(ds._h, qb, qe, sum(m_all[:rank]),
+                                          C.c_void_p(rp.data_ptr() if rp.numel() else 0)))
+        total = torch.tensor([sum(m_all)], dtype=torch.int64, device=res.u.device)
+        res.row_ptr = torch.cat([allgather_varlen(rp, group, row_sizes), total])
         res.gathered = True
-        res.exchange_bytes += res.u.numel() * 16 + n * 8
+        res.exchange_bytes += res.u.numel() * 16 + n * 16
     res.num_edges = int(res.v.numel())
     return res

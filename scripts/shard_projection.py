@@ -3,7 +3,7 @@
 The descent has no collective (parallel.py), so what rank r of N does is a
 function of its query range alone: this script runs each rank's shard
 descent (owner-mode root: fsgg_shard_root_prepare + the records the other
-ranks owe it + fsgg_sample_shard) and its row-sharded finish (fsgg_finish_graph on
+ranks owe it + fsgg_sample_shard_routed) and its row-sharded finish (fsgg_finish_graph on
 the keys routed to it + fsgg_rows_transposed + fsgg_rows_degrees) one after
 another on one GPU, times each with a device sync on both sides (best of
 `--reps`), and reports max over ranks per phase. The NCCL exchanges are not
@@ -78,6 +78,7 @@ def main():
         cfgs = [F.SparsifierConfig(rounds=L, seed=1, query_begin=bounds[r],
                                    query_end=bounds[r + 1]) for r in range(world)]
         sample_s, root_s, pairs, gs, prep_s, recv_s, rec_bytes = [], [], [], [], [], [], []
+        key_counts = []
         for rep_i in range(a.reps):
             recs = []
             for r in range(world):
@@ -98,12 +99,13 @@ def main():
                 t, _ = timed(lambda: parallel.receive_root(handles[d], inbox), 1)
                 recv_s.append(t)
             for r in range(world):
-                t, (sh, rep, pr, g) = timed(lambda: parallel.sample_shard(handles[r], k, cfgs[r]),
-                                            1)
+                t, (sh, rep, pr, cnt, g) = timed(lambda: parallel.sample_shard_routed(
+                    handles[r], k, cfgs[r], bounds), 1)
                 if rep_i == 0:
                     sample_s.append(t)
                     root_s.append(rep.kde_root_seconds)
                     pairs.append(pr)
+                    key_counts.append(cnt)
                     gs.append(g)
                 else:
                     sample_s[r] = min(sample_s[r], t)
@@ -112,8 +114,8 @@ def main():
         sample_s = [sample_s[r] + prep_s[r] + recv_s[r] for r in range(world)]
         g_full = torch.cat(gs)
         routed = [[] for _ in range(world)]
-        for t in pairs:
-            for d, piece in enumerate(torch.split(t, parallel.owner_splits(t >> 32, bounds))):
+        for src, t in enumerate(pairs):
+            for d, piece in enumerate(torch.split(t, key_counts[src])):
                 routed[d].append(piece)
         routed = [torch.cat(x) for x in routed]
         finish_s, lower_bytes, vs, ws = [], [], [], []
@@ -148,9 +150,8 @@ def main():
                 bounds[d + 1], C.c_void_p(deg.data_ptr()))), a.reps)
             deg_s.append(t)
         ds = handles[0]
-        key_bytes = [sum(x.numel() for i, x in enumerate(
-            torch.split(pairs[s], parallel.owner_splits(pairs[s] >> 32, bounds))) if i != s) * 8
-            for s in range(world)]
+        key_bytes = [sum(c for i, c in enumerate(key_counts[s]) if i != s) * 8
+                     for s in range(world)]
         per_rank = [sample_s[r] + finish_s[r] + deg_s[r] for r in range(world)]
         w_out = {
             "sample_s": sample_s, "root_kernel_s": root_s, "finish_s": finish_s,

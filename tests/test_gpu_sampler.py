@@ -352,8 +352,9 @@ def test_owner_mode_root_is_bit_identical(world):
     assert np.array_equal(g.w, full.w) and np.array_equal(g.degrees, full.degrees)
 
 
+@pytest.mark.parametrize("routed", [False, True], ids=["sorted", "routed"])
 @pytest.mark.parametrize("n,world", [(3000, 2), (3500, 3), (14000, 5)])
-def test_row_sharded_finish_is_bit_identical(n, world):
+def test_row_sharded_finish_is_bit_identical(n, world, routed):
     """The multi-GPU finish split by rows (parallel.finish_rows' exchanges
     emulated in-process, one dataset handle per rank): pairs routed to the
     owner of u, rows deduped and weighted there, (v, w) routed to the owner
@@ -369,27 +370,33 @@ def test_row_sharded_finish_is_bit_identical(n, world):
     full = F.build_similarity_graph(F.Dataset(p), k, F.SparsifierConfig(rounds=L, seed=3))
     bounds = parallel.shard_bounds(n, world)
     handles = [F.Dataset(p) for _ in range(world)]
-    pairs, gs = [], []
+    pairs, gs, key_counts = [], [], []
     for r in range(world):
-        sh, _, pr, g = parallel.sample_shard(
-            handles[r], k, F.SparsifierConfig(rounds=L, seed=3, query_begin=bounds[r],
-                                              query_end=bounds[r + 1]))
+        cfg_r = F.SparsifierConfig(rounds=L, seed=3, query_begin=bounds[r],
+                                   query_end=bounds[r + 1])
+        if routed:  # keys grouped by destination, unsorted (fsgg_sample_shard_routed)
+            sh, _, pr, cnt, g = parallel.sample_shard_routed(handles[r], k, cfg_r, bounds)
+            assert sum(cnt) == pr.numel()
+            key_counts.append(cnt)
+        else:
+            sh, _, pr, g = parallel.sample_shard(handles[r], k, cfg_r)
         pairs.append(pr)
         gs.append(g)
     g_full = torch.cat(gs)
 
-    def route(chunks, keyfn):  # emulated all_to_all: dest d gets slices in source order
+    def route(chunks, keyfn, counts=None):  # emulated all_to_all, source order
         out = [[] for _ in range(world)]
-        for t in chunks:
-            splits = parallel.owner_splits(keyfn(t), bounds)
+        for src, t in enumerate(chunks):
+            splits = counts[src] if counts else parallel.owner_splits(keyfn(t), bounds)
             for d, piece in enumerate(torch.split(t, splits)):
                 out[d].append(piece)
         return out
 
-    routed = [torch.cat(x) for x in route(pairs, lambda t: t >> 32)]
+    routed_keys = [torch.cat(x) for x in route(pairs, lambda t: t >> 32,
+                                               key_counts if routed else None)]
     vs, ws, rows = [], [], []
     for d in range(world):
-        graph, _ = parallel.finish_graph(handles[d], k, L, g_full, routed[d])
+        graph, _ = parallel.finish_graph(handles[d], k, L, g_full, routed_keys[d])
         m = int(graph.num_edges)
         v = torch.empty(m, dtype=torch.int32, device="cuda")
         w = torch.empty(m, dtype=torch.float64, device="cuda")
@@ -418,6 +425,16 @@ def test_row_sharded_finish_is_bit_identical(n, world):
     w = np.concatenate([r.w for r in rows])
     assert np.array_equal(u, full.u) and np.array_equal(v, full.v)
     assert w.tobytes() == full.w.tobytes()
+    # global row_ptr from the ranks' shifted slices (fsgg_rows_row_ptr)
+    off, slices = 0, []
+    for d in range(world):
+        rp = torch.empty(bounds[d + 1] - bounds[d], dtype=torch.int64, device="cuda")
+        N.check(N.lib().fsgg_rows_row_ptr(handles[d]._h, bounds[d], bounds[d + 1], off,
+                                          C.c_void_p(rp.data_ptr() if rp.numel() else 0)))
+        slices.append(rp.cpu().numpy())
+        off += len(rows[d].u)
+    row_ptr = np.concatenate(slices + [np.array([off])])
+    assert np.array_equal(row_ptr.astype(np.uint64), full.row_ptr.astype(np.uint64))
     assert np.concatenate(degs).tobytes() == full.degrees.tobytes()
 
 
