@@ -199,6 +199,24 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Expanded-form distances for the gaussian at d >= FSGG_SYM_EXP_MIN_D:
+// |q - x|^2 = |q|^2 + |x|^2 - 2 q.x with the tile-relative scaled
+// coordinates, so a pair costs d + 1 packed FMA-pipe operations instead of
+// 2d (d FADD2 + d FMUL2/FFMA2) — the FMA pipe, not MUFU, bound the d = 5
+// tile (ncu: FMA-pipe cycles 74%, XU 47%). The cancellation error is
+// ~eps_f32 * (|q'|^2 + |x'|^2) in the exponent, |q'|, |x'| measured from the
+// midpoint of the two blocks' boxes (the pair's own scale for the near
+// pairs that carry the sums), far below the tie guard's 1e-4 margin.
+// Per tile, and only when its scaled coordinates are small: max |q'|^2 +
+// max |x'|^2 <= kSymExpMaxNorm over the tile's points (the error is ~7e-8 x
+// that bound, relative, per term); wide blocks (sparse data, small sigma)
+// keep the direct form. The choice depends on the two blocks alone
+// (shard-safe).
+#ifndef FSGG_SYM_EXP_MIN_D
+#define FSGG_SYM_EXP_MIN_D 3
+#endif
+constexpr float kSymExpMaxNorm = 64.f;
+
 template <int D, int FAM, int ROWS, bool OWN>
 __device__ __forceinline__ void sym_tile_body(
     const float* __restrict__ pts, float cs, const SymTile* __restrict__ tiles,
@@ -209,7 +227,9 @@ __device__ __forceinline__ void sym_tile_body(
   constexpr int kSymRows = ROWS;
   constexpr int kSymWarps = ROWS / 2;
   constexpr uint32_t kCap = 32u * ROWS;
-  __shared__ __align__(16) float2 sx[kCap * D];
+  constexpr bool EXP_OK = FAM == 0 && D >= FSGG_SYM_EXP_MIN_D;
+  constexpr int SW = EXP_OK ? D + 1 : D;  // float2 per source in shared memory
+  __shared__ __align__(16) float2 sx[kCap * SW];
   __shared__ float rowred[kSymWarps][kCap];
   __shared__ float colv[kCap];
   const SymTile tl = tiles[blockIdx.x];
@@ -221,28 +241,98 @@ __device__ __forceinline__ void sym_tile_body(
   // less on the FMA pipe, which shares the binding with the XU pipe. The
   // local origin keeps the scaled values small (pre-scaling absolute
   // coordinates lost accuracy for data far from the origin).
+  // (expanded form: origin midway between the two blocks' box centres, which
+  // keeps |q'|^2 + |x'|^2 — the scale of its cancellation error — near the
+  // pair distances themselves)
   float c0[D];
+  bool use_exp = false;
+  if constexpr (EXP_OK) {
+    __shared__ float s_max[2][kCap / 32];
 #pragma unroll
-  for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
+    for (int k = 0; k < D; ++k)
+      c0[k] = 0.25f * ((__ldg(lo + size_t(tl.I) * D + k) + __ldg(hi + size_t(tl.I) * D + k)) +
+                       (__ldg(lo + size_t(tl.J) * D + k) + __ldg(hi + size_t(tl.J) * D + k)));
+    // largest scaled norm among I's points and among J's points
+    float mi = 0.f, mj = 0.f;
+    for (uint32_t t = threadIdx.x; t < kCap; t += blockDim.x) {
+      float a = 0.f, b = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float u = t < ni ? (__ldg(pts + size_t(fi + t) * D + k) - c0[k]) * cs : 0.f;
+        const float v = t < nj ? (__ldg(pts + size_t(fj + t) * D + k) - c0[k]) * cs : 0.f;
+        a = fmaf(u, u, a);
+        b = fmaf(v, v, b);
+      }
+      mi = fmaxf(mi, a);
+      mj = fmaxf(mj, b);
+    }
+    for (int o = 16; o; o >>= 1) {
+      mi = fmaxf(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+      mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_max[0][threadIdx.x >> 5] = mi;
+      s_max[1][threadIdx.x >> 5] = mj;
+    }
+    __syncthreads();
+    mi = mj = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSymWarps; ++k) {
+      mi = fmaxf(mi, s_max[0][k]);
+      mj = fmaxf(mj, s_max[1][k]);
+    }
+    use_exp = mi + mj <= kSymExpMaxNorm;
+  }
+  if (!use_exp) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
+  }
   // sources of J, negated and duplicated; slots past nj sit far away (their
-  // terms underflow to 0), so the unrolled source loop needs no guard
-  for (uint32_t idx = threadIdx.x; idx < kCap * D; idx += blockDim.x) {
-    const float v =
-        idx < nj * D ? -((__ldg(pts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
-    sx[idx] = make_float2(v, v);
+  // terms underflow to 0), so the unrolled source loop needs no guard.
+  // Expanded form: -2 x'_k duplicated, then |x'|^2 (absent: 1e30, x' = 0).
+  if (use_exp) {
+    for (uint32_t j = threadIdx.x; j < kCap; j += blockDim.x) {
+      float nrm = 1e30f;
+      float xv[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) xv[k] = 0.f;
+      if (j < nj) {
+        nrm = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          xv[k] = (__ldg(pts + size_t(fj + j) * D + k) - c0[k]) * cs;
+          nrm = fmaf(xv[k], xv[k], nrm);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) sx[j * SW + k] = make_float2(-2.f * xv[k], -2.f * xv[k]);
+      sx[j * SW + D] = make_float2(nrm, nrm);
+    }
+  } else {
+    for (uint32_t idx = threadIdx.x; idx < kCap * D; idx += blockDim.x) {
+      const float v =
+          idx < nj * D ? -((__ldg(pts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
+      sx[(idx / D) * SW + idx % D] = make_float2(v, v);
+    }
   }
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // this lane's rows (points of I) as 4 packed pairs; absent rows far away
   float2 q2[kSymRows / 2][D];
+  float2 qn[EXP_OK ? kSymRows / 2 : 1];  // expanded form: |q'|^2 of each row pair
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) {
     const uint32_t r0 = lane * kSymRows + 2 * p, r1 = r0 + 1;
+    float na = 0.f, nb = 0.f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : 1e18f;
-      const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : 1e18f;
+      const float far = use_exp ? 0.f : 1e18f;
+      const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : far;
+      const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : far;
       q2[p][k] = make_float2(a, b);
+      na = fmaf(a, a, na);
+      nb = fmaf(b, b, nb);
     }
+    if constexpr (EXP_OK) qn[p] = make_float2(r0 < ni ? na : 1e30f, r1 < ni ? nb : 1e30f);
   }
   __syncthreads();
   float2 racc[kSymRows / 2];
@@ -252,18 +342,27 @@ __device__ __forceinline__ void sym_tile_body(
   // per lane (not 32) keep the kernel at 62 registers, 8 CTAs per SM — the
   // extra shuffles cost less than the occupancy buys (32: 30.0 ms, 16: 29.6,
   // 8: 28.9, 4: 30.1 on C3)
+  auto tile_loop = [&](auto exp_tag) {
+  constexpr bool EXP = decltype(exp_tag)::value;
   for (uint32_t jb = w * 64; jb < w * 64 + 64 && jb < nj; jb += 8) {
     float c[8];  // this lane's 8-row partial of each source's column sum
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
-      const float2* x = sx + (jb + jj) * D;
+      const float2* x = sx + (jb + jj) * SW;
       float2 es = make_float2(0.f, 0.f);
 #pragma unroll
       for (int p = 0; p < kSymRows / 2; ++p) {
-        float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+        float2 t;
+        if constexpr (EXP) {
+          t = __fadd2_rn(qn[p], x[D]);
 #pragma unroll
-        for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
-        t = fam_finish<FAM>(t);
+          for (int k = 0; k < D; ++k) t = __ffma2_rn(q2[p][k], x[k], t);
+        } else {
+          t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+#pragma unroll
+          for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
+          t = fam_finish<FAM>(t);
+        }
         const float2 e = make_float2(ex2_approx(-t.x), ex2_approx(-t.y));
         racc[p] = __fadd2_rn(racc[p], e);
         es = p == 0 ? e : __fadd2_rn(es, e);
@@ -288,6 +387,15 @@ __device__ __forceinline__ void sym_tile_body(
       }
     }
     if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
+  }
+  };
+  if constexpr (EXP_OK) {
+    if (use_exp)
+      tile_loop(std::true_type{});
+    else
+      tile_loop(std::false_type{});
+  } else {
+    tile_loop(std::false_type{});
   }
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) {
