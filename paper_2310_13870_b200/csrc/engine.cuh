@@ -228,6 +228,10 @@ bool kde_tc_supported(const Dataset& ds, int family);
 // block; blk_off must have been computed with 128 entries per block.
 // Partials: one per (entry, sub-chunk at depth sdepth below each child),
 // row width 2^(sdepth+1).
+// Symmetric tensor-core root (each pair once) for a full build's level 0;
+// false when it does not apply (kde_tc_tiled then runs the one-sided pass).
+bool kde_tc_root_symmetric(Dataset& ds, const KernelSpec& ks, const LevelView& lv, uint32_t rl,
+                           double* partials, uint64_t* performed);
 void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
                   const uint32_t* blk_off, uint32_t cdepth, uint32_t sdepth, uint64_t items,
                   double* partials);

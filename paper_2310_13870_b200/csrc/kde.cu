@@ -948,6 +948,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     FSGG_CUDA(cudaEventCreate(&ws.ev1));
   }
   unsigned long long* d_perf = d_evals + 1;
+  uint64_t tc_sym_perf = 0;  // pair evaluations of the symmetric tensor-core root
   FSGG_CUDA(cudaMemsetAsync(d_perf, 0, 8, s));
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
   const bool sym = Lb > 0 && kde_root_symmetric(ds, ks, lv.qbase, lv.qbase + E, rl, partials,
@@ -961,7 +962,9 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
       op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub);
     });
   } else if (tc) {
-    kde_tc_tiled(ds, ks, lv, nb, c, sd, items, partials);
+    // full build: the symmetric root (each pair once, both row sums)
+    if (!kde_tc_root_symmetric(ds, ks, lv, rl, partials, &tc_sym_perf))
+      kde_tc_tiled(ds, ks, lv, nb, c, sd, items, partials);
   } else {
     with_family(ks.family, [&](auto fam) {
       constexpr int FAM = decltype(fam)::value;
@@ -991,7 +994,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   }
   FSGG_LAUNCH_CHECK();
   ds.launches += 2;
-  unsigned long long perf = ev;
+  unsigned long long perf = tc_sym_perf ? tc_sym_perf : ev;
   if (lowd) FSGG_CUDA(cudaMemcpyAsync(&perf, d_perf, 8, cudaMemcpyDeviceToHost, s));
   FSGG_CUDA(cudaStreamSynchronize(s));
   float ms = 0.f;

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "engine.cuh"
 
@@ -37,6 +38,8 @@ constexpr int kTcThreads = 256;
 constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or lo)
 constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
 constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 512;
+// symmetric root: + the epilogue's column partials [4 warps][3 buckets][128]
+constexpr int kSmemSymBytes = kTcStages * kStageBytes + 1024 + 4 * 3 * 128 * 4 + 16 + 1024;
 constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
 constexpr uint32_t kTcGroup = 64;                       // entry blocks per L2 group
 constexpr int kRing = 8;          // work-item ring (persistent kernel)
@@ -502,6 +505,351 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// ---- symmetric root (level 0 of a full build, d >= kTcMinDim) ------------
+// Every pair once: the points are cut into 128-point tiles on a fixed grid,
+// a work item is (query tile I, source tiles [J0, J1)) with J0 >= I, and the
+// epilogue of each 128 x 128 accumulator yields both
+//   * row sums (I's points over J's sources), split at J's bucket
+//     boundaries — as the one-sided kernel does, and
+//   * column sums (J's points over I's points, J > I), split at I's bucket
+//     boundaries: per warp a masked butterfly transpose-reduction for each
+//     bucket among its 32 rows, then the four warps' partials added in warp
+//     order through shared memory.
+// Buckets are the root row's tree nodes at depth rl (<= 128 points, so a
+// bucket meets at most two tiles): a bucket inside one tile is stored, the
+// two parts of a straddling bucket are added to the zeroed row with fp64
+// atomics — two addends, so the sum is the same in either order. Every
+// value depends on its two tiles only: deterministic, and it halves the
+// tensor-core work of the n^2 pass.
+constexpr uint32_t kTcSymR = 8;     // source tiles per work item
+constexpr uint32_t kTcSymGI = 32;   // tiles per side of an L2 block of items
+constexpr int kTcSymMaxSegW = 3;    // buckets among a warp's 32 rows (>= 16 points each)
+// 12 warps: the one-sided kernel's 8 roles, with warps 4-7 taking the row
+// sums and warps 8-11 the column sums of the same accumulator (each group
+// reads it from TMEM and evaluates the exponentials itself — same
+// instructions, same bits): the column side's cross-lane reductions run
+// beside the row side instead of after it (one epilogue group left the
+// MMAs waiting on TMEM: 22.9 ms vs 17.8 ms without the column side)
+constexpr int kTcSymThreads = 384;
+constexpr int kTcSymRingReaders = 10;  // MMA thread, query warp, 8 epilogue warps
+
+__device__ __forceinline__ void flush_bucket(double* __restrict__ prow, uint32_t b, float acc,
+                                             bool whole) {
+  if (whole)
+    prow[b] = double(acc);
+  else
+    atomicAdd(prow + b, double(acc));
+}
+
+template <int FAM>
+__global__ void __launch_bounds__(kTcSymThreads, 1)
+    kde_tc_sym_kernel(const __grid_constant__ CUtensorMap map_hi,
+                      const __grid_constant__ CUtensorMap map_lo, const float* __restrict__ norm,
+                      uint32_t d_pad, uint32_t n, const uint32_t* __restrict__ sitems,
+                      uint32_t items, uint32_t* __restrict__ next_item,
+                      const uint32_t* __restrict__ tile_b0, const uint32_t* __restrict__ bfirst,
+                      const uint32_t* __restrict__ blast, uint32_t rl, float scale,
+                      double* __restrict__ partials, int terms) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kTcStages;
+  uint64_t* tfull = bars + 2 * kTcStages;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ring_full = tempty + 2;
+  uint64_t* ring_empty = ring_full + kRing;
+  uint32_t* ring = reinterpret_cast<uint32_t*>(ring_empty + kRing);
+  uint32_t* tmem_slot = ring + kRing;
+  // column partials of the epilogue warps: [warp][bucket slot][column]
+  float* colpart = reinterpret_cast<float*>(smem + kTcStages * kStageBytes + 1024);
+  uint32_t* wfirst = reinterpret_cast<uint32_t*>(colpart + 4 * kTcSymMaxSegW * kTcN);  // [4]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t kblocks = d_pad / kTcKB;
+  auto next = [&](uint32_t k) -> uint32_t {
+    const uint32_t slot = k % kRing;
+    mbar_wait(&ring_full[slot], (k / kRing) & 1u);
+    return ring[slot];
+  };
+  auto release = [&](uint32_t k) { mbar_arrive(&ring_empty[k % kRing]); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 256);
+    }
+    for (int r = 0; r < kRing; ++r) {
+      mbar_init(&ring_full[r], 1);
+      mbar_init(&ring_empty[r], kTcSymRingReaders);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---- TMA producer: source tiles J0 .. J1-1 ---------------------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t slot = k % kRing;
+        mbar_wait(&ring_empty[slot], ((k / kRing) & 1u) ^ 1u);
+        const uint32_t item = atomicAdd(next_item, 1u);
+        ring[slot] = item;
+        mbar_arrive(&ring_full[slot]);
+        if (item >= items) break;
+        const uint32_t J0 = sitems[3 * item + 1], J1 = sitems[3 * item + 2];
+        const uint32_t total = (J1 - J0) * kblocks;
+        for (uint32_t j = 0; j < total; ++j, ++it) {
+          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+          const uint32_t tile = j / kblocks, kb = j % kblocks;
+          mbar_wait(&empty[s], ph ^ 1u);
+          unsigned char* st = smem + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+          const int row = int((J0 + tile) * kTcN), col = int(kb * kTcKB);
+          tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
+          tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer ------------------------------------------------------
+    if (lane == 0) {
+      uint32_t it = 0, tg = 0;
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t item = next(k);
+        release(k);
+        if (item >= items) break;
+        const uint32_t nt = sitems[3 * item + 2] - sitems[3 * item + 1];
+        for (uint32_t tile = 0; tile < nt; ++tile, ++tg) {
+          const uint32_t buf = tg & 1u;
+          mbar_wait(&tempty[buf], ((tg >> 1) & 1u) ^ 1u);
+          tc_fence_after();
+          const uint32_t tacc = tmem_base + buf * kTcN;
+          for (uint32_t kb = 0; kb < kblocks; ++kb, ++it) {
+            const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t base = smem_u32(smem + s * kStageBytes);
+#pragma unroll
+            for (int ks = 0; ks < kTcKB / 8; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint64_t a_hi = sw128_desc(base + off);
+              const uint64_t a_lo = sw128_desc(base + kTileBytes + off);
+              const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
+              const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
+              mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
+              if (terms & 1) mma_tf32(tacc, a_hi, b_lo, 1);
+              if (terms & 2) mma_tf32(tacc, a_lo, b_hi, 1);
+            }
+            mma_commit(&empty[s]);
+          }
+          mma_commit(&tfull[buf]);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ---- query tile I (one TMA box per K-block and N-tile) ---------------
+    if (warp == 2) {
+      uint32_t it = 0;
+      for (uint32_t k = 0;; ++k) {
+        const uint32_t item = next(k);
+        __syncwarp();
+        if (lane == 0) release(k);
+        if (item >= items) break;
+        const uint32_t I = sitems[3 * item];
+        const uint32_t total = (sitems[3 * item + 2] - sitems[3 * item + 1]) * kblocks;
+        for (uint32_t j = 0; j < total; ++j, ++it) {
+          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+          const int col = int((j % kblocks) * kTcKB);
+          mbar_wait(&empty[s], ph ^ 1u);
+          unsigned char* st = smem + s * kStageBytes;
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
+            tma_load_2d(st, &map_hi, &full[s], col, int(I * kTcM));
+            tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(I * kTcM));
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp < 8) {
+    // ---- row side (warps 4-7: TMEM lanes = I's rows) ----------------------
+    const uint32_t ew = warp & 3;
+    const uint32_t row = ew * 32 + lane;
+    uint32_t tg = 0;
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t item = next(k);
+      __syncwarp();
+      if (lane == 0) release(k);
+      if (item >= items) break;
+      const uint32_t I = sitems[3 * item], J0 = sitems[3 * item + 1],
+                     J1 = sitems[3 * item + 2];
+      const uint32_t q = I * kTcM + row;
+      const bool qv = q < n;
+      const float qn = norm[qv ? q : n - 1];
+      double* prow = partials + (size_t(q) << rl);
+      for (uint32_t J = J0; J < J1; ++J, ++tg) {
+        const uint32_t buf = tg & 1u;
+        mbar_wait(&tfull[buf], (tg >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t n0 = J * kTcN;
+        const uint32_t valid = min(uint32_t(kTcN), n - n0);
+        uint32_t b = tile_b0[J], bend = blast[b];
+        float acc = 0.f;
+#pragma unroll 1
+        for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
+          float v[32];
+          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) {
+            const uint32_t col = chunk * 32 + kk;
+            if (col < valid) {  // uniform across the warp
+              while (n0 + col >= bend) {  // next bucket (uniform)
+                if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0);
+                acc = 0.f;
+                bend = blast[++b];
+              }
+              const float xn = __ldg(norm + n0 + col);
+              float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
+              if constexpr (FAM == 1) d2 = sqrtf(d2);
+              acc += ex2_approx(-scale * d2);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+        if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0 && bend <= n0 + valid);
+      }
+    }
+  } else {
+    // ---- column side (warps 8-11): J's points over I's buckets ------------
+    const uint32_t ew = warp & 3;
+    const uint32_t row = ew * 32 + lane;
+    const uint32_t ct = row;  // this thread's column in the combine
+    uint32_t tg = 0;
+    for (uint32_t k = 0;; ++k) {
+      const uint32_t item = next(k);
+      __syncwarp();
+      if (lane == 0) release(k);
+      if (item >= items) break;
+      const uint32_t I = sitems[3 * item], J0 = sitems[3 * item + 1],
+                     J1 = sitems[3 * item + 2];
+      const uint32_t q0 = I * kTcM, q = q0 + row;
+      const bool qv = q < n;
+      const uint32_t qend = min(q0 + uint32_t(kTcM), n);
+      const float qn = norm[qv ? q : n - 1];
+      // this row's bucket and the warp's first one (rows past n: the last)
+      uint32_t bq = tile_b0[I];
+      const uint32_t qq = qv ? q : n - 1;
+      while (blast[bq] <= qq) ++bq;
+      const uint32_t bw = __shfl_sync(0xffffffffu, bq, 0);
+      const uint32_t nsw = __shfl_sync(0xffffffffu, bq, 31) - bw + 1;  // <= kTcSymMaxSegW
+      // I's buckets and, per warp, the first one among its rows (for the combine)
+      const uint32_t bI0 = tile_b0[I];
+      uint32_t bIend = bI0;
+      while (bIend < (1u << rl) && bfirst[bIend] < qend) ++bIend;
+      for (uint32_t J = J0; J < J1; ++J, ++tg) {
+        const uint32_t buf = tg & 1u;
+        if (J == I) {  // the diagonal tile's rows hold both directions
+          mbar_wait(&tfull[buf], (tg >> 1) & 1u);
+          tc_fence_before();
+          mbar_arrive(&tempty[buf]);
+          continue;
+        }
+        mbar_wait(&tfull[buf], (tg >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t n0 = J * kTcN;
+        const uint32_t valid = min(uint32_t(kTcN), n - n0);
+#pragma unroll 1
+        for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
+          float v[32];
+          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) {
+            const uint32_t col = chunk * 32 + kk;
+            float e = 0.f;
+            if (col < valid) {
+              const float xn = __ldg(norm + n0 + col);
+              float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
+              if constexpr (FAM == 1) d2 = sqrtf(d2);
+              e = ex2_approx(-scale * d2);
+            }
+            v[kk] = qv ? e : 0.f;
+          }
+          // per bucket among the warp's rows: the warp's sum of each of
+          // these 32 columns (lane l: column chunk*32 + l), fixed butterfly
+          for (uint32_t sgm = 0; sgm < nsw; ++sgm) {
+            float c[32];
+            const bool mine = bq == bw + sgm;
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) c[kk] = mine ? v[kk] : 0.f;
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1) {
+              const bool up = (lane & st) != 0;
+#pragma unroll
+              for (int i = 0; i < st; ++i) {
+                const float keep = up ? c[i + st] : c[i];
+                const float send = up ? c[i] : c[i + st];
+                c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+              }
+            }
+            colpart[(ew * kTcSymMaxSegW + sgm) * kTcN + chunk * 32 + lane] = c[0];
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[buf]);
+        if (lane == 0) wfirst[ew] = bw;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // thread ct: column ct of J over each of I's buckets, warps in order
+        if (ct < valid) {
+          double* xrow = partials + (size_t(n0 + ct) << rl);
+          for (uint32_t bb = bI0; bb < bIend; ++bb) {
+            const uint32_t lo = bfirst[bb], hi = blast[bb];
+            float sum = 0.f;
+#pragma unroll
+            for (uint32_t w = 0; w < 4; ++w) {
+              const uint32_t r0 = q0 + 32 * w;
+              const uint32_t r1 = min(r0 + 32, qend);
+              if (r0 < qend && hi > r0 && lo < r1)
+                sum += colpart[(w * kTcSymMaxSegW + (bb - wfirst[w])) * kTcN + ct];
+            }
+            flush_bucket(xrow, bb, sum, lo >= q0 && hi <= qend);
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
 // ---- host: tensor maps -------------------------------------------------------
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -588,6 +936,93 @@ bool kde_tc_supported(const Dataset& ds, int family) {
     return !(e && e[0] == '0');
   }();
   return enabled && ds.d >= kTcMinDim && family != 2;
+}
+
+// Symmetric root (kde_tc_sym_kernel) for a full build's level 0: partials
+// (n rows of 2^rl fp64 buckets) zeroed and filled; returns false (nothing
+// launched) when the layout does not fit it (a query shard, buckets outside
+// 16..128 points) or FSGG_TC_SYM=0.
+bool kde_tc_root_symmetric(Dataset& ds, const KernelSpec& ks, const LevelView& lv, uint32_t rl,
+                           double* partials, uint64_t* performed) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("FSGG_TC_SYM");
+    return !(e && e[0] == '0');
+  }();
+  const uint32_t n = ds.n;
+  if (!enabled || lv.level != 0 || lv.dE || lv.qbase != 0 || lv.num_entries != n || rl == 0 ||
+      rl > 16 || rl > ds.tree.depth)
+    return false;
+  const TreeTable& t = ds.tree;
+  cudaStream_t s = ds.stream;
+  const uint32_t nb = 1u << rl;
+  const uint64_t hb = (uint64_t(1) << rl) - 1;
+  std::vector<uint32_t> bf(nb), bl(nb);
+  FSGG_CUDA(cudaMemcpyAsync(bf.data(), t.first.as<uint32_t>() + hb, size_t(nb) * 4,
+                            cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(bl.data(), t.last.as<uint32_t>() + hb, size_t(nb) * 4,
+                            cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  for (uint32_t b = 0; b < nb; ++b) {
+    const uint32_t sz = bl[b] - bf[b];
+    if (sz < 16 || sz > uint32_t(kTcN)) return false;  // segments per warp / per tile
+  }
+  TcState& st = tc_state(ds);
+  const uint32_t T = (n + kTcM - 1) / kTcM;
+  std::vector<uint32_t> b0(T);
+  for (uint32_t tt = 0, b = 0; tt < T; ++tt) {
+    while (bl[b] <= tt * uint32_t(kTcM)) ++b;
+    b0[tt] = b;
+  }
+  // items (I, J0, J1), J0 >= I, in blocks of kTcSymGI x kTcSymGI tiles: the
+  // items of one block (about one wave of CTAs) read kTcSymGI query and
+  // kTcSymGI source tiles (2 x 26 MB at C5), which stay in L2 (an order by
+  // query tile alone read 81 GB from DRAM per launch)
+  std::vector<uint32_t> it;
+  uint64_t perf = 0;
+  for (uint32_t a0 = 0; a0 < T; a0 += kTcSymGI) {
+    const uint32_t a1 = std::min(T, a0 + kTcSymGI);
+    for (uint32_t c0 = a0; c0 < T; c0 += kTcSymGI) {
+      const uint32_t c1 = std::min(T, c0 + kTcSymGI);
+      for (uint32_t I = a0; I < a1; ++I)
+        for (uint32_t J0 = std::max(I, c0); J0 < c1; J0 += kTcSymR) {
+          it.push_back(I);
+          it.push_back(J0);
+          it.push_back(std::min(c1, J0 + kTcSymR));
+        }
+    }
+  }
+  for (uint32_t I = 0; I < T; ++I) {
+    const uint64_t rows = std::min<uint64_t>(kTcM, n - uint64_t(I) * kTcM);
+    perf += rows * (uint64_t(n) - uint64_t(I) * kTcM);
+  }
+  const uint32_t items = uint32_t(it.size() / 3);
+  DevBuf& ditems = ds.buf("tc.sym_items", it.size() * 4);
+  DevBuf& db0 = ds.buf("tc.sym_b0", size_t(T) * 4);
+  FSGG_CUDA(cudaMemcpyAsync(ditems.as<void>(), it.data(), it.size() * 4, cudaMemcpyHostToDevice,
+                            s));
+  FSGG_CUDA(cudaMemcpyAsync(db0.as<void>(), b0.data(), size_t(T) * 4, cudaMemcpyHostToDevice, s));
+  FSGG_CUDA(cudaMemsetAsync(partials, 0, (size_t(n) << rl) * 8, s));
+  static bool attr[64] = {};
+  if (ds.device < 64 && !attr[ds.device]) {
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym_kernel<0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSymBytes));
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSymBytes));
+    attr[ds.device] = true;
+  }
+  auto kern = ks.family == 1 ? kde_tc_sym_kernel<1> : kde_tc_sym_kernel<0>;
+  DevBuf& counter = ds.buf("tc.next_item", 8);
+  FSGG_CUDA(cudaMemsetAsync(counter.as<void>(), 0, 4, s));
+  const uint32_t grid = std::min<uint32_t>(items, uint32_t(ds.num_sms));
+  kern<<<grid, kTcSymThreads, kSmemSymBytes, s>>>(
+      st.map_hi, st.map_lo, ds.buf("tc.norm", 8).as<float>(), st.d_pad, n,
+      ditems.as<uint32_t>(), items, counter.as<uint32_t>(), db0.as<uint32_t>(),
+      t.first.as<uint32_t>() + hb, t.last.as<uint32_t>() + hb, rl, ks.scale, partials,
+      tc_terms());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
+  if (performed) *performed = perf;
+  return true;
 }
 
 void kde_tc_tiled(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
