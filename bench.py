@@ -527,11 +527,22 @@ def main():
                                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             except (OSError, ValueError, KeyError, IndexError):
                 traffic = None
+        # symmetric root (kde_tc_sym_kernel): each executed pair evaluation
+        # serves two row sums; the reference evaluates n^2 at the root
+        r_ms = (r_s / K if root_s > 0 else tiled_s / max(tiled_launches, 1)) * 1e3
+        ref_alg = (n * n * 2.0 * w.d) / max(r_ms * 1e-3, 1e-12) / 1e12 if root_s > 0 else alg
         roofline = {
-            "bound": "tensor", "kernel": "kde_tc_kernel<gaussian> (tcgen05.mma kind::tf32, 3xTF32)",
+            "bound": "tensor",
+            "kernel": ("kde_tc_sym_kernel<gaussian> (root level, each pair once; tcgen05.mma "
+                       "kind::tf32, 3xTF32)"),
             "achieved": alg, "peak": tf32_peak, "unit": "TFLOP/s",
             "frac": alg / tf32_peak,
             "executed_tflops": 3.0 * alg, "executed_frac": 3.0 * alg / tf32_peak,
+            "reference_equivalent_tflops": ref_alg,
+            "reference_equivalent_frac": ref_alg / tf32_peak,
+            "reference_equivalent_note": ("2*d FLOPs x n^2 evaluations (the reference's root "
+                                          "pass) / the symmetric launch, which executes each "
+                                          "pair once for both row sums"),
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst, cuBLAS) / 2: dense TF32 is "
                             "half the bf16 rate on Blackwell"),
             "algorithmic_unit": "2*d FLOPs per Gaussian evaluation (dot-product form, SURVEY.md §8d)",

@@ -309,12 +309,28 @@ void build_device(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config*
   if (!h->sample) h->sample = std::make_unique<fsgg::SampleResult>();
   fsgg::SampleResult& res = *h->sample;
   uint64_t npairs = 0;
-  run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, h->keys, &npairs, bo);
+  // host output: the pair keys in u-range chunks, each finished and
+  // streamed to the host while the next is sorted (FSGG_E2E_CHUNKS, 0 = one
+  // pass)
+  const char* ce = std::getenv("FSGG_E2E_CHUNKS");
+  const uint32_t nchunks =
+      sink && !want_estimates ? std::min<uint32_t>(ce ? uint32_t(std::atoi(ce)) : 4u, 64u) : 0u;
+  std::vector<uint32_t> cb;
+  std::vector<uint64_t> ccounts(std::max<uint32_t>(nchunks, 1), 0);
+  if (nchunks > 1) {
+    cb.resize(nchunks + 1);
+    for (uint32_t c = 0; c <= nchunks; ++c) cb[c] = uint32_t(uint64_t(ds.n) * c / nchunks);
+    run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, h->keys, &npairs, bo, nchunks, cb.data(),
+                ccounts.data());
+  } else {
+    run_descent(h, kernel, cfg, bo.L, 0, ds.n, res, h->keys, &npairs, bo);
+  }
   double t1 = now();
   const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
   if (!h->graph) h->graph = std::make_unique<fsgg::GraphResult>();
-  fsgg::finish_graph(ds, ks, bo.L, res.groot.as<double>(),
-                     h->keys.as<uint64_t>(), npairs, true, want_estimates, *h->graph, sink);
+  fsgg::finish_graph(ds, ks, bo.L, res.groot.as<double>(), h->keys.as<uint64_t>(), npairs,
+                     true, want_estimates, *h->graph, sink, nchunks > 1 ? ccounts.data() : nullptr,
+                     nchunks > 1 ? nchunks : 0);
   double t2 = now();
   bo.t_graph += t2 - t1;
   if (report) finish_report(report, ds, bo, h->graph.get(), t2 - t0 + bo.t_tree * 0);

@@ -434,9 +434,13 @@ struct HostSink {
 };
 
 // Dedupe (keys may repeat across shards), weight, CSR, degrees.
+// With chunks (nchunks u-range partitions of unsorted keys, in order, from
+// collapse_pairs_routed): each chunk finished and streamed to the sink on
+// its own (no estimates), identical output.
 void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
                   const double* g_full, const uint64_t* keys, uint64_t nkeys,
                   bool keys_sorted_unique, bool want_estimates,
-                  GraphResult& out, const HostSink* sink = nullptr);
+                  GraphResult& out, const HostSink* sink = nullptr,
+                  const uint64_t* chunks = nullptr, uint32_t nchunks = 0);
 
 }  // namespace fsgg

@@ -428,10 +428,196 @@ uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
   return m;
 }
 
+// Step 4 of finish_graph (shared by the chunked finish): upper CSR,
+// transposed CSR, degrees, total weight, and their host copies.
+template <class After>
+void finish_tail(Dataset& ds, uint32_t n, uint64_t m, uint32_t bits, GraphResult& out,
+                 const HostSink* sink, After&& after, cudaStream_t cs) {
+  cudaStream_t s = ds.stream;
+  const uint64_t mm = std::max<uint64_t>(m, 1);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  // upper CSR, transposed CSR, degrees, total weight. The transpose is a
+  // stable radix sort on v alone (ceil(log2 n) bits): edges arrive in (u, v)
+  // order, so each vertex's lower neighbours stay in ascending u.
+  out.row_ptr.ensure(size_t(n + 1) * 8, s);
+  out.degrees.ensure(size_t(n) * 8, s);
+  DevBuf& rpt = ds.buf("g.rpt", size_t(n + 1) * 8);
+  DevBuf& tv = ds.buf("g.tv", mm * 4);
+  DevBuf& tv2 = ds.buf("g.tv2", mm * 4);
+  DevBuf& wt = ds.buf("g.wt", mm * 8);
+  DevBuf& wt2 = ds.buf("g.wt2", mm * 8);
+  row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
+      out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
+  FSGG_LAUNCH_CHECK();
+  if (sink) after(sink->row_ptr, out.row_ptr.as<void>(), (uint64_t(n) + 1) * 8);
+  if (m) {
+    FSGG_CUDA(cudaMemcpyAsync(tv.as<void>(), out.v.as<void>(), m * 4, cudaMemcpyDeviceToDevice, s));
+    FSGG_CUDA(cudaMemcpyAsync(wt.as<void>(), out.w.as<void>(), m * 8,
+                              cudaMemcpyDeviceToDevice, s));
+    cub::DoubleBuffer<uint32_t> dk(tv.as<uint32_t>(), tv2.as<uint32_t>());
+    cub::DoubleBuffer<double> dv(wt.as<double>(), wt2.as<double>());
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(bits), s);
+    });
+    row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
+        dk.Current(), m, n, rpt.as<uint64_t>());
+    FSGG_LAUNCH_CHECK();
+    degrees_kernel<<<ceil_div_u32(n, 256), 256, 0, s>>>(
+        n, rpt.as<uint64_t>(), dv.Current(), out.row_ptr.as<uint64_t>(),
+        out.w.as<double>(), out.degrees.as<double>());
+    FSGG_LAUNCH_CHECK();
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceReduce::Sum(t, b, out.w.as<double>(), wt.as<double>(), m, s);
+    });
+    FSGG_CUDA(cudaMemcpyAsync(&out.total_weight, wt.as<void>(), 8,
+                              cudaMemcpyDeviceToHost, s));
+    ds.launches += 12;
+  } else {
+    FSGG_CUDA(cudaMemsetAsync(out.degrees.as<void>(), 0, size_t(n) * 8, s));
+    out.total_weight = 0.0;
+  }
+  if (sink) {
+    after(sink->degrees, out.degrees.as<void>(), size_t(n) * 8);
+    FSGG_CUDA(cudaStreamSynchronize(cs));
+  }
+  FSGG_CUDA(cudaStreamSynchronize(s));
+}
+
+
+// RAII for the host-output side stream: on any throw, the copies into the
+// caller's buffers are finished and the stream/event released before
+// unwinding.
+struct SideStream {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  ~SideStream() {
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+    }
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+
+// finish_graph over u-range chunks of unsorted keys (collapse_pairs_routed
+// with one "rank" per chunk): each chunk is sorted, deduplicated and
+// weighted on its own and appended, and with a HostSink its v and w go to
+// the host while the next chunk is processed — the graph's 0.78 GB
+// device-to-host copy (C3) starts ~1 ms after the descent instead of after a
+// full 64M-key sort. The arrays are the one-pass finish's bit for bit
+// (chunks are disjoint u ranges in order).
+void finish_graph_chunked(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
+                          const double* g_full, const uint64_t* keys_in,
+                          const uint64_t* chunks, uint32_t nchunks, GraphResult& out,
+                          const HostSink* sink) {
+  cudaStream_t s = ds.stream;
+  const uint32_t n = ds.n, d = ds.d;
+  const uint32_t bits = index_bits(n);
+  const float* pts = ds.pts.as<float>();
+  out.n = n;
+  uint64_t total = 0, cmax = 1;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    total += chunks[c];
+    cmax = std::max<uint64_t>(cmax, chunks[c]);
+  }
+  out.u.ensure(std::max<uint64_t>(total, 1) * 4, s);
+  out.v.ensure(std::max<uint64_t>(total, 1) * 4, s);
+  out.w.ensure(std::max<uint64_t>(total, 1) * 8, s);
+  DevBuf& keys = ds.buf("g.keys", cmax * 8);
+  DevBuf& keep = ds.buf("g.keep", cmax);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  DevBuf& cnt = ds.buf("g.cnt", 16);
+  SideStream side;
+  cudaStream_t& cs = side.cs;
+  cudaEvent_t& ev = side.ev;
+  auto after = [&](void* dst, const void* src, size_t bytes) {
+    if (!dst || !bytes) return;
+    FSGG_CUDA(cudaEventRecord(ev, s));
+    FSGG_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+    FSGG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs));
+  };
+  if (sink) {
+    FSGG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    FSGG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  uint64_t m = 0, in = 0;
+  out.underflow = 0;
+  for (uint32_t c = 0; c < nchunks; ++c) {
+    const uint64_t kc = chunks[c];
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(keys_in) + in;
+    in += kc;
+    if (kc == 0) continue;
+    public_to_compact_kernel<<<ceil_div_u32(kc, 256), 256, 0, s>>>(
+        src, keys.as<unsigned long long>(), kc, bits);
+    FSGG_LAUNCH_CHECK();
+    const uint64_t mc = sort_unique_compact(ds, keys, kc, bits);
+    if (mc == 0) continue;
+    compact_to_public_kernel<<<ceil_div_u32(mc, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), mc, bits);
+    FSGG_LAUNCH_CHECK();
+    ds.launches += 2;
+    if (sink && m + mc > sink->capacity)
+      throw ConfigError("host output capacity below the sampled unique pair count");
+    uint32_t* uc = out.u.as<uint32_t>() + m;
+    uint32_t* vc = out.v.as<uint32_t>() + m;
+    double* wc = out.w.as<double>() + m;
+    const bool early_v = sink && sink->v;
+    if (early_v) {
+      keys_to_v_kernel<<<ceil_div_u32(mc, 256), 256, 0, s>>>(keys.as<unsigned long long>(), mc,
+                                                             vc);
+      FSGG_LAUNCH_CHECK();
+      ds.launches++;
+      after(sink->v + m, vc, mc * 4);
+    }
+    FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
+    edges_kernel<<<ceil_div_u32(mc, 256), 256, 0, s>>>(
+        keys.as<unsigned long long>(), mc, pts, d, ks.family, ks.sigma, double(rounds), g_full,
+        uc, vc, wc, nullptr, keep.as<unsigned char>(), cnt.as<unsigned long long>(),
+        early_v ? 0 : 1);
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+    unsigned long long dropped = 0;
+    FSGG_CUDA(cudaMemcpyAsync(&dropped, cnt.as<void>(), 8, cudaMemcpyDeviceToHost, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    if (dropped) {  // underflow pairs (k_ij < 1e-300): compact this chunk (stable)
+      DevBuf& o4 = ds.buf("g.cu", mc * 4);
+      DevBuf& o8 = ds.buf("g.cw", mc * 8);
+      auto compact4 = [&](uint32_t* arr) {
+        cub_call(tmp, s, [&](void* t, size_t& b) {
+          return cub::DeviceSelect::Flagged(t, b, arr, keep.as<unsigned char>(),
+                                            o4.as<uint32_t>(), cnt.as<uint64_t>() + 1, mc, s);
+        });
+        FSGG_CUDA(cudaMemcpyAsync(arr, o4.as<void>(), (mc - dropped) * 4,
+                                  cudaMemcpyDeviceToDevice, s));
+      };
+      compact4(uc);
+      compact4(vc);
+      cub_call(tmp, s, [&](void* t, size_t& b) {
+        return cub::DeviceSelect::Flagged(t, b, wc, keep.as<unsigned char>(), o8.as<double>(),
+                                          cnt.as<uint64_t>() + 1, mc, s);
+      });
+      FSGG_CUDA(cudaMemcpyAsync(wc, o8.as<void>(), (mc - dropped) * 8, cudaMemcpyDeviceToDevice,
+                                s));
+      ds.launches += 3;
+      if (early_v) after(sink->v + m, vc, (mc - dropped) * 4);  // the compacted v
+    }
+    if (sink) after(sink->w + m, wc, (mc - dropped) * 8);
+    m += mc - dropped;
+    out.underflow += dropped;
+  }
+  if (m > uint64_t(n) * rounds)
+    throw NumericError("sparsity invariant violated: more than n*L edges");
+  out.m = m;
+  finish_tail(ds, n, m, bits, out, sink, after, cs);
+}
+
 void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
                   const double* g_full, const uint64_t* keys_in, uint64_t nkeys,
                   bool keys_sorted_unique, bool want_estimates,
-                  GraphResult& out, const HostSink* sink) {
+                  GraphResult& out, const HostSink* sink, const uint64_t* chunks,
+                  uint32_t nchunks) {
+  if (chunks && nchunks)
+    return finish_graph_chunked(ds, ks, rounds, g_full, keys_in, chunks, nchunks, out, sink);
   cudaStream_t s = ds.stream;
   const uint32_t n = ds.n, d = ds.d;
   const uint32_t bits = index_bits(n);
@@ -474,19 +660,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   // on its own stream as soon as the array is final — v right away (it is
   // the keys' low word), w after the weights, row_ptr and degrees after
   // theirs — overlapping the rest of the finish
-  // RAII: on any throw below, the side stream's copies into the caller's
-  // buffers are finished and the stream/event released before unwinding
-  struct SideStream {
-    cudaStream_t cs = nullptr;
-    cudaEvent_t ev = nullptr;
-    ~SideStream() {
-      if (cs) {
-        cudaStreamSynchronize(cs);
-        cudaStreamDestroy(cs);
-      }
-      if (ev) cudaEventDestroy(ev);
-    }
-  } side;
+  SideStream side;
   cudaStream_t& cs = side.cs;
   cudaEvent_t& ev = side.ev;
   auto after = [&](void* dst, const void* src, size_t bytes) {
@@ -561,7 +735,6 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   if (m > uint64_t(n) * rounds)
     throw NumericError("sparsity invariant violated: more than n*L edges");
   out.m = m;
-  const uint64_t mm = std::max<uint64_t>(m, 1);
 
   if (sink) {
     // dropped underflow pairs compacted v: copy it again (after the first
@@ -570,51 +743,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
     after(sink->w, out.w.as<void>(), m * 8);
   }
 
-  // 4. upper CSR, transposed CSR, degrees, total weight. The transpose is a
-  // stable radix sort on v alone (ceil(log2 n) bits): edges arrive in (u, v)
-  // order, so each vertex's lower neighbours stay in ascending u.
-  out.row_ptr.ensure(size_t(n + 1) * 8, s);
-  out.degrees.ensure(size_t(n) * 8, s);
-  DevBuf& rpt = ds.buf("g.rpt", size_t(n + 1) * 8);
-  DevBuf& tv = ds.buf("g.tv", mm * 4);
-  DevBuf& tv2 = ds.buf("g.tv2", mm * 4);
-  DevBuf& wt = ds.buf("g.wt", mm * 8);
-  DevBuf& wt2 = ds.buf("g.wt2", mm * 8);
-  row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
-      out.u.as<uint32_t>(), m, n, out.row_ptr.as<uint64_t>());
-  FSGG_LAUNCH_CHECK();
-  if (sink) after(sink->row_ptr, out.row_ptr.as<void>(), (uint64_t(n) + 1) * 8);
-  if (m) {
-    FSGG_CUDA(cudaMemcpyAsync(tv.as<void>(), out.v.as<void>(), m * 4, cudaMemcpyDeviceToDevice, s));
-    FSGG_CUDA(cudaMemcpyAsync(wt.as<void>(), out.w.as<void>(), m * 8,
-                              cudaMemcpyDeviceToDevice, s));
-    cub::DoubleBuffer<uint32_t> dk(tv.as<uint32_t>(), tv2.as<uint32_t>());
-    cub::DoubleBuffer<double> dv(wt.as<double>(), wt2.as<double>());
-    cub_call(tmp, s, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(t, b, dk, dv, m, 0, int(bits), s);
-    });
-    row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
-        dk.Current(), m, n, rpt.as<uint64_t>());
-    FSGG_LAUNCH_CHECK();
-    degrees_kernel<<<ceil_div_u32(n, 256), 256, 0, s>>>(
-        n, rpt.as<uint64_t>(), dv.Current(), out.row_ptr.as<uint64_t>(),
-        out.w.as<double>(), out.degrees.as<double>());
-    FSGG_LAUNCH_CHECK();
-    cub_call(tmp, s, [&](void* t, size_t& b) {
-      return cub::DeviceReduce::Sum(t, b, out.w.as<double>(), wt.as<double>(), m, s);
-    });
-    FSGG_CUDA(cudaMemcpyAsync(&out.total_weight, wt.as<void>(), 8,
-                              cudaMemcpyDeviceToHost, s));
-    ds.launches += 12;
-  } else {
-    FSGG_CUDA(cudaMemsetAsync(out.degrees.as<void>(), 0, size_t(n) * 8, s));
-    out.total_weight = 0.0;
-  }
-  if (sink) {
-    after(sink->degrees, out.degrees.as<void>(), size_t(n) * 8);
-    FSGG_CUDA(cudaStreamSynchronize(cs));
-  }
-  FSGG_CUDA(cudaStreamSynchronize(s));
+  finish_tail(ds, n, m, bits, out, sink, after, cs);
 }
 
 // ---- row-sharded finish (multi-GPU, parallel.py) ----------------------------
