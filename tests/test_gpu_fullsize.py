@@ -47,8 +47,11 @@ def c3():
 
 
 @pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
-@pytest.mark.parametrize("name", ["C2", "C4"])
+@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
 def test_full_graph_fingerprint_matches_reference(name, dense):
+    """C5 (n = 70k, d = 784) runs the symmetric tcgen05 root (3xTF32) and the
+    tensor-core levels: edge set by SHA-256, weights within 5e-5 (the MMA's
+    fp32 accumulation, test_gpu_fuzz.py) — the north star's bound is 1e-4."""
     m = meta()
     if name not in m:
         pytest.skip(f"no reference fingerprint for {name}")
@@ -64,8 +67,11 @@ def test_full_graph_fingerprint_matches_reference(name, dense):
     z = np.load(os.path.join(GOLDEN, f"{name.lower()}_full.npz"))
     pick = z["pick"]
     assert np.array_equal(g.u[pick], z["u"]) and np.array_equal(g.v[pick], z["v"])
-    assert rel(g.w[pick], z["w"]).max() <= 1e-5
-    assert abs(g.w.sum() / ref["total_weight"] - 1) <= 1e-6
+    tensor = w.d >= 64
+    assert rel(g.w[pick], z["w"]).max() <= (5e-5 if tensor else 1e-5)
+    assert abs(g.w.sum() / ref["total_weight"] - 1) <= (1e-5 if tensor else 1e-6)
+    if tensor:  # the symmetric tensor-core root ran (each pair once)
+        assert 0 < rep.kde_root_performed_evals < w.n * w.n
 
 
 @pytest.mark.parametrize("dense", [False, True], ids=["pruned", "dense"])
