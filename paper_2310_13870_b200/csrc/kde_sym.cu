@@ -215,7 +215,13 @@ __global__ void __launch_bounds__(128)
 #ifndef FSGG_SYM_EXP_MIN_D
 #define FSGG_SYM_EXP_MIN_D 3
 #endif
-constexpr float kSymExpMaxNorm = 64.f;
+#ifndef FSGG_SYM_R10_CTAS
+#define FSGG_SYM_R10_CTAS 4
+#endif
+#ifndef FSGG_SYM_EXP_MAX
+#define FSGG_SYM_EXP_MAX 64.f
+#endif
+constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
 
 template <int D, int FAM, int ROWS, bool OWN>
 __device__ __forceinline__ void sym_tile_body(
@@ -245,57 +251,30 @@ __device__ __forceinline__ void sym_tile_body(
   // keeps |q'|^2 + |x'|^2 — the scale of its cancellation error — near the
   // pair distances themselves)
   float c0[D];
-  bool use_exp = false;
   if constexpr (EXP_OK) {
-    __shared__ float s_max[2][kCap / 32];
 #pragma unroll
     for (int k = 0; k < D; ++k)
       c0[k] = 0.25f * ((__ldg(lo + size_t(tl.I) * D + k) + __ldg(hi + size_t(tl.I) * D + k)) +
                        (__ldg(lo + size_t(tl.J) * D + k) + __ldg(hi + size_t(tl.J) * D + k)));
-    // largest scaled norm among I's points and among J's points
-    float mi = 0.f, mj = 0.f;
-    for (uint32_t t = threadIdx.x; t < kCap; t += blockDim.x) {
-      float a = 0.f, b = 0.f;
-#pragma unroll
-      for (int k = 0; k < D; ++k) {
-        const float u = t < ni ? (__ldg(pts + size_t(fi + t) * D + k) - c0[k]) * cs : 0.f;
-        const float v = t < nj ? (__ldg(pts + size_t(fj + t) * D + k) - c0[k]) * cs : 0.f;
-        a = fmaf(u, u, a);
-        b = fmaf(v, v, b);
-      }
-      mi = fmaxf(mi, a);
-      mj = fmaxf(mj, b);
-    }
-    for (int o = 16; o; o >>= 1) {
-      mi = fmaxf(mi, __shfl_xor_sync(0xffffffffu, mi, o));
-      mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-      s_max[0][threadIdx.x >> 5] = mi;
-      s_max[1][threadIdx.x >> 5] = mj;
-    }
-    __syncthreads();
-    mi = mj = 0.f;
-#pragma unroll
-    for (int k = 0; k < kSymWarps; ++k) {
-      mi = fmaxf(mi, s_max[0][k]);
-      mj = fmaxf(mj, s_max[1][k]);
-    }
-    use_exp = mi + mj <= kSymExpMaxNorm;
-  }
-  if (!use_exp) {
+  } else {
 #pragma unroll
     for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
   }
-  // sources of J, negated and duplicated; slots past nj sit far away (their
-  // terms underflow to 0), so the unrolled source loop needs no guard.
-  // Expanded form: -2 x'_k duplicated, then |x'|^2 (absent: 1e30, x' = 0).
-  if (use_exp) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // sources of J; slots past nj sit far away (their terms underflow to 0),
+  // so the unrolled source loop needs no guard.
+  // Direct form: -x' duplicated. Expanded-capable kernels store -2 x'
+  // (the direct form takes -x' = 0.5 * (-2 x') exactly through one FFMA2)
+  // and |x'|^2 (absent: x' = 1e18, |x'|^2 = 1e30); the largest norms of the
+  // two blocks, gathered on the way, decide the form.
+  __shared__ float s_max[2][kCap / 32];
+  float mi = 0.f, mj = 0.f;
+  if constexpr (EXP_OK) {
     for (uint32_t j = threadIdx.x; j < kCap; j += blockDim.x) {
       float nrm = 1e30f;
       float xv[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) xv[k] = 0.f;
+      for (int k = 0; k < D; ++k) xv[k] = 1e18f;
       if (j < nj) {
         nrm = 0.f;
 #pragma unroll
@@ -303,6 +282,7 @@ __device__ __forceinline__ void sym_tile_body(
           xv[k] = (__ldg(pts + size_t(fj + j) * D + k) - c0[k]) * cs;
           nrm = fmaf(xv[k], xv[k], nrm);
         }
+        mj = fmaxf(mj, nrm);
       }
 #pragma unroll
       for (int k = 0; k < D; ++k) sx[j * SW + k] = make_float2(-2.f * xv[k], -2.f * xv[k]);
@@ -312,11 +292,10 @@ __device__ __forceinline__ void sym_tile_body(
     for (uint32_t idx = threadIdx.x; idx < kCap * D; idx += blockDim.x) {
       const float v =
           idx < nj * D ? -((__ldg(pts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
-      sx[(idx / D) * SW + idx % D] = make_float2(v, v);
+      sx[idx] = make_float2(v, v);
     }
   }
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  // this lane's rows (points of I) as 4 packed pairs; absent rows far away
+  // this lane's rows (points of I) as packed pairs; absent rows far away
   float2 q2[kSymRows / 2][D];
   float2 qn[EXP_OK ? kSymRows / 2 : 1];  // expanded form: |q'|^2 of each row pair
 #pragma unroll
@@ -325,16 +304,39 @@ __device__ __forceinline__ void sym_tile_body(
     float na = 0.f, nb = 0.f;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-      const float far = use_exp ? 0.f : 1e18f;
-      const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : far;
-      const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : far;
+      const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : 1e18f;
+      const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : 1e18f;
       q2[p][k] = make_float2(a, b);
       na = fmaf(a, a, na);
       nb = fmaf(b, b, nb);
     }
-    if constexpr (EXP_OK) qn[p] = make_float2(r0 < ni ? na : 1e30f, r1 < ni ? nb : 1e30f);
+    if constexpr (EXP_OK) {
+      qn[p] = make_float2(r0 < ni ? na : 1e30f, r1 < ni ? nb : 1e30f);
+      if (r0 < ni) mi = fmaxf(mi, na);
+      if (r1 < ni) mi = fmaxf(mi, nb);
+    }
+  }
+  if constexpr (EXP_OK) {
+    for (int o = 16; o; o >>= 1) {
+      mi = fmaxf(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+      mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
+    }
+    if (lane == 0) {
+      s_max[0][w] = mi;
+      s_max[1][w] = mj;
+    }
   }
   __syncthreads();
+  bool use_exp = false;
+  if constexpr (EXP_OK) {
+    mi = mj = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSymWarps; ++k) {
+      mi = fmaxf(mi, s_max[0][k]);
+      mj = fmaxf(mj, s_max[1][k]);
+    }
+    use_exp = mi + mj <= kSymExpMaxNorm;
+  }
   float2 racc[kSymRows / 2];
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) racc[p] = make_float2(0.f, 0.f);
@@ -357,6 +359,12 @@ __device__ __forceinline__ void sym_tile_body(
           t = __fadd2_rn(qn[p], x[D]);
 #pragma unroll
           for (int k = 0; k < D; ++k) t = __ffma2_rn(q2[p][k], x[k], t);
+        } else if constexpr (EXP_OK) {  // -x' = 0.5 * (-2 x'), exactly
+          const float2 h = make_float2(0.5f, 0.5f);
+          t = fam_first<FAM>(__ffma2_rn(h, x[0], q2[p][0]));
+#pragma unroll
+          for (int k = 1; k < D; ++k) t = fam_next<FAM>(__ffma2_rn(h, x[k], q2[p][k]), t);
+          t = fam_finish<FAM>(t);
         } else {
           t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
 #pragma unroll
@@ -440,7 +448,7 @@ __device__ __forceinline__ void sym_tile_body(
 // The kernel for a shard's own tiles (80 registers at d = 2, 6 CTAs per SM)
 // and the one for owner-mode cross-shard tiles (one side exported).
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? 4 : 0)
+__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
     sym_tile_kernel(const float* __restrict__ pts, float cs,
                     const SymTile* __restrict__ tiles,
                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? 4 : 0)
                                      performed, records);
 }
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? 4 : 0)
+__global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
     sym_tile_own_kernel(const float* __restrict__ pts, float cs,
                         const SymTile* __restrict__ tiles,
                         const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,

@@ -521,8 +521,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // atomics — two addends, so the sum is the same in either order. Every
 // value depends on its two tiles only: deterministic, and it halves the
 // tensor-core work of the n^2 pass.
-constexpr uint32_t kTcSymR = 8;     // source tiles per work item
-constexpr uint32_t kTcSymGI = 32;   // tiles per side of an L2 block of items
+#ifndef FSGG_TC_SYM_R
+#define FSGG_TC_SYM_R 8
+#endif
+#ifndef FSGG_TC_SYM_GI
+#define FSGG_TC_SYM_GI 32
+#endif
+constexpr uint32_t kTcSymR = FSGG_TC_SYM_R;     // source tiles per work item
+constexpr uint32_t kTcSymGI = FSGG_TC_SYM_GI;   // tiles per side of an L2 block of items
 constexpr int kTcSymMaxSegW = 3;    // buckets among a warp's 32 rows (>= 16 points each)
 // 12 warps: the one-sided kernel's 8 roles, with warps 4-7 taking the row
 // sums and warps 8-11 the column sums of the same accumulator (each group
