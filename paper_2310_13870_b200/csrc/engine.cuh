@@ -395,6 +395,11 @@ struct GraphResult {
   double total_weight = 0.0;
   uint64_t underflow = 0;
   DevBuf est;  // fsgg_edge_estimate-compatible records (optional)
+  // the finish's transposed order (v ascending, stable: u ascending within
+  // a v) with its weights, in arena buffers valid until the next finish on
+  // the handle: rows_transposed hands them out instead of sorting again
+  const uint32_t* tv_sorted = nullptr;
+  const double* tw_sorted = nullptr;
 };
 
 // Sorted unique pair keys ((u << 32) | v, u < v) from the leaf rows;

@@ -436,6 +436,8 @@ void finish_tail(Dataset& ds, uint32_t n, uint64_t m, uint32_t bits, GraphResult
   cudaStream_t s = ds.stream;
   const uint64_t mm = std::max<uint64_t>(m, 1);
   DevBuf& tmp = ds.buf("g.tmp", 8);
+  out.tv_sorted = nullptr;
+  out.tw_sorted = nullptr;
   // upper CSR, transposed CSR, degrees, total weight. The transpose is a
   // stable radix sort on v alone (ceil(log2 n) bits): edges arrive in (u, v)
   // order, so each vertex's lower neighbours stay in ascending u.
@@ -462,14 +464,19 @@ void finish_tail(Dataset& ds, uint32_t n, uint64_t m, uint32_t bits, GraphResult
     row_ptr_kernel<<<ceil_div_u32(uint64_t(n) + 1, 256), 256, 0, s>>>(
         dk.Current(), m, n, rpt.as<uint64_t>());
     FSGG_LAUNCH_CHECK();
+    out.tv_sorted = dk.Current();
+    out.tw_sorted = dv.Current();
     degrees_kernel<<<ceil_div_u32(n, 256), 256, 0, s>>>(
         n, rpt.as<uint64_t>(), dv.Current(), out.row_ptr.as<uint64_t>(),
         out.w.as<double>(), out.degrees.as<double>());
     FSGG_LAUNCH_CHECK();
+    // (the sum goes to its own word: wt/wt2 hold the transposed weights that
+    // rows_transposed hands out)
+    DevBuf& tot = ds.buf("g.total", 8);
     cub_call(tmp, s, [&](void* t, size_t& b) {
-      return cub::DeviceReduce::Sum(t, b, out.w.as<double>(), wt.as<double>(), m, s);
+      return cub::DeviceReduce::Sum(t, b, out.w.as<double>(), tot.as<double>(), m, s);
     });
-    FSGG_CUDA(cudaMemcpyAsync(&out.total_weight, wt.as<void>(), 8,
+    FSGG_CUDA(cudaMemcpyAsync(&out.total_weight, tot.as<void>(), 8,
                               cudaMemcpyDeviceToHost, s));
     ds.launches += 12;
   } else {
@@ -752,6 +759,12 @@ void rows_transposed(Dataset& ds, const GraphResult& g, uint32_t* v_out, double*
   cudaStream_t s = ds.stream;
   const uint64_t m = g.m;
   if (m == 0) return;
+  if (g.tv_sorted && g.tw_sorted) {  // the finish's own transposed order
+    FSGG_CUDA(cudaMemcpyAsync(v_out, g.tv_sorted, m * 4, cudaMemcpyDeviceToDevice, s));
+    FSGG_CUDA(cudaMemcpyAsync(w_out, g.tw_sorted, m * 8, cudaMemcpyDeviceToDevice, s));
+    FSGG_CUDA(cudaStreamSynchronize(s));
+    return;
+  }
   const uint32_t bits = index_bits(ds.n);
   DevBuf& tmp = ds.buf("g.tmp", 8);
   DevBuf& k2 = ds.buf("rt.k2", m * 4);

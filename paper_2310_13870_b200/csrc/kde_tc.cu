@@ -950,10 +950,8 @@ bool kde_tc_supported(const Dataset& ds, int family) {
 // 16..128 points) or FSGG_TC_SYM=0.
 bool kde_tc_root_symmetric(Dataset& ds, const KernelSpec& ks, const LevelView& lv, uint32_t rl,
                            double* partials, uint64_t* performed) {
-  static const bool enabled = [] {
-    const char* e = std::getenv("FSGG_TC_SYM");
-    return !(e && e[0] == '0');
-  }();
+  const char* env = std::getenv("FSGG_TC_SYM");  // read per call: tests toggle it
+  const bool enabled = !(env && env[0] == '0');
   const uint32_t n = ds.n;
   if (!enabled || lv.level != 0 || lv.dE || lv.qbase != 0 || lv.num_entries != n || rl == 0 ||
       rl > 16 || rl > ds.tree.depth)

@@ -5,7 +5,7 @@ sizes where that is affordable on the build host, and stores compact
 fingerprints (counts, SHA-256 of the sorted edge arrays, weight samples)
 plus query-subset triples for C3, whose full exact run would take hours.
 
-    python tests/golden/make_golden_large.py [C2] [C3] [C4] [C5]
+    python tests/golden/make_golden_large.py [C2] [C3] [C3full] [C4] [C5]
 
 FSG_GOLDEN_THREADS overrides the worker count (default: all host cores).
 """
@@ -74,6 +74,8 @@ def main():
     for name in which:
         if name == "C3":
             meta["C3_queries"] = query_subset(ref, "C3")
+        elif name == "C3full":  # the whole n = 1M exact graph (~2 h on 7 threads)
+            meta["C3"] = full_graph(ref, "C3")
         else:
             meta[name] = full_graph(ref, name)
         print(name, json.dumps(meta.get(name) or meta.get(name + "_queries"))[:300], flush=True)

@@ -51,13 +51,16 @@ def test_gpu_graph_file_round_trips_through_reference_reader(ref, tmp_path):
     assert ours.read_bytes() == theirs.read_bytes()
 
 
-def test_build_into_pinned_buffers_matches_device_build():
+@pytest.mark.parametrize("chunks", ["0", "1", "4", "16"])
+def test_build_into_pinned_buffers_matches_device_build(chunks, monkeypatch):
     """fsgg_build_similarity_graph_into (host buffers filled while the graph
-    is finished) returns exactly the device build's CSR, weights, degrees
-    and total weight."""
+    is finished — in u-range chunks streamed one by one, FSGG_E2E_CHUNKS)
+    returns exactly the device build's CSR, weights, degrees and total
+    weight."""
     import numpy as np
     import paper_2310_13870_b200 as F
     from paper_2310_13870_b200 import datasets
+    monkeypatch.setenv("FSGG_E2E_CHUNKS", chunks)
     p, _ = datasets.make_moons(20000, 0.05, 4)
     ds = F.Dataset(p)
     k = F.Kernel(F.KernelFamily.gaussian, 0.08)

@@ -575,6 +575,78 @@ def test_symmetric_root_matches_one_sided():
     assert r1.kernel_evals_performed < r0.kernel_evals_performed
 
 
+@pytest.mark.parametrize("d", [2, 3])
+def test_sync_free_levels_match_synchronous(d):
+    """Sync-free levels (device entry counts, grid-strided kernels, the
+    look-back flag scan, fused tie kernels; FSGG_SYNC_FREE) give the same
+    samples and the same diagnostics as the per-level synchronous loop —
+    d = 3 also runs the expanded-form root tiles."""
+    import os
+    rng = np.random.default_rng(5)
+    if d == 2:
+        p, _ = datasets.make_moons(60000, 0.05, 11)
+        sigma = 0.06
+    else:
+        p = (rng.normal(0, 0.3, (40000, 3)) + rng.integers(0, 3, (40000, 1))).astype(np.float32)
+        p = p[np.argsort(p[:, 0], kind="stable")]
+        sigma = 0.15
+    ds = F.Dataset(p.astype(np.float32))
+    k = F.Kernel(F.KernelFamily.gaussian, sigma)
+    outs = []
+    old = os.environ.get("FSGG_SYNC_FREE")
+    try:
+        for sf in ("0", "1"):
+            os.environ["FSGG_SYNC_FREE"] = sf
+            tri, diag = F.sample_neighbors_counted(ds, k, np.arange(len(p)), 16, 5,
+                                                   diagnostics=True)
+            g = F.build_similarity_graph(ds, k, F.SparsifierConfig(rounds=16, seed=5))
+            outs.append((tri, diag, g))
+    finally:
+        if old is None:
+            os.environ.pop("FSGG_SYNC_FREE", None)
+        else:
+            os.environ["FSGG_SYNC_FREE"] = old
+    (t0, d0, g0), (t1, d1, g1) = outs
+    assert np.array_equal(t0, t1)
+    assert list(d0.entries_per_level) == list(d1.entries_per_level)
+    assert list(d0.tickets_per_level) == list(d1.tickets_per_level)
+    assert d0.degenerate_draws == d1.degenerate_draws
+    assert np.array_equal(g0.u, g1.u) and np.array_equal(g0.v, g1.v)
+    assert g0.w.tobytes() == g1.w.tobytes() and g0.degrees.tobytes() == g1.degrees.tobytes()
+
+
+def test_symmetric_tensor_core_root_matches_one_sided(oracle):
+    """The symmetric tcgen05 root (kde_tc_sym_kernel, each pair once) and
+    the one-sided tensor-core root (FSGG_TC_SYM=0) give the oracle's edge
+    set; weights within the tensor cores' 5e-5 of it."""
+    import os
+    rng = np.random.default_rng(17)
+    centers = rng.random((4, 130)) * 4
+    lab = rng.integers(0, 4, 3000)
+    p = (centers[lab] + rng.normal(0, 0.3, (3000, 130))).astype(np.float32)
+    p = p[np.argsort(lab, kind="stable")]
+    med = np.median(np.linalg.norm(p[rng.integers(0, 3000, 64)] - p[rng.integers(0, 3000, 64)],
+                                   axis=1))
+    k = F.Kernel(F.KernelFamily.gaussian, float(med))
+    cfg = F.SparsifierConfig(rounds=8, seed=9)
+    ref = oracle.build_graph(p.astype(np.float64), float(med), 8, seed=9)
+    old = os.environ.get("FSGG_TC_SYM")
+    performed = {}
+    try:
+        for sym in ("0", "1"):
+            os.environ["FSGG_TC_SYM"] = sym
+            g, rep, _ = F.build_similarity_graph(F.Dataset(p), k, cfg, report=True)
+            assert np.array_equal(g.u, ref["u"]) and np.array_equal(g.v, ref["v"])
+            assert (np.abs(g.w - ref["w"]) / ref["w"]).max() <= 5e-5
+            performed[sym] = rep.kde_root_performed_evals
+    finally:
+        if old is None:
+            os.environ.pop("FSGG_TC_SYM", None)
+        else:
+            os.environ["FSGG_TC_SYM"] = old
+    assert performed["1"] < performed["0"]
+
+
 def test_pinned_csr_readback_matches_full_copy():
     """bench.py's e2e read-back (HostGraphBuffers.fetch: CSR + degrees over
     PCIe, u expanded on the host on first use) equals the full host copy."""
