@@ -87,7 +87,10 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
                 const uint32_t* __restrict__ wrow, const float* __restrict__ wrm,
                 const double* __restrict__ rows, uint32_t rows_level) {
   // entries, evals, degen, ties, evals read from rows
-  __shared__ unsigned long long s_stats[5][kMaxLevels];
+  // 32-bit per-CTA tallies (native shared-memory atomics; 64-bit ones are
+  // CAS loops): a CTA's counts per level stay far below 2^32 (at most 128
+  // walks x their node sizes), widened when flushed to the global counters
+  __shared__ unsigned int s_stats[5][kMaxLevels];
   for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
   __syncthreads();
 
@@ -179,17 +182,17 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
       const uint32_t n_dg = rare ? __reduce_add_sync(grp, dg) : 0u;
       const uint32_t n_tie = rare ? __reduce_add_sync(grp, tie) : 0u;
       if ((threadIdx.x & 31) == uint32_t(__ffs(grp) - 1) && at < kMaxLevels) {
-        atomicAdd(&s_stats[0][at], static_cast<unsigned long long>(n_ent));
-        if (n_ev) atomicAdd(&s_stats[1][at], static_cast<unsigned long long>(n_ev));
-        if (n_dg) atomicAdd(&s_stats[2][at], static_cast<unsigned long long>(n_dg));
-        if (n_tie) atomicAdd(&s_stats[3][at], static_cast<unsigned long long>(n_tie));
-        if (n_sv) atomicAdd(&s_stats[4][at], static_cast<unsigned long long>(n_sv));
+        atomicAdd(&s_stats[0][at], n_ent);
+        if (n_ev) atomicAdd(&s_stats[1][at], n_ev);
+        if (n_dg) atomicAdd(&s_stats[2][at], n_dg);
+        if (n_tie) atomicAdd(&s_stats[3][at], n_tie);
+        if (n_sv) atomicAdd(&s_stats[4][at], n_sv);
       }
     }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) {
-    const unsigned long long v = (&s_stats[0][0])[k];
+    const unsigned long long v = (&s_stats[0][0])[k];  // widened
     if (v) atomicAdd(stats + k, v);
   }
 }
