@@ -131,7 +131,7 @@ struct Dataset {
   }
   // tensor-core path (kde_tc.cu): split tf32 hi/lo copies + tensor maps
   bool tc_ready = false;
-  alignas(64) unsigned char tc_blob[576];
+  alignas(64) unsigned char tc_blob[1152];
   void release_all();
 };
 

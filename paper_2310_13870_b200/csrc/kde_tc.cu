@@ -38,8 +38,6 @@ constexpr int kTcThreads = 256;
 constexpr int kTileBytes = kTcM * kTcKB * 4;            // 16 KiB (A or B, hi or lo)
 constexpr int kStageBytes = 4 * kTileBytes;             // Ahi, Alo, Bhi, Blo
 constexpr int kSmemBytes = kTcStages * kStageBytes + 1024 + 512;
-// symmetric root: + the epilogue's column partials [4 warps][3 buckets][128]
-constexpr int kSmemSymBytes = kTcStages * kStageBytes + 1024 + 4 * 3 * 128 * 4 + 16 + 1024;
 constexpr uint32_t kTmemCols = 256;                     // 2 x 128-column accumulators
 constexpr uint32_t kTcGroup = 64;                       // entry blocks per L2 group
 constexpr int kRing = 8;          // work-item ring (persistent kernel)
@@ -506,37 +504,39 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // ---- symmetric root (level 0 of a full build, d >= kTcMinDim) ------------
-// Every pair once: the points are cut into 128-point tiles on a fixed grid,
-// a work item is (query tile I, source tiles [J0, J1)) with J0 >= I, and the
-// epilogue of each 128 x 128 accumulator yields both
-//   * row sums (I's points over J's sources), split at J's bucket
-//     boundaries — as the one-sided kernel does, and
-//   * column sums (J's points over I's points, J > I), split at I's bucket
-//     boundaries: per warp a masked butterfly transpose-reduction for each
-//     bucket among its 32 rows, then the four warps' partials added in warp
-//     order through shared memory.
-// Buckets are the root row's tree nodes at depth rl (<= 128 points, so a
-// bucket meets at most two tiles): a bucket inside one tile is stored, the
-// two parts of a straddling bucket are added to the zeroed row with fp64
-// atomics — two addends, so the sum is the same in either order. Every
-// value depends on its two tiles only: deterministic, and it halves the
-// tensor-core work of the n^2 pass.
-#ifndef FSGG_TC_SYM_R
-#define FSGG_TC_SYM_R 8
-#endif
+// Every pair once: the points are cut into 128-point tiles on a fixed grid
+// and each tile pair I <= J is evaluated once. A work item is (query tile I,
+// super-tiles [S0, S1)), super-tile S = source tiles {2S, 2S + 1}: each MMA
+// is 128 x 256 with 16-wide K blocks in 64-byte-swizzled rows, so a 48 KiB
+// stage carries twice the MMA work of a 128-wide 64 KiB one and four stages
+// fit. Per half of a super-tile the pairing rule picks full (rows and
+// columns), diagonal (rows only: the diagonal tile's rows hold both
+// directions) or skipped (J < I: the pair belongs to the item of tile J).
+// The epilogue of each accumulator yields
+//   * row sums (I's points over the sources), split at the sources' bucket
+//     boundaries — warps 4-7, and
+//   * column sums (the full halves' points over I's points), split at I's
+//     bucket boundaries — warps 8-11: per warp a masked butterfly
+//     transpose-reduction for each bucket among its 32 rows, then the four
+//     warps' partials added in warp order through shared memory.
+// Both groups read the accumulator from TMEM and evaluate the same
+// exponentials (same instructions, same bits), so the column side's
+// cross-lane reductions run beside the row side. The epilogue bodies are
+// kept compact (exponentials, then predicated per-bucket sums): a
+// per-column boundary loop unrolled 32x made the code large enough to evict
+// the MMA warp's instructions (root 19.6 -> 15.4 ms at C5).
+// Buckets are the root row's tree nodes at depth rl (16..128 points, so a
+// bucket meets at most two 128-point tiles): a bucket complete within an
+// item is stored, the two parts of a straddling bucket are added to the
+// zeroed row with fp64 atomics — two addends, so the sum is the same in
+// either order. Every value depends on its tiles only: deterministic, and
+// it halves the tensor-core work of the n^2 pass.
 #ifndef FSGG_TC_SYM_GI
 #define FSGG_TC_SYM_GI 32
 #endif
-constexpr uint32_t kTcSymR = FSGG_TC_SYM_R;     // source tiles per work item
 constexpr uint32_t kTcSymGI = FSGG_TC_SYM_GI;   // tiles per side of an L2 block of items
 constexpr int kTcSymMaxSegW = 3;    // buckets among a warp's 32 rows (>= 16 points each)
-// 12 warps: the one-sided kernel's 8 roles, with warps 4-7 taking the row
-// sums and warps 8-11 the column sums of the same accumulator (each group
-// reads it from TMEM and evaluates the exponentials itself — same
-// instructions, same bits): the column side's cross-lane reductions run
-// beside the row side instead of after it (one epilogue group left the
-// MMAs waiting on TMEM: 22.9 ms vs 17.8 ms without the column side)
-constexpr int kTcSymThreads = 384;
+constexpr int kTcSymThreads = 384;  // the one-sided kernel's 8 roles + 4 column warps
 constexpr int kTcSymRingReaders = 10;  // MMA thread, query warp, 8 epilogue warps
 
 __device__ __forceinline__ void flush_bucket(double* __restrict__ prow, uint32_t b, float acc,
@@ -547,33 +547,74 @@ __device__ __forceinline__ void flush_bucket(double* __restrict__ prow, uint32_t
     atomicAdd(prow + b, double(acc));
 }
 
+constexpr int kS2N = 256;                  // sources per MMA (two tiles)
+constexpr int kS2KB = 16;                  // fp32 per K-block: one 64-byte row
+constexpr int kS2Stages = 4;
+constexpr int kS2ATile = kTcM * kS2KB * 4;    // 8 KiB (A hi or lo)
+constexpr int kS2BTile = kS2N * kS2KB * 4;    // 16 KiB (B hi or lo)
+constexpr int kS2Stage = 2 * kS2ATile + 2 * kS2BTile;  // 48 KiB
+constexpr uint32_t kS2TmemCols = 512;      // 2 x 256-column accumulators
+constexpr uint32_t kS2R = 4;               // super-tiles per work item
+constexpr int kSmemS2Bytes = kS2Stages * kS2Stage + 1024 + 4 * 3 * kS2N * 4 + 16 + 1024;
+
+// K-major, 64-byte-swizzled shared-memory matrix descriptor: SBO = 512 B
+// between 8-row groups, layout type SWIZZLE_64B = 4.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3fff);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
+constexpr uint32_t kIdescS2 = (1u << 4) | (2u << 7) | (2u << 10) |
+                              (uint32_t(kS2N >> 3) << 17) | (uint32_t(kTcM >> 4) << 24);
+__device__ __forceinline__ void mma_tf32_n256(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdescS2), "r"(accumulate)
+      : "memory");
+}
+
+// half mode of super-tile S for query tile I: 0 skipped, 1 diagonal, 2 full
+__device__ __forceinline__ uint32_t s2_mode(uint32_t I, uint32_t J, uint32_t T) {
+  if (J >= T || J < I) return 0u;
+  return J == I ? 1u : 2u;
+}
+
 template <int FAM>
 __global__ void __launch_bounds__(kTcSymThreads, 1)
-    kde_tc_sym_kernel(const __grid_constant__ CUtensorMap map_hi,
-                      const __grid_constant__ CUtensorMap map_lo, const float* __restrict__ norm,
-                      uint32_t d_pad, uint32_t n, const uint32_t* __restrict__ sitems,
-                      uint32_t items, uint32_t* __restrict__ next_item,
-                      const uint32_t* __restrict__ tile_b0, const uint32_t* __restrict__ bfirst,
-                      const uint32_t* __restrict__ blast, uint32_t rl, float scale,
-                      double* __restrict__ partials, int terms) {
+    kde_tc_sym256_kernel(const __grid_constant__ CUtensorMap amap_hi,
+                         const __grid_constant__ CUtensorMap amap_lo,
+                         const __grid_constant__ CUtensorMap bmap_hi,
+                         const __grid_constant__ CUtensorMap bmap_lo,
+                         const float* __restrict__ norm, uint32_t d_pad, uint32_t n,
+                         const uint32_t* __restrict__ sitems, uint32_t items,
+                         uint32_t* __restrict__ next_item, const uint32_t* __restrict__ tile_b0,
+                         const uint32_t* __restrict__ bfirst, const uint32_t* __restrict__ blast,
+                         uint32_t rl, float scale, double* __restrict__ partials, int terms) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kS2Stages * kS2Stage);
   uint64_t* full = bars;
-  uint64_t* empty = bars + kTcStages;
-  uint64_t* tfull = bars + 2 * kTcStages;
+  uint64_t* empty = bars + kS2Stages;
+  uint64_t* tfull = bars + 2 * kS2Stages;
   uint64_t* tempty = tfull + 2;
   uint64_t* ring_full = tempty + 2;
   uint64_t* ring_empty = ring_full + kRing;
   uint32_t* ring = reinterpret_cast<uint32_t*>(ring_empty + kRing);
   uint32_t* tmem_slot = ring + kRing;
-  // column partials of the epilogue warps: [warp][bucket slot][column]
-  float* colpart = reinterpret_cast<float*>(smem + kTcStages * kStageBytes + 1024);
-  uint32_t* wfirst = reinterpret_cast<uint32_t*>(colpart + 4 * kTcSymMaxSegW * kTcN);  // [4]
+  float* colpart = reinterpret_cast<float*>(smem + kS2Stages * kS2Stage + 1024);
+  uint32_t* wfirst = reinterpret_cast<uint32_t*>(colpart + 4 * kTcSymMaxSegW * kS2N);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t kblocks = d_pad / kTcKB;
+  const uint32_t kblocks = d_pad / kS2KB;
+  const uint32_t T = (n + kTcM - 1) / kTcM;
   auto next = [&](uint32_t k) -> uint32_t {
     const uint32_t slot = k % kRing;
     mbar_wait(&ring_full[slot], (k / kRing) & 1u);
@@ -582,7 +623,7 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
   auto release = [&](uint32_t k) { mbar_arrive(&ring_empty[k % kRing]); };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
+    for (int s = 0; s < kS2Stages; ++s) {
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
@@ -599,13 +640,15 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kTmemCols)
+                 "r"(kS2TmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap_lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap_lo)) : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -613,7 +656,7 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---- TMA producer: source tiles J0 .. J1-1 ---------------------------
+    // ---- TMA producer: 256-row source super-tiles --------------------------
     if (lane == 0) {
       uint32_t it = 0;
       for (uint32_t k = 0;; ++k) {
@@ -623,22 +666,22 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
         ring[slot] = item;
         mbar_arrive(&ring_full[slot]);
         if (item >= items) break;
-        const uint32_t J0 = sitems[3 * item + 1], J1 = sitems[3 * item + 2];
-        const uint32_t total = (J1 - J0) * kblocks;
+        const uint32_t S0 = sitems[3 * item + 1], S1 = sitems[3 * item + 2];
+        const uint32_t total = (S1 - S0) * kblocks;
         for (uint32_t j = 0; j < total; ++j, ++it) {
-          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-          const uint32_t tile = j / kblocks, kb = j % kblocks;
+          const uint32_t s = it % kS2Stages, ph = (it / kS2Stages) & 1u;
+          const uint32_t st_ = j / kblocks, kb = j % kblocks;
           mbar_wait(&empty[s], ph ^ 1u);
-          unsigned char* st = smem + s * kStageBytes;
-          mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
-          const int row = int((J0 + tile) * kTcN), col = int(kb * kTcKB);
-          tma_load_2d(st + 2 * kTileBytes, &map_hi, &full[s], col, row);
-          tma_load_2d(st + 3 * kTileBytes, &map_lo, &full[s], col, row);
+          unsigned char* st = smem + s * kS2Stage;
+          mbar_arrive_expect_tx(&full[s], 2 * kS2BTile);
+          const int row = int((S0 + st_) * kS2N), col = int(kb * kS2KB);
+          tma_load_2d(st + 2 * kS2ATile, &bmap_hi, &full[s], col, row);
+          tma_load_2d(st + 2 * kS2ATile + kS2BTile, &bmap_lo, &full[s], col, row);
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ------------------------------------------------------
+    // ---- MMA issuer ----------------------------------------------------------
     if (lane == 0) {
       uint32_t it = 0, tg = 0;
       for (uint32_t k = 0;; ++k) {
@@ -650,22 +693,22 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
           const uint32_t buf = tg & 1u;
           mbar_wait(&tempty[buf], ((tg >> 1) & 1u) ^ 1u);
           tc_fence_after();
-          const uint32_t tacc = tmem_base + buf * kTcN;
+          const uint32_t tacc = tmem_base + buf * kS2N;
           for (uint32_t kb = 0; kb < kblocks; ++kb, ++it) {
-            const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
+            const uint32_t s = it % kS2Stages, ph = (it / kS2Stages) & 1u;
             mbar_wait(&full[s], ph);
             tc_fence_after();
-            const uint32_t base = smem_u32(smem + s * kStageBytes);
+            const uint32_t base = smem_u32(smem + s * kS2Stage);
 #pragma unroll
-            for (int ks = 0; ks < kTcKB / 8; ++ks) {
+            for (int ks = 0; ks < kS2KB / 8; ++ks) {
               const uint32_t off = ks * 32;
-              const uint64_t a_hi = sw128_desc(base + off);
-              const uint64_t a_lo = sw128_desc(base + kTileBytes + off);
-              const uint64_t b_hi = sw128_desc(base + 2 * kTileBytes + off);
-              const uint64_t b_lo = sw128_desc(base + 3 * kTileBytes + off);
-              mma_tf32(tacc, a_hi, b_hi, (kb | ks) != 0);
-              if (terms & 1) mma_tf32(tacc, a_hi, b_lo, 1);
-              if (terms & 2) mma_tf32(tacc, a_lo, b_hi, 1);
+              const uint64_t a_hi = sw64_desc(base + off);
+              const uint64_t a_lo = sw64_desc(base + kS2ATile + off);
+              const uint64_t b_hi = sw64_desc(base + 2 * kS2ATile + off);
+              const uint64_t b_lo = sw64_desc(base + 2 * kS2ATile + kS2BTile + off);
+              mma_tf32_n256(tacc, a_hi, b_hi, (kb | ks) != 0);
+              if (terms & 1) mma_tf32_n256(tacc, a_hi, b_lo, 1);
+              if (terms & 2) mma_tf32_n256(tacc, a_lo, b_hi, 1);
             }
             mma_commit(&empty[s]);
           }
@@ -674,7 +717,7 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
       }
     }
   } else if (warp < 4) {
-    // ---- query tile I (one TMA box per K-block and N-tile) ---------------
+    // ---- query tile I (one TMA box per K-block and super-tile) -------------
     if (warp == 2) {
       uint32_t it = 0;
       for (uint32_t k = 0;; ++k) {
@@ -685,21 +728,21 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
         const uint32_t I = sitems[3 * item];
         const uint32_t total = (sitems[3 * item + 2] - sitems[3 * item + 1]) * kblocks;
         for (uint32_t j = 0; j < total; ++j, ++it) {
-          const uint32_t s = it % kTcStages, ph = (it / kTcStages) & 1u;
-          const int col = int((j % kblocks) * kTcKB);
+          const uint32_t s = it % kS2Stages, ph = (it / kS2Stages) & 1u;
+          const int col = int((j % kblocks) * kS2KB);
           mbar_wait(&empty[s], ph ^ 1u);
-          unsigned char* st = smem + s * kStageBytes;
+          unsigned char* st = smem + s * kS2Stage;
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[s], 2 * kTileBytes);
-            tma_load_2d(st, &map_hi, &full[s], col, int(I * kTcM));
-            tma_load_2d(st + kTileBytes, &map_lo, &full[s], col, int(I * kTcM));
+            mbar_arrive_expect_tx(&full[s], 2 * kS2ATile);
+            tma_load_2d(st, &amap_hi, &full[s], col, int(I * kTcM));
+            tma_load_2d(st + kS2ATile, &amap_lo, &full[s], col, int(I * kTcM));
           }
           __syncwarp();
         }
       }
     }
   } else if (warp < 8) {
-    // ---- row side (warps 4-7: TMEM lanes = I's rows) ----------------------
+    // ---- row side (warps 4-7) ---------------------------------------------
     const uint32_t ew = warp & 3;
     const uint32_t row = ew * 32 + lane;
     uint32_t tg = 0;
@@ -708,126 +751,136 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
       __syncwarp();
       if (lane == 0) release(k);
       if (item >= items) break;
-      const uint32_t I = sitems[3 * item], J0 = sitems[3 * item + 1],
-                     J1 = sitems[3 * item + 2];
+      const uint32_t I = sitems[3 * item], S0 = sitems[3 * item + 1],
+                     S1 = sitems[3 * item + 2];
       const uint32_t q = I * kTcM + row;
       const bool qv = q < n;
       const float qn = norm[qv ? q : n - 1];
       double* prow = partials + (size_t(q) << rl);
-      for (uint32_t J = J0; J < J1; ++J, ++tg) {
+      for (uint32_t S = S0; S < S1; ++S, ++tg) {
         const uint32_t buf = tg & 1u;
         mbar_wait(&tfull[buf], (tg >> 1) & 1u);
         tc_fence_after();
-        const uint32_t n0 = J * kTcN;
-        const uint32_t valid = min(uint32_t(kTcN), n - n0);
-        uint32_t b = tile_b0[J], bend = blast[b];
+        const uint32_t n0 = S * kS2N;
+        // row-valid columns: [c0, c1) (half 0 skipped when its tile precedes I)
+        const uint32_t c0 = s2_mode(I, 2 * S, T) ? 0u : uint32_t(kTcN);
+        const uint32_t c1 = min(uint32_t(kS2N), n - n0);
+        uint32_t b = tile_b0[(n0 + c0) / kTcM], bend = blast[b];
         float acc = 0.f;
+        // compact body: the chunk's exponentials first (no branches), then
+        // its bucket segments (<= 3, bucket >= 16 points) as predicated sums
+        // — a per-column boundary loop unrolled 32x made the epilogue code
+        // large enough to evict the MMA warp's instructions
 #pragma unroll 1
-        for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
+        for (int chunk = int(c0 / 32); chunk < kS2N / 32; ++chunk) {
           float v[32];
-          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kS2N + chunk * 32, v);
+          const uint32_t cb = chunk * 32;
 #pragma unroll
           for (int kk = 0; kk < 32; ++kk) {
-            const uint32_t col = chunk * 32 + kk;
-            if (col < valid) {  // uniform across the warp
-              while (n0 + col >= bend) {  // next bucket (uniform)
-                if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0);
-                acc = 0.f;
-                bend = blast[++b];
-              }
-              const float xn = __ldg(norm + n0 + col);
-              float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
-              if constexpr (FAM == 1) d2 = sqrtf(d2);
-              acc += ex2_approx(-scale * d2);
+            const float xn = __ldg(norm + n0 + min(cb + kk, c1 - 1));
+            float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
+            if constexpr (FAM == 1) d2 = sqrtf(d2);
+            v[kk] = cb + kk < c1 ? ex2_approx(-scale * d2) : 0.f;
+          }
+          uint32_t lo = cb;  // this chunk's columns [lo, min(cb + 32, c1))
+          const uint32_t hi = min(cb + 32u, c1);
+          while (lo < hi) {  // uniform
+            const uint32_t end = min(hi, bend - n0);
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk)
+              acc += (cb + kk >= lo && cb + kk < end) ? v[kk] : 0.f;
+            lo = end;
+            if (lo == bend - n0 && lo < c1) {  // bucket complete
+              if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0 + c0);
+              acc = 0.f;
+              bend = blast[++b];
             }
           }
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
-        if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0 && bend <= n0 + valid);
+        if (qv) flush_bucket(prow, b, acc, bfirst[b] >= n0 + c0 && bend <= n0 + c1);
       }
     }
   } else {
-    // ---- column side (warps 8-11): J's points over I's buckets ------------
+    // ---- column side (warps 8-11): the full halves' points over I's buckets
     const uint32_t ew = warp & 3;
     const uint32_t row = ew * 32 + lane;
-    const uint32_t ct = row;  // this thread's column in the combine
     uint32_t tg = 0;
     for (uint32_t k = 0;; ++k) {
       const uint32_t item = next(k);
       __syncwarp();
       if (lane == 0) release(k);
       if (item >= items) break;
-      const uint32_t I = sitems[3 * item], J0 = sitems[3 * item + 1],
-                     J1 = sitems[3 * item + 2];
+      const uint32_t I = sitems[3 * item], S0 = sitems[3 * item + 1],
+                     S1 = sitems[3 * item + 2];
       const uint32_t q0 = I * kTcM, q = q0 + row;
       const bool qv = q < n;
       const uint32_t qend = min(q0 + uint32_t(kTcM), n);
       const float qn = norm[qv ? q : n - 1];
-      // this row's bucket and the warp's first one (rows past n: the last)
       uint32_t bq = tile_b0[I];
       const uint32_t qq = qv ? q : n - 1;
       while (blast[bq] <= qq) ++bq;
       const uint32_t bw = __shfl_sync(0xffffffffu, bq, 0);
-      const uint32_t nsw = __shfl_sync(0xffffffffu, bq, 31) - bw + 1;  // <= kTcSymMaxSegW
-      // I's buckets and, per warp, the first one among its rows (for the combine)
+      const uint32_t nsw = __shfl_sync(0xffffffffu, bq, 31) - bw + 1;
       const uint32_t bI0 = tile_b0[I];
       uint32_t bIend = bI0;
       while (bIend < (1u << rl) && bfirst[bIend] < qend) ++bIend;
-      for (uint32_t J = J0; J < J1; ++J, ++tg) {
+      for (uint32_t S = S0; S < S1; ++S, ++tg) {
         const uint32_t buf = tg & 1u;
-        if (J == I) {  // the diagonal tile's rows hold both directions
-          mbar_wait(&tfull[buf], (tg >> 1) & 1u);
-          tc_fence_before();
-          mbar_arrive(&tempty[buf]);
-          continue;
-        }
+        const uint32_t m0 = s2_mode(I, 2 * S, T), m1 = s2_mode(I, 2 * S + 1, T);
         mbar_wait(&tfull[buf], (tg >> 1) & 1u);
         tc_fence_after();
-        const uint32_t n0 = J * kTcN;
-        const uint32_t valid = min(uint32_t(kTcN), n - n0);
+        const uint32_t n0 = S * kS2N;
+        const uint32_t c1 = min(uint32_t(kS2N), n - n0);
+        if (m0 == 2 || m1 == 2) {
 #pragma unroll 1
-        for (int chunk = 0; chunk < kTcN / 32; ++chunk) {
-          float v[32];
-          tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kTcN + chunk * 32, v);
+          for (int chunk = 0; chunk < kS2N / 32; ++chunk) {
+            if ((chunk < 4 ? m0 : m1) != 2) continue;  // uniform
+            float v[32];
+            tmem_ld32(tmem_base + ((ew * 32) << 16) + buf * kS2N + chunk * 32, v);
 #pragma unroll
-          for (int kk = 0; kk < 32; ++kk) {
-            const uint32_t col = chunk * 32 + kk;
-            float e = 0.f;
-            if (col < valid) {
-              const float xn = __ldg(norm + n0 + col);
-              float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
-              if constexpr (FAM == 1) d2 = sqrtf(d2);
-              e = ex2_approx(-scale * d2);
-            }
-            v[kk] = qv ? e : 0.f;
-          }
-          // per bucket among the warp's rows: the warp's sum of each of
-          // these 32 columns (lane l: column chunk*32 + l), fixed butterfly
-          for (uint32_t sgm = 0; sgm < nsw; ++sgm) {
-            float c[32];
-            const bool mine = bq == bw + sgm;
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) c[kk] = mine ? v[kk] : 0.f;
-#pragma unroll
-            for (int st = 16; st >= 1; st >>= 1) {
-              const bool up = (lane & st) != 0;
-#pragma unroll
-              for (int i = 0; i < st; ++i) {
-                const float keep = up ? c[i + st] : c[i];
-                const float send = up ? c[i] : c[i + st];
-                c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+            for (int kk = 0; kk < 32; ++kk) {
+              const uint32_t col = chunk * 32 + kk;
+              float e = 0.f;
+              if (col < c1) {
+                const float xn = __ldg(norm + n0 + col);
+                float d2 = fmaxf(fmaf(-2.f, v[kk], qn + xn), 0.f);
+                if constexpr (FAM == 1) d2 = sqrtf(d2);
+                e = ex2_approx(-scale * d2);
               }
+              v[kk] = qv ? e : 0.f;
             }
-            colpart[(ew * kTcSymMaxSegW + sgm) * kTcN + chunk * 32 + lane] = c[0];
+            for (uint32_t sgm = 0; sgm < nsw; ++sgm) {
+              float c[32];
+              const bool mine = bq == bw + sgm;
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) c[kk] = mine ? v[kk] : 0.f;
+#pragma unroll
+              for (int st = 16; st >= 1; st >>= 1) {
+                const bool up = (lane & st) != 0;
+#pragma unroll
+                for (int i = 0; i < st; ++i) {
+                  const float keep = up ? c[i + st] : c[i];
+                  const float send = up ? c[i] : c[i + st];
+                  c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+                }
+              }
+              colpart[(ew * kTcSymMaxSegW + sgm) * kS2N + chunk * 32 + lane] = c[0];
+            }
           }
         }
         tc_fence_before();
         mbar_arrive(&tempty[buf]);
+        if (!(m0 == 2 || m1 == 2)) continue;
         if (lane == 0) wfirst[ew] = bw;
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        // thread ct: column ct of J over each of I's buckets, warps in order
-        if (ct < valid) {
+        // threads: columns row and row + 128 of the full halves
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t ct = row + 128u * h;
+          if ((h ? m1 : m0) != 2 || ct >= c1) continue;
           double* xrow = partials + (size_t(n0 + ct) << rl);
           for (uint32_t bb = bI0; bb < bIend; ++bb) {
             const uint32_t lo = bfirst[bb], hi = blast[bb];
@@ -837,7 +890,7 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
               const uint32_t r0 = q0 + 32 * w;
               const uint32_t r1 = min(r0 + 32, qend);
               if (r0 < qend && hi > r0 && lo < r1)
-                sum += colpart[(w * kTcSymMaxSegW + (bb - wfirst[w])) * kTcN + ct];
+                sum += colpart[(w * kTcSymMaxSegW + (bb - wfirst[w])) * kS2N + ct];
             }
             flush_bucket(xrow, bb, sum, lo >= q0 && hi <= qend);
           }
@@ -851,7 +904,7 @@ __global__ void __launch_bounds__(kTcSymThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols)
+                 "r"(kS2TmemCols)
                  : "memory");
   }
 }
@@ -877,14 +930,16 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad, uint32_t box_rows) {
+void make_map(CUtensorMap* map, float* base, uint32_t n, uint32_t d_pad, uint32_t box_rows,
+              uint32_t box_cols = kTcKB,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   const cuuint64_t dims[2] = {d_pad, n};
   const cuuint64_t strides[1] = {cuuint64_t(d_pad) * 4};
-  const cuuint32_t box[2] = {uint32_t(kTcKB), box_rows};
+  const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides,
-                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
@@ -893,6 +948,9 @@ struct TcState {
   uint32_t d_pad = 0;
   CUtensorMap map_hi, map_lo;    // 128-row boxes (sources, contiguous queries)
   CUtensorMap gmap_hi, gmap_lo;  // 1-row boxes for tile::gather4
+  // symmetric 256-wide root: 16-wide K blocks, 64-byte swizzle
+  CUtensorMap amap_hi, amap_lo;  // 128-row query boxes
+  CUtensorMap bmap_hi, bmap_lo;  // 256-row source boxes
 };
 
 TcState& tc_state(Dataset& ds) {
@@ -918,6 +976,10 @@ TcState& tc_state(Dataset& ds) {
     make_map(&st->map_lo, lo.as<float>(), ds.n, d_pad, kTcN);
     make_map(&st->gmap_hi, hi.as<float>(), ds.n, d_pad, 1);
     make_map(&st->gmap_lo, lo.as<float>(), ds.n, d_pad, 1);
+    make_map(&st->amap_hi, hi.as<float>(), ds.n, d_pad, kTcM, kS2KB, CU_TENSOR_MAP_SWIZZLE_64B);
+    make_map(&st->amap_lo, lo.as<float>(), ds.n, d_pad, kTcM, kS2KB, CU_TENSOR_MAP_SWIZZLE_64B);
+    make_map(&st->bmap_hi, hi.as<float>(), ds.n, d_pad, kS2N, kS2KB, CU_TENSOR_MAP_SWIZZLE_64B);
+    make_map(&st->bmap_lo, lo.as<float>(), ds.n, d_pad, kS2N, kS2KB, CU_TENSOR_MAP_SWIZZLE_64B);
     ds.tc_ready = true;
   }
   return *reinterpret_cast<TcState*>(ds.tc_blob);
@@ -944,7 +1006,7 @@ bool kde_tc_supported(const Dataset& ds, int family) {
   return enabled && ds.d >= kTcMinDim && family != 2;
 }
 
-// Symmetric root (kde_tc_sym_kernel) for a full build's level 0: partials
+// Symmetric root (kde_tc_sym256_kernel) for a full build's level 0: partials
 // (n rows of 2^rl fp64 buckets) zeroed and filled; returns false (nothing
 // launched) when the layout does not fit it (a query shard, buckets outside
 // 16..128 points) or FSGG_TC_SYM=0.
@@ -980,18 +1042,20 @@ bool kde_tc_root_symmetric(Dataset& ds, const KernelSpec& ks, const LevelView& l
   // items (I, J0, J1), J0 >= I, in blocks of kTcSymGI x kTcSymGI tiles: the
   // items of one block (about one wave of CTAs) read kTcSymGI query and
   // kTcSymGI source tiles (2 x 26 MB at C5), which stay in L2 (an order by
-  // query tile alone read 81 GB from DRAM per launch)
+  // query tile alone read 81 GB from DRAM per launch). The 256-wide kernel
+  // takes (I, S0, S1) over super-tiles S = {2S, 2S + 1}, S >= I / 2.
   std::vector<uint32_t> it;
   uint64_t perf = 0;
+  const uint32_t TS = (T + 1) / 2;
   for (uint32_t a0 = 0; a0 < T; a0 += kTcSymGI) {
     const uint32_t a1 = std::min(T, a0 + kTcSymGI);
-    for (uint32_t c0 = a0; c0 < T; c0 += kTcSymGI) {
-      const uint32_t c1 = std::min(T, c0 + kTcSymGI);
+    for (uint32_t c0 = a0 / 2; c0 < TS; c0 += kTcSymGI / 2) {
+      const uint32_t c1 = std::min(TS, c0 + kTcSymGI / 2);
       for (uint32_t I = a0; I < a1; ++I)
-        for (uint32_t J0 = std::max(I, c0); J0 < c1; J0 += kTcSymR) {
+        for (uint32_t S0 = std::max(I / 2, c0); S0 < c1; S0 += kS2R) {
           it.push_back(I);
-          it.push_back(J0);
-          it.push_back(std::min(c1, J0 + kTcSymR));
+          it.push_back(S0);
+          it.push_back(std::min(c1, S0 + kS2R));
         }
     }
   }
@@ -1008,19 +1072,19 @@ bool kde_tc_root_symmetric(Dataset& ds, const KernelSpec& ks, const LevelView& l
   FSGG_CUDA(cudaMemsetAsync(partials, 0, (size_t(n) << rl) * 8, s));
   static bool attr[64] = {};
   if (ds.device < 64 && !attr[ds.device]) {
-    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym_kernel<0>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSymBytes));
-    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSymBytes));
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym256_kernel<0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemS2Bytes));
+    FSGG_CUDA(cudaFuncSetAttribute(kde_tc_sym256_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemS2Bytes));
     attr[ds.device] = true;
   }
-  auto kern = ks.family == 1 ? kde_tc_sym_kernel<1> : kde_tc_sym_kernel<0>;
   DevBuf& counter = ds.buf("tc.next_item", 8);
   FSGG_CUDA(cudaMemsetAsync(counter.as<void>(), 0, 4, s));
   const uint32_t grid = std::min<uint32_t>(items, uint32_t(ds.num_sms));
-  kern<<<grid, kTcSymThreads, kSmemSymBytes, s>>>(
-      st.map_hi, st.map_lo, ds.buf("tc.norm", 8).as<float>(), st.d_pad, n,
-      ditems.as<uint32_t>(), items, counter.as<uint32_t>(), db0.as<uint32_t>(),
+  auto kern = ks.family == 1 ? kde_tc_sym256_kernel<1> : kde_tc_sym256_kernel<0>;
+  kern<<<grid, kTcSymThreads, kSmemS2Bytes, s>>>(
+      st.amap_hi, st.amap_lo, st.bmap_hi, st.bmap_lo, ds.buf("tc.norm", 8).as<float>(),
+      st.d_pad, n, ditems.as<uint32_t>(), items, counter.as<uint32_t>(), db0.as<uint32_t>(),
       t.first.as<uint32_t>() + hb, t.last.as<uint32_t>() + hb, rl, ks.scale, partials,
       tc_terms());
   FSGG_LAUNCH_CHECK();
