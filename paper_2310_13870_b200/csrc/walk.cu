@@ -21,6 +21,9 @@ namespace fsgg {
 namespace {
 
 constexpr int kWalkThreads = 128;
+#ifndef FSGG_WALK_CTAS
+#define FSGG_WALK_CTAS 16
+#endif
 constexpr int kMaxLevels = 64;
 constexpr double kTieMargin = 1e-4;  // as route_kernel (sampler.cu)
 
@@ -71,10 +74,12 @@ __device__ __forceinline__ Decision decide(double a, double b, float em, uint32_
   return d;
 }
 
-// d <= 2: capped at 40 registers (12 CTAs per SM; a few spills) — the
-// kernel is issue/latency-bound and the extra warps measured 6% faster
+// d <= 2: capped at 32 registers (16 CTAs per SM; some spills) — the
+// kernel is latency-bound on its loads (ncu: long-scoreboard stalls lead),
+// and the extra warps measured faster than fewer spills (12 CTAs: 9.10 ms,
+// 14-16: 8.90)
 template <int D, int FAM>
-__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
+__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
     walk_kernel(const float* __restrict__ pts, uint32_t W, const uint32_t* __restrict__ wq,
                 const uint32_t* __restrict__ wh, const float* __restrict__ welm,
                 const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
@@ -103,10 +108,16 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
   uint64_t qlink = 0;
   uint32_t row = 0xffffffffu;  // first step read from the row (see WalkArgs)
   float rmass = 0.f;
+  // the node's point range: loaded once, then carried — a child is
+  // [f, mid) or [mid, l) with mid = f + (l - f) / 2 (the tree's split), so
+  // no step waits on a dependent load of the next node's range
+  uint32_t nf = 0, nl = 0;
   if (live) {
     q = wq[i];
     qlink = query_link(q);
     h = wh[i];
+    nf = tfirst[h];
+    nl = tlast[h];
     em = welm[i];
     lev = 31 - __clz(uint32_t(h) + 1);
     if (rows && lev == rows_level + 1) {
@@ -120,7 +131,7 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
   while (__any_sync(0xffffffffu, live)) {
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     if (live) {
-      const uint32_t f = tfirst[h], l = tlast[h];
+      const uint32_t f = nf, l = nl;
       uint32_t ev = 0, dg = 0, tie = 0, sv = 0;
       const uint32_t at = lev;
       if (l - f == 1) {  // sampler.cpp:196-198: leaf (query, source, 1)
@@ -168,6 +179,9 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? 12 : 0)
         // margin's far-node widening reads it)
         em = float(int((__double_as_longlong(dc.left ? a : b) >> 52) & 0x7ff) - 1023);
         h = dc.left ? 2 * h + 1 : 2 * h + 2;
+        const uint32_t mid = f + (l - f) / 2;
+        nf = dc.left ? f : mid;
+        nl = dc.left ? mid : l;
         ++lev;
       }
       // per-level tallies, one shared-memory update per level group of the
