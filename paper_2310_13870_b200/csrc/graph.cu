@@ -11,6 +11,7 @@
 //    FMA contraction; sparsity invariant (:120-121); degrees summed per
 //    vertex in exactly the reference's edge order via a transposed CSR.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_select.cuh>
@@ -345,6 +346,191 @@ void rows_row_ptr(Dataset& ds, const GraphResult& g, uint32_t rb, uint32_t re,
   FSGG_CUDA(cudaStreamSynchronize(s));
 }
 
+// ---- row-bucketed pair collapse (1-GPU build) ------------------------------
+// A sample (q, s), s != q, is the undirected pair (min, max) and belongs to
+// row min(q, s). Instead of a 40-bit radix sort of all n L pair keys, the
+// partners are bucketed by row (count, scan, fill; one warp per sampled
+// row, coalesced over its sources), each row's partners ranked in shared
+// memory by one warp (rows hold ~L values) and deduplicated: the same sorted
+// unique (u, v) list with a fraction of the memory traffic. Rows longer than
+// kRowSortCap (only with rounds comparable to n) go through CUB's segmented
+// sort instead.
+constexpr uint32_t kRowSortCap = 512;
+constexpr int kRowIdxBits = 9;  // position bits of the rank keys (kRowSortCap)
+constexpr int kRowWarps = 8;
+
+__global__ void rows_count_kernel(uint32_t nq, const uint32_t* __restrict__ uq,
+                                  const uint64_t* __restrict__ row_off,
+                                  const uint32_t* __restrict__ row_cnt,
+                                  const uint32_t* __restrict__ leaf_src,
+                                  const uint32_t* __restrict__ leaf_cnt,
+                                  uint32_t* __restrict__ cnt,
+                                  unsigned long long* __restrict__ counters) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long self = 0, sampled = 0;
+  if (r < nq) {
+    const uint32_t q = uq[r], c = row_cnt[r];
+    const uint64_t a = row_off[r];
+    sampled = c;
+    uint32_t own = 0;  // partners above q land in q's own row: one atomic
+    for (uint32_t k = 0; k < c; ++k) {
+      const uint32_t s = leaf_src[a + k];
+      if (s == q)
+        self += leaf_cnt[a + k];
+      else if (s > q)
+        ++own;
+      else
+        atomicAdd(cnt + s, 1u);
+    }
+    if (own) atomicAdd(cnt + q, own);
+  }
+  for (int o = 16; o; o >>= 1) {
+    self += __shfl_xor_sync(0xffffffffu, self, o);
+    sampled += __shfl_xor_sync(0xffffffffu, sampled, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (self) atomicAdd(counters + 0, self);
+    if (sampled) atomicAdd(counters + 1, sampled);
+  }
+}
+
+__global__ void __launch_bounds__(256) rows_fill_kernel(
+    uint32_t nq, const uint32_t* __restrict__ uq, const uint64_t* __restrict__ row_off,
+    const uint32_t* __restrict__ row_cnt, const uint32_t* __restrict__ leaf_src,
+    const uint32_t* __restrict__ off, uint32_t* __restrict__ fill, uint32_t* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t r = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (r >= nq) return;
+  const uint32_t q = uq[r], c = row_cnt[r];
+  const uint64_t a = row_off[r];
+  uint32_t own = 0;
+  for (uint32_t k = lane; k < c; k += 32) own += leaf_src[a + k] > q;
+  for (int o = 16; o; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
+  uint32_t at = 0;
+  if (lane == 0 && own) at = off[q] + atomicAdd(fill + q, own);
+  at = __shfl_sync(0xffffffffu, at, 0);
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint32_t k0 = 0; k0 < c; k0 += 32) {
+    const uint32_t k = k0 + lane;
+    const uint32_t s = k < c ? leaf_src[a + k] : q;
+    const unsigned up = __ballot_sync(0xffffffffu, s > q);
+    if (s > q)
+      part[at + __popc(up & lt)] = s;
+    else if (s < q)
+      part[off[s] + atomicAdd(fill + s, 1u)] = q;
+    at += __popc(up);
+  }
+}
+
+// One warp per row: partner v at position i becomes the distinct key
+// (v << 9) | i, whose rank among the row's keys is its sorted position
+// (rows <= kRowSortCap = 512, n <= 2^23). Each lane holds up to 8 keys in
+// registers and compares them against every key of the row, read as
+// broadcast uint4 from shared memory; the ranked row is deduplicated by
+// neighbour comparison and written back sorted with its distinct count.
+template <int K>
+__device__ __forceinline__ void rank_pass(const uint32_t* x, uint32_t c4, uint32_t base,
+                                          int lane, uint32_t* y) {
+  uint32_t v[K], r[K];
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    v[t] = x[base + lane + 32 * t];
+    r[t] = 0;
+  }
+  for (uint32_t j = 0; j < c4; j += 4) {
+    const uint4 q = *reinterpret_cast<const uint4*>(x + j);
+#pragma unroll
+    for (int t = 0; t < K; ++t)
+      r[t] += (q.x < v[t]) + (q.y < v[t]) + (q.z < v[t]) + (q.w < v[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < K; ++t)
+    if (v[t] != 0xffffffffu) y[r[t]] = v[t] >> kRowIdxBits;
+}
+
+__global__ void __launch_bounds__(256) rows_sort_kernel(uint32_t n, const uint32_t* __restrict__ off,
+                                                        const uint32_t* __restrict__ part,
+                                                        uint32_t* __restrict__ sorted,
+                                                        uint32_t* __restrict__ ucnt,
+                                                        unsigned long long* __restrict__ longest) {
+  __shared__ __align__(16) uint32_t sx[kRowWarps][kRowSortCap];
+  __shared__ uint32_t sy[kRowWarps][kRowSortCap];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kRowWarps + w;
+  if (u > n) return;
+  if (u == n) {
+    if (lane == 0) ucnt[n] = 0;
+    return;
+  }
+  const uint32_t a = off[u], c = off[u + 1] - a;
+  if (c > kRowSortCap) {  // the host sorts the rows with CUB instead
+    if (lane == 0) atomicMax(longest, (unsigned long long)c);
+    return;
+  }
+  uint32_t* x = sx[w];
+  uint32_t* y = sy[w];
+  const uint32_t c32 = (c + 31) & ~31u;
+  for (uint32_t i = lane; i < c32; i += 32)
+    x[i] = i < c ? (part[a + i] << kRowIdxBits) | i : 0xffffffffu;
+  __syncwarp();
+  const uint32_t c4 = (c + 3) & ~3u;
+  for (uint32_t base = 0; base < c; base += 256) {
+    switch (min(8u, (c - base + 31) >> 5)) {
+      case 1: rank_pass<1>(x, c4, base, lane, y); break;
+      case 2: rank_pass<2>(x, c4, base, lane, y); break;
+      case 3: rank_pass<3>(x, c4, base, lane, y); break;
+      case 4: rank_pass<4>(x, c4, base, lane, y); break;
+      case 5: rank_pass<5>(x, c4, base, lane, y); break;
+      case 6: rank_pass<6>(x, c4, base, lane, y); break;
+      case 7: rank_pass<7>(x, c4, base, lane, y); break;
+      default: rank_pass<8>(x, c4, base, lane, y); break;
+    }
+  }
+  __syncwarp();
+  uint32_t distinct = 0;
+  for (uint32_t i = lane; i < c; i += 32) {
+    const uint32_t v = y[i];
+    distinct += i == 0 || v != y[i - 1];
+    sorted[a + i] = v;
+  }
+  for (int o = 16; o; o >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, o);
+  if (lane == 0) ucnt[u] = distinct;
+}
+
+// distinct partners per row of a sorted segment (the CUB fallback)
+__global__ void rows_unique_count_kernel(uint32_t n, const uint32_t* __restrict__ off,
+                                         const uint32_t* __restrict__ part,
+                                         uint32_t* __restrict__ ucnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (u > n) return;
+  uint32_t k = 0;
+  if (u < n)
+    for (uint32_t e = off[u] + lane; e < off[u + 1]; e += 32)
+      k += (e == off[u] || part[e] != part[e - 1]);
+  for (int o = 16; o; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+  if (lane == 0) ucnt[u] = k;
+}
+
+__global__ void __launch_bounds__(256) rows_unique_write_kernel(
+    uint32_t n, const uint32_t* __restrict__ off, const uint32_t* __restrict__ sorted,
+    const uint32_t* __restrict__ uoff, unsigned long long* __restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t u = blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (u >= n) return;
+  const uint32_t a = off[u], e = off[u + 1];
+  uint32_t at = uoff[u];
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint32_t i0 = a; i0 < e; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < e ? sorted[i] : 0u;
+    const bool keep = i < e && (i == a || sorted[i - 1] != v);
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) keys[at + __popc(m & lt)] = (static_cast<unsigned long long>(u) << 32) | v;
+    at += __popc(m);
+  }
+}
+
 uint64_t collapse_pairs_routed(Dataset& ds, SampleResult& res, DevBuf& keys, uint32_t world,
                                const uint32_t* bounds_host, uint64_t* counts,
                                uint64_t* self_pairs, uint64_t* sampled_pairs) {
@@ -401,31 +587,74 @@ uint64_t collapse_pairs_routed(Dataset& ds, SampleResult& res, DevBuf& keys, uin
 uint64_t collapse_pairs(Dataset& ds, SampleResult& res, DevBuf& keys,
                         uint64_t* self_pairs, uint64_t* sampled_pairs) {
   cudaStream_t s = ds.stream;
-  const uint64_t cap = res.total_tickets;
-  const uint32_t bits = index_bits(ds.n);
-  keys.ensure(std::max<uint64_t>(cap, 1) * 8, s);
-  DevBuf& counters = ds.buf("g.counters", 16);
-  FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 16, s));
-  rows_to_keys_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(
-      res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(),
-      res.row_cnt.as<uint32_t>(), res.leaf_src.as<uint32_t>(),
-      res.leaf_cnt.as<uint32_t>(), bits, keys.as<unsigned long long>(),
-      counters.as<unsigned long long>());
+  const uint32_t n = ds.n;
+  const uint64_t cap = std::max<uint64_t>(res.total_tickets, 1);
+  if (cap > 0xffffffffull) throw ConfigError("too many samples for 32-bit row offsets");
+  keys.ensure(cap * 8, s);
+  DevBuf& counters = ds.buf("g.counters", 24);
+  DevBuf& cnt = ds.buf("g.row_cnt", size_t(n + 2) * 4);
+  DevBuf& off = ds.buf("g.row_off", size_t(n + 2) * 4);
+  DevBuf& fill = ds.buf("g.row_fill", size_t(n + 2) * 4);
+  DevBuf& part = ds.buf("g.part", cap * 4);
+  DevBuf& sorted = ds.buf("g.part2", cap * 4);
+  DevBuf& tmp = ds.buf("g.tmp", 8);
+  FSGG_CUDA(cudaMemsetAsync(counters.as<void>(), 0, 24, s));
+  FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, size_t(n + 2) * 4, s));
+  FSGG_CUDA(cudaMemsetAsync(fill.as<void>(), 0, size_t(n + 2) * 4, s));
+  const uint32_t gq = ceil_div_u32(std::max<uint32_t>(res.nq, 1), kRowWarps);
+  const uint32_t gn = ceil_div_u32(uint64_t(n) + 1, kRowWarps);
+  rows_count_kernel<<<ceil_div_u32(std::max<uint32_t>(res.nq, 1), 256), 256, 0, s>>>(res.nq, res.uq.as<uint32_t>(),
+                                       res.row_off.as<uint64_t>(), res.row_cnt.as<uint32_t>(),
+                                       res.leaf_src.as<uint32_t>(), res.leaf_cnt.as<uint32_t>(),
+                                       cnt.as<uint32_t>(), counters.as<unsigned long long>());
   FSGG_LAUNCH_CHECK();
-  ds.launches++;
-  unsigned long long c[2];
-  FSGG_CUDA(cudaMemcpyAsync(c, counters.as<void>(), 16, cudaMemcpyDeviceToHost, s));
-  FSGG_CUDA(cudaStreamSynchronize(s));
-  *self_pairs = c[0];
-  *sampled_pairs = c[1];
-  const uint64_t m = sort_unique_compact(ds, keys, cap, bits);
-  if (m) {
-    compact_to_public_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
-        keys.as<unsigned long long>(), m, bits);
+  cub_call(tmp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cnt.as<uint32_t>(), off.as<uint32_t>(), n + 1, s);
+  });
+  rows_fill_kernel<<<gq, 256, 0, s>>>(
+      res.nq, res.uq.as<uint32_t>(), res.row_off.as<uint64_t>(), res.row_cnt.as<uint32_t>(),
+      res.leaf_src.as<uint32_t>(), off.as<uint32_t>(), fill.as<uint32_t>(), part.as<uint32_t>());
+  FSGG_LAUNCH_CHECK();
+  const char* env = std::getenv("FSGG_COLLAPSE_SEGSORT");  // read per call: tests toggle it
+  bool segsort = (env && env[0] == '1') || uint64_t(n) > (1ull << (32 - kRowIdxBits));
+  if (!segsort) {
+    rows_sort_kernel<<<gn, 256, 0, s>>>(n, off.as<uint32_t>(), part.as<uint32_t>(),
+                                        sorted.as<uint32_t>(), cnt.as<uint32_t>(),
+                                        counters.as<unsigned long long>() + 2);
     FSGG_LAUNCH_CHECK();
-    ds.launches++;
   }
-  return m;
+  unsigned long long* hw = ds.host_words();
+  FSGG_CUDA(cudaMemcpyAsync(hw, counters.as<void>(), 24, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaMemcpyAsync(hw + 3, off.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  *self_pairs = hw[0];
+  *sampled_pairs = hw[1];
+  segsort = segsort || hw[2] > kRowSortCap;
+  const uint32_t total = *reinterpret_cast<const uint32_t*>(hw + 3);
+  if (total == 0) return 0;
+  ds.launches += 5;
+  if (segsort) {
+    cub_call(tmp, s, [&](void* t, size_t& b) {
+      return cub::DeviceSegmentedSort::SortKeys(t, b, part.as<uint32_t>(),
+                                                sorted.as<uint32_t>(), int(total), int(n),
+                                                off.as<uint32_t>(), off.as<uint32_t>() + 1, s);
+    });
+    rows_unique_count_kernel<<<gn, 256, 0, s>>>(n, off.as<uint32_t>(), sorted.as<uint32_t>(),
+                                                cnt.as<uint32_t>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches += 2;
+  }
+  cub_call(tmp, s, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cnt.as<uint32_t>(), fill.as<uint32_t>(), n + 1, s);
+  });
+  rows_unique_write_kernel<<<ceil_div_u32(n, kRowWarps), 256, 0, s>>>(
+      n, off.as<uint32_t>(), sorted.as<uint32_t>(), fill.as<uint32_t>(),
+      keys.as<unsigned long long>());
+  FSGG_LAUNCH_CHECK();
+  uint32_t* hm = reinterpret_cast<uint32_t*>(ds.host_words());
+  FSGG_CUDA(cudaMemcpyAsync(hm, fill.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, s));
+  FSGG_CUDA(cudaStreamSynchronize(s));
+  return *hm;
 }
 
 // Step 4 of finish_graph (shared by the chunked finish): upper CSR,

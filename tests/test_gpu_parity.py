@@ -125,3 +125,29 @@ def test_ticket_conservation(oracle):
     assert diag.entries_per_level[0] == n
     assert diag.degenerate_draws == 0
     assert int(tri[:, 2].sum()) == n * 37
+
+
+@pytest.mark.parametrize("segsort", ["0", "1"])
+@pytest.mark.parametrize("n,rounds", [(3000, 2048), (2000, 200), (500, 8)])
+def test_pair_collapse_long_and_short_rows(oracle, monkeypatch, n, rounds, segsort):
+    # the 1-GPU collapse (csrc/graph.cu collapse_pairs) ranks rows of up to
+    # kRowSortCap = 512 partners in shared memory (in passes of 256) and hands
+    # longer rows to CUB's segmented sort: rounds=2048 over n=3000 gives rows
+    # of ~1500 partners, rounds=200 over n=2000 rows of 256..512.
+    # Either way the edge list is the sorted unique (min, max) of the
+    # sampled triples (proj/src/sparsifier.cpp collapse)
+    monkeypatch.setenv("FSGG_COLLAPSE_SEGSORT", segsort)
+    pts = oracle.random_dataset(n, 2, 11)
+    ds = F.Dataset(pts)
+    k = F.Kernel(F.KernelFamily.gaussian, 1.0)
+    tri = F.sample_neighbors_counted(ds, k, np.arange(n), rounds, 3)
+    q, s = tri[:, 0].astype(np.int64), tri[:, 1].astype(np.int64)
+    keep = q != s
+    key = np.unique(np.minimum(q, s)[keep] * n + np.maximum(q, s)[keep])
+    g = F.build_similarity_graph(ds, k, F.SparsifierConfig(rounds=rounds, seed=3))
+    assert np.array_equal(g.u.astype(np.int64), key // n)
+    assert np.array_equal(g.v.astype(np.int64), key % n)
+    longest = np.bincount(np.minimum(q, s)[keep]).max()  # before deduplication
+    assert longest > 512 if rounds == 2048 else longest <= 512
+    if rounds == 200:
+        assert longest > 256
