@@ -92,7 +92,10 @@ constexpr uint32_t kBoxMaxDim = 16;
 // mass. With at most 2^20 sub-chunks per node the skipped mass is below
 // 2^-(kPruneBits - 21) of the node mass -- far below the fp32 evaluation
 // error -- and the tie guard widens its margin by that bound (sampler.cu).
-constexpr float kPruneBits = 48.f;
+#ifndef FSGG_PRUNE_BITS
+#define FSGG_PRUNE_BITS 48.f
+#endif
+constexpr float kPruneBits = FSGG_PRUNE_BITS;
 
 struct KdeWorkspace;
 

@@ -22,6 +22,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cfloat>
 #include <vector>
 
 #include "engine.cuh"
@@ -115,6 +116,109 @@ __global__ void sym_fill_kernel(uint32_t B, const float* __restrict__ lo,
     __syncthreads();
     if (threadIdx.x == 0) base += total;
     __syncthreads();
+  }
+}
+
+// Spatial order inside each block, for batch pruning in the tile kernel.
+// The blocks are the reference's index-order tree nodes (sampler.cpp:138-141):
+// on C3 a block is a ~0.28 x 0.28 blob of noise around a short arc, so whole
+// block pairs within the pruning radius still hold many pairs far beyond it.
+// Each block's points are ordered by recursive splits — windows of 512, 256,
+// ..., 16 positions, each sorted along its widest box side — so every aligned
+// batch of kSymBatch positions is a small cluster with its own box (bbox).
+// A tile skips a source batch whose box is beyond the pruning radius of the
+// row block's box. Only the visiting order changes: sums are order-free up to
+// fp32 rounding, and results go back to the points' own positions (perm).
+constexpr uint32_t kSymBatch = 8;
+constexpr uint32_t kSymBatches = kSymBlock / kSymBatch;  // 40
+constexpr uint32_t kSymPermP = 512;                      // pow2 >= kSymBlock
+
+__global__ void __launch_bounds__(256)
+    sym_perm_kernel(const float* __restrict__ pts, uint32_t d, const uint32_t* __restrict__ bf,
+                    const uint32_t* __restrict__ bl, float* __restrict__ ppts,
+                    uint32_t* __restrict__ perm, float* __restrict__ bbox) {
+  // key: window (6 bits) | orderable coordinate (32) | local index (9)
+  __shared__ unsigned long long key[kSymPermP];
+  __shared__ uint32_t wdim[kSymPermP / 16];
+  const uint32_t I = blockIdx.x, f = bf[I], n = bl[I] - f;
+  const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  uint32_t P = 16;
+  while (P < n) P <<= 1;
+  for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) key[i] = i;
+  __syncthreads();
+  for (uint32_t W = P; W >= 16; W >>= 1) {
+    const uint32_t nw = P / W;
+    for (uint32_t w = threadIdx.x >> 5; w < nw; w += nwarps) {
+      float lo[kBoxMaxDim], hi[kBoxMaxDim];
+      for (uint32_t k = 0; k < d; ++k) {
+        lo[k] = FLT_MAX;
+        hi[k] = -FLT_MAX;
+      }
+      for (uint32_t pos = w * W + lane; pos < w * W + W; pos += 32) {
+        const uint32_t i = uint32_t(key[pos] & 511u);
+        if (i < n)
+          for (uint32_t k = 0; k < d; ++k) {
+            const float c = pts[size_t(f + i) * d + k];
+            lo[k] = fminf(lo[k], c);
+            hi[k] = fmaxf(hi[k], c);
+          }
+      }
+      uint32_t best = 0;
+      float ext = -1.f;
+      for (uint32_t k = 0; k < d; ++k) {
+        for (int o = 16; o; o >>= 1) {
+          lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+          hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+        }
+        if (hi[k] - lo[k] > ext) {
+          ext = hi[k] - lo[k];
+          best = k;
+        }
+      }
+      if (lane == 0) wdim[w] = best;
+    }
+    __syncthreads();
+    for (uint32_t pos = threadIdx.x; pos < P; pos += blockDim.x) {
+      const uint32_t i = uint32_t(key[pos] & 511u), w = pos / W;
+      uint32_t u = 0xffffffffu;  // absent positions sort last in their window
+      if (i < n) {
+        u = __float_as_uint(pts[size_t(f + i) * d + wdim[w]]);
+        u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+      }
+      key[pos] = (static_cast<unsigned long long>(w) << 41) |
+                 (static_cast<unsigned long long>(u) << 9) | i;
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t t = threadIdx.x; t < P / 2; t += blockDim.x) {
+          const uint32_t a = 2 * t - (t & (j - 1)), b = a + j;
+          const unsigned long long x = key[a], y = key[b];
+          if ((x > y) == ((a & k) == 0)) {
+            key[a] = y;
+            key[b] = x;
+          }
+        }
+        __syncthreads();
+      }
+  }
+  for (uint32_t pos = threadIdx.x; pos < n; pos += blockDim.x) {
+    const uint32_t i = uint32_t(key[pos] & 511u);
+    perm[f + pos] = i;
+    for (uint32_t k = 0; k < d; ++k) ppts[size_t(f + pos) * d + k] = pts[size_t(f + i) * d + k];
+  }
+  for (uint32_t b = threadIdx.x; b * kSymBatch < n; b += blockDim.x) {
+    float* out = bbox + (size_t(I) * kSymBatches + b) * 2 * d;
+    for (uint32_t k = 0; k < d; ++k) {
+      float lo = FLT_MAX, hi = -FLT_MAX;
+      for (uint32_t pos = b * kSymBatch; pos < min(n, (b + 1) * kSymBatch); ++pos) {
+        const float c = pts[size_t(f + uint32_t(key[pos] & 511u)) * d + k];
+        lo = fminf(lo, c);
+        hi = fmaxf(hi, c);
+      }
+      out[k] = lo;
+      out[d + k] = hi;
+    }
   }
 }
 
@@ -229,7 +333,9 @@ __device__ __forceinline__ void sym_tile_body(
     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
     const float* __restrict__ lo, const float* __restrict__ hi, float scale, float bits,
     const uint32_t* __restrict__ poff, float* __restrict__ P,
-    unsigned long long* __restrict__ performed, float* __restrict__ records) {
+    unsigned long long* __restrict__ performed, float* __restrict__ records,
+    const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
+    const float* __restrict__ bbox) {
   constexpr int kSymRows = ROWS;
   constexpr int kSymWarps = ROWS / 2;
   constexpr uint32_t kCap = 32u * ROWS;
@@ -279,7 +385,7 @@ __device__ __forceinline__ void sym_tile_body(
         nrm = 0.f;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-          xv[k] = (__ldg(pts + size_t(fj + j) * D + k) - c0[k]) * cs;
+          xv[k] = (__ldg(ppts + size_t(fj + j) * D + k) - c0[k]) * cs;
           nrm = fmaf(xv[k], xv[k], nrm);
         }
         mj = fmaxf(mj, nrm);
@@ -291,7 +397,7 @@ __device__ __forceinline__ void sym_tile_body(
   } else {
     for (uint32_t idx = threadIdx.x; idx < kCap * D; idx += blockDim.x) {
       const float v =
-          idx < nj * D ? -((__ldg(pts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
+          idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
       sx[idx] = make_float2(v, v);
     }
   }
@@ -326,7 +432,34 @@ __device__ __forceinline__ void sym_tile_body(
       s_max[1][w] = mj;
     }
   }
+  // source batches of J beyond the pruning radius of I's box: a row of I
+  // loses < nj 2^-thr <= 2^-bits over all of J's skipped batches and a
+  // source of J < ni 2^-thr, the same bound as a pruned block pair
+  __shared__ uint32_t s_skip[2];
+  if (threadIdx.x < 64) {
+    const uint32_t b = threadIdx.x;
+    bool sk = false;
+    if (tl.I != tl.J && b * kSymBatch < nj) {
+      const float* bx = bbox + (size_t(tl.J) * kSymBatches + b) * 2 * D;
+      float acc = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float g = fmaxf(0.f, fmaxf(__ldg(bx + k) - __ldg(hi + size_t(tl.I) * D + k),
+                                         __ldg(lo + size_t(tl.I) * D + k) - __ldg(bx + D + k)));
+        acc = FAM == 2 ? acc + g : fmaf(g, g, acc);
+      }
+      sk = scale * fam_finish1<FAM>(acc) > bits + __log2f(float(max(ni, nj)));
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, sk);
+    if (lane == 0) s_skip[w] = m;
+  }
   __syncthreads();
+  if (threadIdx.x == 0 && performed) {  // pair evaluations this tile executes
+    uint32_t kept = nj;
+    for (uint32_t b = 0; b * kSymBatch < nj; ++b)
+      if ((s_skip[b >> 5] >> (b & 31)) & 1u) kept -= min(kSymBatch, nj - b * kSymBatch);
+    if (kept) atomicAdd(performed, (unsigned long long)ni * kept);
+  }
   bool use_exp = false;
   if constexpr (EXP_OK) {
     mi = mj = 0.f;
@@ -340,13 +473,19 @@ __device__ __forceinline__ void sym_tile_body(
   float2 racc[kSymRows / 2];
 #pragma unroll
   for (int p = 0; p < kSymRows / 2; ++p) racc[p] = make_float2(0.f, 0.f);
-  // warp w: sources [64 w, 64 w + 64) in batches of 8: 8 column partials
+  // warp w: batches of 8 sources (w, w + warps, ...): 8 column partials
   // per lane (not 32) keep the kernel at 62 registers, 8 CTAs per SM — the
   // extra shuffles cost less than the occupancy buys (32: 30.0 ms, 16: 29.6,
   // 8: 28.9, 4: 30.1 on C3)
   auto tile_loop = [&](auto exp_tag) {
   constexpr bool EXP = decltype(exp_tag)::value;
-  for (uint32_t jb = w * 64; jb < w * 64 + 64 && jb < nj; jb += 8) {
+  // batches dealt round-robin: skipped batches cluster in the spatial order,
+  // so contiguous ranges would leave some warps idle while others work
+  for (uint32_t jb = w * 8; jb < nj; jb += 8 * kSymWarps) {
+    if ((s_skip[jb >> 8] >> ((jb >> 3) & 31)) & 1u) {
+      if (lane < 8 && jb + lane < nj) colv[jb + lane] = 0.f;
+      continue;
+    }
     float c[8];  // this lane's 8-row partial of each source's column sum
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj) {
@@ -437,10 +576,10 @@ __device__ __forceinline__ void sym_tile_body(
       float v = colv[t];
       float x[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) x[k] = __ldg(pts + size_t(fj + t) * D + k);
+      for (int k = 0; k < D; ++k) x[k] = __ldg(ppts + size_t(fj + t) * D + k);
       const float off = scale * box_dist<FAM>(x, lo + size_t(tl.I) * D, hi + size_t(tl.I) * D, D);
       if (off > __log2f(float(ni)) + bits) v = 0.f;
-      cdst[t] = v;
+      cdst[__ldg(perm + fj + t)] = v;
     }
   }
 }
@@ -454,9 +593,11 @@ __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
                     const uint32_t* __restrict__ bf, const uint32_t* __restrict__ bl,
                     const float* __restrict__ lo, const float* __restrict__ hi, float scale,
                     float bits, const uint32_t* __restrict__ poff, float* __restrict__ P,
-                    unsigned long long* __restrict__ performed, float* __restrict__ records) {
+                    unsigned long long* __restrict__ performed, float* __restrict__ records,
+                    const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
+                    const float* __restrict__ bbox) {
   sym_tile_body<D, FAM, ROWS, false>(pts, cs, tiles, bf, bl, lo, hi, scale, bits, poff, P,
-                                     performed, records);
+                                     performed, records, ppts, perm, bbox);
 }
 template <int D, int FAM, int ROWS>
 __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
@@ -466,9 +607,10 @@ __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
                         const float* __restrict__ lo, const float* __restrict__ hi,
                         float scale, float bits, const uint32_t* __restrict__ poff,
                         float* __restrict__ P, unsigned long long* __restrict__ performed,
-                        float* __restrict__ records) {
+                        float* __restrict__ records, const float* __restrict__ ppts,
+                        const uint32_t* __restrict__ perm, const float* __restrict__ bbox) {
   sym_tile_body<D, FAM, ROWS, true>(pts, cs, tiles, bf, bl, lo, hi, scale, bits, poff, P,
-                                    performed, records);
+                                    performed, records, ppts, perm, bbox);
 }
 
 // Fold each point's partner values, in ascending partner order, into its
@@ -787,7 +929,7 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   DevBuf& xtiles = ds.buf("sym.xtiles", own ? (size_t(npart) / 2 + 1) * sizeof(SymTile) : 16);
   sym_tiles_kernel<<<B, 128, 0, s>>>(B, poff.as<uint32_t>(), plist.as<uint32_t>(), b0, b1, bf,
                                      bl, tiles.as<SymTile>(), ntiles.as<uint32_t>(),
-                                     d_performed, own ? 1 : 0, ntiles.as<uint32_t>() + 1,
+                                     nullptr, own ? 1 : 0, ntiles.as<uint32_t>() + 1,
                                      rec.as<uint32_t>(), xtiles.as<SymTile>());
   FSGG_LAUNCH_CHECK();
   uint32_t nt2[2] = {0, 0};
@@ -795,6 +937,13 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   FSGG_CUDA(cudaStreamSynchronize(s));
   const uint32_t nt = nt2[0], nx = own ? nt2[1] : 0;
   DevBuf& P = ds.buf("sym.P", size_t(npart) * sym_pstride(ds, Lb) * 4 + 4);
+  DevBuf& ppts = ds.buf("sym.ppts", size_t(ds.n) * ds.d * 4);
+  DevBuf& perm = ds.buf("sym.perm", size_t(ds.n) * 4);
+  DevBuf& bbox = ds.buf("sym.bbox", size_t(B) * kSymBatches * 2 * ds.d * 4);
+  sym_perm_kernel<<<B, 256, 0, s>>>(ds.pts.as<float>(), ds.d, bf, bl, ppts.as<float>(),
+                                    perm.as<uint32_t>(), bbox.as<float>());
+  FSGG_LAUNCH_CHECK();
+  ds.launches++;
   if (ev0) FSGG_CUDA(cudaEventRecord(ev0, s));
   // the shard's own tiles with the single-GPU kernel, then (owner mode) the
   // cross-shard tiles with the kernel that exports one side
@@ -810,7 +959,8 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
         kern<<<cnt, threads, 0, s>>>(ds.pts.as<float>(), cs, tl, bf, bl, lo, hi,
                                      ks.scale, bits,
                                      poff.as<uint32_t>(), P.as<float>(), d_performed,
-                                     rec.as<float>());
+                                     rec.as<float>(), ppts.as<float>(), perm.as<uint32_t>(),
+                                     bbox.as<float>());
       };
       auto by_rows = [&](auto fam) {
         constexpr int FAM = decltype(fam)::value;
