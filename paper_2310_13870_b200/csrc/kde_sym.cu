@@ -613,6 +613,195 @@ __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
                                     performed, records, ppts, perm, bbox);
 }
 
+// Warp-per-tile variant for d <= 2 (C2/C3: the headline path). One warp
+// evaluates a whole tile on its own — its 32 lanes hold all 32 * ROWS rows of
+// I, the sources of J sit in the warp's private shared-memory slice — so a
+// tile needs no CTA barrier and no cross-warp row reduction, and the warps
+// of an SM run at 32 independent phases instead of 8 lock-stepped groups of
+// 4 (the CTA-per-tile kernel lost ~1 issue slot in 12 to barrier stalls once
+// batch pruning made its warps' shares uneven: XU 83% -> 72%). Warps are
+// persistent and take tiles in list order from a device counter, so a warp
+// that drew heavily pruned tiles simply takes more of them. A row's value is
+// the fp32 sum over J's kept batches in batch order; it depends on the two
+// blocks alone (deterministic, shard-safe).
+constexpr int kWtWarps = 4;
+
+template <int D, int FAM, int ROWS, bool OWN>
+__device__ __forceinline__ void sym_wtile_body(
+    const float* __restrict__ pts, float cs, const SymTile* __restrict__ tiles,
+    uint32_t ntiles, uint32_t* __restrict__ next, const uint32_t* __restrict__ bf,
+    const uint32_t* __restrict__ bl, const float* __restrict__ lo,
+    const float* __restrict__ hi, float scale, float bits,
+    const uint32_t* __restrict__ poff, float* __restrict__ P,
+    unsigned long long* __restrict__ performed, float* __restrict__ records,
+    const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
+    const float* __restrict__ bbox) {
+  constexpr uint32_t kCap = 32u * ROWS;
+  __shared__ __align__(16) float2 sx_all[kWtWarps][kCap * D];
+  __shared__ float colv_all[kWtWarps][kCap];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float2* sx = sx_all[w];
+  float* colv = colv_all[w];
+  float* rowv = reinterpret_cast<float*>(sx);  // reused after the tile loop
+  unsigned long long ev = 0;                   // pair evaluations of this warp's tiles
+  for (;;) {
+    uint32_t ti = 0;
+    if (lane == 0) ti = atomicAdd(next, 1u);
+    ti = __shfl_sync(0xffffffffu, ti, 0);
+    if (ti >= ntiles) break;
+    const SymTile tl = tiles[ti];
+    const uint32_t fi = __ldg(bf + tl.I), ni = __ldg(bl + tl.I) - fi;
+    const uint32_t fj = __ldg(bf + tl.J), nj = __ldg(bl + tl.J) - fj;
+    // coordinates relative to I's first point, pre-scaled (see sym_tile_body)
+    float c0[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
+    const uint32_t njp = (nj + 7u) & ~7u;  // whole batches; slots past nj far away
+    for (uint32_t idx = lane; idx < njp * D; idx += 32) {
+      const float v =
+          idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
+      sx[idx] = make_float2(v, v);
+    }
+    float2 q2[ROWS / 2][D];
+#pragma unroll
+    for (int p = 0; p < ROWS / 2; ++p) {
+      const uint32_t r0 = lane * ROWS + 2 * p, r1 = r0 + 1;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : 1e18f;
+        const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : 1e18f;
+        q2[p][k] = make_float2(a, b);
+      }
+    }
+    // source batches of J beyond the pruning radius of I's box (sym_tile_body)
+    uint32_t skip[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t b = lane + 32u * h;
+      bool sk = false;
+      if (tl.I != tl.J && b * kSymBatch < nj) {
+        const float* bx = bbox + (size_t(tl.J) * kSymBatches + b) * 2 * D;
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float g = fmaxf(0.f, fmaxf(__ldg(bx + k) - __ldg(hi + size_t(tl.I) * D + k),
+                                           __ldg(lo + size_t(tl.I) * D + k) - __ldg(bx + D + k)));
+          acc = FAM == 2 ? acc + g : fmaf(g, g, acc);
+        }
+        sk = scale * fam_finish1<FAM>(acc) > bits + __log2f(float(max(ni, nj)));
+      }
+      skip[h] = __ballot_sync(0xffffffffu, sk);
+    }
+    {
+      const uint32_t lb = (nj - 1u) >> 3;  // the last batch may be partial
+      uint32_t dropped = 8u * (__popc(skip[0]) + __popc(skip[1]));
+      if ((skip[lb >> 5] >> (lb & 31)) & 1u) dropped -= 8u * (lb + 1u) - nj;
+      ev += (unsigned long long)ni * (nj - dropped);
+    }
+    __syncwarp();
+    float2 racc[ROWS / 2];
+#pragma unroll
+    for (int p = 0; p < ROWS / 2; ++p) racc[p] = make_float2(0.f, 0.f);
+    for (uint32_t jb = 0; jb < nj; jb += 8) {
+      if ((skip[jb >> 8] >> ((jb >> 3) & 31)) & 1u) {
+        if (lane < 8 && jb + lane < nj) colv[jb + lane] = 0.f;
+        continue;
+      }
+      float c[8];  // this lane's ROWS-row partial of each source's column sum
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const float2* x = sx + (jb + jj) * D;
+        float2 es = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int p = 0; p < ROWS / 2; ++p) {
+          float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+#pragma unroll
+          for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
+          t = fam_finish<FAM>(t);
+          const float2 e = make_float2(ex2_approx(-t.x), ex2_approx(-t.y));
+          racc[p] = __fadd2_rn(racc[p], e);
+          es = p == 0 ? e : __fadd2_rn(es, e);
+        }
+        c[jj] = es.x + es.y;
+      }
+      // lanes l ^ 16 and l ^ 8 folded, then a transpose-reduction butterfly
+      // over 8 lanes: lane l ends with the column sum of source jb + (l & 7)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 8);
+#pragma unroll
+      for (int st = 4; st >= 1; st >>= 1) {
+        const bool up = (lane & st) != 0;
+#pragma unroll
+        for (int i = 0; i < st; ++i) {
+          const float keep = up ? c[i + st] : c[i];
+          const float send = up ? c[i] : c[i + st];
+          c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+        }
+      }
+      if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < ROWS / 2; ++p) {
+      rowv[lane * ROWS + 2 * p] = racc[p].x;
+      rowv[lane * ROWS + 2 * p + 1] = racc[p].y;
+    }
+    __syncwarp();
+    float* rdst = P + (size_t(poff[tl.I]) + tl.slotI) * kCap;
+    float* cdst = P + (size_t(poff[tl.J]) + tl.slotJ) * kCap;
+    if constexpr (OWN) {
+      if (tl.remote & 1u) rdst = records + size_t(tl.rec) * kSymRecWords + 4;
+      if (tl.remote & 2u) cdst = records + size_t(tl.rec) * kSymRecWords + 4;
+    }
+    // a point that prunes the partner block drops its value
+    for (uint32_t t = lane; t < ni; t += 32) {
+      float q[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) q[k] = __ldg(pts + size_t(fi + t) * D + k);
+      const float off = scale * box_dist<FAM>(q, lo + size_t(tl.J) * D, hi + size_t(tl.J) * D, D);
+      rdst[t] = off > __log2f(float(nj)) + bits ? 0.f : rowv[t];
+    }
+    if (tl.I != tl.J) {
+      for (uint32_t t = lane; t < nj; t += 32) {
+        float x[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = __ldg(ppts + size_t(fj + t) * D + k);
+        const float off =
+            scale * box_dist<FAM>(x, lo + size_t(tl.I) * D, hi + size_t(tl.I) * D, D);
+        cdst[__ldg(perm + fj + t)] = off > __log2f(float(ni)) + bits ? 0.f : colv[t];
+      }
+    }
+    __syncwarp();  // rowv/colv are refilled by the next tile
+  }
+  if (performed) {
+    if (lane == 0 && ev) atomicAdd(performed, ev);
+  }
+}
+
+#define FSGG_WT_ARGS                                                                          \
+  const float *__restrict__ pts, float cs, const SymTile *__restrict__ tiles, uint32_t ntiles, \
+      uint32_t *__restrict__ next, const uint32_t *__restrict__ bf,                            \
+      const uint32_t *__restrict__ bl, const float *__restrict__ lo,                           \
+      const float *__restrict__ hi, float scale, float bits, const uint32_t *__restrict__ poff, \
+      float *__restrict__ P, unsigned long long *__restrict__ performed,                       \
+      float *__restrict__ records, const float *__restrict__ ppts,                             \
+      const uint32_t *__restrict__ perm, const float *__restrict__ bbox
+template <int D, int FAM, int ROWS>
+__global__ void __launch_bounds__(kWtWarps * 32, ROWS == 8 ? 8 : 6)
+    sym_wtile_kernel(FSGG_WT_ARGS) {
+  sym_wtile_body<D, FAM, ROWS, false>(pts, cs, tiles, ntiles, next, bf, bl, lo, hi, scale, bits,
+                                      poff, P, performed, records, ppts, perm, bbox);
+}
+template <int D, int FAM, int ROWS>
+__global__ void __launch_bounds__(kWtWarps * 32, ROWS == 8 ? 8 : 6)
+    sym_wtile_own_kernel(FSGG_WT_ARGS) {
+  sym_wtile_body<D, FAM, ROWS, true>(pts, cs, tiles, ntiles, next, bf, bl, lo, hi, scale, bits,
+                                     poff, P, performed, records, ppts, perm, bbox);
+}
+#undef FSGG_WT_ARGS
+
 // Fold each point's partner values, in ascending partner order, into its
 // fp64 bucket row (bucket of partner J = J >> shift).
 constexpr uint32_t kSymBucketChunk = 16;  // 16 x 257 fp64 = 32 KiB of shared memory
@@ -922,8 +1111,9 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
                                     poff.as<uint32_t>(), plist.as<uint32_t>());
   FSGG_LAUNCH_CHECK();
   DevBuf& tiles = ds.buf("sym.tiles", size_t(npart) * sizeof(SymTile) + 16);
-  DevBuf& ntiles = ds.buf("sym.ntiles", 8);
-  FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 8, s));
+  // [tiles, cross tiles, the warp-per-tile kernels' two take counters]
+  DevBuf& ntiles = ds.buf("sym.ntiles", 16);
+  FSGG_CUDA(cudaMemsetAsync(ntiles.as<void>(), 0, 16, s));
   // a cross tile has one remote side: at most half the partner slots
   DevBuf& rec = ds.buf("sym.rec", own ? (size_t(npart) / 2 + 1) * kSymRecWords * 4 : 4);
   DevBuf& xtiles = ds.buf("sym.xtiles", own ? (size_t(npart) / 2 + 1) * sizeof(SymTile) : 16);
@@ -949,12 +1139,46 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   // cross-shard tiles with the kernel that exports one side
   const int rows = sym_rows_per_lane(ds, Lb);
   const float cs = ks.family == 0 ? sqrtf(ks.scale) : ks.scale;
+  static const bool wpt = [] {
+    const char* e = std::getenv("FSGG_SYM_WPT");
+    return !e || std::atoi(e) != 0;
+  }();
   for (int pass = 0; pass < 2; ++pass) {
     const uint32_t cnt = pass == 0 ? nt : nx;
     if (cnt == 0) continue;
     const SymTile* tl = pass == 0 ? tiles.as<SymTile>() : xtiles.as<SymTile>();
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
+      // d <= 2: persistent warp-per-tile kernel, tiles taken from a counter
+      if constexpr (D <= 2) {
+        if (wpt) {
+          auto wlaunch = [&](auto kern) {
+            int per_sm = 0;
+            FSGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                                    kWtWarps * 32, 0));
+            const uint32_t grid = std::min<uint32_t>(
+                (cnt + kWtWarps - 1) / kWtWarps, uint32_t(std::max(per_sm, 1)) * uint32_t(ds.num_sms));
+            kern<<<grid, kWtWarps * 32, 0, s>>>(
+                ds.pts.as<float>(), cs, tl, cnt, ntiles.as<uint32_t>() + 2 + pass, bf, bl, lo,
+                hi, ks.scale, bits, poff.as<uint32_t>(), P.as<float>(), d_performed,
+                rec.as<float>(), ppts.as<float>(), perm.as<uint32_t>(), bbox.as<float>());
+          };
+          auto wby_rows = [&](auto fam) {
+            constexpr int FAM = decltype(fam)::value;
+            if (rows == 10)
+              return pass ? wlaunch(sym_wtile_own_kernel<D, FAM, 10>)
+                          : wlaunch(sym_wtile_kernel<D, FAM, 10>);
+            pass ? wlaunch(sym_wtile_own_kernel<D, FAM, 8>)
+                 : wlaunch(sym_wtile_kernel<D, FAM, 8>);
+          };
+          switch (ks.family) {
+            case 0: wby_rows(std::integral_constant<int, 0>{}); break;
+            case 1: wby_rows(std::integral_constant<int, 1>{}); break;
+            default: wby_rows(std::integral_constant<int, 2>{}); break;
+          }
+          return;
+        }
+      }
       auto launch = [&](auto kern, int threads) {
         kern<<<cnt, threads, 0, s>>>(ds.pts.as<float>(), cs, tl, bf, bl, lo, hi,
                                      ks.scale, bits,
