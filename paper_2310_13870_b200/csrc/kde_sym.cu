@@ -626,6 +626,15 @@ __global__ void __launch_bounds__(ROWS * 16, ROWS == 10 ? FSGG_SYM_R10_CTAS : 0)
 // blocks alone (deterministic, shard-safe).
 constexpr int kWtWarps = 4;
 
+// Sources of J staged per warp: all of them for d <= 2, else stages of
+// kWtStage<..> sources (<= 8 KiB of shared memory per warp) — the warp fills
+// its own slice, so staging costs nothing but the loop.
+template <int SW, uint32_t CAP>
+constexpr uint32_t wt_stage() {
+  const uint32_t fit = (8192u / (SW * 8u)) & ~7u;
+  return fit < CAP ? fit : CAP;
+}
+
 template <int D, int FAM, int ROWS, bool OWN>
 __device__ __forceinline__ void sym_wtile_body(
     const float* __restrict__ pts, float cs, const SymTile* __restrict__ tiles,
@@ -637,7 +646,11 @@ __device__ __forceinline__ void sym_wtile_body(
     const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
     const float* __restrict__ bbox) {
   constexpr uint32_t kCap = 32u * ROWS;
-  __shared__ __align__(16) float2 sx_all[kWtWarps][kCap * D];
+  constexpr bool EXP_OK = FAM == 0 && D >= FSGG_SYM_EXP_MIN_D;
+  constexpr int SW = EXP_OK ? D + 1 : D;  // float2 per source in shared memory
+  constexpr uint32_t SC = wt_stage<SW, kCap>();
+  static_assert(SC * SW * 2 >= kCap, "the stage buffer doubles as the row buffer");
+  __shared__ __align__(16) float2 sx_all[kWtWarps][SC * SW];
   __shared__ float colv_all[kWtWarps][kCap];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float2* sx = sx_all[w];
@@ -652,26 +665,56 @@ __device__ __forceinline__ void sym_wtile_body(
     const SymTile tl = tiles[ti];
     const uint32_t fi = __ldg(bf + tl.I), ni = __ldg(bl + tl.I) - fi;
     const uint32_t fj = __ldg(bf + tl.J), nj = __ldg(bl + tl.J) - fj;
-    // coordinates relative to I's first point, pre-scaled (see sym_tile_body)
+    // coordinates relative to I's first point (expanded form: the midpoint of
+    // the two blocks' box centres), pre-scaled (see sym_tile_body)
     float c0[D];
+    if constexpr (EXP_OK) {
 #pragma unroll
-    for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
-    const uint32_t njp = (nj + 7u) & ~7u;  // whole batches; slots past nj far away
-    for (uint32_t idx = lane; idx < njp * D; idx += 32) {
-      const float v =
-          idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
-      sx[idx] = make_float2(v, v);
+      for (int k = 0; k < D; ++k)
+        c0[k] = 0.25f * ((__ldg(lo + size_t(tl.I) * D + k) + __ldg(hi + size_t(tl.I) * D + k)) +
+                         (__ldg(lo + size_t(tl.J) * D + k) + __ldg(hi + size_t(tl.J) * D + k)));
+    } else {
+#pragma unroll
+      for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
     }
     float2 q2[ROWS / 2][D];
+    float2 qn[EXP_OK ? ROWS / 2 : 1];  // expanded form: |q'|^2 of each row pair
+    float mi = 0.f, mj = 0.f;
 #pragma unroll
     for (int p = 0; p < ROWS / 2; ++p) {
       const uint32_t r0 = lane * ROWS + 2 * p, r1 = r0 + 1;
+      float na = 0.f, nb = 0.f;
 #pragma unroll
       for (int k = 0; k < D; ++k) {
         const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : 1e18f;
         const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : 1e18f;
         q2[p][k] = make_float2(a, b);
+        na = fmaf(a, a, na);
+        nb = fmaf(b, b, nb);
       }
+      if constexpr (EXP_OK) {
+        qn[p] = make_float2(r0 < ni ? na : 1e30f, r1 < ni ? nb : 1e30f);
+        if (r0 < ni) mi = fmaxf(mi, na);
+        if (r1 < ni) mi = fmaxf(mi, nb);
+      }
+    }
+    bool use_exp = false;
+    if constexpr (EXP_OK) {
+      // the form is the tile's: largest scaled norms of its two blocks
+      for (uint32_t j = lane; j < nj; j += 32) {
+        float nrm = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+          const float xv = (__ldg(ppts + size_t(fj + j) * D + k) - c0[k]) * cs;
+          nrm = fmaf(xv, xv, nrm);
+        }
+        mj = fmaxf(mj, nrm);
+      }
+      for (int o = 16; o; o >>= 1) {
+        mi = fmaxf(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+        mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
+      }
+      use_exp = mi + mj <= kSymExpMaxNorm;
     }
     // source batches of J beyond the pruning radius of I's box (sym_tile_body)
     uint32_t skip[2];
@@ -698,49 +741,106 @@ __device__ __forceinline__ void sym_wtile_body(
       if ((skip[lb >> 5] >> (lb & 31)) & 1u) dropped -= 8u * (lb + 1u) - nj;
       ev += (unsigned long long)ni * (nj - dropped);
     }
-    __syncwarp();
     float2 racc[ROWS / 2];
 #pragma unroll
     for (int p = 0; p < ROWS / 2; ++p) racc[p] = make_float2(0.f, 0.f);
-    for (uint32_t jb = 0; jb < nj; jb += 8) {
-      if ((skip[jb >> 8] >> ((jb >> 3) & 31)) & 1u) {
-        if (lane < 8 && jb + lane < nj) colv[jb + lane] = 0.f;
-        continue;
-      }
-      float c[8];  // this lane's ROWS-row partial of each source's column sum
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const float2* x = sx + (jb + jj) * D;
-        float2 es = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int p = 0; p < ROWS / 2; ++p) {
-          float2 t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
-#pragma unroll
-          for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
-          t = fam_finish<FAM>(t);
-          const float2 e = make_float2(ex2_approx(-t.x), ex2_approx(-t.y));
-          racc[p] = __fadd2_rn(racc[p], e);
-          es = p == 0 ? e : __fadd2_rn(es, e);
+    auto stage_loop = [&](auto exp_tag, uint32_t s0, uint32_t s1) {
+      constexpr bool EXP = decltype(exp_tag)::value;
+      for (uint32_t jb = s0; jb < s1; jb += 8) {
+        if ((skip[jb >> 8] >> ((jb >> 3) & 31)) & 1u) {
+          if (lane < 8 && jb + lane < nj) colv[jb + lane] = 0.f;
+          continue;
         }
-        c[jj] = es.x + es.y;
+        float c[8];  // this lane's ROWS-row partial of each source's column sum
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const float2* x = sx + (jb - s0 + jj) * SW;
+          float2 es = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < ROWS / 2; ++p) {
+            float2 t;
+            if constexpr (EXP) {
+              t = __fadd2_rn(qn[p], x[D]);
+#pragma unroll
+              for (int k = 0; k < D; ++k) t = __ffma2_rn(q2[p][k], x[k], t);
+            } else if constexpr (EXP_OK) {  // -x' = 0.5 * (-2 x'), exactly
+              const float2 h = make_float2(0.5f, 0.5f);
+              t = fam_first<FAM>(__ffma2_rn(h, x[0], q2[p][0]));
+#pragma unroll
+              for (int k = 1; k < D; ++k) t = fam_next<FAM>(__ffma2_rn(h, x[k], q2[p][k]), t);
+              t = fam_finish<FAM>(t);
+            } else {
+              t = fam_first<FAM>(__fadd2_rn(q2[p][0], x[0]));
+#pragma unroll
+              for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[p][k], x[k]), t);
+              t = fam_finish<FAM>(t);
+            }
+            const float2 e = make_float2(ex2_approx(-t.x), ex2_approx(-t.y));
+            racc[p] = __fadd2_rn(racc[p], e);
+            es = p == 0 ? e : __fadd2_rn(es, e);
+          }
+          c[jj] = es.x + es.y;
+        }
+        // lanes l ^ 16 and l ^ 8 folded, then a transpose-reduction butterfly
+        // over 8 lanes: lane l ends with the column sum of source jb + (l & 7)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 8);
+#pragma unroll
+        for (int st = 4; st >= 1; st >>= 1) {
+          const bool up = (lane & st) != 0;
+#pragma unroll
+          for (int i = 0; i < st; ++i) {
+            const float keep = up ? c[i + st] : c[i];
+            const float send = up ? c[i] : c[i + st];
+            c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+          }
+        }
+        if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
       }
-      // lanes l ^ 16 and l ^ 8 folded, then a transpose-reduction butterfly
-      // over 8 lanes: lane l ends with the column sum of source jb + (l & 7)
+    };
+    const uint32_t njp = (nj + 7u) & ~7u;  // whole batches; slots past nj far away
+    for (uint32_t s0 = 0; s0 < njp; s0 += SC) {
+      const uint32_t s1 = min(njp, s0 + SC);
+      if (s0) __syncwarp();  // the previous stage has been read
+      if constexpr (EXP_OK) {
+        // -2 x' and |x'|^2 (absent: x' = 1e18, |x'|^2 = 1e30): the direct form
+        // takes -x' = 0.5 * (-2 x') exactly through one FFMA2
+        for (uint32_t j = s0 + lane; j < s1; j += 32) {
+          float nrm = 1e30f;
+          float xv[D];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
+          for (int k = 0; k < D; ++k) xv[k] = 1e18f;
+          if (j < nj) {
+            nrm = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 8);
+            for (int k = 0; k < D; ++k) {
+              xv[k] = (__ldg(ppts + size_t(fj + j) * D + k) - c0[k]) * cs;
+              nrm = fmaf(xv[k], xv[k], nrm);
+            }
+          }
 #pragma unroll
-      for (int st = 4; st >= 1; st >>= 1) {
-        const bool up = (lane & st) != 0;
-#pragma unroll
-        for (int i = 0; i < st; ++i) {
-          const float keep = up ? c[i + st] : c[i];
-          const float send = up ? c[i] : c[i + st];
-          c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+          for (int k = 0; k < D; ++k)
+            sx[(j - s0) * SW + k] = make_float2(-2.f * xv[k], -2.f * xv[k]);
+          sx[(j - s0) * SW + D] = make_float2(nrm, nrm);
+        }
+      } else {
+        for (uint32_t idx = s0 * D + lane; idx < s1 * D; idx += 32) {
+          const float v =
+              idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
+          sx[idx - s0 * D] = make_float2(v, v);
         }
       }
-      if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
+      __syncwarp();
+      if constexpr (EXP_OK) {
+        if (use_exp)
+          stage_loop(std::true_type{}, s0, s1);
+        else
+          stage_loop(std::false_type{}, s0, s1);
+      } else {
+        stage_loop(std::false_type{}, s0, s1);
+      }
     }
     __syncwarp();
 #pragma unroll
@@ -780,6 +880,13 @@ __device__ __forceinline__ void sym_wtile_body(
   }
 }
 
+#ifndef FSGG_WT_CTAS_HID
+#define FSGG_WT_CTAS_HID 5
+#endif
+template <int D, int ROWS>
+constexpr int wt_ctas() {
+  return D <= 2 ? (ROWS == 8 ? 8 : 6) : (ROWS == 8 ? 6 : FSGG_WT_CTAS_HID);
+}
 #define FSGG_WT_ARGS                                                                          \
   const float *__restrict__ pts, float cs, const SymTile *__restrict__ tiles, uint32_t ntiles, \
       uint32_t *__restrict__ next, const uint32_t *__restrict__ bf,                            \
@@ -789,13 +896,13 @@ __device__ __forceinline__ void sym_wtile_body(
       float *__restrict__ records, const float *__restrict__ ppts,                             \
       const uint32_t *__restrict__ perm, const float *__restrict__ bbox
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(kWtWarps * 32, ROWS == 8 ? 8 : 6)
+__global__ void __launch_bounds__(kWtWarps * 32, wt_ctas<D, ROWS>())
     sym_wtile_kernel(FSGG_WT_ARGS) {
   sym_wtile_body<D, FAM, ROWS, false>(pts, cs, tiles, ntiles, next, bf, bl, lo, hi, scale, bits,
                                       poff, P, performed, records, ppts, perm, bbox);
 }
 template <int D, int FAM, int ROWS>
-__global__ void __launch_bounds__(kWtWarps * 32, ROWS == 8 ? 8 : 6)
+__global__ void __launch_bounds__(kWtWarps * 32, wt_ctas<D, ROWS>())
     sym_wtile_own_kernel(FSGG_WT_ARGS) {
   sym_wtile_body<D, FAM, ROWS, true>(pts, cs, tiles, ntiles, next, bf, bl, lo, hi, scale, bits,
                                      poff, P, performed, records, ppts, perm, bbox);
@@ -1139,9 +1246,10 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
   // cross-shard tiles with the kernel that exports one side
   const int rows = sym_rows_per_lane(ds, Lb);
   const float cs = ks.family == 0 ? sqrtf(ks.scale) : ks.scale;
-  static const bool wpt = [] {
+  // FSGG_SYM_WPT: 0 CTA-per-tile kernels, 1 warp-per-tile for d <= 2, 2 for d <= 6
+  static const int wpt = [] {
     const char* e = std::getenv("FSGG_SYM_WPT");
-    return !e || std::atoi(e) != 0;
+    return e ? std::atoi(e) : 2;
   }();
   for (int pass = 0; pass < 2; ++pass) {
     const uint32_t cnt = pass == 0 ? nt : nx;
@@ -1149,9 +1257,9 @@ void sym_tile_pass(Dataset& ds, const KernelSpec& ks, uint32_t qb, uint32_t qe, 
     const SymTile* tl = pass == 0 ? tiles.as<SymTile>() : xtiles.as<SymTile>();
     sym_by_dim(ds.d, [&](auto dim) {
       constexpr int D = decltype(dim)::value;
-      // d <= 2: persistent warp-per-tile kernel, tiles taken from a counter
-      if constexpr (D <= 2) {
-        if (wpt) {
+      // persistent warp-per-tile kernel, tiles taken from a counter
+      if constexpr (D <= 6) {
+        if (wpt >= 2 || (wpt == 1 && D <= 2)) {
           auto wlaunch = [&](auto kern) {
             int per_sm = 0;
             FSGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
