@@ -14,6 +14,8 @@
 // in the lists; scatter_kernel routes children with exactly one ticket here.
 // Per-level counters (entries, tickets, evaluations, degenerate draws) are
 // aggregated per warp by level, so the reference's diagnostics are intact.
+#include <cstdlib>
+
 #include "engine.cuh"
 #include "kde_math.cuh"
 
@@ -211,6 +213,230 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
   }
 }
 
+// ---- fast walk (reference RNG with the tie guard on) ------------------------
+// With the tie guard every fp32-based decision whose draw lies within the
+// sums' error of p is re-decided on exact fp64 sums, so the fast path only
+// has to be (a) within the guard's margin of the exact p and (b) cheap:
+//   * one exponent offset per node (its own box) instead of one per child, so
+//     the two children's fp32 sums share a scale and p needs no rescaling;
+//     the children are summed in one loop (two independent accumulators);
+//   * no division and no float-to-integer conversions: with u = m 2^-53 the
+//     draw u < a / (a + b) is u (a + b) - a < 0, and "near" is
+//     |u (a + b) - a| <= rel min(a, b) + (pruned + 2^-51)(a + b) — the same
+//     test as decide()'s, multiplied through by a + b;
+//   * per-level tallies once per walk: a thread keeps its start level, start
+//     size and the left/right bits of its path; node sizes along the path
+//     follow from those, and the warp adds them up per level after the loop
+//     (the per-step version spent 15% of the kernel's instructions on it).
+// Steps the fast path cannot take — both fp32 sums zero, or an offset so
+// large that the 1e-300 floor could matter — run the per-child-offset sums
+// and decide() exactly as walk_kernel does (slow_step).
+struct StepOut {
+  bool left;
+  uint32_t dg, tie;
+  float em;
+};
+
+template <int D, int FAM>
+__device__ __noinline__ StepOut slow_step(const float* __restrict__ pts, uint32_t q, uint64_t h,
+                                          uint32_t f, uint32_t l,
+                                          const float* __restrict__ tlo,
+                                          const float* __restrict__ thi, int has_boxes,
+                                          float scale, int family, double sigma, float em,
+                                          uint64_t qlink, uint64_t key_prefix, uint64_t seed,
+                                          const uint64_t* __restrict__ nlink, bool fp32_first) {
+  StepOut o{false, 0u, 0u, 0.f};
+  float qc[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
+  double a = 0.0, b = 0.0;
+  Decision dc{false, true, false};
+  if (fp32_first) {
+    double s[2];
+    direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
+    a = fmax(s[0], kSumFloor);
+    b = fmax(s[1], kSumFloor);
+    dc = decide(a, b, em, f, l, q, qlink, key_prefix, 0, seed, true, nlink, h, 0.0);
+  }
+  if (dc.near) {  // tie guard: exact fp64 sums (kernel_f64, index order)
+    const uint32_t mid = f + (l - f) / 2;
+    const float* xq = pts + size_t(q) * D;
+    double e0 = 0.0, e1 = 0.0;
+    for (uint32_t j = f; j < mid; ++j) e0 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
+    for (uint32_t j = mid; j < l; ++j) e1 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
+    a = fmax(e0, kSumFloor);
+    b = fmax(e1, kSumFloor);
+    dc = decide(a, b, em, f, l, q, qlink, key_prefix, 0, seed, false, nlink, h, 0.0);
+    o.tie = 1u;
+  }
+  o.left = dc.left;
+  o.dg = dc.degenerate ? 1u : 0u;
+  o.em = float(int((__double_as_longlong(dc.left ? a : b) >> 52) & 0x7ff) - 1023);
+  return o;
+}
+
+template <int D, int FAM>
+__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
+    walk_fast_kernel(const float* __restrict__ pts, uint32_t W, const uint32_t* __restrict__ wq,
+                     const uint32_t* __restrict__ wh, const float* __restrict__ welm,
+                     const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
+                     const float* __restrict__ tlo, const float* __restrict__ thi,
+                     int has_boxes, float scale, int family, double sigma,
+                     uint64_t key_prefix, uint64_t seed, const uint32_t* __restrict__ qrow,
+                     const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_cnt,
+                     uint32_t* __restrict__ leaf_src, uint32_t* __restrict__ leaf_cnt,
+                     unsigned long long* __restrict__ stats,
+                     const uint64_t* __restrict__ nlink, const uint32_t* __restrict__ wrow,
+                     const float* __restrict__ wrm, const double* __restrict__ rows,
+                     uint32_t rows_level) {
+  __shared__ unsigned int s_stats[5][kMaxLevels];
+  for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
+  __syncthreads();
+
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool mine = i < W;
+  uint32_t q = 0, lev0 = 0xffffffffu, n0 = 0, path = 0, steps = 0, sv0 = 0;
+  if (mine) {
+    q = wq[i];
+    const uint64_t qlink = query_link(q);
+    uint64_t h = wh[i];
+    uint32_t nf = tfirst[h], nl = tlast[h];
+    float em = welm[i];
+    lev0 = 31 - __clz(uint32_t(h) + 1);
+    n0 = nl - nf;
+    uint32_t row = 0xffffffffu;
+    float rmass = 0.f;
+    if (rows && lev0 == rows_level + 1) {
+      row = wrow[i];
+      rmass = wrm[i];
+    }
+    float qc[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
+    while (nl - nf > 1) {
+      const uint32_t f = nf, l = nl, mid = f + (l - f) / 2;
+      double a, b, pruned = 0.0;
+      float offn = 0.f;
+      bool fast;
+      const bool rowstep = row != 0xffffffffu;
+      if (rowstep) {
+        // the node's children are buckets 2 side, 2 side + 1 of the row (see
+        // walk_kernel); absolute fp64 sums
+        const double* r = rows + (size_t(row) << 2) + ((h & 1u) ? 0u : 2u);
+        a = fmax(r[0], kSumFloor);
+        b = fmax(r[1], kSumFloor);
+        pruned = double(exp2f(rmass - (kPruneBits - 24.f) - em));
+        sv0 = l - f;
+        row = 0xffffffffu;
+        fast = a > kSumFloor || b > kSumFloor;
+      } else {
+        offn = has_boxes ? scale * box_dist_d<D, FAM>(qc, tlo + h * D, thi + h * D) : 0.f;
+        float a0 = 0.f, a1 = 0.f;
+        const uint32_t nleft = mid - f;  // the right child has nleft or nleft + 1 points
+        for (uint32_t j = 0; j < nleft; ++j) {
+          float t0 = 0.f, t1 = 0.f;
+          if constexpr (D == 2) {
+            const float2 x0 = __ldg(reinterpret_cast<const float2*>(pts) + f + j);
+            const float2 x1 = __ldg(reinterpret_cast<const float2*>(pts) + mid + j);
+            t0 = fam_acc1<FAM>(qc[0] - x0.x, t0);
+            t0 = fam_acc1<FAM>(qc[1] - x0.y, t0);
+            t1 = fam_acc1<FAM>(qc[0] - x1.x, t1);
+            t1 = fam_acc1<FAM>(qc[1] - x1.y, t1);
+          } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+              t0 = fam_acc1<FAM>(qc[k] - __ldg(pts + size_t(f + j) * D + k), t0);
+              t1 = fam_acc1<FAM>(qc[k] - __ldg(pts + size_t(mid + j) * D + k), t1);
+            }
+          }
+          a0 += ex2_approx(fmaf(fam_finish1<FAM>(t0), -scale, offn));
+          a1 += ex2_approx(fmaf(fam_finish1<FAM>(t1), -scale, offn));
+        }
+        if (l - mid > nleft) {
+          float t1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < D; ++k)
+            t1 = fam_acc1<FAM>(qc[k] - __ldg(pts + size_t(l - 1) * D + k), t1);
+          a1 += ex2_approx(fmaf(fam_finish1<FAM>(t1), -scale, offn));
+        }
+        a = double(a0);
+        b = double(a1);
+        fast = (a0 > 0.f || a1 > 0.f) && offn < 800.f;
+      }
+      bool left;
+      if (fast) {
+        const uint64_t key = nlink ? splitmix64(__ldg(nlink + h) ^ qlink)
+                                   : route_key_q(key_prefix, (uint64_t(f) << 32) | l, qlink);
+        const uint64_t m = splitmix64(key) >> 11;
+        const double ssum = a + b;
+        const double t = fma(double(m) * 0x1p-53, ssum, -a);
+        const float rel = float(kTieMargin) * (1.f + fmaxf(0.f, -em) * (1.f / 32.f));
+        const double M = fma(double(rel), fmin(a, b), (pruned + 0x1p-51) * ssum);
+        left = t < 0.0;
+        if (fabs(t) <= M) {  // tie guard
+          const StepOut o = slow_step<D, FAM>(pts, q, h, f, l, tlo, thi, has_boxes, scale, family,
+                                              sigma, em, qlink, key_prefix, seed, nlink, false);
+          left = o.left;
+          em = o.em;
+          atomicAdd(&s_stats[3][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
+          if (o.dg) atomicAdd(&s_stats[2][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
+        } else if (rowstep) {  // absolute fp64 sums: exponent of the chosen double
+          em = float(int((__double_as_longlong(left ? a : b) >> 52) & 0x7ff) - 1023);
+        } else {
+          const float c = left ? float(a) : float(b);
+          em = float(int((__float_as_uint(c) >> 23) & 0xffu) - 127) - offn;
+        }
+      } else {
+        const StepOut o = slow_step<D, FAM>(pts, q, h, f, l, tlo, thi, has_boxes, scale, family,
+                                            sigma, em, qlink, key_prefix, seed, nlink, !rowstep);
+        left = o.left;
+        em = o.em;
+        if (o.tie) atomicAdd(&s_stats[3][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
+        if (o.dg) atomicAdd(&s_stats[2][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
+      }
+      path |= (left ? 1u : 0u) << steps;
+      ++steps;
+      h = left ? 2 * h + 1 : 2 * h + 2;
+      nf = left ? f : mid;
+      nl = left ? mid : l;
+    }
+    // sampler.cpp:196-198: leaf (query, source, 1)
+    const uint32_t row_q = qrow[q];
+    const uint32_t slot = atomicAdd(row_cnt + row_q, 1u);
+    const uint64_t o = row_off[row_q] + slot;
+    leaf_src[o] = nf;
+    leaf_cnt[o] = 1u;
+  }
+  // per-level tallies of the warp's walks: level lev0 + k holds the walks
+  // with at least k steps (the last one is the leaf entry), evaluating their
+  // k-th node's size when they step on
+  {
+    const unsigned grp = __match_any_sync(0xffffffffu, lev0);
+    const uint32_t maxsteps = __reduce_max_sync(0xffffffffu, steps);
+    const bool lead = (threadIdx.x & 31) == uint32_t(__ffs(grp) - 1);
+    uint32_t nk = n0;
+    for (uint32_t k = 0; k <= maxsteps; ++k) {
+      const uint32_t n_ent = __popc(__ballot_sync(0xffffffffu, mine && k <= steps) & grp);
+      const uint32_t n_ev = __reduce_add_sync(grp, k < steps ? nk : 0u);
+      const uint32_t at = lev0 + k;
+      if (lead && n_ent && at < kMaxLevels) {
+        atomicAdd(&s_stats[0][at], n_ent);
+        atomicAdd(&s_stats[1][at], n_ev);
+      }
+      if (k == 0) {
+        const uint32_t n_sv = __reduce_add_sync(grp, sv0);
+        if (lead && n_sv && at < kMaxLevels) atomicAdd(&s_stats[4][at], n_sv);
+      }
+      nk = ((path >> k) & 1u) ? nk / 2 : nk - nk / 2;
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) {
+    const unsigned long long v = (&s_stats[0][0])[k];  // widened
+    if (v) atomicAdd(stats + k, v);
+  }
+}
+
 template <class F>
 void walk_by_dim(uint32_t d, F&& f) {
   switch (d) {
@@ -234,9 +460,21 @@ void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& a) {
   if (a.W == 0) return;
   const TreeTable& t = ds.tree;
   cudaStream_t s = ds.stream;
+  // the fast kernel relies on the tie guard (reference RNG, verify on);
+  // FSGG_WALK_FAST=0 keeps the per-child-offset kernel
+  const char* e = std::getenv("FSGG_WALK_FAST");  // read per call: tests toggle it
+  const bool fast = a.verify && a.rng_mode == 0 && !(e && e[0] == '0');
   auto launch = [&](auto dim, auto fam) {
     constexpr int D = decltype(dim)::value;
     constexpr int FAM = decltype(fam)::value;
+    if (fast) {
+      walk_fast_kernel<D, FAM><<<ceil_div_u32(a.W, kWalkThreads), kWalkThreads, 0, s>>>(
+          ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
+          t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
+          ks.family, ks.sigma, a.key_prefix, a.seed, a.qrow, a.row_off, a.row_cnt, a.leaf_src,
+          a.leaf_cnt, a.stats, a.nlink, a.wrow, a.wrm, a.rows, a.rows_level);
+      return;
+    }
     walk_kernel<D, FAM><<<ceil_div_u32(a.W, kWalkThreads), kWalkThreads, 0, s>>>(
         ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
