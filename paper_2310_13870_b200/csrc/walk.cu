@@ -14,6 +14,7 @@
 // in the lists; scatter_kernel routes children with exactly one ticket here.
 // Per-level counters (entries, tickets, evaluations, degenerate draws) are
 // aggregated per warp by level, so the reference's diagnostics are intact.
+#include <algorithm>
 #include <cstdlib>
 
 #include "engine.cuh"
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
                 uint32_t* __restrict__ leaf_src, uint32_t* __restrict__ leaf_cnt,
                 unsigned long long* __restrict__ stats, const uint64_t* __restrict__ nlink,
                 const uint32_t* __restrict__ wrow, const float* __restrict__ wrm,
-                const double* __restrict__ rows, uint32_t rows_level) {
+                const double* __restrict__ rows, uint32_t rows_level,
+                const uint32_t* __restrict__ widx, const uint32_t* __restrict__ wcount) {
   // entries, evals, degen, ties, evals read from rows
   // 32-bit per-CTA tallies (native shared-memory atomics; 64-bit ones are
   // CAS loops): a CTA's counts per level stay far below 2^32 (at most 128
@@ -101,8 +103,13 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
   for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) (&s_stats[0][0])[k] = 0;
   __syncthreads();
 
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool live = i < W;
+  // widx/wcount: the walks the fast kernel deferred (indices into the walk
+  // list, count on the device); otherwise all W walks, one per thread
+  const uint32_t count = wcount ? *wcount : W;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < count; base += gridDim.x * blockDim.x) {
+  const uint32_t slot_t = base + threadIdx.x;
+  bool live = slot_t < count;
+  const uint32_t i = live ? (widx ? widx[slot_t] : slot_t) : 0u;
   uint32_t q = 0, lev = 0;
   uint64_t h = 0;
   float em = 0.f;
@@ -206,6 +213,7 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
       }
     }
   }
+  }
   __syncthreads();
   for (int k = threadIdx.x; k < 5 * kMaxLevels; k += blockDim.x) {
     const unsigned long long v = (&s_stats[0][0])[k];  // widened
@@ -228,61 +236,24 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
 //     size and the left/right bits of its path; node sizes along the path
 //     follow from those, and the warp adds them up per level after the loop
 //     (the per-step version spent 15% of the kernel's instructions on it).
-// Steps the fast path cannot take — both fp32 sums zero, or an offset so
-// large that the 1e-300 floor could matter — run the per-child-offset sums
-// and decide() exactly as walk_kernel does (slow_step).
-struct StepOut {
-  bool left;
-  uint32_t dg, tie;
-  float em;
-};
-
+// A walk whose step the fast path cannot take — a draw inside the margin,
+// both fp32 sums zero, or an offset so large that the 1e-300 floor could
+// matter — stops there: its node and mass go back into its walk-list slot and
+// its index onto a deferred list, and walk_kernel (per-child offsets,
+// decide(), fp64 re-decision) finishes the deferred walks afterwards (~1 in
+// 10^3 at C3). The fast kernel then holds no fp64 sums and no calls.
+#ifndef FSGG_WALKF_CTAS
+#define FSGG_WALKF_CTAS 12
+#endif
 template <int D, int FAM>
-__device__ __noinline__ StepOut slow_step(const float* __restrict__ pts, uint32_t q, uint64_t h,
-                                          uint32_t f, uint32_t l,
-                                          const float* __restrict__ tlo,
-                                          const float* __restrict__ thi, int has_boxes,
-                                          float scale, int family, double sigma, float em,
-                                          uint64_t qlink, uint64_t key_prefix, uint64_t seed,
-                                          const uint64_t* __restrict__ nlink, bool fp32_first) {
-  StepOut o{false, 0u, 0u, 0.f};
-  float qc[D];
-#pragma unroll
-  for (int k = 0; k < D; ++k) qc[k] = __ldg(pts + size_t(q) * D + k);
-  double a = 0.0, b = 0.0;
-  Decision dc{false, true, false};
-  if (fp32_first) {
-    double s[2];
-    direct_child_sums<D, FAM>(pts, qc, h, f, l, tlo, thi, has_boxes, scale, s);
-    a = fmax(s[0], kSumFloor);
-    b = fmax(s[1], kSumFloor);
-    dc = decide(a, b, em, f, l, q, qlink, key_prefix, 0, seed, true, nlink, h, 0.0);
-  }
-  if (dc.near) {  // tie guard: exact fp64 sums (kernel_f64, index order)
-    const uint32_t mid = f + (l - f) / 2;
-    const float* xq = pts + size_t(q) * D;
-    double e0 = 0.0, e1 = 0.0;
-    for (uint32_t j = f; j < mid; ++j) e0 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
-    for (uint32_t j = mid; j < l; ++j) e1 += kernel_f64(family, sigma, xq, pts + size_t(j) * D, D);
-    a = fmax(e0, kSumFloor);
-    b = fmax(e1, kSumFloor);
-    dc = decide(a, b, em, f, l, q, qlink, key_prefix, 0, seed, false, nlink, h, 0.0);
-    o.tie = 1u;
-  }
-  o.left = dc.left;
-  o.dg = dc.degenerate ? 1u : 0u;
-  o.em = float(int((__double_as_longlong(dc.left ? a : b) >> 52) & 0x7ff) - 1023);
-  return o;
-}
-
-template <int D, int FAM>
-__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
+__global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALKF_CTAS : 0)
     walk_fast_kernel(const float* __restrict__ pts, uint32_t W, const uint32_t* __restrict__ wq,
-                     const uint32_t* __restrict__ wh, const float* __restrict__ welm,
+                     uint32_t* __restrict__ wh, float* __restrict__ welm,
+                     uint32_t* __restrict__ widx, uint32_t* __restrict__ wcount,
                      const uint32_t* __restrict__ tfirst, const uint32_t* __restrict__ tlast,
                      const float* __restrict__ tlo, const float* __restrict__ thi,
-                     int has_boxes, float scale, int family, double sigma,
-                     uint64_t key_prefix, uint64_t seed, const uint32_t* __restrict__ qrow,
+                     int has_boxes, float scale, uint64_t key_prefix,
+                     const uint32_t* __restrict__ qrow,
                      const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_cnt,
                      uint32_t* __restrict__ leaf_src, uint32_t* __restrict__ leaf_cnt,
                      unsigned long long* __restrict__ stats,
@@ -296,6 +267,7 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool mine = i < W;
   uint32_t q = 0, lev0 = 0xffffffffu, n0 = 0, path = 0, steps = 0, sv0 = 0;
+  bool deferred = false;
   if (mine) {
     q = wq[i];
     const uint64_t qlink = query_link(q);
@@ -363,7 +335,8 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
         b = double(a1);
         fast = (a0 > 0.f || a1 > 0.f) && offn < 800.f;
       }
-      bool left;
+      bool left = false;
+      bool defer = !fast;
       if (fast) {
         const uint64_t key = nlink ? splitmix64(__ldg(nlink + h) ^ qlink)
                                    : route_key_q(key_prefix, (uint64_t(f) << 32) | l, qlink);
@@ -373,26 +346,21 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
         const float rel = float(kTieMargin) * (1.f + fmaxf(0.f, -em) * (1.f / 32.f));
         const double M = fma(double(rel), fmin(a, b), (pruned + 0x1p-51) * ssum);
         left = t < 0.0;
-        if (fabs(t) <= M) {  // tie guard
-          const StepOut o = slow_step<D, FAM>(pts, q, h, f, l, tlo, thi, has_boxes, scale, family,
-                                              sigma, em, qlink, key_prefix, seed, nlink, false);
-          left = o.left;
-          em = o.em;
-          atomicAdd(&s_stats[3][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
-          if (o.dg) atomicAdd(&s_stats[2][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
-        } else if (rowstep) {  // absolute fp64 sums: exponent of the chosen double
-          em = float(int((__double_as_longlong(left ? a : b) >> 52) & 0x7ff) - 1023);
-        } else {
-          const float c = left ? float(a) : float(b);
-          em = float(int((__float_as_uint(c) >> 23) & 0xffu) - 127) - offn;
-        }
+        defer = fabs(t) <= M;  // tie guard
+      }
+      if (defer) {  // walk_kernel takes this walk on from here
+        wh[i] = uint32_t(h);
+        welm[i] = em;
+        widx[atomicAdd(wcount, 1u)] = i;
+        deferred = true;
+        if (rowstep) sv0 = 0;  // the row step is walk_kernel's to count
+        break;
+      }
+      if (rowstep) {  // absolute fp64 sums: exponent of the chosen double
+        em = float(int((__double_as_longlong(left ? a : b) >> 52) & 0x7ff) - 1023);
       } else {
-        const StepOut o = slow_step<D, FAM>(pts, q, h, f, l, tlo, thi, has_boxes, scale, family,
-                                            sigma, em, qlink, key_prefix, seed, nlink, !rowstep);
-        left = o.left;
-        em = o.em;
-        if (o.tie) atomicAdd(&s_stats[3][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
-        if (o.dg) atomicAdd(&s_stats[2][min(lev0 + steps, uint32_t(kMaxLevels - 1))], 1u);
+        const float c = left ? float(a) : float(b);
+        em = float(int((__float_as_uint(c) >> 23) & 0xffu) - 127) - offn;
       }
       path |= (left ? 1u : 0u) << steps;
       ++steps;
@@ -400,12 +368,13 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
       nf = left ? f : mid;
       nl = left ? mid : l;
     }
-    // sampler.cpp:196-198: leaf (query, source, 1)
-    const uint32_t row_q = qrow[q];
-    const uint32_t slot = atomicAdd(row_cnt + row_q, 1u);
-    const uint64_t o = row_off[row_q] + slot;
-    leaf_src[o] = nf;
-    leaf_cnt[o] = 1u;
+    if (!deferred) {  // sampler.cpp:196-198: leaf (query, source, 1)
+      const uint32_t row_q = qrow[q];
+      const uint32_t slot = atomicAdd(row_cnt + row_q, 1u);
+      const uint64_t o = row_off[row_q] + slot;
+      leaf_src[o] = nf;
+      leaf_cnt[o] = 1u;
+    }
   }
   // per-level tallies of the warp's walks: level lev0 + k holds the walks
   // with at least k steps (the last one is the leaf entry), evaluating their
@@ -416,7 +385,9 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALK_CTAS : 0)
     const bool lead = (threadIdx.x & 31) == uint32_t(__ffs(grp) - 1);
     uint32_t nk = n0;
     for (uint32_t k = 0; k <= maxsteps; ++k) {
-      const uint32_t n_ent = __popc(__ballot_sync(0xffffffffu, mine && k <= steps) & grp);
+      // (a deferred walk's last node is walk_kernel's entry)
+      const uint32_t n_ent =
+          __popc(__ballot_sync(0xffffffffu, mine && k + (deferred ? 1u : 0u) <= steps) & grp);
       const uint32_t n_ev = __reduce_add_sync(grp, k < steps ? nk : 0u);
       const uint32_t at = lev0 + k;
       if (lead && n_ent && at < kMaxLevels) {
@@ -464,23 +435,32 @@ void walk_finish(Dataset& ds, const KernelSpec& ks, const WalkArgs& a) {
   // FSGG_WALK_FAST=0 keeps the per-child-offset kernel
   const char* e = std::getenv("FSGG_WALK_FAST");  // read per call: tests toggle it
   const bool fast = a.verify && a.rng_mode == 0 && !(e && e[0] == '0');
+  uint32_t *widx = nullptr, *wcount = nullptr;
+  if (fast) {
+    widx = ds.buf("walk.deferred", size_t(a.W) * 4).as<uint32_t>();
+    wcount = ds.buf("walk.ndeferred", 4).as<uint32_t>();
+    FSGG_CUDA(cudaMemsetAsync(wcount, 0, 4, s));
+    ds.launches++;
+  }
   auto launch = [&](auto dim, auto fam) {
     constexpr int D = decltype(dim)::value;
     constexpr int FAM = decltype(fam)::value;
+    uint32_t grid = ceil_div_u32(a.W, kWalkThreads);
     if (fast) {
-      walk_fast_kernel<D, FAM><<<ceil_div_u32(a.W, kWalkThreads), kWalkThreads, 0, s>>>(
-          ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
+      walk_fast_kernel<D, FAM><<<grid, kWalkThreads, 0, s>>>(
+          ds.pts.as<float>(), a.W, a.wq, const_cast<uint32_t*>(a.wh),
+          const_cast<float*>(a.welm), widx, wcount, t.first.as<uint32_t>(),
           t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
-          ks.family, ks.sigma, a.key_prefix, a.seed, a.qrow, a.row_off, a.row_cnt, a.leaf_src,
-          a.leaf_cnt, a.stats, a.nlink, a.wrow, a.wrm, a.rows, a.rows_level);
-      return;
+          a.key_prefix, a.qrow, a.row_off, a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats, a.nlink,
+          a.wrow, a.wrm, a.rows, a.rows_level);
+      grid = std::min<uint32_t>(grid, uint32_t(ds.num_sms) * 4);  // the deferred few
     }
-    walk_kernel<D, FAM><<<ceil_div_u32(a.W, kWalkThreads), kWalkThreads, 0, s>>>(
+    walk_kernel<D, FAM><<<grid, kWalkThreads, 0, s>>>(
         ds.pts.as<float>(), a.W, a.wq, a.wh, a.welm, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(), t.has_boxes, ks.scale,
         ks.family, ks.sigma, a.key_prefix, a.rng_mode, a.seed, a.verify, a.qrow, a.row_off,
         a.row_cnt, a.leaf_src, a.leaf_cnt, a.stats, a.nlink, a.wrow, a.wrm, a.rows,
-        a.rows_level);
+        a.rows_level, widx, wcount);
   };
   switch (ks.family) {
     case 0: walk_by_dim(ds.d, [&](auto dim) { launch(dim, std::integral_constant<int, 0>{}); }); break;

@@ -4,7 +4,4 @@ cap() { # name regex config
   ncu -i /tmp/ncu/$1.ncu-rep --page raw --csv > gpurun_out/$1_raw.csv 2>/dev/null
   ncu -i /tmp/ncu/$1.ncu-rep --page source --csv > gpurun_out/$1_source.csv 2>/dev/null
 }
-cap c3_walk walk_kernel C3
-cap c3_wtile sym_wtile_kernel C3
-cap c4_wtile sym_wtile_kernel C4
-ls -la gpurun_out/
+cap c3_walkf walk_fast_kernel C3
