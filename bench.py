@@ -490,7 +490,9 @@ def main():
     nominal = NOMINAL_EX2_PER_CLK_PER_SM * props.multi_processor_count * 1965e6
     achieved = tiled_perf / max(tiled_s, 1e-12)  # evaluations the kernel executed
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "kde_sym_ncu.json" if root_s > 0 else "kde_tiled_ncu.json")
+    # the committed ncu capture of this config's dominant kernel (scripts/ncu_summary.py)
+    prof = os.path.join(ROOT, "profiles", f"r2_{args.config.lower()}_wtile_ncu.json"
+                        if root_s > 0 else "kde_tiled_ncu.json")
     if os.path.exists(prof):
         try:
             cap = json.load(open(prof))
@@ -561,7 +563,10 @@ def main():
         # serving both q's and x's rows; timed around the tile kernel alone
         root_rate = root_perf / root_s
         roofline = {
-            "bound": "mufu", "kernel": "sym_tile_kernel<2,gaussian> (root level, each pair once)",
+            "bound": "mufu",
+            "kernel": (f"sym_wtile_kernel<{w.d},gaussian> (root level, each pair once; one warp "
+                       "per block-pair tile, persistent)" if w.d <= 6 else
+                       f"sym_tile_kernel<{w.d},gaussian> (root level, each pair once)"),
             "achieved": root_rate / 1e9, "peak": ex2.value / 1e9, "unit": "Gex2/s",
             "frac": root_rate / ex2.value if ex2.value else None,
             "peak_source": "measured in this run: MUFU.EX2 microbenchmark (fsgg_probe_ex2_throughput)",

@@ -92,43 +92,30 @@ __device__ __forceinline__ uint32_t find_slot(const uint32_t* blk_off,
   return lo;
 }
 
-// Sum of 2^(off - scale*dist) over sources [cf, cl) for two packed entries;
-// sources staged negated and duplicated in shared memory.
+// Sum of 2^(off - scale*dist) over the lenp staged sources (negated,
+// duplicated, padded to a multiple of 4) for two packed entries: fp32 partial
+// sums over runs of kFlush sources, flushed into fp64 (keeps the accumulation
+// error ~1e-7 relative at no measurable cost).
 template <int D, int FAM>
-__device__ __forceinline__ void lowd_range_sum(
-    const float* __restrict__ pts, float2* sm, const float2 (&q2)[D],
-    float2 off2, float scale, uint32_t cf, uint32_t cl, double& accA,
-    double& accB, bool warp_skip = false) {
-  constexpr int T = LowDTile<D>::T;
+__device__ __forceinline__ void lowd_staged_sum(const float2* sm, uint32_t lenp,
+                                                const float2 (&q2)[D], float2 off2,
+                                                float scale, double& accA, double& accB) {
   const float2 ms = make_float2(-scale, -scale);
-  for (uint32_t t0 = cf; t0 < cl; t0 += T) {
-    const uint32_t len = min(uint32_t(T), cl - t0);
-    const uint32_t lenp = (len + 3u) & ~3u;
-    __syncthreads();
-    const float* src = pts + size_t(t0) * D;
-    for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
-      float v = idx < len * D ? -__ldg(src + idx) : -kPad;
-      sm[idx] = make_float2(v, v);
-    }
-    __syncthreads();
-    if (warp_skip) continue;  // this warp's entries all prune the range
-    // fp32 partial sums over runs of kFlush sources, flushed into fp64:
-    // keeps the accumulation error ~1e-7 relative at no measurable cost.
-    for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
-      const uint32_t j1 = min(lenp, j0 + kFlush);
-      float2 acc = make_float2(0.f, 0.f);
-      auto arg_of = [&](uint32_t j) {
-        const float2* x = sm + j * D;
-        float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
+  for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
+    const uint32_t j1 = min(lenp, j0 + kFlush);
+    float2 acc = make_float2(0.f, 0.f);
+    auto arg_of = [&](uint32_t j) {
+      const float2* x = sm + j * D;
+      float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
 #pragma unroll
-        for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
-        t = fam_finish<FAM>(t);
-        return __ffma2_rn(t, ms, off2);
-      };
-      uint32_t j = j0;
-      // one source in kPolyEvery takes the FP32-pipe exp2, the rest MUFU:
-      // balances the two pipes (the loop is MUFU-bound otherwise)
-      if (kPolyEvery > 0)
+      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
+      t = fam_finish<FAM>(t);
+      return __ffma2_rn(t, ms, off2);
+    };
+    uint32_t j = j0;
+    // one source in kPolyEvery takes the FP32-pipe exp2, the rest MUFU:
+    // balances the two pipes (the loop is MUFU-bound otherwise)
+    if (kPolyEvery > 0)
       for (; j + kPolyEvery <= j1; j += kPolyEvery) {
 #pragma unroll
         for (uint32_t u = 0; u < kPolyEvery; ++u) {
@@ -140,13 +127,35 @@ __device__ __forceinline__ void lowd_range_sum(
         }
       }
 #pragma unroll 4
-      for (; j < j1; ++j) {
-        const float2 arg = arg_of(j);
-        acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
-      }
-      accA += acc.x;
-      accB += acc.y;
+    for (; j < j1; ++j) {
+      const float2 arg = arg_of(j);
+      acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
     }
+    accA += acc.x;
+    accB += acc.y;
+  }
+}
+
+// Sum of 2^(off - scale*dist) over sources [cf, cl) for two packed entries;
+// sources staged negated and duplicated in shared memory.
+template <int D, int FAM>
+__device__ __forceinline__ void lowd_range_sum(
+    const float* __restrict__ pts, float2* sm, const float2 (&q2)[D],
+    float2 off2, float scale, uint32_t cf, uint32_t cl, double& accA,
+    double& accB, bool warp_skip = false) {
+  constexpr int T = LowDTile<D>::T;
+  for (uint32_t t0 = cf; t0 < cl; t0 += T) {
+    const uint32_t len = min(uint32_t(T), cl - t0);
+    const uint32_t lenp = (len + 3u) & ~3u;
+    __syncthreads();
+    const float* src = pts + size_t(t0) * D;
+    for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
+      float v = idx < len * D ? -__ldg(src + idx) : -kPad;
+      sm[idx] = make_float2(v, v);
+    }
+    __syncthreads();
+    if (warp_skip) continue;  // this warp's entries all prune the range
+    lowd_staged_sum<D, FAM>(sm, lenp, q2, off2, scale, accA, accB);
   }
 }
 
@@ -259,6 +268,101 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t stride = 2u * K, col = side * K + kk;
     if (va) partials[size_t(ia) * stride + col] = accA;
     if (vb) partials[size_t(ib) * stride + col] = accB;
+  }
+  if (performed) {
+    if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_done, done);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_done) atomicAdd(performed, s_done);
+  }
+}
+
+// ---- low-d node kernel: two-deep rows of small nodes ------------------------
+// The per-sub-chunk case of the tiled kernel with one work item per (node
+// slot, block of <= 256 entries) instead of one per child side (C3 level 12:
+// 245-point nodes, four ~61-point sub-chunks): the node's points are staged
+// once, each sub-chunk at its own 4-aligned offset, and the four sub-chunk
+// sums follow without a barrier in between — half the work items (slot
+// search, query gathers) and one barrier instead of seven. Sub-chunk sums,
+// offsets, pruning rule and partial layout are the tiled kernel's, bit for bit.
+constexpr uint32_t kNodeMax = 4 * kSubMinSmall;  // node points (2 children x 2 x < 64)
+
+template <int D, int FAM>
+__global__ void __launch_bounds__(kThreads)
+    kde_lowd_node_kernel(const float* __restrict__ pts, const uint32_t* __restrict__ eq,
+                         const float* __restrict__ elm, const uint32_t* __restrict__ goff,
+                         const uint32_t* __restrict__ blk_off, uint32_t num_slots,
+                         uint32_t level, const uint32_t* __restrict__ tfirst,
+                         const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
+                         const float* __restrict__ thi, int has_boxes, float scale,
+                         float prune_bits, double* __restrict__ partials,
+                         unsigned long long* __restrict__ performed) {
+  const bool prune = prune_bits > 0.f;
+  __shared__ __align__(16) float2 sm[(kNodeMax + 16) * D];
+  __shared__ unsigned long long s_done;
+  const uint32_t blk = blockIdx.x;
+  const uint32_t g = find_slot(blk_off, num_slots, blk);
+  const uint32_t e0 = goff[g] + (blk - blk_off[g]) * kBE;
+  const uint32_t e1 = min(e0 + kBE, goff[g + 1]);
+  // sub-chunks: the node's descendants two levels down, in order
+  const uint64_t hbase = ((1ull << (level + 2)) - 1) + (uint64_t(g) << 2);
+  uint32_t cf[4], cl[4], so[4];
+  uint32_t at = 0;
+#pragma unroll
+  for (int sc = 0; sc < 4; ++sc) {
+    cf[sc] = tfirst[hbase + sc];
+    cl[sc] = tlast[hbase + sc];
+    so[sc] = at;
+    at += (cl[sc] - cf[sc] + 3u) & ~3u;
+  }
+  if (threadIdx.x == 0) s_done = 0;
+#pragma unroll
+  for (int sc = 0; sc < 4; ++sc) {
+    const uint32_t len = cl[sc] - cf[sc], lenp = (len + 3u) & ~3u;
+    const float* src = pts + size_t(cf[sc]) * D;
+    for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
+      const float v = idx < len * D ? -__ldg(src + idx) : -kPad;
+      sm[so[sc] * D + idx] = make_float2(v, v);
+    }
+  }
+  const uint32_t ia = e0 + threadIdx.x, ib = ia + kThreads;
+  const bool va = ia < e1, vb = ib < e1;
+  const uint32_t qa = eq[va ? ia : e0], qb = eq[vb ? ib : e0];
+  float qa_c[D], qb_c[D];
+  float2 q2[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    qa_c[k] = __ldg(pts + size_t(qa) * D + k);
+    qb_c[k] = __ldg(pts + size_t(qb) * D + k);
+    q2[k] = make_float2(qa_c[k], qb_c[k]);
+  }
+  const float lbA = prune ? (elm ? elm[va ? ia : e0] : 0.f) - 1.f : 0.f;
+  const float lbB = prune ? (elm ? elm[vb ? ib : e0] : 0.f) - 1.f : 0.f;
+  const uint32_t nvalid_warp =
+      __popc(__ballot_sync(0xffffffffu, va)) + __popc(__ballot_sync(0xffffffffu, vb));
+  __syncthreads();
+  unsigned long long done = 0;
+#pragma unroll
+  for (int sc = 0; sc < 4; ++sc) {
+    const uint64_t h = hbase + sc;
+    float offA = 0.f, offB = 0.f;
+    if (has_boxes) {
+      offA = scale * box_dist<FAM>(qa_c, tlo + h * D, thi + h * D, D);
+      offB = scale * box_dist<FAM>(qb_c, tlo + h * D, thi + h * D, D);
+    }
+    bool skipA = false, skipB = false;
+    if (prune) {
+      const float lim = __log2f(float(cl[sc] - cf[sc])) + prune_bits;
+      skipA = !va || offA > lim - lbA;
+      skipB = !vb || offB > lim - lbB;
+    }
+    double sA = 0.0, sB = 0.0;
+    if (!__all_sync(0xffffffffu, skipA && skipB)) {
+      lowd_staged_sum<D, FAM>(sm + so[sc] * D, (cl[sc] - cf[sc] + 3u) & ~3u, q2,
+                              make_float2(offA, offB), scale, sA, sB);
+      done += uint64_t(cl[sc] - cf[sc]) * nvalid_warp;
+    }
+    if (va) partials[size_t(ia) * 4 + sc] = skipA ? 0.0 : rescale(sA, offA);
+    if (vb) partials[size_t(ib) * 4 + sc] = skipB ? 0.0 : rescale(sB, offB);
   }
   if (performed) {
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_done, done);
@@ -702,7 +806,15 @@ struct LowD {
                     const LevelView& lv, const uint32_t* blk_off,
                     uint32_t cdepth, uint32_t sdepth, const TreeTable& t,
                     float scale, double* partials,
-                    unsigned long long* performed, int per_sub) {
+                    unsigned long long* performed, int per_sub, bool whole_node) {
+    if (whole_node) {  // two-deep rows of small nodes: one item per entry block
+      kde_lowd_node_kernel<D, FAM><<<grid.x / 2, kThreads, 0, s>>>(
+          pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level,
+          t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
+          t.has_boxes, scale, (lv.prune && t.has_boxes) ? lv.prune_bits : 0.f, partials,
+          performed);
+      return;
+    }
     kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
         pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level, cdepth,
         sdepth, t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(),
@@ -959,7 +1071,10 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     // every pair evaluated once (kde_sym.cu)
   } else if (lowd) {
     with_lowd(ks.family, d, [&](auto op) {
-      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub);
+      // (per_sub implies c == 0, sd == 1 and nodes below 4 * kSubMinSmall points)
+      const bool whole_node = per_sub && node_min + 1 < kNodeMax &&
+                              env_u32("FSGG_NODE_KERNEL", 1) != 0;
+      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub, whole_node);
     });
   } else if (tc) {
     // full build: the symmetric root (each pair once, both row sums)

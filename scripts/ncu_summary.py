@@ -1,6 +1,6 @@
 """Summarise one kernel of an ncu --set full report into profiles/*.json.
 
-    python scripts/ncu_summary.py REPORT.ncu-rep OUT.json "<kernel title>" "<config>" "<capture cmd>"
+    python scripts/ncu_summary.py REPORT.ncu-rep|REPORT_raw.csv OUT.json "<kernel title>" "<config>" "<capture cmd>"
 """
 import csv
 import io
@@ -23,8 +23,13 @@ KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 def main():
     rep, out, title, config, cmd = sys.argv[1:6]
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    # REPORT may also be the csv already exported on the GPU box
+    # (ncu -i X.ncu-rep --page raw --csv > X_raw.csv: reports exceed gpurun's copy-back cap)
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     launches = []
