@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(kThreads)
                          const uint32_t* __restrict__ tlast, const float* __restrict__ tlo,
                          const float* __restrict__ thi, int has_boxes, float scale,
                          float prune_bits, double* __restrict__ partials,
-                         unsigned long long* __restrict__ performed) {
+                         unsigned long long* __restrict__ performed,
+                         double* __restrict__ g1, double* __restrict__ g2) {
   const bool prune = prune_bits > 0.f;
   __shared__ __align__(16) float2 sm[(kNodeMax + 16) * D];
   __shared__ unsigned long long s_done;
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(kThreads)
       __popc(__ballot_sync(0xffffffffu, va)) + __popc(__ballot_sync(0xffffffffu, vb));
   __syncthreads();
   unsigned long long done = 0;
+  double rA[4], rB[4];
 #pragma unroll
   for (int sc = 0; sc < 4; ++sc) {
     const uint64_t h = hbase + sc;
@@ -361,8 +363,24 @@ __global__ void __launch_bounds__(kThreads)
                               make_float2(offA, offB), scale, sA, sB);
       done += uint64_t(cl[sc] - cf[sc]) * nvalid_warp;
     }
-    if (va) partials[size_t(ia) * 4 + sc] = skipA ? 0.0 : rescale(sA, offA);
-    if (vb) partials[size_t(ib) * 4 + sc] = skipB ? 0.0 : rescale(sB, offB);
+    rA[sc] = skipA ? 0.0 : rescale(sA, offA);
+    rB[sc] = skipB ? 0.0 : rescale(sB, offB);
+  }
+  // the row, and the entry's child sums (finalize_kernel's: buckets added in
+  // order, floored)
+  if (va) {
+    double2* p = reinterpret_cast<double2*>(partials + size_t(ia) * 4);
+    p[0] = make_double2(rA[0], rA[1]);
+    p[1] = make_double2(rA[2], rA[3]);
+    g1[ia] = fmax(rA[0] + rA[1], kSumFloor);
+    g2[ia] = fmax(rA[2] + rA[3], kSumFloor);
+  }
+  if (vb) {
+    double2* p = reinterpret_cast<double2*>(partials + size_t(ib) * 4);
+    p[0] = make_double2(rB[0], rB[1]);
+    p[1] = make_double2(rB[2], rB[3]);
+    g1[ib] = fmax(rB[0] + rB[1], kSumFloor);
+    g2[ib] = fmax(rB[2] + rB[3], kSumFloor);
   }
   if (performed) {
     if ((threadIdx.x & 31) == 0 && done) atomicAdd(&s_done, done);
@@ -806,13 +824,14 @@ struct LowD {
                     const LevelView& lv, const uint32_t* blk_off,
                     uint32_t cdepth, uint32_t sdepth, const TreeTable& t,
                     float scale, double* partials,
-                    unsigned long long* performed, int per_sub, bool whole_node) {
+                    unsigned long long* performed, int per_sub, bool whole_node,
+                    double* g1, double* g2) {
     if (whole_node) {  // two-deep rows of small nodes: one item per entry block
       kde_lowd_node_kernel<D, FAM><<<grid.x / 2, kThreads, 0, s>>>(
           pts, lv.eq, lv.elm, lv.goff, blk_off, lv.num_slots, lv.level,
           t.first.as<uint32_t>(), t.last.as<uint32_t>(), t.lo.as<float>(), t.hi.as<float>(),
           t.has_boxes, scale, (lv.prune && t.has_boxes) ? lv.prune_bits : 0.f, partials,
-          performed);
+          performed, g1, g2);
       return;
     }
     kde_lowd_tiled_kernel<D, FAM><<<grid, kThreads, 0, s>>>(
@@ -1060,6 +1079,10 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     FSGG_CUDA(cudaEventCreate(&ws.ev1));
   }
   unsigned long long* d_perf = d_evals + 1;
+  // two-deep rows of small nodes: the whole-node kernel, which also writes the
+  // entries' child sums (per_sub implies c == 0, sd == 1; never the root)
+  const bool whole_node = lowd && per_sub && Lb == 0 && !groot && node_min + 1 < kNodeMax &&
+                          env_u32("FSGG_NODE_KERNEL", 1) != 0;
   uint64_t tc_sym_perf = 0;  // pair evaluations of the symmetric tensor-core root
   FSGG_CUDA(cudaMemsetAsync(d_perf, 0, 8, s));
   FSGG_CUDA(cudaEventRecord(ws.ev0, s));
@@ -1072,9 +1095,8 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
   } else if (lowd) {
     with_lowd(ks.family, d, [&](auto op) {
       // (per_sub implies c == 0, sd == 1 and nodes below 4 * kSubMinSmall points)
-      const bool whole_node = per_sub && node_min + 1 < kNodeMax &&
-                              env_u32("FSGG_NODE_KERNEL", 1) != 0;
-      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub, whole_node);
+      op.tiled(grid, s, pts, lv, nb, c, sd, t, ks.scale, partials, d_perf, per_sub, whole_node,
+               g1, g2);
     });
   } else if (tc) {
     // full build: the symmetric root (each pair once, both row sums)
@@ -1102,7 +1124,7 @@ void kde_level(Dataset& ds, const KernelSpec& ks, const LevelView& lv,
     pyramid_kernel<<<ceil_div_u32(E, warps), warps * 32, per_warp * warps, s>>>(
         partials, rl, lv.eg, E, lv.level, t.first.as<uint32_t>(), t.last.as<uint32_t>(),
         ws.pyr.as<double>(), g1, g2, groot);
-  } else {
+  } else if (!whole_node) {
     finalize_kernel<<<ceil_div_u32(E, 256), 256, 0, s>>>(
         partials, 1u << (rl - 1), lv.eg, E, lv.level, t.first.as<uint32_t>(),
         t.last.as<uint32_t>(), g1, g2, groot);

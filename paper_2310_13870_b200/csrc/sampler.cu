@@ -1138,7 +1138,13 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
 // earlier levels invisible, so the state array is cleared once per descent.
 // The thread holding index E also writes the next level's entry count.
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
+#ifndef FSGG_SCAN_ITEMS
+#define FSGG_SCAN_ITEMS 16
+#endif
+#ifndef FSGG_SCAN_CTAS
+#define FSGG_SCAN_CTAS 4
+#endif
+constexpr int kScanItems = FSGG_SCAN_ITEMS;
 constexpr uint32_t kScanTile = kScanThreads * kScanItems;
 
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
@@ -1839,7 +1845,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
 
     if (trace) FSGG_CUDA(cudaEventRecord(tev[2], s));
     if (level + 1 > kMaxLevelsLog) throw NumericError("descent exceeded the level log");
-    flags_scan_kernel<<<grid_of(uint64_t(En) + 1, kScanTile, 4), kScanThreads, 0, s>>>(
+    flags_scan_kernel<<<grid_of(uint64_t(En) + 1, kScanTile, FSGG_SCAN_CTAS), kScanThreads, 0, s>>>(
         dE, flags.as<unsigned long long>(), P.as<unsigned long long>(), tstate.as<uint32_t>(),
         tagg.as<unsigned long long>(), tinc.as<unsigned long long>(), tctr + level, level + 1,
         elog.as<uint32_t>() + level + 1);
