@@ -575,6 +575,54 @@ def test_symmetric_root_matches_one_sided():
     assert r1.kernel_evals_performed < r0.kernel_evals_performed
 
 
+@pytest.mark.parametrize("d,n,sigma", [(2, 250000, 0.05), (5, 40000, 0.3)])
+def test_round2_kernels_leave_output_unchanged(d, n, sigma):
+    """The warp-per-tile symmetric root (FSGG_SYM_WPT), the fast single-ticket
+    walks with deferred tie steps (FSGG_WALK_FAST) and the whole-node kernel of
+    the two-deep rows level (FSGG_NODE_KERNEL) are each switched off in turn:
+    samples, reference diagnostics and the built graph's edge set stay the
+    same (weights to fp32 summation order). n = 250k at d = 2 gives 245-point
+    nodes with two-deep rows (the C3 level-12 shape) and walks that start
+    from them; d = 5 takes the staged, expanded-form warp tiles."""
+    import os
+    if d == 2:
+        p, _ = datasets.make_moons(n, 0.05, 11)
+    else:
+        rng = np.random.default_rng(5)
+        p = rng.normal(size=(n, d)) * 0.5 + rng.integers(0, 3, size=(n, 1))
+    ds = F.Dataset(p.astype(np.float32))
+    k = F.Kernel(F.KernelFamily.gaussian, sigma)
+    cfg = F.SparsifierConfig(rounds=12, seed=9)
+    names = ("FSGG_SYM_WPT", "FSGG_WALK_FAST", "FSGG_NODE_KERNEL")
+    saved = {v: os.environ.get(v) for v in names}
+    outs = []
+    try:
+        for off in (None,) + names:
+            for v in names:
+                os.environ.pop(v, None)
+            if off:
+                os.environ[off] = "0"
+            tri, diag = F.sample_neighbors_counted(ds, k, np.arange(n), 12, 9, diagnostics=True)
+            g, rep, _ = F.build_similarity_graph(ds, k, cfg, report=True)
+            outs.append((off, tri, diag, g, rep))
+    finally:
+        for v, old in saved.items():
+            if old is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = old
+    _, tri0, d0, g0, rep0 = outs[0]
+    assert rep0.kde_root_performed_evals > 0  # the symmetric root ran
+    for off, tri, diag, g, rep in outs[1:]:
+        assert np.array_equal(tri0, tri), off
+        assert list(d0.entries_per_level) == list(diag.entries_per_level), off
+        assert list(d0.tickets_per_level) == list(diag.tickets_per_level), off
+        assert d0.degenerate_draws == diag.degenerate_draws, off
+        assert np.array_equal(g0.u, g.u) and np.array_equal(g0.v, g.v), off
+        assert (np.abs(g.w - g0.w) <= 5e-6 * g0.w).all(), off
+        assert rep.kernel_evals == rep0.kernel_evals, off
+
+
 @pytest.mark.parametrize("d", [2, 3])
 def test_sync_free_levels_match_synchronous(d):
     """Sync-free levels (device entry counts, grid-strided kernels, the
