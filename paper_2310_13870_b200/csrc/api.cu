@@ -224,6 +224,7 @@ void run_descent(fsgg_dataset* h, const fsgg_kernel* kernel, const fsgg_config& 
   if (!h->tree_fresh) {
     ds.tree_valid = false;
     ds.tc_ready = false;
+    ds.tie_xn_ready = false;
     fsgg::build_tree(ds);
   }
   h->tree_fresh = false;
@@ -582,6 +583,7 @@ int fsgg_dataset_upload(fsgg_dataset* h, const float* host_points) {
     h->ds.tree_valid = false;  // bounding boxes depend on the coordinates
     h->tree_fresh = false;
     h->ds.tc_ready = false;    // so do the tf32 split copies
+    h->ds.tie_xn_ready = false;
   });
 }
 
@@ -1093,6 +1095,7 @@ int fsgg_shard_root_prepare(fsgg_dataset* h, const fsgg_kernel* kernel, const fs
     const fsgg::KernelSpec ks = fsgg::make_kernel_spec(kernel->family, kernel->sigma);
     ds.tree_valid = false;
     ds.tc_ready = false;
+    ds.tie_xn_ready = false;
     fsgg::build_tree(ds);
     h->tree_fresh = true;  // the shard's descent reuses this table
     {  // the descent's pruning threshold (exact or fast backend)

@@ -134,6 +134,7 @@ struct Dataset {
   }
   // tensor-core path (kde_tc.cu): split tf32 hi/lo copies + tensor maps
   bool tc_ready = false;
+  bool tie_xn_ready = false;  // fp64 point norms of the batched tie guard (sampler.cu)
   alignas(64) unsigned char tc_blob[1152];
   void release_all();
 };

@@ -754,6 +754,159 @@ __global__ void __launch_bounds__(kTieThreads)
   }
 }
 
+// The same recomputation as an fp64 register-tiled product (gaussian and
+// exponential kernels, d a multiple of 4): |q - x|^2 = |q|^2 + |x|^2 - 2 q.x
+// with every factor an fp32 value held in fp64, so each product is exact and
+// only the fp64 accumulation rounds (the direct form has the same property;
+// both are the exact sum to ~1e-16 relative per term). The dot products and
+// the norms accumulate over the dimensions in index order with one fma per
+// term — for x = q the three agree bit for bit and the distance is exactly 0.
+// A CTA takes a batch of <= 32 ties against a chunk of the node's sources:
+// source tiles of 128 rows and tie rows are staged 16 dimensions at a time
+// (coalesced 64-byte row pieces, converted once) and each thread keeps a
+// 4 tie x 8 source block of dot products in registers: one DFMA per (tie,
+// source, dimension) where tie_batch_kernel spends a DADD and a DFMA and
+// re-reads every source row once per 8 ties (C5 root: 24 passes over 220 MB).
+constexpr int kTgTies = 32;
+constexpr int kTgSrc = 128;
+constexpr int kTgK = 16;
+constexpr int kTgThreads = 128;
+
+// fp64 squared norms, dimensions in index order (thread per point, rows
+// staged through shared memory so the reads stay coalesced)
+__global__ void __launch_bounds__(128)
+    point_norms_kernel(const float* __restrict__ pts, uint32_t n, uint32_t d,
+                       double* __restrict__ xn) {
+  __shared__ float tile[128][33];
+  const uint32_t j0 = blockIdx.x * 128;
+  double acc = 0.0;
+  for (uint32_t k0 = 0; k0 < d; k0 += 32) {
+    __syncthreads();
+    for (uint32_t idx = threadIdx.x; idx < 128 * 32; idx += 128) {
+      const uint32_t r = idx >> 5, c = idx & 31;
+      tile[r][c] = (j0 + r < n && k0 + c < d) ? __ldg(pts + size_t(j0 + r) * d + k0 + c) : 0.f;
+    }
+    __syncthreads();
+    const uint32_t kc = min(32u, d - k0);
+    for (uint32_t c = 0; c < kc; ++c) {
+      const double v = double(tile[threadIdx.x][c]);
+      acc = fma(v, v, acc);
+    }
+  }
+  if (j0 + threadIdx.x < n) xn[j0 + threadIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(kTgThreads)
+    tie_gemm_kernel(const float* __restrict__ pts, uint32_t d, int family, double sigma,
+                    const uint32_t* __restrict__ eq, const uint32_t* __restrict__ sorted,
+                    const TieItem* __restrict__ items, uint32_t max_chunks,
+                    const double* __restrict__ xn, double* __restrict__ partials) {
+  __shared__ __align__(16) double qs[kTgK][kTgTies];
+  __shared__ __align__(16) double xs[kTgK][kTgSrc + 1];
+  __shared__ uint32_t qrow[kTgTies];
+  const TieItem it = items[blockIdx.x];
+  // warp ty holds ties 8 ty .. 8 ty + 7 (its shared-memory reads of the tie
+  // rows are broadcasts), lane tx sources tx, tx + 32, tx + 64, tx + 96
+  // (conflict-free 8-byte reads): 12-16 shared-memory cycles per 32 DFMA
+  // (16 cycles) and warp — a 4 x 8 block with the sources in the wider
+  // direction was bound by shared-memory bandwidth
+  const uint32_t tid = threadIdx.x, tx = tid & 31u, ty = tid >> 5;
+  if (tid < uint32_t(kTgTies)) qrow[tid] = tid < it.count ? eq[sorted[it.first + tid]] : 0xffffffffu;
+  __syncthreads();
+  const double inv = family == 0 ? 1.0 / (sigma * sigma) : 1.0 / sigma;
+  double qn[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const uint32_t r = qrow[8 * ty + a];
+    qn[a] = r != 0xffffffffu ? xn[r] : 0.0;
+  }
+  double s0[8], s1[8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a) s0[a] = s1[a] = 0.0;
+  const bool warp_on = 8 * ty < it.count;  // this warp's ties exist
+  for (uint32_t j0 = it.src0; j0 < it.src1; j0 += kTgSrc) {
+    double acc[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (uint32_t k0 = 0; k0 < d; k0 += kTgK) {
+      __syncthreads();  // the previous tiles have been read
+      {  // tie rows: 32 x 16 values, one float4 per thread
+        const uint32_t t = tid >> 2, kq = (tid & 3u) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (qrow[t] != 0xffffffffu && k0 + kq < d)
+          v = __ldg(reinterpret_cast<const float4*>(pts + size_t(qrow[t]) * d + k0 + kq));
+        qs[kq][t] = double(v.x);
+        qs[kq + 1][t] = double(v.y);
+        qs[kq + 2][t] = double(v.z);
+        qs[kq + 3][t] = double(v.w);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {  // source rows: 128 x 16 values
+        const uint32_t idx = tid + uint32_t(kTgThreads) * r;
+        const uint32_t sj = idx >> 2, kq = (idx & 3u) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j0 + sj < it.src1 && k0 + kq < d)
+          v = __ldg(reinterpret_cast<const float4*>(pts + size_t(j0 + sj) * d + k0 + kq));
+        xs[kq][sj] = double(v.x);
+        xs[kq + 1][sj] = double(v.y);
+        xs[kq + 2][sj] = double(v.z);
+        xs[kq + 3][sj] = double(v.w);
+      }
+      __syncthreads();
+      if (warp_on) {
+#pragma unroll
+        for (int kk = 0; kk < kTgK; ++kk) {
+          double q[8], x[4];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) q[a] = qs[kk][8 * ty + a];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) x[b] = xs[kk][tx + 32 * b];
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = fma(q[a], x[b], acc[a][b]);
+        }
+      }
+    }
+    if (warp_on) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t j = j0 + tx + 32 * b;
+        if (j < it.src1) {
+          const double xj = xn[j];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            if (8 * ty + a < it.count) {
+              const double d2 = fmax((qn[a] + xj) - 2.0 * acc[a][b], 0.0);
+              const double v = family == 1 ? exp(-sqrt(d2) * inv) : exp(-d2 * inv);
+              if (j < it.mid)
+                s0[a] += v;
+              else
+                s1[a] += v;
+            }
+          }
+        }
+      }
+    }
+  }
+  // the warp's 32 source lanes: fixed butterfly
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    double a0 = s0[a], a1 = s1[a];
+    for (int o = 16; o; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (tx == 0 && 8 * ty + a < it.count) {
+      double* p = partials + (size_t(it.first + 8 * ty + a) * max_chunks + it.chunk) * 2;
+      p[0] = a0;
+      p[1] = a1;
+    }
+  }
+}
+
 __global__ void gather_u32_kernel(uint32_t n, const uint32_t* __restrict__ idx,
                                   const uint32_t* __restrict__ src, uint32_t* __restrict__ out) {
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1315,21 +1468,34 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
       hl[b] = fl[2 * b + 1];
     }
   }
+  // the register-tiled product (tie_gemm_kernel) for gaussian / exponential
+  // kernels and d a multiple of 4; FSGG_TIE_GEMM=0 keeps tie_batch_kernel
+  const char* tg_env = std::getenv("FSGG_TIE_GEMM");  // read per call: tests toggle it
+  // ... and when the level's nodes hold a few ties each (a 32-tie tile costs
+  // the same with 2 ties as with 8: measured on C5, the tiles win from ~3
+  // ties per node; FSGG_TIE_GEMM_MIN overrides)
+  const char* tm_env = std::getenv("FSGG_TIE_GEMM_MIN");
+  const uint32_t tg_min = tm_env ? uint32_t(std::atoi(tm_env)) : 3u;
+  uint32_t tie_nodes = cnt ? 1 : 0;
+  for (uint32_t b = 1; b < cnt; ++b) tie_nodes += slot[b] != slot[b - 1];
+  const bool gemm = ks.family != 2 && (ds.d & 3u) == 0 && !(tg_env && tg_env[0] == '0') &&
+                    cnt >= tg_min * tie_nodes;
+  const uint32_t batch = gemm ? uint32_t(kTgTies) : uint32_t(kTieBatch);
   // source chunk: kTieChunk, shortened (to >= 128 sources) when the level's
   // batches x chunks would not give every SM several CTAs
   uint64_t batch_sources = 0;
   for (uint32_t b = 0; b < cnt;) {
     uint32_t e = b + 1;
-    while (e < cnt && slot[e] == slot[b] && e - b < uint32_t(kTieBatch)) ++e;
+    while (e < cnt && slot[e] == slot[b] && e - b < batch) ++e;
     batch_sources += hl[b] - hf[b];
     b = e;
   }
-  const uint64_t want_items = uint64_t(ds.num_sms) * 16;
+  const uint64_t want_items = uint64_t(ds.num_sms) * (gemm ? 4 : 16);
   uint32_t chunk_len = kTieChunk;
   while (chunk_len > 128 && batch_sources / chunk_len < want_items) chunk_len >>= 1;
   for (uint32_t b = 0; b < cnt;) {
     uint32_t e = b + 1;
-    while (e < cnt && slot[e] == slot[b] && e - b < uint32_t(kTieBatch)) ++e;
+    while (e < cnt && slot[e] == slot[b] && e - b < batch) ++e;
     const uint32_t f = hf[b], l = hl[b], mid = f + (l - f) / 2;
     const uint32_t chunks = std::max<uint32_t>(1, (l - f + chunk_len - 1) / chunk_len);
     max_chunks = std::max(max_chunks, chunks);
@@ -1354,12 +1520,26 @@ void batched_tie_sums(Dataset& ds, const KernelSpec& ks, uint32_t level, const u
   FSGG_CUDA(cudaMemcpyAsync(ditems.as<void>(), items.data(), items.size() * sizeof(TieItem),
                             cudaMemcpyHostToDevice, s));
   FSGG_CUDA(cudaMemcpyAsync(dnch.as<void>(), nch.data(), size_t(cnt) * 4, cudaMemcpyHostToDevice, s));
-  const size_t smem = size_t(kTieBatch) * ds.d * 8;
-  FSGG_CUDA(cudaFuncSetAttribute(tie_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(std::max<size_t>(smem, 48u << 10))));
-  tie_batch_kernel<<<uint32_t(items.size()), kTieThreads, smem, s>>>(
-      ds.pts.as<float>(), ds.d, ks.family, ks.sigma, eq, sorted.as<uint32_t>(),
-      ditems.as<TieItem>(), max_chunks, parts.as<double>());
+  if (gemm) {
+    DevBuf& xn = ds.buf("s.tie_xn", size_t(ds.n) * 8);
+    if (!ds.tie_xn_ready) {  // once per point set
+      point_norms_kernel<<<ceil_div_u32(ds.n, 128), 128, 0, s>>>(ds.pts.as<float>(), ds.n, ds.d,
+                                                                xn.as<double>());
+      FSGG_LAUNCH_CHECK();
+      ds.tie_xn_ready = true;
+      ds.launches++;
+    }
+    tie_gemm_kernel<<<uint32_t(items.size()), kTgThreads, 0, s>>>(
+        ds.pts.as<float>(), ds.d, ks.family, ks.sigma, eq, sorted.as<uint32_t>(),
+        ditems.as<TieItem>(), max_chunks, xn.as<double>(), parts.as<double>());
+  } else {
+    const size_t smem = size_t(kTieBatch) * ds.d * 8;
+    FSGG_CUDA(cudaFuncSetAttribute(tie_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(std::max<size_t>(smem, 48u << 10))));
+    tie_batch_kernel<<<uint32_t(items.size()), kTieThreads, smem, s>>>(
+        ds.pts.as<float>(), ds.d, ks.family, ks.sigma, eq, sorted.as<uint32_t>(),
+        ditems.as<TieItem>(), max_chunks, parts.as<double>());
+  }
   FSGG_LAUNCH_CHECK();
   tie_reduce_kernel<<<ceil_div_u32(cnt, 128), 128, 0, s>>>(cnt, sorted.as<uint32_t>(),
                                                           dnch.as<uint32_t>(), max_chunks,

@@ -623,6 +623,36 @@ def test_round2_kernels_leave_output_unchanged(d, n, sigma):
         assert rep.kernel_evals == rep0.kernel_evals, off
 
 
+def test_tie_guard_tiled_product_matches_batched_sums(oracle):
+    """High-d tie guard: the fp64 register-tiled product (tie_gemm_kernel,
+    |q|^2 + |x|^2 - 2 q.x) and the batched direct-difference sums
+    (tie_batch_kernel, FSGG_TIE_GEMM=0) re-decide every flagged draw the same
+    way — identical samples — and both give the oracle's edge set."""
+    import os
+    rng = np.random.default_rng(21)
+    n, d = 6000, 64
+    p = (rng.normal(size=(n, d)) * 0.35 + rng.integers(0, 4, size=(n, 1))).astype(np.float32)
+    ds = F.Dataset(p)
+    k = F.Kernel(F.KernelFamily.gaussian, 1.8)
+    old = os.environ.get("FSGG_TIE_GEMM")
+    outs = []
+    try:
+        for v in ("1", "0"):
+            os.environ["FSGG_TIE_GEMM"] = v
+            tri, diag = F.sample_neighbors_counted(ds, k, np.arange(n), 12, 4, diagnostics=True)
+            outs.append((tri, diag))
+    finally:
+        if old is None:
+            os.environ.pop("FSGG_TIE_GEMM", None)
+        else:
+            os.environ["FSGG_TIE_GEMM"] = old
+    assert np.array_equal(outs[0][0], outs[1][0])
+    g, rep, _ = F.build_similarity_graph(ds, k, F.SparsifierConfig(rounds=12, seed=4), report=True)
+    assert rep.tie_verified_entries > 0  # the guard ran
+    ref = oracle.build_graph(p.astype(np.float64), 1.8, 12, seed=4)
+    assert np.array_equal(g.u, ref["u"]) and np.array_equal(g.v, ref["v"])
+
+
 @pytest.mark.parametrize("d", [2, 3])
 def test_sync_free_levels_match_synchronous(d):
     """Sync-free levels (device entry counts, grid-strided kernels, the
