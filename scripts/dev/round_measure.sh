@@ -13,6 +13,7 @@ cap() { # name regex config
 cap c3_wtile sym_wtile_kernel C3
 cap c4_wtile sym_wtile_kernel C4
 cap c3_walkf walk_fast_kernel C3
-cap c3_tiled kde_lowd_tiled_kernel C3
+cap c3_node kde_lowd_node_kernel C3
+cap c5_tcsym kde_tc_sym256 C5
 python scripts/shard_projection.py --out gpurun_out/r2_shard_projection_c3.json > gpurun_out/r2_shard_projection_c3.log 2>&1
 tail -3 gpurun_out/r2_pytest_gpu.log; tail -2 gpurun_out/smoke.log
