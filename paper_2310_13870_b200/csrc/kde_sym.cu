@@ -326,6 +326,22 @@ __global__ void __launch_bounds__(128)
 #define FSGG_SYM_EXP_MAX 64.f
 #endif
 constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
+// Factored form (warp-per-tile kernel, gaussian, d <= FSGG_SYM_FACT_MAX_D):
+// 2^-|q' - x'|^2 = 2^-|q'|^2 * 2^-(|x'|^2 - 2 q'.x'). The row factor leaves
+// the row sum (one multiply per row per tile) and enters the column sum as
+// the multiplicand of the accumulating FFMA2, so a pair costs d packed
+// FMA-pipe operations for the exponent + 2 for the two sums (d = 2: 4
+// instead of the direct form's 6). Same tile-relative origin, same per-tile
+// norm bound and the same error scale as the expanded form above
+// (~eps_f32 * (|q'|^2 + |x'|^2) in the exponent, <= 64: ~5e-6 relative at
+// worst, far inside the tie guard's 1e-4).
+#ifndef FSGG_SYM_FACT_MAX_D
+#define FSGG_SYM_FACT_MAX_D 0
+#endif
+#ifndef FSGG_SYM_FACT_MAX
+#define FSGG_SYM_FACT_MAX 160.f
+#endif
+constexpr float kSymFactMaxNorm = FSGG_SYM_FACT_MAX;
 
 template <int D, int FAM, int ROWS, bool OWN>
 __device__ __forceinline__ void sym_tile_body(
@@ -629,9 +645,9 @@ constexpr int kWtWarps = 4;
 // Sources of J staged per warp: all of them for d <= 2, else stages of
 // kWtStage<..> sources (<= 8 KiB of shared memory per warp) — the warp fills
 // its own slice, so staging costs nothing but the loop.
-template <int SW, uint32_t CAP>
+template <int SW, uint32_t CAP, uint32_t BYTES = 8192u>
 constexpr uint32_t wt_stage() {
-  const uint32_t fit = (8192u / (SW * 8u)) & ~7u;
+  const uint32_t fit = (BYTES / (SW * 8u)) & ~7u;
   return fit < CAP ? fit : CAP;
 }
 
@@ -646,9 +662,12 @@ __device__ __forceinline__ void sym_wtile_body(
     const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
     const float* __restrict__ bbox) {
   constexpr uint32_t kCap = 32u * ROWS;
-  constexpr bool EXP_OK = FAM == 0 && D >= FSGG_SYM_EXP_MIN_D;
+  constexpr bool FACT = FAM == 0 && D <= FSGG_SYM_FACT_MAX_D;  // factored form
+  constexpr bool EXP_OK = FACT || (FAM == 0 && D >= FSGG_SYM_EXP_MIN_D);
   constexpr int SW = EXP_OK ? D + 1 : D;  // float2 per source in shared memory
-  constexpr uint32_t SC = wt_stage<SW, kCap>();
+  // d <= 2 holds 8 CTAs per SM: 4 KiB of sources per warp (two stages per tile
+  // in the factored form's 3-word format)
+  constexpr uint32_t SC = wt_stage<SW, kCap, (D <= 2 ? 4096u : 8192u)>();
   static_assert(SC * SW * 2 >= kCap, "the stage buffer doubles as the row buffer");
   __shared__ __align__(16) float2 sx_all[kWtWarps][SC * SW];
   __shared__ float colv_all[kWtWarps][kCap];
@@ -678,16 +697,21 @@ __device__ __forceinline__ void sym_wtile_body(
       for (int k = 0; k < D; ++k) c0[k] = __ldg(pts + size_t(fi) * D + k);
     }
     float2 q2[ROWS / 2][D];
-    float2 qn[EXP_OK ? ROWS / 2 : 1];  // expanded form: |q'|^2 of each row pair
+    // expanded form: |q'|^2 of each row pair; factored form: the rows'
+    // factors 2^-|q'|^2 (direct tiles: 1), 0 for an absent row
+    float2 qn[EXP_OK ? ROWS / 2 : 1];
     float mi = 0.f, mj = 0.f;
+    // an absent row sits far away; in the factored form at the origin with
+    // factor 0 (its exponent must stay finite)
+    constexpr float kAbsent = FACT ? 0.f : 1e18f;
 #pragma unroll
     for (int p = 0; p < ROWS / 2; ++p) {
       const uint32_t r0 = lane * ROWS + 2 * p, r1 = r0 + 1;
       float na = 0.f, nb = 0.f;
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : 1e18f;
-        const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : 1e18f;
+        const float a = r0 < ni ? (__ldg(pts + size_t(fi + r0) * D + k) - c0[k]) * cs : kAbsent;
+        const float b = r1 < ni ? (__ldg(pts + size_t(fi + r1) * D + k) - c0[k]) * cs : kAbsent;
         q2[p][k] = make_float2(a, b);
         na = fmaf(a, a, na);
         nb = fmaf(b, b, nb);
@@ -699,7 +723,27 @@ __device__ __forceinline__ void sym_wtile_body(
       }
     }
     bool use_exp = false;
-    if constexpr (EXP_OK) {
+    if constexpr (FACT) {
+      // the form is the tile's: the scaled norms of its two boxes' farthest
+      // corners from the origin (no pass over the points)
+      float bi = 0.f, bj = 0.f;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float li = __ldg(lo + size_t(tl.I) * D + k), hi_ = __ldg(hi + size_t(tl.I) * D + k);
+        const float lj = __ldg(lo + size_t(tl.J) * D + k), hj = __ldg(hi + size_t(tl.J) * D + k);
+        const float ai = fmaxf(fabsf(li - c0[k]), fabsf(hi_ - c0[k])) * cs;
+        const float aj = fmaxf(fabsf(lj - c0[k]), fabsf(hj - c0[k])) * cs;
+        bi = fmaf(ai, ai, bi);
+        bj = fmaf(aj, aj, bj);
+      }
+      use_exp = bi + bj <= kSymFactMaxNorm;
+#pragma unroll
+      for (int p = 0; p < ROWS / 2; ++p) {
+        const uint32_t r0 = lane * ROWS + 2 * p, r1 = r0 + 1;
+        qn[p] = make_float2(r0 < ni ? (use_exp ? ex2_approx(-qn[p].x) : 1.f) : 0.f,
+                            r1 < ni ? (use_exp ? ex2_approx(-qn[p].y) : 1.f) : 0.f);
+      }
+    } else if constexpr (EXP_OK) {
       // the form is the tile's: largest scaled norms of its two blocks
       for (uint32_t j = lane; j < nj; j += 32) {
         float nrm = 0.f;
@@ -759,7 +803,11 @@ __device__ __forceinline__ void sym_wtile_body(
 #pragma unroll
           for (int p = 0; p < ROWS / 2; ++p) {
             float2 t;
-            if constexpr (EXP) {
+            if constexpr (EXP && FACT) {  // |x'|^2 - 2 q'.x'
+              t = __ffma2_rn(q2[p][0], x[0], x[D]);
+#pragma unroll
+              for (int k = 1; k < D; ++k) t = __ffma2_rn(q2[p][k], x[k], t);
+            } else if constexpr (EXP) {
               t = __fadd2_rn(qn[p], x[D]);
 #pragma unroll
               for (int k = 0; k < D; ++k) t = __ffma2_rn(q2[p][k], x[k], t);
@@ -777,27 +825,34 @@ __device__ __forceinline__ void sym_wtile_body(
             }
             const float2 e = make_float2(ex2_approx(-t.x), ex2_approx(-t.y));
             racc[p] = __fadd2_rn(racc[p], e);
-            es = p == 0 ? e : __fadd2_rn(es, e);
+            if constexpr (FACT)
+              es = p == 0 ? __fmul2_rn(e, qn[0]) : __ffma2_rn(e, qn[p], es);
+            else
+              es = p == 0 ? e : __fadd2_rn(es, e);
           }
           c[jj] = es.x + es.y;
         }
-        // lanes l ^ 16 and l ^ 8 folded, then a transpose-reduction butterfly
-        // over 8 lanes: lane l ends with the column sum of source jb + (l & 7)
+        // transpose-reduction butterfly over lane bits 4, 3, 2 (each stage
+        // keeps half of the values and sends the other half: 4 + 2 + 1
+        // shuffles), then two plain folds: the four lanes with
+        // lane >> 2 == s end with the column sum of source jb + bitrev3(s)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 16);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] += __shfl_xor_sync(0xffffffffu, c[i], 8);
-#pragma unroll
-        for (int st = 4; st >= 1; st >>= 1) {
+        for (int st = 16, h = 4; h >= 1; st >>= 1, h >>= 1) {
           const bool up = (lane & st) != 0;
 #pragma unroll
-          for (int i = 0; i < st; ++i) {
-            const float keep = up ? c[i + st] : c[i];
-            const float send = up ? c[i] : c[i + st];
+          for (int i = 0; i < h; ++i) {
+            const float keep = up ? c[i + h] : c[i];
+            const float send = up ? c[i] : c[i + h];
             c[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
           }
         }
-        if (lane < 8 && jb + lane < nj) colv[jb + lane] = c[0];
+        c[0] += __shfl_xor_sync(0xffffffffu, c[0], 2);
+        c[0] += __shfl_xor_sync(0xffffffffu, c[0], 1);
+        {
+          const uint32_t sj = jb + ((lane >> 4) & 1u) * 4u + ((lane >> 3) & 1u) * 2u +
+                              ((lane >> 2) & 1u);
+          if ((lane & 3u) == 0 && sj < nj) colv[sj] = c[0];
+        }
       }
     };
     const uint32_t njp = (nj + 7u) & ~7u;  // whole batches; slots past nj far away
@@ -845,6 +900,7 @@ __device__ __forceinline__ void sym_wtile_body(
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < ROWS / 2; ++p) {
+      if constexpr (FACT) racc[p] = __fmul2_rn(racc[p], qn[p]);
       rowv[lane * ROWS + 2 * p] = racc[p].x;
       rowv[lane * ROWS + 2 * p + 1] = racc[p].y;
     }
