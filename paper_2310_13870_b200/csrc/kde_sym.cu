@@ -338,6 +338,9 @@ constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
 #ifndef FSGG_SYM_FACT_MAX_D
 #define FSGG_SYM_FACT_MAX_D 0
 #endif
+#ifndef FSGG_SYM_NDUP
+#define FSGG_SYM_NDUP 1
+#endif
 #ifndef FSGG_SYM_FACT_MAX
 #define FSGG_SYM_FACT_MAX 160.f
 #endif
@@ -665,6 +668,10 @@ __device__ __forceinline__ void sym_wtile_body(
   constexpr bool FACT = FAM == 0 && D <= FSGG_SYM_FACT_MAX_D;  // factored form
   constexpr bool EXP_OK = FACT || (FAM == 0 && D >= FSGG_SYM_EXP_MIN_D);
   constexpr int SW = EXP_OK ? D + 1 : D;  // float2 per source in shared memory
+  // d = 2, direct form: sources are stored once (x, y), two per 16-byte load,
+  // and duplicated into register pairs by the ALU pipe — shared-memory loads
+  // share the MIO queue and its return path with MUFU, the binding pipe
+  constexpr bool NDUP = !EXP_OK && D == 2 && FSGG_SYM_NDUP;
   // d <= 2 holds 8 CTAs per SM: 4 KiB of sources per warp (two stages per tile
   // in the factored form's 3-word format)
   constexpr uint32_t SC = wt_stage<SW, kCap, (D <= 2 ? 4096u : 8192u)>();
@@ -799,6 +806,14 @@ __device__ __forceinline__ void sym_wtile_body(
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
           const float2* x = sx + (jb - s0 + jj) * SW;
+          float2 xd[NDUP ? D : 1];
+          if constexpr (NDUP) {
+            const float4 v = *reinterpret_cast<const float4*>(
+                reinterpret_cast<const float*>(sx) + (jb - s0 + (jj & ~1)) * 2);
+            xd[0] = (jj & 1) ? make_float2(v.z, v.z) : make_float2(v.x, v.x);
+            xd[1] = (jj & 1) ? make_float2(v.w, v.w) : make_float2(v.y, v.y);
+            x = xd;
+          }
           float2 es = make_float2(0.f, 0.f);
 #pragma unroll
           for (int p = 0; p < ROWS / 2; ++p) {
@@ -884,7 +899,10 @@ __device__ __forceinline__ void sym_wtile_body(
         for (uint32_t idx = s0 * D + lane; idx < s1 * D; idx += 32) {
           const float v =
               idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
-          sx[idx - s0 * D] = make_float2(v, v);
+          if constexpr (NDUP)
+            reinterpret_cast<float*>(sx)[idx - s0 * D] = v;
+          else
+            sx[idx - s0 * D] = make_float2(v, v);
         }
       }
       __syncwarp();
