@@ -338,9 +338,6 @@ constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
 #ifndef FSGG_SYM_FACT_MAX_D
 #define FSGG_SYM_FACT_MAX_D 0
 #endif
-#ifndef FSGG_SYM_NDUP
-#define FSGG_SYM_NDUP 1
-#endif
 #ifndef FSGG_SYM_FACT_MAX
 #define FSGG_SYM_FACT_MAX 160.f
 #endif
@@ -650,7 +647,7 @@ constexpr int kWtWarps = 4;
 // its own slice, so staging costs nothing but the loop.
 template <int SW, uint32_t CAP, uint32_t BYTES = 8192u>
 constexpr uint32_t wt_stage() {
-  const uint32_t fit = (BYTES / (SW * 8u)) & ~7u;
+  const uint32_t fit = (BYTES / (SW * 4u)) & ~7u;
   return fit < CAP ? fit : CAP;
 }
 
@@ -667,21 +664,22 @@ __device__ __forceinline__ void sym_wtile_body(
   constexpr uint32_t kCap = 32u * ROWS;
   constexpr bool FACT = FAM == 0 && D <= FSGG_SYM_FACT_MAX_D;  // factored form
   constexpr bool EXP_OK = FACT || (FAM == 0 && D >= FSGG_SYM_EXP_MIN_D);
-  constexpr int SW = EXP_OK ? D + 1 : D;  // float2 per source in shared memory
-  // d = 2, direct form: sources are stored once (x, y), two per 16-byte load,
-  // and duplicated into register pairs by the ALU pipe — shared-memory loads
-  // share the MIO queue and its return path with MUFU, the binding pipe
-  constexpr bool NDUP = !EXP_OK && D == 2 && FSGG_SYM_NDUP;
+  // Words per source in shared memory, padded to an even count so that a
+  // pair of sources is a whole number of 16-byte loads. Each word is stored
+  // once: the packed operations take it as a broadcast scalar operand
+  // (FADD2 R, R.F32x2, R.F32), so no duplicated (v, v) pairs are staged —
+  // shared-memory loads share the MIO queue with MUFU, the binding pipe.
+  constexpr int SW = ((EXP_OK ? D + 1 : D) + 1) & ~1;
   // d <= 2 holds 8 CTAs per SM: 4 KiB of sources per warp (two stages per tile
   // in the factored form's 3-word format)
   constexpr uint32_t SC = wt_stage<SW, kCap, (D <= 2 ? 4096u : 8192u)>();
-  static_assert(SC * SW * 2 >= kCap, "the stage buffer doubles as the row buffer");
-  __shared__ __align__(16) float2 sx_all[kWtWarps][SC * SW];
+  static_assert(SC * SW >= kCap, "the stage buffer doubles as the row buffer");
+  __shared__ __align__(16) float sx_all[kWtWarps][SC * SW];
   __shared__ float colv_all[kWtWarps][kCap];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float2* sx = sx_all[w];
+  float* sx = sx_all[w];
   float* colv = colv_all[w];
-  float* rowv = reinterpret_cast<float*>(sx);  // reused after the tile loop
+  float* rowv = sx;  // reused after the tile loop
   unsigned long long ev = 0;                   // pair evaluations of this warp's tiles
   for (;;) {
     uint32_t ti = 0;
@@ -805,15 +803,24 @@ __device__ __forceinline__ void sym_wtile_body(
         float c[8];  // this lane's ROWS-row partial of each source's column sum
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          const float2* x = sx + (jb - s0 + jj) * SW;
-          float2 xd[NDUP ? D : 1];
-          if constexpr (NDUP) {
-            const float4 v = *reinterpret_cast<const float4*>(
-                reinterpret_cast<const float*>(sx) + (jb - s0 + (jj & ~1)) * 2);
-            xd[0] = (jj & 1) ? make_float2(v.z, v.z) : make_float2(v.x, v.x);
-            xd[1] = (jj & 1) ? make_float2(v.w, v.w) : make_float2(v.y, v.y);
-            x = xd;
+          // the words of sources jj and jj ^ 1 come in together (16-byte
+          // loads; the unrolled loop keeps one copy per pair)
+          float xw[2 * SW];
+          {
+            const float4* src = reinterpret_cast<const float4*>(sx + (jb - s0 + (jj & ~1)) * SW);
+#pragma unroll
+            for (int v4 = 0; v4 < SW / 2; ++v4) {
+              const float4 v = src[v4];
+              xw[4 * v4] = v.x;
+              xw[4 * v4 + 1] = v.y;
+              xw[4 * v4 + 2] = v.z;
+              xw[4 * v4 + 3] = v.w;
+            }
           }
+          float2 x[SW];
+#pragma unroll
+          for (int k = 0; k < SW; ++k)
+            x[k] = make_float2(xw[(jj & 1) * SW + k], xw[(jj & 1) * SW + k]);
           float2 es = make_float2(0.f, 0.f);
 #pragma unroll
           for (int p = 0; p < ROWS / 2; ++p) {
@@ -891,18 +898,17 @@ __device__ __forceinline__ void sym_wtile_body(
             }
           }
 #pragma unroll
-          for (int k = 0; k < D; ++k)
-            sx[(j - s0) * SW + k] = make_float2(-2.f * xv[k], -2.f * xv[k]);
-          sx[(j - s0) * SW + D] = make_float2(nrm, nrm);
+          for (int k = 0; k < D; ++k) sx[(j - s0) * SW + k] = -2.f * xv[k];
+          sx[(j - s0) * SW + D] = nrm;
         }
       } else {
         for (uint32_t idx = s0 * D + lane; idx < s1 * D; idx += 32) {
           const float v =
               idx < nj * D ? -((__ldg(ppts + size_t(fj) * D + idx) - c0[idx % D]) * cs) : -1e18f;
-          if constexpr (NDUP)
-            reinterpret_cast<float*>(sx)[idx - s0 * D] = v;
+          if constexpr (SW == D)
+            sx[idx - s0 * D] = v;
           else
-            sx[idx - s0 * D] = make_float2(v, v);
+            sx[(idx / D - s0) * SW + idx % D] = v;
         }
       }
       __syncwarp();
