@@ -335,8 +335,11 @@ constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
 // norm bound and the same error scale as the expanded form above
 // (~eps_f32 * (|q'|^2 + |x'|^2) in the exponent, <= 64: ~5e-6 relative at
 // worst, far inside the tie guard's 1e-4).
+#ifndef FSGG_SYM_FACT_MIN_D
+#define FSGG_SYM_FACT_MIN_D 3
+#endif
 #ifndef FSGG_SYM_FACT_MAX_D
-#define FSGG_SYM_FACT_MAX_D 0
+#define FSGG_SYM_FACT_MAX_D 6
 #endif
 #ifndef FSGG_SYM_FACT_MAX
 #define FSGG_SYM_FACT_MAX 160.f
@@ -662,7 +665,8 @@ __device__ __forceinline__ void sym_wtile_body(
     const float* __restrict__ ppts, const uint32_t* __restrict__ perm,
     const float* __restrict__ bbox) {
   constexpr uint32_t kCap = 32u * ROWS;
-  constexpr bool FACT = FAM == 0 && D <= FSGG_SYM_FACT_MAX_D;  // factored form
+  constexpr bool FACT =
+      FAM == 0 && D >= FSGG_SYM_FACT_MIN_D && D <= FSGG_SYM_FACT_MAX_D;  // factored form
   constexpr bool EXP_OK = FACT || (FAM == 0 && D >= FSGG_SYM_EXP_MIN_D);
   // Words per source in shared memory, padded to an even count so that a
   // pair of sources is a whole number of 16-byte loads. Each word is stored
@@ -728,7 +732,7 @@ __device__ __forceinline__ void sym_wtile_body(
       }
     }
     bool use_exp = false;
-    if constexpr (FACT) {
+    if constexpr (FACT && D <= 2) {
       // the form is the tile's: the scaled norms of its two boxes' farthest
       // corners from the origin (no pass over the points)
       float bi = 0.f, bj = 0.f;
@@ -764,6 +768,14 @@ __device__ __forceinline__ void sym_wtile_body(
         mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
       }
       use_exp = mi + mj <= kSymExpMaxNorm;
+      if constexpr (FACT) {
+#pragma unroll
+        for (int p = 0; p < ROWS / 2; ++p) {
+          const uint32_t r0 = lane * ROWS + 2 * p, r1 = r0 + 1;
+          qn[p] = make_float2(r0 < ni ? (use_exp ? ex2_approx(-qn[p].x) : 1.f) : 0.f,
+                              r1 < ni ? (use_exp ? ex2_approx(-qn[p].y) : 1.f) : 0.f);
+        }
+      }
     }
     // source batches of J beyond the pruning radius of I's box (sym_tile_body)
     uint32_t skip[2];
