@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(kWalkThreads, D <= 2 ? FSGG_WALKF_CTAS : 0)
   bool deferred = false;
   if (mine) {
     q = wq[i];
-    const uint64_t qlink = query_link(q);
+    // opaque: under the register cap the compiler otherwise recomputes the
+    // query's splitmix64 at every step instead of keeping two registers
+    uint64_t qlink = query_link(q);
+    asm volatile("" : "+l"(qlink));
     uint64_t h = wh[i];
     uint32_t nf = tfirst[h], nl = tlast[h];
     float em = welm[i];
