@@ -1159,6 +1159,17 @@ __global__ void __launch_bounds__(kLookupThreads)
   }
 }
 
+// log2 of a positive normal double to fp32 accuracy: exponent field plus
+// MUFU.LG2 of the mantissa. An entry's mass exponent only scales pruning
+// thresholds and tie margins (which carry bits of slack); the fp64 log2 it
+// replaces was ~45% of scatter_kernel's instructions.
+__device__ __forceinline__ float log2_mass(double g) {
+  const long long b = __double_as_longlong(g);
+  const int e = int((b >> 52) & 0x7ff) - 1023;
+  const float m = float(__longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL));
+  return float(e) + __log2f(m);
+}
+
 __device__ __forceinline__ uint32_t hiw(unsigned long long x) {
   return uint32_t(x >> 32);
 }
@@ -1214,7 +1225,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
         neq[pos] = q;
         net[pos] = l;
         neg[pos] = 2 * g;
-        nelm[pos] = static_cast<float>(log2(g1[i]));
+        nelm[pos] = log2_mass(g1[i]);
         neprow[pos] = prow;
       }
       if (low(fl)) {
@@ -1222,7 +1233,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
         neq[pos] = q;
         net[pos] = t - l;
         neg[pos] = 2 * g + 1;
-        nelm[pos] = static_cast<float>(log2(g2[i]));
+        nelm[pos] = log2_mass(g2[i]);
         neprow[pos] = prow;
       }
     }
