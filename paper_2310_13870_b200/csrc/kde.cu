@@ -92,44 +92,70 @@ __device__ __forceinline__ uint32_t find_slot(const uint32_t* blk_off,
   return lo;
 }
 
-// Sum of 2^(off - scale*dist) over the lenp staged sources (negated,
-// duplicated, padded to a multiple of 4) for two packed entries: fp32 partial
-// sums over runs of kFlush sources, flushed into fp64 (keeps the accumulation
-// error ~1e-7 relative at no measurable cost).
+// Sum of 2^(off - scale*dist) over the lenp staged sources (negated, each
+// coordinate stored once, padded to a multiple of 4 sources) for two packed
+// entries: fp32 partial sums over runs of kFlush sources, flushed into fp64
+// (keeps the accumulation error ~1e-7 relative at no measurable cost).
+// Four sources come in with D 16-byte loads and enter the packed operations
+// as broadcast scalar operands (FADD2 R, R.F32x2, R.F32): shared-memory
+// loads share the MIO queue with MUFU, the binding pipe, so a source costs a
+// quarter to a half of a load instead of one.
 template <int D, int FAM>
-__device__ __forceinline__ void lowd_staged_sum(const float2* sm, uint32_t lenp,
+__device__ __forceinline__ void lowd_staged_sum(const float* sm, uint32_t lenp,
                                                 const float2 (&q2)[D], float2 off2,
                                                 float scale, double& accA, double& accB) {
   const float2 ms = make_float2(-scale, -scale);
   for (uint32_t j0 = 0; j0 < lenp; j0 += kFlush) {
     const uint32_t j1 = min(lenp, j0 + kFlush);
     float2 acc = make_float2(0.f, 0.f);
-    auto arg_of = [&](uint32_t j) {
-      const float2* x = sm + j * D;
-      float2 t = fam_first<FAM>(__fadd2_rn(q2[0], x[0]));
+    // the four sources j .. j + 3 (j a multiple of 4)
+    auto load4 = [&](uint32_t j, float (&xs)[4 * D]) {
+      const float4* p = reinterpret_cast<const float4*>(sm + size_t(j) * D);
 #pragma unroll
-      for (int k = 1; k < D; ++k) t = fam_next<FAM>(__fadd2_rn(q2[k], x[k]), t);
+      for (int v4 = 0; v4 < D; ++v4) {
+        const float4 v = p[v4];
+        xs[4 * v4] = v.x;
+        xs[4 * v4 + 1] = v.y;
+        xs[4 * v4 + 2] = v.z;
+        xs[4 * v4 + 3] = v.w;
+      }
+    };
+    auto arg_of = [&](const float* x) {
+      float2 t = fam_first<FAM>(__fadd2_rn(q2[0], make_float2(x[0], x[0])));
+#pragma unroll
+      for (int k = 1; k < D; ++k)
+        t = fam_next<FAM>(__fadd2_rn(q2[k], make_float2(x[k], x[k])), t);
       t = fam_finish<FAM>(t);
       return __ffma2_rn(t, ms, off2);
     };
     uint32_t j = j0;
     // one source in kPolyEvery takes the FP32-pipe exp2, the rest MUFU:
     // balances the two pipes (the loop is MUFU-bound otherwise)
+    static_assert(kPolyEvery % 4 == 0, "sources are loaded four at a time");
     if (kPolyEvery > 0)
       for (; j + kPolyEvery <= j1; j += kPolyEvery) {
 #pragma unroll
-        for (uint32_t u = 0; u < kPolyEvery; ++u) {
-          const float2 arg = arg_of(j + u);
-          if (u == kPolyEvery - 1)
-            acc = __fadd2_rn(acc, ex2_poly2(arg));
-          else
-            acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+        for (uint32_t u4 = 0; u4 < kPolyEvery; u4 += 4) {
+          float xs[4 * D];
+          load4(j + u4, xs);
+#pragma unroll
+          for (uint32_t u = 0; u < 4; ++u) {
+            const float2 arg = arg_of(xs + u * D);
+            if (u4 + u == kPolyEvery - 1)
+              acc = __fadd2_rn(acc, ex2_poly2(arg));
+            else
+              acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+          }
         }
       }
-#pragma unroll 4
-    for (; j < j1; ++j) {
-      const float2 arg = arg_of(j);
-      acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+    for (; j < j1; j += 4) {
+      float xs[4 * D];
+      load4(j, xs);
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) {
+        const float2 arg = arg_of(xs + u * D);
+        acc = __fadd2_rn(acc, make_float2(ex2_approx(arg.x), ex2_approx(arg.y)));
+      }
     }
     accA += acc.x;
     accB += acc.y;
@@ -137,10 +163,10 @@ __device__ __forceinline__ void lowd_staged_sum(const float2* sm, uint32_t lenp,
 }
 
 // Sum of 2^(off - scale*dist) over sources [cf, cl) for two packed entries;
-// sources staged negated and duplicated in shared memory.
+// sources staged negated in shared memory.
 template <int D, int FAM>
 __device__ __forceinline__ void lowd_range_sum(
-    const float* __restrict__ pts, float2* sm, const float2 (&q2)[D],
+    const float* __restrict__ pts, float* sm, const float2 (&q2)[D],
     float2 off2, float scale, uint32_t cf, uint32_t cl, double& accA,
     double& accB, bool warp_skip = false) {
   constexpr int T = LowDTile<D>::T;
@@ -150,8 +176,7 @@ __device__ __forceinline__ void lowd_range_sum(
     __syncthreads();
     const float* src = pts + size_t(t0) * D;
     for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
-      float v = idx < len * D ? -__ldg(src + idx) : -kPad;
-      sm[idx] = make_float2(v, v);
+      sm[idx] = idx < len * D ? -__ldg(src + idx) : -kPad;
     }
     __syncthreads();
     if (warp_skip) continue;  // this warp's entries all prune the range
@@ -194,7 +219,7 @@ __global__ void __launch_bounds__(kThreads)
                           unsigned long long* __restrict__ performed, int per_sub) {
   const bool prune = prune_bits > 0.f;
   constexpr int T = LowDTile<D>::T;
-  __shared__ __align__(16) float2 sm[T * D];
+  __shared__ __align__(16) float sm[T * D];
   __shared__ unsigned long long s_done;
   const uint32_t K = 1u << cdepth;
   const uint32_t item = blockIdx.x;
@@ -298,7 +323,7 @@ __global__ void __launch_bounds__(kThreads)
                          unsigned long long* __restrict__ performed,
                          double* __restrict__ g1, double* __restrict__ g2) {
   const bool prune = prune_bits > 0.f;
-  __shared__ __align__(16) float2 sm[(kNodeMax + 16) * D];
+  __shared__ __align__(16) float sm[(kNodeMax + 16) * D];
   __shared__ unsigned long long s_done;
   const uint32_t blk = blockIdx.x;
   const uint32_t g = find_slot(blk_off, num_slots, blk);
@@ -321,8 +346,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t len = cl[sc] - cf[sc], lenp = (len + 3u) & ~3u;
     const float* src = pts + size_t(cf[sc]) * D;
     for (uint32_t idx = threadIdx.x; idx < lenp * D; idx += blockDim.x) {
-      const float v = idx < len * D ? -__ldg(src + idx) : -kPad;
-      sm[so[sc] * D + idx] = make_float2(v, v);
+      sm[so[sc] * D + idx] = idx < len * D ? -__ldg(src + idx) : -kPad;
     }
   }
   const uint32_t ia = e0 + threadIdx.x, ib = ia + kThreads;
@@ -748,7 +772,7 @@ __global__ void __launch_bounds__(kThreads)
                           const float* __restrict__ hi, float scale,
                           double* __restrict__ partials) {
   constexpr int T = LowDTile<D>::T;
-  __shared__ __align__(16) float2 sm[T * D];
+  __shared__ __align__(16) float sm[T * D];
   const uint32_t blk = blockIdx.x / nchunks, c = blockIdx.x % nchunks;
   const uint32_t cf = first + c * chunk, cl = min(last, cf + chunk);
   const uint32_t e0 = blk * kBE;
