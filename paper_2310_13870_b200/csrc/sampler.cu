@@ -79,6 +79,13 @@ __global__ void node_link_kernel(uint64_t nslots, const uint32_t* __restrict__ t
   if (h < nslots) out[h] = node_link(prefix, (uint64_t(tfirst[h]) << 32) | tlast[h]);
 }
 
+// query_link (common.cuh) of every point: route_kernel reads it instead of
+// computing a splitmix64 per entry (~10% of its instructions at C3's deep levels).
+__global__ void query_link_kernel(uint32_t n, uint64_t* __restrict__ out) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) out[q] = query_link(q);
+}
+
 // Range request: queries qb.., `tickets` each, leaf rows of that size.
 __global__ void range_request_kernel(uint32_t qb, uint32_t nq, uint32_t tickets,
                                      uint32_t* __restrict__ uq, uint32_t* __restrict__ tk,
@@ -137,7 +144,8 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
                  unsigned long long* __restrict__ counters, const float* __restrict__ elm,
                  const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
                  uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk,
-                 const uint64_t* __restrict__ nlink, const uint32_t* __restrict__ dE) {
+                 const uint64_t* __restrict__ nlink, const uint32_t* __restrict__ dE,
+                 const uint64_t* __restrict__ qlink) {
   constexpr int U = kRouteUnroll;
   if (dE) E = *dE;  // the level's entry count on the device (sync-free levels)
   unsigned long long tsum = 0, degen = 0;
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
   uint32_t gi[U], q[U], t[U], f[U], l[U];
   double a[U], b[U];
   float em[U], rm[U];
-  uint64_t nl[U];
+  uint64_t nl[U];  // node link ^ query link
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * kRouteThreads;
@@ -166,7 +174,7 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
     const uint64_t h = ((1ull << level) - 1) + gi[u];
     f[u] = i < E ? tfirst[h] : 0u;
     l[u] = i < E ? tlast[h] : 0u;
-    nl[u] = (i < E && nlink) ? nlink[h] : 0ull;
+    nl[u] = (i < E && nlink) ? (nlink[h] ^ qlink[q[u]]) : 0ull;
     rm[u] = (i < E && row_mass) ? row_mass[eprow ? eprow[i] : i] : 0.f;
   }
 #pragma unroll
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
         if (rng_mode == 0) {
           // RngStream::keyed(seed, kRouteTag, (first<<32)|last, query)
           const uint64_t key =
-              nlink ? splitmix64(nl[u] ^ query_link(q[u]))
+              nlink ? splitmix64(nl[u])
                     : route_key(key_prefix, (uint64_t(f[u]) << 32) | l[u], uint64_t(q[u]));
           if (vlist) {
             // Tie guard: a draw within the fp32 sums' error bound of p is
@@ -1740,7 +1748,14 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
     FSGG_LAUNCH_CHECK();
     ds.launches++;
   }
+  DevBuf& qlink = ds.buf("s.qlink", req.rng_mode == 0 ? size_t(ds.n) * 8 : 8);
+  if (req.rng_mode == 0) {
+    query_link_kernel<<<ceil_div_u32(ds.n, 256), 256, 0, s>>>(ds.n, qlink.as<uint64_t>());
+    FSGG_LAUNCH_CHECK();
+    ds.launches++;
+  }
   const uint64_t* nlink_p = req.rng_mode == 0 ? nlink.as<uint64_t>() : nullptr;
+  const uint64_t* qlink_p = req.rng_mode == 0 ? qlink.as<uint64_t>() : nullptr;
   // E: the current level's entry count when known on the host (E_known);
   // E_hi: an upper bound otherwise. Sync-free descent (low d): a level's
   // kernels read the count from elog on the device and grid-stride, so the
@@ -1951,7 +1966,7 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
         level == 0 ? nullptr : elm[cur]->as<float>(),
         self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
-        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p, dEp);
+        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p, dEp, qlink_p);
     FSGG_LAUNCH_CHECK();
     if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
         smax_level >= kTieBatchMinNode) {
