@@ -7,7 +7,7 @@ for c in C2 C4 C5; do timeout 300 python bench.py --config $c --steps 10 --warmu
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2_bench_reference_c3.json 2>> gpurun_out/bench_all.err
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_c3.csv python scripts/dev/shard_once.py --full > /dev/null 2>&1
 cap() { # name regex config
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o /tmp/ncu/$1 python scripts/profile_once.py $3 1 > /dev/null 2>&1
+  timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:$2 -c 1 -o /tmp/ncu/$1 python scripts/profile_once.py $3 1 > /dev/null 2>&1
   ncu -i /tmp/ncu/$1.ncu-rep --page raw --csv > gpurun_out/$1_raw.csv 2>/dev/null
 }
 cap c3_wtile sym_wtile_kernel C3
