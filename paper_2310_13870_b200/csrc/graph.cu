@@ -93,6 +93,50 @@ __global__ void public_to_compact_kernel(const unsigned long long* in,
 // Steps 2 + 3 in one pass: k_ij once per pair, the underflow flag
 // (sparsifier.cpp:105-109) and the weight (:110-113); dropped pairs are
 // compacted afterwards (rare).
+// kernel_f64 (common.cuh) for the 32 edges of a warp at high d: the same
+// operations in the same order per edge, but the rows of the edges' second
+// endpoints are staged through shared memory in 32-coordinate chunks with
+// coalesced loads (lane = coordinate) and each lane then walks its own row.
+// One thread per edge reading its row from global memory took 4.4 ms for
+// C5's 2.2M edges x 784 coordinates (a 4-byte load per 3136-byte stride);
+// the first endpoint is shared by most lanes of a warp (edges are sorted by
+// u) and stays a direct load.
+constexpr uint32_t kEdgeWideMinDim = 32;
+__device__ __forceinline__ double kernel_f64_staged(int family, double sigma,
+                                                    const float* __restrict__ pts, uint32_t d,
+                                                    uint32_t i, uint32_t j, float (*ys)[33]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const float* x = pts + size_t(i) * d;
+  const uint32_t lim = family == 2 ? d : (d & ~1u);
+  double s = 0.0;
+  for (uint32_t k0 = 0; k0 < lim; k0 += 32) {
+    const uint32_t kn = min(32u, lim - k0);
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t jr = __shfl_sync(0xffffffffu, j, r);
+      ys[r][lane] = lane < kn ? __ldg(pts + size_t(jr) * d + k0 + lane) : 0.f;
+    }
+    __syncwarp();
+    if (family == 2) {
+      for (uint32_t kk = 0; kk < kn; ++kk)
+        s = __dadd_rn(s, fabs(__dsub_rn(double(__ldg(x + k0 + kk)), double(ys[lane][kk]))));
+    } else {
+      for (uint32_t kk = 0; kk < kn; ++kk) {
+        const double t = __dsub_rn(double(__ldg(x + k0 + kk)), double(ys[lane][kk]));
+        s = __dadd_rn(s, __dmul_rn(t, t));
+      }
+    }
+    __syncwarp();
+  }
+  if (family == 2) return exp(-s / sigma);
+  if (d & 1u) {
+    const double t = __dsub_rn(double(x[d - 1]), double(__ldg(pts + size_t(j) * d + d - 1)));
+    s = __fma_rn(t, t, s);
+  }
+  if (family == 1) return exp(-sqrt(s) / sigma);
+  return exp(-s / __dmul_rn(sigma, sigma));
+}
+
+template <bool WIDE>
 __global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64_t m,
                              const float* __restrict__ pts, uint32_t d, int family,
                              double sigma, double L, const double* __restrict__ g_full,
@@ -101,11 +145,19 @@ __global__ void edges_kernel(const unsigned long long* __restrict__ keys, uint64
                              unsigned char* __restrict__ keep,
                              unsigned long long* __restrict__ dropped, int write_v) {
   __shared__ unsigned long long red[8];
+  __shared__ float ys[WIDE ? 8 : 1][WIDE ? 32 : 1][33];
   const uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   unsigned long long drop = 0;
+  double kw = 0.0;
+  if constexpr (WIDE) {  // whole warps: lanes past m stage point 0
+    const unsigned long long key = e < m ? keys[e] : 0ull;
+    kw = kernel_f64_staged(family, sigma, pts, d, uint32_t(key >> 32), uint32_t(key),
+                           ys[threadIdx.x >> 5]);
+  }
   if (e < m) {
     const uint32_t i = uint32_t(keys[e] >> 32), j = uint32_t(keys[e]);
-    const double k = kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
+    const double k =
+        WIDE ? kw : kernel_f64(family, sigma, pts + size_t(i) * d, pts + size_t(j) * d, d);
     const bool ok = k >= 1e-300;
     keep[e] = ok;
     drop = ok ? 0 : 1;
@@ -806,7 +858,7 @@ void finish_graph_chunked(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
       after(sink->v + m, vc, mc * 4);
     }
     FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
-    edges_kernel<<<ceil_div_u32(mc, 256), 256, 0, s>>>(
+    (d >= kEdgeWideMinDim ? edges_kernel<true> : edges_kernel<false>)<<<ceil_div_u32(mc, 256), 256, 0, s>>>(
         keys.as<unsigned long long>(), mc, pts, d, ks.family, ks.sigma, double(rounds), g_full,
         uc, vc, wc, nullptr, keep.as<unsigned char>(), cnt.as<unsigned long long>(),
         early_v ? 0 : 1);
@@ -924,7 +976,7 @@ void finish_graph(Dataset& ds, const KernelSpec& ks, uint32_t rounds,
   if (m) {
     DevBuf& keep = ds.buf("g.keep", m);
     FSGG_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, 16, s));
-    edges_kernel<<<ceil_div_u32(m, 256), 256, 0, s>>>(
+    (d >= kEdgeWideMinDim ? edges_kernel<true> : edges_kernel<false>)<<<ceil_div_u32(m, 256), 256, 0, s>>>(
         keys.as<unsigned long long>(), m, pts, d, ks.family, ks.sigma, double(rounds), g_full,
         out.u.as<uint32_t>(), out.v.as<uint32_t>(), out.w.as<double>(),
         want_estimates ? out.est.as<EdgeEstimateDev>() : nullptr, keep.as<unsigned char>(),
