@@ -326,15 +326,23 @@ __global__ void __launch_bounds__(128)
 #define FSGG_SYM_EXP_MAX 64.f
 #endif
 constexpr float kSymExpMaxNorm = FSGG_SYM_EXP_MAX;
-// Factored form (warp-per-tile kernel, gaussian, d <= FSGG_SYM_FACT_MAX_D):
-// 2^-|q' - x'|^2 = 2^-|q'|^2 * 2^-(|x'|^2 - 2 q'.x'). The row factor leaves
-// the row sum (one multiply per row per tile) and enters the column sum as
-// the multiplicand of the accumulating FFMA2, so a pair costs d packed
-// FMA-pipe operations for the exponent + 2 for the two sums (d = 2: 4
-// instead of the direct form's 6). Same tile-relative origin, same per-tile
-// norm bound and the same error scale as the expanded form above
-// (~eps_f32 * (|q'|^2 + |x'|^2) in the exponent, <= 64: ~5e-6 relative at
-// worst, far inside the tie guard's 1e-4).
+// Factored form (warp-per-tile kernel, gaussian, FSGG_SYM_FACT_MIN_D <= d <=
+// FSGG_SYM_FACT_MAX_D): 2^-|q' - x'|^2 = 2^-|q'|^2 * 2^-(|x'|^2 - 2 q'.x').
+// The row factor leaves the row sum (one multiply per row per tile) and
+// enters the column sum as the multiplicand of the accumulating FFMA2, so a
+// pair costs d packed FMA-pipe operations for the exponent + 2 for the two
+// sums (the expanded form: d + 3). Same tile-relative origin, same per-tile
+// norm bound (on the tile's actual points) and the same error scale as the
+// expanded form above (~eps_f32 * (|q'|^2 + |x'|^2) in the exponent, <= 64:
+// ~5e-6 relative at worst, far inside the tie guard's 1e-4). C4 (d = 5):
+// root 4.56 -> 4.39 ms.
+// d <= 2 can take it too (FSGG_SYM_FACT_MIN_D = 1: 4 packed operations per
+// pair instead of the direct form's 6, the tile's form decided from the two
+// boxes' farthest corners, bound kSymFactMaxNorm, with no pass over the
+// points) but measured no faster (21.7 vs 21.3 ms at C3 with FMA-pipe cycles
+// down from 67% to 55%): that kernel is bound by the MIO queue MUFU shares
+// with LDS and SHFL, not by the FMA pipe, so d <= 2 keeps the more accurate
+// direct form.
 #ifndef FSGG_SYM_FACT_MIN_D
 #define FSGG_SYM_FACT_MIN_D 3
 #endif
