@@ -71,6 +71,12 @@ uint32_t walk_max_node() {
   return e ? uint32_t(std::atoi(e)) : kWalkMaxNode;
 }
 
+// FSGG_ROUTE_FEW=0 keeps the threshold draw test at every level (tests)
+bool route_few() {
+  const char* e = std::getenv("FSGG_ROUTE_FEW");  // read per call: tests toggle it
+  return !(e && e[0] == '0');
+}
+
 // node_link (common.cuh) for every heap slot of the tree (reference RNG).
 __global__ void node_link_kernel(uint64_t nslots, const uint32_t* __restrict__ tfirst,
                                  const uint32_t* __restrict__ tlast, uint64_t prefix,
@@ -145,9 +151,16 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
                  const uint32_t* __restrict__ eprow, const float* __restrict__ row_mass,
                  uint32_t* __restrict__ vlist, uint32_t* __restrict__ vcount, int walk,
                  const uint64_t* __restrict__ nlink, const uint32_t* __restrict__ dE,
-                 const uint64_t* __restrict__ qlink) {
+                 const uint64_t* __restrict__ qlink, uint64_t few_tickets) {
   constexpr int U = kRouteUnroll;
   if (dE) E = *dE;  // the level's entry count on the device (sync-free levels)
+  // Deep levels hold a ticket or two per entry (C3 level 12: 1.25): there the
+  // draw test is the fast walks' division-free u (a + b) - a < 0 with the same
+  // margin, instead of the thresholds ceil(p 2^53) -/+ M (an fp64 division
+  // and three double->integer conversions per entry). The tie guard re-decides
+  // everything inside the margin on exact sums, so both forms give the
+  // reference's decisions. Grid-uniform: few_tickets = the descent's tickets.
+  const bool few = vlist && rng_mode == 0 && few_tickets && uint64_t(E) * 6 >= few_tickets;
   unsigned long long tsum = 0, degen = 0;
   // grid-stride over tiles of kRouteThreads * U entries (index E: sentinel)
   for (uint32_t tile = blockIdx.x; uint64_t(tile) * (kRouteThreads * U) <= E;
@@ -201,11 +214,28 @@ __global__ void __launch_bounds__(kRouteThreads, 6)
           verify = true;  // degenerate by fp32 sums: decided on exact sums
         else
           degen += t[u];
+      } else if (few) {
+        p = -1.0;  // decided below without p
       } else {
         p = a[u] / (a[u] + b[u]);  // :211
       }
       uint32_t left = 0;
-      if (p >= 1.0) {  // rng.hpp:66-67
+      if (p < 0.0) {
+        const uint64_t key = splitmix64(nl[u]);
+        const double ssum = a[u] + b[u];
+        const double rel = kTieMargin * (1.0 + fmaxf(0.f, -em[u]) / 32.0);
+        const double pruned =
+            row_mass ? double(exp2f(rm[u] - (kPruneBits - 24.f) - em[u])) : 0.0;
+        const double M = fma(rel, fmin(a[u], b[u]), (pruned + 0x1p-51) * ssum);
+        bool near = false;
+        for (uint32_t c = 0; c < t[u]; ++c) {
+          const uint64_t m = splitmix64(key + c) >> 11;
+          const double d = fma(double(m) * 0x1p-53, ssum, -a[u]);
+          left += d < 0.0 ? 1u : 0u;
+          near |= fabs(d) <= M;
+        }
+        verify |= near;
+      } else if (p >= 1.0) {  // rng.hpp:66-67
         left = t[u];
       } else if (p > 0.0) {
         // u_c = (x_c >> 11) * 2^-53 < p  <=>  (x_c >> 11) < ceil(p * 2^53)
@@ -1966,7 +1996,8 @@ void sample_counted(Dataset& ds, const KernelSpec& ks, const SampleRequest& req_
         level == 0 ? nullptr : elm[cur]->as<float>(),
         self_rows ? nullptr : eprow[cur]->as<uint32_t>(),
         (have_rows && req.prune) ? row_mass.as<float>() : nullptr,
-        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p, dEp, qlink_p);
+        verify ? vlist.as<uint32_t>() : nullptr, vcount, wk, nlink_p, dEp, qlink_p,
+        nlink_p && route_few() ? out.total_tickets : 0ull);
     FSGG_LAUNCH_CHECK();
     if (verify && ds.d >= kTieBatchMinDim && ds.d <= kTieBatchMaxDim &&
         smax_level >= kTieBatchMinNode) {

@@ -578,8 +578,9 @@ def test_symmetric_root_matches_one_sided():
 @pytest.mark.parametrize("d,n,sigma", [(2, 250000, 0.05), (5, 40000, 0.3)])
 def test_round2_kernels_leave_output_unchanged(d, n, sigma):
     """The warp-per-tile symmetric root (FSGG_SYM_WPT), the fast single-ticket
-    walks with deferred tie steps (FSGG_WALK_FAST) and the whole-node kernel of
-    the two-deep rows level (FSGG_NODE_KERNEL) are each switched off in turn:
+    walks with deferred tie steps (FSGG_WALK_FAST), the whole-node kernel of
+    the two-deep rows level (FSGG_NODE_KERNEL) and the division-free draw test
+    of the deep routing levels (FSGG_ROUTE_FEW) are each switched off in turn:
     samples, reference diagnostics and the built graph's edge set stay the
     same (weights to fp32 summation order). n = 250k at d = 2 gives 245-point
     nodes with two-deep rows (the C3 level-12 shape) and walks that start
@@ -593,7 +594,7 @@ def test_round2_kernels_leave_output_unchanged(d, n, sigma):
     ds = F.Dataset(p.astype(np.float32))
     k = F.Kernel(F.KernelFamily.gaussian, sigma)
     cfg = F.SparsifierConfig(rounds=12, seed=9)
-    names = ("FSGG_SYM_WPT", "FSGG_WALK_FAST", "FSGG_NODE_KERNEL")
+    names = ("FSGG_SYM_WPT", "FSGG_WALK_FAST", "FSGG_NODE_KERNEL", "FSGG_ROUTE_FEW")
     saved = {v: os.environ.get(v) for v in names}
     outs = []
     try:
