@@ -1246,11 +1246,18 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
   const uint32_t i = tile * blockDim.x + threadIdx.x;
   uint32_t nw = 0, wmask = 0;  // single-ticket children handed to the walk
   uint32_t g = 0, q = 0;
+  // the child sums are loaded with the entry (the walk writes below used to
+  // wait for them after the reservation's barriers)
+  double ga = 0.0, gb = 0.0;
   if (i < E) {
     const unsigned long long fl = flags[i];
     const uint32_t t = et[i], l = tl[i];
     g = eg[i];
     q = eq[i];
+    if (l != kLeafMark) {
+      ga = g1[i];
+      gb = g2[i];
+    }
     if (wq && l != kLeafMark) {
       wmask = (l == 1 ? 1u : 0u) | (t - l == 1 ? 2u : 0u);
       nw = __popc(wmask);
@@ -1263,7 +1270,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
         neq[pos] = q;
         net[pos] = l;
         neg[pos] = 2 * g;
-        nelm[pos] = log2_mass(g1[i]);
+        nelm[pos] = log2_mass(ga);
         neprow[pos] = prow;
       }
       if (low(fl)) {
@@ -1271,7 +1278,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
         neq[pos] = q;
         net[pos] = t - l;
         neg[pos] = 2 * g + 1;
-        nelm[pos] = log2_mass(g2[i]);
+        nelm[pos] = log2_mass(gb);
         neprow[pos] = prow;
       }
     }
@@ -1315,7 +1322,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
   if (wmask & 1u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g;
-    welm[pos] = float(int((__double_as_longlong(g1[i]) >> 52) & 0x7ff) - 1023);
+    welm[pos] = float(int((__double_as_longlong(ga) >> 52) & 0x7ff) - 1023);
     wrow[pos] = rw;
     wrm[pos] = rm;
     ++pos;
@@ -1323,7 +1330,7 @@ __global__ void scatter_kernel(uint32_t E, const uint32_t* __restrict__ eq,
   if (wmask & 2u) {
     wq[pos] = q;
     wh[pos] = hbase + 2 * g + 1;
-    welm[pos] = float(int((__double_as_longlong(g2[i]) >> 52) & 0x7ff) - 1023);
+    welm[pos] = float(int((__double_as_longlong(gb) >> 52) & 0x7ff) - 1023);
     wrow[pos] = rw;
     wrm[pos] = rm;
   }
